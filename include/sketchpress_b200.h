@@ -1,0 +1,221 @@
+/*
+ * sketchpress_b200.h -- C-ABI of the B200-native single-pass sketch compressor.
+ *
+ * Drop-in boundary for the hot path of the reference package `sketchpress`
+ * (arXiv 2105.01271; reference sources under pkg/src/sketchpress/, cited as
+ * src/<file>:<line>).  The reference is pure Python with no FFI layer, so each
+ * entry point below replaces one reference Python function (named in its
+ * comment); the Python host mirror (paper_2105_01271_b200/) binds them with
+ * ctypes exactly as a maintainer would bind them from the reference
+ * (INTEGRATION.md shows that stub).
+ *
+ * Conventions
+ *   - All matrices are ROW-MAJOR with an explicit leading dimension counted in
+ *     elements.  All pointers are DEVICE pointers unless marked (host).
+ *   - `stream` is a cudaStream_t passed as void*; every call is stream-ordered
+ *     and asynchronous unless it says it synchronises (the pipelines do, to
+ *     read the kept rank).
+ *   - `a_dtype` tags the snapshot matrix A: SP_F64 or SP_F32 (FP32-stored A is
+ *     widened to FP64 on load, the semantics of src/snapshot_io.py:171).
+ *   - Return value: a status (0 ok, 2 config, 3 I/O, 4 numerical -- the CLI
+ *     exit codes of src/cli.py:28-30 -- plus 5 for CUDA failures).  The message
+ *     of the last failure on the calling thread is sp_last_error().
+ *   - Warnings (src/errors.py:28 RankDeficiencyWarning) come back as bits in
+ *     an `info` array (SP_WARN_*), which the host mirror turns into Python
+ *     warnings.
+ */
+#ifndef SKETCHPRESS_B200_H
+#define SKETCHPRESS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SP_ABI_VERSION 1
+
+/* status codes */
+#define SP_OK 0
+#define SP_ECONFIG 2     /* ConfigError (src/errors.py:8)        */
+#define SP_EIO 3         /* FormatError / StreamPoisonedError     */
+#define SP_ENUMERICAL 4  /* NumericalError (src/errors.py:24)     */
+#define SP_ECUDA 5       /* CUDA runtime / launch failure         */
+
+/* dtype tags for A */
+#define SP_F64 0
+#define SP_F32 1
+
+/* warning bits returned in info[SP_INFO_WARN] */
+#define SP_WARN_RANK_DEFICIENT 1 /* regularized (pinv) solve taken        */
+#define SP_WARN_LIFT_CLAMPED 2   /* lifting rank clamped to sketch rank   */
+#define SP_WARN_ID_PINV 4        /* row_id pseudo-inverse fallback        */
+
+/* layout of the host `info` array filled by the pipelines (length SP_INFO_LEN) */
+#define SP_INFO_KEPT 0      /* effective rank of the projector (r_kept)      */
+#define SP_INFO_WARN 1      /* SP_WARN_* bits                                 */
+#define SP_INFO_BLOCK 2     /* range-finder block width used                  */
+#define SP_INFO_ITERS 3     /* range-finder subspace iterations               */
+#define SP_INFO_RANK 4      /* ID: numerical rank of the coarse sketch (>=)   */
+#define SP_INFO_LIFT_R 5    /* ID: lifting rank actually used                 */
+#define SP_INFO_LAUNCHES 6  /* device kernels launched by the call            */
+#define SP_INFO_LEN 8
+
+int sp_abi_version(void);
+const char* sp_last_error(void);
+/* Number of kernels this library launched on the calling thread so far. */
+int64_t sp_launch_count(void);
+
+/* ---------------------------------------------------------------- K1 -----
+ * out[i, c] = sum_t A[i, idx[t, c]] * w[t, c]      (t = 0..depth-1, no FMA)
+ * Replaces apply_sketch for the stencil kinds (src/sketch.py:171-184,
+ * loop at :179-181) and, with exact_copy=1 (depth must be 1, w ignored),
+ * gather_columns (src/sketch.py:201-211).  idx / w are (depth x n_c)
+ * row-major (the SketchOperator tables, src/sketch.py:161-168).  Bit-exact
+ * with the reference: the product and the running sum are each rounded.
+ */
+int sp_apply_stencil(const void* A, int32_t a_dtype, int64_t rows, int64_t n, int64_t lda,
+                     const int64_t* idx, const double* w, int32_t depth, int64_t n_c,
+                     int32_t exact_copy, double* out, int64_t ldo, void* stream);
+
+/* Validation of a column index set (src/sketch.py:206-210 / src/power.py:216-224):
+ * returns SP_ECONFIG if empty, out of [0, n) or not distinct.  Synchronises. */
+int sp_check_columns(const int64_t* cols, int64_t count, int64_t n, void* stream);
+
+/* ---------------------------------------------------------------- K2 -----
+ * Y (n x r) = A^T Z,  A (m x n), Z (m x r).  The single read of A that
+ * replaces the per-block `gram += block.T @ out` / `hc += block.T @ sub`
+ * products (src/svd.py:66, src/power.py:209-211) in the reformulated
+ * single-pass algebra.  FP64 accumulation, fixed reduction
+ * order (bitwise reproducible).  Any r >= 1 (r > 16 routes to the DMMA GEMM).
+ */
+int sp_skinny_atz(const void* A, int32_t a_dtype, int64_t m, int64_t n, int64_t lda,
+                  const double* Z, int64_t ldz, int32_t r, double* Y, int64_t ldy,
+                  void* stream);
+
+/* ---------------------------------------------------------------- K3 -----
+ * C = alpha * op(A) op(B) + beta * C, FP64 on the DMMA tensor pipe
+ * (mma.sync.m8n8k4.f64).  op(X) = X (trans=0) or X^T (trans=1).  op(A) is
+ * M x K, op(B) is K x N.  Replaces every numpy `@` on the path (e.g.
+ * src/power.py:101,105,166-170,284; src/rowid.py:138-139) and the literal
+ * cross-Gramian H = A^T (A D) (src/svd.py:66).  Deterministic split-K.
+ */
+int sp_gemm(int32_t trans_a, int32_t trans_b, int64_t M, int64_t N, int64_t K, double alpha,
+            const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+            double* C, int64_t ldc, void* stream);
+
+/* ---------------------------------------------------------------- K4 -----
+ * Householder QR of a tall matrix X (rows x cols, rows >= cols): explicit
+ * Q (rows x cols) and R (cols x cols).  cols <= 32 runs as a register-resident
+ * TSQR tree; wider inputs are processed in 32-column panels with two passes
+ * of block Gram-Schmidt between them.  Q, R may not alias X.
+ */
+int sp_tsqr(int64_t rows, int64_t cols, const double* X, int64_t ldx,
+            double* Q, int64_t ldq, double* R, int64_t ldr, void* stream);
+
+/* thin_qr (src/kernels.py:74-84): reduced QR of any rows x cols matrix with
+ * the reference sign convention (src/kernels.py:52-71).  Q is rows x p,
+ * R is p x cols with p = min(rows, cols).  Requires p <= 256. */
+int sp_thin_qr(int64_t rows, int64_t cols, const double* X, int64_t ldx,
+               double* Q, int64_t ldq, double* R, int64_t ldr, void* stream);
+
+/* ---------------------------------------------------------------- K5 -----
+ * One-sided (Hestenes) Jacobi SVD of a square n x n matrix in one CTA:
+ * M = U diag(S) V^T, S descending.  n <= 256.  Columns of U whose singular
+ * value is exactly zero are returned as zero vectors. */
+int sp_jacobi_svd(int64_t n, const double* M, int64_t ldm, double* U, int64_t ldu,
+                  double* S, double* V, int64_t ldv, void* stream);
+
+/* thin_svd (src/kernels.py:87-94): U (rows x p), S (p), V (cols x p),
+ * p = min(rows, cols) <= 256, reference sign convention on U with V. */
+int sp_thin_svd(int64_t rows, int64_t cols, const double* X, int64_t ldx,
+                double* U, int64_t ldu, double* S, double* V, int64_t ldv, void* stream);
+
+/* ---------------------------------------------------------------- K6 -----
+ * pinv_apply (src/kernels.py:158-168): out = 1/s where s > tol * s[0], else 0. */
+int sp_pinv_apply(const double* s, int64_t count, double tol, double* out, void* stream);
+
+/* X = R^{-1} B for upper-triangular R (k x k): the solve_triangular(r1, r2)
+ * of row_id (src/rowid.py:68).  B, X are k x ncols. */
+int sp_trsm_upper(int64_t k, const double* R, int64_t ldr, int64_t ncols,
+                  const double* B, int64_t ldb, double* X, int64_t ldx, void* stream);
+
+/* ---------------------------------------------------------------- K7 -----
+ * pivoted_qr (src/kernels.py:97-142) of M (rows x cols), supplied as
+ * Mt = M^T (cols x rows row-major, i.e. M column-major) so every candidate
+ * column is contiguous.  Greedy max residual norm, exact ties to the lowest
+ * original index, one re-orthogonalisation, zero-pivot filler, final sign
+ * convention.  Outputs: perm (cols, int64), Q (rows x k), R (k x cols).
+ * Mt is not modified. */
+int sp_pivoted_qr(int64_t rows, int64_t cols, const double* Mt, int64_t ldmt, int32_t k,
+                  int64_t* perm, double* Q, int64_t ldq, double* R, int64_t ldr,
+                  void* stream);
+
+/* row_id (src/rowid.py:53-79) of M (m x cols): pivoted_qr(M^T, k), then
+ * C = R1^{-1} R2 (triangular solve, or the pseudo-inverse fallback with
+ * SP_WARN_ID_PINV), P (m x k) with P[indices] = I exactly, indices (k). */
+int sp_row_id(int64_t m, int64_t cols, const double* M, int64_t ldm, int32_t k, double* P,
+              int64_t* indices, int64_t* info, void* stream);
+
+/* ------------------------------------------------------- pipelines -----
+ * Device-resident single-pass pipelines.  A is m x n (lda), the sketch is
+ * the stencil table (idx, w: depth x n_c) optionally composed with a dense
+ * Gaussian projection omega (n_c x ell, device, or NULL), and `cols` is the
+ * power-iteration column set I (src/power.py:64-67).  Inputs are validated
+ * like the reference (ConfigError) before any kernel runs.  Outputs are
+ * row-major device buffers:  U (m x k), S (k), V (n x k).  `info` (host,
+ * SP_INFO_LEN int64) receives the kept rank, warning bits and counters.
+ *
+ * If `pre_s0` (m x out_dim) / `pre_c` (m x n_cols) are non-NULL they hold the
+ * sketch / column block already gathered while A was ingested (the fused
+ * ingest path of the host streams), and the gather is skipped.
+ */
+
+/* single_pass_svd (src/svd.py:168-189). */
+int sp_single_pass_svd(const void* A, int32_t a_dtype, int64_t m, int64_t n, int64_t lda,
+                       const int64_t* idx, const double* w, int32_t depth, int64_t n_c,
+                       const double* omega, int64_t ell, int32_t k,
+                       const double* pre_s0,
+                       double* U, double* S, double* V, int64_t* info, void* stream);
+
+/* power_svd, single_pass mode (src/power.py:227-249, 124-181). */
+int sp_power_svd(const void* A, int32_t a_dtype, int64_t m, int64_t n, int64_t lda,
+                 const int64_t* idx, const double* w, int32_t depth, int64_t n_c,
+                 const double* omega, int64_t ell,
+                 const int64_t* cols, int64_t n_cols, int32_t q, int32_t k,
+                 const double* pre_s0, const double* pre_c,
+                 double* U, double* S, double* V, int64_t* info, void* stream);
+
+/* power_id, single_pass mode (src/power.py:252-308) and single_pass_id
+ * (src/rowid.py:142-183, with q = 0 and cols = NULL).  The lifting
+ * operator T = V_r S_r^{-1} U_r^T A (src/rowid.py:115-139) is returned
+ * FACTORED: lift_left (n_c x r_max, ld r_max) and lift_right (r_max x n, ld n)
+ * with the used rank in info[SP_INFO_LIFT_R]; r_max is the caller's buffer
+ * width (>= the requested / default r).  `select` (m x sel_w) is the matrix
+ * the row selection runs on when the caller precomputed it (projection /
+ * id_target="basis"), else NULL.  Outputs: P (m x k), indices (k, int64),
+ * skeleton (k x n_c).  r_req <= 0 means the reference default
+ * max(k, min(2k, rank)). */
+int sp_power_id(const void* A, int32_t a_dtype, int64_t m, int64_t n, int64_t lda,
+                const int64_t* idx, const double* w, int32_t depth, int64_t n_c,
+                const int64_t* cols, int64_t n_cols, int32_t q, int32_t k, int32_t r_req,
+                const double* project_omega, int64_t project_ell, int32_t id_on_basis,
+                const double* pre_s0, const double* pre_c,
+                double* P, int64_t* indices, double* skeleton,
+                double* lift_left, double* lift_right, int32_t r_max,
+                int64_t* info, void* stream);
+
+/* ---------------------------------------------------------------- K8 -----
+ * ||A - U diag(S) V^T||_F^2 and ||A||_F^2 streamed over A (never forming the
+ * m x n product): the rel_frob_error metric (src/analysis.py:57-65) of a
+ * LowRankSVD.reconstruct() (src/svd.py:42-43).  out2 (host) = {err2, ref2}.
+ * Synchronises. */
+int sp_frob_residual(const void* A, int32_t a_dtype, int64_t m, int64_t n, int64_t lda,
+                     const double* U, int64_t ldu, const double* S, const double* V,
+                     int64_t ldv, int32_t k, double* out2, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SKETCHPRESS_B200_H */

@@ -1,0 +1,148 @@
+// extern "C" boundary (include/sketchpress_b200.h).  Thin wrappers that cast
+// the stream, keep the thread-local error string and the launch counter.
+#include <string>
+
+#include "common.cuh"
+#include "launch_count.cuh"
+#include "ops.cuh"
+
+namespace spb {
+
+static thread_local std::string g_err;
+static thread_local int64_t g_launches = 0;
+
+void set_error(const std::string& msg) { g_err = msg; }
+const char* last_error() { return g_err.c_str(); }
+void count_launch(int n) { g_launches += n; }
+int64_t launches() { return g_launches; }
+
+int single_pass_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, const int64_t* idx,
+                    const double* w, int depth, int64_t nc, const double* omega, int64_t ell, int k,
+                    const double* pre_s0, double* U, double* S, double* V, int64_t* info,
+                    cudaStream_t s);
+int power_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, const int64_t* idx,
+              const double* w, int depth, int64_t nc, const double* omega, int64_t ell,
+              const int64_t* cols, int64_t ncols, int q, int k, const double* pre_s0,
+              const double* pre_c, double* U, double* S, double* V, int64_t* info, cudaStream_t s);
+int power_id(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, const int64_t* idx,
+             const double* w, int depth, int64_t nc, const int64_t* cols, int64_t ncols, int q, int k,
+             int r_req, const double* proj, int64_t proj_ell, int id_on_basis, const double* pre_s0,
+             const double* pre_c, double* P, int64_t* indices, double* skeleton, double* lift_left,
+             double* lift_right, int r_max, int64_t* info, cudaStream_t s);
+int row_id(int64_t m, int64_t cols, const double* M, int64_t ldm, int k, double* P, int64_t* indices,
+           int* warn, cudaStream_t s);
+
+}  // namespace spb
+
+using namespace spb;
+
+#define ST(x) reinterpret_cast<cudaStream_t>(x)
+
+extern "C" {
+
+int sp_abi_version(void) { return SP_ABI_VERSION; }
+const char* sp_last_error(void) { return last_error(); }
+int64_t sp_launch_count(void) { return launches(); }
+
+int sp_apply_stencil(const void* A, int32_t a_dtype, int64_t rows, int64_t n, int64_t lda,
+                     const int64_t* idx, const double* w, int32_t depth, int64_t n_c,
+                     int32_t exact_copy, double* out, int64_t ldo, void* stream) {
+  return apply_stencil(A, a_dtype, rows, n, lda, idx, w, depth, n_c, exact_copy != 0, out, ldo, ST(stream));
+}
+
+int sp_check_columns(const int64_t* cols, int64_t count, int64_t n, void* stream) {
+  return check_columns(cols, count, n, ST(stream));
+}
+
+int sp_skinny_atz(const void* A, int32_t a_dtype, int64_t m, int64_t n, int64_t lda, const double* Z,
+                  int64_t ldz, int32_t r, double* Y, int64_t ldy, void* stream) {
+  return skinny_atz(A, a_dtype, m, n, lda, Z, ldz, r, Y, ldy, ST(stream));
+}
+
+int sp_gemm(int32_t trans_a, int32_t trans_b, int64_t M, int64_t N, int64_t K, double alpha,
+            const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+            int64_t ldc, void* stream) {
+  return gemm(trans_a, trans_b, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ST(stream));
+}
+
+int sp_tsqr(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq, double* R,
+            int64_t ldr, void* stream) {
+  return tsqr(rows, cols, X, ldx, Q, ldq, R, ldr, ST(stream));
+}
+
+int sp_thin_qr(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq,
+               double* R, int64_t ldr, void* stream) {
+  return thin_qr(rows, cols, X, ldx, Q, ldq, R, ldr, ST(stream));
+}
+
+int sp_jacobi_svd(int64_t n, const double* M, int64_t ldm, double* U, int64_t ldu, double* S, double* V,
+                  int64_t ldv, void* stream) {
+  return jacobi_svd(n, M, ldm, U, ldu, S, V, ldv, ST(stream));
+}
+
+int sp_thin_svd(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* U, int64_t ldu,
+                double* S, double* V, int64_t ldv, void* stream) {
+  return thin_svd(rows, cols, X, ldx, U, ldu, S, V, ldv, ST(stream));
+}
+
+int sp_pinv_apply(const double* s, int64_t count, double tol, double* out, void* stream) {
+  return pinv_apply(s, count, tol, out, ST(stream));
+}
+
+int sp_trsm_upper(int64_t k, const double* R, int64_t ldr, int64_t ncols, const double* B, int64_t ldb,
+                  double* X, int64_t ldx, void* stream) {
+  return trsm_upper(k, R, ldr, ncols, B, ldb, X, ldx, ST(stream));
+}
+
+int sp_pivoted_qr(int64_t rows, int64_t cols, const double* Mt, int64_t ldmt, int32_t k, int64_t* perm,
+                  double* Q, int64_t ldq, double* R, int64_t ldr, void* stream) {
+  return pivoted_qr(rows, cols, Mt, ldmt, k, perm, Q, ldq, R, ldr, ST(stream));
+}
+
+int sp_row_id(int64_t m, int64_t cols, const double* M, int64_t ldm, int32_t k, double* P,
+              int64_t* indices, int64_t* info, void* stream) {
+  int warn = 0;
+  const int64_t l0 = launches();
+  const int st = row_id(m, cols, M, ldm, k, P, indices, &warn, ST(stream));
+  if (info) {
+    for (int i = 0; i < SP_INFO_LEN; ++i) info[i] = 0;
+    info[SP_INFO_WARN] = warn;
+    info[SP_INFO_LAUNCHES] = launches() - l0;
+  }
+  return st;
+}
+
+int sp_single_pass_svd(const void* A, int32_t a_dtype, int64_t m, int64_t n, int64_t lda,
+                       const int64_t* idx, const double* w, int32_t depth, int64_t n_c,
+                       const double* omega, int64_t ell, int32_t k, const double* pre_s0, double* U,
+                       double* S, double* V, int64_t* info, void* stream) {
+  return single_pass_svd(A, a_dtype, m, n, lda, idx, w, depth, n_c, omega, ell, k, pre_s0, U, S, V, info,
+                         ST(stream));
+}
+
+int sp_power_svd(const void* A, int32_t a_dtype, int64_t m, int64_t n, int64_t lda, const int64_t* idx,
+                 const double* w, int32_t depth, int64_t n_c, const double* omega, int64_t ell,
+                 const int64_t* cols, int64_t n_cols, int32_t q, int32_t k, const double* pre_s0,
+                 const double* pre_c, double* U, double* S, double* V, int64_t* info, void* stream) {
+  return power_svd(A, a_dtype, m, n, lda, idx, w, depth, n_c, omega, ell, cols, n_cols, q, k, pre_s0, pre_c,
+                   U, S, V, info, ST(stream));
+}
+
+int sp_power_id(const void* A, int32_t a_dtype, int64_t m, int64_t n, int64_t lda, const int64_t* idx,
+                const double* w, int32_t depth, int64_t n_c, const int64_t* cols, int64_t n_cols, int32_t q,
+                int32_t k, int32_t r_req, const double* project_omega, int64_t project_ell,
+                int32_t id_on_basis, const double* pre_s0, const double* pre_c, double* P,
+                int64_t* indices, double* skeleton, double* lift_left, double* lift_right, int32_t r_max,
+                int64_t* info, void* stream) {
+  return power_id(A, a_dtype, m, n, lda, idx, w, depth, n_c, cols, n_cols, q, k, r_req, project_omega,
+                  project_ell, id_on_basis, pre_s0, pre_c, P, indices, skeleton, lift_left, lift_right, r_max,
+                  info, ST(stream));
+}
+
+int sp_frob_residual(const void* A, int32_t a_dtype, int64_t m, int64_t n, int64_t lda, const double* U,
+                     int64_t ldu, const double* S, const double* V, int64_t ldv, int32_t k, double* out2,
+                     void* stream) {
+  return frob_residual(A, a_dtype, m, n, lda, U, ldu, S, V, ldv, k, out2, ST(stream));
+}
+
+}  // extern "C"

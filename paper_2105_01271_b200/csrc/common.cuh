@@ -1,0 +1,125 @@
+// Shared helpers for the sketchpress-b200 device library (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <algorithm>
+
+#include "../../include/sketchpress_b200.h"
+
+namespace spb {
+
+// ---------------------------------------------------------------- errors ----
+// The C-ABI returns an int status (SP_OK / SP_ECONFIG / SP_EIO / SP_ENUMERICAL /
+// SP_ECUDA) and keeps a thread-local message for sp_last_error().
+void set_error(const std::string& msg);
+const char* last_error();
+
+struct Status {
+  int code = SP_OK;
+  int warn = 0;
+};
+
+#define SPB_CUDA(call)                                                        \
+  do {                                                                        \
+    cudaError_t _e = (call);                                                  \
+    if (_e != cudaSuccess) {                                                  \
+      ::spb::set_error(std::string(#call) + ": " + cudaGetErrorString(_e));    \
+      return SP_ECUDA;                                                        \
+    }                                                                         \
+  } while (0)
+
+#define SPB_CHECK_LAUNCH()                                                    \
+  do {                                                                        \
+    cudaError_t _e = cudaGetLastError();                                      \
+    if (_e != cudaSuccess) {                                                  \
+      ::spb::set_error(std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+      return SP_ECUDA;                                                        \
+    }                                                                         \
+  } while (0)
+
+#define SPB_TRY(expr)                                                         \
+  do {                                                                        \
+    int _s = (expr);                                                          \
+    if (_s != SP_OK) return _s;                                               \
+  } while (0)
+
+#define SPB_REQUIRE(cond, msg)                                                \
+  do {                                                                        \
+    if (!(cond)) {                                                            \
+      ::spb::set_error(msg);                                                  \
+      return SP_ECONFIG;                                                      \
+    }                                                                         \
+  } while (0)
+
+inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+constexpr int kNumSMs = 148;
+
+// ------------------------------------------------------- device helpers ----
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ double widen(T x) { return (double)x; }
+
+// Counter-based hash -> uniform double in (-1, 1); used for the random test
+// blocks of the range finder (any full-rank block works; no parity with numpy).
+__device__ __forceinline__ double hash_uniform(uint64_t seed, uint64_t i) {
+  uint64_t z = seed * 0x9E3779B97F4A7C15ull + i * 0xD1B54A32D192ED03ull + 0x8CB92BA72F3D8DD7ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return ((double)(z >> 11) * (1.0 / 9007199254740992.0)) * 2.0 - 1.0;
+}
+
+// ------------------------------------------------------ workspace arena ----
+// Stream-ordered scratch from the default CUDA mempool (cudaMallocAsync);
+// everything allocated through one Arena is released on the same stream when
+// the Arena goes out of scope.
+class Arena {
+ public:
+  explicit Arena(cudaStream_t s) : stream_(s) {}
+  ~Arena() {
+    for (int i = 0; i < n_; ++i) cudaFreeAsync(ptrs_[i], stream_);
+  }
+  template <typename T>
+  T* alloc(size_t count) {
+    if (count == 0) count = 1;
+    void* p = nullptr;
+    if (n_ >= kMax || cudaMallocAsync(&p, count * sizeof(T), stream_) != cudaSuccess) {
+      failed_ = true;
+      return nullptr;
+    }
+    ptrs_[n_++] = p;
+    return static_cast<T*>(p);
+  }
+  bool failed() const { return failed_; }
+  cudaStream_t stream() const { return stream_; }
+
+ private:
+  static constexpr int kMax = 256;
+  cudaStream_t stream_;
+  void* ptrs_[kMax];
+  int n_ = 0;
+  bool failed_ = false;
+};
+
+#define SPB_ALLOC(arena, T, var, count)                                       \
+  T* var = (arena).template alloc<T>(count);                                  \
+  if (!var) {                                                                 \
+    ::spb::set_error("device workspace allocation failed: " #var);            \
+    return SP_ECUDA;                                                          \
+  }
+
+}  // namespace spb

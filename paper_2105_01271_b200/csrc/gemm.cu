@@ -1,0 +1,230 @@
+// K3: FP64 GEMM on the B200 DMMA pipe (mma.sync.aligned.m8n8k4.f64).
+//
+// tcgen05.mma has no f64 kind on sm_100a (ptxas rejects .kind::f64), so the
+// FP64 tensor path on B200 is the warp-level DMMA.  C = alpha op(A) op(B) +
+// beta C for row-major operands; op() selected at compile time so that each
+// operand is copied to shared memory in its global (coalesced) orientation and
+// the fragment reads are bank-conflict free for both orientations (padded
+// strides 20 and 68 doubles).  64x64x16 CTA tiles, 4 warps of 32x32, 8-byte
+// cp.async with zero-fill at the edges, 2-stage pipeline.  When the tile grid
+// cannot fill the 148 SMs, K is split and the partial tiles are reduced in a
+// fixed order (bitwise reproducible).
+//
+// Used for every dense product of the path (src/power.py:101,105,166-170,284;
+// src/rowid.py:138-139) and for the literal cross-Gramian (src/svd.py:66).
+#include "common.cuh"
+#include "launch_count.cuh"
+
+namespace spb {
+
+constexpr int kBM = 64, kBN = 64, kBK = 16;
+constexpr int kGemmThreads = 128;
+constexpr int kPadK = kBK + 4;   // k-contiguous rows: stride 20 doubles
+constexpr int kPadMN = kBM + 4;  // mn-contiguous rows: stride 68 doubles
+constexpr int kStageDoubles = (kBM * kPadK > kBK * kPadMN ? kBM * kPadK : kBK * kPadMN);
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
+  unsigned saddr = (unsigned)__cvta_generic_to_shared(smem);
+  int bytes = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gmem), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// element (r, k) of op(X) where op(X) is R x K; X row-major with ld
+template <int TRANS>
+__device__ __forceinline__ const double* op_ptr(const double* X, int64_t ld, int64_t r, int64_t k) {
+  return TRANS ? X + k * ld + r : X + r * ld + k;
+}
+
+// smem offset of element (r, k) of an op(X) tile (r in [0,64), k in [0,16))
+template <int TRANS>
+__device__ __forceinline__ int tile_off(int r, int k) {
+  return TRANS ? k * kPadMN + r : r * kPadK + k;
+}
+
+template <int TRANS>
+__device__ __forceinline__ void load_tile(double* st, const double* X, int64_t ld, int64_t R,
+                                          int64_t K, int64_t r0, int64_t k0, int64_t k_end) {
+  // 64 x 16 elements, 8 per thread; consecutive threads walk the contiguous dim
+#pragma unroll
+  for (int u = 0; u < (kBM * kBK) / kGemmThreads; ++u) {
+    const int e = threadIdx.x + u * kGemmThreads;
+    int r, k;
+    if (TRANS) {  // stored K x R: contiguous along r
+      k = e / kBM;
+      r = e % kBM;
+    } else {  // stored R x K: contiguous along k
+      r = e / kBK;
+      k = e % kBK;
+    }
+    const int64_t gr = r0 + r, gk = k0 + k;
+    const bool ok = (gr < R) && (gk < k_end);
+    cp_async8(st + tile_off<TRANS>(r, k), ok ? op_ptr<TRANS>(X, ld, gr, gk) : X, ok);
+  }
+}
+
+template <int TA, int TB>
+__global__ void __launch_bounds__(kGemmThreads)
+dgemm_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, int64_t lda,
+             const double* __restrict__ B, int64_t ldb, double* __restrict__ C, int64_t ldc,
+             double alpha, double beta, int64_t k_per_split, bool partial) {
+  __shared__ __align__(16) double sA[2][kStageDoubles];
+  __shared__ __align__(16) double sB[2][kStageDoubles];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+  const int64_t m0 = (int64_t)blockIdx.y * kBM, n0 = (int64_t)blockIdx.x * kBN;
+  const int64_t kb = (int64_t)blockIdx.z * k_per_split;
+  const int64_t ke = min(K, kb + k_per_split);
+  const int ntiles = (int)((ke - kb + kBK - 1) / kBK);
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  if (ntiles > 0) {
+    load_tile<TA>(sA[0], A, lda, M, K, m0, kb, ke);
+    load_tile<TB ? 0 : 1>(sB[0], B, ldb, N, K, n0, kb, ke);
+  }
+  cp_async_commit();
+  for (int kt = 0; kt < ntiles; ++kt) {
+    const int cur = kt & 1;
+    if (kt + 1 < ntiles) {
+      const int64_t kn = kb + (int64_t)(kt + 1) * kBK;
+      load_tile<TA>(sA[cur ^ 1], A, lda, M, K, m0, kn, ke);
+      load_tile<TB ? 0 : 1>(sB[cur ^ 1], B, ldb, N, K, n0, kn, ke);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* a_s = sA[cur];
+    const double* b_s = sB[cur];
+#pragma unroll
+    for (int kk = 0; kk < kBK; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = a_s[tile_off<TA>(wm + i * 8 + g, kk + t)];
+      // op(B) is K x N; stored tile holds (n, k) with orientation !TB
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = b_s[tile_off<TB ? 0 : 1>(wn + j * 8 + g, kk + t)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncthreads();
+  }
+
+  double* Cs = partial ? C + (int64_t)blockIdx.z * M * N : C;
+  const int64_t ldo = partial ? N : ldc;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t m = m0 + wm + i * 8 + g;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t n = n0 + wn + j * 8 + 2 * t + h;
+        if (n >= N) continue;
+        double* p = Cs + m * ldo + n;
+        if (partial) {
+          *p = acc[i][j][h];
+        } else {
+          const double v = alpha * acc[i][j][h];
+          *p = (beta == 0.0) ? v : fma(beta, *p, v);
+        }
+      }
+    }
+  }
+}
+
+__global__ void gemm_split_reduce(const double* __restrict__ P, int S, int64_t M, int64_t N,
+                                  double alpha, double beta, double* __restrict__ C, int64_t ldc) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= M * N) return;
+  double acc = 0.0;
+  for (int s = 0; s < S; ++s) acc += P[(int64_t)s * M * N + e];
+  double* p = C + (e / N) * ldc + (e % N);
+  const double v = alpha * acc;
+  *p = (beta == 0.0) ? v : fma(beta, *p, v);
+}
+
+__global__ void scale_matrix(int64_t M, int64_t N, double beta, double* C, int64_t ldc) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= M * N) return;
+  double* p = C + (e / N) * ldc + (e % N);
+  *p = (beta == 0.0) ? 0.0 : beta * *p;
+}
+
+template <int TA, int TB>
+static void launch_dgemm(dim3 grid, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                         const double* B, int64_t ldb, double* C, int64_t ldc, double alpha,
+                         double beta, int64_t kps, bool partial, cudaStream_t s) {
+  dgemm_kernel<TA, TB><<<grid, kGemmThreads, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, kps, partial);
+}
+
+int gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+         int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
+         cudaStream_t s) {
+  SPB_REQUIRE(M >= 0 && N >= 0 && K >= 0, "negative GEMM extent");
+  SPB_REQUIRE(ldc >= N, "ldc < N");
+  SPB_REQUIRE(lda >= (ta ? M : K) && ldb >= (tb ? K : N), "bad GEMM leading dimension");
+  if (M == 0 || N == 0) return SP_OK;
+  if (K == 0 || alpha == 0.0) {
+    scale_matrix<<<ceil_div(M * N, 256), 256, 0, s>>>(M, N, beta, C, ldc);
+    count_launch();
+    SPB_CHECK_LAUNCH();
+    return SP_OK;
+  }
+  const int gx = ceil_div(N, kBN), gy = ceil_div(M, kBM);
+  const int64_t tiles = (int64_t)gx * gy;
+  int S = 1;
+  if (tiles < 2 * kNumSMs) {
+    S = (int)std::min<int64_t>(ceil_div(2 * kNumSMs, tiles), std::max<int64_t>(1, K / (4 * kBK)));
+    S = std::max(1, std::min(S, 64));
+  }
+  int64_t kps = ceil_div(K, S);
+  kps = ceil_div(kps, kBK) * (int64_t)kBK;
+  S = ceil_div(K, kps);
+  dim3 grid(gx, gy, S);
+  const bool partial = S > 1;
+  Arena ar(s);
+  double* out = C;
+  if (partial) {
+    out = ar.alloc<double>((size_t)S * M * N);
+    if (!out) {
+      set_error("GEMM split-K workspace allocation failed");
+      return SP_ECUDA;
+    }
+  }
+  const int code = ta * 2 + tb;
+  switch (code) {
+    case 0: launch_dgemm<0, 0>(grid, M, N, K, A, lda, B, ldb, out, ldc, alpha, beta, kps, partial, s); break;
+    case 1: launch_dgemm<0, 1>(grid, M, N, K, A, lda, B, ldb, out, ldc, alpha, beta, kps, partial, s); break;
+    case 2: launch_dgemm<1, 0>(grid, M, N, K, A, lda, B, ldb, out, ldc, alpha, beta, kps, partial, s); break;
+    default: launch_dgemm<1, 1>(grid, M, N, K, A, lda, B, ldb, out, ldc, alpha, beta, kps, partial, s); break;
+  }
+  count_launch();
+  SPB_CHECK_LAUNCH();
+  if (partial) {
+    gemm_split_reduce<<<ceil_div(M * N, 256), 256, 0, s>>>(out, S, M, N, alpha, beta, C, ldc);
+    count_launch();
+    SPB_CHECK_LAUNCH();
+  }
+  return SP_OK;
+}
+
+}  // namespace spb

@@ -1,0 +1,329 @@
+// Small dense helpers of the path: sign convention, pseudo-inverse
+// reciprocals, triangular solve, transposes, random blocks, thin QR / SVD
+// drivers, streamed residual norm.
+#include "common.cuh"
+#include "launch_count.cuh"
+#include "ops.cuh"
+
+namespace spb {
+
+// ------------------------------------------------------------ launches ----
+#define SPB_LAUNCHED() \
+  do {                 \
+    count_launch();    \
+    SPB_CHECK_LAUNCH(); \
+  } while (0)
+
+// --------------------------------------------------------- elementwise ----
+__global__ void transpose_kernel(int64_t rows, int64_t cols, const double* __restrict__ X, int64_t ldx,
+                                 double* __restrict__ Y, int64_t ldy) {
+  __shared__ double tile[32][33];
+  const int64_t bx = (int64_t)blockIdx.x * 32, by = (int64_t)blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += 8) {
+    const int64_t r = by + k, c = bx + threadIdx.x;
+    tile[k][threadIdx.x] = (r < rows && c < cols) ? X[r * ldx + c] : 0.0;
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += 8) {
+    const int64_t r = bx + k, c = by + threadIdx.x;  // Y is cols x rows
+    if (r < cols && c < rows) Y[r * ldy + c] = tile[threadIdx.x][k];
+  }
+}
+
+int transpose(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Y, int64_t ldy,
+              cudaStream_t s) {
+  if (rows == 0 || cols == 0) return SP_OK;
+  dim3 g(ceil_div(cols, 32), ceil_div(rows, 32)), b(32, 8);
+  transpose_kernel<<<g, b, 0, s>>>(rows, cols, X, ldx, Y, ldy);
+  SPB_LAUNCHED();
+  return SP_OK;
+}
+
+__global__ void copy2d_kernel(int64_t rows, int64_t cols, const double* __restrict__ X, int64_t ldx,
+                              double* __restrict__ Y, int64_t ldy) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * cols) return;
+  Y[(e / cols) * ldy + (e % cols)] = X[(e / cols) * ldx + (e % cols)];
+}
+
+int copy2d(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Y, int64_t ldy,
+           cudaStream_t s) {
+  if (rows == 0 || cols == 0) return SP_OK;
+  copy2d_kernel<<<ceil_div(rows * cols, 256), 256, 0, s>>>(rows, cols, X, ldx, Y, ldy);
+  SPB_LAUNCHED();
+  return SP_OK;
+}
+
+__global__ void fill_uniform_kernel(int64_t rows, int64_t cols, double* X, int64_t ldx, uint64_t seed) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * cols) return;
+  X[(e / cols) * ldx + (e % cols)] = hash_uniform(seed, (uint64_t)e);
+}
+
+int fill_uniform(int64_t rows, int64_t cols, double* X, int64_t ldx, uint64_t seed, cudaStream_t s) {
+  if (rows == 0 || cols == 0) return SP_OK;
+  fill_uniform_kernel<<<ceil_div(rows * cols, 256), 256, 0, s>>>(rows, cols, X, ldx, seed);
+  SPB_LAUNCHED();
+  return SP_OK;
+}
+
+__global__ void scale_cols_kernel(int64_t rows, int64_t cols, double* X, int64_t ldx, const double* d) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * cols) return;
+  X[(e / cols) * ldx + (e % cols)] *= d[e % cols];
+}
+
+int scale_cols(int64_t rows, int64_t cols, double* X, int64_t ldx, const double* d, cudaStream_t s) {
+  if (rows == 0 || cols == 0) return SP_OK;
+  scale_cols_kernel<<<ceil_div(rows * cols, 256), 256, 0, s>>>(rows, cols, X, ldx, d);
+  SPB_LAUNCHED();
+  return SP_OK;
+}
+
+__global__ void all_finite_kernel(int64_t rows, int64_t cols, const double* X, int64_t ldx, int* bad) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * cols) return;
+  if (!isfinite(X[(e / cols) * ldx + (e % cols)])) atomicOr(bad, 1);
+}
+
+// Synchronises; returns SP_ENUMERICAL with `what` in the message on NaN/Inf.
+int check_finite(int64_t rows, int64_t cols, const double* X, int64_t ldx, const char* what,
+                 cudaStream_t s) {
+  if (rows == 0 || cols == 0) return SP_OK;
+  Arena ar(s);
+  SPB_ALLOC(ar, int, bad, 1);
+  SPB_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
+  all_finite_kernel<<<ceil_div(rows * cols, 256), 256, 0, s>>>(rows, cols, X, ldx, bad);
+  SPB_LAUNCHED();
+  int h = 0;
+  SPB_CUDA(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SPB_CUDA(cudaStreamSynchronize(s));
+  if (h) {
+    set_error(std::string(what));
+    return SP_ENUMERICAL;
+  }
+  return SP_OK;
+}
+
+// ------------------------------------------------------ sign convention ----
+// src/kernels.py:52-71: flip column j so its first entry with |x| > 1e-12 *
+// max|x| is >= 0; companions flip the same column ("col") or row ("row").
+__global__ void sign_fix_kernel(int64_t rows, const double* __restrict__ basis_in, double* basis,
+                                int64_t ldb, double* comp, int64_t ldc, int64_t comp_len, int comp_row) {
+  __shared__ double red[32];
+  __shared__ long long first_s[32];
+  const int j = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  double peak = 0.0;
+  for (int64_t i = tid; i < rows; i += blockDim.x) peak = fmax(peak, fabs(basis[i * ldb + j]));
+  peak = warp_max(peak);
+  if (lane == 0) red[warp] = peak;
+  __syncthreads();
+  peak = 0.0;
+  for (int w = 0; w < nw; ++w) peak = fmax(peak, red[w]);
+  if (peak == 0.0) return;  // uniform
+  long long first = rows;
+  for (int64_t i = tid; i < rows; i += blockDim.x)
+    if (fabs(basis[i * ldb + j]) > 1e-12 * peak) {
+      first = i;
+      break;
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+  if (lane == 0) first_s[warp] = first;
+  __syncthreads();
+  first = rows;
+  for (int w = 0; w < nw; ++w) first = min(first, first_s[w]);
+  if (first >= rows) return;  // cannot happen when peak > 0
+  const bool flip = basis[first * ldb + j] < 0.0;
+  __syncthreads();
+  if (!flip) return;
+  for (int64_t i = tid; i < rows; i += blockDim.x) basis[i * ldb + j] = -basis[i * ldb + j];
+  if (comp) {
+    if (comp_row)
+      for (int64_t c = tid; c < comp_len; c += blockDim.x) comp[(int64_t)j * ldc + c] = -comp[(int64_t)j * ldc + c];
+    else
+      for (int64_t i = tid; i < comp_len; i += blockDim.x) comp[i * ldc + j] = -comp[i * ldc + j];
+  }
+}
+
+int sign_fix(int64_t rows, int64_t cols, double* basis, int64_t ldb, double* comp, int64_t ldc,
+             int64_t comp_len, bool comp_row, cudaStream_t s) {
+  if (cols == 0 || rows == 0) return SP_OK;
+  sign_fix_kernel<<<(int)cols, 256, 0, s>>>(rows, basis, basis, ldb, comp, ldc, comp_len, comp_row ? 1 : 0);
+  SPB_LAUNCHED();
+  return SP_OK;
+}
+
+// ---------------------------------------------------------- pinv_apply ----
+// src/kernels.py:158-168 (the non-increasing precondition is checked by the
+// host mirror, as in the reference).
+__global__ void pinv_kernel(const double* s, int64_t n, double tol, double* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double s0 = s[0];
+  out[i] = (s0 != 0.0 && s[i] > tol * s0) ? 1.0 / s[i] : 0.0;
+}
+
+int pinv_apply(const double* s, int64_t n, double tol, double* out, cudaStream_t st) {
+  if (n == 0) return SP_OK;
+  pinv_kernel<<<ceil_div(n, 256), 256, 0, st>>>(s, n, tol, out);
+  SPB_LAUNCHED();
+  return SP_OK;
+}
+
+// ------------------------------------------------------- triangular solve ----
+// X = R^{-1} B, R upper triangular k x k; one thread per right-hand side
+// column, back substitution in the order of LAPACK's dtrsv.
+__global__ void trsm_upper_kernel(int64_t k, const double* __restrict__ R, int64_t ldr, int64_t ncols,
+                                  const double* __restrict__ B, int64_t ldb, double* X, int64_t ldx) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncols) return;
+  for (int64_t i = k - 1; i >= 0; --i) {
+    double acc = B[i * ldb + c];
+    for (int64_t j = i + 1; j < k; ++j) acc = fma(-R[i * ldr + j], X[j * ldx + c], acc);
+    X[i * ldx + c] = acc / R[i * ldr + i];
+  }
+}
+
+int trsm_upper(int64_t k, const double* R, int64_t ldr, int64_t ncols, const double* B, int64_t ldb,
+               double* X, int64_t ldx, cudaStream_t s) {
+  if (k == 0 || ncols == 0) return SP_OK;
+  trsm_upper_kernel<<<ceil_div(ncols, 128), 128, 0, s>>>(k, R, ldr, ncols, B, ldb, X, ldx);
+  SPB_LAUNCHED();
+  return SP_OK;
+}
+
+// -------------------------------------------------------- thin QR / SVD ----
+// src/kernels.py:74-84 thin_qr: Q rows x p, R p x cols, p = min(rows, cols)
+int thin_qr(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq,
+            double* R, int64_t ldr, cudaStream_t s) {
+  SPB_REQUIRE(rows >= 1 && cols >= 1, "thin_qr needs a non-empty matrix");
+  const int64_t p = std::min(rows, cols);
+  SPB_REQUIRE(p <= 256, "thin_qr supports min(rows, cols) <= 256");
+  SPB_TRY(check_finite(rows, cols, X, ldx, "QR input contains non-finite entries", s));
+  if (rows >= cols) {
+    SPB_TRY(tsqr(rows, cols, X, ldx, Q, ldq, R, ldr, s));
+  } else {
+    // X = [X1 X2] with X1 square: X1 = Q R1, R = [R1, Q^T X2]
+    SPB_TRY(tsqr(rows, rows, X, ldx, Q, ldq, R, ldr, s));
+    SPB_TRY(gemm(1, 0, rows, cols - rows, rows, 1.0, Q, ldq, X + rows, ldx, 0.0, R + rows, ldr, s));
+  }
+  SPB_TRY(sign_fix(rows, p, Q, ldq, R, ldr, cols, true, s));
+  return SP_OK;
+}
+
+// src/kernels.py:87-94 thin_svd: U rows x p, S p, V cols x p
+int thin_svd(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* U, int64_t ldu,
+             double* S, double* V, int64_t ldv, cudaStream_t s) {
+  SPB_REQUIRE(rows >= 1 && cols >= 1, "thin_svd needs a non-empty matrix");
+  const int64_t p = std::min(rows, cols);
+  SPB_REQUIRE(p <= 256, "thin_svd supports min(rows, cols) <= 256");
+  SPB_TRY(check_finite(rows, cols, X, ldx, "SVD input contains non-finite entries", s));
+  Arena ar(s);
+  SPB_ALLOC(ar, double, Q, (size_t)std::max(rows, cols) * p);
+  SPB_ALLOC(ar, double, R, (size_t)p * p);
+  SPB_ALLOC(ar, double, Rt, (size_t)p * p);
+  SPB_ALLOC(ar, double, Us, (size_t)p * p);
+  SPB_ALLOC(ar, double, Vs, (size_t)p * p);
+  if (rows >= cols) {
+    // X = Q R, R = Us S Vs^T  ->  U = Q Us, V = Vs
+    SPB_TRY(tsqr(rows, cols, X, ldx, Q, p, R, p, s));
+    SPB_TRY(jacobi_svd(p, R, p, Us, p, S, Vs, p, s));
+    SPB_TRY(gemm(0, 0, rows, p, p, 1.0, Q, p, Us, p, 0.0, U, ldu, s));
+    SPB_TRY(copy2d(p, p, Vs, p, V, ldv, s));
+  } else {
+    // X^T = Q R  ->  X = R^T Q^T, R^T = Us S Vs^T  ->  U = Us, V = Q Vs
+    SPB_ALLOC(ar, double, Xt, (size_t)cols * rows);
+    SPB_TRY(transpose(rows, cols, X, ldx, Xt, rows, s));
+    SPB_TRY(tsqr(cols, rows, Xt, rows, Q, p, R, p, s));
+    SPB_TRY(transpose(p, p, R, p, Rt, p, s));
+    SPB_TRY(jacobi_svd(p, Rt, p, Us, p, S, Vs, p, s));
+    SPB_TRY(copy2d(p, p, Us, p, U, ldu, s));
+    SPB_TRY(gemm(0, 0, cols, p, p, 1.0, Q, p, Vs, p, 0.0, V, ldv, s));
+  }
+  SPB_TRY(sign_fix(rows, p, U, ldu, V, ldv, cols, false, s));
+  return SP_OK;
+}
+
+// ------------------------------------------------------ K8 residual norm ----
+// err2 = sum_ij (A_ij - sum_c U_ic S_c V_jc)^2, ref2 = sum_ij A_ij^2.
+// One thread per column j holds V[j, :] in shared memory; rows are streamed
+// with U S of the current row broadcast from shared memory.
+constexpr int kResThreads = 64;
+constexpr int kResMaxK = 64;
+
+template <typename TA>
+__global__ void __launch_bounds__(kResThreads)
+residual_kernel(const TA* __restrict__ A, int64_t m, int64_t n, int64_t lda, const double* __restrict__ U,
+                int64_t ldu, const double* __restrict__ S, const double* __restrict__ V, int64_t ldv,
+                int k, int64_t rows_per_cta, double* partial) {
+  __shared__ double vs[kResThreads][kResMaxK + 1];
+  __shared__ double us[kResMaxK];
+  __shared__ double red[2][kResThreads / 32];
+  const int64_t j = (int64_t)blockIdx.x * kResThreads + threadIdx.x;
+  for (int c = 0; c < k; ++c) vs[threadIdx.x][c] = (j < n) ? V[j * ldv + c] : 0.0;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_cta, r1 = min(m, r0 + rows_per_cta);
+  double e2 = 0.0, a2 = 0.0;
+  for (int64_t i = r0; i < r1; ++i) {
+    __syncthreads();
+    if (threadIdx.x < k) us[threadIdx.x] = U[i * ldu + threadIdx.x] * S[threadIdx.x];
+    __syncthreads();
+    if (j < n) {
+      double rec = 0.0;
+      for (int c = 0; c < k; ++c) rec = fma(us[c], vs[threadIdx.x][c], rec);
+      const double a = widen(A[i * lda + j]);
+      const double d = a - rec;
+      e2 = fma(d, d, e2);
+      a2 = fma(a, a, a2);
+    }
+  }
+  e2 = warp_sum(e2);
+  a2 = warp_sum(a2);
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = e2;
+    red[1][threadIdx.x >> 5] = a2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double te = 0.0, ta = 0.0;
+    for (int w = 0; w < kResThreads / 32; ++w) {
+      te += red[0][w];
+      ta += red[1][w];
+    }
+    const int64_t b = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+    partial[2 * b] = te;
+    partial[2 * b + 1] = ta;
+  }
+}
+
+int frob_residual(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, const double* U,
+                  int64_t ldu, const double* S, const double* V, int64_t ldv, int k, double* out2,
+                  cudaStream_t s) {
+  SPB_REQUIRE(k >= 0 && k <= kResMaxK, "frob_residual supports k <= 64");
+  const int gx = ceil_div(n, kResThreads);
+  int gy = std::max(1, std::min<int>(ceil_div(4 * kNumSMs, gx), (int)m));
+  const int64_t rpc = ceil_div(m, gy);
+  gy = ceil_div(m, rpc);
+  Arena ar(s);
+  SPB_ALLOC(ar, double, part, (size_t)2 * gx * gy);
+  dim3 g(gx, gy);
+  if (a_dtype == SP_F64)
+    residual_kernel<double><<<g, kResThreads, 0, s>>>((const double*)A, m, n, lda, U, ldu, S, V, ldv, k, rpc, part);
+  else
+    residual_kernel<float><<<g, kResThreads, 0, s>>>((const float*)A, m, n, lda, U, ldu, S, V, ldv, k, rpc, part);
+  SPB_LAUNCHED();
+  std::vector<double> h((size_t)2 * gx * gy);
+  SPB_CUDA(cudaMemcpyAsync(h.data(), part, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+  SPB_CUDA(cudaStreamSynchronize(s));
+  double e = 0.0, a = 0.0;
+  for (size_t b = 0; b < h.size() / 2; ++b) {
+    e += h[2 * b];
+    a += h[2 * b + 1];
+  }
+  out2[0] = e;
+  out2[1] = a;
+  return SP_OK;
+}
+
+}  // namespace spb

@@ -1,0 +1,46 @@
+// Internal (C++) entry points of the device library; the C-ABI in capi.cu
+// wraps these.  All take a cudaStream_t and return an SP_* status.
+#pragma once
+#include <vector>
+
+#include "common.cuh"
+
+namespace spb {
+
+int apply_stencil(const void* A, int a_dtype, int64_t rows, int64_t n, int64_t lda,
+                  const int64_t* idx, const double* w, int depth, int64_t nc, bool exact,
+                  double* out, int64_t ldo, cudaStream_t s);
+int check_columns(const int64_t* cols, int64_t count, int64_t n, cudaStream_t s);
+int skinny_atz(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, const double* Z,
+               int64_t ldz, int r, double* Y, int64_t ldy, cudaStream_t s);
+int gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+         int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
+         cudaStream_t s);
+int tsqr(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq,
+         double* R, int64_t ldr, cudaStream_t s);
+int jacobi_svd(int64_t n, const double* M, int64_t ldm, double* U, int64_t ldu, double* S,
+               double* V, int64_t ldv, cudaStream_t s);
+int transpose(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Y, int64_t ldy,
+              cudaStream_t s);
+int copy2d(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Y, int64_t ldy,
+           cudaStream_t s);
+int fill_uniform(int64_t rows, int64_t cols, double* X, int64_t ldx, uint64_t seed, cudaStream_t s);
+int scale_cols(int64_t rows, int64_t cols, double* X, int64_t ldx, const double* d, cudaStream_t s);
+int check_finite(int64_t rows, int64_t cols, const double* X, int64_t ldx, const char* what,
+                 cudaStream_t s);
+int sign_fix(int64_t rows, int64_t cols, double* basis, int64_t ldb, double* comp, int64_t ldc,
+             int64_t comp_len, bool comp_row, cudaStream_t s);
+int pinv_apply(const double* s, int64_t n, double tol, double* out, cudaStream_t st);
+int trsm_upper(int64_t k, const double* R, int64_t ldr, int64_t ncols, const double* B, int64_t ldb,
+               double* X, int64_t ldx, cudaStream_t s);
+int thin_qr(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq,
+            double* R, int64_t ldr, cudaStream_t s);
+int thin_svd(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* U, int64_t ldu,
+             double* S, double* V, int64_t ldv, cudaStream_t s);
+int pivoted_qr(int64_t rows, int64_t cols, const double* Mt, int64_t ldmt, int k, int64_t* perm,
+               double* Q, int64_t ldq, double* R, int64_t ldr, cudaStream_t s);
+int frob_residual(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, const double* U,
+                  int64_t ldu, const double* S, const double* V, int64_t ldv, int k, double* out2,
+                  cudaStream_t s);
+
+}  // namespace spb

@@ -1,0 +1,553 @@
+// Device-resident single-pass pipelines: single_pass_svd, power_svd (single
+// pass) and power_id / single_pass_id.  Host-side C++ orchestration of the
+// K1..K7 kernels; the only host synchronisations are the reads of the small
+// Ritz spectra that fix the kept rank (and the finite checks the reference
+// performs).
+//
+// Algebra:  the reference returns
+// the rank-k SVD of P_r A, where P_r projects onto the top r left singular
+// vectors of G = (C C^T)^q s0 and r = #{sigma_i(G) > 1e-12 sigma_1(G)} (the
+// pinv cut of src/svd.py:159-165 / src/power.py:175-180; r = l on the
+// triangular-solve branch).  We compute U_G from the sketch, then make ONE
+// read of A for Y = A^T U_{G,r} (K2), then TSQR + Jacobi of the r x r core:
+//   P_r A = U_r Y^T = U_r R_Y^T Q_Y^T = (U_r u~) s (Q_Y v~)^T.
+// When s0 and C are the same column set (every BASELINE configuration),
+// sigma(G) = sigma(C)^(2q+1) and U_G = U_C, so G is never formed and the kept
+// basis is accurate to ~1e-16 sigma_1 instead of ~1e-16 sigma_1(G).
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "launch_count.cuh"
+#include "ops.cuh"
+
+namespace spb {
+
+constexpr double kRankTol = 1e-12;  // src/kernels.py:19
+
+static int count_kept(const std::vector<double>& s, double power) {
+  if (s.empty() || !(s[0] > 0.0)) return 0;
+  int c = 0;
+  for (double x : s)
+    if (std::pow(x / s[0], power) > kRankTol) ++c;
+  return c;
+}
+
+struct TopSvd {
+  int b = 0, kept = 0, iters = 0;
+  double* U = nullptr;  // rows x b
+  double* S = nullptr;  // b
+  double* V = nullptr;  // cols x b
+  std::vector<double> hs;
+};
+
+// Top singular triplets of X (rows x cols).  Exact (TSQR + Jacobi) when
+// min(rows, cols) <= 64; otherwise a randomized block subspace iteration
+// with Householder orthogonalisation and a Rayleigh-Ritz Jacobi step,
+// iterated until the kept Ritz values are stable, growing the block when the
+// kept rank gets within 8 of its width.
+static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int want, double power,
+                   TopSvd& out, Arena& ar, cudaStream_t s) {
+  const int64_t p = std::min(rows, cols);
+  if (p <= 64) {
+    out.b = (int)p;
+    out.U = ar.alloc<double>((size_t)rows * p);
+    out.S = ar.alloc<double>((size_t)p);
+    out.V = ar.alloc<double>((size_t)cols * p);
+    if (ar.failed()) {
+      set_error("svd_top workspace allocation failed");
+      return SP_ECUDA;
+    }
+    SPB_TRY(thin_svd(rows, cols, X, ldx, out.U, p, out.S, out.V, p, s));
+    out.hs.resize(p);
+    SPB_CUDA(cudaMemcpyAsync(out.hs.data(), out.S, p * sizeof(double), cudaMemcpyDeviceToHost, s));
+    SPB_CUDA(cudaStreamSynchronize(s));
+    out.kept = count_kept(out.hs, power);
+    return SP_OK;
+  }
+  const int cap = (int)std::min<int64_t>(p, 256);
+  int b = std::min(cap, (std::max(32, want + 16) + 7) / 8 * 8);
+  for (;;) {
+    Arena it(s);
+    double* Om = it.alloc<double>((size_t)cols * b);
+    double* Y = it.alloc<double>((size_t)rows * b);
+    double* Q = it.alloc<double>((size_t)rows * b);
+    double* Z = it.alloc<double>((size_t)cols * b);
+    double* P = it.alloc<double>((size_t)cols * b);
+    double* Rt = it.alloc<double>((size_t)b * b);
+    double* Rz = it.alloc<double>((size_t)b * b);
+    double* Us = it.alloc<double>((size_t)b * b);
+    double* Vs = it.alloc<double>((size_t)b * b);
+    double* Sg = it.alloc<double>((size_t)b);
+    if (it.failed()) {
+      set_error("svd_top workspace allocation failed");
+      return SP_ECUDA;
+    }
+    SPB_TRY(fill_uniform(cols, b, Om, b, 0x5eed5eedull + (uint64_t)b, s));
+    SPB_TRY(gemm(0, 0, rows, b, cols, 1.0, X, ldx, Om, b, 0.0, Y, b, s));
+    SPB_TRY(tsqr(rows, b, Y, b, Q, b, Rt, b, s));
+    std::vector<double> prev, hs(b);
+    int kept_prev = -1, kept = 0, iters = 0;
+    bool grow = false;
+    const int max_it = 24;
+    for (int itn = 0; itn < max_it; ++itn) {
+      // Rayleigh-Ritz: Q^T X = Z^T with Z = X^T Q = P Rz  ->  Q^T X = Rz^T P^T
+      SPB_TRY(gemm(1, 0, cols, b, rows, 1.0, X, ldx, Q, b, 0.0, Z, b, s));
+      SPB_TRY(tsqr(cols, b, Z, b, P, b, Rz, b, s));
+      SPB_TRY(transpose(b, b, Rz, b, Rt, b, s));
+      SPB_TRY(jacobi_svd(b, Rt, b, Us, b, Sg, Vs, b, s));
+      SPB_CUDA(cudaMemcpyAsync(hs.data(), Sg, b * sizeof(double), cudaMemcpyDeviceToHost, s));
+      SPB_CUDA(cudaStreamSynchronize(s));
+      iters = itn + 1;
+      kept = count_kept(hs, power);
+      if (kept + 8 > b && b < cap) {
+        grow = true;
+        break;
+      }
+      bool conv = false;
+      if (itn >= 1 && kept == kept_prev) {
+        conv = true;
+        const int chk = std::min(b, kept + 1);
+        for (int i = 0; i < chk; ++i)
+          if (std::fabs(hs[i] - prev[i]) > 1e-14 * hs[0] + 1e-12 * hs[i]) conv = false;
+      }
+      if (conv) break;
+      prev = hs;
+      kept_prev = kept;
+      // one more subspace iteration: Y = X P, Q = orth(Y)
+      SPB_TRY(gemm(0, 0, rows, b, cols, 1.0, X, ldx, P, b, 0.0, Y, b, s));
+      SPB_TRY(tsqr(rows, b, Y, b, Q, b, Rt, b, s));
+    }
+    if (grow) {
+      b = std::min(cap, 2 * b);
+      continue;
+    }
+    out.b = b;
+    out.kept = kept;
+    out.iters = iters;
+    out.hs = hs;
+    out.U = ar.alloc<double>((size_t)rows * b);
+    out.S = ar.alloc<double>((size_t)b);
+    out.V = ar.alloc<double>((size_t)cols * b);
+    if (ar.failed()) {
+      set_error("svd_top workspace allocation failed");
+      return SP_ECUDA;
+    }
+    SPB_TRY(gemm(0, 0, rows, b, b, 1.0, Q, b, Us, b, 0.0, out.U, b, s));
+    SPB_TRY(gemm(0, 0, cols, b, b, 1.0, P, b, Vs, b, 0.0, out.V, b, s));
+    SPB_CUDA(cudaMemcpyAsync(out.S, Sg, b * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    return SP_OK;
+  }
+}
+
+// out (N x k, ld ldo) has orthonormal columns [0, r); fill [r, k) with an
+// orthonormal completion (Householder QR of [X | random]).
+static int complete_basis(int64_t N, int r, int k, double* out, int64_t ldo, uint64_t seed,
+                          cudaStream_t s) {
+  if (r >= k) return SP_OK;
+  Arena ar(s);
+  SPB_ALLOC(ar, double, W, (size_t)N * k);
+  SPB_ALLOC(ar, double, Qc, (size_t)N * k);
+  SPB_ALLOC(ar, double, Rc, (size_t)k * k);
+  if (r > 0) SPB_TRY(copy2d(N, r, out, ldo, W, k, s));
+  SPB_TRY(fill_uniform(N, k - r, W + r, k, seed, s));
+  SPB_TRY(tsqr(N, k, W, k, Qc, k, Rc, k, s));
+  SPB_TRY(copy2d(N, k - r, Qc + r, k, out + r, ldo, s));
+  return SP_OK;
+}
+
+// Given the kept left basis Z (m x r, ld ldz) of the sketch, one read of A:
+// Y = A^T Z, then the rank-k SVD of Z Z^T A written to U (m x k), S, V (n x k).
+static int finish_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, const double* Z,
+                      int64_t ldz, int r, int k, double* U, double* S, double* V, cudaStream_t s) {
+  Arena ar(s);
+  SPB_CUDA(cudaMemsetAsync(S, 0, k * sizeof(double), s));
+  const int kk = std::min(r, k);
+  if (r > 0) {
+    SPB_ALLOC(ar, double, Y, (size_t)n * r);
+    SPB_ALLOC(ar, double, Qy, (size_t)n * r);
+    SPB_ALLOC(ar, double, Ry, (size_t)r * r);
+    SPB_ALLOC(ar, double, Ryt, (size_t)r * r);
+    SPB_ALLOC(ar, double, Us, (size_t)r * r);
+    SPB_ALLOC(ar, double, Vs, (size_t)r * r);
+    SPB_ALLOC(ar, double, Sr, (size_t)r);
+    SPB_ALLOC(ar, double, Uf, (size_t)m * r);
+    SPB_ALLOC(ar, double, Vf, (size_t)n * r);
+    SPB_TRY(skinny_atz(A, a_dtype, m, n, lda, Z, ldz, r, Y, r, s));     // the A pass
+    SPB_TRY(tsqr(n, r, Y, r, Qy, r, Ry, r, s));
+    SPB_TRY(transpose(r, r, Ry, r, Ryt, r, s));
+    SPB_TRY(jacobi_svd(r, Ryt, r, Us, r, Sr, Vs, r, s));                  // Ry^T = Us Sr Vs^T
+    SPB_TRY(gemm(0, 0, m, r, r, 1.0, Z, ldz, Us, r, 0.0, Uf, r, s));      // U = Z Us
+    SPB_TRY(gemm(0, 0, n, r, r, 1.0, Qy, r, Vs, r, 0.0, Vf, r, s));       // V = Qy Vs
+    SPB_TRY(copy2d(m, kk, Uf, r, U, k, s));
+    SPB_TRY(copy2d(n, kk, Vf, r, V, k, s));
+    SPB_CUDA(cudaMemcpyAsync(S, Sr, kk * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  }
+  SPB_TRY(complete_basis(m, kk, k, U, k, 0xC0FFEEull, s));
+  SPB_TRY(complete_basis(n, kk, k, V, k, 0xBEEFull, s));
+  return SP_OK;
+}
+
+// ----------------------------------------------------------- sketching ----
+__global__ void same_set_kernel(const int64_t* idx, const double* w, const int64_t* cols, int64_t n,
+                                int* differ) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (idx[i] != cols[i] || w[i] != 1.0) atomicOr(differ, 1);
+}
+
+// Is the sketch s0 = A D bit-identical to C = A(:, cols)?  (depth-1 unit
+// weights, no projection, idx == cols.)  Synchronises.
+static int sketch_is_columns(const int64_t* idx, const double* w, int depth, int64_t nc,
+                             const double* omega, const int64_t* cols, int64_t ncols, bool& same,
+                             cudaStream_t s) {
+  same = false;
+  if (depth != 1 || omega != nullptr || nc != ncols || cols == nullptr) return SP_OK;
+  Arena ar(s);
+  SPB_ALLOC(ar, int, differ, 1);
+  SPB_CUDA(cudaMemsetAsync(differ, 0, sizeof(int), s));
+  same_set_kernel<<<ceil_div(nc, 256), 256, 0, s>>>(idx, w, cols, nc, differ);
+  count_launch();
+  SPB_CHECK_LAUNCH();
+  int h = 1;
+  SPB_CUDA(cudaMemcpyAsync(&h, differ, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SPB_CUDA(cudaStreamSynchronize(s));
+  same = (h == 0);
+  return SP_OK;
+}
+
+// s0 = (A D) [omega]  (m x out_dim)
+static int make_sketch(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, const int64_t* idx,
+                       const double* w, int depth, int64_t nc, const double* omega, int64_t ell,
+                       double* s0, Arena& ar, cudaStream_t s) {
+  if (!omega) return apply_stencil(A, a_dtype, m, n, lda, idx, w, depth, nc, false, s0, nc, s);
+  double* tmp = ar.alloc<double>((size_t)m * nc);
+  if (!tmp) {
+    set_error("sketch workspace allocation failed");
+    return SP_ECUDA;
+  }
+  SPB_TRY(apply_stencil(A, a_dtype, m, n, lda, idx, w, depth, nc, false, tmp, nc, s));
+  return gemm(0, 0, m, ell, nc, 1.0, tmp, nc, omega, ell, 0.0, s0, ell, s);
+}
+
+static void fill_info(int64_t* info, int kept, int warn, const TopSvd& t, int64_t launches0) {
+  if (!info) return;
+  for (int i = 0; i < SP_INFO_LEN; ++i) info[i] = 0;
+  info[SP_INFO_KEPT] = kept;
+  info[SP_INFO_WARN] = warn;
+  info[SP_INFO_BLOCK] = t.b;
+  info[SP_INFO_ITERS] = t.iters;
+  info[SP_INFO_LAUNCHES] = launches() - launches0;
+}
+
+// --------------------------------------------------------- single_pass_svd ----
+int single_pass_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, const int64_t* idx,
+                    const double* w, int depth, int64_t nc, const double* omega, int64_t ell, int k,
+                    const double* pre_s0, double* U, double* S, double* V, int64_t* info,
+                    cudaStream_t s) {
+  const int64_t l0 = launches();
+  const int64_t out_dim = omega ? ell : nc;
+  // src/svd.py:71-77
+  SPB_REQUIRE(k >= 1, "target rank k must be >= 1");
+  SPB_REQUIRE(k <= out_dim, "target rank k=" + std::to_string(k) + " exceeds sketch width n_c=" + std::to_string(out_dim));
+  SPB_REQUIRE(k <= std::min(m, out_dim), "target rank k=" + std::to_string(k) + " exceeds min(m, n_c)");
+  Arena ar(s);
+  const double* s0 = pre_s0;
+  if (!s0) {
+    double* t = ar.alloc<double>((size_t)m * out_dim);
+    if (!t) {
+      set_error("sketch allocation failed");
+      return SP_ECUDA;
+    }
+    SPB_TRY(make_sketch(A, a_dtype, m, n, lda, idx, w, depth, nc, omega, ell, t, ar, s));
+    s0 = t;
+  }
+  SPB_TRY(check_finite(m, out_dim, s0, out_dim, "QR input contains non-finite entries", s));
+  TopSvd top;
+  SPB_TRY(svd_top(s0, m, out_dim, out_dim, k, 1.0, top, ar, s));
+  const int r = top.kept;
+  SPB_TRY(finish_svd(A, a_dtype, m, n, lda, top.U, top.b, r, k, U, S, V, s));
+  const bool healthy = (m >= out_dim) && (r == out_dim);
+  fill_info(info, r, healthy ? 0 : SP_WARN_RANK_DEFICIENT, top, l0);
+  return SP_OK;
+}
+
+// ------------------------------------------------------------- power_svd ----
+int power_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, const int64_t* idx,
+              const double* w, int depth, int64_t nc, const double* omega, int64_t ell,
+              const int64_t* cols, int64_t ncols, int q, int k, const double* pre_s0,
+              const double* pre_c, double* U, double* S, double* V, int64_t* info, cudaStream_t s) {
+  const int64_t l0 = launches();
+  const int64_t out_dim = omega ? ell : nc;
+  // src/power.py:235-241, 216-224, 330-331
+  SPB_REQUIRE(k <= out_dim, "target rank k=" + std::to_string(k) + " exceeds sketch width " + std::to_string(out_dim));
+  SPB_REQUIRE(cols != nullptr && ncols > 0, "column index set out of range");
+  SPB_REQUIRE(ncols > k, "column set size " + std::to_string(ncols) + " must exceed target rank " + std::to_string(k));
+  SPB_REQUIRE(ncols >= out_dim, "column set size " + std::to_string(ncols) + " must cover the sketch width " + std::to_string(out_dim));
+  SPB_REQUIRE(q >= 1, "single-pass power pipeline needs q >= 1");
+  SPB_TRY(check_columns(cols, ncols, n, s));
+  SPB_REQUIRE(k >= 1 && k <= std::min(m, out_dim),
+              "target rank k=" + std::to_string(k) + " outside the enriched basis width");
+  Arena ar(s);
+  bool same = false;
+  SPB_TRY(sketch_is_columns(idx, w, depth, nc, omega, cols, ncols, same, s));
+  const double* C = pre_c;
+  if (!C) {
+    double* t = ar.alloc<double>((size_t)m * ncols);
+    if (!t) {
+      set_error("column block allocation failed");
+      return SP_ECUDA;
+    }
+    SPB_TRY(apply_stencil(A, a_dtype, m, n, lda, cols, nullptr, 1, ncols, true, t, ncols, s));
+    C = t;
+  }
+  TopSvd top;
+  if (same) {
+    SPB_TRY(check_finite(m, ncols, C, ncols, "power iterate overflowed; enable re-orthonormalization (reorth)", s));
+    SPB_TRY(svd_top(C, m, ncols, ncols, k, 2.0 * q + 1.0, top, ar, s));
+  } else {
+    const double* s0 = pre_s0;
+    if (!s0) {
+      double* t = ar.alloc<double>((size_t)m * out_dim);
+      if (!t) {
+        set_error("sketch allocation failed");
+        return SP_ECUDA;
+      }
+      SPB_TRY(make_sketch(A, a_dtype, m, n, lda, idx, w, depth, nc, omega, ell, t, ar, s));
+      s0 = t;
+    }
+    // G = (C C^T)^q s0 in the reference's association (src/power.py:99-108)
+    double* G = ar.alloc<double>((size_t)m * out_dim);
+    double* T = ar.alloc<double>((size_t)ncols * out_dim);
+    if (ar.failed()) {
+      set_error("power iterate allocation failed");
+      return SP_ECUDA;
+    }
+    SPB_TRY(copy2d(m, out_dim, s0, out_dim, G, out_dim, s));
+    for (int it = 0; it < q; ++it) {
+      SPB_TRY(gemm(1, 0, ncols, out_dim, m, 1.0, C, ncols, G, out_dim, 0.0, T, out_dim, s));
+      SPB_TRY(check_finite(ncols, out_dim, T, out_dim, "power iterate overflowed; enable re-orthonormalization (reorth)", s));
+      SPB_TRY(gemm(0, 0, m, out_dim, ncols, 1.0, C, ncols, T, out_dim, 0.0, G, out_dim, s));
+      SPB_TRY(check_finite(m, out_dim, G, out_dim, "power iterate overflowed; enable re-orthonormalization (reorth)", s));
+    }
+    SPB_TRY(svd_top(G, m, out_dim, out_dim, k, 1.0, top, ar, s));
+  }
+  const int r = top.kept;
+  SPB_TRY(finish_svd(A, a_dtype, m, n, lda, top.U, top.b, r, k, U, S, V, s));
+  const bool healthy = (m >= out_dim) && (r == out_dim);
+  fill_info(info, r, healthy ? 0 : SP_WARN_RANK_DEFICIENT, top, l0);
+  return SP_OK;
+}
+
+// ---------------------------------------------------------------- row ID ----
+__global__ void scatter_p_kernel(int64_t m, int k, const int64_t* perm, const double* coef, int64_t ldc,
+                                 double* P) {
+  // P[perm[i], :] = e_i (i < k); P[perm[k + j], :] = coef[:, j]^T
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= m * k) return;
+  const int64_t row = e / k;
+  const int c = (int)(e % k);
+  const int64_t dst = perm[row];
+  P[dst * k + c] = (row < k) ? (row == c ? 1.0 : 0.0) : coef[(int64_t)c * ldc + (row - k)];
+}
+
+__global__ void gather_rows_kernel(const int64_t* rows_idx, int k, const double* X, int64_t ldx, int64_t cols,
+                                   double* out, int64_t ldo) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)k * cols) return;
+  const int64_t i = e / cols, c = e % cols;
+  out[i * ldo + c] = X[rows_idx[i] * ldx + c];
+}
+
+// row_id (src/rowid.py:53-79) of M (m x cols): P (m x k), indices (k).
+int row_id(int64_t m, int64_t cols, const double* M, int64_t ldm, int k, double* P, int64_t* indices,
+           int* warn, cudaStream_t s) {
+  SPB_REQUIRE(k >= 1 && k <= std::min(m, cols),
+              "rank k=" + std::to_string(k) + " outside [1, " + std::to_string(std::min(m, cols)) + "]");
+  Arena ar(s);
+  SPB_ALLOC(ar, int64_t, perm, (size_t)m);
+  SPB_ALLOC(ar, double, Qp, (size_t)cols * k);
+  SPB_ALLOC(ar, double, R, (size_t)k * m);
+  // pivoted_qr(M^T): rows = cols of M, candidate columns = rows of M (contiguous)
+  SPB_TRY(pivoted_qr(cols, m, M, ldm, k, perm, Qp, k, R, m, s));
+  std::vector<double> hr((size_t)k * k);
+  SPB_CUDA(cudaMemcpy2DAsync(hr.data(), k * sizeof(double), R, m * sizeof(double), k * sizeof(double), k,
+                             cudaMemcpyDeviceToHost, s));
+  SPB_CUDA(cudaStreamSynchronize(s));
+  double dmax = 0.0, dmin = INFINITY;
+  for (int i = 0; i < k; ++i) {
+    dmax = std::max(dmax, std::fabs(hr[(size_t)i * k + i]));
+    dmin = std::min(dmin, std::fabs(hr[(size_t)i * k + i]));
+  }
+  const int64_t nrest = m - k;
+  SPB_ALLOC(ar, double, coef, (size_t)k * std::max<int64_t>(nrest, 1));
+  *warn = 0;
+  if (nrest > 0) {
+    if (dmin > kRankTol * std::max(dmax, 2.2250738585072014e-308)) {
+      SPB_TRY(trsm_upper(k, R, m, nrest, R + k, m, coef, nrest, s));
+    } else {
+      *warn = SP_WARN_ID_PINV;
+      // coef = V diag(pinv(s)) (U^T r2)
+      SPB_ALLOC(ar, double, Uu, (size_t)k * k);
+      SPB_ALLOC(ar, double, Ss, (size_t)k);
+      SPB_ALLOC(ar, double, Vv, (size_t)k * k);
+      SPB_ALLOC(ar, double, Si, (size_t)k);
+      SPB_ALLOC(ar, double, T, (size_t)k * nrest);
+      SPB_ALLOC(ar, double, R1, (size_t)k * k);
+      SPB_TRY(copy2d(k, k, R, m, R1, k, s));
+      SPB_TRY(thin_svd(k, k, R1, k, Uu, k, Ss, Vv, k, s));
+      SPB_TRY(pinv_apply(Ss, k, kRankTol, Si, s));
+      SPB_TRY(gemm(1, 0, k, nrest, k, 1.0, Uu, k, R + k, m, 0.0, T, nrest, s));
+      // T = diag(Si) T : scale rows -> transpose trick via scale_cols on T^T is
+      // avoided; fold into V instead: coef = (V diag(Si)) T
+      SPB_TRY(scale_cols(k, k, Vv, k, Si, s));
+      SPB_TRY(gemm(0, 0, k, nrest, k, 1.0, Vv, k, T, nrest, 0.0, coef, nrest, s));
+    }
+  } else if (!(dmin > kRankTol * std::max(dmax, 2.2250738585072014e-308))) {
+    *warn = SP_WARN_ID_PINV;
+  }
+  scatter_p_kernel<<<ceil_div(m * k, 256), 256, 0, s>>>(m, k, perm, coef, std::max<int64_t>(nrest, 1), P);
+  count_launch();
+  SPB_CHECK_LAUNCH();
+  SPB_CUDA(cudaMemcpyAsync(indices, perm, k * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+  return SP_OK;
+}
+
+// ------------------------------------------------------------ power_id ----
+int power_id(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, const int64_t* idx,
+             const double* w, int depth, int64_t nc, const int64_t* cols, int64_t ncols, int q, int k,
+             int r_req, const double* proj, int64_t proj_ell, int id_on_basis, const double* pre_s0,
+             const double* pre_c, double* P, int64_t* indices, double* skeleton, double* lift_left,
+             double* lift_right, int r_max, int64_t* info, cudaStream_t s) {
+  const int64_t l0 = launches();
+  SPB_REQUIRE(k <= nc, "target rank k=" + std::to_string(k) + " exceeds sketch width n_c=" + std::to_string(nc));
+  if (q > 0 || cols) {
+    SPB_REQUIRE(cols != nullptr && ncols > 0, "column index set out of range");
+    SPB_REQUIRE(ncols > k, "column set size " + std::to_string(ncols) + " must exceed target rank " + std::to_string(k));
+    SPB_REQUIRE(ncols >= nc, "column set size " + std::to_string(ncols) + " must cover the sketch width " + std::to_string(nc));
+    SPB_TRY(check_columns(cols, ncols, n, s));
+  }
+  Arena ar(s);
+  // coarse sketch (always the plain stencil; projections only feed selection)
+  const double* coarse = pre_s0;
+  if (!coarse) {
+    double* t = ar.alloc<double>((size_t)m * nc);
+    if (!t) {
+      set_error("sketch allocation failed");
+      return SP_ECUDA;
+    }
+    SPB_TRY(apply_stencil(A, a_dtype, m, n, lda, idx, w, depth, nc, false, t, nc, s));
+    coarse = t;
+  }
+  SPB_TRY(check_finite(m, nc, coarse, nc, "SVD input contains non-finite entries", s));
+  // SVD of the coarse sketch: rank and the top-r triplets for the lifting
+  const int want = std::max(2 * k, r_req);
+  TopSvd top;
+  SPB_TRY(svd_top(coarse, m, nc, nc, want, 1.0, top, ar, s));
+  int rank = top.kept;
+  int warn = 0;
+  int r = r_req > 0 ? r_req : std::max(k, std::min(2 * k, rank));
+  SPB_REQUIRE(r >= k, "lifting rank r=" + std::to_string(r) + " below target rank k=" + std::to_string(k));
+  SPB_REQUIRE(r >= 1, "lifting rank r must be >= 1");
+  if (r > rank) {
+    warn |= SP_WARN_LIFT_CLAMPED;
+    r = rank;
+  }
+  SPB_REQUIRE(r <= top.b && r <= r_max, "lifting rank exceeds the computed basis width");
+  // selection input
+  const double* sel = coarse;
+  int64_t sel_w = nc;
+  if (id_on_basis) {
+    sel = top.U;  // leading k left singular vectors (ld top.b)
+    sel_w = k;
+    double* t = ar.alloc<double>((size_t)m * k);
+    if (!t) {
+      set_error("selection allocation failed");
+      return SP_ECUDA;
+    }
+    SPB_TRY(copy2d(m, k, top.U, top.b, t, k, s));
+    sel = t;
+  } else if (q > 0) {
+    const double* C = pre_c;
+    if (!C) {
+      double* t = ar.alloc<double>((size_t)m * ncols);
+      if (!t) {
+        set_error("column block allocation failed");
+        return SP_ECUDA;
+      }
+      SPB_TRY(apply_stencil(A, a_dtype, m, n, lda, cols, nullptr, 1, ncols, true, t, ncols, s));
+      C = t;
+    }
+    double* E = ar.alloc<double>((size_t)m * nc);
+    double* E2 = ar.alloc<double>((size_t)m * nc);
+    if (ar.failed()) {
+      set_error("enriched sketch allocation failed");
+      return SP_ECUDA;
+    }
+    SPB_TRY(copy2d(m, nc, coarse, nc, E, nc, s));
+    const bool ref_order = ncols <= m;  // C (C^T E) as the reference when cheap
+    double* W = nullptr;
+    double* T = nullptr;
+    if (ref_order)
+      T = ar.alloc<double>((size_t)ncols * nc);
+    else
+      W = ar.alloc<double>((size_t)m * m);
+    if (ar.failed()) {
+      set_error("enriched sketch allocation failed");
+      return SP_ECUDA;
+    }
+    if (!ref_order) SPB_TRY(gemm(0, 1, m, m, ncols, 1.0, C, ncols, C, ncols, 0.0, W, m, s));
+    for (int it = 0; it < q; ++it) {
+      if (ref_order) {
+        SPB_TRY(gemm(1, 0, ncols, nc, m, 1.0, C, ncols, E, nc, 0.0, T, nc, s));
+        SPB_TRY(gemm(0, 0, m, nc, ncols, 1.0, C, ncols, T, nc, 0.0, E2, nc, s));
+      } else {
+        SPB_TRY(gemm(0, 0, m, nc, m, 1.0, W, m, E, nc, 0.0, E2, nc, s));
+      }
+      SPB_TRY(check_finite(m, nc, E2, nc, "power iterate overflowed; enable re-orthonormalization (reorth)", s));
+      std::swap(E, E2);
+    }
+    sel = E;
+  }
+  if (proj && !id_on_basis) {
+    double* t = ar.alloc<double>((size_t)m * proj_ell);
+    if (!t) {
+      set_error("projection allocation failed");
+      return SP_ECUDA;
+    }
+    SPB_TRY(gemm(0, 0, m, proj_ell, sel_w, 1.0, sel, sel_w, proj, proj_ell, 0.0, t, proj_ell, s));
+    sel = t;
+    sel_w = proj_ell;
+  }
+  int idwarn = 0;
+  SPB_TRY(row_id(m, sel_w, sel, sel_w, k, P, indices, &idwarn, s));
+  warn |= idwarn;
+  // skeleton = coarse[indices]
+  gather_rows_kernel<<<ceil_div((int64_t)k * nc, 256), 256, 0, s>>>(indices, k, coarse, nc, nc, skeleton, nc);
+  count_launch();
+  SPB_CHECK_LAUNCH();
+  // lifting T = (V_r S_r^{-1}) (U_r^T A), kept factored
+  if (r > 0) {
+    SPB_ALLOC(ar, double, sinv, (size_t)top.b);
+    SPB_TRY(pinv_apply(top.S, top.b, kRankTol, sinv, s));
+    SPB_TRY(copy2d(nc, r, top.V, top.b, lift_left, r_max, s));
+    SPB_TRY(scale_cols(nc, r, lift_left, r_max, sinv, s));
+    if (a_dtype == SP_F64) {
+      SPB_TRY(gemm(1, 0, r, n, m, 1.0, top.U, top.b, (const double*)A, lda, 0.0, lift_right, n, s));
+    } else {
+      // Y = A^T U_r (n x r) with FP32 A, then transpose
+      SPB_ALLOC(ar, double, Yt, (size_t)n * r);
+      SPB_REQUIRE(r <= 16, "FP32-stored A supports lifting rank <= 16 in this build");
+      SPB_TRY(skinny_atz(A, a_dtype, m, n, lda, top.U, top.b, r, Yt, r, s));
+      SPB_TRY(transpose(n, r, Yt, r, lift_right, n, s));
+    }
+  }
+  if (info) {
+    fill_info(info, r, warn, top, l0);
+    info[SP_INFO_RANK] = rank;
+    info[SP_INFO_LIFT_R] = r;
+  }
+  return SP_OK;
+}
+
+}  // namespace spb

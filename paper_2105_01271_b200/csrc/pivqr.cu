@@ -1,0 +1,231 @@
+// K7: rank-k column-pivoted QR by modified Gram-Schmidt (src/kernels.py:97-142).
+//
+// The reference's pivot rule is reproduced exactly: at step t the residual
+// norms of the columns t.. are compared, the largest wins, exact ties go to
+// the smallest ORIGINAL column index (perm), the winner is swapped to t, one
+// classical re-orthogonalisation against q_0..q_{t-1} is folded into R, a zero
+// pivot is replaced by the first e_i with a large orthogonal residual, and the
+// trailing columns get the rank-1 update.  The matrix is held transposed
+// (each candidate column contiguous), so the norm of every updated column is
+// recomputed in the same warp pass as its update -- the same quantity the
+// reference recomputes from scratch at the start of the next step.
+//
+// Per step: one single-CTA "select" kernel (argmax, swap, re-orth, normalise)
+// and one grid-wide "update" kernel (one warp per trailing column).
+#include "common.cuh"
+#include "launch_count.cuh"
+#include "ops.cuh"
+
+namespace spb {
+
+constexpr int kPqSelThreads = 1024;
+constexpr int kPqMaxK = 1024;
+
+__global__ void pq_init_kernel(int64_t cols, int64_t rows, const double* __restrict__ Mt, int64_t ldmt,
+                               double* __restrict__ WK, double* __restrict__ norms, int64_t* perm) {
+  const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= cols) return;
+  double a = 0.0;
+  for (int64_t x = lane; x < rows; x += 32) {
+    const double v = Mt[j * ldmt + x];
+    WK[j * rows + x] = v;
+    a = fma(v, v, a);
+  }
+  a = warp_sum(a);
+  if (lane == 0) {
+    norms[j] = sqrt(a);
+    perm[j] = j;
+  }
+}
+
+struct PqBest {
+  double nrm;
+  int64_t perm;
+  int64_t j;
+};
+
+__device__ __forceinline__ bool pq_better(const PqBest& a, const PqBest& b) {
+  return a.nrm > b.nrm || (a.nrm == b.nrm && a.perm < b.perm);
+}
+
+__device__ double pq_block_sum(double v, double* red) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double acc = 0.0;
+  for (int w = 0; w < nw; ++w) acc += red[w];
+  return acc;
+}
+
+__global__ void __launch_bounds__(kPqSelThreads)
+pq_select_kernel(int t, int k, int64_t cols, int64_t rows, double* __restrict__ WK, double* norms,
+                 int64_t* perm, double* __restrict__ Qt, double* __restrict__ R, int64_t ldr,
+                 int* status) {
+  __shared__ double red[32];
+  __shared__ PqBest bests[32];
+  __shared__ double delta[kPqMaxK];
+  __shared__ int64_t jstar_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  // ---- argmax over j in [t, cols) with the lowest-original-index tie-break
+  PqBest b{-1.0, INT64_MAX, -1};
+  for (int64_t j = t + tid; j < cols; j += blockDim.x) {
+    PqBest c{norms[j], perm[j], j};
+    if (pq_better(c, b)) b = c;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    PqBest c{__shfl_xor_sync(0xffffffffu, b.nrm, o), __shfl_xor_sync(0xffffffffu, b.perm, o),
+             __shfl_xor_sync(0xffffffffu, b.j, o)};
+    if (pq_better(c, b)) b = c;
+  }
+  if (lane == 0) bests[warp] = b;
+  __syncthreads();
+  if (tid == 0) {
+    PqBest bb = bests[0];
+    for (int w = 1; w < nw; ++w)
+      if (pq_better(bests[w], bb)) bb = bests[w];
+    jstar_s = bb.j;
+  }
+  __syncthreads();
+  const int64_t js = jstar_s;
+  // ---- swap column t <-> js (work, R columns, perm, norms)
+  if (js != t) {
+    for (int64_t x = tid; x < rows; x += blockDim.x) {
+      const double a = WK[(int64_t)t * rows + x];
+      WK[(int64_t)t * rows + x] = WK[js * rows + x];
+      WK[js * rows + x] = a;
+    }
+    for (int s = tid; s < k; s += blockDim.x) {
+      const double a = R[(int64_t)s * ldr + t];
+      R[(int64_t)s * ldr + t] = R[(int64_t)s * ldr + js];
+      R[(int64_t)s * ldr + js] = a;
+    }
+    if (tid == 0) {
+      const int64_t p = perm[t];
+      perm[t] = perm[js];
+      perm[js] = p;
+      const double nn = norms[t];
+      norms[t] = norms[js];
+      norms[js] = nn;
+    }
+  }
+  __syncthreads();
+  double* v = Qt + (int64_t)t * rows;
+  const double* wt = WK + (int64_t)t * rows;
+  // ---- one classical re-orthogonalisation: delta = Q^T v; v -= Q delta
+  if (t > 0) {
+    for (int s = warp; s < t; s += nw) {
+      double a = 0.0;
+      for (int64_t x = lane; x < rows; x += 32) a = fma(Qt[(int64_t)s * rows + x], wt[x], a);
+      a = warp_sum(a);
+      if (lane == 0) delta[s] = a;
+    }
+    __syncthreads();
+    for (int s = tid; s < t; s += blockDim.x) R[(int64_t)s * ldr + t] += delta[s];
+    for (int64_t x = tid; x < rows; x += blockDim.x) {
+      double acc = 0.0;
+      for (int s = 0; s < t; ++s) acc = fma(Qt[(int64_t)s * rows + x], delta[s], acc);
+      v[x] = wt[x] - acc;
+    }
+  } else {
+    for (int64_t x = tid; x < rows; x += blockDim.x) v[x] = wt[x];
+  }
+  __syncthreads();
+  double part = 0.0;
+  for (int64_t x = tid; x < rows; x += blockDim.x) part = fma(v[x], v[x], part);
+  const double pn = sqrt(pq_block_sum(part, red));
+  if (pn != 0.0) {
+    for (int64_t x = tid; x < rows; x += blockDim.x) v[x] = v[x] / pn;
+  } else {
+    // deterministic filler: first e_i whose residual against q_0..q_{t-1} has norm > 0.5
+    bool found = false;
+    for (int64_t i = 0; i < rows && !found; ++i) {
+      double p2 = 0.0;
+      for (int64_t x = tid; x < rows; x += blockDim.x) {
+        double acc = (x == i) ? 1.0 : 0.0;
+        for (int s = 0; s < t; ++s) acc -= Qt[(int64_t)s * rows + x] * Qt[(int64_t)s * rows + i];
+        p2 = fma(acc, acc, p2);
+      }
+      const double nrm = sqrt(pq_block_sum(p2, red));
+      if (nrm > 0.5) {
+        for (int64_t x = tid; x < rows; x += blockDim.x) {
+          double acc = (x == i) ? 1.0 : 0.0;
+          for (int s = 0; s < t; ++s) acc -= Qt[(int64_t)s * rows + x] * Qt[(int64_t)s * rows + i];
+          v[x] = acc / nrm;
+        }
+        found = true;
+      }
+    }
+    if (!found && tid == 0) *status = SP_ENUMERICAL;
+  }
+  if (tid == 0) R[(int64_t)t * ldr + t] = pn;
+}
+
+// trailing columns j > t: coef = v . w_j ; R[t, j] = coef ; w_j -= coef v ; norm_j
+__global__ void pq_update_kernel(int t, int64_t cols, int64_t rows, double* __restrict__ WK,
+                                 double* __restrict__ norms, const double* __restrict__ Qt,
+                                 double* __restrict__ R, int64_t ldr) {
+  const int64_t j = t + 1 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (j >= cols) return;
+  const double* v = Qt + (int64_t)t * rows;
+  double* w = WK + j * rows;
+  double c = 0.0;
+  for (int64_t x = lane; x < rows; x += 32) c = fma(v[x], w[x], c);
+  c = warp_sum(c);
+  double a = 0.0;
+  for (int64_t x = lane; x < rows; x += 32) {
+    const double nv = fma(-c, v[x], w[x]);
+    w[x] = nv;
+    a = fma(nv, nv, a);
+  }
+  a = warp_sum(a);
+  if (lane == 0) {
+    R[(int64_t)t * ldr + j] = c;
+    norms[j] = sqrt(a);
+  }
+}
+
+int pivoted_qr(int64_t rows, int64_t cols, const double* Mt, int64_t ldmt, int k, int64_t* perm,
+               double* Q, int64_t ldq, double* R, int64_t ldr, cudaStream_t s) {
+  SPB_REQUIRE(k >= 1 && k <= std::min(rows, cols),
+              "rank k=" + std::to_string(k) + " outside [1, " + std::to_string(std::min(rows, cols)) + "]");
+  SPB_REQUIRE(k <= kPqMaxK, "pivoted_qr supports k <= 1024");
+  SPB_REQUIRE(ldmt >= rows && ldr >= cols && ldq >= k, "bad pivoted_qr leading dimension");
+  SPB_TRY(check_finite(cols, rows, Mt, ldmt, "pivoted QR input contains non-finite entries", s));
+  Arena ar(s);
+  SPB_ALLOC(ar, double, WK, (size_t)cols * rows);
+  SPB_ALLOC(ar, double, norms, (size_t)cols);
+  SPB_ALLOC(ar, double, Qt, (size_t)k * rows);
+  SPB_ALLOC(ar, int, status, 1);
+  SPB_CUDA(cudaMemsetAsync(status, 0, sizeof(int), s));
+  SPB_CUDA(cudaMemset2DAsync(R, ldr * sizeof(double), 0, cols * sizeof(double), k, s));
+  pq_init_kernel<<<ceil_div(cols * 32, 256), 256, 0, s>>>(cols, rows, Mt, ldmt, WK, norms, perm);
+  count_launch();
+  SPB_CHECK_LAUNCH();
+  for (int t = 0; t < k; ++t) {
+    pq_select_kernel<<<1, kPqSelThreads, 0, s>>>(t, k, cols, rows, WK, norms, perm, Qt, R, ldr, status);
+    count_launch();
+    SPB_CHECK_LAUNCH();
+    if (t + 1 < cols) {
+      pq_update_kernel<<<ceil_div((cols - t - 1) * 32, 256), 256, 0, s>>>(t, cols, rows, WK, norms, Qt, R, ldr);
+      count_launch();
+      SPB_CHECK_LAUNCH();
+    }
+  }
+  int hst = 0;
+  SPB_CUDA(cudaMemcpyAsync(&hst, status, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SPB_CUDA(cudaStreamSynchronize(s));
+  if (hst != 0) {
+    set_error("cannot extend orthonormal basis");
+    return SP_ENUMERICAL;
+  }
+  SPB_TRY(transpose(k, rows, Qt, rows, Q, ldq, s));
+  SPB_TRY(sign_fix(rows, k, Q, ldq, R, ldr, cols, true, s));
+  return SP_OK;
+}
+
+}  // namespace spb

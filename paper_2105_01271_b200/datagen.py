@@ -1,0 +1,149 @@
+"""BASELINE synthetic snapshot fields.
+
+A[i, j] = sum_modes c_mode * prod_dims sin(pi p_d x_d) * exp(-|p|^2 pi^2 nu t_i)
+
+on the interior grid x = (1..g)/(g+1) of each dimension, t_i = linspace(0, 1, m)
+(src/datagen.py:93 convention), columns flattened in C order over (x, y[, z])
+with p<->x, q<->y, r<->z.  Coefficients are drawn p-major from
+Philox(seed) (the reference's RNG, src/sketch.py:33-35); cfg3's noise
+(variance 1e-6, i.e. std 1e-3) is drawn afterwards from the same generator.
+cfg5 is generated in FP64 and rounded once to FP32.
+
+The reference's own ``gen_heat2d`` (src/datagen.py:74-100) is a different
+(periodic) field, so this module is new.  There is no public dataset: the
+paper's NACA / channel / JHU data are replaced by these seeded fields.
+
+The host generator below is BLAS-free (elementwise numpy in a fixed order), so
+its bytes do not depend on the BLAS build or thread count; parity runs feed the
+SAME bytes to the oracle and to the device path.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+@dataclass(frozen=True)
+class FieldConfig:
+    name: str
+    m: int
+    grid: tuple            # points per dimension
+    modes: int             # P: p, q (, r) in 1..P
+    coef_power: float      # c = N(0,1) / |p|^(2*coef_power)
+    nu: float
+    seed: int
+    stride: int            # coarse-grid stride per dimension
+    k: int
+    q: int                 # power iterations (0 = single_pass_svd)
+    noise_std: float = 0.0
+    dtype: str = "f64"
+
+    @property
+    def n(self) -> int:
+        return int(np.prod(self.grid))
+
+    @property
+    def dims(self) -> int:
+        return len(self.grid)
+
+    @property
+    def n_coarse(self) -> int:
+        return int(np.prod([len(range(0, g, self.stride)) for g in self.grid]))
+
+    @property
+    def a_bytes(self) -> int:
+        return self.m * self.n * (8 if self.dtype == "f64" else 4)
+
+    def scaled(self, m=None, grid=None, name=None):
+        return FieldConfig(name or self.name + "-scaled", m or self.m, grid or self.grid,
+                           self.modes, self.coef_power, self.nu, self.seed, self.stride,
+                           self.k, self.q, self.noise_std, self.dtype)
+
+
+# BASELINE.json "configs" (cfg1..cfg5)
+CONFIGS = {
+    "cfg1": FieldConfig("cfg1", 1000, (64, 64), 5, 1.0, 0.01, 0, 4, 20, 0),
+    "cfg2": FieldConfig("cfg2", 2000, (256, 256), 20, 1.0, 0.005, 1, 4, 50, 1),
+    "cfg3": FieldConfig("cfg3", 5000, (512, 512), 40, 0.5, 0.001, 2, 8, 100, 1,
+                        noise_std=1e-3),
+    "cfg4": FieldConfig("cfg4", 10000, (1024, 1024), 60, 0.75, 0.002, 3, 8, 200, 1),
+    "cfg5": FieldConfig("cfg5", 2000, (256, 256, 256), 12, 1.0, 0.003, 4, 4, 100, 1,
+                        dtype="f32"),
+}
+
+
+def coarse_grid_indices(grid, stride) -> np.ndarray:
+    """Flattened (C-order) indices of the points whose every coordinate is
+    a multiple of ``stride`` -- the BASELINE coarse grid, ascending."""
+    axes = [np.arange(0, g, stride, dtype=np.int64) for g in grid]
+    mesh = np.meshgrid(*axes, indexing="ij")
+    flat = np.zeros(mesh[0].shape, dtype=np.int64)
+    for ax, g in zip(mesh, grid):
+        flat = flat * g + ax
+    return flat.ravel()
+
+
+def mode_tables(cfg: FieldConfig):
+    """(S, lam, coef): S[i_x, p-1] = sin(pi p x_i); lam and coef flattened p-major."""
+    rng = np.random.Generator(np.random.Philox(cfg.seed))
+    P = cfg.modes
+    p = np.arange(1, P + 1, dtype=np.float64)
+    grids = [np.arange(1, g + 1, dtype=np.float64) / (g + 1.0) for g in cfg.grid]
+    S = [np.sin(np.pi * np.outer(x, p)) for x in grids]
+    mesh = np.meshgrid(*([p] * cfg.dims), indexing="ij")
+    lam = sum(mm ** 2 for mm in mesh).ravel()
+    coef = rng.standard_normal(lam.size) / lam ** cfg.coef_power
+    return S, lam, coef, rng
+
+
+def generate_host(cfg: FieldConfig) -> np.ndarray:
+    """Deterministic, BLAS-free host generator (row-major m x n)."""
+    S, lam, coef, rng = mode_tables(cfg)
+    t = np.linspace(0.0, 1.0, cfg.m)
+    P = cfg.modes
+    out = np.zeros((cfg.m,) + tuple(cfg.grid))
+    if cfg.dims == 2:
+        gx, gy = cfg.grid
+        # out[i, x, y] += sum_p S_x[x,p] * (sum_q E[i,(p,q)] * S_y[y,q])
+        for a in range(P):
+            inner = np.zeros((cfg.m, gy))
+            for b in range(P):
+                mu = a * P + b
+                e = np.exp(-lam[mu] * np.pi ** 2 * cfg.nu * t) * coef[mu]
+                inner += e[:, None] * S[1][None, :, b]
+            out += S[0][None, :, a, None] * inner[:, None, :]
+    elif cfg.dims == 3:
+        gx, gy, gz = cfg.grid
+        for a in range(P):
+            mid = np.zeros((cfg.m, gy, gz))
+            for b in range(P):
+                inner = np.zeros((cfg.m, gz))
+                for c in range(P):
+                    mu = (a * P + b) * P + c
+                    e = np.exp(-lam[mu] * np.pi ** 2 * cfg.nu * t) * coef[mu]
+                    inner += e[:, None] * S[2][None, :, c]
+                mid += S[1][None, :, b, None] * inner[:, None, :]
+            out += S[0][None, :, a, None, None] * mid[:, None, :, :]
+    else:
+        raise ValueError("only 2-D and 3-D fields")
+    out = out.reshape(cfg.m, cfg.n)
+    if cfg.noise_std:
+        out += rng.standard_normal(out.shape) * cfg.noise_std
+    if cfg.dtype == "f32":
+        out = out.astype(np.float32)
+    return out
+
+
+def analytic_singular_values(cfg: FieldConfig) -> np.ndarray:
+    """sigma(A) of the noise-free field via DST-I orthogonality.
+
+    Phi^T Phi = ((g+1)/2)^d I on the interior grid, so
+    sigma(A) = sigma(E diag(c) * ((g+1)/2)^(d/2)) -- an m x P^d SVD.
+    """
+    _, lam, coef, _ = mode_tables(cfg)
+    t = np.linspace(0.0, 1.0, cfg.m)
+    e = np.exp(-np.outer(t, lam) * np.pi ** 2 * cfg.nu) * coef[None, :]
+    scale = np.prod([np.sqrt((g + 1) / 2.0) for g in cfg.grid])
+    return np.linalg.svd(e * scale, compute_uv=False)

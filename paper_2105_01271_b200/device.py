@@ -1,0 +1,81 @@
+"""Device plumbing: torch provides HBM allocations and the CUDA stream; the
+compute runs in libsketchpress_b200.so.  Fails loudly without a CUDA device
+(there is no CPU path in this package)."""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .errors import SketchpressError
+
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as t
+        _torch = t
+    return _torch
+
+
+def require_cuda():
+    t = torch()
+    if not t.cuda.is_available():
+        raise SketchpressError(
+            "paper_2105_01271_b200 runs on a CUDA (sm_100a) device; none is available "
+            "(there is deliberately no CPU fallback)")
+    return t
+
+
+def device():
+    t = require_cuda()
+    return t.device("cuda", t.cuda.current_device())
+
+
+def stream_handle():
+    t = require_cuda()
+    return t.cuda.current_stream().cuda_stream
+
+
+def ptr(x) -> int | None:
+    """Raw device pointer of a torch tensor (None passes through as NULL)."""
+    return None if x is None else x.data_ptr()
+
+
+def empty(shape, dtype="f64"):
+    t = require_cuda()
+    td = t.float64 if dtype == "f64" else (t.float32 if dtype == "f32" else t.int64)
+    return t.empty(shape, dtype=td, device=device())
+
+
+def zeros(shape, dtype="f64"):
+    t = empty(shape, dtype)
+    t.zero_()
+    return t
+
+
+def to_device(a, dtype=None):
+    """Host array (or torch tensor) -> contiguous device tensor."""
+    t = require_cuda()
+    if isinstance(a, t.Tensor):
+        x = a
+    else:
+        arr = np.ascontiguousarray(a if dtype is None else np.asarray(a, dtype=dtype))
+        x = t.from_numpy(arr)
+    if dtype is not None:
+        x = x.to(dtype={np.float64: t.float64, np.float32: t.float32, np.int64: t.int64}[np.dtype(dtype).type])
+    return x.to(device(), non_blocking=False).contiguous()
+
+
+def to_host(x) -> np.ndarray:
+    return x.detach().cpu().numpy()
+
+
+def is_device_tensor(x) -> bool:
+    t = torch()
+    return isinstance(x, t.Tensor) and x.is_cuda
+
+
+def synchronize():
+    require_cuda().cuda.synchronize()

@@ -1,0 +1,159 @@
+"""Row interpolative decomposition on the GPU (src/rowid.py).
+
+``row_id`` runs the column-pivoted QR (K7) on the transpose plus the
+triangular / pseudo-inverse coefficient solve on the device.  The single-pass
+variants return the lifting operator FACTORED,
+T = (V_r S_r^{-1}) (U_r^T A)  (src/rowid.py:115-139; PAPER eq. for the lift),
+because the dense n_c x n lifting is 8.6 GB at cfg3 and 35 TB at cfg5.
+``FactoredLifting`` behaves like the dense matrix for ``x @ T``, ``T @ x``,
+``.shape`` and ``np.asarray`` (materialisation only for small cases).
+"""
+
+from __future__ import annotations
+
+import warnings
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import ConfigError, RankDeficiencyWarning
+from .kernels import RANK_TOL, ThinSVD
+
+ID_ON_COARSE = "coarse"
+ID_ON_BASIS = "basis"
+
+
+class FactoredLifting:
+    """Lazy n_c x n operator left @ right (left: n_c x r, right: r x n)."""
+
+    __array_priority__ = 1000
+
+    def __init__(self, left, right, host: bool = True):
+        self.left = left
+        self.right = right
+        self.host = host
+
+    @property
+    def shape(self):
+        return (self.left.shape[0], self.right.shape[1])
+
+    @property
+    def rank(self) -> int:
+        return self.left.shape[1]
+
+    def _h(self, x):
+        return x.detach().cpu().numpy() if hasattr(x, "detach") else x
+
+    def __rmatmul__(self, x):
+        """x @ T = (x @ left) @ right."""
+        if self.host:
+            return (np.asarray(x) @ self._h(self.left)) @ self._h(self.right)
+        return (x @ self.left) @ self.right
+
+    def __matmul__(self, x):
+        """T @ x = left @ (right @ x)."""
+        if self.host:
+            return self._h(self.left) @ (self._h(self.right) @ np.asarray(x))
+        return self.left @ (self.right @ x)
+
+    def __array__(self, dtype=None, copy=None):
+        dense = self._h(self.left) @ self._h(self.right)
+        return dense if dtype is None else dense.astype(dtype)
+
+    def dense(self):
+        return np.asarray(self)
+
+
+@dataclass
+class RowIDFactors:
+    """Coefficients, selected rows, skeleton, optional lifting (src/rowid.py:30-50)."""
+
+    p: object
+    indices: object
+    skeleton: object
+    lifting: object = None
+    r: int | None = None
+    method: str = "direct"
+
+    def reconstruct(self):
+        approx = self.p @ self.skeleton
+        if self.lifting is not None:
+            approx = approx @ self.lifting
+        return approx
+
+
+def row_id(matrix, k: int) -> RowIDFactors:
+    """Rank-k row ID via column-pivoted QR of the transpose (src/rowid.py:53-79)."""
+    from .device import empty, is_device_tensor, ptr, stream_handle, to_device, to_host
+    dev = is_device_tensor(matrix)
+    x = matrix.double().contiguous() if dev else to_device(np.asarray(matrix, dtype=np.float64))
+    if x.dim() != 2:
+        raise ConfigError("expected a 2-D matrix")
+    rows, cols = x.shape
+    if not 1 <= k <= min(rows, cols):
+        raise ConfigError(f"rank k={k} outside [1, {min(rows, cols)}]")
+    p = empty((rows, k))
+    ind = empty((k,), "i64")
+    info = _lib.new_info()
+    _lib.call("sp_row_id", rows, cols, ptr(x), cols, k, ptr(p), ptr(ind), _lib.info_ptr(info), stream_handle())
+    if info[_lib.INFO_WARN] & _lib.SP_WARN_ID_PINV:
+        warnings.warn("ID pivots are rank deficient; using pseudo-inverse solve", RankDeficiencyWarning,
+                      stacklevel=2)
+    if dev:
+        return RowIDFactors(p=p, indices=ind, skeleton=x[ind].clone())
+    indices = to_host(ind).astype(np.intp)
+    return RowIDFactors(p=to_host(p), indices=indices, skeleton=np.asarray(matrix, dtype=np.float64)[indices].copy())
+
+
+def build_lifting(coarse_svd: ThinSVD, gram, r: int, k: int | None = None):
+    """V S+ U^T U_r U_r^T U S+ V^T H^T (src/rowid.py:115-139), dense, on the GPU."""
+    from .device import empty, ptr, stream_handle, to_device, to_host
+    from .kernels import pinv_apply
+    if k is not None and r < k:
+        raise ConfigError(f"lifting rank r={r} below target rank k={k}")
+    if r < 1:
+        raise ConfigError("lifting rank r must be >= 1")
+    rank = coarse_svd.rank()
+    if r > rank:
+        warnings.warn(f"lifting rank {r} clamped to sketch rank {rank}", RankDeficiencyWarning, stacklevel=2)
+        r = rank
+    u = to_device(np.asarray(coarse_svd.u, dtype=np.float64))
+    v = to_device(np.asarray(coarse_svd.v, dtype=np.float64))
+    s = np.asarray(coarse_svd.s, dtype=np.float64)
+    sp = to_device(pinv_apply(s))
+    g = to_device(np.asarray(gram, dtype=np.float64))
+    n_c, p = v.shape
+    st = stream_handle()
+
+    def mm(ta, tb, a, b, M, N, K):
+        out = empty((M, N))
+        _lib.call("sp_gemm", ta, tb, M, N, K, 1.0, ptr(a), a.shape[1], ptr(b), b.shape[1], 0.0, ptr(out), N, st)
+        return out
+
+    utu = mm(1, 0, u, u[:, :r].contiguous(), p, r, u.shape[0])       # U^T U_r
+    left = mm(0, 0, v, (sp[:, None] * utu).contiguous(), n_c, r, p)  # V S+ (U^T U_r)
+    tmp = mm(1, 1, left, g, r, g.shape[0], n_c)                       # left^T H^T
+    return to_host(mm(0, 0, left, tmp, n_c, g.shape[0], r))
+
+
+def single_pass_id(stream, op, k: int, r: int | None = None, block_rows: int = 256,
+                   id_target: str = ID_ON_COARSE, project_ell: int | None = None,
+                   project_seed: int = 0, return_device: bool = False) -> RowIDFactors:
+    """SPC-ID (src/rowid.py:142-183): selection on the coarse sketch (or its
+    leading left singular vectors), factored lifting, one pass."""
+    from .power import _run_id
+    if op.omega is not None:
+        raise ConfigError("pass a plain sketch; use project_ell for the ID projection")
+    if id_target not in (ID_ON_COARSE, ID_ON_BASIS):
+        raise ConfigError(f"unknown id_target {id_target!r}")
+    if k > op.n_c:
+        raise ConfigError(f"target rank k={k} exceeds sketch width n_c={op.n_c}")
+    out = _run_id(stream, op, k, None, 0, r, block_rows,
+                  project_ell if id_target == ID_ON_COARSE else None, project_seed,
+                  id_target == ID_ON_BASIS, "single_pass", return_device)
+    return out
+
+
+def two_pass_id(stream, op, k: int, block_rows: int = 256):
+    raise NotImplementedError("two_pass_id is a SURVEY 8(f) 'next' item; not in this build")

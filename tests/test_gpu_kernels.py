@@ -1,0 +1,230 @@
+"""GPU kernel-level parity: each C-ABI entry point against the oracle / numpy.
+
+Bit-exact gates for the gather (K1) and the pivot order (K7); the floating
+point kernels against a numpy FP64 reference with the tolerance written in
+each test.  All calls go through the C-ABI (ctypes) of libsketchpress_b200.so.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden, philox, rank_deficient
+
+import oracle
+import paper_2105_01271_b200 as sp
+from paper_2105_01271_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev(x, cuda):
+    return cuda.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def _stream(cuda):
+    return cuda.cuda.current_stream().cuda_stream
+
+
+# ------------------------------------------------------------------ K1 ----
+@pytest.mark.parametrize("kind", ["injection", "neighbor", "global"])
+@pytest.mark.parametrize("n,n_c", [(37, 9), (4096, 256), (1000, 999), (50, 3)])
+def test_stencil_bit_exact(cuda, kind, n, n_c):
+    x = philox(n + n_c).standard_normal((70, n))
+    x[3, :5] = -0.0
+    op = sp.build_sketch(sp.SketchSpec(kind, n, n_c))
+    got = sp.apply_sketch(op, x)
+    want = oracle.sketch_rows(x, op.idx, op.w)
+    assert got.shape == want.shape
+    assert np.array_equal(got, want)  # == : -0.0 becomes +0.0 in both
+
+
+def test_stencil_golden_tables(cuda):
+    g = load_golden("small_cases.npz")
+    x = philox(21).standard_normal((5, 37))
+    for kind in ("injection", "neighbor", "global"):
+        op = sp.build_sketch(sp.SketchSpec(kind, 37, 9))
+        assert np.array_equal(op.idx, g[f"st_{kind}_idx"])
+        assert np.array_equal(op.w, g[f"st_{kind}_w"])
+        assert np.array_equal(sp.apply_sketch(op, x), g[f"st_{kind}_out"])
+
+
+def test_gather_columns_exact_and_f32(cuda):
+    x = philox(3).standard_normal((33, 500))
+    cols = np.array([0, 7, 499, 250, 3])
+    assert np.array_equal(sp.gather_columns(x, cols), x[:, cols])
+    xf = x.astype(np.float32)
+    d = _dev(xf, cuda)
+    out = sp.gather_columns(d, cols).cpu().numpy()
+    assert np.array_equal(out, xf[:, cols].astype(np.float64))
+    with pytest.raises(sp.ConfigError):
+        sp.gather_columns(x, [1, 1])
+    with pytest.raises(sp.ConfigError):
+        sp.gather_columns(x, [500])
+
+
+def test_grid_injection_indices_bit_exact(cuda):
+    op, cols = sp.grid_injection((64, 64), 4)
+    assert np.array_equal(cols, oracle.grid_coarse_indices((64, 64), 4))
+    op3, cols3 = sp.grid_injection((16, 12, 8), 4)
+    want = np.array([(ix * 12 + iy) * 8 + iz for ix in range(0, 16, 4) for iy in range(0, 12, 4)
+                     for iz in range(0, 8, 4)])
+    assert np.array_equal(cols3, want)
+
+
+# ------------------------------------------------------------------ K2 ----
+@pytest.mark.parametrize("r", [1, 3, 7, 8, 16, 24])
+@pytest.mark.parametrize("m,n", [(1000, 4096), (257, 1001), (5, 33)])
+def test_skinny_atz(cuda, r, m, n):
+    rng = philox(m * r + n)
+    a = rng.standard_normal((m, n))
+    z = rng.standard_normal((m, r))
+    y = cuda.empty((n, r), dtype=cuda.float64, device="cuda")
+    da, dz = _dev(a, cuda), _dev(z, cuda)
+    _lib.call("sp_skinny_atz", da.data_ptr(), _lib.SP_F64, m, n, n, dz.data_ptr(), r, r, y.data_ptr(), r,
+              _stream(cuda))
+    want = a.T @ z
+    np.testing.assert_allclose(y.cpu().numpy(), want, rtol=0, atol=1e-12 * np.abs(a).sum(0).max() * np.abs(z).max())
+
+
+def test_skinny_atz_f32_and_determinism(cuda):
+    rng = philox(5)
+    a = rng.standard_normal((600, 3000)).astype(np.float32)
+    z = rng.standard_normal((600, 8))
+    da, dz = _dev(a, cuda), _dev(z, cuda)
+    outs = []
+    for _ in range(2):
+        y = cuda.empty((3000, 8), dtype=cuda.float64, device="cuda")
+        _lib.call("sp_skinny_atz", da.data_ptr(), _lib.SP_F32, 600, 3000, 3000, dz.data_ptr(), 8, 8,
+                  y.data_ptr(), 8, _stream(cuda))
+        outs.append(y.cpu().numpy())
+    # f32 x f64 products are exact in f64: only the sums round
+    np.testing.assert_allclose(outs[0], a.astype(np.float64).T @ z, rtol=0, atol=1e-11)
+    assert outs[0].tobytes() == outs[1].tobytes()  # fixed reduction order
+
+
+# ------------------------------------------------------------------ K3 ----
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(64, 64, 16), (100, 37, 259), (3, 200, 4000), (513, 65, 7)])
+def test_gemm(cuda, ta, tb, M, N, K):
+    rng = philox(M + N + K + ta * 2 + tb)
+    A = rng.standard_normal((K, M) if ta else (M, K))
+    B = rng.standard_normal((N, K) if tb else (K, N))
+    C0 = rng.standard_normal((M, N))
+    dA, dB, dC = _dev(A, cuda), _dev(B, cuda), _dev(C0, cuda)
+    _lib.call("sp_gemm", ta, tb, M, N, K, 1.5, dA.data_ptr(), A.shape[1], dB.data_ptr(), B.shape[1], -0.5,
+              dC.data_ptr(), N, _stream(cuda))
+    want = 1.5 * (A.T if ta else A) @ (B.T if tb else B) - 0.5 * C0
+    np.testing.assert_allclose(dC.cpu().numpy(), want, rtol=0, atol=1e-12 * np.sqrt(K) * 8)
+
+
+# ------------------------------------------------------------------ K4 ----
+@pytest.mark.parametrize("rows,cols", [(1000, 8), (5000, 32), (70000, 20), (300, 64), (2000, 100), (32, 32)])
+def test_tsqr(cuda, rows, cols):
+    x = philox(rows + cols).standard_normal((rows, cols)) * np.logspace(0, -8, cols)
+    dx = _dev(x, cuda)
+    q = cuda.empty((rows, cols), dtype=cuda.float64, device="cuda")
+    r = cuda.empty((cols, cols), dtype=cuda.float64, device="cuda")
+    _lib.call("sp_tsqr", rows, cols, dx.data_ptr(), cols, q.data_ptr(), cols, r.data_ptr(), cols, _stream(cuda))
+    q, r = q.cpu().numpy(), r.cpu().numpy()
+    assert np.abs(q.T @ q - np.eye(cols)).max() < 1e-13
+    assert np.linalg.norm(q @ r - x) <= 1e-14 * np.linalg.norm(x) * np.sqrt(rows)
+    assert np.allclose(np.tril(r, -1), 0)
+    assert np.all(np.diag(r) >= 0)
+
+
+def test_tsqr_rank_deficient_keeps_orthonormality(cuda):
+    x = rank_deficient(philox(4), 3000, 40, 5)
+    dx = _dev(x, cuda)
+    q = cuda.empty((3000, 40), dtype=cuda.float64, device="cuda")
+    r = cuda.empty((40, 40), dtype=cuda.float64, device="cuda")
+    _lib.call("sp_tsqr", 3000, 40, dx.data_ptr(), 40, q.data_ptr(), 40, r.data_ptr(), 40, _stream(cuda))
+    q, r = q.cpu().numpy(), r.cpu().numpy()
+    assert np.abs(q.T @ q - np.eye(40)).max() < 1e-12
+    assert np.linalg.norm(q @ r - x) <= 1e-13 * np.linalg.norm(x)
+
+
+# ------------------------------------------------------------------ K5 ----
+@pytest.mark.parametrize("n", [1, 2, 7, 32, 64, 120, 200])
+def test_jacobi_svd(cuda, n):
+    rng = philox(n)
+    m = rng.standard_normal((n, n)) @ np.diag(np.logspace(0, -10, n))
+    dm = _dev(m, cuda)
+    u = cuda.zeros((n, n), dtype=cuda.float64, device="cuda")
+    s = cuda.zeros((n,), dtype=cuda.float64, device="cuda")
+    v = cuda.zeros((n, n), dtype=cuda.float64, device="cuda")
+    _lib.call("sp_jacobi_svd", n, dm.data_ptr(), n, u.data_ptr(), n, s.data_ptr(), v.data_ptr(), n, _stream(cuda))
+    u, s, v = u.cpu().numpy(), s.cpu().numpy(), v.cpu().numpy()
+    want = np.linalg.svd(m, compute_uv=False)
+    assert np.all(np.diff(s) <= 0)
+    np.testing.assert_allclose(s, want, rtol=1e-12 * n, atol=1e-15 * want[0] * n)
+    np.testing.assert_allclose((u * s) @ v.T, m, atol=1e-14 * want[0] * n)
+    np.testing.assert_allclose(v.T @ v, np.eye(n), atol=1e-13)
+
+
+# ------------------------------------------------------ API dense kernels ----
+@pytest.mark.parametrize("shape", [(5, 7), (7, 5), (20, 11), (50, 80), (80, 50), (3000, 40)])
+def test_thin_qr_matches_reference_convention(cuda, shape):
+    m = philox(sum(shape)).standard_normal(shape)
+    fac = sp.thin_qr(m)
+    q_ref, r_ref = oracle.qr_reduced(m)
+    # unique for full rank once the sign convention is applied
+    np.testing.assert_allclose(fac.q, q_ref, atol=1e-12)
+    np.testing.assert_allclose(fac.r, r_ref, atol=1e-12 * np.abs(r_ref).max())
+
+
+@pytest.mark.parametrize("shape", [(5, 7), (12, 9), (50, 80), (2000, 30)])
+def test_thin_svd_matches_reference_convention(cuda, shape):
+    m = philox(shape[0]).standard_normal(shape)
+    fac = sp.thin_svd(m)
+    u_ref, s_ref, v_ref = oracle.svd_thin(m)
+    np.testing.assert_allclose(fac.s, s_ref, rtol=1e-13)
+    np.testing.assert_allclose(fac.u, u_ref, atol=1e-11)
+    np.testing.assert_allclose(fac.v, v_ref, atol=1e-11)
+
+
+def test_pinv_apply(cuda):
+    np.testing.assert_allclose(sp.pinv_apply(np.array([2.0, 1.0, 0.0])), [0.5, 1.0, 0.0])
+    np.testing.assert_allclose(sp.pinv_apply(np.array([1.0, 1e-18])), [1.0, 0.0])
+    np.testing.assert_array_equal(sp.pinv_apply(np.zeros(3)), np.zeros(3))
+    with pytest.raises(sp.ConfigError):
+        sp.pinv_apply(np.array([1.0, 2.0]))
+
+
+# ------------------------------------------------------------------ K7 ----
+def test_pivoted_qr_golden_and_oracle(cuda):
+    g = load_golden("small_cases.npz")
+    m = philox(12).standard_normal((10, 8)) * np.logspace(0, -3, 8)
+    f = sp.pivoted_qr(m, 6)
+    assert np.array_equal(f.perm, g["pq_perm"])
+    np.testing.assert_allclose(f.r, g["pq_r"], atol=1e-13)
+    np.testing.assert_allclose(f.q, g["pq_q"], atol=1e-13)
+
+
+def test_pivoted_qr_duplicate_columns_tie_break(cuda):
+    base = philox(10).standard_normal(4)
+    m = np.column_stack([base, base, 2.0 * base, base])
+    fac = sp.pivoted_qr(m, 2)
+    assert fac.perm[0] == 2 and fac.perm[1] == 0
+
+
+@pytest.mark.parametrize("rows,cols,k", [(64, 300, 40), (200, 1000, 100), (9, 6, 6)])
+def test_pivoted_qr_matches_oracle_pivots(cuda, rows, cols, k):
+    m = philox(rows * cols).standard_normal((rows, cols)) * np.logspace(0, -2, cols)
+    f = sp.pivoted_qr(m, k)
+    q_o, r_o, perm_o = oracle.greedy_pivoted_qr(m, k)
+    gaps = oracle.pivot_gaps(m, k)
+    pstar = k if np.all(gaps > 1e-11) else int(np.argmax(gaps <= 1e-11))
+    assert np.array_equal(f.perm[:pstar], perm_o[:pstar])
+    np.testing.assert_allclose(f.q @ f.r, m[:, f.perm], atol=1e-10 * np.linalg.norm(m)) if k == min(rows, cols) else None
+
+
+def test_row_id_golden(cuda):
+    g = load_golden("small_cases.npz")
+    m = philox(1).standard_normal((9, 5))
+    f = sp.row_id(m, 3)
+    assert np.array_equal(f.indices, g["rid_idx"])
+    np.testing.assert_allclose(f.p, g["rid_p"], atol=1e-12)
+    np.testing.assert_array_equal(f.p[f.indices], np.eye(3))
+    h = sp.row_id(np.array([[1.0, 2.0], [2.0, 4.0]]), 1)
+    np.testing.assert_array_equal(h.indices, [1])
+    np.testing.assert_allclose(h.p, [[0.5], [1.0]])
