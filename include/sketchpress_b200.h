@@ -113,6 +113,13 @@ int sp_gemm(int32_t trans_a, int32_t trans_b, int64_t M, int64_t N, int64_t K, d
 int sp_tsqr(int64_t rows, int64_t cols, const double* X, int64_t ldx,
             double* Q, int64_t ldq, double* R, int64_t ldr, void* stream);
 
+/* Tall QR with a conditioning hint: well_conditioned != 0 (caller certifies
+ * kappa(X) < ~1e6, cols <= 112) runs CholeskyQR2 (Gram + Cholesky on the DMMA
+ * GEMM, two passes), falling back to Householder TSQR on breakdown;
+ * otherwise Householder TSQR.  Synchronises once on the CholeskyQR2 path. */
+int sp_qr_tall(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq,
+               double* R, int64_t ldr, int32_t well_conditioned, void* stream);
+
 /* thin_qr (src/kernels.py:74-84): reduced QR of any rows x cols matrix with
  * the reference sign convention (src/kernels.py:52-71).  Q is rows x p,
  * R is p x cols with p = min(rows, cols).  Requires p <= 256. */

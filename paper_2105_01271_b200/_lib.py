@@ -42,6 +42,7 @@ SIGNATURES = {
     "sp_skinny_atz": [_P, _I32, _I64, _I64, _I64, _P, _I64, _I32, _P, _I64, _P],
     "sp_gemm": [_I32, _I32, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64, _P],
     "sp_tsqr": [_I64, _I64, _P, _I64, _P, _I64, _P, _I64, _P],
+    "sp_qr_tall": [_I64, _I64, _P, _I64, _P, _I64, _P, _I64, _I32, _P],
     "sp_thin_qr": [_I64, _I64, _P, _I64, _P, _I64, _P, _I64, _P],
     "sp_jacobi_svd": [_I64, _P, _I64, _P, _I64, _P, _P, _I64, _P],
     "sp_thin_svd": [_I64, _I64, _P, _I64, _P, _I64, _P, _P, _I64, _P],

@@ -70,6 +70,11 @@ int sp_tsqr(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q,
   return tsqr(rows, cols, X, ldx, Q, ldq, R, ldr, ST(stream));
 }
 
+int sp_qr_tall(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq, double* R,
+               int64_t ldr, int32_t well_conditioned, void* stream) {
+  return qr_tall(rows, cols, X, ldx, Q, ldq, R, ldr, well_conditioned != 0, ST(stream));
+}
+
 int sp_thin_qr(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq,
                double* R, int64_t ldr, void* stream) {
   return thin_qr(rows, cols, X, ldx, Q, ldq, R, ldr, ST(stream));

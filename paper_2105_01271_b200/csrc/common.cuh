@@ -58,6 +58,8 @@ inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 constexpr int kNumSMs = 148;
 
 // ------------------------------------------------------- device helpers ----
+__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -87,9 +89,24 @@ __device__ __forceinline__ double hash_uniform(uint64_t seed, uint64_t i) {
 // Stream-ordered scratch from the default CUDA mempool (cudaMallocAsync);
 // everything allocated through one Arena is released on the same stream when
 // the Arena goes out of scope.
+// Keep freed workspace in the device's default pool across synchronisations
+// (the default release threshold of 0 would hand it back to the driver at
+// every sync and re-map it on the next cudaMallocAsync).
+inline void retain_pool_memory() {
+  static int done[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = 1;
+}
+
 class Arena {
  public:
-  explicit Arena(cudaStream_t s) : stream_(s) {}
+  explicit Arena(cudaStream_t s) : stream_(s) { retain_pool_memory(); }
   ~Arena() {
     for (int i = 0; i < n_; ++i) cudaFreeAsync(ptrs_[i], stream_);
   }

@@ -47,12 +47,22 @@ jacobi_kernel(int n, int np, const double* __restrict__ M, int64_t ldm, double* 
   double* Vm = use_smem ? dyn + np * np : gV;
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int warp = tid >> 5, lane = tid & 31, nwarps = nthr >> 5;
+  __shared__ double fro_part[32];
+  double fro = 0.0;
   for (int e = tid; e < np * np; e += nthr) {
     const int c = e / np, i = e % np;
-    W[e] = (i < n && c < n) ? M[(int64_t)i * ldm + c] : 0.0;
+    const double x = (i < n && c < n) ? M[(int64_t)i * ldm + c] : 0.0;
+    W[e] = x;
+    fro = fma(x, x, fro);
     Vm[e] = (i == c) ? 1.0 : 0.0;
   }
+  fro = warp_sum(fro);
+  if (lane == 0) fro_part[warp] = fro;
   __syncthreads();
+  fro = 0.0;
+  for (int w = 0; w < nwarps; ++w) fro += fro_part[w];
+  // columns below 1e-15 ||M||_F are rounding noise: never rotate two of them
+  const double negl = 1e-30 * fro;
   for (int sweep = 0; sweep < kJacMaxSweeps; ++sweep) {
     if (tid == 0) rot_count = 0;
     __syncthreads();
@@ -72,7 +82,7 @@ jacobi_kernel(int n, int np, const double* __restrict__ M, int64_t ldm, double* 
         a = warp_sum(a);
         b = warp_sum(b);
         g = warp_sum(g);
-        if (g != 0.0 && fabs(g) > kJacTol * sqrt(a) * sqrt(b)) {
+        if (g != 0.0 && fmin(a, b) > negl && fabs(g) > kJacTol * sqrt(a) * sqrt(b)) {
           const double zeta = (b - a) / (2.0 * g);
           double t;
           if (fabs(zeta) > 1e150)

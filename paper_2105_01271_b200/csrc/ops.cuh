@@ -18,6 +18,10 @@ int gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const do
          cudaStream_t s);
 int tsqr(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq,
          double* R, int64_t ldr, cudaStream_t s);
+int cholqr2(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq,
+            double* R, int64_t ldr, bool* breakdown, cudaStream_t s);
+int qr_tall(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq, double* R,
+            int64_t ldr, bool well_conditioned, cudaStream_t s);
 int jacobi_svd(int64_t n, const double* M, int64_t ldm, double* U, int64_t ldu, double* S,
                double* V, int64_t ldv, cudaStream_t s);
 int transpose(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Y, int64_t ldy,

@@ -105,6 +105,10 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
         break;
       }
       bool conv = false;
+      // One Rayleigh-Ritz step already resolves the kept triplets to
+      // (sigma_{b+1}/sigma_kept)^2 when the spectrum has fallen to the
+      // rounding floor inside the block (oversampling 8): accept it.
+      if (itn == 0 && kept > 0 && b - 8 > kept && hs[b - 8] <= 1e-8 * hs[kept - 1]) conv = true;
       if (itn >= 1 && kept == kept_prev) {
         conv = true;
         const int chk = std::min(b, kept + 1);
@@ -151,7 +155,7 @@ static int complete_basis(int64_t N, int r, int k, double* out, int64_t ldo, uin
   SPB_ALLOC(ar, double, Rc, (size_t)k * k);
   if (r > 0) SPB_TRY(copy2d(N, r, out, ldo, W, k, s));
   SPB_TRY(fill_uniform(N, k - r, W + r, k, seed, s));
-  SPB_TRY(tsqr(N, k, W, k, Qc, k, Rc, k, s));
+  SPB_TRY(qr_tall(N, k, W, k, Qc, k, Rc, k, /*well_conditioned=*/true, s));
   SPB_TRY(copy2d(N, k - r, Qc + r, k, out + r, ldo, s));
   return SP_OK;
 }
@@ -159,7 +163,8 @@ static int complete_basis(int64_t N, int r, int k, double* out, int64_t ldo, uin
 // Given the kept left basis Z (m x r, ld ldz) of the sketch, one read of A:
 // Y = A^T Z, then the rank-k SVD of Z Z^T A written to U (m x k), S, V (n x k).
 static int finish_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, const double* Z,
-                      int64_t ldz, int r, int k, double* U, double* S, double* V, cudaStream_t s) {
+                      int64_t ldz, int r, int k, double* U, double* S, double* V, double kappa_est,
+                      cudaStream_t s) {
   Arena ar(s);
   SPB_CUDA(cudaMemsetAsync(S, 0, k * sizeof(double), s));
   const int kk = std::min(r, k);
@@ -174,7 +179,8 @@ static int finish_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t 
     SPB_ALLOC(ar, double, Uf, (size_t)m * r);
     SPB_ALLOC(ar, double, Vf, (size_t)n * r);
     SPB_TRY(skinny_atz(A, a_dtype, m, n, lda, Z, ldz, r, Y, r, s));     // the A pass
-    SPB_TRY(tsqr(n, r, Y, r, Qy, r, Ry, r, s));
+    // kappa(Y) ~ the kept spectral range: CholeskyQR2 below 1e6, else Householder
+    SPB_TRY(qr_tall(n, r, Y, r, Qy, r, Ry, r, kappa_est < 1e6, s));
     SPB_TRY(transpose(r, r, Ry, r, Ryt, r, s));
     SPB_TRY(jacobi_svd(r, Ryt, r, Us, r, Sr, Vs, r, s));                  // Ry^T = Us Sr Vs^T
     SPB_TRY(gemm(0, 0, m, r, r, 1.0, Z, ldz, Us, r, 0.0, Uf, r, s));      // U = Z Us
@@ -264,9 +270,10 @@ int single_pass_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t ld
   }
   SPB_TRY(check_finite(m, out_dim, s0, out_dim, "QR input contains non-finite entries", s));
   TopSvd top;
-  SPB_TRY(svd_top(s0, m, out_dim, out_dim, k, 1.0, top, ar, s));
+  SPB_TRY(svd_top(s0, m, out_dim, out_dim, 1, 1.0, top, ar, s));
   const int r = top.kept;
-  SPB_TRY(finish_svd(A, a_dtype, m, n, lda, top.U, top.b, r, k, U, S, V, s));
+  const double kappa = (r > 0 && top.hs[r - 1] > 0.0) ? top.hs[0] / top.hs[r - 1] : INFINITY;
+  SPB_TRY(finish_svd(A, a_dtype, m, n, lda, top.U, top.b, r, k, U, S, V, kappa, s));
   const bool healthy = (m >= out_dim) && (r == out_dim);
   fill_info(info, r, healthy ? 0 : SP_WARN_RANK_DEFICIENT, top, l0);
   return SP_OK;
@@ -304,7 +311,14 @@ int power_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, con
   TopSvd top;
   if (same) {
     SPB_TRY(check_finite(m, ncols, C, ncols, "power iterate overflowed; enable re-orthonormalization (reorth)", s));
-    SPB_TRY(svd_top(C, m, ncols, ncols, k, 2.0 * q + 1.0, top, ar, s));
+    SPB_TRY(svd_top(C, m, ncols, ncols, 1, 2.0 * q + 1.0, top, ar, s));
+    // the reference forms G = (C C^T)^q C explicitly and raises once it
+    // overflows (src/power.py:81-85); G is never formed here, so mirror the
+    // condition on its largest singular value sigma_1(C)^(2q+1)
+    if (!top.hs.empty() && !std::isfinite(std::pow(top.hs[0], 2.0 * q + 1.0))) {
+      set_error("power iterate overflowed; enable re-orthonormalization (reorth)");
+      return SP_ENUMERICAL;
+    }
   } else {
     const double* s0 = pre_s0;
     if (!s0) {
@@ -330,10 +344,11 @@ int power_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, con
       SPB_TRY(gemm(0, 0, m, out_dim, ncols, 1.0, C, ncols, T, out_dim, 0.0, G, out_dim, s));
       SPB_TRY(check_finite(m, out_dim, G, out_dim, "power iterate overflowed; enable re-orthonormalization (reorth)", s));
     }
-    SPB_TRY(svd_top(G, m, out_dim, out_dim, k, 1.0, top, ar, s));
+    SPB_TRY(svd_top(G, m, out_dim, out_dim, 1, 1.0, top, ar, s));
   }
   const int r = top.kept;
-  SPB_TRY(finish_svd(A, a_dtype, m, n, lda, top.U, top.b, r, k, U, S, V, s));
+  const double kappa = (r > 0 && top.hs[r - 1] > 0.0) ? top.hs[0] / top.hs[r - 1] : INFINITY;
+  SPB_TRY(finish_svd(A, a_dtype, m, n, lda, top.U, top.b, r, k, U, S, V, kappa, s));
   const bool healthy = (m >= out_dim) && (r == out_dim);
   fill_info(info, r, healthy ? 0 : SP_WARN_RANK_DEFICIENT, top, l0);
   return SP_OK;

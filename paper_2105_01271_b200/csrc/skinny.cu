@@ -127,9 +127,24 @@ __global__ void split_reduce_kernel(const double* __restrict__ P, int S, int64_t
 }
 
 template <int R, typename TA>
+int skinny_tma_launch(const TA* A, int64_t m, int64_t n, int64_t lda, const double* Zc, double* Y, int64_t ldy,
+                      cudaStream_t s);
+bool skinny_tma_ok(const void* A, int a_dtype, int64_t n, int64_t lda);
+int copy2d(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Y, int64_t ldy, cudaStream_t s);
+
+template <int R, typename TA>
 static int launch_skinny_r(const TA* A, int64_t m, int64_t n, int64_t lda, const double* Z,
                            int64_t ldz, double* Y, int64_t ldy, cudaStream_t s) {
   constexpr int V = sizeof(TA) == 8 ? 2 : 4;
+  if (skinny_tma_ok(A, sizeof(TA) == 8 ? SP_F64 : SP_F32, n, lda) && m >= 1 &&
+      !std::getenv("SPB_SKINNY_LEGACY")) {
+    // TMA-streamed persistent path: Z packed contiguously (+ pad for the
+    // 16-byte rounded bulk copy of the last row group)
+    Arena ar(s);
+    SPB_ALLOC(ar, double, Zc, (size_t)m * R + 2);
+    SPB_TRY(copy2d(m, R, Z, ldz, Zc, R, s));
+    return skinny_tma_launch<R, TA>(A, m, n, lda, Zc, Y, ldy, s);
+  }
   const bool vec_ok = (lda % V == 0) && ((reinterpret_cast<uintptr_t>(A) % 16) == 0);
   const int gx = ceil_div(n, (int64_t)kSkThreads * V);
   // split rows so that ~6 CTAs per SM are in flight, with >= 64 rows per strip

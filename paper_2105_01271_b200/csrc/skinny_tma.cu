@@ -1,0 +1,182 @@
+// K2 (TMA version): Y (n x r) = A^T Z with the tiles of A streamed by the TMA
+// bulk-copy engine into a 4-stage shared-memory ring.
+//
+// Persistent, one CTA per SM: CTA b owns the contiguous column slab
+// [b*n/G, (b+1)*n/G) (rounded to 16-byte boundaries) and streams ALL m rows
+// of it, so every CTA does the same amount of work, there is no split-K, no
+// partial buffer and no reduction kernel -- A is read exactly once and Y is
+// written once.  Warp 8 is the producer: one elected lane issues, per stage,
+// 8 row-segment bulk copies of A (cp.async.bulk ... complete_tx) plus the
+// matching 8 rows of Z on a full/empty mbarrier pair.  Warps 0-7 consume:
+// each thread owns 16 bytes of columns (2 x f64 or 4 x f32) and keeps its
+// V x R FP64 accumulator in registers; the Z row is a shared-memory broadcast.
+// Bytes in flight per SM = 4 stages x 32 KB, independent of register pressure.
+#include "async.cuh"
+#include "common.cuh"
+#include "launch_count.cuh"
+
+namespace spb {
+
+constexpr int kTmaConsumers = 256;
+constexpr int kTmaThreads = kTmaConsumers + 32;
+constexpr int kTmaRows = 8;       // rows per stage
+constexpr int kTmaStages = 4;
+constexpr int kTmaRowBytes = kTmaConsumers * 16;  // 4 KB of A per row per tile
+
+template <int R>
+struct TmaLayout {
+  static constexpr int kZStage = kTmaRows * R * 8;                       // bytes of Z per stage
+  static constexpr int kZStagePad = (kZStage + 127) / 128 * 128;
+  static constexpr int kStageBytes = kTmaRows * kTmaRowBytes + kZStagePad;
+  static constexpr int kSmem = kTmaStages * kStageBytes;
+};
+
+template <int R, typename TA>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+skinny_tma_kernel(const TA* __restrict__ A, int64_t m, int64_t n, int64_t lda, const double* __restrict__ Zc,
+                  double* __restrict__ Y, int64_t ldy) {
+  constexpr int V = 16 / sizeof(TA);
+  constexpr int TC = kTmaConsumers * V;  // columns per tile
+  using L = TmaLayout<R>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t full[kTmaStages];
+  __shared__ __align__(8) uint64_t empty[kTmaStages];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  // contiguous, 16-byte aligned column slab of this CTA
+  const int64_t units = n / V;  // n % V == 0 is a launch precondition
+  const int64_t cb = (units * blockIdx.x / gridDim.x) * V;
+  const int64_t ce = (units * (blockIdx.x + 1) / gridDim.x) * V;
+
+  if (tid == 0) {
+    for (int s = 0; s < kTmaStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kTmaConsumers / 32);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (warp == kTmaConsumers / 32) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t ph = 0;
+      for (int64_t c0 = cb; c0 < ce; c0 += TC) {
+        const uint32_t seg = (uint32_t)(imin64(TC, ce - c0) * sizeof(TA));
+        for (int64_t r0 = 0; r0 < m; r0 += kTmaRows) {
+          const int nr = (int)imin64(kTmaRows, m - r0);
+          unsigned char* sb = smem + stage * L::kStageBytes;
+          mbar_wait(&empty[stage], ph ^ 1);
+          const uint32_t zbytes = (uint32_t)(nr * R * 8);
+          mbar_arrive_expect_tx(&full[stage], nr * seg + ((zbytes + 15) / 16) * 16);
+          for (int i = 0; i < nr; ++i)
+            bulk_g2s(sb + i * kTmaRowBytes, A + (r0 + i) * lda + c0, seg, &full[stage]);
+          bulk_g2s(sb + kTmaRows * kTmaRowBytes, Zc + r0 * R, ((zbytes + 15) / 16) * 16, &full[stage]);
+          if (++stage == kTmaStages) {
+            stage = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  int stage = 0;
+  uint32_t ph = 0;
+  for (int64_t c0 = cb; c0 < ce; c0 += TC) {
+    const int64_t col = c0 + (int64_t)tid * V;
+    double acc[V][R];
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+#pragma unroll
+      for (int c = 0; c < R; ++c) acc[v][c] = 0.0;
+    for (int64_t r0 = 0; r0 < m; r0 += kTmaRows) {
+      const int nr = (int)imin64(kTmaRows, m - r0);
+      const unsigned char* sb = smem + stage * L::kStageBytes;
+      const double* zs = reinterpret_cast<const double*>(sb + kTmaRows * kTmaRowBytes);
+      mbar_wait(&full[stage], ph);
+      if (nr == kTmaRows) {
+#pragma unroll
+        for (int i = 0; i < kTmaRows; ++i) {
+          double a[V];
+          if constexpr (V == 2) {
+            const double2 x = *reinterpret_cast<const double2*>(sb + i * kTmaRowBytes + tid * 16);
+            a[0] = x.x;
+            a[1] = x.y;
+          } else {
+            const float4 x = *reinterpret_cast<const float4*>(sb + i * kTmaRowBytes + tid * 16);
+            a[0] = x.x;
+            a[1] = x.y;
+            a[2] = x.z;
+            a[3] = x.w;
+          }
+#pragma unroll
+          for (int c = 0; c < R; ++c) {
+            const double z = zs[i * R + c];
+#pragma unroll
+            for (int v = 0; v < V; ++v) acc[v][c] = fma(a[v], z, acc[v][c]);
+          }
+        }
+      } else {
+        for (int i = 0; i < nr; ++i) {
+          const TA* ap = reinterpret_cast<const TA*>(sb + i * kTmaRowBytes) + tid * V;
+#pragma unroll
+          for (int c = 0; c < R; ++c) {
+            const double z = zs[i * R + c];
+#pragma unroll
+            for (int v = 0; v < V; ++v) acc[v][c] = fma((double)ap[v], z, acc[v][c]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == kTmaStages) {
+        stage = 0;
+        ph ^= 1;
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      if (col + v < ce) {
+#pragma unroll
+        for (int c = 0; c < R; ++c) Y[(col + v) * ldy + c] = acc[v][c];
+      }
+    }
+  }
+}
+
+template <int R, typename TA>
+int skinny_tma_launch(const TA* A, int64_t m, int64_t n, int64_t lda, const double* Zc, double* Y, int64_t ldy,
+                      cudaStream_t s) {
+  using L = TmaLayout<R>;
+  constexpr int V = 16 / sizeof(TA);
+  SPB_CUDA(cudaFuncSetAttribute(skinny_tma_kernel<R, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmem));
+  const int64_t units = n / V;
+  const int grid = (int)std::min<int64_t>(kNumSMs, std::max<int64_t>(1, units / 16));
+  skinny_tma_kernel<R, TA><<<grid, kTmaThreads, L::kSmem, s>>>(A, m, n, lda, Zc, Y, ldy);
+  count_launch();
+  SPB_CHECK_LAUNCH();
+  return SP_OK;
+}
+
+// Preconditions of the bulk-copy path: 16-byte aligned base, row pitch and
+// slab boundaries (n a multiple of the 16-byte vector).
+bool skinny_tma_ok(const void* A, int a_dtype, int64_t n, int64_t lda) {
+  const int es = a_dtype == SP_F64 ? 8 : 4;
+  const int V = 16 / es;
+  return (reinterpret_cast<uintptr_t>(A) % 16 == 0) && ((lda * es) % 16 == 0) && (n % V == 0) && n >= V;
+}
+
+#define SPB_INST(RR)                                                                                       \
+  template int skinny_tma_launch<RR, double>(const double*, int64_t, int64_t, int64_t, const double*, double*, \
+                                             int64_t, cudaStream_t);                                        \
+  template int skinny_tma_launch<RR, float>(const float*, int64_t, int64_t, int64_t, const double*, double*,   \
+                                            int64_t, cudaStream_t);
+SPB_INST(1) SPB_INST(2) SPB_INST(3) SPB_INST(4) SPB_INST(5) SPB_INST(6) SPB_INST(7) SPB_INST(8)
+SPB_INST(9) SPB_INST(10) SPB_INST(11) SPB_INST(12) SPB_INST(13) SPB_INST(14) SPB_INST(15) SPB_INST(16)
+#undef SPB_INST
+
+}  // namespace spb

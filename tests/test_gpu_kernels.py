@@ -73,7 +73,7 @@ def test_grid_injection_indices_bit_exact(cuda):
 
 # ------------------------------------------------------------------ K2 ----
 @pytest.mark.parametrize("r", [1, 3, 7, 8, 16, 24])
-@pytest.mark.parametrize("m,n", [(1000, 4096), (257, 1001), (5, 33)])
+@pytest.mark.parametrize("m,n", [(1000, 4096), (257, 1001), (5, 33), (5, 34), (3, 4096), (2001, 20002)])
 def test_skinny_atz(cuda, r, m, n):
     rng = philox(m * r + n)
     a = rng.standard_normal((m, n))
@@ -130,6 +130,31 @@ def test_tsqr(cuda, rows, cols):
     assert np.linalg.norm(q @ r - x) <= 1e-14 * np.linalg.norm(x) * np.sqrt(rows)
     assert np.allclose(np.tril(r, -1), 0)
     assert np.all(np.diag(r) >= 0)
+
+
+@pytest.mark.parametrize("rows,cols,cond", [(65536, 7, 1e4), (2000, 50, 10.0), (300, 64, 1e5), (5000, 112, 1e3)])
+def test_cholqr2_well_conditioned(cuda, rows, cols, cond):
+    x = philox(rows + cols).standard_normal((rows, cols)) * np.logspace(0, -np.log10(cond), cols)
+    dx = _dev(x, cuda)
+    q = cuda.empty((rows, cols), dtype=cuda.float64, device="cuda")
+    r = cuda.empty((cols, cols), dtype=cuda.float64, device="cuda")
+    _lib.call("sp_qr_tall", rows, cols, dx.data_ptr(), cols, q.data_ptr(), cols, r.data_ptr(), cols, 1,
+              _stream(cuda))
+    q, r = q.cpu().numpy(), r.cpu().numpy()
+    assert np.abs(q.T @ q - np.eye(cols)).max() < 1e-13
+    assert np.linalg.norm(q @ r - x) <= 1e-14 * np.linalg.norm(x) * np.sqrt(cols)
+    assert np.allclose(np.tril(r, -1), 0) and np.all(np.diag(r) > 0)
+
+
+def test_cholqr2_breakdown_falls_back(cuda):
+    x = rank_deficient(philox(9), 2000, 20, 4)
+    dx = _dev(x, cuda)
+    q = cuda.empty((2000, 20), dtype=cuda.float64, device="cuda")
+    r = cuda.empty((20, 20), dtype=cuda.float64, device="cuda")
+    _lib.call("sp_qr_tall", 2000, 20, dx.data_ptr(), 20, q.data_ptr(), 20, r.data_ptr(), 20, 1, _stream(cuda))
+    q, r = q.cpu().numpy(), r.cpu().numpy()
+    assert np.abs(q.T @ q - np.eye(20)).max() < 1e-12
+    assert np.linalg.norm(q @ r - x) <= 1e-13 * np.linalg.norm(x)
 
 
 def test_tsqr_rank_deficient_keeps_orthonormality(cuda):
