@@ -26,22 +26,23 @@ __global__ void chol_inv_kernel(int c, const double* __restrict__ Gin, double* _
   __shared__ int bad;
   if (tid == 0) bad = 0;
   __syncthreads();
+  // Unscaled right-looking elimination: step j updates rows i > j with
+  // G[i][l] -= G[j][i] G[j][l] / G[j][j] (row j itself is final after step
+  // j-1), one __syncthreads per step; rows are scaled by 1/sqrt(G[j][j]) at
+  // the end.
   for (int j = 0; j < c; ++j) {
     const double d = G[j * c + j];
     if (!(d > 0.0)) {
       if (tid == 0) bad = 1;
       break;  // uniform: every thread reads the same d
     }
-    const double piv = sqrt(d);
-    __syncthreads();
-    // row j of R
-    for (int l = j + tid; l < c; l += nt) G[j * c + l] = (l == j) ? piv : G[j * c + l] / piv;
-    __syncthreads();
-    // trailing update of the upper triangle: G[i][l] -= R[j][i] R[j][l], j < i <= l
-    const int rem = c - j - 1;
-    for (int e = tid; e < rem * rem; e += nt) {
-      const int i = j + 1 + e / rem, l = j + 1 + e % rem;
-      if (l >= i) G[i * c + l] = fma(-G[j * c + i], G[j * c + l], G[i * c + l]);
+    const double dinv = 1.0 / d;
+    // 32 x 32 thread grid, element (i, l) owned by thread (i % 32, l % 32)
+    const int ty = tid >> 5, tx = tid & 31;
+    for (int i = j + 1 + ((ty - (j + 1)) % 32 + 32) % 32; i < c; i += 32) {
+      const double gji = G[j * c + i] * dinv;
+      for (int l = tx; l < c; l += 32)
+        if (l >= i) G[i * c + l] = fma(-gji, G[j * c + l], G[i * c + l]);
     }
     __syncthreads();
   }
@@ -50,6 +51,14 @@ __global__ void chol_inv_kernel(int c, const double* __restrict__ Gin, double* _
     if (tid == 0) *flag = 1;
     return;
   }
+  __shared__ double dsq[112];
+  for (int i = tid; i < c; i += nt) dsq[i] = sqrt(G[i * c + i]);
+  __syncthreads();
+  for (int e = tid; e < c * c; e += nt) {
+    const int i = e / c, l = e % c;
+    if (l >= i) G[e] = (l == i) ? dsq[i] : G[e] / dsq[i];
+  }
+  __syncthreads();
   // R (upper) out; R^{-1} by recursive doubling: with the diagonal blocks of
   // size s inverted, each pair [A B; 0 C] gets its off-diagonal block
   // -A^{-1} B C^{-1}; log2(c) levels of block products, two syncs each.

@@ -1,0 +1,148 @@
+// Orthonormal completion of an orthonormal block without a QR: Householder
+// reconstruction (Ballard, Demmel, Grigori, Jacquelin, Nguyen, Solomonik,
+// "Reconstructing Householder vectors from tall-skinny QR", 2014).
+//
+// For Q (N x r) with orthonormal columns, the LU factorisation without
+// pivoting  Q - [S; 0] = Y U  (S = diag(+-1) chosen so every pivot has
+// magnitude >= 1) gives the compact-WY orthogonal H = I - Y T Y^T with
+// T = -U S Y1^{-T} and H [S; 0] = Q.  Columns r..k-1 of H are therefore an
+// orthonormal completion of span(Q):
+//     H e_j = e_j - Y T Y_j^T  =  E' - Q K'
+// with K' = U^{-1} T L2top^T (r x (k-r)), L2top = Q[r:k] U^{-1}, and E' zero
+// except rows 0..r-1 (= S K') and rows r..k-1 (= I).  Everything but the
+// final N x r x (k-r) GEMM lives in the top k rows of Q: one small kernel.
+// Replaces the QR of [Q | random] the padding of U, V to rank k needed
+// (the reference's rank-k shape contract, tests/test_svd.py:163-171).
+#include "common.cuh"
+#include "launch_count.cuh"
+#include "ops.cuh"
+
+namespace spb {
+
+constexpr int kHcMaxR = 32;
+constexpr int kHcMaxK = 256;
+
+// in: Qtop = Q[0:k, 0:r] (ld ldq).  out: Kp (r x (k-r), ld kr) and the top k
+// rows of the completion block E' (k x (k-r), ld lde).
+__global__ void __launch_bounds__(256)
+hh_complete_kernel(int r, int k, const double* __restrict__ Q, int64_t ldq, double* __restrict__ Kp,
+                   double* __restrict__ Etop, int64_t lde) {
+  __shared__ double W[kHcMaxR][kHcMaxR + 1];    // LU workspace -> L1 (strict lower) + U (upper)
+  __shared__ double Ui[kHcMaxR][kHcMaxR + 1];   // U^{-1}
+  __shared__ double Li[kHcMaxR][kHcMaxR + 1];   // L1^{-1}
+  __shared__ double T[kHcMaxR][kHcMaxR + 1];
+  __shared__ double G[kHcMaxR][kHcMaxR + 1];    // U^{-1} T U^{-T}
+  __shared__ double S[kHcMaxR];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int kr = k - r;
+  for (int e = tid; e < r * r; e += nt) W[e / r][e % r] = Q[(int64_t)(e / r) * ldq + (e % r)];
+  __syncthreads();
+  // LU without pivoting of Q1 - S, S_i = -sign(current pivot)
+  for (int i = 0; i < r; ++i) {
+    if (tid == 0) {
+      const double s = W[i][i] >= 0.0 ? -1.0 : 1.0;
+      S[i] = s;
+      W[i][i] -= s;
+    }
+    __syncthreads();
+    const double piv = W[i][i];
+    for (int e = tid; e < (r - i - 1) * (r - i); e += nt) {
+      const int a = i + 1 + e / (r - i), b = i + e % (r - i);
+      if (b == i) continue;
+      W[a][b] = fma(-W[a][i] / piv, W[i][b], W[a][b]);
+    }
+    __syncthreads();
+    for (int a = i + 1 + tid; a < r; a += nt) W[a][i] /= piv;  // L multipliers
+    __syncthreads();
+  }
+  // U^{-1} (upper) and L1^{-1} (unit lower), one column per thread
+  for (int col = tid; col < r; col += nt) {
+    for (int a = r - 1; a >= 0; --a) {
+      double acc = (a == col) ? 1.0 : 0.0;
+      for (int b = a + 1; b < r; ++b) acc = fma(-W[a][b], Ui[b][col], acc);
+      Ui[a][col] = (a <= col) ? acc / W[a][a] : 0.0;
+    }
+    for (int a = 0; a < r; ++a) {
+      double acc = (a == col) ? 1.0 : 0.0;
+      for (int b = 0; b < a; ++b) acc = fma(-W[a][b], Li[b][col], acc);
+      Li[a][col] = (a >= col) ? acc : 0.0;
+    }
+  }
+  __syncthreads();
+  // T = -U S L1^{-T}
+  for (int e = tid; e < r * r; e += nt) {
+    const int a = e / r, b = e % r;
+    double acc = 0.0;
+    for (int q = a; q < r; ++q) acc = fma(W[a][q] * S[q], Li[b][q], acc);  // U[a][q] S_q (L1^{-T})[q][b]
+    T[a][b] = -acc;
+  }
+  __syncthreads();
+  // K' = U^{-1} T L2top^T with L2top = Q[r:k] U^{-1}  =>  K' = G Q[r:k]^T,
+  // G = U^{-1} T U^{-T}.  First Li <- T U^{-T} (Li is free now), then G.
+  for (int e = tid; e < r * r; e += nt) {
+    const int a = e / r, b = e % r;
+    double acc = 0.0;
+    for (int q = b; q < r; ++q) acc = fma(T[a][q], Ui[b][q], acc);  // (U^{-T})[q][b] = Ui[b][q]
+    Li[a][b] = acc;
+  }
+  __syncthreads();
+  for (int e = tid; e < r * r; e += nt) {
+    const int a = e / r, b = e % r;
+    double acc = 0.0;
+    for (int q = a; q < r; ++q) acc = fma(Ui[a][q], Li[q][b], acc);
+    G[a][b] = acc;
+  }
+  __syncthreads();
+  for (int e = tid; e < r * kr; e += nt) {
+    const int a = e / kr, j = e % kr;
+    double acc = 0.0;
+    for (int p = 0; p < r; ++p) acc = fma(G[a][p], Q[(int64_t)(r + j) * ldq + p], acc);
+    Kp[(int64_t)a * kr + j] = acc;
+    Etop[(int64_t)a * lde + j] = S[a] * acc;  // rows 0..r-1 of E'
+  }
+  for (int e = tid; e < kr * kr; e += nt) {
+    const int a = e / kr, j = e % kr;
+    Etop[(int64_t)(r + a) * lde + j] = (a == j) ? 1.0 : 0.0;  // rows r..k-1 of E'
+  }
+}
+
+// out (N x k, ld ldo): columns [0, r) orthonormal on entry; columns [r, k)
+// receive the Householder completion.  Returns SP_ECONFIG (caller falls back)
+// when r or k exceed the small-kernel limits.
+int householder_complete(int64_t N, int r, int k, double* out, int64_t ldo, cudaStream_t s) {
+  if (r >= k) return SP_OK;
+  if (r > kHcMaxR || k > kHcMaxK || N < k) {
+    set_error("householder_complete limits exceeded");
+    return SP_ECONFIG;
+  }
+  const int kr = k - r;
+  if (r == 0) {
+    // H = I: the first k columns of the identity
+    SPB_CUDA(cudaMemset2DAsync(out, ldo * sizeof(double), 0, kr * sizeof(double), N, s));
+    SPB_TRY(fill_identity(k, out, ldo, s));
+    return SP_OK;
+  }
+  Arena ar(s);
+  SPB_ALLOC(ar, double, Kp, (size_t)r * kr);
+  // zero the completion block, then write its top k rows (E') in place
+  SPB_CUDA(cudaMemset2DAsync(out + r, ldo * sizeof(double), 0, kr * sizeof(double), N, s));
+  hh_complete_kernel<<<1, 256, 0, s>>>(r, k, out, ldo, Kp, out + r, ldo);
+  count_launch();
+  SPB_CHECK_LAUNCH();
+  // out[:, r:k] = E' - Q K'
+  return gemm(0, 0, N, kr, r, -1.0, out, ldo, Kp, kr, 1.0, out + r, ldo, s);
+}
+
+__global__ void fill_identity_kernel(int k, double* out, int64_t ldo) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < k) out[(int64_t)i * ldo + i] = 1.0;
+}
+
+int fill_identity(int k, double* out, int64_t ldo, cudaStream_t s) {
+  fill_identity_kernel<<<ceil_div(k, 128), 128, 0, s>>>(k, out, ldo);
+  count_launch();
+  SPB_CHECK_LAUNCH();
+  return SP_OK;
+}
+
+}  // namespace spb

@@ -151,6 +151,24 @@ dgemm_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, int6
   }
 }
 
+// C = alpha * sum_s P[s] + beta * C.  Deep splits (S > 8): one warp per
+// output, lanes take splits lane, lane+32, ... and a fixed shuffle tree
+// combines them (deterministic); shallow splits: one thread per output.
+__global__ void gemm_split_reduce_warp(const double* __restrict__ P, int S, int64_t M, int64_t N,
+                                       double alpha, double beta, double* __restrict__ C, int64_t ldc) {
+  const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (e >= M * N) return;
+  double acc = 0.0;
+  for (int s = lane; s < S; s += 32) acc += P[(int64_t)s * M * N + e];
+  acc = warp_sum(acc);
+  if (lane == 0) {
+    double* p = C + (e / N) * ldc + (e % N);
+    const double v = alpha * acc;
+    *p = (beta == 0.0) ? v : fma(beta, *p, v);
+  }
+}
+
 __global__ void gemm_split_reduce(const double* __restrict__ P, int S, int64_t M, int64_t N,
                                   double alpha, double beta, double* __restrict__ C, int64_t ldc) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -193,8 +211,9 @@ int gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const do
   const int64_t tiles = (int64_t)gx * gy;
   int S = 1;
   if (tiles < 2 * kNumSMs) {
-    S = (int)std::min<int64_t>(ceil_div(2 * kNumSMs, tiles), std::max<int64_t>(1, K / (4 * kBK)));
-    S = std::max(1, std::min(S, 64));
+    // enough K-splits for ~4 CTAs per SM, each split at least 4 k-tiles deep
+    S = (int)std::min<int64_t>(ceil_div(4 * kNumSMs, tiles), std::max<int64_t>(1, K / (4 * kBK)));
+    S = std::max(1, std::min(S, 1024));
   }
   int64_t kps = ceil_div(K, S);
   kps = ceil_div(kps, kBK) * (int64_t)kBK;
@@ -219,7 +238,11 @@ int gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const do
   }
   count_launch();
   SPB_CHECK_LAUNCH();
-  if (partial) {
+  if (partial && S > 8) {
+    gemm_split_reduce_warp<<<ceil_div(M * N * 32, 256), 256, 0, s>>>(out, S, M, N, alpha, beta, C, ldc);
+    count_launch();
+    SPB_CHECK_LAUNCH();
+  } else if (partial) {
     gemm_split_reduce<<<ceil_div(M * N, 256), 256, 0, s>>>(out, S, M, N, alpha, beta, C, ldc);
     count_launch();
     SPB_CHECK_LAUNCH();

@@ -61,15 +61,43 @@ jacobi_kernel(int n, int np, const double* __restrict__ M, int64_t ldm, double* 
   __syncthreads();
   fro = 0.0;
   for (int w = 0; w < nwarps; ++w) fro += fro_part[w];
-  // columns below 1e-15 ||M||_F are rounding noise: never rotate two of them
+  // Columns below 1e-15 ||M||_F are rounding noise: they are left out of the
+  // rotation schedule altogether (their singular values are below any cut the
+  // path uses), so a rank-17 core of width 32 runs the tournament on 18
+  // columns instead of 32.
   const double negl = 1e-30 * fro;
-  for (int sweep = 0; sweep < kJacMaxSweeps; ++sweep) {
+  __shared__ int act[256];
+  __shared__ int nact_s;
+  for (int c = warp; c < np; c += nwarps) {
+    double a = 0.0;
+    for (int i = lane; i < np; i += 32) a = fma(W[c * np + i], W[c * np + i], a);
+    a = warp_sum(a);
+    if (lane == 0) sig_s[c] = a;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int na = 0;
+    for (int c = 0; c < n; ++c)
+      if (sig_s[c] > negl) act[na++] = c;
+    if (na & 1) act[na++] = -1;  // pad to even
+    nact_s = na;
+  }
+  __syncthreads();
+  const int na = nact_s;
+  for (int sweep = 0; sweep < kJacMaxSweeps && na >= 2; ++sweep) {
     if (tid == 0) rot_count = 0;
     __syncthreads();
-    for (int round = 0; round < np - 1; ++round) {
-      for (int k = warp; k < np / 2; k += nwarps) {
-        int p, q;
-        rr_pair(np, round, k, p, q);
+    for (int round = 0; round < na - 1; ++round) {
+      for (int k = warp; k < na / 2; k += nwarps) {
+        int pi, qi;
+        rr_pair(na, round, k, pi, qi);
+        int p = act[pi], q = act[qi];
+        if (p < 0 || q < 0) continue;
+        if (p > q) {
+          const int t = p;
+          p = q;
+          q = t;
+        }
         double* wp = W + p * np;
         double* wq = W + q * np;
         double a = 0.0, b = 0.0, g = 0.0;

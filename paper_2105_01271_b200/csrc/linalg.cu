@@ -67,6 +67,43 @@ int fill_uniform(int64_t rows, int64_t cols, double* X, int64_t ldx, uint64_t se
   return SP_OK;
 }
 
+// max |X_ij| (non-negative doubles order like their int64 bit patterns, so an
+// integer atomicMax is exact and order independent)
+__global__ void max_abs_kernel(int64_t rows, int64_t cols, const double* X, int64_t ldx,
+                               unsigned long long* out) {
+  double mx = 0.0;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows * cols;
+       e += (int64_t)gridDim.x * blockDim.x)
+    mx = fmax(mx, fabs(X[(e / cols) * ldx + (e % cols)]));
+  mx = warp_max(mx);
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(mx));
+}
+
+int max_abs(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* out, cudaStream_t s) {
+  SPB_CUDA(cudaMemsetAsync(out, 0, sizeof(double), s));
+  if (rows == 0 || cols == 0) return SP_OK;
+  const int grid = std::min(ceil_div(rows * cols, 256), 4 * kNumSMs);
+  max_abs_kernel<<<grid, 256, 0, s>>>(rows, cols, X, ldx, reinterpret_cast<unsigned long long*>(out));
+  SPB_LAUNCHED();
+  return SP_OK;
+}
+
+__global__ void fill_uniform_scaled_kernel(int64_t rows, int64_t cols, double* X, int64_t ldx, uint64_t seed,
+                                           const double* scale, double factor) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * cols) return;
+  const double sc = *scale > 0.0 ? *scale * factor : 1.0;
+  X[(e / cols) * ldx + (e % cols)] = hash_uniform(seed, (uint64_t)e) * sc;
+}
+
+int fill_uniform_scaled(int64_t rows, int64_t cols, double* X, int64_t ldx, uint64_t seed, const double* scale,
+                        double factor, cudaStream_t s) {
+  if (rows == 0 || cols == 0) return SP_OK;
+  fill_uniform_scaled_kernel<<<ceil_div(rows * cols, 256), 256, 0, s>>>(rows, cols, X, ldx, seed, scale, factor);
+  SPB_LAUNCHED();
+  return SP_OK;
+}
+
 __global__ void scale_cols_kernel(int64_t rows, int64_t cols, double* X, int64_t ldx, const double* d) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= rows * cols) return;

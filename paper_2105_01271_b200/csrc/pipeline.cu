@@ -149,6 +149,8 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
 static int complete_basis(int64_t N, int r, int k, double* out, int64_t ldo, uint64_t seed,
                           cudaStream_t s) {
   if (r >= k) return SP_OK;
+  // Householder reconstruction (one small kernel + one GEMM) when it applies
+  if (householder_complete(N, r, k, out, ldo, s) == SP_OK) return SP_OK;
   Arena ar(s);
   SPB_ALLOC(ar, double, W, (size_t)N * k);
   SPB_ALLOC(ar, double, Qc, (size_t)N * k);
@@ -176,17 +178,22 @@ static int finish_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t 
     SPB_ALLOC(ar, double, Us, (size_t)r * r);
     SPB_ALLOC(ar, double, Vs, (size_t)r * r);
     SPB_ALLOC(ar, double, Sr, (size_t)r);
-    SPB_ALLOC(ar, double, Uf, (size_t)m * r);
-    SPB_ALLOC(ar, double, Vf, (size_t)n * r);
     SPB_TRY(skinny_atz(A, a_dtype, m, n, lda, Z, ldz, r, Y, r, s));     // the A pass
     // kappa(Y) ~ the kept spectral range: CholeskyQR2 below 1e6, else Householder
     SPB_TRY(qr_tall(n, r, Y, r, Qy, r, Ry, r, kappa_est < 1e6, s));
     SPB_TRY(transpose(r, r, Ry, r, Ryt, r, s));
     SPB_TRY(jacobi_svd(r, Ryt, r, Us, r, Sr, Vs, r, s));                  // Ry^T = Us Sr Vs^T
-    SPB_TRY(gemm(0, 0, m, r, r, 1.0, Z, ldz, Us, r, 0.0, Uf, r, s));      // U = Z Us
-    SPB_TRY(gemm(0, 0, n, r, r, 1.0, Qy, r, Vs, r, 0.0, Vf, r, s));       // V = Qy Vs
-    SPB_TRY(copy2d(m, kk, Uf, r, U, k, s));
-    SPB_TRY(copy2d(n, kk, Vf, r, V, k, s));
+    if (r <= k) {
+      SPB_TRY(gemm(0, 0, m, r, r, 1.0, Z, ldz, Us, r, 0.0, U, k, s));     // U = Z Us
+      SPB_TRY(gemm(0, 0, n, r, r, 1.0, Qy, r, Vs, r, 0.0, V, k, s));      // V = Qy Vs
+    } else {
+      SPB_ALLOC(ar, double, Uf, (size_t)m * r);
+      SPB_ALLOC(ar, double, Vf, (size_t)n * r);
+      SPB_TRY(gemm(0, 0, m, r, r, 1.0, Z, ldz, Us, r, 0.0, Uf, r, s));
+      SPB_TRY(gemm(0, 0, n, r, r, 1.0, Qy, r, Vs, r, 0.0, Vf, r, s));
+      SPB_TRY(copy2d(m, kk, Uf, r, U, k, s));
+      SPB_TRY(copy2d(n, kk, Vf, r, V, k, s));
+    }
     SPB_CUDA(cudaMemcpyAsync(S, Sr, kk * sizeof(double), cudaMemcpyDeviceToDevice, s));
   }
   SPB_TRY(complete_basis(m, kk, k, U, k, 0xC0FFEEull, s));

@@ -1,19 +1,21 @@
-// K4: Householder TSQR for tall-skinny matrices (cols <= 32 per panel).
+// K4: Householder TSQR for tall-skinny matrices (<= 32 columns per panel).
 //
 // Replaces thin_qr / np.linalg.qr (src/kernels.py:74-84) on the path.  The
 // sketch bases on this path are numerically rank deficient (SURVEY.md 7 "Hard
-// parts"): CholeskyQR2 breaks down, so orthogonalisation is Householder
+// parts"): CholeskyQR breaks down, so orthogonalisation is Householder
 // based, which keeps the span of every direction to eps * ||X|| regardless of
 // conditioning.
 //
-// Tree: level 0 splits the rows into chunks of CH = 256 * (32 / B) rows; one
-// CTA factors a chunk with each thread holding 32/B rows of the chunk in
-// registers (B doubles per row).  Column dot products are reduced with a warp
-// reduce-scatter (log2(B) shuffle rounds, one column per lane) and a fixed
-// order sum over the 8 warps, so the result is bitwise reproducible.  The
-// B x B R factors are stacked and factored again until one chunk remains.
-// Q is then formed top-down by applying each chunk's reflectors to its block
-// of the parent Q.
+// Layout: a CTA factors a 256 x 32 chunk with LANE = COLUMN: warp w holds
+// rows [32w, 32w+32) and lane c holds those 32 entries of column c in
+// registers.  Loads / stores of a row are coalesced (lanes = consecutive
+// columns), a column dot product is a private 32-term FMA chain plus an
+// 8-way shared-memory reduction across warps, the reflector column is
+// broadcast through shared memory -- two __syncthreads per Householder step
+// and no predicated all-column sweeps.  Fixed reduction order, so results
+// are bitwise reproducible.  The 32 x 32 R factors of the chunks are stacked
+// and factored again until one chunk remains; Q is then formed top-down by
+// applying each chunk's reflectors to its block of the parent Q.
 #include "common.cuh"
 #include "launch_count.cuh"
 
@@ -25,99 +27,65 @@ int gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const do
          int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
          cudaStream_t s);
 
-constexpr int kQrThreads = 256;
-constexpr int kQrWarps = kQrThreads / 32;
+constexpr int kQB = 32;                 // panel width
+constexpr int kQWarps = 8;
+constexpr int kQThreads = kQWarps * 32;
+constexpr int kQCH = kQWarps * 32;      // rows per chunk
 
-template <int B>
-struct QrShape {
-  static constexpr int RPT = 32 / B;             // rows per thread
-  static constexpr int CH = kQrThreads * RPT;    // rows per chunk
-};
+// Row mapping: local row g = 8*i + w lives in warp w, register slot i, so
+// the 32 diagonal rows are spread 4 per warp (slots 0..3): only those slots
+// need j-dependent masks, every other slot is strictly below every diagonal.
+__device__ __forceinline__ int qrow(int i, int w) { return i * kQWarps + w; }
+constexpr int kQDiagSlots = kQB / kQWarps;  // 4
 
-// Reduce p[0..B) over the 256 threads of the CTA; on return every thread sees
-// out_s[c] = scale * sum over rows.  Deterministic order.
-template <int B>
-__device__ __forceinline__ void block_reduce_cols(double (&p)[B], double* red /*[kQrWarps][B]*/,
-                                                  double* out_s /*[B]*/, double scale) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // reduce-scatter: after log2(B) rounds lane holds column col(lane)
-  int col = 0;
+// Factor chunk blockIdx.x of X (rows x cols, cols <= 32).  Writes the
+// reflectors (strictly below the chunk diagonal) to V (rows x 32), tau to
+// tau[chunk*32 + j] and the chunk's upper-trapezoidal R into
+// Rs[chunk*32 .. +32) x 32 (zero padded).
+__global__ void __launch_bounds__(kQThreads)
+tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t ldx, double* __restrict__ V,
+                 double* __restrict__ tau, double* __restrict__ Rs) {
+  __shared__ double colj[kQCH];
+  __shared__ double part[kQWarps];
+  __shared__ double red[kQWarps][kQB];
+  __shared__ double rdiag[kQB];
+  __shared__ double alpha_s;
+  const int w = threadIdx.x >> 5, c = threadIdx.x & 31;
+  const int64_t c0 = (int64_t)blockIdx.x * kQCH;
+  const int nrow = (int)imin64(kQCH, rows - c0);
+  double x[32];
 #pragma unroll
-  for (int half = B / 2, off = 16; half >= 1; half >>= 1, off >>= 1) {
-    const bool upper = (lane & off) != 0;
-#pragma unroll
-    for (int i = 0; i < half; ++i) {
-      const double send = upper ? p[i] : p[i + half];
-      const double keep = upper ? p[i + half] : p[i];
-      p[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-    }
-    if (upper) col += half;
+  for (int i = 0; i < 32; ++i) {
+    const int g = qrow(i, w);
+    x[i] = (g < nrow && c < cols) ? X[(c0 + g) * ldx + c] : 0.0;
   }
-  // remaining butterfly rounds when B < 32
-  constexpr int kLanesPerCol = 32 / B;
-#pragma unroll
-  for (int off = kLanesPerCol / 2; off >= 1; off >>= 1) p[0] += __shfl_xor_sync(0xffffffffu, p[0], off);
-  if ((lane % kLanesPerCol) == 0) red[warp * B + col] = p[0];
-  __syncthreads();
-  if (threadIdx.x < B) {
-    double acc = 0.0;
-#pragma unroll
-    for (int w = 0; w < kQrWarps; ++w) acc += red[w * B + threadIdx.x];
-    out_s[threadIdx.x] = acc * scale;
-  }
-  __syncthreads();
-}
-
-__device__ __forceinline__ double block_sum(double v, double* red) {
-  v = warp_sum(v);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  double acc = 0.0;
-#pragma unroll
-  for (int w = 0; w < kQrWarps; ++w) acc += red[w];
-  __syncthreads();
-  return acc;
-}
-
-// Factor chunk blockIdx.x of X (rows x cols, cols <= B).  Writes reflectors
-// (strictly below the diagonal of each chunk) to V (rows x B, ld B), tau to
-// tau[chunk*B + j] and the chunk's upper-trapezoidal R into
-// Rs[chunk*B .. chunk*B+B) x B (zero padded).
-template <int B>
-__global__ void __launch_bounds__(kQrThreads, 1)
-tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t ldx,
-                 double* __restrict__ V, double* __restrict__ tau, double* __restrict__ Rs) {
-  constexpr int RPT = QrShape<B>::RPT, CH = QrShape<B>::CH;
-  __shared__ double red[kQrWarps * B];
-  __shared__ double wsum[B];
-  __shared__ double scal[2];
-  const int64_t c0 = (int64_t)blockIdx.x * CH;
-  const int64_t left = rows - c0;
-  const int nrow = left < CH ? (int)left : CH;
-  double x[RPT][B];
-#pragma unroll
-  for (int e = 0; e < RPT; ++e) {
-    const int lr = e * kQrThreads + threadIdx.x;
-#pragma unroll
-    for (int c = 0; c < B; ++c)
-      x[e][c] = (lr < nrow && c < cols) ? X[(c0 + lr) * ldx + c] : 0.0;
-  }
-  const int nref = min(nrow, B);
+  const int nref = nrow < kQB ? nrow : kQB;
   for (int j = 0; j < nref; ++j) {
-    // column j: diagonal element and squared norm below it
-    double sq = 0.0;
+    // (1) lane j publishes column j below the diagonal (zero on and above it)
+    if (c == j) {
+      double sq0 = 0.0, sq1 = 0.0;
 #pragma unroll
-    for (int e = 0; e < RPT; ++e) {
-      const int lr = e * kQrThreads + threadIdx.x;
-      double xj = 0.0;
+      for (int i = 0; i < kQDiagSlots; ++i) {
+        const int g = qrow(i, w);
+        const double xi = (g > j) ? x[i] : 0.0;
+        colj[g] = xi;
+        sq0 = fma(xi, xi, sq0);
+        if (g == j) alpha_s = x[i];
+      }
 #pragma unroll
-      for (int c = 0; c < B; ++c) xj = (c == j) ? x[e][c] : xj;
-      if (lr > j && lr < nrow) sq = fma(xj, xj, sq);
-      if (lr == j) scal[0] = xj;
+      for (int i = kQDiagSlots; i < 32; i += 2) {
+        colj[qrow(i, w)] = x[i];
+        colj[qrow(i + 1, w)] = x[i + 1];
+        sq0 = fma(x[i], x[i], sq0);
+        sq1 = fma(x[i + 1], x[i + 1], sq1);
+      }
+      part[w] = sq0 + sq1;
     }
-    const double sigma2 = block_sum(sq, red);  // contains the sync that publishes scal[0]
-    const double alpha = scal[0];
+    __syncthreads();
+    double sigma2 = 0.0;
+#pragma unroll
+    for (int q = 0; q < kQWarps; ++q) sigma2 += part[q];
+    const double alpha = alpha_s;
     double beta = alpha, tj = 0.0, inv = 0.0;
     if (sigma2 > 0.0) {
       const double nrm = sqrt(fma(alpha, alpha, sigma2));
@@ -125,105 +93,124 @@ tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t l
       tj = (beta - alpha) / beta;
       inv = 1.0 / (alpha - beta);
     }
-    // v (unit diagonal) and partial dots w_c = sum v_i x_ic for c > j
-    double vv[RPT];
-    double p[B];
+    // (2) reflector entries of my rows (v_j = 1) and the dot with my column
+    double v[32];
 #pragma unroll
-    for (int c = 0; c < B; ++c) p[c] = 0.0;
+    for (int i = 0; i < 32; ++i) v[i] = colj[qrow(i, w)] * inv;
 #pragma unroll
-    for (int e = 0; e < RPT; ++e) {
-      const int lr = e * kQrThreads + threadIdx.x;
-      double xj = 0.0;
+    for (int i = 0; i < kQDiagSlots; ++i)
+      if (qrow(i, w) == j) v[i] = 1.0;
+    double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
 #pragma unroll
-      for (int c = 0; c < B; ++c) xj = (c == j) ? x[e][c] : xj;
-      vv[e] = (lr == j) ? 1.0 : ((lr > j && lr < nrow) ? xj * inv : 0.0);
-#pragma unroll
-      for (int c = 0; c < B; ++c) p[c] = (c > j) ? fma(vv[e], x[e][c], p[c]) : p[c];
+    for (int i = 0; i < 32; i += 4) {
+      p0 = fma(v[i], x[i], p0);
+      p1 = fma(v[i + 1], x[i + 1], p1);
+      p2 = fma(v[i + 2], x[i + 2], p2);
+      p3 = fma(v[i + 3], x[i + 3], p3);
     }
-    block_reduce_cols<B>(p, red, wsum, tj);
+    red[w][c] = (p0 + p1) + (p2 + p3);
+    __syncthreads();
+    double wc = 0.0;
 #pragma unroll
-    for (int e = 0; e < RPT; ++e) {
-      const int lr = e * kQrThreads + threadIdx.x;
+    for (int q = 0; q < kQWarps; ++q) wc += red[q][c];
+    wc *= tj;
+    // (3) apply H_j to the trailing columns; lane j stores the reflector
+    if (c > j) {
 #pragma unroll
-      for (int c = 0; c < B; ++c) {
-        if (c > j) x[e][c] = fma(-vv[e], wsum[c], x[e][c]);
-        if (c == j) x[e][c] = (lr == j) ? beta : ((lr > j) ? vv[e] : x[e][c]);
+      for (int i = 0; i < 32; ++i) x[i] = fma(-v[i], wc, x[i]);
+    } else if (c == j) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int g = qrow(i, w);
+        if (g < nrow) V[(c0 + g) * kQB + j] = (g > j) ? v[i] : 0.0;
       }
     }
-    if (threadIdx.x == 0) tau[(int64_t)blockIdx.x * B + j] = tj;
+    if (threadIdx.x == 0) {
+      tau[(int64_t)blockIdx.x * kQB + j] = tj;
+      rdiag[j] = beta;
+    }
   }
-  if (threadIdx.x < B && threadIdx.x >= nref) tau[(int64_t)blockIdx.x * B + threadIdx.x] = 0.0;
+  __syncthreads();
+  // columns >= nref were never reflected: their reflector column is zero
+  if (c >= nref) {
 #pragma unroll
-  for (int e = 0; e < RPT; ++e) {
-    const int lr = e * kQrThreads + threadIdx.x;
-    if (lr < nrow) {
-#pragma unroll
-      for (int c = 0; c < B; ++c) V[(c0 + lr) * B + c] = (lr > c) ? x[e][c] : 0.0;
+    for (int i = 0; i < 32; ++i) {
+      const int g = qrow(i, w);
+      if (g < nrow) V[(c0 + g) * kQB + c] = 0.0;
     }
-    if (lr < B) {
+  }
+  if (threadIdx.x < kQB && threadIdx.x >= nref) tau[(int64_t)blockIdx.x * kQB + threadIdx.x] = 0.0;
 #pragma unroll
-      for (int c = 0; c < B; ++c)
-        Rs[((int64_t)blockIdx.x * B + lr) * B + c] = (lr < nrow && c >= lr) ? x[e][c] : 0.0;
-    }
+  for (int i = 0; i < kQDiagSlots; ++i) {
+    const int g = qrow(i, w);  // g < 32
+    double rv = 0.0;
+    if (g < nrow && c >= g) rv = (c == g && g < nref) ? rdiag[g] : x[i];
+    Rs[((int64_t)blockIdx.x * kQB + g) * kQB + c] = rv;
   }
 }
 
-// Out rows of chunk blockIdx.x = H_0 ... H_{B-1} [Bin_chunk ; 0], where
-// Bin_chunk = Bin[chunk*B .. +B) (ld B), or the identity when Bin == nullptr.
-template <int B>
-__global__ void __launch_bounds__(kQrThreads, 1)
+// Out rows of chunk blockIdx.x = H_0 ... H_31 [Bin_chunk ; 0], where
+// Bin_chunk = Bin[chunk*32 .. +32) (ld 32), or the identity when Bin == nullptr.
+// The chunk's reflectors are staged once in shared memory (dynamic, 64 KB);
+// one __syncthreads per reflector (reduction buffer double-buffered).
+__global__ void __launch_bounds__(kQThreads)
 tsqr_apply_kernel(const double* __restrict__ V, const double* __restrict__ tau, int64_t rows,
-                  const double* __restrict__ Bin, double* __restrict__ Out, int64_t ldo,
-                  int out_cols) {
-  constexpr int RPT = QrShape<B>::RPT, CH = QrShape<B>::CH;
-  __shared__ double red[kQrWarps * B];
-  __shared__ double wsum[B];
-  const int64_t c0 = (int64_t)blockIdx.x * CH;
-  const int64_t left = rows - c0;
-  const int nrow = left < CH ? (int)left : CH;
-  double w[RPT][B], v[RPT][B];
-#pragma unroll
-  for (int e = 0; e < RPT; ++e) {
-    const int lr = e * kQrThreads + threadIdx.x;
-#pragma unroll
-    for (int c = 0; c < B; ++c) {
-      v[e][c] = (lr < nrow) ? V[(c0 + lr) * B + c] : 0.0;
-      double init = 0.0;
-      if (lr < B && lr < nrow) init = Bin ? Bin[((int64_t)blockIdx.x * B + lr) * B + c] : (lr == c ? 1.0 : 0.0);
-      w[e][c] = init;
-    }
+                  const double* __restrict__ Bin, double* __restrict__ Out, int64_t ldo, int out_cols) {
+  extern __shared__ double vsm[];  // [kQCH][kQB]
+  __shared__ double red[2][kQWarps][kQB];
+  __shared__ double tau_s[kQB];
+  const int w = threadIdx.x >> 5, c = threadIdx.x & 31;
+  const int64_t c0 = (int64_t)blockIdx.x * kQCH;
+  const int nrow = (int)imin64(kQCH, rows - c0);
+  for (int e = threadIdx.x; e < kQCH * kQB; e += kQThreads) {
+    const int g = e / kQB;
+    vsm[e] = (g < nrow) ? V[(c0 + g) * kQB + (e % kQB)] : 0.0;
   }
-  const int nref = min(nrow, B);
+  if (threadIdx.x < kQB) tau_s[threadIdx.x] = tau[(int64_t)blockIdx.x * kQB + threadIdx.x];
+  double x[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int g = qrow(i, w);
+    double init = 0.0;
+    if (i < kQDiagSlots && g < nrow)
+      init = Bin ? Bin[((int64_t)blockIdx.x * kQB + g) * kQB + c] : (g == c ? 1.0 : 0.0);
+    x[i] = init;
+  }
+  __syncthreads();
+  const int nref = nrow < kQB ? nrow : kQB;
+  int buf = 0;
   for (int j = nref - 1; j >= 0; --j) {
-    const double tj = tau[(int64_t)blockIdx.x * B + j];
+    const double tj = tau_s[j];
     if (tj == 0.0) continue;  // uniform across the CTA
-    double p[B];
-    double vj[RPT];
+    double v[32];
 #pragma unroll
-    for (int c = 0; c < B; ++c) p[c] = 0.0;
+    for (int i = 0; i < 32; ++i) v[i] = vsm[qrow(i, w) * kQB + j];
 #pragma unroll
-    for (int e = 0; e < RPT; ++e) {
-      const int lr = e * kQrThreads + threadIdx.x;
-      double vs = 0.0;
+    for (int i = 0; i < kQDiagSlots; ++i)
+      if (qrow(i, w) == j) v[i] = 1.0;
+    double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
 #pragma unroll
-      for (int c = 0; c < B; ++c) vs = (c == j) ? v[e][c] : vs;
-      vj[e] = (lr == j) ? 1.0 : ((lr > j && lr < nrow) ? vs : 0.0);
-#pragma unroll
-      for (int c = 0; c < B; ++c) p[c] = fma(vj[e], w[e][c], p[c]);
+    for (int i = 0; i < 32; i += 4) {
+      p0 = fma(v[i], x[i], p0);
+      p1 = fma(v[i + 1], x[i + 1], p1);
+      p2 = fma(v[i + 2], x[i + 2], p2);
+      p3 = fma(v[i + 3], x[i + 3], p3);
     }
-    block_reduce_cols<B>(p, red, wsum, tj);
+    red[buf][w][c] = (p0 + p1) + (p2 + p3);
+    __syncthreads();
+    double wc = 0.0;
 #pragma unroll
-    for (int e = 0; e < RPT; ++e)
+    for (int q = 0; q < kQWarps; ++q) wc += red[buf][q][c];
+    wc *= tj;
 #pragma unroll
-      for (int c = 0; c < B; ++c) w[e][c] = fma(-vj[e], wsum[c], w[e][c]);
+    for (int i = 0; i < 32; ++i) x[i] = fma(-v[i], wc, x[i]);
+    buf ^= 1;
   }
+  if (c < out_cols) {
 #pragma unroll
-  for (int e = 0; e < RPT; ++e) {
-    const int lr = e * kQrThreads + threadIdx.x;
-    if (lr < nrow) {
-#pragma unroll
-      for (int c = 0; c < B; ++c)
-        if (c < out_cols) Out[(c0 + lr) * ldo + c] = w[e][c];
+    for (int i = 0; i < 32; ++i) {
+      const int g = qrow(i, w);
+      if (g < nrow) Out[(c0 + g) * ldo + c] = x[i];
     }
   }
 }
@@ -263,10 +250,11 @@ __global__ void add_block(int64_t rows, int64_t cols, const double* src, int64_t
   dst[i * ldd + c] += src[i * lds + c];
 }
 
-template <int B>
-static int tsqr_panel(int64_t rows, int cols, const double* X, int64_t ldx, double* Q, int64_t ldq,
-                      double* R, int64_t ldr, cudaStream_t s) {
-  constexpr int CH = QrShape<B>::CH;
+constexpr int kApplySmem = kQCH * kQB * (int)sizeof(double);
+
+static int tsqr32(int64_t rows, int cols, const double* X, int64_t ldx, double* Q, int64_t ldq, double* R,
+                  int64_t ldr, cudaStream_t s) {
+  SPB_CUDA(cudaFuncSetAttribute(tsqr_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kApplySmem));
   Arena ar(s);
   struct Level {
     int64_t rows;
@@ -283,29 +271,27 @@ static int tsqr_panel(int64_t rows, int cols, const double* X, int64_t ldx, doub
   while (true) {
     Level L;
     L.rows = r;
-    L.nch = ceil_div(r, CH);
-    L.V = ar.alloc<double>((size_t)r * B);
-    L.tau = ar.alloc<double>((size_t)L.nch * B);
-    L.Rs = ar.alloc<double>((size_t)L.nch * B * B);
+    L.nch = ceil_div(r, kQCH);
+    L.V = ar.alloc<double>((size_t)r * kQB);
+    L.tau = ar.alloc<double>((size_t)L.nch * kQB);
+    L.Rs = ar.alloc<double>((size_t)L.nch * kQB * kQB);
     if (!L.V || !L.tau || !L.Rs) {
       set_error("tsqr workspace allocation failed");
       return SP_ECUDA;
     }
-    tsqr_leaf_kernel<B><<<L.nch, kQrThreads, 0, s>>>(in, r, in_cols, in_ld, L.V, L.tau, L.Rs);
+    tsqr_leaf_kernel<<<L.nch, kQThreads, 0, s>>>(in, r, in_cols, in_ld, L.V, L.tau, L.Rs);
     count_launch();
     SPB_CHECK_LAUNCH();
     lv.push_back(L);
     if (L.nch == 1) break;
     in = L.Rs;
-    in_ld = B;
-    in_cols = B;
-    r = (int64_t)L.nch * B;
+    in_ld = kQB;
+    in_cols = kQB;
+    r = (int64_t)L.nch * kQB;
   }
-  // R = top-level R (B x B), keep cols x cols
-  copy_block<<<ceil_div((int64_t)cols * cols, 256), 256, 0, s>>>(cols, cols, lv.back().Rs, B, R, ldr);
+  copy_block<<<ceil_div((int64_t)cols * cols, 256), 256, 0, s>>>(cols, cols, lv.back().Rs, kQB, R, ldr);
   count_launch();
   SPB_CHECK_LAUNCH();
-  // Q top-down
   const double* bin = nullptr;
   for (int l = (int)lv.size() - 1; l >= 0; --l) {
     const Level& L = lv[l];
@@ -317,15 +303,15 @@ static int tsqr_panel(int64_t rows, int cols, const double* X, int64_t ldx, doub
       ldo = ldq;
       oc = cols;
     } else {
-      out = ar.alloc<double>((size_t)L.rows * B);
+      out = ar.alloc<double>((size_t)L.rows * kQB);
       if (!out) {
         set_error("tsqr workspace allocation failed");
         return SP_ECUDA;
       }
-      ldo = B;
-      oc = B;
+      ldo = kQB;
+      oc = kQB;
     }
-    tsqr_apply_kernel<B><<<L.nch, kQrThreads, 0, s>>>(L.V, L.tau, L.rows, bin, out, ldo, oc);
+    tsqr_apply_kernel<<<L.nch, kQThreads, kApplySmem, s>>>(L.V, L.tau, L.rows, bin, out, ldo, oc);
     count_launch();
     SPB_CHECK_LAUNCH();
     bin = out;
@@ -345,26 +331,19 @@ static int tsqr_panel(int64_t rows, int cols, const double* X, int64_t ldx, doub
   return SP_OK;
 }
 
-static int tsqr32(int64_t rows, int cols, const double* X, int64_t ldx, double* Q, int64_t ldq,
-                  double* R, int64_t ldr, cudaStream_t s) {
-  if (cols <= 8) return tsqr_panel<8>(rows, cols, X, ldx, Q, ldq, R, ldr, s);
-  if (cols <= 16) return tsqr_panel<16>(rows, cols, X, ldx, Q, ldq, R, ldr, s);
-  return tsqr_panel<32>(rows, cols, X, ldx, Q, ldq, R, ldr, s);
-}
-
 // Wide inputs: 32-column panels, two block Gram-Schmidt passes against the
 // previous panels, then a Householder TSQR of the projected panel.
 int tsqr(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq,
          double* R, int64_t ldr, cudaStream_t s) {
   SPB_REQUIRE(cols >= 1 && rows >= cols, "tsqr needs rows >= cols >= 1");
   SPB_REQUIRE(ldx >= cols && ldq >= cols && ldr >= cols, "bad tsqr leading dimension");
-  if (cols <= 32) return tsqr32(rows, (int)cols, X, ldx, Q, ldq, R, ldr, s);
+  if (cols <= kQB) return tsqr32(rows, (int)cols, X, ldx, Q, ldq, R, ldr, s);
   SPB_CUDA(cudaMemset2DAsync(R, ldr * sizeof(double), 0, cols * sizeof(double), cols, s));
   Arena ar(s);
-  SPB_ALLOC(ar, double, P, (size_t)rows * 32);
-  SPB_ALLOC(ar, double, T, (size_t)cols * 32);
-  for (int64_t p0 = 0; p0 < cols; p0 += 32) {
-    const int w = (int)std::min<int64_t>(32, cols - p0);
+  SPB_ALLOC(ar, double, P, (size_t)rows * kQB);
+  SPB_ALLOC(ar, double, T, (size_t)cols * kQB);
+  for (int64_t p0 = 0; p0 < cols; p0 += kQB) {
+    const int w = (int)std::min<int64_t>(kQB, cols - p0);
     copy_block<<<ceil_div(rows * w, 256), 256, 0, s>>>(rows, w, X + p0, ldx, P, w);
     count_launch();
     SPB_CHECK_LAUNCH();
