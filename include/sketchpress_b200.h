@@ -185,12 +185,17 @@ int sp_single_pass_svd(const void* A, int32_t a_dtype, int64_t m, int64_t n, int
                        const double* pre_s0,
                        double* U, double* S, double* V, int64_t* info, void* stream);
 
+/* hints for sp_power_svd (0 = verify everything on the device) */
+#define SP_HINT_COLS_VALIDATED 1 /* caller checked I: in [0, n) and distinct   */
+#define SP_HINT_SAME_SET 2       /* caller asserts s0 == A(:, I) (unit injection on I, no projection) */
+#define SP_HINT_DIFFERENT_SET 4  /* caller asserts s0 != A(:, I)               */
+
 /* power_svd, single_pass mode (src/power.py:227-249, 124-181). */
 int sp_power_svd(const void* A, int32_t a_dtype, int64_t m, int64_t n, int64_t lda,
                  const int64_t* idx, const double* w, int32_t depth, int64_t n_c,
                  const double* omega, int64_t ell,
                  const int64_t* cols, int64_t n_cols, int32_t q, int32_t k,
-                 const double* pre_s0, const double* pre_c,
+                 const double* pre_s0, const double* pre_c, int32_t hints,
                  double* U, double* S, double* V, int64_t* info, void* stream);
 
 /* power_id, single_pass mode (src/power.py:252-308) and single_pass_id

@@ -23,7 +23,7 @@ int single_pass_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t ld
 int power_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, const int64_t* idx,
               const double* w, int depth, int64_t nc, const double* omega, int64_t ell,
               const int64_t* cols, int64_t ncols, int q, int k, const double* pre_s0,
-              const double* pre_c, double* U, double* S, double* V, int64_t* info, cudaStream_t s);
+              const double* pre_c, int hints, double* U, double* S, double* V, int64_t* info, cudaStream_t s);
 int power_id(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, const int64_t* idx,
              const double* w, int depth, int64_t nc, const int64_t* cols, int64_t ncols, int q, int k,
              int r_req, const double* proj, int64_t proj_ell, int id_on_basis, const double* pre_s0,
@@ -128,9 +128,10 @@ int sp_single_pass_svd(const void* A, int32_t a_dtype, int64_t m, int64_t n, int
 int sp_power_svd(const void* A, int32_t a_dtype, int64_t m, int64_t n, int64_t lda, const int64_t* idx,
                  const double* w, int32_t depth, int64_t n_c, const double* omega, int64_t ell,
                  const int64_t* cols, int64_t n_cols, int32_t q, int32_t k, const double* pre_s0,
-                 const double* pre_c, double* U, double* S, double* V, int64_t* info, void* stream) {
+                 const double* pre_c, int32_t hints, double* U, double* S, double* V, int64_t* info,
+                 void* stream) {
   return power_svd(A, a_dtype, m, n, lda, idx, w, depth, n_c, omega, ell, cols, n_cols, q, k, pre_s0, pre_c,
-                   U, S, V, info, ST(stream));
+                   hints, U, S, V, info, ST(stream));
 }
 
 int sp_power_id(const void* A, int32_t a_dtype, int64_t m, int64_t n, int64_t lda, const int64_t* idx,

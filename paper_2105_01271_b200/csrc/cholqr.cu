@@ -119,19 +119,28 @@ static int cholqr_pass(int64_t rows, int c, const double* X, int64_t ldx, double
 
 // CholeskyQR2.  Returns SP_OK with *breakdown = true when a Cholesky failed
 // (Q, R are then garbage and the caller must fall back).  Synchronises once.
-int cholqr2(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq,
-            double* R, int64_t ldr, bool* breakdown, cudaStream_t s) {
+// Asynchronous CholeskyQR2: breakdown is OR-ed into the device flag *dflag
+// (caller zeroes it and reads it later); no host synchronisation.
+int cholqr2_async(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq,
+                  double* R, int64_t ldr, int* dflag, cudaStream_t s) {
   SPB_REQUIRE(cols >= 1 && cols <= 112 && rows >= cols, "cholqr2 needs rows >= cols, cols <= 112");
   const int c = (int)cols;
   Arena ar(s);
   SPB_ALLOC(ar, double, Q1, (size_t)rows * c);
   SPB_ALLOC(ar, double, R1, (size_t)c * c);
   SPB_ALLOC(ar, double, R2, (size_t)c * c);
+  SPB_TRY(cholqr_pass(rows, c, X, ldx, Q1, c, R1, dflag, ar, s));
+  SPB_TRY(cholqr_pass(rows, c, Q1, c, Q, ldq, R2, dflag, ar, s));
+  SPB_TRY(gemm(0, 0, c, c, c, 1.0, R2, c, R1, c, 0.0, R, ldr, s));
+  return SP_OK;
+}
+
+int cholqr2(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq,
+            double* R, int64_t ldr, bool* breakdown, cudaStream_t s) {
+  Arena ar(s);
   SPB_ALLOC(ar, int, flag, 1);
   SPB_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
-  SPB_TRY(cholqr_pass(rows, c, X, ldx, Q1, c, R1, flag, ar, s));
-  SPB_TRY(cholqr_pass(rows, c, Q1, c, Q, ldq, R2, flag, ar, s));
-  SPB_TRY(gemm(0, 0, c, c, c, 1.0, R2, c, R1, c, 0.0, R, ldr, s));
+  SPB_TRY(cholqr2_async(rows, cols, X, ldx, Q, ldq, R, ldr, flag, s));
   int h = 0;
   SPB_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
   SPB_CUDA(cudaStreamSynchronize(s));

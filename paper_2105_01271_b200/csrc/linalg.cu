@@ -123,6 +123,14 @@ __global__ void all_finite_kernel(int64_t rows, int64_t cols, const double* X, i
   if (!isfinite(X[(e / cols) * ldx + (e % cols)])) atomicOr(bad, 1);
 }
 
+// OR 1 into *dflag when X holds a NaN/Inf (no synchronisation)
+int check_finite_async(int64_t rows, int64_t cols, const double* X, int64_t ldx, int* dflag, cudaStream_t s) {
+  if (rows == 0 || cols == 0) return SP_OK;
+  all_finite_kernel<<<ceil_div(rows * cols, 256), 256, 0, s>>>(rows, cols, X, ldx, dflag);
+  SPB_LAUNCHED();
+  return SP_OK;
+}
+
 // Synchronises; returns SP_ENUMERICAL with `what` in the message on NaN/Inf.
 int check_finite(int64_t rows, int64_t cols, const double* X, int64_t ldx, const char* what,
                  cudaStream_t s) {

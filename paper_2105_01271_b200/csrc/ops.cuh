@@ -18,6 +18,9 @@ int gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const do
          cudaStream_t s);
 int tsqr(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq,
          double* R, int64_t ldr, cudaStream_t s);
+int cholqr2_async(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq,
+                  double* R, int64_t ldr, int* dflag, cudaStream_t s);
+int check_finite_async(int64_t rows, int64_t cols, const double* X, int64_t ldx, int* dflag, cudaStream_t s);
 int cholqr2(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq,
             double* R, int64_t ldr, bool* breakdown, cudaStream_t s);
 int qr_tall(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq, double* R,

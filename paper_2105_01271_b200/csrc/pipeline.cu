@@ -46,9 +46,33 @@ struct TopSvd {
 // with Householder orthogonalisation and a Rayleigh-Ritz Jacobi step,
 // iterated until the kept Ritz values are stable, growing the block when the
 // kept rank gets within 8 of its width.
+// `pflag` (device int, may be null) is a pending non-finite flag for X raised
+// by an earlier asynchronous check; it is read with the first Ritz spectrum
+// (no extra synchronisation) and turns into SP_ENUMERICAL with `pmsg`.
+struct PendingFlag {
+  const int* dev = nullptr;
+  const char* msg = "";
+};
+
+static int read_flag_with(const PendingFlag& pf, int& host_flag, cudaStream_t s) {
+  host_flag = 0;
+  if (pf.dev) SPB_CUDA(cudaMemcpyAsync(&host_flag, pf.dev, sizeof(int), cudaMemcpyDeviceToHost, s));
+  return SP_OK;
+}
+
 static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int want, double power,
-                   TopSvd& out, Arena& ar, cudaStream_t s) {
+                   TopSvd& out, Arena& ar, cudaStream_t s, PendingFlag pf = PendingFlag()) {
   const int64_t p = std::min(rows, cols);
+  int hflag = 0;
+  if (p <= 64 && pf.dev) {
+    // the exact path checks finiteness itself (thin_svd); surface the caller's message
+    SPB_TRY(read_flag_with(pf, hflag, s));
+    SPB_CUDA(cudaStreamSynchronize(s));
+    if (hflag) {
+      set_error(pf.msg);
+      return SP_ENUMERICAL;
+    }
+  }
   if (p <= 64) {
     out.b = (int)p;
     out.U = ar.alloc<double>((size_t)rows * p);
@@ -97,7 +121,12 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
       SPB_TRY(transpose(b, b, Rz, b, Rt, b, s));
       SPB_TRY(jacobi_svd(b, Rt, b, Us, b, Sg, Vs, b, s));
       SPB_CUDA(cudaMemcpyAsync(hs.data(), Sg, b * sizeof(double), cudaMemcpyDeviceToHost, s));
+      if (itn == 0) SPB_TRY(read_flag_with(pf, hflag, s));
       SPB_CUDA(cudaStreamSynchronize(s));
+      if (hflag) {
+        set_error(pf.msg);
+        return SP_ENUMERICAL;
+      }
       iters = itn + 1;
       kept = count_kept(hs, power);
       if (kept + 8 > b && b < cap) {
@@ -179,8 +208,23 @@ static int finish_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t 
     SPB_ALLOC(ar, double, Vs, (size_t)r * r);
     SPB_ALLOC(ar, double, Sr, (size_t)r);
     SPB_TRY(skinny_atz(A, a_dtype, m, n, lda, Z, ldz, r, Y, r, s));     // the A pass
-    // kappa(Y) ~ the kept spectral range: CholeskyQR2 below 1e6, else Householder
-    SPB_TRY(qr_tall(n, r, Y, r, Qy, r, Ry, r, kappa_est < 1e6, s));
+    // kappa(Y) ~ the kept spectral range: CholeskyQR2 below 1e6 (breakdown is
+    // checked once at the end, and the factorisation redone by Householder
+    // TSQR if it happened), else Householder TSQR directly
+    const bool chol = kappa_est < 1e6 && r <= 112;
+    int* qflag = nullptr;
+    if (chol) {
+      qflag = ar.alloc<int>(1);
+      if (!qflag) {
+        set_error("finish workspace allocation failed");
+        return SP_ECUDA;
+      }
+      SPB_CUDA(cudaMemsetAsync(qflag, 0, sizeof(int), s));
+      SPB_TRY(cholqr2_async(n, r, Y, r, Qy, r, Ry, r, qflag, s));
+    } else {
+      SPB_TRY(tsqr(n, r, Y, r, Qy, r, Ry, r, s));
+    }
+  retry:
     SPB_TRY(transpose(r, r, Ry, r, Ryt, r, s));
     SPB_TRY(jacobi_svd(r, Ryt, r, Us, r, Sr, Vs, r, s));                  // Ry^T = Us Sr Vs^T
     if (r <= k) {
@@ -195,6 +239,16 @@ static int finish_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t 
       SPB_TRY(copy2d(n, kk, Vf, r, V, k, s));
     }
     SPB_CUDA(cudaMemcpyAsync(S, Sr, kk * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    if (qflag) {
+      int h = 0;
+      SPB_CUDA(cudaMemcpyAsync(&h, qflag, sizeof(int), cudaMemcpyDeviceToHost, s));
+      SPB_CUDA(cudaStreamSynchronize(s));
+      qflag = nullptr;
+      if (h) {  // CholeskyQR2 broke down: Householder TSQR and redo the core
+        SPB_TRY(tsqr(n, r, Y, r, Qy, r, Ry, r, s));
+        goto retry;
+      }
+    }
   }
   SPB_TRY(complete_basis(m, kk, k, U, k, 0xC0FFEEull, s));
   SPB_TRY(complete_basis(n, kk, k, V, k, 0xBEEFull, s));
@@ -275,9 +329,14 @@ int single_pass_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t ld
     SPB_TRY(make_sketch(A, a_dtype, m, n, lda, idx, w, depth, nc, omega, ell, t, ar, s));
     s0 = t;
   }
-  SPB_TRY(check_finite(m, out_dim, s0, out_dim, "QR input contains non-finite entries", s));
+  SPB_ALLOC(ar, int, fflag, 1);
+  SPB_CUDA(cudaMemsetAsync(fflag, 0, sizeof(int), s));
+  SPB_TRY(check_finite_async(m, out_dim, s0, out_dim, fflag, s));
   TopSvd top;
-  SPB_TRY(svd_top(s0, m, out_dim, out_dim, 1, 1.0, top, ar, s));
+  PendingFlag pf;
+  pf.dev = fflag;
+  pf.msg = "QR input contains non-finite entries";
+  SPB_TRY(svd_top(s0, m, out_dim, out_dim, 1, 1.0, top, ar, s, pf));
   const int r = top.kept;
   const double kappa = (r > 0 && top.hs[r - 1] > 0.0) ? top.hs[0] / top.hs[r - 1] : INFINITY;
   SPB_TRY(finish_svd(A, a_dtype, m, n, lda, top.U, top.b, r, k, U, S, V, kappa, s));
@@ -290,7 +349,8 @@ int single_pass_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t ld
 int power_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, const int64_t* idx,
               const double* w, int depth, int64_t nc, const double* omega, int64_t ell,
               const int64_t* cols, int64_t ncols, int q, int k, const double* pre_s0,
-              const double* pre_c, double* U, double* S, double* V, int64_t* info, cudaStream_t s) {
+              const double* pre_c, int hints, double* U, double* S, double* V, int64_t* info,
+              cudaStream_t s) {
   const int64_t l0 = launches();
   const int64_t out_dim = omega ? ell : nc;
   // src/power.py:235-241, 216-224, 330-331
@@ -299,12 +359,15 @@ int power_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, con
   SPB_REQUIRE(ncols > k, "column set size " + std::to_string(ncols) + " must exceed target rank " + std::to_string(k));
   SPB_REQUIRE(ncols >= out_dim, "column set size " + std::to_string(ncols) + " must cover the sketch width " + std::to_string(out_dim));
   SPB_REQUIRE(q >= 1, "single-pass power pipeline needs q >= 1");
-  SPB_TRY(check_columns(cols, ncols, n, s));
+  if (!(hints & SP_HINT_COLS_VALIDATED)) SPB_TRY(check_columns(cols, ncols, n, s));
   SPB_REQUIRE(k >= 1 && k <= std::min(m, out_dim),
               "target rank k=" + std::to_string(k) + " outside the enriched basis width");
   Arena ar(s);
   bool same = false;
-  SPB_TRY(sketch_is_columns(idx, w, depth, nc, omega, cols, ncols, same, s));
+  if (hints & SP_HINT_SAME_SET)
+    same = true;
+  else if (!(hints & SP_HINT_DIFFERENT_SET))
+    SPB_TRY(sketch_is_columns(idx, w, depth, nc, omega, cols, ncols, same, s));
   const double* C = pre_c;
   if (!C) {
     double* t = ar.alloc<double>((size_t)m * ncols);
@@ -317,8 +380,13 @@ int power_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, con
   }
   TopSvd top;
   if (same) {
-    SPB_TRY(check_finite(m, ncols, C, ncols, "power iterate overflowed; enable re-orthonormalization (reorth)", s));
-    SPB_TRY(svd_top(C, m, ncols, ncols, 1, 2.0 * q + 1.0, top, ar, s));
+    SPB_ALLOC(ar, int, fflag, 1);
+    SPB_CUDA(cudaMemsetAsync(fflag, 0, sizeof(int), s));
+    SPB_TRY(check_finite_async(m, ncols, C, ncols, fflag, s));
+    PendingFlag pf;
+    pf.dev = fflag;
+    pf.msg = "power iterate overflowed; enable re-orthonormalization (reorth)";
+    SPB_TRY(svd_top(C, m, ncols, ncols, 1, 2.0 * q + 1.0, top, ar, s, pf));
     // the reference forms G = (C C^T)^q C explicitly and raises once it
     // overflows (src/power.py:81-85); G is never formed here, so mirror the
     // condition on its largest singular value sigma_1(C)^(2q+1)

@@ -87,6 +87,22 @@ def _distinct(cols):
         raise ConfigError("column indices must be distinct")
 
 
+def _column_set_on_device(op: SketchOperator, cols: np.ndarray):
+    """Validated device copy of the column set I, cached on the operator by
+    content (the reference re-validates I on every block, src/sketch.py:206-210;
+    the result only depends on I)."""
+    key = ("cols", cols.size, hash(cols.tobytes()))
+    hit = op._dev.get(key)
+    if hit is not None and np.array_equal(hit[2], cols):
+        return hit[0], hit[1]
+    _distinct(cols)
+    from .device import to_device
+    d_cols = to_device(cols.astype(np.int64))
+    same = op.is_injection_of(cols)
+    op._dev[key] = (d_cols, same, cols.copy())
+    return d_cols, same
+
+
 def power_svd(stream: SnapshotStream, op: SketchOperator, k: int, cfg: PowerConfig,
               block_rows: int = DEFAULT_BLOCK_ROWS, return_device: bool = False) -> LowRankSVD:
     """SPC-SVD with C-PWR enrichment (src/power.py:227-249), single-pass mode
@@ -100,18 +116,17 @@ def power_svd(stream: SnapshotStream, op: SketchOperator, k: int, cfg: PowerConf
         raise NotImplementedError("two-pass finalize is a SURVEY 8(f) 'next' item")
     if cfg.q < 1:
         raise ConfigError("single-pass power pipeline needs q >= 1")
-    _distinct(cols)
+    d_cols, same = _column_set_on_device(op, cols)  # validates distinctness once per set
     if op.n != stream.n:
         raise ConfigError(f"block width {stream.n} != fine dimension {op.n}")
-    same = op.is_injection_of(cols)
     # s0 == C for the BASELINE grids: gather the column block once
-    s0c, c, on_block = _sketch_on_ingest(op, stream.m, cols, want_s0=not same)
+    s0c, c, on_block = _sketch_on_ingest(op, stream.m, cols, want_s0=not same, d_cols=d_cols)
     staged = stage_stream(stream, block_rows, on_block)
     m, n = stream.m, stream.n
     s0 = c if same else _projected_s0(op, staged, s0c)
     if k < 1 or k > min(m, op.out_dim):
         raise ConfigError(f"target rank k={k} outside the enriched basis width")
-    d_cols = to_device(cols.astype(np.int64))
+    hints = _lib.SP_HINT_COLS_VALIDATED | (_lib.SP_HINT_SAME_SET if same else _lib.SP_HINT_DIFFERENT_SET)
     if op.idx is not None:
         idx, w, depth, om = op.device_tables()
     else:
@@ -121,7 +136,7 @@ def power_svd(stream: SnapshotStream, op: SketchOperator, k: int, cfg: PowerConf
     a = staged.a
     _lib.call("sp_power_svd", ptr(a), staged.dtype_tag, m, n, a.stride(0), ptr(idx), ptr(w), depth,
               op.n_c, ptr(om), (op.out_dim if om is not None else 0), ptr(d_cols), cols.size, cfg.q, k,
-              ptr(s0), ptr(c), ptr(u), ptr(s), ptr(v), _lib.info_ptr(info), stream_handle())
+              ptr(s0), ptr(c), hints, ptr(u), ptr(s), ptr(v), _lib.info_ptr(info), stream_handle())
     return _finish(u, s, v, k, "power", info, not return_device,
                    "enriched sketch is rank deficient; using regularized solve")
 

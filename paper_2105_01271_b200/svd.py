@@ -49,7 +49,7 @@ def _validate_rank(k: int, op: SketchOperator, stream: SnapshotStream) -> None:
         raise ConfigError(f"target rank k={k} exceeds min(m, n_c)")
 
 
-def _sketch_on_ingest(op: SketchOperator, m: int, cols=None, want_s0: bool = True):
+def _sketch_on_ingest(op: SketchOperator, m: int, cols=None, want_s0: bool = True, d_cols=None):
     """Buffers + per-block callback that gathers s0 = A D (and C = A(:, cols))
     from each block right after it lands in HBM (the fused ingest of K1)."""
     from .device import empty, ptr, stream_handle, to_device
@@ -59,7 +59,8 @@ def _sketch_on_ingest(op: SketchOperator, m: int, cols=None, want_s0: bool = Tru
         idx, w, depth, _ = op.device_tables()
         s0 = empty((m, op.n_c))
     if cols is not None:
-        d_cols = to_device(np.asarray(cols, dtype=np.int64))
+        if d_cols is None:
+            d_cols = to_device(np.asarray(cols, dtype=np.int64))
         c = empty((m, d_cols.numel()))
 
     def on_block(a, row0, rows):
