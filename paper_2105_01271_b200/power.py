@@ -208,8 +208,10 @@ def _run_id(stream, op, k, cols, q, r, block_rows, project_ell, project_seed, on
     lifting = FactoredLifting(left[:, :r_used], right[:r_used], host=not return_device)
     if return_device:
         return RowIDFactors(p=p, indices=ind, skeleton=skel, lifting=lifting, r=r_used, method=method)
-    return RowIDFactors(p=to_host(p), indices=to_host(ind).astype(np.intp), skeleton=to_host(skel),
-                        lifting=lifting, r=r_used, method=method)
+    from .device import to_host_many
+    hp, hind, hskel = to_host_many(p, ind, skel)
+    return RowIDFactors(p=hp, indices=hind.astype(np.intp), skeleton=hskel, lifting=lifting, r=r_used,
+                        method=method)
 
 
 # --------------------------------------------------- literal API helpers ----

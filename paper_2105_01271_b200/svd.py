@@ -101,11 +101,11 @@ def _projected_s0(op: SketchOperator, staged, s0_coarse):
 
 
 def _finish(u, s, v, k, method, info, host, warn_msg):
-    from .device import to_host
+    from .device import to_host_many
     if info[_lib.INFO_WARN] & _lib.SP_WARN_RANK_DEFICIENT:
         warnings.warn(warn_msg, RankDeficiencyWarning, stacklevel=3)
     if host:
-        u, s, v = to_host(u), to_host(s), to_host(v)
+        u, s, v = to_host_many(u, s, v)
     return LowRankSVD(u=u, s=s, v=v, k=k, method=method, kept_rank=int(info[_lib.INFO_KEPT]))
 
 
