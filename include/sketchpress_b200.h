@@ -201,20 +201,22 @@ int sp_power_svd(const void* A, int32_t a_dtype, int64_t m, int64_t n, int64_t l
 /* power_id, single_pass mode (src/power.py:252-308) and single_pass_id
  * (src/rowid.py:142-183, with q = 0 and cols = NULL).  The lifting
  * operator T = V_r S_r^{-1} U_r^T A (src/rowid.py:115-139) is returned
- * FACTORED: lift_left (n_c x r_max, ld r_max) and lift_right (r_max x n, ld n)
- * with the used rank in info[SP_INFO_LIFT_R]; r_max is the caller's buffer
- * width (>= the requested / default r).  `select` (m x sel_w) is the matrix
- * the row selection runs on when the caller precomputed it (projection /
- * id_target="basis"), else NULL.  Outputs: P (m x k), indices (k, int64),
- * skeleton (k x n_c).  r_req <= 0 means the reference default
- * max(k, min(2k, rank)). */
+ * FACTORED: lift_left = V_r S_r^{-1} (n_c x r_max, ld r_max) and, when
+ * non-NULL, lift_right = U_r^T A (r_max x n, ld n) and/or lift_ur = U_r
+ * (m x r_max, ld r_max) -- the right factor can stay implicit (U_r with A)
+ * when r x n does not fit beside A.  The used rank is info[SP_INFO_LIFT_R];
+ * r_max is the caller's buffer width (>= the requested / default r).
+ * project_omega (n_c x project_ell) narrows the selection input; id_on_basis
+ * selects on the leading k left singular vectors of the sketch instead.
+ * Outputs: P (m x k), indices (k, int64), skeleton (k x n_c).  r_req <= 0
+ * means the reference default max(k, min(2k, rank)). */
 int sp_power_id(const void* A, int32_t a_dtype, int64_t m, int64_t n, int64_t lda,
                 const int64_t* idx, const double* w, int32_t depth, int64_t n_c,
                 const int64_t* cols, int64_t n_cols, int32_t q, int32_t k, int32_t r_req,
                 const double* project_omega, int64_t project_ell, int32_t id_on_basis,
                 const double* pre_s0, const double* pre_c,
                 double* P, int64_t* indices, double* skeleton,
-                double* lift_left, double* lift_right, int32_t r_max,
+                double* lift_left, double* lift_right, double* lift_ur, int32_t r_max,
                 int64_t* info, void* stream);
 
 /* ---------------------------------------------------------------- K8 -----

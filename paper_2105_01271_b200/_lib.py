@@ -56,7 +56,7 @@ SIGNATURES = {
     "sp_power_svd": [_P, _I32, _I64, _I64, _I64, _P, _P, _I32, _I64, _P, _I64, _P, _I64, _I32,
                      _I32, _P, _P, _I32, _P, _P, _P, _P, _P],
     "sp_power_id": [_P, _I32, _I64, _I64, _I64, _P, _P, _I32, _I64, _P, _I64, _I32, _I32, _I32,
-                    _P, _I64, _I32, _P, _P, _P, _P, _P, _P, _P, _I32, _P, _P],
+                    _P, _I64, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P, _P],
     "sp_frob_residual": [_P, _I32, _I64, _I64, _I64, _P, _I64, _P, _P, _I64, _I32, _P, _P],
 }
 _RESTYPES = {"sp_last_error": ctypes.c_char_p, "sp_launch_count": ctypes.c_int64}

@@ -28,7 +28,7 @@ int power_id(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, cons
              const double* w, int depth, int64_t nc, const int64_t* cols, int64_t ncols, int q, int k,
              int r_req, const double* proj, int64_t proj_ell, int id_on_basis, const double* pre_s0,
              const double* pre_c, double* P, int64_t* indices, double* skeleton, double* lift_left,
-             double* lift_right, int r_max, int64_t* info, cudaStream_t s);
+             double* lift_right, double* lift_ur, int r_max, int64_t* info, cudaStream_t s);
 int row_id(int64_t m, int64_t cols, const double* M, int64_t ldm, int k, double* P, int64_t* indices,
            int* warn, cudaStream_t s);
 
@@ -138,11 +138,11 @@ int sp_power_id(const void* A, int32_t a_dtype, int64_t m, int64_t n, int64_t ld
                 const double* w, int32_t depth, int64_t n_c, const int64_t* cols, int64_t n_cols, int32_t q,
                 int32_t k, int32_t r_req, const double* project_omega, int64_t project_ell,
                 int32_t id_on_basis, const double* pre_s0, const double* pre_c, double* P,
-                int64_t* indices, double* skeleton, double* lift_left, double* lift_right, int32_t r_max,
-                int64_t* info, void* stream) {
+                int64_t* indices, double* skeleton, double* lift_left, double* lift_right, double* lift_ur,
+                int32_t r_max, int64_t* info, void* stream) {
   return power_id(A, a_dtype, m, n, lda, idx, w, depth, n_c, cols, n_cols, q, k, r_req, project_omega,
-                  project_ell, id_on_basis, pre_s0, pre_c, P, indices, skeleton, lift_left, lift_right, r_max,
-                  info, ST(stream));
+                  project_ell, id_on_basis, pre_s0, pre_c, P, indices, skeleton, lift_left, lift_right, lift_ur,
+                  r_max, info, ST(stream));
 }
 
 int sp_frob_residual(const void* A, int32_t a_dtype, int64_t m, int64_t n, int64_t lda, const double* U,

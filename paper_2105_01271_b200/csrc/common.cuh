@@ -34,7 +34,8 @@ struct Status {
   do {                                                                        \
     cudaError_t _e = cudaGetLastError();                                      \
     if (_e != cudaSuccess) {                                                  \
-      ::spb::set_error(std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+      ::spb::set_error(std::string("kernel launch (") + __FILE__ + ":" + std::to_string(__LINE__) + "): " + \
+                       cudaGetErrorString(_e));                               \
       return SP_ECUDA;                                                        \
     }                                                                         \
   } while (0)

@@ -81,7 +81,9 @@ dgemm_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, int6
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
-  const int64_t m0 = (int64_t)blockIdx.y * kBM, n0 = (int64_t)blockIdx.x * kBN;
+  // linear tile index (grid.x can exceed 65535 tiles for n-row operands)
+  const int64_t tiles_n = (N + kBN - 1) / kBN;
+  const int64_t m0 = ((int64_t)blockIdx.x / tiles_n) * kBM, n0 = ((int64_t)blockIdx.x % tiles_n) * kBN;
   const int64_t kb = (int64_t)blockIdx.z * k_per_split;
   const int64_t ke = min(K, kb + k_per_split);
   const int ntiles = (int)((ke - kb + kBK - 1) / kBK);
@@ -218,7 +220,7 @@ int gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const do
   int64_t kps = ceil_div(K, S);
   kps = ceil_div(kps, kBK) * (int64_t)kBK;
   S = ceil_div(K, kps);
-  dim3 grid(gx, gy, S);
+  dim3 grid((unsigned)tiles, 1, S);
   const bool partial = S > 1;
   Arena ar(s);
   double* out = C;

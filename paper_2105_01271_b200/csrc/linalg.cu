@@ -18,7 +18,8 @@ namespace spb {
 __global__ void transpose_kernel(int64_t rows, int64_t cols, const double* __restrict__ X, int64_t ldx,
                                  double* __restrict__ Y, int64_t ldy) {
   __shared__ double tile[32][33];
-  const int64_t bx = (int64_t)blockIdx.x * 32, by = (int64_t)blockIdx.y * 32;
+  const int64_t tiles_x = (cols + 31) / 32;  // linear tile index: no 65535 limit on either side
+  const int64_t bx = ((int64_t)blockIdx.x % tiles_x) * 32, by = ((int64_t)blockIdx.x / tiles_x) * 32;
   for (int k = threadIdx.y; k < 32; k += 8) {
     const int64_t r = by + k, c = bx + threadIdx.x;
     tile[k][threadIdx.x] = (r < rows && c < cols) ? X[r * ldx + c] : 0.0;
@@ -33,7 +34,7 @@ __global__ void transpose_kernel(int64_t rows, int64_t cols, const double* __res
 int transpose(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Y, int64_t ldy,
               cudaStream_t s) {
   if (rows == 0 || cols == 0) return SP_OK;
-  dim3 g(ceil_div(cols, 32), ceil_div(rows, 32)), b(32, 8);
+  dim3 g((unsigned)((int64_t)ceil_div(cols, 32) * ceil_div(rows, 32))), b(32, 8);
   transpose_kernel<<<g, b, 0, s>>>(rows, cols, X, ldx, Y, ldy);
   SPB_LAUNCHED();
   return SP_OK;

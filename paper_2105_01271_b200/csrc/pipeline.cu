@@ -508,7 +508,7 @@ int power_id(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, cons
              const double* w, int depth, int64_t nc, const int64_t* cols, int64_t ncols, int q, int k,
              int r_req, const double* proj, int64_t proj_ell, int id_on_basis, const double* pre_s0,
              const double* pre_c, double* P, int64_t* indices, double* skeleton, double* lift_left,
-             double* lift_right, int r_max, int64_t* info, cudaStream_t s) {
+             double* lift_right, double* lift_ur, int r_max, int64_t* info, cudaStream_t s) {
   const int64_t l0 = launches();
   SPB_REQUIRE(k <= nc, "target rank k=" + std::to_string(k) + " exceeds sketch width n_c=" + std::to_string(nc));
   if (q > 0 || cols) {
@@ -622,12 +622,12 @@ int power_id(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, cons
     SPB_TRY(pinv_apply(top.S, top.b, kRankTol, sinv, s));
     SPB_TRY(copy2d(nc, r, top.V, top.b, lift_left, r_max, s));
     SPB_TRY(scale_cols(nc, r, lift_left, r_max, sinv, s));
-    if (a_dtype == SP_F64) {
+    if (lift_ur) SPB_TRY(copy2d(m, r, top.U, top.b, lift_ur, r_max, s));
+    if (lift_right && a_dtype == SP_F64) {
       SPB_TRY(gemm(1, 0, r, n, m, 1.0, top.U, top.b, (const double*)A, lda, 0.0, lift_right, n, s));
-    } else {
-      // Y = A^T U_r (n x r) with FP32 A, then transpose
+    } else if (lift_right) {
+      // Y = A^T U_r (n x r) with FP32 A (16-column slabs), then transpose
       SPB_ALLOC(ar, double, Yt, (size_t)n * r);
-      SPB_REQUIRE(r <= 16, "FP32-stored A supports lifting rank <= 16 in this build");
       SPB_TRY(skinny_atz(A, a_dtype, m, n, lda, top.U, top.b, r, Yt, r, s));
       SPB_TRY(transpose(n, r, Yt, r, lift_right, n, s));
     }

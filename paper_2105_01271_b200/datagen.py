@@ -136,6 +136,49 @@ def generate_host(cfg: FieldConfig) -> np.ndarray:
     return out
 
 
+def generate_device(cfg: FieldConfig, device=None, chunk_rows: int = 0):
+    """The same field built on the GPU with FP64 GEMMs (input setup for the
+    configurations too large for the host generator: cfg4 is 84 GB, cfg5
+    134 GB).  Separable evaluation A[i, x, y(, z)] = sum_p Sx[x,p] T_p where
+    T contracts the remaining dimensions; rows are produced in chunks so the
+    FP64 intermediates stay small.  cfg3's noise is drawn on the host in row
+    chunks from the same Philox stream as generate_host (same values).
+    Returns a CUDA tensor (float64, or float32 for dtype "f32")."""
+    import torch
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    S, lam, coef, rng = mode_tables(cfg)
+    t = np.linspace(0.0, 1.0, cfg.m)
+    P = cfg.modes
+    out_dtype = torch.float64 if cfg.dtype == "f64" else torch.float32
+    A = torch.empty((cfg.m, cfg.n), dtype=out_dtype, device=dev)
+    Sd = [torch.from_numpy(s).to(dev) for s in S]
+    lam_d = torch.from_numpy(lam).to(dev)
+    coef_d = torch.from_numpy(coef).to(dev)
+    if chunk_rows <= 0:
+        per_row = cfg.n * 8 * (2 if cfg.dims == 3 else 1)
+        chunk_rows = max(1, min(cfg.m, (2 << 30) // max(per_row, 1)))
+    for r0 in range(0, cfg.m, chunk_rows):
+        r1 = min(cfg.m, r0 + chunk_rows)
+        tt = torch.from_numpy(t[r0:r1]).to(dev)
+        ec = torch.exp(-torch.outer(tt, lam_d) * (np.pi ** 2 * cfg.nu)) * coef_d[None, :]
+        if cfg.dims == 2:
+            T = torch.matmul(ec.view(-1, P, P), Sd[1].t())            # rows x P(p) x gy
+            blk = torch.matmul(Sd[0], T)                               # rows x gx x gy
+        else:
+            T = torch.matmul(ec.view(-1, P * P, P), Sd[2].t())        # rows x (p,q) x gz
+            T = T.view(-1, P, P, cfg.grid[2])
+            T = torch.einsum("yq,rpqz->rpyz", Sd[1], T)                # rows x P x gy x gz
+            blk = torch.einsum("xp,rpyz->rxyz", Sd[0], T)              # rows x gx x gy x gz
+        A[r0:r1] = blk.reshape(r1 - r0, cfg.n).to(out_dtype)
+        del T, blk, ec
+    if cfg.noise_std:
+        for r0 in range(0, cfg.m, 64):
+            r1 = min(cfg.m, r0 + 64)
+            noise = rng.standard_normal((r1 - r0, cfg.n)) * cfg.noise_std
+            A[r0:r1] += torch.from_numpy(noise).to(dev).to(out_dtype)
+    return A
+
+
 def analytic_singular_values(cfg: FieldConfig) -> np.ndarray:
     """sigma(A) of the noise-free field via DST-I orthogonality.
 

@@ -25,7 +25,7 @@ from .errors import ConfigError, NumericalError, RankDeficiencyWarning
 from .kernels import RANK_TOL, thin_qr, thin_svd, pinv_apply
 from .rowid import FactoredLifting, RowIDFactors
 from .sketch import SketchOperator, _rng
-from .snapshot_io import SnapshotStream, stage_stream
+from .snapshot_io import DeviceSnapshotStream, SnapshotStream, stage_stream
 from .svd import DEFAULT_BLOCK_ROWS, LowRankSVD, _finish, _projected_s0, _sketch_on_ingest
 
 SINGLE_PASS = "single_pass"
@@ -187,14 +187,21 @@ def _run_id(stream, op, k, cols, q, r, block_rows, project_ell, project_seed, on
     ind = empty((k,), "i64")
     skel = empty((k, op.n_c))
     left = empty((op.n_c, r_max))
-    right = empty((r_max, n))
+    # U_r^T A (r x n) is materialised unless it would crowd A out of HBM
+    # (cfg5: 200 x 16.8M doubles = 27 GB beside a 134 GB A); then the right
+    # factor stays implicit as (U_r, A) for a device-resident A.
+    from .device import torch as _torch
+    free_b, _ = _torch().cuda.mem_get_info()
+    lazy = isinstance(stream, DeviceSnapshotStream) and r_max * n * 8 > free_b // 3
+    right = None if lazy else empty((r_max, n))
+    ur = empty((m, r_max)) if lazy else None
     info = _lib.new_info()
     d_cols = to_device(np.asarray(cols, dtype=np.int64)) if cols is not None else None
     a = staged.a
     _lib.call("sp_power_id", ptr(a), staged.dtype_tag, m, n, a.stride(0), ptr(idx), ptr(w), depth,
               op.n_c, ptr(d_cols), (0 if cols is None else len(cols)), q, k, r_req, ptr(proj),
               (project_ell or 0), int(on_basis), ptr(s0c), ptr(c), ptr(p), ptr(ind), ptr(skel),
-              ptr(left), ptr(right), r_max, _lib.info_ptr(info), stream_handle())
+              ptr(left), ptr(right), ptr(ur), r_max, _lib.info_ptr(info), stream_handle())
     warn = int(info[_lib.INFO_WARN])
     r_used = int(info[_lib.INFO_LIFT_R])
     rank = int(info[_lib.INFO_RANK])
@@ -205,7 +212,10 @@ def _run_id(stream, op, k, cols, q, r, block_rows, project_ell, project_seed, on
         req = r_req if r_req else max(k, min(2 * k, rank))
         warnings.warn(f"lifting rank {req} clamped to sketch rank {rank}", RankDeficiencyWarning,
                       stacklevel=3)
-    lifting = FactoredLifting(left[:, :r_used], right[:r_used], host=not return_device)
+    if lazy:
+        lifting = FactoredLifting(left[:, :r_used], None, host=not return_device, ur=ur[:, :r_used], a=a)
+    else:
+        lifting = FactoredLifting(left[:, :r_used], right[:r_used], host=not return_device)
     if return_device:
         return RowIDFactors(p=p, indices=ind, skeleton=skel, lifting=lifting, r=r_used, method=method)
     from .device import to_host_many

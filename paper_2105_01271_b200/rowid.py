@@ -25,40 +25,107 @@ ID_ON_BASIS = "basis"
 
 
 class FactoredLifting:
-    """Lazy n_c x n operator left @ right (left: n_c x r, right: r x n)."""
+    """Lazy n_c x n operator T = left @ right, left = V_r S_r^{-1} (n_c x r).
+
+    ``right`` = U_r^T A (r x n) when it was materialised; otherwise it stays
+    implicit as (ur = U_r (m x r), a = the device-resident A) and every product
+    with T streams A through the device kernels.
+    """
 
     __array_priority__ = 1000
 
-    def __init__(self, left, right, host: bool = True):
+    def __init__(self, left, right, host: bool = True, ur=None, a=None):
+        if right is None and (ur is None or a is None):
+            raise ValueError("FactoredLifting needs right, or ur and a")
         self.left = left
         self.right = right
+        self.ur = ur
+        self.a = a
         self.host = host
+        self._cache = {}
 
     @property
     def shape(self):
-        return (self.left.shape[0], self.right.shape[1])
+        n = self.right.shape[1] if self.right is not None else self.a.shape[1]
+        return (self.left.shape[0], n)
 
     @property
     def rank(self) -> int:
         return self.left.shape[1]
 
-    def _h(self, x):
-        return x.detach().cpu().numpy() if hasattr(x, "detach") else x
+    def _h(self, name, x):
+        if not hasattr(x, "detach"):
+            return x
+        if name not in self._cache:
+            from .device import to_host_many
+            self._cache[name] = to_host_many(x)[0]
+        return self._cache[name]
+
+    # ---- implicit right factor: products with A on the device
+    def _mm(self, ta, tb, a, b, M, N, K):
+        from .device import empty, ptr, stream_handle
+        out = empty((M, N))
+        _lib.call("sp_gemm", ta, tb, M, N, K, 1.0, ptr(a), a.shape[1], ptr(b), b.shape[1], 0.0, ptr(out), N,
+                  stream_handle())
+        return out
+
+    def _times_a(self, wt):
+        """w @ A for w = wt^T (rows x m), wt (m x rows): one read of A per call
+        (FP32 A: the A^T Z pass, 16 columns per read)."""
+        from .device import empty, ptr, stream_handle
+        m, n = self.a.shape
+        rows = wt.shape[1]
+        if self.a.dtype.itemsize == 8:
+            return self._mm(1, 0, rows, n, m, wt, self.a)
+        y = empty((n, rows))
+        _lib.call("sp_skinny_atz", ptr(self.a), _lib.SP_F32, m, n, self.a.stride(0), ptr(wt), rows, rows, ptr(y),
+                  rows, stream_handle())
+        return y.t().contiguous()
+
+    def _dev_rmatmul(self, xd):
+        w1 = self._mm(0, 0, xd, self.left, xd.shape[0], self.left.shape[1], xd.shape[1])   # x L
+        if self.right is not None:
+            return self._mm(0, 0, w1, self.right, w1.shape[0], self.right.shape[1], w1.shape[1])
+        wt = self._mm(0, 1, self.ur, w1, self.ur.shape[0], w1.shape[0], self.ur.shape[1])  # U_r (x L)^T
+        return self._times_a(wt)
 
     def __rmatmul__(self, x):
         """x @ T = (x @ left) @ right."""
-        if self.host:
-            return (np.asarray(x) @ self._h(self.left)) @ self._h(self.right)
-        return (x @ self.left) @ self.right
+        if self.right is not None and self.host:
+            return (np.asarray(x) @ self._h("l", self.left)) @ self._h("r", self.right)
+        from .device import is_device_tensor, to_device, to_host
+        xd = x.double().contiguous() if is_device_tensor(x) else to_device(np.atleast_2d(np.asarray(x, np.float64)))
+        out = self._dev_rmatmul(xd)
+        if is_device_tensor(x):
+            return out
+        out = to_host(out)
+        return out[0] if np.asarray(x).ndim == 1 else out
 
     def __matmul__(self, x):
         """T @ x = left @ (right @ x)."""
-        if self.host:
-            return self._h(self.left) @ (self._h(self.right) @ np.asarray(x))
-        return self.left @ (self.right @ x)
+        if self.right is not None:
+            if self.host:
+                return self._h("l", self.left) @ (self._h("r", self.right) @ np.asarray(x))
+            return self.left @ (self.right @ x)
+        if self.a.dtype.itemsize != 8:
+            raise NotImplementedError("T @ x with an implicit right factor needs FP64 A")
+        from .device import is_device_tensor, to_device, to_host
+        xd = x.double() if is_device_tensor(x) else to_device(np.asarray(x, np.float64))
+        col = xd.dim() == 1
+        xd = (xd.reshape(-1, 1) if col else xd).contiguous()
+        ax = self._mm(0, 0, self.a, xd, self.a.shape[0], xd.shape[1], self.a.shape[1])      # A x
+        z = self._mm(1, 0, self.ur, ax, self.ur.shape[1], ax.shape[1], self.ur.shape[0])     # U_r^T A x
+        out = self._mm(0, 0, self.left, z, self.left.shape[0], z.shape[1], z.shape[0])
+        out = out[:, 0] if col else out
+        return out if is_device_tensor(x) else to_host(out)
 
     def __array__(self, dtype=None, copy=None):
-        dense = self._h(self.left) @ self._h(self.right)
+        if self.right is not None:
+            dense = self._h("l", self.left) @ self._h("r", self.right)
+        else:
+            from .device import to_device, to_host
+            eye = to_device(np.eye(self.left.shape[0]))
+            dense = to_host(self._dev_rmatmul(eye))
         return dense if dtype is None else dense.astype(dtype)
 
     def dense(self):
