@@ -164,6 +164,24 @@ int sp_pivoted_qr(int64_t rows, int64_t cols, const double* Mt, int64_t ldmt, in
 int sp_row_id(int64_t m, int64_t cols, const double* M, int64_t ldm, int32_t k, double* P,
               int64_t* indices, int64_t* info, void* stream);
 
+/* Kept left basis of a sketch X (rows x cols): the top singular triplets by
+ * randomized block subspace iteration (Householder TSQR + Jacobi Rayleigh-
+ * Ritz; exact TSQR + Jacobi when min(rows, cols) <= 64) and the reference's
+ * kept-rank rule r = #{(s_i/s_1)^power > 1e-12} (src/kernels.py:19, 158-168;
+ * power = 2q+1 for the power pipeline's G = (C C^T)^q C).  Writes U (rows x
+ * min(r, r_max), ld ldu) and S; info[SP_INFO_KEPT] = r.  Used by the
+ * column-sharded driver on the all-gathered C.  Synchronises. */
+int sp_sketch_basis(const double* X, int64_t rows, int64_t cols, int64_t ldx, double power, int32_t r_max,
+                    double* U, int64_t ldu, double* S, int64_t* info, void* stream);
+
+/* Orthonormal completion of out[:, 0:r) (orthonormal, N x r) into
+ * out[:, r:k) by Householder reconstruction (LU of Q - [S;0]; no QR).  If
+ * kp_out (r x (k-r)) is non-NULL it receives K', so that for a row-sharded Q
+ * every other row block i of the completion is -Q_i K' (the rows 0..k-1 live
+ * in the block this call factors).  Requires r <= 32, k <= 256, N >= k. */
+int sp_householder_complete(int64_t N, int32_t r, int32_t k, double* out, int64_t ldo, double* kp_out,
+                            void* stream);
+
 /* ------------------------------------------------------- pipelines -----
  * Device-resident single-pass pipelines.  A is m x n (lda), the sketch is
  * the stencil table (idx, w: depth x n_c) optionally composed with a dense

@@ -31,6 +31,8 @@ int power_id(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, cons
              double* lift_right, double* lift_ur, int r_max, int64_t* info, cudaStream_t s);
 int row_id(int64_t m, int64_t cols, const double* M, int64_t ldm, int k, double* P, int64_t* indices,
            int* warn, cudaStream_t s);
+int sketch_basis(const double* X, int64_t rows, int64_t cols, int64_t ldx, double power, int r_max, double* U,
+                 int64_t ldu, double* S, int64_t* info, cudaStream_t s);
 
 }  // namespace spb
 
@@ -115,6 +117,16 @@ int sp_row_id(int64_t m, int64_t cols, const double* M, int64_t ldm, int32_t k, 
     info[SP_INFO_LAUNCHES] = launches() - l0;
   }
   return st;
+}
+
+int sp_sketch_basis(const double* X, int64_t rows, int64_t cols, int64_t ldx, double power, int32_t r_max,
+                    double* U, int64_t ldu, double* S, int64_t* info, void* stream) {
+  return sketch_basis(X, rows, cols, ldx, power, r_max, U, ldu, S, info, ST(stream));
+}
+
+int sp_householder_complete(int64_t N, int32_t r, int32_t k, double* out, int64_t ldo, double* kp_out,
+                            void* stream) {
+  return householder_complete(N, r, k, out, ldo, ST(stream), kp_out);
 }
 
 int sp_single_pass_svd(const void* A, int32_t a_dtype, int64_t m, int64_t n, int64_t lda,

@@ -109,7 +109,8 @@ hh_complete_kernel(int r, int k, const double* __restrict__ Q, int64_t ldq, doub
 // out (N x k, ld ldo): columns [0, r) orthonormal on entry; columns [r, k)
 // receive the Householder completion.  Returns SP_ECONFIG (caller falls back)
 // when r or k exceed the small-kernel limits.
-int householder_complete(int64_t N, int r, int k, double* out, int64_t ldo, cudaStream_t s) {
+int householder_complete(int64_t N, int r, int k, double* out, int64_t ldo, cudaStream_t s,
+                         double* kp_out) {
   if (r >= k) return SP_OK;
   if (r > kHcMaxR || k > kHcMaxK || N < k) {
     set_error("householder_complete limits exceeded");
@@ -129,6 +130,8 @@ int householder_complete(int64_t N, int r, int k, double* out, int64_t ldo, cuda
   hh_complete_kernel<<<1, 256, 0, s>>>(r, k, out, ldo, Kp, out + r, ldo);
   count_launch();
   SPB_CHECK_LAUNCH();
+  // sharded callers: the other row blocks of the completion are -Q_i K'
+  if (kp_out) SPB_CUDA(cudaMemcpyAsync(kp_out, Kp, (size_t)r * kr * sizeof(double), cudaMemcpyDeviceToDevice, s));
   // out[:, r:k] = E' - Q K'
   return gemm(0, 0, N, kr, r, -1.0, out, ldo, Kp, kr, 1.0, out + r, ldo, s);
 }

@@ -429,6 +429,32 @@ int power_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, con
   return SP_OK;
 }
 
+// ------------------------------------------------------- sketch basis ----
+// Kept left basis of a sketch-sized X (the svd_top + kept-rank step of the
+// pipelines, exported for the column-sharded driver): U (rows x min(r, r_max)),
+// S; info[KEPT] = r = #{(s_i/s_1)^power > 1e-12}.
+int sketch_basis(const double* X, int64_t rows, int64_t cols, int64_t ldx, double power, int r_max, double* U,
+                 int64_t ldu, double* S, int64_t* info, cudaStream_t s) {
+  const int64_t l0 = launches();
+  SPB_REQUIRE(rows >= 1 && cols >= 1 && r_max >= 1, "sketch_basis needs a non-empty matrix");
+  Arena ar(s);
+  SPB_ALLOC(ar, int, fflag, 1);
+  SPB_CUDA(cudaMemsetAsync(fflag, 0, sizeof(int), s));
+  SPB_TRY(check_finite_async(rows, cols, X, ldx, fflag, s));
+  PendingFlag pf;
+  pf.dev = fflag;
+  pf.msg = "sketch contains non-finite entries";
+  TopSvd top;
+  SPB_TRY(svd_top(X, rows, cols, ldx, 1, power, top, ar, s, pf));
+  const int r = std::min(top.kept, r_max);
+  if (r > 0) {
+    SPB_TRY(copy2d(rows, r, top.U, top.b, U, ldu, s));
+    SPB_CUDA(cudaMemcpyAsync(S, top.S, r * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  }
+  fill_info(info, top.kept, 0, top, l0);
+  return SP_OK;
+}
+
 // ---------------------------------------------------------------- row ID ----
 __global__ void scatter_p_kernel(int64_t m, int k, const int64_t* perm, const double* coef, int64_t ldc,
                                  double* P) {

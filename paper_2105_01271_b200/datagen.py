@@ -136,22 +136,32 @@ def generate_host(cfg: FieldConfig) -> np.ndarray:
     return out
 
 
-def generate_device(cfg: FieldConfig, device=None, chunk_rows: int = 0):
+def generate_device(cfg: FieldConfig, device=None, chunk_rows: int = 0, x_range=None):
     """The same field built on the GPU with FP64 GEMMs (input setup for the
     configurations too large for the host generator: cfg4 is 84 GB, cfg5
     134 GB).  Separable evaluation A[i, x, y(, z)] = sum_p Sx[x,p] T_p where
     T contracts the remaining dimensions; rows are produced in chunks so the
     FP64 intermediates stay small.  cfg3's noise is drawn on the host in row
     chunks from the same Philox stream as generate_host (same values).
-    Returns a CUDA tensor (float64, or float32 for dtype "f32")."""
+    Returns a CUDA tensor (float64, or float32 for dtype "f32").
+
+    ``x_range = (x0, x1)`` builds only the x-slab x0 <= ix < x1 of the grid
+    (columns [x0*g_rest, x1*g_rest) of the full matrix): one rank's shard of
+    the column-sharded layout (noise-free fields only)."""
     import torch
     dev = device or torch.device("cuda", torch.cuda.current_device())
     S, lam, coef, rng = mode_tables(cfg)
     t = np.linspace(0.0, 1.0, cfg.m)
     P = cfg.modes
     out_dtype = torch.float64 if cfg.dtype == "f64" else torch.float32
-    A = torch.empty((cfg.m, cfg.n), dtype=out_dtype, device=dev)
-    Sd = [torch.from_numpy(s).to(dev) for s in S]
+    ncols = cfg.n
+    if x_range is not None:
+        if cfg.noise_std:
+            raise ValueError("x-slab generation is for noise-free fields")
+        S = [S[0][x_range[0]:x_range[1]]] + list(S[1:])
+        ncols = (x_range[1] - x_range[0]) * int(np.prod(cfg.grid[1:]))
+    A = torch.empty((cfg.m, ncols), dtype=out_dtype, device=dev)
+    Sd = [torch.from_numpy(np.ascontiguousarray(s)).to(dev) for s in S]
     lam_d = torch.from_numpy(lam).to(dev)
     coef_d = torch.from_numpy(coef).to(dev)
     if chunk_rows <= 0:
@@ -169,7 +179,7 @@ def generate_device(cfg: FieldConfig, device=None, chunk_rows: int = 0):
             T = T.view(-1, P, P, cfg.grid[2])
             T = torch.einsum("yq,rpqz->rpyz", Sd[1], T)                # rows x P x gy x gz
             blk = torch.einsum("xp,rpyz->rxyz", Sd[0], T)              # rows x gx x gy x gz
-        A[r0:r1] = blk.reshape(r1 - r0, cfg.n).to(out_dtype)
+        A[r0:r1] = blk.reshape(r1 - r0, ncols).to(out_dtype)
         del T, blk, ec
     if cfg.noise_std:
         for r0 in range(0, cfg.m, 64):

@@ -1,0 +1,242 @@
+"""Column-sharded single-pass power SVD across the GPUs of one node
+(SURVEY.md 8(e)).
+
+A is split by contiguous column slabs (x-slabs of the C-order flattened grid:
+rank i owns columns [c_b, c_e)); the coarse-grid points of a slab live on
+that rank, so the gather is local.  Exchange steps (the only NVLink traffic):
+
+1. all-gather of the column blocks C_i -> C (m x |I|, 65 MB at cfg2);
+2. the sketch basis U_{C,r} is computed redundantly and bitwise identically
+   on every rank (deterministic kernels, identical input);
+3. the local A pass Y_i = A_i^T U_r (the HBM-bound kernel, no communication);
+4. TSQR across ranks: local QR Y_i = Q_i R_i, all-gather of the r x r R_i,
+   QR of the stack (redundant), Q_Y,i = Q_i Q_top,i;
+5. the r x r core SVD (redundant); U and S replicated, V stays sharded;
+6. the V completion to rank k: rank 0 (which holds the top k global rows)
+   factors it and broadcasts the r x (k-r) K'; rank i appends -V_i K'.
+
+This handles the s0 == A(:, I) case (the BASELINE coarse grids) of
+``power_svd(..., PowerConfig(q, columns=I))`` in single-pass mode.
+The arithmetic is pluggable (``ops``) so the exchange logic is tested on CPU
+with gloo (tests/test_sharded_cpu.py); ``DeviceOps`` is the product path
+(C-ABI kernels + torch.distributed / NCCL).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+
+RANK_TOL = 1e-12
+
+
+class TorchComm:
+    """torch.distributed collectives on the ops' tensors (NCCL or gloo)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+
+    def allgather_cols(self, x, ops):
+        """Concatenate each rank's (m x w_i) block along columns, rank order."""
+        if self.world == 1:
+            return x
+        import torch
+        widths = torch.tensor([x.shape[1]], dtype=torch.int64, device=ops.tensor_device)
+        ws = [torch.zeros_like(widths) for _ in range(self.world)]
+        self.dist.all_gather(ws, widths, group=self.group)
+        ws = [int(w.item()) for w in ws]
+        wmax = max(ws)
+        pad = ops.pad_cols(x, wmax)
+        parts = [ops.empty_like(pad) for _ in range(self.world)]
+        self.dist.all_gather(parts, pad, group=self.group)
+        return ops.cat_cols([p[:, :w] for p, w in zip(parts, ws)])
+
+    def allgather_rows(self, x, ops):
+        if self.world == 1:
+            return x
+        parts = [ops.empty_like(x) for _ in range(self.world)]
+        self.dist.all_gather(parts, ops.contig(x), group=self.group)
+        return ops.cat_rows(parts)
+
+    def broadcast(self, x, root, ops):
+        if self.world == 1:
+            return x
+        x = ops.contig(x)
+        self.dist.broadcast(x, root, group=self.group)
+        return x
+
+
+def sharded_power_svd(a_local, c_begin: int, cols, k: int, q: int, comm, ops):
+    """Rank-local part of the column-sharded single-pass power SVD.
+
+    a_local: this rank's columns [c_begin, c_begin + n_i) of A (m x n_i).
+    cols: the global, ascending column set I.  Returns (U m x k, S k, V_i
+    n_i x k, kept_rank, rank_deficient_warning) with U, S replicated.
+    """
+    cols = np.asarray(cols, dtype=np.int64)
+    m, n_i = a_local.shape
+    sel = (cols >= c_begin) & (cols < c_begin + n_i)
+    c_i = ops.gather(a_local, cols[sel] - c_begin)
+    c_all = comm.allgather_cols(c_i, ops)
+    ncols = cols.size
+    z, s_c, r = ops.sketch_basis(c_all, 2.0 * q + 1.0)
+    r_use = max(r, 0)
+    u = ops.zeros((m, k))
+    v = ops.zeros((n_i, k))
+    s = np.zeros(k)
+    kk = min(r_use, k)
+    if r_use > 0:
+        y_i = ops.atz(a_local, z)                                   # n_i x r (the A pass)
+        kappa = s_c[0] / s_c[r_use - 1] if s_c[r_use - 1] > 0 else np.inf
+        q_i, r_i = ops.qr(y_i, well_conditioned=kappa < 1e6)        # local TSQR leaf
+        r_stack = comm.allgather_rows(r_i, ops)                     # (P r) x r
+        q_top, r_y = ops.qr(r_stack, well_conditioned=False)
+        q_y = ops.matmul(q_i, ops.rows(q_top, comm.rank * r_use, (comm.rank + 1) * r_use))
+        # SVD of R_y^T via that of R_y: R_y = A S B^T  =>  R_y^T = B S A^T
+        a_, s_core, b_ = ops.svd_small(r_y)
+        uf = ops.matmul(z, b_)                                      # U = Z u~,  u~ = B
+        vf = ops.matmul(q_y, a_)                                    # V = Q_Y v~, v~ = A
+        u = ops.set_cols(u, ops.cols(uf, 0, kk), 0)
+        v = ops.set_cols(v, ops.cols(vf, 0, kk), 0)
+        s[:kk] = ops.to_numpy(s_core)[:kk]
+    if kk < k:
+        u = ops.complete(u, kk, k)
+        if comm.rank == 0:
+            v, kp = ops.complete_root(v, kk, k)
+        else:
+            kp = ops.zeros((kk, k - kk))
+        kp = comm.broadcast(kp, 0, ops)
+        if comm.rank != 0:
+            v = ops.complete_other(v, kk, k, kp)
+    warn = not (m >= ncols and r == ncols)
+    return u, s, v, r, warn
+
+
+class DeviceOps:
+    """Product arithmetic: the C-ABI kernels on CUDA tensors."""
+
+    def __init__(self):
+        from .device import device, require_cuda
+        self.t = require_cuda()
+        self.tensor_device = device()
+
+    # --- plumbing
+    def _s(self):
+        return self.t.cuda.current_stream().cuda_stream
+
+    def zeros(self, shape):
+        return self.t.zeros(shape, dtype=self.t.float64, device=self.tensor_device)
+
+    def empty_like(self, x):
+        return self.t.empty_like(x)
+
+    def contig(self, x):
+        return x.contiguous()
+
+    def pad_cols(self, x, w):
+        out = self.zeros((x.shape[0], w))
+        out[:, :x.shape[1]] = x
+        return out
+
+    def cat_cols(self, parts):
+        return self.t.cat(parts, dim=1).contiguous()
+
+    def cat_rows(self, parts):
+        return self.t.cat(parts, dim=0).contiguous()
+
+    def rows(self, x, a, b):
+        return x[a:b].contiguous()
+
+    def cols(self, x, a, b):
+        return x[:, a:b].contiguous()
+
+    def set_cols(self, x, blk, c0):
+        x[:, c0:c0 + blk.shape[1]] = blk
+        return x
+
+    def to_numpy(self, x):
+        return x.cpu().numpy()
+
+    # --- kernels
+    def gather(self, a, idx_local):
+        n_c = int(idx_local.size)
+        out = self.t.empty((a.shape[0], n_c), dtype=self.t.float64, device=self.tensor_device)
+        if n_c:
+            d_idx = self.t.from_numpy(np.ascontiguousarray(idx_local, dtype=np.int64)).to(self.tensor_device)
+            tag = _lib.SP_F64 if a.dtype.itemsize == 8 else _lib.SP_F32
+            _lib.call("sp_apply_stencil", a.data_ptr(), tag, a.shape[0], a.shape[1], a.stride(0), d_idx.data_ptr(),
+                      None, 1, n_c, 1, out.data_ptr(), n_c, self._s())
+        return out
+
+    def sketch_basis(self, c, power):
+        m, nc = c.shape
+        rmax = min(m, nc, 256)
+        u = self.t.empty((m, rmax), dtype=self.t.float64, device=self.tensor_device)
+        s = self.t.empty((rmax,), dtype=self.t.float64, device=self.tensor_device)
+        info = _lib.new_info()
+        _lib.call("sp_sketch_basis", c.data_ptr(), m, nc, nc, float(power), rmax, u.data_ptr(), rmax, s.data_ptr(),
+                  _lib.info_ptr(info), self._s())
+        r = min(int(info[_lib.INFO_KEPT]), rmax)
+        return u[:, :r].contiguous(), s[:r].cpu().numpy(), r
+
+    def atz(self, a, z):
+        n = a.shape[1]
+        r = z.shape[1]
+        y = self.t.empty((n, r), dtype=self.t.float64, device=self.tensor_device)
+        tag = _lib.SP_F64 if a.dtype.itemsize == 8 else _lib.SP_F32
+        _lib.call("sp_skinny_atz", a.data_ptr(), tag, a.shape[0], n, a.stride(0), z.data_ptr(), r, r, y.data_ptr(), r,
+                  self._s())
+        return y
+
+    def qr(self, x, well_conditioned):
+        rows, c = x.shape
+        qm = self.t.empty((rows, c), dtype=self.t.float64, device=self.tensor_device)
+        rm = self.t.empty((c, c), dtype=self.t.float64, device=self.tensor_device)
+        _lib.call("sp_qr_tall", rows, c, x.data_ptr(), c, qm.data_ptr(), c, rm.data_ptr(), c, int(well_conditioned),
+                  self._s())
+        return qm, rm
+
+    def matmul(self, a, b):
+        m, kdim = a.shape
+        n = b.shape[1]
+        out = self.t.empty((m, n), dtype=self.t.float64, device=self.tensor_device)
+        _lib.call("sp_gemm", 0, 0, m, n, kdim, 1.0, a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), 0.0,
+                  out.data_ptr(), n, self._s())
+        return out
+
+    def svd_small(self, mtx):
+        n = mtx.shape[0]
+        u = self.t.empty((n, n), dtype=self.t.float64, device=self.tensor_device)
+        s = self.t.empty((n,), dtype=self.t.float64, device=self.tensor_device)
+        v = self.t.empty((n, n), dtype=self.t.float64, device=self.tensor_device)
+        _lib.call("sp_jacobi_svd", n, mtx.data_ptr(), n, u.data_ptr(), n, s.data_ptr(), v.data_ptr(), n, self._s())
+        return u, s, v
+
+    def complete(self, x, r, k):
+        _lib.call("sp_householder_complete", x.shape[0], r, k, x.data_ptr(), x.stride(0), None, self._s())
+        return x
+
+    def complete_root(self, x, r, k):
+        kp = self.t.empty((r, k - r), dtype=self.t.float64, device=self.tensor_device)
+        _lib.call("sp_householder_complete", x.shape[0], r, k, x.data_ptr(), x.stride(0),
+                  kp.data_ptr() if r > 0 else None, self._s())
+        return x, kp
+
+    def complete_other(self, x, r, k, kp):
+        if r > 0:
+            _lib.call("sp_gemm", 0, 0, x.shape[0], k - r, r, -1.0, x.data_ptr(), x.stride(0), kp.data_ptr(), k - r,
+                      0.0, x[:, r:].data_ptr(), x.stride(0), self._s())
+        return x
+
+
+def shard_columns(n: int, world: int, rank: int, align: int = 1) -> tuple[int, int]:
+    """Contiguous column slab of a rank (rounded to ``align`` columns)."""
+    units = n // align
+    b = (units * rank // world) * align
+    e = (units * (rank + 1) // world) * align if rank + 1 < world else n
+    return b, e

@@ -1,0 +1,95 @@
+"""Column-sharded driver on the device kernels (DeviceOps).  One GPU only:
+world 1 through TorchComm, and two shards emulated by two host threads that
+exchange device tensors through a host-side barrier (no kernel ever waits on
+another, so sharing one GPU is safe)."""
+
+import threading
+import warnings
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2105_01271_b200 as sp
+from paper_2105_01271_b200.datagen import CONFIGS, generate_host
+from paper_2105_01271_b200.sharded import DeviceOps, TorchComm, shard_columns, sharded_power_svd
+
+pytestmark = pytest.mark.gpu
+
+
+class ThreadComm:
+    def __init__(self, rank, world, shared):
+        self.rank, self.world, self.sh = rank, world, shared
+
+    def _exchange(self, x):
+        self.sh["slots"][self.rank] = x
+        self.sh["bar"].wait()
+        parts = list(self.sh["slots"])
+        self.sh["bar"].wait()
+        return parts
+
+    def allgather_cols(self, x, ops):
+        return ops.cat_cols(self._exchange(x))
+
+    def allgather_rows(self, x, ops):
+        return ops.cat_rows(self._exchange(ops.contig(x)))
+
+    def broadcast(self, x, root, ops):
+        return self._exchange(x)[root].clone()
+
+
+def _case():
+    cfg = CONFIGS["cfg2"].scaled(m=400, grid=(64, 64), name="shard")
+    a = generate_host(cfg)
+    op, cols = sp.grid_injection(cfg.grid, cfg.stride)
+    return cfg, a, op, cols
+
+
+def test_world1_equals_power_svd(cuda):
+    cfg, a, op, cols = _case()
+    ops = DeviceOps()
+    ad = cuda.from_numpy(a).cuda()
+    u, s, v, r, warn = sharded_power_svd(ad, 0, cols, 50, 1, TorchComm(), ops)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        ref = sp.power_svd(sp.ArraySnapshotStream(a), op, 50, sp.PowerConfig(q=1, columns=cols))
+    assert r == ref.kept_rank and warn
+    np.testing.assert_allclose(s, ref.s, rtol=0, atol=1e-13 * ref.s[0])
+    vh = v.cpu().numpy()
+    np.testing.assert_allclose(vh.T @ vh, np.eye(50), atol=1e-12)
+
+
+def test_two_shards_match_target(cuda):
+    cfg, a, op, cols = _case()
+    world = 2
+    shared = {"slots": [None] * world, "bar": threading.Barrier(world)}
+    results = [None] * world
+    errors = []
+
+    def run(rank):
+        try:
+            cuda.cuda.set_device(0)
+            b, e = shard_columns(cfg.n, world, rank, align=cfg.grid[1])
+            ad = cuda.from_numpy(a[:, b:e].copy()).cuda()
+            results[rank] = (b,) + sharded_power_svd(ad, b, cols, 50, 1, ThreadComm(rank, world, shared), DeviceOps())
+        except Exception as exc:  # surface in the main thread
+            errors.append(exc)
+            shared["bar"].abort()
+
+    th = [threading.Thread(target=run, args=(rk,)) for rk in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errors, errors
+    u = results[0][1].cpu().numpy()
+    s = results[0][2]
+    v = np.concatenate([results[rk][3].cpu().numpy() for rk in range(world)])
+    r = results[0][4]
+    assert np.array_equal(results[1][1].cpu().numpy(), u)  # replicated, bitwise identical
+    tu, ts, tv, tr = oracle.projector_target_svd(a, a[:, cols], 50, 3)
+    assert r == tr
+    np.testing.assert_allclose(s[:r], ts, rtol=0, atol=1e-12 * ts[0])
+    np.testing.assert_allclose(v.T @ v, np.eye(50), atol=1e-12)
+    np.testing.assert_allclose(u.T @ u, np.eye(50), atol=1e-12)
+    np.testing.assert_allclose((u * s) @ v.T, (tu * ts) @ tv.T, atol=1e-10 * np.abs(a).max())

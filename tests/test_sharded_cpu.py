@@ -1,0 +1,181 @@
+"""Column-sharded power SVD on CPU: world_size 2 over gloo, the exchange
+logic of paper_2105_01271_b200.sharded driven with a numpy arithmetic
+backend (test infrastructure), checked against the single-process target
+and against world_size 1."""
+
+import os
+import socket
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+
+class NumpyOps:
+    """CPU stand-in for DeviceOps (float64 torch CPU tensors, LAPACK math)."""
+
+    tensor_device = torch.device("cpu")
+
+    def _t(self, a):
+        return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
+
+    def zeros(self, shape):
+        return torch.zeros(shape, dtype=torch.float64)
+
+    def empty_like(self, x):
+        return torch.empty_like(x)
+
+    def contig(self, x):
+        return x.contiguous()
+
+    def pad_cols(self, x, w):
+        out = self.zeros((x.shape[0], w))
+        out[:, :x.shape[1]] = x
+        return out
+
+    def cat_cols(self, parts):
+        return torch.cat(parts, 1).contiguous()
+
+    def cat_rows(self, parts):
+        return torch.cat(parts, 0).contiguous()
+
+    def rows(self, x, a, b):
+        return x[a:b].contiguous()
+
+    def cols(self, x, a, b):
+        return x[:, a:b].contiguous()
+
+    def set_cols(self, x, blk, c0):
+        x[:, c0:c0 + blk.shape[1]] = blk
+        return x
+
+    def to_numpy(self, x):
+        return x.numpy()
+
+    def gather(self, a, idx):
+        return self._t(a.numpy()[:, idx])
+
+    def sketch_basis(self, c, power):
+        u, s, _ = np.linalg.svd(c.numpy(), full_matrices=False)
+        r = int(np.count_nonzero((s / s[0]) ** power > 1e-12)) if s[0] > 0 else 0
+        return self._t(u[:, :r]), s[:r], r
+
+    def atz(self, a, z):
+        return self._t(a.numpy().T @ z.numpy())
+
+    def qr(self, x, well_conditioned):
+        q, r = np.linalg.qr(x.numpy())
+        sg = np.where(np.diag(r) < 0, -1.0, 1.0)
+        return self._t(q * sg), self._t(r * sg[:, None])
+
+    def matmul(self, a, b):
+        return self._t(a.numpy() @ b.numpy())
+
+    def svd_small(self, m):
+        u, s, vt = np.linalg.svd(m.numpy())
+        return self._t(u), self._t(s), self._t(vt.T)
+
+    def _hh(self, q, r, k):
+        # Householder reconstruction: LU of Q - [S; 0] (csrc/complete.cu)
+        w = q[:k, :r].copy()
+        sgn = np.zeros(r)
+        lmat = np.zeros((k, r))
+        umat = np.zeros((r, r))
+        for i in range(r):
+            sgn[i] = -1.0 if w[i, i] >= 0 else 1.0
+            w[i, i] -= sgn[i]
+            umat[i, i:] = w[i, i:]
+            lmat[i:, i] = w[i:, i] / w[i, i]
+            w[i + 1:, i + 1:] -= np.outer(lmat[i + 1:, i], umat[i, i + 1:])
+        ui = np.linalg.inv(umat)
+        t = -umat @ np.diag(sgn) @ np.linalg.inv(lmat[:r]).T
+        kp = ui @ t @ ui.T @ q[r:k, :r].T
+        etop = np.zeros((k, k - r))
+        etop[:r] = sgn[:, None] * kp
+        etop[r:] = np.eye(k - r)
+        return kp, etop
+
+    def complete(self, x, r, k):
+        q = x.numpy()
+        if r == 0:
+            q[:, :] = 0.0
+            q[:k, :k] = np.eye(k)
+            return x
+        kp, etop = self._hh(q, r, k)
+        q[:, r:] = -q[:, :r] @ kp
+        q[:k, r:] += etop
+        return x
+
+    def complete_root(self, x, r, k):
+        q = x.numpy()
+        if r == 0:
+            return self.complete(x, r, k), self.zeros((0, k))
+        kp, _ = self._hh(q, r, k)
+        self.complete(x, r, k)
+        return x, self._t(kp)
+
+    def complete_other(self, x, r, k, kp):
+        q = x.numpy()
+        if r > 0:
+            q[:, r:] = -q[:, :r] @ kp.numpy()
+        return x
+
+
+def _field():
+    from paper_2105_01271_b200.datagen import CONFIGS, coarse_grid_indices, generate_host
+    cfg = CONFIGS["cfg2"].scaled(m=300, grid=(48, 64), name="shard")
+    return cfg, generate_host(cfg), coarse_grid_indices(cfg.grid, cfg.stride)
+
+
+def _worker(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2105_01271_b200.sharded import TorchComm, shard_columns, sharded_power_svd
+    cfg, a, cols = _field()
+    b, e = shard_columns(cfg.n, world, rank, align=cfg.grid[1])  # x-slabs of the grid
+    ops = NumpyOps()
+    u, s, v, r, warn = sharded_power_svd(torch.from_numpy(a[:, b:e].copy()), b, cols, 30, 1, TorchComm(), ops)
+    parts = [None] * world
+    dist.all_gather_object(parts, (b, e, v.numpy()))
+    if rank == 0:
+        out_q.put((u.numpy(), s, np.concatenate([p[2] for p in sorted(parts, key=lambda t: t[0])]), r, warn))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_sharded_matches_target(world):
+    import oracle
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(rk, world, port, q)) for rk in range(world)]
+    for p in procs:
+        p.start()
+    u, s, v, r, warn = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cfg, a, cols = _field()
+    tu, ts, tv, tr = oracle.projector_target_svd(a, a[:, cols], 30, 3)
+    assert r == tr and warn
+    np.testing.assert_allclose(s[:r], ts, rtol=0, atol=1e-12 * ts[0])
+    assert np.all(s[r:] == 0)
+    np.testing.assert_allclose(u.T @ u, np.eye(30), atol=1e-12)
+    np.testing.assert_allclose(v.T @ v, np.eye(30), atol=1e-12)
+    rec = (u * s) @ v.T
+    np.testing.assert_allclose(rec, (tu * ts) @ tv.T, atol=1e-10 * np.abs(a).max())
