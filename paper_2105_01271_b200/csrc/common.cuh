@@ -76,6 +76,18 @@ __device__ __forceinline__ double warp_max(double v) {
 template <typename T>
 __device__ __forceinline__ double widen(T x) { return (double)x; }
 
+// Staging global -> shared without a register round trip: every thread
+// issues all of its 8-byte copies back to back (zero-fill when !pred; gmem
+// must still be a mapped address then, e.g. the array base), so a staging
+// loop costs one memory latency instead of one per iteration.
+__device__ __forceinline__ void cp_async_f64(double* smem, const double* gmem, bool pred) {
+  const unsigned saddr = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gmem), "r"(pred ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
 // Counter-based hash -> uniform double in (-1, 1); used for the random test
 // blocks of the range finder (any full-rank block works; no parity with numpy).
 __device__ __forceinline__ double hash_uniform(uint64_t seed, uint64_t i) {

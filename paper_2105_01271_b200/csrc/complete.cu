@@ -125,6 +125,14 @@ int householder_complete(int64_t N, int r, int k, double* out, int64_t ldo, cuda
   }
   Arena ar(s);
   SPB_ALLOC(ar, double, Kp, (size_t)r * kr);
+  if (kr <= 64) {
+    // out[:, r:k] = E' - Q K' in one streaming pass (E' added on the top k rows)
+    SPB_ALLOC(ar, double, Et, (size_t)k * kr);
+    hh_complete_kernel<<<1, 256, 0, s>>>(r, k, out, ldo, kp_out ? kp_out : Kp, Et, kr);
+    count_launch();
+    SPB_CHECK_LAUNCH();
+    return tall_mul(N, r, out, ldo, kr, kp_out ? kp_out : Kp, kr, -1.0, 0.0, out + r, ldo, s, Et, kr, k);
+  }
   // zero the completion block, then write its top k rows (E') in place
   SPB_CUDA(cudaMemset2DAsync(out + r, ldo * sizeof(double), 0, kr * sizeof(double), N, s));
   hh_complete_kernel<<<1, 256, 0, s>>>(r, k, out, ldo, Kp, out + r, ldo);

@@ -14,6 +14,7 @@
 // src/rowid.py:138-139) and for the literal cross-Gramian (src/svd.py:66).
 #include "common.cuh"
 #include "launch_count.cuh"
+#include "ops.cuh"
 
 namespace spb {
 
@@ -153,20 +154,30 @@ dgemm_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, int6
   }
 }
 
-// C = alpha * sum_s P[s] + beta * C.  Deep splits (S > 8): one warp per
-// output, lanes take splits lane, lane+32, ... and a fixed shuffle tree
-// combines them (deterministic); shallow splits: one thread per output.
-__global__ void gemm_split_reduce_warp(const double* __restrict__ P, int S, int64_t M, int64_t N,
-                                       double alpha, double beta, double* __restrict__ C, int64_t ldc) {
-  const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (e >= M * N) return;
+// C = alpha * sum_s P[s] + beta * C.  Deep splits (S > 8): a 256-thread CTA
+// owns 32 consecutive outputs; warp g sums splits g, g+8, ... (lanes read
+// consecutive outputs: coalesced) and the 8 warp partials are combined in a
+// fixed order (deterministic); shallow splits: one thread per output.
+__global__ void __launch_bounds__(256) gemm_split_reduce_warp(const double* __restrict__ P, int S, int64_t M,
+                                                              int64_t N, double alpha, double beta,
+                                                              double* __restrict__ C, int64_t ldc) {
+  __shared__ double part[8][33];
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t e = (int64_t)blockIdx.x * 32 + lane;
+  const int64_t MN = M * N;
   double acc = 0.0;
-  for (int s = lane; s < S; s += 32) acc += P[(int64_t)s * M * N + e];
-  acc = warp_sum(acc);
-  if (lane == 0) {
+  if (e < MN) {
+#pragma unroll 8
+    for (int s = g; s < S; s += 8) acc += P[(int64_t)s * MN + e];
+  }
+  part[g][lane] = acc;
+  __syncthreads();
+  if (g == 0 && e < MN) {
+    double t = part[0][lane];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) t += part[k][lane];
     double* p = C + (e / N) * ldc + (e % N);
-    const double v = alpha * acc;
+    const double v = alpha * t;
     *p = (beta == 0.0) ? v : fma(beta, *p, v);
   }
 }
@@ -209,6 +220,11 @@ int gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const do
     SPB_CHECK_LAUNCH();
     return SP_OK;
   }
+  // tall-skinny shapes where 64x64 DMMA tiles would idle: streaming kernels
+  if (ta == 1 && tb == 0 && M <= 64 && N <= 64 && K >= 256)
+    return tall_gram(K, (int)M, A, lda, (int)N, B, ldb, alpha, beta, C, ldc, s);
+  if (ta == 0 && tb == 0 && K <= 64 && N <= 64 && M >= 256)
+    return tall_mul(M, (int)K, A, lda, (int)N, B, ldb, alpha, beta, C, ldc, s);
   const int gx = ceil_div(N, kBN), gy = ceil_div(M, kBM);
   const int64_t tiles = (int64_t)gx * gy;
   int S = 1;
@@ -240,15 +256,19 @@ int gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const do
   }
   count_launch();
   SPB_CHECK_LAUNCH();
-  if (partial && S > 8) {
-    gemm_split_reduce_warp<<<ceil_div(M * N * 32, 256), 256, 0, s>>>(out, S, M, N, alpha, beta, C, ldc);
-    count_launch();
-    SPB_CHECK_LAUNCH();
-  } else if (partial) {
-    gemm_split_reduce<<<ceil_div(M * N, 256), 256, 0, s>>>(out, S, M, N, alpha, beta, C, ldc);
-    count_launch();
-    SPB_CHECK_LAUNCH();
+  if (partial) return split_reduce(out, S, M, N, alpha, beta, C, ldc, s);
+  return SP_OK;
+}
+
+int split_reduce(const double* P, int S, int64_t M, int64_t N, double alpha, double beta, double* C, int64_t ldc,
+                 cudaStream_t s) {
+  if (S > 8) {
+    gemm_split_reduce_warp<<<ceil_div(M * N, 32), 256, 0, s>>>(P, S, M, N, alpha, beta, C, ldc);
+  } else {
+    gemm_split_reduce<<<ceil_div(M * N, 256), 256, 0, s>>>(P, S, M, N, alpha, beta, C, ldc);
   }
+  count_launch();
+  SPB_CHECK_LAUNCH();
   return SP_OK;
 }
 

@@ -164,9 +164,159 @@ jacobi_kernel(int n, int np, const double* __restrict__ M, int64_t ldm, double* 
   }
 }
 
+// ---------------------------------------------------------- n <= 32 ----
+// LANE = COLUMN variant for the cores of the path (b <= 32): warp w holds
+// rows [8w, 8w + 8) of every column, lane c column c, so a pair's partner
+// column arrives by 8 shuffles per warp and the three dot products are one
+// 4-way shared-memory reduction (one __syncthreads per round, double
+// buffered).  Both lanes of a pair compute the same rotation from the same
+// sums in the same order (bitwise identical).  The rotation uses
+//   t = sign(d) h / (|d| + hypot(d, h)),  d = b - a,  h = 2 g,
+//   c = 1 / sqrt(1 + t^2),  s = c t
+// (the tan(theta) root of t^2 + 2 (d/h) t - 1 = 0 of the classical formula).
+constexpr int kJ32Warps = 4;
+
+// circle-method partner of position x among na (even) players in round r
+__device__ __forceinline__ int rr_partner(int x, int r, int na) {
+  const int n1 = na - 1;
+  if (x == 0) return 1 + (r % n1);
+  int y = (2 * r - (x - 1)) % n1;
+  if (y < 0) y += n1;
+  y += 1;
+  return y == x ? 0 : y;
+}
+
+__global__ void __launch_bounds__(kJ32Warps * 32)
+jacobi32_kernel(int n, const double* __restrict__ M, int64_t ldm, double* __restrict__ U, int64_t ldu,
+                double* __restrict__ S, double* __restrict__ Vout, int64_t ldv) {
+  __shared__ double part[2][kJ32Warps][32][2];
+  __shared__ double nrm_s[kJ32Warps][32];
+  __shared__ double sig_s[32];
+  __shared__ int act[32], pos_s[32];
+  __shared__ int na_s;
+  const int w = threadIdx.x >> 5, c = threadIdx.x & 31;
+  const bool want_v = Vout != nullptr;
+  double x[8], v[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int i = w * 8 + k;
+    x[k] = (i < n && c < n) ? M[(int64_t)i * ldm + c] : 0.0;
+    v[k] = (i == c) ? 1.0 : 0.0;
+  }
+  // column norms and ||M||_F^2 (fixed order)
+  double a0 = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a0 = fma(x[k], x[k], a0);
+  nrm_s[w][c] = a0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double fro = 0.0;
+    double cn[32];
+    for (int cc = 0; cc < 32; ++cc) {
+      cn[cc] = ((nrm_s[0][cc] + nrm_s[1][cc]) + (nrm_s[2][cc] + nrm_s[3][cc]));
+      fro += cn[cc];
+    }
+    // columns below 1e-15 ||M||_F are rounding noise: left out of the schedule
+    const double negl = 1e-30 * fro;
+    int na = 0;
+    for (int cc = 0; cc < 32; ++cc) pos_s[cc] = -1;
+    for (int cc = 0; cc < n; ++cc)
+      if (cn[cc] > negl) {
+        pos_s[cc] = na;
+        act[na++] = cc;
+      }
+    if (na & 1) act[na++] = -1;  // pad to even
+    na_s = na;
+  }
+  __syncthreads();
+  const int na = na_s, mypos = pos_s[c];
+  double fro2 = 0.0;
+  for (int cc = 0; cc < 32; ++cc) fro2 += ((nrm_s[0][cc] + nrm_s[1][cc]) + (nrm_s[2][cc] + nrm_s[3][cc]));
+  const double negl = 1e-30 * fro2;
+  int buf = 0;
+  for (int sweep = 0; sweep < kJacMaxSweeps && na >= 2; ++sweep) {
+    int rotated = 0;
+    for (int round = 0; round < na - 1; ++round) {
+      int plane = -1;
+      if (mypos >= 0) plane = act[rr_partner(mypos, round, na)];
+      const int src = plane >= 0 ? plane : c;
+      double y[8], z[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) y[k] = __shfl_sync(0xffffffffu, x[k], src);
+      if (want_v) {  // uniform across the CTA
+#pragma unroll
+        for (int k = 0; k < 8; ++k) z[k] = __shfl_sync(0xffffffffu, v[k], src);
+      }
+      double pa = 0.0, pg = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        pa = fma(x[k], x[k], pa);
+        pg = fma(x[k], y[k], pg);
+      }
+      part[buf][w][c][0] = pa;
+      part[buf][w][c][1] = pg;
+      __syncthreads();
+      const double a = (part[buf][0][c][0] + part[buf][1][c][0]) + (part[buf][2][c][0] + part[buf][3][c][0]);
+      const double g = (part[buf][0][c][1] + part[buf][1][c][1]) + (part[buf][2][c][1] + part[buf][3][c][1]);
+      const double b = __shfl_sync(0xffffffffu, a, src);
+      buf ^= 1;
+      if (plane < 0) continue;
+      const bool low = c < plane;  // canonical (p, q) = (min, max)
+      const double ap = low ? a : b, aq = low ? b : a;
+      if (!(g != 0.0 && fmin(ap, aq) > negl && fabs(g) > kJacTol * sqrt(ap) * sqrt(aq))) continue;
+      const double d = aq - ap, h = 2.0 * g;
+      const double t = copysign(1.0, d) * h / (fabs(d) + hypot(d, h));
+      const double cs = rsqrt(fma(t, t, 1.0));
+      const double sn = cs * t;
+      // p' = cs p - sn q ; q' = sn p + cs q
+      const double so = low ? -sn : sn;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = fma(so, y[k], cs * x[k]);
+      if (want_v) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = fma(so, z[k], cs * v[k]);
+      }
+      rotated = 1;
+    }
+    if (!__syncthreads_or(rotated)) break;
+  }
+  // singular values = column norms, sorted descending (stable by index)
+  double a1 = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a1 = fma(x[k], x[k], a1);
+  nrm_s[w][c] = a1;
+  __syncthreads();
+  if (w == 0) sig_s[c] = sqrt((nrm_s[0][c] + nrm_s[1][c]) + (nrm_s[2][c] + nrm_s[3][c]));
+  __syncthreads();
+  const double sc = sig_s[c];
+  int rank = 0;
+  for (int d = 0; d < 32; ++d) {
+    const double sd = sig_s[d];
+    rank += (sd > sc || (sd == sc && d < c)) ? 1 : 0;
+  }
+  if (rank >= n) return;
+  if (w == 0) S[rank] = sc;
+  const double inv = sc > 0.0 ? 1.0 / sc : 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int i = w * 8 + k;
+    if (i < n) {
+      U[(int64_t)i * ldu + rank] = x[k] * inv;
+      if (want_v) Vout[(int64_t)i * ldv + rank] = v[k];
+    }
+  }
+}
+
 int jacobi_svd(int64_t n, const double* M, int64_t ldm, double* U, int64_t ldu, double* S,
                double* V, int64_t ldv, cudaStream_t s) {
   SPB_REQUIRE(n >= 1 && n <= 256, "Jacobi SVD supports 1 <= n <= 256");
+  if (n <= 32) {
+    jacobi32_kernel<<<1, kJ32Warps * 32, 0, s>>>((int)n, M, ldm, U, ldu, S, V, ldv);
+    count_launch();
+    SPB_CHECK_LAUNCH();
+    return SP_OK;
+  }
+  SPB_REQUIRE(V != nullptr, "Jacobi SVD needs V for n > 32");
   const int np = std::max<int>(2, (int)(n + (n & 1)));
   const int threads = std::min(1024, std::max(64, 32 * (np / 2)));
   const size_t smem = (size_t)2 * np * np * sizeof(double);

@@ -18,6 +18,15 @@ int gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const do
          cudaStream_t s);
 int tsqr(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq,
          double* R, int64_t ldr, cudaStream_t s);
+int tall_gram(int64_t rows, int c, const double* X, int64_t ldx, int d, const double* Y, int64_t ldy,
+              double alpha, double beta, double* G, int64_t ldg, cudaStream_t s);
+// C (M x N, ldc) = alpha * sum_{s < S} P[s] + beta * C, P dense M x N slabs, fixed order
+int split_reduce(const double* P, int S, int64_t M, int64_t N, double alpha, double beta, double* C, int64_t ldc,
+                 cudaStream_t s);
+// O = alpha X M + beta O (+ top[row] for row < top_rows); O may alias X's rows
+int tall_mul(int64_t rows, int c, const double* X, int64_t ldx, int d, const double* M, int64_t ldm, double alpha,
+             double beta, double* O, int64_t ldo, cudaStream_t s, const double* top = nullptr, int64_t ldt = 0,
+             int64_t top_rows = 0);
 int cholqr2_async(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq,
                   double* R, int64_t ldr, int* dflag, cudaStream_t s);
 int check_finite_async(int64_t rows, int64_t cols, const double* X, int64_t ldx, int* dflag, cudaStream_t s);

@@ -49,9 +49,14 @@ struct TopSvd {
 // `pflag` (device int, may be null) is a pending non-finite flag for X raised
 // by an earlier asynchronous check; it is read with the first Ritz spectrum
 // (no extra synchronisation) and turns into SP_ENUMERICAL with `pmsg`.
+// check_input: svd_top raises the flag itself when X has a non-finite entry,
+// detected on its first product Y = X Omega (Omega has no zero entries, so a
+// non-finite X always yields a non-finite Y): an m x b check instead of a
+// full pass over X.
 struct PendingFlag {
-  const int* dev = nullptr;
+  int* dev = nullptr;
   const char* msg = "";
+  bool check_input = false;
 };
 
 static int read_flag_with(const PendingFlag& pf, int& host_flag, cudaStream_t s) {
@@ -61,11 +66,12 @@ static int read_flag_with(const PendingFlag& pf, int& host_flag, cudaStream_t s)
 }
 
 static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int want, double power,
-                   TopSvd& out, Arena& ar, cudaStream_t s, PendingFlag pf = PendingFlag()) {
+                   TopSvd& out, Arena& ar, cudaStream_t s, PendingFlag pf = PendingFlag(), bool want_v = false) {
   const int64_t p = std::min(rows, cols);
   int hflag = 0;
   if (p <= 64 && pf.dev) {
     // the exact path checks finiteness itself (thin_svd); surface the caller's message
+    if (pf.check_input) SPB_TRY(check_finite_async(rows, cols, X, ldx, pf.dev, s));
     SPB_TRY(read_flag_with(pf, hflag, s));
     SPB_CUDA(cudaStreamSynchronize(s));
     if (hflag) {
@@ -109,6 +115,7 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
     }
     SPB_TRY(fill_uniform(cols, b, Om, b, 0x5eed5eedull + (uint64_t)b, s));
     SPB_TRY(gemm(0, 0, rows, b, cols, 1.0, X, ldx, Om, b, 0.0, Y, b, s));
+    if (pf.dev && pf.check_input) SPB_TRY(check_finite_async(rows, b, Y, b, pf.dev, s));
     SPB_TRY(tsqr(rows, b, Y, b, Q, b, Rt, b, s));
     std::vector<double> prev, hs(b);
     int kept_prev = -1, kept = 0, iters = 0;
@@ -119,7 +126,7 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
       SPB_TRY(gemm(1, 0, cols, b, rows, 1.0, X, ldx, Q, b, 0.0, Z, b, s));
       SPB_TRY(tsqr(cols, b, Z, b, P, b, Rz, b, s));
       SPB_TRY(transpose(b, b, Rz, b, Rt, b, s));
-      SPB_TRY(jacobi_svd(b, Rt, b, Us, b, Sg, Vs, b, s));
+      SPB_TRY(jacobi_svd(b, Rt, b, Us, b, Sg, want_v ? Vs : nullptr, b, s));
       SPB_CUDA(cudaMemcpyAsync(hs.data(), Sg, b * sizeof(double), cudaMemcpyDeviceToHost, s));
       if (itn == 0) SPB_TRY(read_flag_with(pf, hflag, s));
       SPB_CUDA(cudaStreamSynchronize(s));
@@ -161,13 +168,13 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
     out.hs = hs;
     out.U = ar.alloc<double>((size_t)rows * b);
     out.S = ar.alloc<double>((size_t)b);
-    out.V = ar.alloc<double>((size_t)cols * b);
+    if (want_v) out.V = ar.alloc<double>((size_t)cols * b);
     if (ar.failed()) {
       set_error("svd_top workspace allocation failed");
       return SP_ECUDA;
     }
     SPB_TRY(gemm(0, 0, rows, b, b, 1.0, Q, b, Us, b, 0.0, out.U, b, s));
-    SPB_TRY(gemm(0, 0, cols, b, b, 1.0, P, b, Vs, b, 0.0, out.V, b, s));
+    if (want_v) SPB_TRY(gemm(0, 0, cols, b, b, 1.0, P, b, Vs, b, 0.0, out.V, b, s));
     SPB_CUDA(cudaMemcpyAsync(out.S, Sg, b * sizeof(double), cudaMemcpyDeviceToDevice, s));
     return SP_OK;
   }
@@ -331,10 +338,10 @@ int single_pass_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t ld
   }
   SPB_ALLOC(ar, int, fflag, 1);
   SPB_CUDA(cudaMemsetAsync(fflag, 0, sizeof(int), s));
-  SPB_TRY(check_finite_async(m, out_dim, s0, out_dim, fflag, s));
   TopSvd top;
   PendingFlag pf;
   pf.dev = fflag;
+  pf.check_input = true;
   pf.msg = "QR input contains non-finite entries";
   SPB_TRY(svd_top(s0, m, out_dim, out_dim, 1, 1.0, top, ar, s, pf));
   const int r = top.kept;
@@ -382,9 +389,9 @@ int power_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, con
   if (same) {
     SPB_ALLOC(ar, int, fflag, 1);
     SPB_CUDA(cudaMemsetAsync(fflag, 0, sizeof(int), s));
-    SPB_TRY(check_finite_async(m, ncols, C, ncols, fflag, s));
     PendingFlag pf;
     pf.dev = fflag;
+    pf.check_input = true;
     pf.msg = "power iterate overflowed; enable re-orthonormalization (reorth)";
     SPB_TRY(svd_top(C, m, ncols, ncols, 1, 2.0 * q + 1.0, top, ar, s, pf));
     // the reference forms G = (C C^T)^q C explicitly and raises once it
@@ -440,9 +447,9 @@ int sketch_basis(const double* X, int64_t rows, int64_t cols, int64_t ldx, doubl
   Arena ar(s);
   SPB_ALLOC(ar, int, fflag, 1);
   SPB_CUDA(cudaMemsetAsync(fflag, 0, sizeof(int), s));
-  SPB_TRY(check_finite_async(rows, cols, X, ldx, fflag, s));
   PendingFlag pf;
   pf.dev = fflag;
+  pf.check_input = true;
   pf.msg = "sketch contains non-finite entries";
   TopSvd top;
   SPB_TRY(svd_top(X, rows, cols, ldx, 1, power, top, ar, s, pf));
@@ -559,7 +566,7 @@ int power_id(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, cons
   // SVD of the coarse sketch: rank and the top-r triplets for the lifting
   const int want = std::max(2 * k, r_req);
   TopSvd top;
-  SPB_TRY(svd_top(coarse, m, nc, nc, want, 1.0, top, ar, s));
+  SPB_TRY(svd_top(coarse, m, nc, nc, want, 1.0, top, ar, s, PendingFlag(), /*want_v=*/true));
   int rank = top.kept;
   int warn = 0;
   int r = r_req > 0 ? r_req : std::max(k, std::min(2 * k, rank));

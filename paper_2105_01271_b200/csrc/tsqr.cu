@@ -6,16 +6,23 @@
 // based, which keeps the span of every direction to eps * ||X|| regardless of
 // conditioning.
 //
-// Layout: a CTA factors a 256 x 32 chunk with LANE = COLUMN: warp w holds
-// rows [32w, 32w+32) and lane c holds those 32 entries of column c in
-// registers.  Loads / stores of a row are coalesced (lanes = consecutive
-// columns), a column dot product is a private 32-term FMA chain plus an
-// 8-way shared-memory reduction across warps, the reflector column is
-// broadcast through shared memory -- two __syncthreads per Householder step
-// and no predicated all-column sweeps.  Fixed reduction order, so results
-// are bitwise reproducible.  The 32 x 32 R factors of the chunks are stacked
-// and factored again until one chunk remains; Q is then formed top-down by
-// applying each chunk's reflectors to its block of the parent Q.
+// Factor (tsqr_leaf_kernel): a CTA factors a 256 x cols chunk with
+// LANE = COLUMN: warp w holds rows g = 8 i + w (register slot i) and lane c
+// holds those 32 entries of column c.  Householder step j needs ONE block
+// reduction: lane j's column reaches the other lanes of its warp by shuffles,
+// and the vector of dot products <x_j(below j), x_c> -- whose j-th entry is
+// the norm^2 below the diagonal -- is reduced across the 8 warps together
+// with row j (double-buffered, one __syncthreads per step).  The same dot
+// products give v_c^T v_j for c < j, from which the compact-WY factor T
+// (H_0 ... H_{n-1} = I - V T V^T) is formed in the CTA at the end.
+// The chunks' R factors (cols x cols) are stacked and factored again until a
+// single chunk remains; its R, sign-normalised to diag(R) >= 0, is the result.
+//
+// Q (tsqr_apply_kernel, top-down): each chunk's block of the parent Q is
+// Q_h [B_h; 0] = [B_h; 0] - V_h (T_h (V_top,h^T B_h)), a parallel 64-row-tile
+// product (no per-reflector synchronisation); the root starts from
+// B = diag(sign(R_jj)).  Fixed reduction orders throughout: bitwise
+// reproducible.
 #include "common.cuh"
 #include "launch_count.cuh"
 
@@ -27,7 +34,7 @@ int gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const do
          int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
          cudaStream_t s);
 
-constexpr int kQB = 32;                 // panel width
+constexpr int kQB = 32;                 // panel width (register columns)
 constexpr int kQWarps = 8;
 constexpr int kQThreads = kQWarps * 32;
 constexpr int kQCH = kQWarps * 32;      // rows per chunk
@@ -38,18 +45,22 @@ constexpr int kQCH = kQWarps * 32;      // rows per chunk
 __device__ __forceinline__ int qrow(int i, int w) { return i * kQWarps + w; }
 constexpr int kQDiagSlots = kQB / kQWarps;  // 4
 
-// Factor chunk blockIdx.x of X (rows x cols, cols <= 32).  Writes the
-// reflectors (strictly below the chunk diagonal) to V (rows x 32), tau to
-// tau[chunk*32 + j] and the chunk's upper-trapezoidal R into
-// Rs[chunk*32 .. +32) x 32 (zero padded).
+// Factor chunk blockIdx.x of X (rows x cols).  Writes the reflectors
+// (strictly below the chunk diagonal, unit diagonal implicit) to V
+// (rows x 32), the chunk's 32 x 32 compact-WY factor to Tg, and its
+// cols x cols upper-triangular R to Rs[chunk * cols ..) (ld 32).  When
+// Rfinal != nullptr (single chunk = root) R is also written there with
+// diag(R) >= 0 and the row signs to sgn.
 __global__ void __launch_bounds__(kQThreads)
 tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t ldx, double* __restrict__ V,
-                 double* __restrict__ tau, double* __restrict__ Rs) {
-  __shared__ double colj[kQCH];
-  __shared__ double part[kQWarps];
-  __shared__ double red[kQWarps][kQB];
-  __shared__ double rdiag[kQB];
-  __shared__ double alpha_s;
+                 double* __restrict__ Tg, double* __restrict__ Rs, double* __restrict__ Rfinal, int64_t ldr,
+                 double* __restrict__ sgn) {
+  __shared__ double red[2][kQWarps][kQB];
+  __shared__ double rowj[2][kQB];
+  __shared__ double zs[kQB][kQB + 1];  // zs[c][j] = v_c^T v_j (c < j)
+  __shared__ double ts[kQB][kQB + 1];  // T (upper triangular)
+  __shared__ double tau_s[kQB], inv_s[kQB], beta_s[kQB];
+  __shared__ __align__(16) double colb[kQWarps][kQB];
   const int w = threadIdx.x >> 5, c = threadIdx.x & 31;
   const int64_t c0 = (int64_t)blockIdx.x * kQCH;
   const int nrow = (int)imin64(kQCH, rows - c0);
@@ -59,179 +70,306 @@ tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t l
     const int g = qrow(i, w);
     x[i] = (g < nrow && c < cols) ? X[(c0 + g) * ldx + c] : 0.0;
   }
-  const int nref = nrow < kQB ? nrow : kQB;
+  const int nref = nrow < cols ? nrow : cols;
+  for (int e = threadIdx.x; e < kQB * (kQB + 1); e += kQThreads) (&zs[0][0])[e] = 0.0;
+  // Column j is left untouched by its own step (it keeps alpha_j on the
+  // diagonal and (alpha_j - beta_j) v_j below it); the scaled reflector and
+  // beta_j are substituted when the chunk is written out.  Steps therefore
+  // update columns c > j only, uniformly across the warp:
+  //   x_c -= x_j * (inv_j * w_c),  w_c = tau_j v_j^T x_c.
+  int buf = 0;
   for (int j = 0; j < nref; ++j) {
-    // (1) lane j publishes column j below the diagonal (zero on and above it)
+    // (1) lane j publishes its column (my warp's rows) through shared memory;
+    // partial <x_j, x_c> over my rows
     if (c == j) {
-      double sq0 = 0.0, sq1 = 0.0;
 #pragma unroll
-      for (int i = 0; i < kQDiagSlots; ++i) {
-        const int g = qrow(i, w);
-        const double xi = (g > j) ? x[i] : 0.0;
-        colj[g] = xi;
-        sq0 = fma(xi, xi, sq0);
-        if (g == j) alpha_s = x[i];
-      }
-#pragma unroll
-      for (int i = kQDiagSlots; i < 32; i += 2) {
-        colj[qrow(i, w)] = x[i];
-        colj[qrow(i + 1, w)] = x[i + 1];
-        sq0 = fma(x[i], x[i], sq0);
-        sq1 = fma(x[i + 1], x[i + 1], sq1);
-      }
-      part[w] = sq0 + sq1;
+      for (int i = 0; i < 32; i += 2) *reinterpret_cast<double2*>(&colb[w][i]) = make_double2(x[i], x[i + 1]);
     }
-    __syncthreads();
-    double sigma2 = 0.0;
+    __syncwarp();
+    double xj[32];
 #pragma unroll
-    for (int q = 0; q < kQWarps; ++q) sigma2 += part[q];
-    const double alpha = alpha_s;
-    double beta = alpha, tj = 0.0, inv = 0.0;
-    if (sigma2 > 0.0) {
-      const double nrm = sqrt(fma(alpha, alpha, sigma2));
-      beta = alpha >= 0.0 ? -nrm : nrm;
-      tj = (beta - alpha) / beta;
-      inv = 1.0 / (alpha - beta);
+    for (int i = 0; i < 32; i += 2) {
+      const double2 t = *reinterpret_cast<const double2*>(&colb[w][i]);
+      xj[i] = t.x;
+      xj[i + 1] = t.y;
     }
-    // (2) reflector entries of my rows (v_j = 1) and the dot with my column
-    double v[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = colj[qrow(i, w)] * inv;
 #pragma unroll
     for (int i = 0; i < kQDiagSlots; ++i)
-      if (qrow(i, w) == j) v[i] = 1.0;
-    double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+      if (qrow(i, w) <= j) xj[i] = 0.0;
+    double pa[8];
 #pragma unroll
-    for (int i = 0; i < 32; i += 4) {
-      p0 = fma(v[i], x[i], p0);
-      p1 = fma(v[i + 1], x[i + 1], p1);
-      p2 = fma(v[i + 2], x[i + 2], p2);
-      p3 = fma(v[i + 3], x[i + 3], p3);
+    for (int u = 0; u < 8; ++u) pa[u] = xj[u] * x[u];
+#pragma unroll
+    for (int i = 8; i < 32; i += 8)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) pa[u] = fma(xj[i + u], x[i + u], pa[u]);
+    red[buf][w][c] = ((pa[0] + pa[1]) + (pa[2] + pa[3])) + ((pa[4] + pa[5]) + (pa[6] + pa[7]));
+    const int jw = j & (kQWarps - 1), js = j >> 3;  // owner warp / slot of row j
+    if (w == jw) {
+      double rj = x[0];
+#pragma unroll
+      for (int i = 1; i < kQDiagSlots; ++i)
+        if (i == js) rj = x[i];
+      rowj[buf][c] = rj;
     }
-    red[w][c] = (p0 + p1) + (p2 + p3);
     __syncthreads();
-    double wc = 0.0;
+    // (2) reflector scalars (every thread, same order: identical values)
+    double rc[kQWarps], rj[kQWarps];
 #pragma unroll
-    for (int q = 0; q < kQWarps; ++q) wc += red[q][c];
-    wc *= tj;
-    // (3) apply H_j to the trailing columns; lane j stores the reflector
-    if (c > j) {
-#pragma unroll
-      for (int i = 0; i < 32; ++i) x[i] = fma(-v[i], wc, x[i]);
-    } else if (c == j) {
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int g = qrow(i, w);
-        if (g < nrow) V[(c0 + g) * kQB + j] = (g > j) ? v[i] : 0.0;
-      }
+    for (int q = 0; q < kQWarps; ++q) {
+      rc[q] = red[buf][q][c];
+      rj[q] = red[buf][q][j];
     }
+    const double dc = ((rc[0] + rc[1]) + (rc[2] + rc[3])) + ((rc[4] + rc[5]) + (rc[6] + rc[7]));
+    const double sigma2 = ((rj[0] + rj[1]) + (rj[2] + rj[3])) + ((rj[4] + rj[5]) + (rj[6] + rj[7]));
+    const double alpha = rowj[buf][j], ac = rowj[buf][c];
+    double beta = alpha, tj = 0.0, inv = 0.0;
+    if (sigma2 > 0.0) {
+      // one rsqrt and one division: nrm = s2 / sqrt(s2), tau = -(alpha - beta) / beta
+      const double s2 = fma(alpha, alpha, sigma2);
+      const double rs = rsqrt(s2);
+      const double sg = alpha >= 0.0 ? 1.0 : -1.0;
+      beta = -sg * (s2 * rs);
+      const double dd = alpha - beta;  // |dd| >= ||x_j(j:)|| > 0
+      inv = 1.0 / dd;
+      tj = sg * dd * rs;
+    }
+    const double vv = fma(inv, dc, ac);  // v_j^T x_c (c > j);  (alpha_c - beta_c) v_c^T v_j (c < j)
+    // (3) apply H_j to the trailing columns
+    const double wc = c > j ? tj * vv : 0.0;
+    const double sc = inv * wc;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) x[i] = fma(-xj[i], sc, x[i]);
+    if (w == jw) {
+#pragma unroll
+      for (int i = 0; i < kQDiagSlots; ++i)
+        if (i == js) x[i] -= wc;
+    }
+    if (c < j && w == 0) zs[c][j] = inv_s[c] * vv;
     if (threadIdx.x == 0) {
-      tau[(int64_t)blockIdx.x * kQB + j] = tj;
-      rdiag[j] = beta;
+      tau_s[j] = tj;
+      inv_s[j] = inv;
+      beta_s[j] = beta;
     }
+    buf ^= 1;
   }
   __syncthreads();
-  // columns >= nref were never reflected: their reflector column is zero
-  if (c >= nref) {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const int g = qrow(i, w);
-      if (g < nrow) V[(c0 + g) * kQB + c] = 0.0;
+  // compact-WY T by recursive doubling: for adjacent blocks [V1 V2] of width
+  // b, T12 = -T11 (V1^T V2) T22 (exact for tau = 0 too); 5 levels of two
+  // parallel small products instead of a 32-step serial recurrence.
+  for (int e = threadIdx.x; e < kQB * kQB; e += kQThreads) {
+    const int r = e / kQB, q = e % kQB;
+    ts[r][q] = (r == q && q < nref) ? tau_s[q] : 0.0;
+  }
+  __syncthreads();
+  double* wsm = &red[0][0][0];  // 16 b <= 256 products per level
+  for (int b = 1; b < kQB; b <<= 1) {
+    const int nout = (kQB / 2) * b;
+    if (threadIdx.x < nout) {
+      const int e = threadIdx.x, p = e / (b * b), rq = e % (b * b), r = rq / b, q = rq % b;
+      const int o1 = p * 2 * b, o2 = o1 + b;
+      double a = 0.0;
+      for (int l = 0; l <= q; ++l) a = fma(zs[o1 + r][o2 + l], ts[o2 + l][o2 + q], a);
+      wsm[e] = a;
     }
+    __syncthreads();
+    if (threadIdx.x < nout) {
+      const int e = threadIdx.x, p = e / (b * b), rq = e % (b * b), r = rq / b, q = rq % b;
+      const int o1 = p * 2 * b, o2 = o1 + b;
+      double a = 0.0;
+      for (int l = r; l < b; ++l) a = fma(ts[o1 + r][o1 + l], wsm[p * b * b + l * b + q], a);
+      ts[o1 + r][o2 + q] = -a;
+    }
+    __syncthreads();
   }
-  if (threadIdx.x < kQB && threadIdx.x >= nref) tau[(int64_t)blockIdx.x * kQB + threadIdx.x] = 0.0;
-#pragma unroll
-  for (int i = 0; i < kQDiagSlots; ++i) {
-    const int g = qrow(i, w);  // g < 32
-    double rv = 0.0;
-    if (g < nrow && c >= g) rv = (c == g && g < nref) ? rdiag[g] : x[i];
-    Rs[((int64_t)blockIdx.x * kQB + g) * kQB + c] = rv;
-  }
-}
-
-// Out rows of chunk blockIdx.x = H_0 ... H_31 [Bin_chunk ; 0], where
-// Bin_chunk = Bin[chunk*32 .. +32) (ld 32), or the identity when Bin == nullptr.
-// The chunk's reflectors are staged once in shared memory (dynamic, 64 KB);
-// one __syncthreads per reflector (reduction buffer double-buffered).
-__global__ void __launch_bounds__(kQThreads)
-tsqr_apply_kernel(const double* __restrict__ V, const double* __restrict__ tau, int64_t rows,
-                  const double* __restrict__ Bin, double* __restrict__ Out, int64_t ldo, int out_cols) {
-  extern __shared__ double vsm[];  // [kQCH][kQB]
-  __shared__ double red[2][kQWarps][kQB];
-  __shared__ double tau_s[kQB];
-  const int w = threadIdx.x >> 5, c = threadIdx.x & 31;
-  const int64_t c0 = (int64_t)blockIdx.x * kQCH;
-  const int nrow = (int)imin64(kQCH, rows - c0);
-  for (int e = threadIdx.x; e < kQCH * kQB; e += kQThreads) {
-    const int g = e / kQB;
-    vsm[e] = (g < nrow) ? V[(c0 + g) * kQB + (e % kQB)] : 0.0;
-  }
-  if (threadIdx.x < kQB) tau_s[threadIdx.x] = tau[(int64_t)blockIdx.x * kQB + threadIdx.x];
-  double x[32];
+  // reflectors (coalesced rows), R rows, T
+  const double inv_c = c < nref ? inv_s[c] : 0.0;
 #pragma unroll
   for (int i = 0; i < 32; ++i) {
     const int g = qrow(i, w);
-    double init = 0.0;
-    if (i < kQDiagSlots && g < nrow)
-      init = Bin ? Bin[((int64_t)blockIdx.x * kQB + g) * kQB + c] : (g == c ? 1.0 : 0.0);
-    x[i] = init;
+    if (g < nrow) V[(c0 + g) * kQB + c] = (g > c && c < nref) ? x[i] * inv_c : 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < kQDiagSlots; ++i) {
+    const int g = qrow(i, w);  // g < 32
+    if (g < cols) {
+      double rv = (g < nrow && c >= g && c < cols) ? x[i] : 0.0;
+      if (c == g && g < nref) rv = beta_s[g];
+      x[i] = rv;
+      Rs[((int64_t)blockIdx.x * cols + g) * kQB + c] = rv;
+    }
   }
   __syncthreads();
-  const int nref = nrow < kQB ? nrow : kQB;
-  int buf = 0;
-  for (int j = nref - 1; j >= 0; --j) {
-    const double tj = tau_s[j];
-    if (tj == 0.0) continue;  // uniform across the CTA
-    double v[32];
+  for (int e = threadIdx.x; e < kQB * kQB; e += kQThreads)
+    Tg[(int64_t)blockIdx.x * kQB * kQB + e] = ts[e / kQB][e % kQB];
+  if (Rfinal != nullptr) {
+    // root: rows of R with diag(R) >= 0 (the diagonal sits in warp g & 7, slot g >> 3)
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = vsm[qrow(i, w) * kQB + j];
-#pragma unroll
-    for (int i = 0; i < kQDiagSlots; ++i)
-      if (qrow(i, w) == j) v[i] = 1.0;
-    double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
-#pragma unroll
-    for (int i = 0; i < 32; i += 4) {
-      p0 = fma(v[i], x[i], p0);
-      p1 = fma(v[i + 1], x[i + 1], p1);
-      p2 = fma(v[i + 2], x[i + 2], p2);
-      p3 = fma(v[i + 3], x[i + 3], p3);
-    }
-    red[buf][w][c] = (p0 + p1) + (p2 + p3);
-    __syncthreads();
-    double wc = 0.0;
-#pragma unroll
-    for (int q = 0; q < kQWarps; ++q) wc += red[buf][q][c];
-    wc *= tj;
-#pragma unroll
-    for (int i = 0; i < 32; ++i) x[i] = fma(-v[i], wc, x[i]);
-    buf ^= 1;
-  }
-  if (c < out_cols) {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
+    for (int i = 0; i < kQDiagSlots; ++i) {
       const int g = qrow(i, w);
-      if (g < nrow) Out[(c0 + g) * ldo + c] = x[i];
+      if (g < cols) {
+        const double d = __shfl_sync(0xffffffffu, x[i], g);
+        const double sg = d < 0.0 ? -1.0 : 1.0;
+        if (c < cols) Rfinal[(int64_t)g * ldr + c] = (c >= g) ? sg * x[i] : 0.0;
+        if (c == 0) sgn[g] = sg;
+      }
     }
   }
 }
 
-// make diag(R) >= 0: flip column j of Q and row j of R when R_jj < 0.  The
-// signs are latched first (qr_diag_signs) because block 0 rewrites R_jj.
-__global__ void qr_diag_signs(int cols, const double* R, int64_t ldr, int* flip) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j < cols) flip[j] = R[(int64_t)j * ldr + j] < 0.0;
+// Top-down Q formation for chunk h = blockIdx.x / tiles, rows tile
+// (blockIdx.x % tiles) * 64 of it:  Out = [B_h; 0] - V_h M_h,
+// M_h = T_h (V_top^T B_h), B_h = Bin[h * cols ..) (cols x cols, ld 32) or
+// diag(sgn) at the root.  Out has cols columns.
+constexpr int kApRows = 64;
+constexpr int kApTiles = kQCH / kApRows;
+
+__global__ void __launch_bounds__(kQThreads)
+tsqr_apply_kernel(const double* __restrict__ V, const double* __restrict__ Tg, int64_t rows, int cols,
+                  const double* __restrict__ Bin, const double* __restrict__ sgn, double* __restrict__ Out,
+                  int64_t ldo) {
+  constexpr int P = kQB + 1;
+  __shared__ double ub[kApRows * P];  // V_top | B_h, later the V rows of the tile
+  __shared__ double tsm[kQB * P];     // T_h
+  __shared__ double ws[kQB * P];      // V_top^T B, then M
+  double* vt = ub;
+  double* bs = ub + kQB * P;
+  double* vr = ub;
+  const int h = blockIdx.x / kApTiles, tile = blockIdx.x % kApTiles;
+  const int64_t c0 = (int64_t)h * kQCH;
+  const int nrow = (int)imin64(kQCH, rows - c0);
+  const int r0 = tile * kApRows;
+  if (r0 >= nrow) return;  // uniform per CTA
+  const int nr = nrow - r0 < kApRows ? nrow - r0 : kApRows;
+  const int tid = threadIdx.x;
+  auto b_at = [&](int g, int k) -> double {
+    if (g >= cols || k >= cols) return 0.0;
+    return Bin ? Bin[((int64_t)h * cols + g) * kQB + k] : (g == k ? sgn[g] : 0.0);
+  };
+  // reflectors carry an implicit unit diagonal (stored zeros on/above it)
+  for (int e = tid; e < kQB * kQB; e += kQThreads) {
+    const int g = e / kQB, k = e % kQB;
+    cp_async_f64(&vt[g * P + k], V + (c0 + (g < nrow ? g : 0)) * kQB + k, g < nrow);
+    cp_async_f64(&tsm[g * P + k], Tg + (int64_t)h * kQB * kQB + e, true);
+    if (Bin) {
+      const bool ok = g < cols && k < cols;
+      cp_async_f64(&bs[g * P + k], ok ? Bin + ((int64_t)h * cols + g) * kQB + k : Bin, ok);
+    } else {
+      bs[g * P + k] = b_at(g, k);
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  if (tid < kQB && tid < nrow) vt[tid * P + tid] = 1.0;
+  __syncthreads();
+  // W = V_top^T B  (only the top cols rows of [B; 0] are nonzero)
+  for (int e = tid; e < kQB * kQB; e += kQThreads) {
+    const int k = e / kQB, c = e % kQB;
+    double a = 0.0;
+    for (int g = 0; g < cols; ++g) a = fma(vt[g * P + k], bs[g * P + c], a);
+    ws[k * P + c] = a;
+  }
+  __syncthreads();
+  // M = T W (T upper triangular), staged through registers; V rows of the tile
+  constexpr int kPer = kQB * kQB / kQThreads;
+  double mreg[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int e = tid + u * kQThreads;
+    const int k = e / kQB, c = e % kQB;
+    double a = 0.0;
+    for (int l = k; l < kQB; ++l) a = fma(tsm[k * P + l], ws[l * P + c], a);
+    mreg[u] = a;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int e = tid + u * kQThreads;
+    ws[(e / kQB) * P + (e % kQB)] = mreg[u];
+  }
+  for (int e = tid; e < kApRows * kQB; e += kQThreads) {
+    const int g = e / kQB, k = e % kQB, gl = r0 + g;
+    cp_async_f64(&vr[g * P + k], V + (c0 + (g < nr ? gl : 0)) * kQB + k, g < nr);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  if (r0 < kQB && tid < kApRows && r0 + tid < kQB && tid < nr) vr[tid * P + r0 + tid] = 1.0;
+  __syncthreads();
+  // Out rows = [B; 0] - V M
+  for (int e = tid; e < kApRows * kQB; e += kQThreads) {
+    const int g = e / kQB, c = e % kQB;
+    if (g >= nr || c >= cols) continue;
+    const int gl = r0 + g;
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int k = 0; k < kQB; k += 2) {
+      a = fma(vr[g * P + k], ws[k * P + c], a);
+      b = fma(vr[g * P + k + 1], ws[(k + 1) * P + c], b);
+    }
+    const double base = gl < kQB ? b_at(gl, c) : 0.0;
+    Out[(c0 + gl) * ldo + c] = base - (a + b);
+  }
 }
 
-__global__ void qr_positive_diag(int64_t rows, int cols, double* Q, int64_t ldq, double* R,
-                                 int64_t ldr, const int* flip) {
-  const int j = blockIdx.y;
-  if (!flip[j]) return;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows;
-       i += (int64_t)gridDim.x * blockDim.x)
-    Q[i * ldq + j] = -Q[i * ldq + j];
-  if (blockIdx.x == 0)
-    for (int c = threadIdx.x; c < cols; c += blockDim.x)
-      if (c >= j) R[(int64_t)j * ldr + c] = -R[(int64_t)j * ldr + c];
+static int tsqr32(int64_t rows, int cols, const double* X, int64_t ldx, double* Q, int64_t ldq, double* R,
+                  int64_t ldr, cudaStream_t s) {
+  Arena ar(s);
+  struct Level {
+    int64_t rows;
+    int nch;
+    double* V;
+    double* T;
+    double* Rs;
+  };
+  std::vector<Level> lv;
+  const double* in = X;
+  int64_t in_ld = ldx;
+  int64_t r = rows;
+  SPB_ALLOC(ar, double, sgn, kQB);
+  while (true) {
+    Level L;
+    L.rows = r;
+    L.nch = (int)ceil_div(r, kQCH);
+    L.V = ar.alloc<double>((size_t)r * kQB);
+    L.T = ar.alloc<double>((size_t)L.nch * kQB * kQB);
+    L.Rs = ar.alloc<double>((size_t)L.nch * cols * kQB);
+    if (!L.V || !L.T || !L.Rs) {
+      set_error("tsqr workspace allocation failed");
+      return SP_ECUDA;
+    }
+    const bool root = L.nch == 1;
+    tsqr_leaf_kernel<<<L.nch, kQThreads, 0, s>>>(in, r, cols, in_ld, L.V, L.T, L.Rs, root ? R : nullptr, ldr,
+                                                 root ? sgn : nullptr);
+    count_launch();
+    SPB_CHECK_LAUNCH();
+    lv.push_back(L);
+    if (root) break;
+    in = L.Rs;
+    in_ld = kQB;
+    r = (int64_t)L.nch * cols;
+  }
+  const double* bin = nullptr;
+  for (int l = (int)lv.size() - 1; l >= 0; --l) {
+    const Level& L = lv[l];
+    double* out;
+    int64_t ldo;
+    if (l == 0) {
+      out = Q;
+      ldo = ldq;
+    } else {
+      out = ar.alloc<double>((size_t)L.rows * kQB);
+      if (!out) {
+        set_error("tsqr workspace allocation failed");
+        return SP_ECUDA;
+      }
+      ldo = kQB;
+    }
+    tsqr_apply_kernel<<<L.nch * kApTiles, kQThreads, 0, s>>>(L.V, L.T, L.rows, cols, bin, sgn, out, ldo);
+    count_launch();
+    SPB_CHECK_LAUNCH();
+    bin = out;
+  }
+  return SP_OK;
 }
 
 __global__ void copy_block(int64_t rows, int64_t cols, const double* src, int64_t lds, double* dst,
@@ -248,87 +386,6 @@ __global__ void add_block(int64_t rows, int64_t cols, const double* src, int64_t
   if (e >= rows * cols) return;
   const int64_t i = e / cols, c = e % cols;
   dst[i * ldd + c] += src[i * lds + c];
-}
-
-constexpr int kApplySmem = kQCH * kQB * (int)sizeof(double);
-
-static int tsqr32(int64_t rows, int cols, const double* X, int64_t ldx, double* Q, int64_t ldq, double* R,
-                  int64_t ldr, cudaStream_t s) {
-  SPB_CUDA(cudaFuncSetAttribute(tsqr_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kApplySmem));
-  Arena ar(s);
-  struct Level {
-    int64_t rows;
-    int nch;
-    double* V;
-    double* tau;
-    double* Rs;
-  };
-  std::vector<Level> lv;
-  const double* in = X;
-  int64_t in_ld = ldx;
-  int in_cols = cols;
-  int64_t r = rows;
-  while (true) {
-    Level L;
-    L.rows = r;
-    L.nch = ceil_div(r, kQCH);
-    L.V = ar.alloc<double>((size_t)r * kQB);
-    L.tau = ar.alloc<double>((size_t)L.nch * kQB);
-    L.Rs = ar.alloc<double>((size_t)L.nch * kQB * kQB);
-    if (!L.V || !L.tau || !L.Rs) {
-      set_error("tsqr workspace allocation failed");
-      return SP_ECUDA;
-    }
-    tsqr_leaf_kernel<<<L.nch, kQThreads, 0, s>>>(in, r, in_cols, in_ld, L.V, L.tau, L.Rs);
-    count_launch();
-    SPB_CHECK_LAUNCH();
-    lv.push_back(L);
-    if (L.nch == 1) break;
-    in = L.Rs;
-    in_ld = kQB;
-    in_cols = kQB;
-    r = (int64_t)L.nch * kQB;
-  }
-  copy_block<<<ceil_div((int64_t)cols * cols, 256), 256, 0, s>>>(cols, cols, lv.back().Rs, kQB, R, ldr);
-  count_launch();
-  SPB_CHECK_LAUNCH();
-  const double* bin = nullptr;
-  for (int l = (int)lv.size() - 1; l >= 0; --l) {
-    const Level& L = lv[l];
-    double* out;
-    int64_t ldo;
-    int oc;
-    if (l == 0) {
-      out = Q;
-      ldo = ldq;
-      oc = cols;
-    } else {
-      out = ar.alloc<double>((size_t)L.rows * kQB);
-      if (!out) {
-        set_error("tsqr workspace allocation failed");
-        return SP_ECUDA;
-      }
-      ldo = kQB;
-      oc = kQB;
-    }
-    tsqr_apply_kernel<<<L.nch, kQThreads, kApplySmem, s>>>(L.V, L.tau, L.rows, bin, out, ldo, oc);
-    count_launch();
-    SPB_CHECK_LAUNCH();
-    bin = out;
-  }
-  int* flip = ar.alloc<int>((size_t)cols);
-  if (!flip) {
-    set_error("tsqr workspace allocation failed");
-    return SP_ECUDA;
-  }
-  qr_diag_signs<<<ceil_div(cols, 64), 64, 0, s>>>(cols, R, ldr, flip);
-  count_launch();
-  SPB_CHECK_LAUNCH();
-  dim3 g(std::min(ceil_div(rows, 256), 64), cols);
-  qr_positive_diag<<<g, 256, 0, s>>>(rows, cols, Q, ldq, R, ldr, flip);
-  count_launch();
-  SPB_CHECK_LAUNCH();
-  return SP_OK;
 }
 
 // Wide inputs: 32-column panels, two block Gram-Schmidt passes against the

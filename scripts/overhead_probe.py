@@ -6,10 +6,10 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import paper_2105_01271_b200 as sp
 from paper_2105_01271_b200 import _lib
 from paper_2105_01271_b200.datagen import CONFIGS
-from bench import generate_device
+from paper_2105_01271_b200.datagen import generate_device
 warnings.simplefilter("ignore")
 cfg = CONFIGS["cfg2"]; dev = torch.device("cuda", 0)
-A = generate_device(cfg, torch, dev)
+A = generate_device(cfg, dev)
 op, cols = sp.grid_injection(cfg.grid, cfg.stride)
 pc = sp.PowerConfig(q=1, columns=cols)
 def api():
@@ -30,10 +30,19 @@ U = torch.empty((cfg.m, cfg.k), dtype=torch.float64, device=dev); S = torch.empt
 info = _lib.new_info()
 def bare():
     _lib.call("sp_power_svd", A.data_ptr(), 0, cfg.m, cfg.n, cfg.n, idx.data_ptr(), w.data_ptr(), depth, op.n_c, None, 0,
-              dcols.data_ptr(), cols.size, 1, cfg.k, C.data_ptr(), C.data_ptr(), U.data_ptr(), S.data_ptr(), V.data_ptr(), _lib.info_ptr(info), s)
+              dcols.data_ptr(), cols.size, 1, cfg.k, C.data_ptr(), C.data_ptr(), 3, U.data_ptr(), S.data_ptr(), V.data_ptr(), _lib.info_ptr(info), s)
 for _ in range(3): bare()
 torch.cuda.synchronize()
 t0 = time.perf_counter()
 for _ in range(10): bare()
 torch.cuda.synchronize()
 print("bare C wall ms", (time.perf_counter() - t0) / 10 * 1e3, "launches", info[_lib.INFO_LAUNCHES])
+# step-only section for ncu launch lists: PROBE_STEPS API calls, nothing else
+import os
+n = int(os.environ.get("PROBE_STEPS", "0"))
+if n:
+    torch.cuda.synchronize()
+    torch.cuda.cudart().cudaProfilerStart()
+    for _ in range(n): api()
+    torch.cuda.synchronize()
+    torch.cuda.cudart().cudaProfilerStop()

@@ -104,7 +104,9 @@ def test_skinny_atz_f32_and_determinism(cuda):
 
 # ------------------------------------------------------------------ K3 ----
 @pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
-@pytest.mark.parametrize("M,N,K", [(64, 64, 16), (100, 37, 259), (3, 200, 4000), (513, 65, 7)])
+@pytest.mark.parametrize("M,N,K", [(64, 64, 16), (100, 37, 259), (3, 200, 4000), (513, 65, 7),
+                                   (7, 7, 65536), (40, 33, 3000), (64, 64, 5000), (2, 3, 700),
+                                   (3000, 33, 40), (5000, 64, 64), (700, 1, 1), (65536, 43, 7)])
 def test_gemm(cuda, ta, tb, M, N, K):
     rng = philox(M + N + K + ta * 2 + tb)
     A = rng.standard_normal((K, M) if ta else (M, K))
@@ -118,7 +120,9 @@ def test_gemm(cuda, ta, tb, M, N, K):
 
 
 # ------------------------------------------------------------------ K4 ----
-@pytest.mark.parametrize("rows,cols", [(1000, 8), (5000, 32), (70000, 20), (300, 64), (2000, 100), (32, 32)])
+@pytest.mark.parametrize("rows,cols", [(1000, 8), (5000, 32), (70000, 20), (300, 64), (2000, 100), (32, 32),
+                                       (4096, 32), (65536, 7), (257, 32), (33, 32), (512, 1), (100, 3),
+                                       (200000, 32), (7, 7)])
 def test_tsqr(cuda, rows, cols):
     x = philox(rows + cols).standard_normal((rows, cols)) * np.logspace(0, -8, cols)
     dx = _dev(x, cuda)
@@ -157,6 +161,26 @@ def test_cholqr2_breakdown_falls_back(cuda):
     assert np.linalg.norm(q @ r - x) <= 1e-13 * np.linalg.norm(x)
 
 
+@pytest.mark.parametrize("rows,cols,rank", [(4096, 32, 9), (2000, 32, 1), (65536, 7, 3), (300, 20, 0)])
+def test_tsqr32_rank_deficient(cuda, rows, cols, rank):
+    x = rank_deficient(philox(rows + rank), rows, cols, rank) if rank else np.zeros((rows, cols))
+    if rank:
+        x[:, 3] = 0.0  # an exactly zero column
+    dx = _dev(x, cuda)
+    q = cuda.empty((rows, cols), dtype=cuda.float64, device="cuda")
+    r = cuda.empty((cols, cols), dtype=cuda.float64, device="cuda")
+    for _ in range(2):
+        _lib.call("sp_tsqr", rows, cols, dx.data_ptr(), cols, q.data_ptr(), cols, r.data_ptr(), cols,
+                  _stream(cuda))
+        qn, rn = q.cpu().numpy(), r.cpu().numpy()
+        assert np.abs(qn.T @ qn - np.eye(cols)).max() < 1e-12
+        assert np.linalg.norm(qn @ rn - x) <= 1e-13 * max(np.linalg.norm(x), 1e-300)
+        assert np.allclose(np.tril(rn, -1), 0) and np.all(np.diag(rn) >= 0)
+        if _ == 0:
+            first = (qn.tobytes(), rn.tobytes())
+    assert (qn.tobytes(), rn.tobytes()) == first  # bitwise reproducible
+
+
 def test_tsqr_rank_deficient_keeps_orthonormality(cuda):
     x = rank_deficient(philox(4), 3000, 40, 5)
     dx = _dev(x, cuda)
@@ -184,6 +208,24 @@ def test_jacobi_svd(cuda, n):
     np.testing.assert_allclose(s, want, rtol=1e-12 * n, atol=1e-15 * want[0] * n)
     np.testing.assert_allclose((u * s) @ v.T, m, atol=1e-14 * want[0] * n)
     np.testing.assert_allclose(v.T @ v, np.eye(n), atol=1e-13)
+
+
+@pytest.mark.parametrize("n,decay", [(3, 0.0), (16, -14.0), (31, -3.0), (32, -16.0), (32, -30.0)])
+def test_jacobi_svd_small_without_v(cuda, n, decay):
+    """n <= 32 lane-per-column kernel, U and S only (V not accumulated)."""
+    rng = philox(100 + n)
+    m = rng.standard_normal((n, n)) @ np.diag(np.logspace(0, decay, n)) @ rng.standard_normal((n, n))
+    dm = _dev(m, cuda)
+    u = cuda.zeros((n, n), dtype=cuda.float64, device="cuda")
+    s = cuda.zeros((n,), dtype=cuda.float64, device="cuda")
+    _lib.call("sp_jacobi_svd", n, dm.data_ptr(), n, u.data_ptr(), n, s.data_ptr(), None, n, _stream(cuda))
+    u, s = u.cpu().numpy(), s.cpu().numpy()
+    want = np.linalg.svd(m, compute_uv=False)
+    assert np.all(np.diff(s) <= 0)
+    np.testing.assert_allclose(s, want, rtol=0, atol=1e-14 * want[0] * n)
+    keep = s > 1e-8 * s[0]  # well separated, well above rounding: unique up to sign
+    uref = np.linalg.svd(m)[0][:, keep]
+    np.testing.assert_allclose(np.abs(np.sum(u[:, keep] * uref, axis=0)), 1.0, atol=1e-9)
 
 
 # ------------------------------------------------------ API dense kernels ----
