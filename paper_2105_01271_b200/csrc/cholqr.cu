@@ -117,6 +117,189 @@ static int cholqr_pass(int64_t rows, int c, const double* X, int64_t ldx, double
   return SP_OK;
 }
 
+// ------------------------------------------------ fused path, c <= 32 ----
+// Five launches for CholeskyQR2 of a tall block with c <= 32 columns:
+//   tall_gram partials(X) -> chol_small -> mul_gram (Q1 = X R1^{-1} and the
+//   partial Gram of Q1 in the same pass) -> chol_small (R = R2 R1) -> tall_mul.
+// Partials are summed in a fixed order: bitwise reproducible.
+constexpr int kCsThreads = 1024;
+
+// G = sum_b P[b] (nb slabs of c x c), Cholesky G = R^T R, Rinv = R^{-1};
+// when R1 != nullptr also Rout = R R1 (upper triangular product).
+__global__ void __launch_bounds__(kCsThreads)
+chol_small_kernel(int c, int nb, const double* __restrict__ P, double* __restrict__ R, double* __restrict__ Rinv,
+                  const double* __restrict__ R1, double* __restrict__ Rout, int64_t ldro, int* flag) {
+  __shared__ double G[32][33];
+  __shared__ double Ri[32][33];
+  __shared__ double part[8][32 * 32 / 8 + 1];
+  const int tid = threadIdx.x, nout = c * c;
+  // fixed-order reduction: thread (o, g) sums slabs g, g + G, ... of output o
+  const int gsplit = kCsThreads / nout >= 32 ? 32 : (kCsThreads / nout >= 1 ? kCsThreads / nout : 1);
+  for (int o0 = 0; o0 < nout; o0 += kCsThreads / gsplit) {
+    const int o = o0 + tid / gsplit, g = tid % gsplit;
+    double a = 0.0;
+    if (o < nout && tid / gsplit < kCsThreads / gsplit) {
+#pragma unroll 4
+      for (int b = g; b < nb; b += gsplit) a += P[(int64_t)b * nout + o];
+    }
+    __shared__ double tmp[kCsThreads];
+    tmp[tid] = a;
+    __syncthreads();
+    if (g == 0 && o < nout && tid / gsplit < kCsThreads / gsplit) {
+      double t = tmp[tid];
+      for (int q = 1; q < gsplit; ++q) t += tmp[tid + q];
+      G[o / c][o % c] = t;
+    }
+    __syncthreads();
+  }
+  // right-looking Cholesky, one warp-synchronous step per column
+  __shared__ int bad;
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  for (int j = 0; j < c; ++j) {
+    const double d = G[j][j];
+    if (!(d > 0.0)) {
+      if (tid == 0) bad = 1;
+      break;
+    }
+    const double dinv = 1.0 / d;
+    for (int e = tid; e < (c - j - 1) * (c - j - 1); e += kCsThreads) {
+      const int i = j + 1 + e / (c - j - 1), l = j + 1 + e % (c - j - 1);
+      if (l >= i) G[i][l] = fma(-G[j][i] * dinv, G[j][l], G[i][l]);
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (bad) {
+    if (tid == 0) atomicOr(flag, 1);
+    return;
+  }
+  __shared__ double dsq[32];
+  if (tid < c) dsq[tid] = sqrt(G[tid][tid]);
+  __syncthreads();
+  for (int e = tid; e < nout; e += kCsThreads) {
+    const int i = e / c, l = e % c;
+    G[i][l] = (l > i) ? G[i][l] / dsq[i] : (l == i ? dsq[i] : 0.0);
+  }
+  __syncthreads();
+  // R^{-1}: column l solved by thread l (back substitution, c <= 32)
+  if (tid < c) {
+    const int l = tid;
+    for (int i = c - 1; i >= 0; --i) {
+      double acc = (i == l) ? 1.0 : 0.0;
+      for (int q = i + 1; q <= l; ++q) acc = fma(-G[i][q], Ri[q][l], acc);
+      Ri[i][l] = (i <= l) ? acc / G[i][i] : 0.0;
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < nout; e += kCsThreads) {
+    const int i = e / c, l = e % c;
+    R[e] = G[i][l];
+    Rinv[e] = Ri[i][l];
+    if (Rout) {
+      double acc = 0.0;
+      for (int q = i; q <= l; ++q) acc = fma(G[i][q], R1[q * c + l], acc);
+      Rout[(int64_t)i * ldro + l] = (l >= i) ? acc : 0.0;
+    }
+  }
+}
+
+// Q1 rows = X rows R^{-1} (c x c) and partial[blk] = Q1_blk^T Q1_blk; one
+// thread per row (c <= 32), rows staged through shared memory.
+constexpr int kMgRows = 128;
+constexpr int kMgTiles = 2;  // row tiles per CTA (fewer Gram partials)
+
+__global__ void __launch_bounds__(kMgRows)
+mul_gram_kernel(int64_t rows, int c, const double* __restrict__ X, int64_t ldx, const double* __restrict__ Ri,
+                double* __restrict__ Q, int64_t ldq, double* __restrict__ partial) {
+  __shared__ double ms[32][32];
+  __shared__ double ts[kMgRows][33];
+  const int t = threadIdx.x;
+  for (int e = t; e < c * c; e += kMgRows) cp_async_f64(&ms[e / c][e % c], Ri + e, true);
+  // thread t accumulates Gram outputs t, t + 128, ... over the CTA's tiles
+  double gacc[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) gacc[u] = 0.0;
+  for (int tile = 0; tile < kMgTiles; ++tile) {
+    const int64_t base = ((int64_t)blockIdx.x * kMgTiles + tile) * kMgRows;
+    if (base >= rows) break;  // uniform
+    const int nr = (int)imin64(kMgRows, rows - base);
+    for (int e = t; e < nr * c; e += kMgRows) {
+      const int rr = e / c, cc = e - (e / c) * c;
+      cp_async_f64(&ts[rr][cc], X + (base + rr) * ldx + cc, true);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    double acc[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) acc[j] = 0.0;
+    if (t < nr) {
+      for (int i = 0; i < c; ++i) {
+        const double xi = ts[t][i];
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < c) acc[j] = fma(xi, ms[i][j], acc[j]);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < c) ts[t][j] = t < nr ? acc[j] : 0.0;
+    __syncthreads();
+    for (int e = t; e < nr * c; e += kMgRows) {
+      const int rr = e / c, cc = e - (e / c) * c;
+      Q[(base + rr) * ldq + cc] = ts[rr][cc];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int o = t + u * kMgRows;
+      if (o < c * c) {
+        const int a = o / c, b = o % c;
+        double s0 = 0.0, s1 = 0.0;
+        int rr = 0;
+        for (; rr + 1 < nr; rr += 2) {
+          s0 = fma(ts[rr][a], ts[rr][b], s0);
+          s1 = fma(ts[rr + 1][a], ts[rr + 1][b], s1);
+        }
+        if (rr < nr) s0 = fma(ts[rr][a], ts[rr][b], s0);
+        gacc[u] += s0 + s1;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int o = t + u * kMgRows;
+    if (o < c * c) partial[(int64_t)blockIdx.x * c * c + o] = gacc[u];
+  }
+}
+
+static int cholqr2_small(int64_t rows, int c, const double* X, int64_t ldx, double* Q, int64_t ldq, double* R,
+                         int64_t ldr, int* dflag, cudaStream_t s) {
+  Arena ar(s);
+  const int nb1 = (int)std::min<int64_t>(kNumSMs, ceil_div(rows, 128));
+  const int nb2 = ceil_div(rows, (int64_t)kMgRows * kMgTiles);
+  SPB_ALLOC(ar, double, P1, (size_t)nb1 * c * c);
+  SPB_ALLOC(ar, double, P2, (size_t)nb2 * c * c);
+  SPB_ALLOC(ar, double, R1, (size_t)c * c);
+  SPB_ALLOC(ar, double, R1i, (size_t)c * c);
+  SPB_ALLOC(ar, double, R2, (size_t)c * c);
+  SPB_ALLOC(ar, double, R2i, (size_t)c * c);
+  SPB_ALLOC(ar, double, Q1, (size_t)rows * c);
+  int nb = 0;
+  SPB_TRY(tall_gram_partials(rows, c, X, ldx, c, X, ldx, P1, nb1, &nb, s));
+  chol_small_kernel<<<1, kCsThreads, 0, s>>>(c, nb, P1, R1, R1i, nullptr, nullptr, 0, dflag);
+  count_launch();
+  SPB_CHECK_LAUNCH();
+  mul_gram_kernel<<<nb2, kMgRows, 0, s>>>(rows, c, X, ldx, R1i, Q1, c, P2);
+  count_launch();
+  SPB_CHECK_LAUNCH();
+  chol_small_kernel<<<1, kCsThreads, 0, s>>>(c, nb2, P2, R2, R2i, R1, R, ldr, dflag);
+  count_launch();
+  SPB_CHECK_LAUNCH();
+  return tall_mul(rows, c, Q1, c, c, R2i, c, 1.0, 0.0, Q, ldq, s);
+}
+
 // CholeskyQR2.  Returns SP_OK with *breakdown = true when a Cholesky failed
 // (Q, R are then garbage and the caller must fall back).  Synchronises once.
 // Asynchronous CholeskyQR2: breakdown is OR-ed into the device flag *dflag
@@ -125,6 +308,7 @@ int cholqr2_async(int64_t rows, int64_t cols, const double* X, int64_t ldx, doub
                   double* R, int64_t ldr, int* dflag, cudaStream_t s) {
   SPB_REQUIRE(cols >= 1 && cols <= 112 && rows >= cols, "cholqr2 needs rows >= cols, cols <= 112");
   const int c = (int)cols;
+  if (c <= 32 && rows >= 256) return cholqr2_small(rows, c, X, ldx, Q, ldq, R, ldr, dflag, s);
   Arena ar(s);
   SPB_ALLOC(ar, double, Q1, (size_t)rows * c);
   SPB_ALLOC(ar, double, R1, (size_t)c * c);

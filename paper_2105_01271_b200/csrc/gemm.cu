@@ -18,11 +18,22 @@
 
 namespace spb {
 
-constexpr int kBM = 64, kBN = 64, kBK = 16;
+constexpr int kBK = 16;
 constexpr int kGemmThreads = 128;
-constexpr int kPadK = kBK + 4;   // k-contiguous rows: stride 20 doubles
-constexpr int kPadMN = kBM + 4;  // mn-contiguous rows: stride 68 doubles
-constexpr int kStageDoubles = (kBM * kPadK > kBK * kPadMN ? kBM * kPadK : kBK * kPadMN);
+// k-contiguous rows: stride 20 doubles (18 for the 128-row tiles, which
+// would otherwise not fit two stages in 48 KB of static shared memory)
+template <int ROWS>
+struct PadK {
+  static constexpr int v = ROWS > 64 ? kBK + 2 : kBK + 4;
+};
+
+// Tile shapes: 64 x 64 (2 x 2 warps of 32 x 32) and, for N <= 32, 128 x 32
+// (4 x 1 warps) so the narrow products of the path do not pad N to 64.
+template <int BM, int BN>
+struct Tile {
+  static constexpr int kWarpsM = BM / 32;
+  static_assert(kWarpsM * (BN / 32) == 4, "4 warps of 32 x 32");
+};
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
   unsigned saddr = (unsigned)__cvta_generic_to_shared(smem);
@@ -45,46 +56,50 @@ __device__ __forceinline__ const double* op_ptr(const double* X, int64_t ld, int
   return TRANS ? X + k * ld + r : X + r * ld + k;
 }
 
-// smem offset of element (r, k) of an op(X) tile (r in [0,64), k in [0,16))
-template <int TRANS>
+// smem offset of element (r, k) of an op(X) tile (r in [0, ROWS), k in [0,16))
+template <int TRANS, int ROWS>
 __device__ __forceinline__ int tile_off(int r, int k) {
-  return TRANS ? k * kPadMN + r : r * kPadK + k;
+  return TRANS ? k * (ROWS + 4) + r : r * PadK<ROWS>::v + k;
 }
 
-template <int TRANS>
+template <int TRANS, int ROWS>
 __device__ __forceinline__ void load_tile(double* st, const double* X, int64_t ld, int64_t R,
                                           int64_t K, int64_t r0, int64_t k0, int64_t k_end) {
-  // 64 x 16 elements, 8 per thread; consecutive threads walk the contiguous dim
+  // ROWS x 16 elements; consecutive threads walk the contiguous dim
 #pragma unroll
-  for (int u = 0; u < (kBM * kBK) / kGemmThreads; ++u) {
+  for (int u = 0; u < (ROWS * kBK) / kGemmThreads; ++u) {
     const int e = threadIdx.x + u * kGemmThreads;
     int r, k;
     if (TRANS) {  // stored K x R: contiguous along r
-      k = e / kBM;
-      r = e % kBM;
+      k = e / ROWS;
+      r = e % ROWS;
     } else {  // stored R x K: contiguous along k
       r = e / kBK;
       k = e % kBK;
     }
     const int64_t gr = r0 + r, gk = k0 + k;
     const bool ok = (gr < R) && (gk < k_end);
-    cp_async8(st + tile_off<TRANS>(r, k), ok ? op_ptr<TRANS>(X, ld, gr, gk) : X, ok);
+    cp_async8(st + tile_off<TRANS, ROWS>(r, k), ok ? op_ptr<TRANS>(X, ld, gr, gk) : X, ok);
   }
 }
 
-template <int TA, int TB>
+template <int TA, int TB, int BM, int BN>
 __global__ void __launch_bounds__(kGemmThreads)
 dgemm_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, int64_t lda,
              const double* __restrict__ B, int64_t ldb, double* __restrict__ C, int64_t ldc,
              double alpha, double beta, int64_t k_per_split, bool partial) {
-  __shared__ __align__(16) double sA[2][kStageDoubles];
-  __shared__ __align__(16) double sB[2][kStageDoubles];
+  using TL = Tile<BM, BN>;
+  // stage sizes for the operand orientations (op(B) tile is stored as (n, k) with orientation !TB)
+  constexpr int kSA = TA ? kBK * (BM + 4) : BM * PadK<BM>::v;
+  constexpr int kSB = TB ? BN * PadK<BN>::v : kBK * (BN + 4);
+  __shared__ __align__(16) double sA[2][kSA];
+  __shared__ __align__(16) double sB[2][kSB];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+  const int wm = (warp % TL::kWarpsM) * 32, wn = (warp / TL::kWarpsM) * 32;
   // linear tile index (grid.x can exceed 65535 tiles for n-row operands)
-  const int64_t tiles_n = (N + kBN - 1) / kBN;
-  const int64_t m0 = ((int64_t)blockIdx.x / tiles_n) * kBM, n0 = ((int64_t)blockIdx.x % tiles_n) * kBN;
+  const int64_t tiles_n = (N + BN - 1) / BN;
+  const int64_t m0 = ((int64_t)blockIdx.x / tiles_n) * BM, n0 = ((int64_t)blockIdx.x % tiles_n) * BN;
   const int64_t kb = (int64_t)blockIdx.z * k_per_split;
   const int64_t ke = min(K, kb + k_per_split);
   const int ntiles = (int)((ke - kb + kBK - 1) / kBK);
@@ -96,16 +111,16 @@ dgemm_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, int6
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   if (ntiles > 0) {
-    load_tile<TA>(sA[0], A, lda, M, K, m0, kb, ke);
-    load_tile<TB ? 0 : 1>(sB[0], B, ldb, N, K, n0, kb, ke);
+    load_tile<TA, BM>(sA[0], A, lda, M, K, m0, kb, ke);
+    load_tile<TB ? 0 : 1, BN>(sB[0], B, ldb, N, K, n0, kb, ke);
   }
   cp_async_commit();
   for (int kt = 0; kt < ntiles; ++kt) {
     const int cur = kt & 1;
     if (kt + 1 < ntiles) {
       const int64_t kn = kb + (int64_t)(kt + 1) * kBK;
-      load_tile<TA>(sA[cur ^ 1], A, lda, M, K, m0, kn, ke);
-      load_tile<TB ? 0 : 1>(sB[cur ^ 1], B, ldb, N, K, n0, kn, ke);
+      load_tile<TA, BM>(sA[cur ^ 1], A, lda, M, K, m0, kn, ke);
+      load_tile<TB ? 0 : 1, BN>(sB[cur ^ 1], B, ldb, N, K, n0, kn, ke);
       cp_async_commit();
       cp_async_wait<1>();
     } else {
@@ -118,10 +133,10 @@ dgemm_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, int6
     for (int kk = 0; kk < kBK; kk += 4) {
       double af[4], bf[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = a_s[tile_off<TA>(wm + i * 8 + g, kk + t)];
+      for (int i = 0; i < 4; ++i) af[i] = a_s[tile_off<TA, BM>(wm + i * 8 + g, kk + t)];
       // op(B) is K x N; stored tile holds (n, k) with orientation !TB
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = b_s[tile_off<TB ? 0 : 1>(wn + j * 8 + g, kk + t)];
+      for (int j = 0; j < 4; ++j) bf[j] = b_s[tile_off<TB ? 0 : 1, BN>(wn + j * 8 + g, kk + t)];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -200,11 +215,24 @@ __global__ void scale_matrix(int64_t M, int64_t N, double beta, double* C, int64
   *p = (beta == 0.0) ? 0.0 : beta * *p;
 }
 
-template <int TA, int TB>
+template <int TA, int TB, int BM, int BN>
 static void launch_dgemm(dim3 grid, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                          const double* B, int64_t ldb, double* C, int64_t ldc, double alpha,
                          double beta, int64_t kps, bool partial, cudaStream_t s) {
-  dgemm_kernel<TA, TB><<<grid, kGemmThreads, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, kps, partial);
+  dgemm_kernel<TA, TB, BM, BN><<<grid, kGemmThreads, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, kps,
+                                                             partial);
+}
+
+template <int BM, int BN>
+static void launch_dgemm_any(int code, dim3 grid, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                             const double* B, int64_t ldb, double* C, int64_t ldc, double alpha, double beta,
+                             int64_t kps, bool partial, cudaStream_t s) {
+  switch (code) {
+    case 0: launch_dgemm<0, 0, BM, BN>(grid, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, kps, partial, s); break;
+    case 1: launch_dgemm<0, 1, BM, BN>(grid, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, kps, partial, s); break;
+    case 2: launch_dgemm<1, 0, BM, BN>(grid, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, kps, partial, s); break;
+    default: launch_dgemm<1, 1, BM, BN>(grid, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, kps, partial, s); break;
+  }
 }
 
 int gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
@@ -225,7 +253,9 @@ int gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const do
     return tall_gram(K, (int)M, A, lda, (int)N, B, ldb, alpha, beta, C, ldc, s);
   if (ta == 0 && tb == 0 && K <= 64 && N <= 64 && M >= 256)
     return tall_mul(M, (int)K, A, lda, (int)N, B, ldb, alpha, beta, C, ldc, s);
-  const int gx = ceil_div(N, kBN), gy = ceil_div(M, kBM);
+  const bool narrow = N <= 32;
+  const int bm = narrow ? 128 : 64, bn = narrow ? 32 : 64;
+  const int gx = ceil_div(N, bn), gy = ceil_div(M, bm);
   const int64_t tiles = (int64_t)gx * gy;
   int S = 1;
   if (tiles < 2 * kNumSMs) {
@@ -248,12 +278,10 @@ int gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const do
     }
   }
   const int code = ta * 2 + tb;
-  switch (code) {
-    case 0: launch_dgemm<0, 0>(grid, M, N, K, A, lda, B, ldb, out, ldc, alpha, beta, kps, partial, s); break;
-    case 1: launch_dgemm<0, 1>(grid, M, N, K, A, lda, B, ldb, out, ldc, alpha, beta, kps, partial, s); break;
-    case 2: launch_dgemm<1, 0>(grid, M, N, K, A, lda, B, ldb, out, ldc, alpha, beta, kps, partial, s); break;
-    default: launch_dgemm<1, 1>(grid, M, N, K, A, lda, B, ldb, out, ldc, alpha, beta, kps, partial, s); break;
-  }
+  if (narrow)
+    launch_dgemm_any<128, 32>(code, grid, M, N, K, A, lda, B, ldb, out, ldc, alpha, beta, kps, partial, s);
+  else
+    launch_dgemm_any<64, 64>(code, grid, M, N, K, A, lda, B, ldb, out, ldc, alpha, beta, kps, partial, s);
   count_launch();
   SPB_CHECK_LAUNCH();
   if (partial) return split_reduce(out, S, M, N, alpha, beta, C, ldc, s);

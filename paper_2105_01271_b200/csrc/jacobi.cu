@@ -263,9 +263,16 @@ jacobi32_kernel(int n, const double* __restrict__ M, int64_t ldm, double* __rest
       if (plane < 0) continue;
       const bool low = c < plane;  // canonical (p, q) = (min, max)
       const double ap = low ? a : b, aq = low ? b : a;
-      if (!(g != 0.0 && fmin(ap, aq) > negl && fabs(g) > kJacTol * sqrt(ap) * sqrt(aq))) continue;
+      const double apq = ap * aq;
+      const bool big = !(apq < 1e300);  // rare: fall back to the overflow-safe forms
+      if (!(g != 0.0 && fmin(ap, aq) > negl &&
+            (big ? fabs(g) > kJacTol * sqrt(ap) * sqrt(aq) : g * g > (kJacTol * kJacTol) * apq)))
+        continue;
       const double d = aq - ap, h = 2.0 * g;
-      const double t = copysign(1.0, d) * h / (fabs(d) + hypot(d, h));
+      const double ad = fabs(d), ah = fabs(h);
+      const double hyp = (ad < 1e150 && ah < 1e150 && (ad > 1e-150 || ah > 1e-150)) ? sqrt(fma(d, d, h * h))
+                                                                                  : hypot(d, h);
+      const double t = copysign(1.0, d) * h / (ad + hyp);
       const double cs = rsqrt(fma(t, t, 1.0));
       const double sn = cs * t;
       // p' = cs p - sn q ; q' = sn p + cs q
@@ -316,7 +323,15 @@ int jacobi_svd(int64_t n, const double* M, int64_t ldm, double* U, int64_t ldu, 
     SPB_CHECK_LAUNCH();
     return SP_OK;
   }
-  SPB_REQUIRE(V != nullptr, "Jacobi SVD needs V for n > 32");
+  Arena vscratch(s);
+  if (V == nullptr) {  // the multi-warp kernel always accumulates V
+    V = vscratch.alloc<double>((size_t)n * n);
+    ldv = n;
+    if (!V) {
+      set_error("jacobi workspace allocation failed");
+      return SP_ECUDA;
+    }
+  }
   const int np = std::max<int>(2, (int)(n + (n & 1)));
   const int threads = std::min(1024, std::max(64, 32 * (np / 2)));
   const size_t smem = (size_t)2 * np * np * sizeof(double);

@@ -20,6 +20,8 @@ int tsqr(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, in
          double* R, int64_t ldr, cudaStream_t s);
 int tall_gram(int64_t rows, int c, const double* X, int64_t ldx, int d, const double* Y, int64_t ldy,
               double alpha, double beta, double* G, int64_t ldg, cudaStream_t s);
+int tall_gram_partials(int64_t rows, int c, const double* X, int64_t ldx, int d, const double* Y, int64_t ldy,
+                       double* part, int nb_max, int* nb_out, cudaStream_t s);
 // C (M x N, ldc) = alpha * sum_{s < S} P[s] + beta * C, P dense M x N slabs, fixed order
 int split_reduce(const double* P, int S, int64_t M, int64_t N, double alpha, double beta, double* C, int64_t ldc,
                  cudaStream_t s);

@@ -112,6 +112,19 @@ static int launch_tall_gram(int nb, int64_t rows, int c, const double* X, int64_
   return SP_OK;
 }
 
+// per-CTA partials only (nb_max slabs of c x d available in part; *nb_out = used)
+int tall_gram_partials(int64_t rows, int c, const double* X, int64_t ldx, int d, const double* Y, int64_t ldy,
+                       double* part, int nb_max, int* nb_out, cudaStream_t s) {
+  SPB_REQUIRE(c >= 1 && d >= 1 && c <= kTallMax && d <= kTallMax, "tall_gram supports widths <= 64");
+  SPB_REQUIRE(rows >= 1 && nb_max >= 1, "tall_gram needs rows >= 1");
+  int nb = (int)std::min<int64_t>(nb_max, ceil_div(rows, 2 * kTgTile));
+  const int64_t rpc = ceil_div(ceil_div(rows, nb), kTgTile) * (int64_t)kTgTile;
+  nb = (int)ceil_div(rows, rpc);
+  *nb_out = nb;
+  return (c <= 32 && d <= 32) ? launch_tall_gram<2>(nb, rows, c, X, ldx, d, Y, ldy, rpc, part, s)
+                              : launch_tall_gram<4>(nb, rows, c, X, ldx, d, Y, ldy, rpc, part, s);
+}
+
 int tall_gram(int64_t rows, int c, const double* X, int64_t ldx, int d, const double* Y, int64_t ldy,
               double alpha, double beta, double* G, int64_t ldg, cudaStream_t s) {
   SPB_REQUIRE(c >= 1 && d >= 1 && c <= kTallMax && d <= kTallMax, "tall_gram supports widths <= 64");
@@ -128,30 +141,27 @@ int tall_gram(int64_t rows, int c, const double* X, int64_t ldx, int d, const do
   return split_reduce(part, nb, c, d, alpha, beta, G, ldg, s);
 }
 
-// O = alpha X M + beta O.  Thread (row, g) forms the 8 output columns
-// [8g, 8g + 8) of one row (so a 2000-row product still spreads over ~1000
-// warps); a CTA stages its rows of X (coalesced cp.async) and M in shared
-// memory.  Each output row depends only on the same row of X, and the CTA's
-// rows are staged before any output is written, so O may alias X (same rows,
-// any columns).
+// O = alpha X M + beta O.  A CTA owns R = min(128, 1024 / d) consecutive rows
+// and each thread forms output elements t, t + 256, ... of that row-major
+// R x d block, so loads and stores are coalesced whatever d is; the rows of X
+// and all of M are staged in shared memory (cp.async).  Each output row
+// depends only on the same row of X, and the CTA's rows are staged before
+// any output is written, so O may alias X (same rows, any columns).
 constexpr int kTmThreads = 256;
-constexpr int kTmGroup = 8;
 
 __global__ void __launch_bounds__(kTmThreads)
 tall_mul_kernel(int64_t rows, int c, const double* X, int64_t ldx, int d, const double* __restrict__ M,
                 int64_t ldm, double alpha, double beta, double* O, int64_t ldo, const double* __restrict__ top,
-                int64_t ldt, int64_t top_rows) {
+                int64_t ldt, int64_t top_rows, int rpc) {
   extern __shared__ __align__(16) double tm_smem[];
-  const int ng = (d + kTmGroup - 1) / kTmGroup, dpad = ng * kTmGroup;
-  const int rpc = kTmThreads / ng;  // rows per CTA
   const int sp = c + 1;
-  double* ms = tm_smem;             // [c][dpad], zero padded
-  double* ts = tm_smem + c * dpad;  // [rpc][sp]
+  double* ms = tm_smem;          // [c][d]
+  double* ts = tm_smem + c * d;  // [rpc][sp]
   const int64_t base = (int64_t)blockIdx.x * rpc;
   const int nr = (int)imin64(rpc, rows - base);
-  for (int e = threadIdx.x; e < c * dpad; e += kTmThreads) {
-    const int i = e / dpad, j = e - (e / dpad) * dpad;
-    cp_async_f64(&ms[e], j < d ? M + (int64_t)i * ldm + j : M, j < d);
+  for (int e = threadIdx.x; e < c * d; e += kTmThreads) {
+    const int i = e / d, j = e - (e / d) * d;
+    cp_async_f64(&ms[e], M + (int64_t)i * ldm + j, true);
   }
   for (int e = threadIdx.x; e < nr * c; e += kTmThreads) {
     const int rr = e / c, cc = e - (e / c) * c;
@@ -159,34 +169,31 @@ tall_mul_kernel(int64_t rows, int c, const double* X, int64_t ldx, int d, const 
   }
   cp_async_wait_all();
   __syncthreads();
-  const int rr = threadIdx.x / ng, g = threadIdx.x - (threadIdx.x / ng) * ng;
-  if (rr >= nr) return;
-  const int j0 = g * kTmGroup;
-  double acc[kTmGroup];
+  const int ne = nr * d;
+  for (int e0 = threadIdx.x; e0 < ne; e0 += 4 * kTmThreads) {
+    double acc[4], old[4];
+    int rr[4], cc[4];
 #pragma unroll
-  for (int u = 0; u < kTmGroup; ++u) acc[u] = 0.0;
-  const double* xr = ts + rr * sp;
-  for (int i = 0; i < c; ++i) {
-    const double xi = xr[i];
-    const double2* mr = reinterpret_cast<const double2*>(ms + i * dpad + j0);
-#pragma unroll
-    for (int u = 0; u < kTmGroup / 2; ++u) {
-      const double2 m2 = mr[u];
-      acc[2 * u] = fma(xi, m2.x, acc[2 * u]);
-      acc[2 * u + 1] = fma(xi, m2.y, acc[2 * u + 1]);
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * kTmThreads;
+      rr[u] = e < ne ? e / d : 0;
+      cc[u] = e < ne ? e - rr[u] * d : 0;
+      acc[u] = 0.0;
+      old[u] = (beta != 0.0 && e < ne) ? O[(base + rr[u]) * ldo + cc[u]] : 0.0;
     }
-  }
-  const int64_t row = base + rr;
-  double* orow = O + row * ldo;
-  double old[kTmGroup];
+    for (int i = 0; i < c; ++i) {
 #pragma unroll
-  for (int u = 0; u < kTmGroup; ++u) old[u] = (beta != 0.0 && j0 + u < d) ? orow[j0 + u] : 0.0;
+      for (int u = 0; u < 4; ++u) acc[u] = fma(ts[rr[u] * sp + i], ms[i * d + cc[u]], acc[u]);
+    }
 #pragma unroll
-  for (int u = 0; u < kTmGroup; ++u) {
-    if (j0 + u < d) {
-      double v = alpha * acc[u];
-      if (row < top_rows) v += top[row * ldt + j0 + u];
-      orow[j0 + u] = (beta == 0.0) ? v : fma(beta, old[u], v);
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * kTmThreads;
+      if (e < ne) {
+        const int64_t row = base + rr[u];
+        double v = alpha * acc[u];
+        if (row < top_rows) v += top[row * ldt + cc[u]];
+        O[row * ldo + cc[u]] = (beta == 0.0) ? v : fma(beta, old[u], v);
+      }
     }
   }
 }
@@ -201,11 +208,10 @@ int tall_mul(int64_t rows, int c, const double* X, int64_t ldx, int d, const dou
     SPB_CUDA(cudaFuncSetAttribute(tall_mul_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
     attr = true;
   }
-  const int ng = (d + kTmGroup - 1) / kTmGroup, dpad = ng * kTmGroup;
-  const int rpc = kTmThreads / ng;
-  const size_t smem = ((size_t)c * dpad + (size_t)rpc * (c + 1)) * sizeof(double);
+  const int rpc = std::max(1, std::min(128, 1024 / d));
+  const size_t smem = ((size_t)c * d + (size_t)rpc * (c + 1)) * sizeof(double);
   tall_mul_kernel<<<ceil_div(rows, rpc), kTmThreads, smem, s>>>(rows, c, X, ldx, d, M, ldm, alpha, beta, O, ldo,
-                                                                top, ldt, top ? top_rows : 0);
+                                                                top, ldt, top ? top_rows : 0, rpc);
   count_launch();
   SPB_CHECK_LAUNCH();
   return SP_OK;

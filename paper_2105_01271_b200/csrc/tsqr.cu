@@ -23,10 +23,14 @@
 // product (no per-reflector synchronisation); the root starts from
 // B = diag(sign(R_jj)).  Fixed reduction orders throughout: bitwise
 // reproducible.
+#include "async.cuh"
 #include "common.cuh"
 #include "launch_count.cuh"
 
+#include <cooperative_groups.h>
 #include <vector>
+
+namespace cg = cooperative_groups;
 
 namespace spb {
 
@@ -37,7 +41,8 @@ int gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const do
 constexpr int kQB = 32;                 // panel width (register columns)
 constexpr int kQWarps = 8;
 constexpr int kQThreads = kQWarps * 32;
-constexpr int kQCH = kQWarps * 32;      // rows per chunk
+constexpr int kQCH = kQWarps * 32;      // rows per CTA
+constexpr int kQMaxCluster = 16;        // CTAs per chunk (non-portable cluster size)
 
 // Row mapping: local row g = 8*i + w lives in warp w, register slot i, so
 // the 32 diagonal rows are spread 4 per warp (slots 0..3): only those slots
@@ -45,11 +50,16 @@ constexpr int kQCH = kQWarps * 32;      // rows per chunk
 __device__ __forceinline__ int qrow(int i, int w) { return i * kQWarps + w; }
 constexpr int kQDiagSlots = kQB / kQWarps;  // 4
 
-// Factor chunk blockIdx.x of X (rows x cols).  Writes the reflectors
-// (strictly below the chunk diagonal, unit diagonal implicit) to V
-// (rows x 32), the chunk's 32 x 32 compact-WY factor to Tg, and its
-// cols x cols upper-triangular R to Rs[chunk * cols ..) (ld 32).  When
-// Rfinal != nullptr (single chunk = root) R is also written there with
+// Factor chunk h of X (rows x cols).  A chunk is one thread-block CLUSTER of
+// `cl` CTAs (cl * 256 rows): every CTA reduces its 8 warps' partial dot
+// products, pushes the 32-vector to every CTA of the cluster through
+// distributed shared memory, and after one cluster barrier all CTAs sum the
+// cl partials in rank order -- identical scalars everywhere, one cluster
+// barrier per Householder step, and one level of the tree for up to 4096
+// rows.  Writes the reflectors (strictly below the chunk diagonal, unit
+// diagonal implicit) to V (rows x 32), the chunk's 32 x 32 compact-WY factor
+// to Tg, and its cols x cols upper-triangular R to Rs[h * cols ..) (ld 32).
+// When Rfinal != nullptr (single chunk = root) R is also written there with
 // diag(R) >= 0 and the row signs to sgn.
 __global__ void __launch_bounds__(kQThreads)
 tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t ldx, double* __restrict__ V,
@@ -57,21 +67,43 @@ tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t l
                  double* __restrict__ sgn) {
   __shared__ double red[2][kQWarps][kQB];
   __shared__ double rowj[2][kQB];
+  __shared__ double cbuf[2][kQMaxCluster][kQB];  // cluster partials (pushed by peers)
+  __shared__ double crow[2][kQB];                // row j (pushed by rank 0)
+  __shared__ __align__(8) uint64_t cbar[2];      // tx-counted arrival of a step's pushes
   __shared__ double zs[kQB][kQB + 1];  // zs[c][j] = v_c^T v_j (c < j)
   __shared__ double ts[kQB][kQB + 1];  // T (upper triangular)
   __shared__ double tau_s[kQB], inv_s[kQB], beta_s[kQB];
   __shared__ __align__(16) double colb[kQWarps][kQB];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int cl = (int)cluster.num_blocks();
+  const int cr = (int)cluster.block_rank();
   const int w = threadIdx.x >> 5, c = threadIdx.x & 31;
-  const int64_t c0 = (int64_t)blockIdx.x * kQCH;
-  const int nrow = (int)imin64(kQCH, rows - c0);
+  const int64_t h = blockIdx.x / cl;
+  const int64_t chunk0 = h * (int64_t)cl * kQCH;
+  const int64_t c0 = chunk0 + (int64_t)cr * kQCH;  // my first row
+  const int nrow = (int)std::max<int64_t>(0, imin64(kQCH, rows - c0));
+  const int chunk_rows = (int)imin64((int64_t)cl * kQCH, rows - chunk0);
+  const bool top = cr == 0;  // rows 0..31 of the chunk live in rank 0
   double x[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) {
     const int g = qrow(i, w);
     x[i] = (g < nrow && c < cols) ? X[(c0 + g) * ldx + c] : 0.0;
   }
-  const int nref = nrow < cols ? nrow : cols;
+  const int nref = chunk_rows < cols ? chunk_rows : cols;
   for (int e = threadIdx.x; e < kQB * (kQB + 1); e += kQThreads) (&zs[0][0])[e] = 0.0;
+  // per step every CTA receives cl partial vectors and row j: (cl + 1) * 256 bytes
+  const uint32_t step_bytes = (uint32_t)(cl + 1) * kQB * sizeof(double);
+  if (cl > 1) {
+    if (threadIdx.x == 0) {
+      mbar_init(&cbar[0], 1);
+      mbar_init(&cbar[1], 1);
+      mbar_fence_init();
+      mbar_arrive_expect_tx(&cbar[0], step_bytes);
+      mbar_arrive_expect_tx(&cbar[1], step_bytes);
+    }
+    cluster.sync();  // barriers initialised before any peer pushes
+  }
   // Column j is left untouched by its own step (it keeps alpha_j on the
   // diagonal and (alpha_j - beta_j) v_j below it); the scaled reflector and
   // beta_j are substituted when the chunk is written out.  Steps therefore
@@ -93,9 +125,11 @@ tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t l
       xj[i] = t.x;
       xj[i + 1] = t.y;
     }
+    if (top) {
 #pragma unroll
-    for (int i = 0; i < kQDiagSlots; ++i)
-      if (qrow(i, w) <= j) xj[i] = 0.0;
+      for (int i = 0; i < kQDiagSlots; ++i)
+        if (qrow(i, w) <= j) xj[i] = 0.0;
+    }
     double pa[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) pa[u] = xj[u] * x[u];
@@ -104,8 +138,8 @@ tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t l
 #pragma unroll
       for (int u = 0; u < 8; ++u) pa[u] = fma(xj[i + u], x[i + u], pa[u]);
     red[buf][w][c] = ((pa[0] + pa[1]) + (pa[2] + pa[3])) + ((pa[4] + pa[5]) + (pa[6] + pa[7]));
-    const int jw = j & (kQWarps - 1), js = j >> 3;  // owner warp / slot of row j
-    if (w == jw) {
+    const int jw = j & (kQWarps - 1), js = j >> 3;  // owner warp / slot of row j (rank 0)
+    if (top && w == jw) {
       double rj = x[0];
 #pragma unroll
       for (int i = 1; i < kQDiagSlots; ++i)
@@ -113,16 +147,45 @@ tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t l
       rowj[buf][c] = rj;
     }
     __syncthreads();
-    // (2) reflector scalars (every thread, same order: identical values)
-    double rc[kQWarps], rj[kQWarps];
+    // (2) reflector scalars (every thread of the cluster, same order: identical values)
+    double dc, sigma2, alpha, ac;
+    {
+      double rc[kQWarps], rq[kQWarps];
 #pragma unroll
-    for (int q = 0; q < kQWarps; ++q) {
-      rc[q] = red[buf][q][c];
-      rj[q] = red[buf][q][j];
+      for (int q = 0; q < kQWarps; ++q) {
+        rc[q] = red[buf][q][c];
+        rq[q] = red[buf][q][j];
+      }
+      dc = ((rc[0] + rc[1]) + (rc[2] + rc[3])) + ((rc[4] + rc[5]) + (rc[6] + rc[7]));
+      sigma2 = ((rq[0] + rq[1]) + (rq[2] + rq[3])) + ((rq[4] + rq[5]) + (rq[6] + rq[7]));
     }
-    const double dc = ((rc[0] + rc[1]) + (rc[2] + rc[3])) + ((rc[4] + rc[5]) + (rc[6] + rc[7]));
-    const double sigma2 = ((rj[0] + rj[1]) + (rj[2] + rj[3])) + ((rj[4] + rj[5]) + (rj[6] + rj[7]));
-    const double alpha = rowj[buf][j], ac = rowj[buf][c];
+    if (cl > 1) {
+      if (w == 0) {
+        const double rv = top ? rowj[buf][c] : 0.0;
+        for (int d = 0; d < cl; ++d) {
+          const uint32_t bar = cluster_addr(&cbar[buf], d);
+          st_async_f64(cluster_addr(&cbuf[buf][cr][c], d), dc, bar);
+          if (top) st_async_f64(cluster_addr(&crow[buf][c], d), rv, bar);
+        }
+      }
+      mbar_wait_cluster(&cbar[buf], (uint32_t)(j >> 1) & 1u);
+      // re-arm this buffer for step j + 2 (every thread has passed the wait
+      // of step j - 1 on the other buffer, and reads of step j happen before
+      // the __syncthreads of step j + 1, which precedes any push of step j + 2
+      // by this CTA's peers)
+      dc = 0.0;
+      sigma2 = 0.0;
+      for (int d = 0; d < cl; ++d) {
+        dc += cbuf[buf][d][c];
+        sigma2 += cbuf[buf][d][j];
+      }
+      alpha = crow[buf][j];
+      ac = crow[buf][c];
+      if (threadIdx.x == 0) mbar_arrive_expect_tx(&cbar[buf], step_bytes);
+    } else {
+      alpha = rowj[buf][j];
+      ac = rowj[buf][c];
+    }
     double beta = alpha, tj = 0.0, inv = 0.0;
     if (sigma2 > 0.0) {
       // one rsqrt and one division: nrm = s2 / sqrt(s2), tau = -(alpha - beta) / beta
@@ -140,7 +203,7 @@ tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t l
     const double sc = inv * wc;
 #pragma unroll
     for (int i = 0; i < 32; ++i) x[i] = fma(-xj[i], sc, x[i]);
-    if (w == jw) {
+    if (top && w == jw) {
 #pragma unroll
       for (int i = 0; i < kQDiagSlots; ++i)
         if (i == js) x[i] -= wc;
@@ -153,7 +216,17 @@ tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t l
     }
     buf ^= 1;
   }
+  if (cl > 1) cluster.sync();  // no CTA leaves while peers' pushes are in flight
   __syncthreads();
+  // reflectors (coalesced rows)
+  const double inv_c = c < nref ? inv_s[c] : 0.0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int g = qrow(i, w);
+    const int gc = cr * kQCH + g;  // chunk-local row
+    if (g < nrow) V[(c0 + g) * kQB + c] = (gc > c && c < nref) ? x[i] * inv_c : 0.0;
+  }
+  if (!top) return;
   // compact-WY T by recursive doubling: for adjacent blocks [V1 V2] of width
   // b, T12 = -T11 (V1^T V2) T22 (exact for tau = 0 too); 5 levels of two
   // parallel small products instead of a 32-step serial recurrence.
@@ -182,13 +255,7 @@ tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t l
     }
     __syncthreads();
   }
-  // reflectors (coalesced rows), R rows, T
-  const double inv_c = c < nref ? inv_s[c] : 0.0;
-#pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    const int g = qrow(i, w);
-    if (g < nrow) V[(c0 + g) * kQB + c] = (g > c && c < nref) ? x[i] * inv_c : 0.0;
-  }
+  // R rows (rank 0 holds chunk rows 0..31), T
 #pragma unroll
   for (int i = 0; i < kQDiagSlots; ++i) {
     const int g = qrow(i, w);  // g < 32
@@ -196,12 +263,10 @@ tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t l
       double rv = (g < nrow && c >= g && c < cols) ? x[i] : 0.0;
       if (c == g && g < nref) rv = beta_s[g];
       x[i] = rv;
-      Rs[((int64_t)blockIdx.x * cols + g) * kQB + c] = rv;
+      Rs[(h * cols + g) * kQB + c] = rv;
     }
   }
-  __syncthreads();
-  for (int e = threadIdx.x; e < kQB * kQB; e += kQThreads)
-    Tg[(int64_t)blockIdx.x * kQB * kQB + e] = ts[e / kQB][e % kQB];
+  for (int e = threadIdx.x; e < kQB * kQB; e += kQThreads) Tg[h * kQB * kQB + e] = ts[e / kQB][e % kQB];
   if (Rfinal != nullptr) {
     // root: rows of R with diag(R) >= 0 (the diagonal sits in warp g & 7, slot g >> 3)
 #pragma unroll
@@ -217,17 +282,16 @@ tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t l
   }
 }
 
-// Top-down Q formation for chunk h = blockIdx.x / tiles, rows tile
-// (blockIdx.x % tiles) * 64 of it:  Out = [B_h; 0] - V_h M_h,
+// Top-down Q formation for chunk h = blockIdx.x / tiles (chunk_rows rows),
+// rows tile (blockIdx.x % tiles) * 64 of it:  Out = [B_h; 0] - V_h M_h,
 // M_h = T_h (V_top^T B_h), B_h = Bin[h * cols ..) (cols x cols, ld 32) or
 // diag(sgn) at the root.  Out has cols columns.
 constexpr int kApRows = 64;
-constexpr int kApTiles = kQCH / kApRows;
 
 __global__ void __launch_bounds__(kQThreads)
 tsqr_apply_kernel(const double* __restrict__ V, const double* __restrict__ Tg, int64_t rows, int cols,
-                  const double* __restrict__ Bin, const double* __restrict__ sgn, double* __restrict__ Out,
-                  int64_t ldo) {
+                  int chunk_rows, const double* __restrict__ Bin, const double* __restrict__ sgn,
+                  double* __restrict__ Out, int64_t ldo) {
   constexpr int P = kQB + 1;
   __shared__ double ub[kApRows * P];  // V_top | B_h, later the V rows of the tile
   __shared__ double tsm[kQB * P];     // T_h
@@ -235,9 +299,10 @@ tsqr_apply_kernel(const double* __restrict__ V, const double* __restrict__ Tg, i
   double* vt = ub;
   double* bs = ub + kQB * P;
   double* vr = ub;
-  const int h = blockIdx.x / kApTiles, tile = blockIdx.x % kApTiles;
-  const int64_t c0 = (int64_t)h * kQCH;
-  const int nrow = (int)imin64(kQCH, rows - c0);
+  const int tiles = chunk_rows / kApRows;
+  const int h = blockIdx.x / tiles, tile = blockIdx.x % tiles;
+  const int64_t c0 = (int64_t)h * chunk_rows;
+  const int nrow = (int)imin64(chunk_rows, rows - c0);
   const int r0 = tile * kApRows;
   if (r0 >= nrow) return;  // uniform per CTA
   const int nr = nrow - r0 < kApRows ? nrow - r0 : kApRows;
@@ -311,12 +376,64 @@ tsqr_apply_kernel(const double* __restrict__ V, const double* __restrict__ Tg, i
   }
 }
 
+// cluster size for a level of `r` rows: one cluster covers up to 16 CTAs
+// (4096 rows); 16-CTA clusters are a non-portable size -- fall back to 8
+static int g_max_cluster = 0;
+
+static int launch_leaf(int nch, int cl, const double* in, int64_t r, int cols, int64_t in_ld, double* V, double* T,
+                       double* Rs, double* R, int64_t ldr, double* sgn, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nch * cl);
+  cfg.blockDim = dim3(kQThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, tsqr_leaf_kernel, in, r, cols, in_ld, V, T, Rs, R, ldr, sgn);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_error(std::string("tsqr leaf launch: ") + cudaGetErrorString(e));
+    return SP_ECUDA;
+  }
+  count_launch();
+  return SP_OK;
+}
+
+static int max_cluster() {
+  if (g_max_cluster == 0) {
+    int mc = 8;
+    if (cudaFuncSetAttribute(tsqr_leaf_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(kQMaxCluster);
+      cfg.blockDim = dim3(kQThreads);
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = kQMaxCluster;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int nclusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclusters, tsqr_leaf_kernel, &cfg) == cudaSuccess && nclusters > 0)
+        mc = kQMaxCluster;
+    }
+    cudaGetLastError();
+    g_max_cluster = mc;
+  }
+  return g_max_cluster;
+}
+
 static int tsqr32(int64_t rows, int cols, const double* X, int64_t ldx, double* Q, int64_t ldq, double* R,
                   int64_t ldr, cudaStream_t s) {
   Arena ar(s);
   struct Level {
     int64_t rows;
-    int nch;
+    int nch, cl;
     double* V;
     double* T;
     double* Rs;
@@ -326,10 +443,12 @@ static int tsqr32(int64_t rows, int cols, const double* X, int64_t ldx, double* 
   int64_t in_ld = ldx;
   int64_t r = rows;
   SPB_ALLOC(ar, double, sgn, kQB);
+  const int mc = max_cluster();
   while (true) {
     Level L;
     L.rows = r;
-    L.nch = (int)ceil_div(r, kQCH);
+    L.cl = (int)std::min<int64_t>(mc, ceil_div(r, kQCH));
+    L.nch = (int)ceil_div(r, (int64_t)L.cl * kQCH);
     L.V = ar.alloc<double>((size_t)r * kQB);
     L.T = ar.alloc<double>((size_t)L.nch * kQB * kQB);
     L.Rs = ar.alloc<double>((size_t)L.nch * cols * kQB);
@@ -338,10 +457,8 @@ static int tsqr32(int64_t rows, int cols, const double* X, int64_t ldx, double* 
       return SP_ECUDA;
     }
     const bool root = L.nch == 1;
-    tsqr_leaf_kernel<<<L.nch, kQThreads, 0, s>>>(in, r, cols, in_ld, L.V, L.T, L.Rs, root ? R : nullptr, ldr,
-                                                 root ? sgn : nullptr);
-    count_launch();
-    SPB_CHECK_LAUNCH();
+    SPB_TRY(launch_leaf(L.nch, L.cl, in, r, cols, in_ld, L.V, L.T, L.Rs, root ? R : nullptr, ldr,
+                        root ? sgn : nullptr, s));
     lv.push_back(L);
     if (root) break;
     in = L.Rs;
@@ -364,7 +481,9 @@ static int tsqr32(int64_t rows, int cols, const double* X, int64_t ldx, double* 
       }
       ldo = kQB;
     }
-    tsqr_apply_kernel<<<L.nch * kApTiles, kQThreads, 0, s>>>(L.V, L.T, L.rows, cols, bin, sgn, out, ldo);
+    const int chunk_rows = L.cl * kQCH;
+    tsqr_apply_kernel<<<L.nch * (chunk_rows / kApRows), kQThreads, 0, s>>>(L.V, L.T, L.rows, cols, chunk_rows, bin,
+                                                                          sgn, out, ldo);
     count_launch();
     SPB_CHECK_LAUNCH();
     bin = out;

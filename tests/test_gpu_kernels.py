@@ -106,7 +106,8 @@ def test_skinny_atz_f32_and_determinism(cuda):
 @pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
 @pytest.mark.parametrize("M,N,K", [(64, 64, 16), (100, 37, 259), (3, 200, 4000), (513, 65, 7),
                                    (7, 7, 65536), (40, 33, 3000), (64, 64, 5000), (2, 3, 700),
-                                   (3000, 33, 40), (5000, 64, 64), (700, 1, 1), (65536, 43, 7)])
+                                   (3000, 33, 40), (5000, 64, 64), (700, 1, 1), (65536, 43, 7),
+                                   (2000, 32, 4096), (4096, 32, 2000), (130, 5, 300), (129, 31, 70)])
 def test_gemm(cuda, ta, tb, M, N, K):
     rng = philox(M + N + K + ta * 2 + tb)
     A = rng.standard_normal((K, M) if ta else (M, K))
