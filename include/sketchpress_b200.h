@@ -138,6 +138,23 @@ int sp_jacobi_svd(int64_t n, const double* M, int64_t ldm, double* U, int64_t ld
 int sp_thin_svd(int64_t rows, int64_t cols, const double* X, int64_t ldx,
                 double* U, int64_t ldu, double* S, double* V, int64_t ldv, void* stream);
 
+/* thin_svd of X (rows x cols, rows <= cols) given Xt = X^T (cols x rows,
+ * ld ldxt) without transposing: the projected matrix of the two-pass SVDs
+ * (src/svd.py:137-143, src/power.py:143-156) arrives from the A pass as
+ * (Q^T A)^T = A^T Q.  Same outputs and sign convention as sp_thin_svd. */
+int sp_thin_svd_t(int64_t rows, int64_t cols, const double* Xt, int64_t ldxt,
+                  double* U, int64_t ldu, double* S, double* V, int64_t ldv, void* stream);
+
+/* X[:, j] /= d[j] (divide != 0, the `vt /= s_k` of direct_svd,
+ * src/svd.py:113) or X[:, j] *= d[j]. */
+int sp_scale_columns(int64_t rows, int64_t cols, double* X, int64_t ldx, const double* d,
+                     int32_t divide, void* stream);
+
+/* out[i, :] = X[idx[i], :] for i < k (X f64 or f32, widened to f64): the
+ * fine skeleton rows of the two-pass IDs (_gather_rows, src/rowid.py:82-95). */
+int sp_gather_rows(const void* X, int32_t x_dtype, int64_t ldx, int64_t cols,
+                   const int64_t* idx, int64_t k, double* out, int64_t ldo, void* stream);
+
 /* ---------------------------------------------------------------- K6 -----
  * pinv_apply (src/kernels.py:158-168): out = 1/s where s > tol * s[0], else 0. */
 int sp_pinv_apply(const double* s, int64_t count, double tol, double* out, void* stream);

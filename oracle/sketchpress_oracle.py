@@ -576,6 +576,112 @@ def spc_id(a, idx, w, k, r=None, block_rows=BLOCK, id_target="coarse",
 
 
 # ----------------------------------------------------------------------------
+# two-pass variants
+# ----------------------------------------------------------------------------
+
+def second_pass_project(a, z, block_rows=BLOCK):
+    """The `projected += basis[rows].T @ block` loop (src/svd.py:108-112,
+    135-140; src/power.py:149-154): Z^T A accumulated block by block."""
+    out = np.zeros((z.shape[1], a.shape[1]))
+    for lo, blk in _row_blocks(a, block_rows):
+        out += z[lo:lo + blk.shape[0]].T @ blk
+    return out
+
+
+def direct_svd(a, idx, w, k, p=None, block_rows=BLOCK):
+    """src/svd.py:80-113: SVD of the sketch, V by a pseudo-inverse pass."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    n_c = idx.shape[1]
+    _check_rank(k, n_c, a.shape[0])
+    if p is None:
+        p = n_c - k
+    if k + p != n_c:
+        raise OracleConfigError(f"sketch width {n_c} != k + p = {k + p}")
+    coarse, _ = one_pass_sketch(a, idx, w, block_rows)
+    u, s, _ = svd_thin(coarse)
+    if s[k - 1] <= TOL * s[0]:
+        raise OracleNumericalError(f"coarse matrix numerical rank {kept_rank(s)} is below target rank {k}")
+    vt = second_pass_project(a, u[:, :k], block_rows) / s[:k, None]
+    return OracleSVD(u[:, :k].copy(), s[:k].copy(), vt.T.copy(), k, "direct")
+
+
+def _svd_of_projected(basis, projected, k, method):
+    """src/svd.py:141-143 / src/power.py:115-121."""
+    u, s, v = svd_thin(projected)
+    if s.size < k:
+        raise OracleNumericalError(f"projected matrix supplies only {s.size} directions")
+    return OracleSVD(basis @ u[:, :k], s[:k].copy(), v[:, :k].copy(), k, method)
+
+
+def two_pass_svd(a, idx, w, k, block_rows=BLOCK):
+    """src/svd.py:116-143: QR basis of the sketch, projection in pass two."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    _check_rank(k, idx.shape[1], a.shape[0])
+    coarse, _ = one_pass_sketch(a, idx, w, block_rows)
+    s = np.linalg.svd(coarse, compute_uv=False)
+    achieved = int(np.count_nonzero(s > TOL * s[0])) if s[0] > 0 else 0
+    if achieved < k:
+        raise OracleNumericalError(f"coarse matrix numerical rank {achieved} is below target rank {k}")
+    basis, _ = qr_reduced(coarse)
+    return _svd_of_projected(basis, second_pass_project(a, basis, block_rows), k, "two_pass")
+
+
+def gather_fine_rows(a, indices):
+    """src/rowid.py:82-95 (_gather_rows): the rows, order of `indices` kept."""
+    return np.ascontiguousarray(a, dtype=np.float64)[np.asarray(indices)].copy()
+
+
+def two_pass_id(a, idx, w, k, block_rows=BLOCK):
+    """src/rowid.py:98-112: row ID of the sketch, fine skeleton in pass two."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if k > idx.shape[1]:
+        raise OracleConfigError(f"target rank k={k} exceeds sketch width n_c={idx.shape[1]}")
+    coarse, _ = one_pass_sketch(a, idx, w, block_rows)
+    picked = interp_rows(coarse, k)
+    return OracleID(picked.p, picked.indices, gather_fine_rows(a, picked.indices), None, None, "two_pass")
+
+
+def power_svd_two_pass(a, idx, w, cols, k, q=1, block_rows=BLOCK):
+    """src/power.py:227-249 with finalize_svd TWO_PASS (:143-156)."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    cols = np.asarray(cols, dtype=np.intp)
+    out_dim = idx.shape[1]
+    if k > out_dim:
+        raise OracleConfigError(f"target rank k={k} exceeds sketch width {out_dim}")
+    _check_cols(cols, k, out_dim, a.shape[1])
+    s0, c, _, _, _ = one_pass_power(a, idx, w, cols, block_rows, False, False)
+    qb, _ = enrich_basis(c, s0, q)
+    if k < 1 or k > qb.shape[1]:
+        raise OracleConfigError(f"target rank k={k} outside the enriched basis width")
+    return _svd_of_projected(qb, second_pass_project(a, qb, block_rows), k, "power")
+
+
+def power_id_two_pass(a, idx, w, cols, k, q=1, block_rows=BLOCK, project_ell=None, project_seed=0):
+    """src/power.py:252-308, two-pass mode: fine skeleton rows, method power_two_pass."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    cols = np.asarray(cols, dtype=np.intp)
+    n_c = idx.shape[1]
+    if k > n_c:
+        raise OracleConfigError(f"target rank k={k} exceeds sketch width n_c={n_c}")
+    _check_cols(cols, k, n_c, a.shape[1])
+    _, c, coarse, _, _ = one_pass_power(a, idx, w, cols, block_rows, True, False)
+    enriched = coarse.copy()
+    for _ in range(q):
+        enriched = c @ (c.T @ enriched)
+        _finite_iterate(enriched)
+    sel_in = enriched
+    if project_ell is not None:
+        if not 1 <= project_ell < n_c:
+            raise OracleConfigError(f"need 1 <= project_ell < n_c, got {project_ell}")
+        om = np.random.Generator(np.random.Philox(project_seed)).standard_normal((n_c, project_ell))
+        sel_in = enriched @ om
+    picked = interp_rows(sel_in, k)
+    out = OracleID(picked.p, picked.indices, gather_fine_rows(a, picked.indices), None, None, "power_two_pass")
+    out.pivot_gaps = pivot_gaps(sel_in.T, k)
+    return out
+
+
+# ----------------------------------------------------------------------------
 # metrics used by the parity gates (src/analysis.py:57-74)
 # ----------------------------------------------------------------------------
 

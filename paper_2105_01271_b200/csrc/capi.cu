@@ -92,6 +92,21 @@ int sp_thin_svd(int64_t rows, int64_t cols, const double* X, int64_t ldx, double
   return thin_svd(rows, cols, X, ldx, U, ldu, S, V, ldv, ST(stream));
 }
 
+int sp_thin_svd_t(int64_t rows, int64_t cols, const double* Xt, int64_t ldxt, double* U, int64_t ldu, double* S,
+                  double* V, int64_t ldv, void* stream) {
+  return thin_svd_t(rows, cols, Xt, ldxt, U, ldu, S, V, ldv, ST(stream));
+}
+
+int sp_scale_columns(int64_t rows, int64_t cols, double* X, int64_t ldx, const double* d, int32_t divide,
+                     void* stream) {
+  return scale_columns(rows, cols, X, ldx, d, divide != 0, ST(stream));
+}
+
+int sp_gather_rows(const void* X, int32_t x_dtype, int64_t ldx, int64_t cols, const int64_t* idx, int64_t k,
+                   double* out, int64_t ldo, void* stream) {
+  return gather_rows(X, x_dtype, ldx, cols, idx, k, out, ldo, ST(stream));
+}
+
 int sp_pinv_apply(const double* s, int64_t count, double tol, double* out, void* stream) {
   return pinv_apply(s, count, tol, out, ST(stream));
 }

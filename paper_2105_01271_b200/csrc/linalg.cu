@@ -118,6 +118,47 @@ int scale_cols(int64_t rows, int64_t cols, double* X, int64_t ldx, const double*
   return SP_OK;
 }
 
+__global__ void div_cols_kernel(int64_t rows, int64_t cols, double* X, int64_t ldx, const double* d) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * cols) return;
+  X[(e / cols) * ldx + (e % cols)] /= d[e % cols];
+}
+
+// X[:, j] /= d[j] (the vt /= s_k of direct_svd, src/svd.py:113) or *= d[j]
+int scale_columns(int64_t rows, int64_t cols, double* X, int64_t ldx, const double* d, bool divide, cudaStream_t s) {
+  if (rows == 0 || cols == 0) return SP_OK;
+  if (!divide) return scale_cols(rows, cols, X, ldx, d, s);
+  div_cols_kernel<<<ceil_div(rows * cols, 256), 256, 0, s>>>(rows, cols, X, ldx, d);
+  SPB_LAUNCHED();
+  return SP_OK;
+}
+
+// out[i, :] = X[idx[i], :] (k x cols, widened to f64): the fine skeleton rows
+// of the two-pass IDs (src/rowid.py:82-95)
+template <typename T>
+__global__ void gather_rows_any(const T* __restrict__ X, int64_t ldx, int64_t cols, const int64_t* __restrict__ idx,
+                                int64_t k, double* __restrict__ out, int64_t ldo) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= k * cols) return;
+  const int64_t i = e / cols, j = e % cols;
+  out[i * ldo + j] = (double)X[idx[i] * ldx + j];
+}
+
+int gather_rows(const void* X, int dtype, int64_t ldx, int64_t cols, const int64_t* idx, int64_t k, double* out,
+                int64_t ldo, cudaStream_t s) {
+  if (k == 0 || cols == 0) return SP_OK;
+  if (dtype == SP_F64)
+    gather_rows_any<double><<<ceil_div(k * cols, 256), 256, 0, s>>>((const double*)X, ldx, cols, idx, k, out, ldo);
+  else if (dtype == SP_F32)
+    gather_rows_any<float><<<ceil_div(k * cols, 256), 256, 0, s>>>((const float*)X, ldx, cols, idx, k, out, ldo);
+  else {
+    set_error("unknown dtype tag");
+    return SP_ECONFIG;
+  }
+  SPB_LAUNCHED();
+  return SP_OK;
+}
+
 __global__ void all_finite_kernel(int64_t rows, int64_t cols, const double* X, int64_t ldx, int* bad) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= rows * cols) return;
@@ -279,15 +320,33 @@ int thin_svd(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* U
     SPB_TRY(gemm(0, 0, rows, p, p, 1.0, Q, p, Us, p, 0.0, U, ldu, s));
     SPB_TRY(copy2d(p, p, Vs, p, V, ldv, s));
   } else {
-    // X^T = Q R  ->  X = R^T Q^T, R^T = Us S Vs^T  ->  U = Us, V = Q Vs
     SPB_ALLOC(ar, double, Xt, (size_t)cols * rows);
     SPB_TRY(transpose(rows, cols, X, ldx, Xt, rows, s));
-    SPB_TRY(tsqr(cols, rows, Xt, rows, Q, p, R, p, s));
-    SPB_TRY(transpose(p, p, R, p, Rt, p, s));
-    SPB_TRY(jacobi_svd(p, Rt, p, Us, p, S, Vs, p, s));
-    SPB_TRY(copy2d(p, p, Us, p, U, ldu, s));
-    SPB_TRY(gemm(0, 0, cols, p, p, 1.0, Q, p, Vs, p, 0.0, V, ldv, s));
+    return thin_svd_t(rows, cols, Xt, rows, U, ldu, S, V, ldv, s);
   }
+  SPB_TRY(sign_fix(rows, p, U, ldu, V, ldv, cols, false, s));
+  return SP_OK;
+}
+
+// thin_svd of X (rows x cols, rows <= cols) given Xt = X^T (cols x rows):
+// the wide branch without the transpose -- the projected matrix of the
+// two-pass SVDs arrives as (Q^T A)^T = A^T Q from the A pass.
+// X^T = Q R  ->  X = R^T Q^T, R^T = Us S Vs^T  ->  U = Us, V = Q Vs
+int thin_svd_t(int64_t rows, int64_t cols, const double* Xt, int64_t ldxt, double* U, int64_t ldu, double* S,
+               double* V, int64_t ldv, cudaStream_t s) {
+  SPB_REQUIRE(rows >= 1 && cols >= rows, "thin_svd_t needs 1 <= rows <= cols");
+  SPB_REQUIRE(rows <= 256, "thin_svd supports min(rows, cols) <= 256");
+  SPB_TRY(check_finite(cols, rows, Xt, ldxt, "SVD input contains non-finite entries", s));
+  const int64_t p = rows;
+  Arena ar(s);
+  SPB_ALLOC(ar, double, Q, (size_t)cols * p);
+  SPB_ALLOC(ar, double, R, (size_t)p * p);
+  SPB_ALLOC(ar, double, Rt, (size_t)p * p);
+  SPB_ALLOC(ar, double, Vs, (size_t)p * p);
+  SPB_TRY(tsqr(cols, rows, Xt, ldxt, Q, p, R, p, s));
+  SPB_TRY(transpose(p, p, R, p, Rt, p, s));
+  SPB_TRY(jacobi_svd(p, Rt, p, U, ldu, S, Vs, p, s));
+  SPB_TRY(gemm(0, 0, cols, p, p, 1.0, Q, p, Vs, p, 0.0, V, ldv, s));
   SPB_TRY(sign_fix(rows, p, U, ldu, V, ldv, cols, false, s));
   return SP_OK;
 }

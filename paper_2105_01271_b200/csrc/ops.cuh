@@ -61,6 +61,11 @@ int thin_qr(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q,
             double* R, int64_t ldr, cudaStream_t s);
 int thin_svd(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* U, int64_t ldu,
              double* S, double* V, int64_t ldv, cudaStream_t s);
+int thin_svd_t(int64_t rows, int64_t cols, const double* Xt, int64_t ldxt, double* U, int64_t ldu, double* S,
+               double* V, int64_t ldv, cudaStream_t s);
+int scale_columns(int64_t rows, int64_t cols, double* X, int64_t ldx, const double* d, bool divide, cudaStream_t s);
+int gather_rows(const void* X, int dtype, int64_t ldx, int64_t cols, const int64_t* idx, int64_t k, double* out,
+                int64_t ldo, cudaStream_t s);
 int pivoted_qr(int64_t rows, int64_t cols, const double* Mt, int64_t ldmt, int k, int64_t* perm,
                double* Q, int64_t ldq, double* R, int64_t ldr, cudaStream_t s);
 int frob_residual(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, const double* U,

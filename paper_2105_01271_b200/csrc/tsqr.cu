@@ -518,6 +518,9 @@ int tsqr(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, in
   Arena ar(s);
   SPB_ALLOC(ar, double, P, (size_t)rows * kQB);
   SPB_ALLOC(ar, double, T, (size_t)cols * kQB);
+  SPB_ALLOC(ar, double, S2, (size_t)cols * kQB);
+  SPB_ALLOC(ar, double, R2, (size_t)kQB * kQB);
+  SPB_ALLOC(ar, double, R3, (size_t)kQB * kQB);
   for (int64_t p0 = 0; p0 < cols; p0 += kQB) {
     const int w = (int)std::min<int64_t>(kQB, cols - p0);
     copy_block<<<ceil_div(rows * w, 256), 256, 0, s>>>(rows, w, X + p0, ldx, P, w);
@@ -533,7 +536,33 @@ int tsqr(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, in
         SPB_CHECK_LAUNCH();
       }
     }
-    SPB_TRY(tsqr32(rows, w, P, w, Q + p0, ldq, R + p0 * ldr + p0, ldr, s));
+    double* Qp = Q + p0;
+    double* Rp = R + p0 * ldr + p0;
+    SPB_TRY(tsqr32(rows, w, P, w, Qp, ldq, Rp, ldr, s));
+    if (p0 > 0) {
+      // A numerically rank-deficient panel leaves a residual P of rounding
+      // size whose components along Q[:, :p0] are as large as the rest, so
+      // orth(P) is not orthogonal to the previous panels: re-orthogonalise
+      // the NORMALISED panel (twice) and QR it again.
+      //   Qp = Q S + Q' R'  ->  R[:p0, panel] += S Rp,  R_panel = R' Rp
+      for (int pass = 0; pass < 2; ++pass) {
+        double* Sx = pass == 0 ? T : S2;
+        SPB_TRY(gemm(1, 0, p0, w, rows, 1.0, Q, ldq, Qp, ldq, 0.0, Sx, w, s));
+        SPB_TRY(gemm(0, 0, rows, w, p0, -1.0, Q, ldq, Sx, w, 1.0, Qp, ldq, s));
+      }
+      add_block<<<ceil_div(p0 * w, 256), 256, 0, s>>>(p0, w, S2, w, T, w);
+      count_launch();
+      SPB_CHECK_LAUNCH();
+      SPB_TRY(gemm(0, 0, p0, w, w, 1.0, T, w, Rp, ldr, 1.0, R + p0, ldr, s));
+      copy_block<<<ceil_div(rows * w, 256), 256, 0, s>>>(rows, w, Qp, ldq, P, w);
+      count_launch();
+      SPB_CHECK_LAUNCH();
+      SPB_TRY(tsqr32(rows, w, P, w, Qp, ldq, R2, w, s));
+      SPB_TRY(gemm(0, 0, w, w, w, 1.0, R2, w, Rp, ldr, 0.0, R3, w, s));
+      copy_block<<<ceil_div(w * w, 256), 256, 0, s>>>(w, w, R3, w, Rp, ldr);
+      count_launch();
+      SPB_CHECK_LAUNCH();
+    }
   }
   return SP_OK;
 }

@@ -26,7 +26,8 @@ from .kernels import RANK_TOL, thin_qr, thin_svd, pinv_apply
 from .rowid import FactoredLifting, RowIDFactors
 from .sketch import SketchOperator, _rng
 from .snapshot_io import DeviceSnapshotStream, SnapshotStream, stage_stream
-from .svd import DEFAULT_BLOCK_ROWS, LowRankSVD, _finish, _projected_s0, _sketch_on_ingest
+from .svd import (DEFAULT_BLOCK_ROWS, LowRankSVD, _finish, _projected_s0, _sketch_on_ingest, _svd_of_projected_t,
+                  second_pass_atz, second_pass_rows)
 
 SINGLE_PASS = "single_pass"
 TWO_PASS = "two_pass"
@@ -105,15 +106,15 @@ def _column_set_on_device(op: SketchOperator, cols: np.ndarray):
 
 def power_svd(stream: SnapshotStream, op: SketchOperator, k: int, cfg: PowerConfig,
               block_rows: int = DEFAULT_BLOCK_ROWS, return_device: bool = False) -> LowRankSVD:
-    """SPC-SVD with C-PWR enrichment (src/power.py:227-249), single-pass mode
-    on the GPU; two-pass mode is a SURVEY 8(f) 'next' item."""
+    """SPC-SVD with C-PWR enrichment (src/power.py:227-249): single-pass mode
+    as one device pipeline; two-pass mode as power_basis + a second A pass."""
     from .device import empty, ptr, stream_handle, to_device
     if k > op.out_dim:
         raise ConfigError(f"target rank k={k} exceeds sketch width {op.out_dim}")
     cols = cfg.column_set(stream.n)
     _validate_columns(cols, k, op.out_dim, stream.n)
     if cfg.mode != SINGLE_PASS:
-        raise NotImplementedError("two-pass finalize is a SURVEY 8(f) 'next' item")
+        return _power_svd_two_pass(stream, op, k, cfg, cols, block_rows, return_device)
     if cfg.q < 1:
         raise ConfigError("single-pass power pipeline needs q >= 1")
     d_cols, same = _column_set_on_device(op, cols)  # validates distinctness once per set
@@ -141,6 +142,25 @@ def power_svd(stream: SnapshotStream, op: SketchOperator, k: int, cfg: PowerConf
                    "enriched sketch is rank deficient; using regularized solve")
 
 
+def _power_svd_two_pass(stream, op, k, cfg, cols, block_rows, return_device):
+    """power_basis on the first pass's accumulators, projection in a second
+    pass (src/power.py:243-249 with finalize_svd TWO_PASS, :143-156)."""
+    d_cols, same = _column_set_on_device(op, cols)
+    if op.n != stream.n:
+        raise ConfigError(f"block width {stream.n} != fine dimension {op.n}")
+    s0c, c, on_block = _sketch_on_ingest(op, stream.m, cols, want_s0=not same, d_cols=d_cols)
+    staged = stage_stream(stream, block_rows, on_block)
+    s0 = c if same else _projected_s0(op, staged, s0c)
+    del staged
+    basis = power_basis(c, s0, cfg)
+    res = finalize_svd(basis, k, TWO_PASS, stream=stream, block_rows=block_rows, _device=True)
+    if return_device:
+        return res
+    from .device import to_host_many
+    u, s, v = to_host_many(res.u, res.s, res.v)
+    return LowRankSVD(u=u, s=s, v=v, k=k, method=res.method)
+
+
 def power_id(stream: SnapshotStream, op: SketchOperator, k: int, cfg: PowerConfig,
              r: int | None = None, block_rows: int = DEFAULT_BLOCK_ROWS,
              project_ell: int | None = None, project_seed: int = 0,
@@ -155,11 +175,38 @@ def power_id(stream: SnapshotStream, op: SketchOperator, k: int, cfg: PowerConfi
         raise ConfigError(f"target rank k={k} exceeds sketch width n_c={op.n_c}")
     cols = cfg.column_set(stream.n)
     _validate_columns(cols, k, op.n_c, stream.n)
-    if cfg.mode != SINGLE_PASS:
-        raise NotImplementedError("two-pass power_id is a SURVEY 8(f) 'next' item")
     _distinct(cols)
+    if cfg.mode != SINGLE_PASS:
+        return _power_id_two_pass(stream, op, k, cfg, cols, block_rows, project_ell, project_seed,
+                                  return_device)
     return _run_id(stream, op, k, cols, cfg.q, r, block_rows, project_ell, project_seed,
                    False, "power", return_device)
+
+
+def _power_id_two_pass(stream, op, k, cfg, cols, block_rows, project_ell, project_seed, return_device):
+    """Selection on the enriched sketch (C C^T)^q (A D), fine skeleton rows
+    gathered in a second pass (src/power.py:274-308, method power_two_pass)."""
+    from .device import to_device
+    from .rowid import _two_pass_factors, row_id
+    if op.idx is None:
+        raise ConfigError("the ID pipeline needs a stencil (deterministic) sketch")
+    s0c, c, on_block = _sketch_on_ingest(op, stream.m, cols if cfg.q > 0 else None)
+    staged = stage_stream(stream, block_rows, on_block)
+    del staged
+    enriched = s0c
+    for _ in range(cfg.q):
+        enriched = _mm(0, 0, c, _mm(1, 0, c, enriched))
+        _check_growth(enriched)
+    id_input = enriched
+    if project_ell is not None:
+        if not 1 <= project_ell < op.n_c:
+            raise ConfigError(f"need 1 <= project_ell < n_c, got {project_ell}")
+        omega = to_device(_rng(project_seed).standard_normal((op.n_c, project_ell)))
+        id_input = _mm(0, 0, enriched, omega)
+    picked = row_id(id_input, k)
+    stream.rewind()
+    skeleton = second_pass_rows(stream, picked.indices, block_rows)
+    return _two_pass_factors(picked, skeleton, "power_two_pass", return_device)
 
 
 def _run_id(stream, op, k, cols, q, r, block_rows, project_ell, project_seed, on_basis, method,
@@ -274,7 +321,8 @@ def power_basis(c, s0, cfg: PowerConfig) -> RangeBasis:
 
 
 def finalize_svd(basis: RangeBasis, k: int, mode: str, stream: SnapshotStream | None = None,
-                 hc=None, c=None, s0=None, block_rows: int = DEFAULT_BLOCK_ROWS) -> LowRankSVD:
+                 hc=None, c=None, s0=None, block_rows: int = DEFAULT_BLOCK_ROWS,
+                 _device: bool = False) -> LowRankSVD:
     """Turn the enriched basis into a rank-k SVD (src/power.py:124-181), literal
     algebra on the GPU."""
     from .device import to_host
@@ -289,10 +337,8 @@ def finalize_svd(basis: RangeBasis, k: int, mode: str, stream: SnapshotStream | 
         elif stream.cursor != 0:
             raise ConfigError("stream must be fresh or at end of pass")
         qb, host = _dev(basis.q_b)
-        staged = stage_stream(stream, block_rows)
-        a = staged.a if staged.a.dtype.itemsize == 8 else staged.a.double()
-        projected = _mm(1, 0, qb, a)
-        return _svd_from_projected(qb, projected, k, "power", host)
+        y = second_pass_atz(stream, qb, block_rows)  # projected^T = A^T Q_b
+        return _svd_of_projected_t(qb, y, k, "power", host and not _device)
     if mode != SINGLE_PASS:
         raise ConfigError(f"unknown finalize mode {mode!r}")
     if basis.reorth_used:

@@ -222,5 +222,22 @@ def single_pass_id(stream, op, k: int, r: int | None = None, block_rows: int = 2
     return out
 
 
-def two_pass_id(stream, op, k: int, block_rows: int = 256):
-    raise NotImplementedError("two_pass_id is a SURVEY 8(f) 'next' item; not in this build")
+def two_pass_id(stream, op, k: int, block_rows: int = 256, return_device: bool = False) -> RowIDFactors:
+    """Row selection on the sketch (pass one), fine skeleton gathered in pass
+    two (src/rowid.py:98-112)."""
+    from .svd import accumulate_sketch, second_pass_rows
+    if k > op.out_dim:
+        raise ConfigError(f"target rank k={k} exceeds sketch width n_c={op.out_dim}")
+    coarse, _ = accumulate_sketch(stream, op, block_rows, return_device=True)
+    picked = row_id(coarse, k)
+    stream.rewind()
+    skeleton = second_pass_rows(stream, picked.indices, block_rows)
+    return _two_pass_factors(picked, skeleton, "two_pass", return_device)
+
+
+def _two_pass_factors(picked, skeleton, method, return_device):
+    if return_device:
+        return RowIDFactors(p=picked.p, indices=picked.indices, skeleton=skeleton, method=method)
+    from .device import to_host_many
+    hp, hind, hskel = to_host_many(picked.p, picked.indices, skeleton)
+    return RowIDFactors(p=hp, indices=hind.astype(np.intp), skeleton=hskel, method=method)

@@ -16,9 +16,9 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .errors import ConfigError, RankDeficiencyWarning
+from .errors import ConfigError, NumericalError, RankDeficiencyWarning
 from .sketch import SketchOperator
-from .snapshot_io import SnapshotStream, stage_stream
+from .snapshot_io import DeviceSnapshotStream, SnapshotStream, stage_stream
 
 DEFAULT_BLOCK_ROWS = 256  # src/svd.py:28
 
@@ -153,11 +153,126 @@ def single_pass_svd(stream: SnapshotStream, op: SketchOperator, k: int,
                    "coarse sketch is rank deficient; using regularized triangular solve")
 
 
+# ------------------------------------------------------------ second pass ----
+
+def second_pass_atz(stream: SnapshotStream, z, block_rows: int = DEFAULT_BLOCK_ROWS):
+    """One more pass over the stream: Y = A^T Z (n x l) on the device -- the
+    ``projected += basis[rows].T @ block`` loops of the two-pass variants
+    (src/svd.py:108-112, 135-140; src/power.py:149-154) with the result kept
+    transposed.  A device-resident stream is one K2 call (TMA skinny pass for
+    l <= 16, DMMA otherwise); host streams accumulate block by block in stream
+    order on the DMMA GEMM (fixed order: reproducible)."""
+    from .device import empty, ptr, stream_handle, to_device
+    m, n, l = stream.m, stream.n, z.shape[1]
+    y = empty((n, l))
+    st = stream_handle()
+    if isinstance(stream, DeviceSnapshotStream):
+        a = stream.take_pass()
+        tag = _lib.SP_F64 if a.dtype.itemsize == 8 else _lib.SP_F32
+        _lib.call("sp_skinny_atz", ptr(a), tag, m, n, a.stride(0), ptr(z), l, l, ptr(y), l, st)
+        return y
+    row = 0
+    for blk in stream.blocks(block_rows):
+        b = to_device(np.ascontiguousarray(blk, dtype=np.float64))
+        rows = b.shape[0]
+        _lib.call("sp_gemm", 1, 0, n, l, rows, 1.0, ptr(b), n, ptr(z[row:row + rows]), l,
+                  0.0 if row == 0 else 1.0, ptr(y), l, st)
+        row += rows
+    return y
+
+
+def second_pass_rows(stream: SnapshotStream, indices, block_rows: int = DEFAULT_BLOCK_ROWS):
+    """One more pass collecting the fine rows A[indices] (k x n, f64, order of
+    ``indices`` kept): _gather_rows of src/rowid.py:82-95."""
+    from .device import empty, is_device_tensor, ptr, stream_handle, to_device, to_host
+    idx_h = to_host(indices) if is_device_tensor(indices) else np.asarray(indices)
+    idx_h = idx_h.astype(np.int64)
+    k, n = idx_h.size, stream.n
+    if isinstance(stream, DeviceSnapshotStream):
+        a = stream.take_pass()
+        tag = _lib.SP_F64 if a.dtype.itemsize == 8 else _lib.SP_F32
+        out = empty((k, n))
+        d_idx = indices if is_device_tensor(indices) else to_device(idx_h)
+        _lib.call("sp_gather_rows", ptr(a), tag, a.stride(0), n, ptr(d_idx), k, ptr(out), n, stream_handle())
+        return out
+    out_h = np.empty((k, n))
+    order = np.argsort(idx_h, kind="stable")
+    row = pos = 0
+    for blk in stream.blocks(block_rows):
+        hi = row + blk.shape[0]
+        while pos < order.size and idx_h[order[pos]] < hi:
+            out_h[order[pos]] = blk[idx_h[order[pos]] - row]
+            pos += 1
+        row = hi
+    return to_device(out_h)
+
+
+def _svd_of_projected_t(basis, y, k, method, host, v_orthonormal=True):
+    """Rank-k SVD of projected = Y^T (l x n) and U = basis @ u_k
+    (src/svd.py:141-143, src/power.py:115-121)."""
+    from .device import empty, ptr, stream_handle, to_host_many
+    n, l = y.shape
+    st = stream_handle()
+    if l > n:  # narrow stream: the ordinary thin SVD of the (tall) projected matrix
+        from .kernels import thin_svd
+        fac = thin_svd(y.t().contiguous())
+        uu, ss, vv = fac.u, fac.s, fac.v
+    else:
+        uu, ss, vv = empty((l, l)), empty((l,)), empty((n, l))
+        _lib.call("sp_thin_svd_t", l, n, ptr(y), l, ptr(uu), l, ptr(ss), ptr(vv), l, st)
+    if ss.shape[0] < k:
+        raise NumericalError(f"projected matrix supplies only {ss.shape[0]} directions")
+    uk = uu[:, :k].contiguous()
+    u = empty((basis.shape[0], k))
+    _lib.call("sp_gemm", 0, 0, basis.shape[0], k, basis.shape[1], 1.0, ptr(basis), basis.shape[1], ptr(uk), k,
+              0.0, ptr(u), k, st)
+    s = ss[:k].clone()
+    v = vv[:, :k].contiguous()
+    if host:
+        u, s, v = to_host_many(u, s, v)
+    return LowRankSVD(u=u, s=s, v=v, k=k, method=method, v_orthonormal=v_orthonormal)
+
+
 def two_pass_svd(stream: SnapshotStream, op: SketchOperator, k: int,
-                 block_rows: int = DEFAULT_BLOCK_ROWS):
-    raise NotImplementedError("two_pass_svd is a SURVEY 8(f) 'next' item; not in this build")
+                 block_rows: int = DEFAULT_BLOCK_ROWS, return_device: bool = False) -> LowRankSVD:
+    """Range basis from the sketch, projection in a second pass
+    (src/svd.py:116-143): QR of the coarse sketch (K4), Y = A^T Q (K2 /
+    DMMA), SVD of the projected matrix without transposing it (K4 + K5)."""
+    from .device import to_host
+    from .kernels import RANK_TOL, thin_qr, thin_svd
+    _validate_rank(k, op, stream)
+    coarse, _ = accumulate_sketch(stream, op, block_rows, return_device=True)
+    s_coarse = to_host(thin_svd(coarse).s)
+    achieved = int(np.count_nonzero(s_coarse > RANK_TOL * s_coarse[0])) if s_coarse[0] > 0 else 0
+    if achieved < k:
+        raise NumericalError(f"coarse matrix numerical rank {achieved} is below target rank {k}")
+    basis = thin_qr(coarse).q
+    stream.rewind()
+    y = second_pass_atz(stream, basis, block_rows)
+    return _svd_of_projected_t(basis, y, k, "two_pass", not return_device)
 
 
 def direct_svd(stream: SnapshotStream, op: SketchOperator, k: int, p=None,
-               block_rows: int = DEFAULT_BLOCK_ROWS):
-    raise NotImplementedError("direct_svd is a SURVEY 8(f) 'next' item; not in this build")
+               block_rows: int = DEFAULT_BLOCK_ROWS, return_device: bool = False) -> LowRankSVD:
+    """SVD of the sketch, right factors by a pseudo-inverse second pass
+    (src/svd.py:80-113): V = (A^T U_k) / s_k, not orthonormal."""
+    from .device import ptr, stream_handle, to_host, to_host_many
+    from .kernels import RANK_TOL, thin_svd
+    _validate_rank(k, op, stream)
+    if p is None:
+        p = op.out_dim - k
+    if k + p != op.out_dim:
+        raise ConfigError(f"sketch width {op.out_dim} != k + p = {k + p}")
+    coarse, _ = accumulate_sketch(stream, op, block_rows, return_device=True)
+    fac = thin_svd(coarse)
+    s_h = to_host(fac.s)
+    if s_h[k - 1] <= RANK_TOL * s_h[0]:
+        raise NumericalError(f"coarse matrix numerical rank {fac.rank()} is below target rank {k}")
+    u_k = fac.u[:, :k].contiguous()
+    s_k = fac.s[:k].clone()
+    stream.rewind()
+    v = second_pass_atz(stream, u_k, block_rows)
+    _lib.call("sp_scale_columns", stream.n, k, ptr(v), k, ptr(s_k), 1, stream_handle())
+    if not return_device:
+        u_k, s_k, v = to_host_many(u_k, s_k, v)
+    return LowRankSVD(u=u_k, s=s_k, v=v, k=k, method="direct", v_orthonormal=False)

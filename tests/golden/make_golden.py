@@ -167,7 +167,46 @@ def small_cases(out):
     print("small", sorted(rec))
 
 
+def twopass_cases(out):
+    """The two-pass variants: direct_svd, two_pass_svd,
+    two_pass_id, power_svd / power_id in mode two_pass."""
+    rec = {}
+    # cfg1 field (the reference's CPU-runnable config), stride-4 grid
+    cfg = CONFIGS["cfg1"]
+    a = generate_host(cfg)
+    idx = coarse_grid_indices(cfg.grid, cfg.stride)
+    op = grid_op(cfg.n, idx)
+    r = sp.two_pass_svd(sp.ArraySnapshotStream(a), op, 8)
+    rec.update(tp_s=r.s, tp_u=r.u, tp_v=r.v)
+    r = sp.direct_svd(sp.ArraySnapshotStream(a), op, 8, p=idx.size - 8)
+    rec.update(dr_s=r.s, dr_u=r.u, dr_v=r.v)
+    f = sp.two_pass_id(sp.ArraySnapshotStream(a), op, 10)
+    rec.update(tpid_idx=f.indices, tpid_p=f.p, tpid_skel=f.skeleton)
+    pc = sp.PowerConfig(q=1, columns=idx, mode="two_pass")
+    r = sp.power_svd(sp.ArraySnapshotStream(a), op, 8, pc)
+    rec.update(pwtp_s=r.s, pwtp_u=r.u, pwtp_v=r.v)
+    f = sp.power_id(sp.ArraySnapshotStream(a), op, 10, pc)
+    rec.update(pidtp_idx=f.indices, pidtp_p=f.p, pidtp_skel=f.skeleton)
+    # random full-rank problems with 1-D injection sketches
+    a = philox(33).standard_normal((60, 150))
+    op1 = sp.build_sketch(sp.SketchSpec("injection", 150, 12))
+    r = sp.two_pass_svd(sp.ArraySnapshotStream(a), op1, 6)
+    rec.update(rtp_s=r.s, rtp_u=r.u, rtp_v=r.v)
+    r = sp.direct_svd(sp.ArraySnapshotStream(a), op1, 6)
+    rec.update(rdr_s=r.s, rdr_u=r.u, rdr_v=r.v)
+    r = sp.power_svd(sp.ArraySnapshotStream(a), op1, 5, sp.PowerConfig(q=0, stride=6, mode="two_pass"))
+    rec.update(rpw0_s=r.s, rpw0_u=r.u, rpw0_v=r.v)
+    f = sp.two_pass_id(sp.ArraySnapshotStream(a), op1, 7)
+    rec.update(rtpid_idx=f.indices, rtpid_p=f.p)
+    np.savez_compressed(out / "twopass_cases.npz", **rec)
+    print("twopass", sorted(rec))
+
+
 if __name__ == "__main__":
     with threadpool_limits(1):
-        small_cases(HERE)
-        field_cases(HERE)
+        if len(sys.argv) > 1 and sys.argv[1] == "twopass":
+            twopass_cases(HERE)
+        else:
+            small_cases(HERE)
+            field_cases(HERE)
+            twopass_cases(HERE)

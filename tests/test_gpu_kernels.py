@@ -162,7 +162,8 @@ def test_cholqr2_breakdown_falls_back(cuda):
     assert np.linalg.norm(q @ r - x) <= 1e-13 * np.linalg.norm(x)
 
 
-@pytest.mark.parametrize("rows,cols,rank", [(4096, 32, 9), (2000, 32, 1), (65536, 7, 3), (300, 20, 0)])
+@pytest.mark.parametrize("rows,cols,rank", [(4096, 32, 9), (2000, 32, 1), (65536, 7, 3), (300, 20, 0),
+                                            (1000, 256, 10), (4096, 100, 3)])
 def test_tsqr32_rank_deficient(cuda, rows, cols, rank):
     x = rank_deficient(philox(rows + rank), rows, cols, rank) if rank else np.zeros((rows, cols))
     if rank:

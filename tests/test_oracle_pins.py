@@ -149,3 +149,55 @@ def test_projector_target_equals_reference_in_exact_rank_case():
     u, s, v, r = oracle.projector_target_svd(a, a[:, idx], 5, 1)
     assert r == 5
     assert oracle.rel_frob(a, (u * s) @ v.T) <= 1e-12
+
+
+def _same_up_to_sign(x, y, atol):
+    """Columns equal up to a per-column sign flip."""
+    sgn = np.sign(np.sum(x * y, axis=0))
+    sgn[sgn == 0] = 1.0
+    np.testing.assert_allclose(x * sgn, y, rtol=0, atol=atol)
+
+
+def test_oracle_two_pass_variants_match_reference():
+    """direct_svd, two_pass_svd, two_pass_id and the
+    two-pass power modes, oracle vs the reference's own outputs."""
+    g = load_golden("twopass_cases.npz")
+    cfg = CONFIGS["cfg1"]
+    a = generate_host(cfg)
+    idx = oracle.grid_coarse_indices(cfg.grid, cfg.stride)
+    tab, w = idx[None, :], _ones(idx)
+    r = oracle.two_pass_svd(a, tab, w, 8)
+    np.testing.assert_allclose(r.s, g["tp_s"], rtol=1e-13)
+    _same_up_to_sign(r.u, g["tp_u"], 1e-10)
+    _same_up_to_sign(r.v, g["tp_v"], 1e-10)
+    r = oracle.direct_svd(a, tab, w, 8, p=idx.size - 8)
+    np.testing.assert_allclose(r.s, g["dr_s"], rtol=1e-13)
+    _same_up_to_sign(r.u, g["dr_u"], 1e-10)
+    _same_up_to_sign(r.v, g["dr_v"], 1e-10 * np.abs(g["dr_v"]).max())
+    f = oracle.two_pass_id(a, tab, w, 10)
+    assert np.array_equal(f.indices, g["tpid_idx"])
+    np.testing.assert_allclose(f.p, g["tpid_p"], rtol=0, atol=1e-10)
+    assert np.array_equal(f.skeleton, g["tpid_skel"])  # fine rows: exact copies
+    r = oracle.power_svd_two_pass(a, tab, w, idx, 8, q=1)
+    np.testing.assert_allclose(r.s, g["pwtp_s"], rtol=1e-12)
+    _same_up_to_sign(r.u, g["pwtp_u"], 1e-8)
+    f = oracle.power_id_two_pass(a, tab, w, idx, 10, q=1)
+    assert np.array_equal(f.indices, g["pidtp_idx"])
+    assert np.array_equal(f.skeleton, g["pidtp_skel"])
+    # random full-rank problems, 1-D injection sketch (n=150, n_c=12)
+    a = philox(33).standard_normal((60, 150))
+    t1 = oracle.stencil_tables("injection", 150, 12)
+    tab1, w1 = t1[0], t1[1]
+    r = oracle.two_pass_svd(a, tab1, w1, 6)
+    np.testing.assert_allclose(r.s, g["rtp_s"], rtol=1e-13)
+    _same_up_to_sign(r.u, g["rtp_u"], 1e-11)
+    r = oracle.direct_svd(a, tab1, w1, 6)
+    np.testing.assert_allclose(r.s, g["rdr_s"], rtol=1e-13)
+    _same_up_to_sign(r.v, g["rdr_v"], 1e-11 * np.abs(g["rdr_v"]).max())
+    cols = np.arange(0, 150, 6)
+    r = oracle.power_svd_two_pass(a, tab1, w1, cols, 5, q=0)
+    np.testing.assert_allclose(r.s, g["rpw0_s"], rtol=1e-13)
+    _same_up_to_sign(r.v, g["rpw0_v"], 1e-11)
+    f = oracle.two_pass_id(a, tab1, w1, 7)
+    assert np.array_equal(f.indices, g["rtpid_idx"])
+    np.testing.assert_allclose(f.p, g["rtpid_p"], rtol=0, atol=1e-11)
