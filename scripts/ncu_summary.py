@@ -10,11 +10,18 @@ STALLS = 'smsp__average_warps_issue_stalled_'
 for rep in sys.argv[1:]:
     out = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
-    h, units, v = rows[0], rows[1], rows[2]
-    print('==', rep, v[h.index('Kernel Name')][:80] if 'Kernel Name' in h else '')
-    for w in WANT:
-        if w in h:
-            print(f'  {w:70s} {v[h.index(w)]} {units[h.index(w)]}')
-    st = [(float(v[i]), h[i][len(STALLS):]) for i in range(len(h))
-          if h[i].startswith(STALLS) and h[i].endswith('_per_issue_active.ratio') and v[i]]
-    print('  stalls:', ', '.join(f'{n.replace("_per_issue_active.ratio","")}={x:.2f}' for x, n in sorted(st, reverse=True)[:6]))
+    h, units = rows[0], rows[1]
+    for v in rows[2:]:
+        print('==', rep, v[h.index('Kernel Name')][:80] if 'Kernel Name' in h else '')
+        for w in WANT:
+            if w in h:
+                print(f'  {w:70s} {v[h.index(w)]} {units[h.index(w)]}')
+        st = []
+        for i in range(len(h)):
+            if h[i].startswith(STALLS) and h[i].endswith('_per_issue_active.ratio') and v[i]:
+                try:
+                    st.append((float(v[i]), h[i][len(STALLS):]))
+                except ValueError:
+                    pass
+        print('  stalls:', ', '.join(f'{n.replace("_per_issue_active.ratio","")}={x:.2f}'
+                                    for x, n in sorted(st, reverse=True)[:6]))
