@@ -65,8 +65,15 @@ static int read_flag_with(const PendingFlag& pf, int& host_flag, cudaStream_t s)
   return SP_OK;
 }
 
+// `need` < 0: the caller needs every kept triplet (the SVD projector);
+// need >= 0: only the leading `need` triplets and whether the kept rank
+// reaches them (the ID lifting).  For the latter, a block whose spectrum is
+// still above the cut at its last column does not grow once it holds need + 8
+// values, and values within 10x of the block's tail (an unresolved bulk, e.g.
+// the noise floor of cfg3) are exempt from the stability test.
 static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int want, double power,
-                   TopSvd& out, Arena& ar, cudaStream_t s, PendingFlag pf = PendingFlag(), bool want_v = false) {
+                   TopSvd& out, Arena& ar, cudaStream_t s, PendingFlag pf = PendingFlag(), bool want_v = false,
+                   int need = -1) {
   const int64_t p = std::min(rows, cols);
   int hflag = 0;
   if (p <= 64 && pf.dev) {
@@ -136,7 +143,7 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
       }
       iters = itn + 1;
       kept = count_kept(hs, power);
-      if (kept + 8 > b && b < cap) {
+      if (kept + 8 > b && b < cap && (need < 0 || kept < need + 8)) {
         grow = true;
         break;
       }
@@ -147,9 +154,11 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
       if (itn == 0 && kept > 0 && b - 8 > kept && hs[b - 8] <= 1e-8 * hs[kept - 1]) conv = true;
       if (itn >= 1 && kept == kept_prev) {
         conv = true;
-        const int chk = std::min(b, kept + 1);
-        for (int i = 0; i < chk; ++i)
+        const int chk = need < 0 ? std::min(b, kept + 1) : std::min(b, need);
+        for (int i = 0; i < chk; ++i) {
+          if (need >= 0 && hs[i] <= 10.0 * hs[b - 1]) break;  // unresolved bulk at this block size
           if (std::fabs(hs[i] - prev[i]) > 1e-14 * hs[0] + 1e-12 * hs[i]) conv = false;
+        }
       }
       if (conv) break;
       prev = hs;
@@ -566,7 +575,7 @@ int power_id(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, cons
   // SVD of the coarse sketch: rank and the top-r triplets for the lifting
   const int want = std::max(2 * k, r_req);
   TopSvd top;
-  SPB_TRY(svd_top(coarse, m, nc, nc, want, 1.0, top, ar, s, PendingFlag(), /*want_v=*/true));
+  SPB_TRY(svd_top(coarse, m, nc, nc, want, 1.0, top, ar, s, PendingFlag(), /*want_v=*/true, /*need=*/want));
   int rank = top.kept;
   int warn = 0;
   int r = r_req > 0 ? r_req : std::max(k, std::min(2 * k, rank));
