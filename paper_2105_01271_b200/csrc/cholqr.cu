@@ -207,11 +207,15 @@ chol_small_kernel(int c, int nb, const double* __restrict__ P, double* __restric
 // Q1 rows = X rows R^{-1} (c x c) and partial[blk] = Q1_blk^T Q1_blk; one
 // thread per row (c <= 32), rows staged through shared memory.
 constexpr int kMgRows = 128;
-constexpr int kMgTiles = 2;  // row tiles per CTA (fewer Gram partials)
+// row tiles per CTA: at least 2, and enough that the partial count stays <= 2048
+__host__ __device__ inline int mg_tiles(int64_t rows) {
+  const int64_t t = (rows + (int64_t)128 * 2048 - 1) / ((int64_t)128 * 2048);
+  return (int)(t < 2 ? 2 : t);
+}
 
 __global__ void __launch_bounds__(kMgRows)
 mul_gram_kernel(int64_t rows, int c, const double* __restrict__ X, int64_t ldx, const double* __restrict__ Ri,
-                double* __restrict__ Q, int64_t ldq, double* __restrict__ partial) {
+                double* __restrict__ Q, int64_t ldq, double* __restrict__ partial, int kMgTiles) {
   __shared__ double ms[32][32];
   __shared__ double ts[kMgRows][33];
   const int t = threadIdx.x;
@@ -277,7 +281,8 @@ mul_gram_kernel(int64_t rows, int c, const double* __restrict__ X, int64_t ldx, 
 static int cholqr2_small(int64_t rows, int c, const double* X, int64_t ldx, double* Q, int64_t ldq, double* R,
                          int64_t ldr, int* dflag, cudaStream_t s) {
   Arena ar(s);
-  const int nb1 = (int)std::min<int64_t>(kNumSMs, ceil_div(rows, 128));
+  const int nb1 = (int)std::min<int64_t>(4 * kNumSMs, ceil_div(rows, 128));
+  const int kMgTiles = mg_tiles(rows);
   const int nb2 = ceil_div(rows, (int64_t)kMgRows * kMgTiles);
   SPB_ALLOC(ar, double, P1, (size_t)nb1 * c * c);
   SPB_ALLOC(ar, double, P2, (size_t)nb2 * c * c);
@@ -291,7 +296,7 @@ static int cholqr2_small(int64_t rows, int c, const double* X, int64_t ldx, doub
   chol_small_kernel<<<1, kCsThreads, 0, s>>>(c, nb, P1, R1, R1i, nullptr, nullptr, 0, dflag);
   count_launch();
   SPB_CHECK_LAUNCH();
-  mul_gram_kernel<<<nb2, kMgRows, 0, s>>>(rows, c, X, ldx, R1i, Q1, c, P2);
+  mul_gram_kernel<<<nb2, kMgRows, 0, s>>>(rows, c, X, ldx, R1i, Q1, c, P2, kMgTiles);
   count_launch();
   SPB_CHECK_LAUNCH();
   chol_small_kernel<<<1, kCsThreads, 0, s>>>(c, nb2, P2, R2, R2i, R1, R, ldr, dflag);

@@ -125,7 +125,7 @@ int householder_complete(int64_t N, int r, int k, double* out, int64_t ldo, cuda
   }
   Arena ar(s);
   SPB_ALLOC(ar, double, Kp, (size_t)r * kr);
-  if (kr <= 64) {
+  if (r * kr <= 64 * 64 && kr <= 256) {
     // out[:, r:k] = E' - Q K' in one streaming pass (E' added on the top k rows)
     SPB_ALLOC(ar, double, Et, (size_t)k * kr);
     hh_complete_kernel<<<1, 256, 0, s>>>(r, k, out, ldo, kp_out ? kp_out : Kp, Et, kr);

@@ -152,7 +152,15 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
       // (sigma_{b+1}/sigma_kept)^2 when the spectrum has fallen to the
       // rounding floor inside the block (oversampling 8): accept it.
       if (itn == 0 && kept > 0 && b - 8 > kept && hs[b - 8] <= 1e-8 * hs[kept - 1]) conv = true;
-      if (itn >= 1 && kept == kept_prev) {
+      // A priori: after itn + 1 Rayleigh-Ritz steps the kept Ritz values are
+      // accurate to ~(sigma_{b-7} / sigma_kept)^(2 itn + 2) (oversampling 8;
+      // hs[b-8] >= sigma_{b+1} makes the estimate conservative).  E.g. an
+      // FP32-stored A floors the sketch spectrum at ~1e-7 sigma_1, so the
+      // ratio is ~1e-4 and two steps reach 1e-16 without a third to confirm.
+      if (itn >= 1 && kept == kept_prev && kept > 0 && b - 8 > kept &&
+          std::pow(hs[b - 8] / hs[kept - 1], 2.0 * itn + 2.0) <= 1e-16)
+        conv = true;
+      if (!conv && itn >= 1 && kept == kept_prev) {
         conv = true;
         const int chk = need < 0 ? std::min(b, kept + 1) : std::min(b, need);
         for (int i = 0; i < chk; ++i) {

@@ -39,8 +39,7 @@ tall_gram_kernel(int64_t rows, int c, const double* __restrict__ X, int64_t ldx,
                  const double* __restrict__ Y, int64_t ldy, int64_t rows_per_cta, double* __restrict__ partial) {
   extern __shared__ double tg_smem[];
   const int cp = round_up_dev(c, MT) + 1, dp = round_up_dev(d, MT) + 1;
-  double* xs = tg_smem;
-  double* ys = tg_smem + kTgTile * cp;
+  const int stage = kTgTile * (cp + dp);  // doubles per pipeline stage
   const int nmc = (c + MT - 1) / MT, nmd = (d + MT - 1) / MT, nmicro = nmc * nmd;
   const int G = kTgThreads / nmicro;
   const int mt = threadIdx.x % nmicro, rg = threadIdx.x / nmicro;
@@ -48,18 +47,33 @@ tall_gram_kernel(int64_t rows, int c, const double* __restrict__ X, int64_t ldx,
   const int i0 = (mt / nmd) * MT, j0 = (mt % nmd) * MT;
   const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
   const int64_t r1 = imin64(rows, r0 + rows_per_cta);
+  const int ntile = (int)((r1 - r0 + kTgTile - 1) / kTgTile);
   double acc[MT][MT];
 #pragma unroll
   for (int u = 0; u < MT; ++u)
 #pragma unroll
     for (int v = 0; v < MT; ++v) acc[u][v] = 0.0;
-  for (int64_t base = r0; base < r1; base += kTgTile) {
+  auto issue = [&](int t) {
+    const int64_t base = r0 + (int64_t)t * kTgTile;
     const int nr = (int)imin64(kTgTile, r1 - base);
-    __syncthreads();
+    double* xs = tg_smem + (t & 1) * stage;
     stage_rows(xs, cp, kTgTile, X, ldx, base, nr, c);
-    stage_rows(ys, dp, kTgTile, Y, ldy, base, nr, d);
-    cp_async_wait_all();
+    stage_rows(xs + kTgTile * cp, dp, kTgTile, Y, ldy, base, nr, d);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  // two-stage cp.async pipeline over the CTA's row tiles
+  if (ntile > 0) issue(0);
+  for (int t = 0; t < ntile; ++t) {
+    if (t + 1 < ntile) {
+      issue(t + 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
     __syncthreads();
+    const double* xs = tg_smem + (t & 1) * stage;
+    const double* ys = xs + kTgTile * cp;
+    const int nr = (int)imin64(kTgTile, r1 - (r0 + (int64_t)t * kTgTile));
     if (active) {
       for (int rr = rg; rr < nr; rr += G) {
         double xv[MT], yv[MT];
@@ -74,9 +88,9 @@ tall_gram_kernel(int64_t rows, int c, const double* __restrict__ X, int64_t ldx,
           for (int v = 0; v < MT; ++v) acc[u][v] = fma(xv[u], yv[v], acc[u][v]);
       }
     }
+    __syncthreads();  // stage (t & 1) is refilled by issue(t + 2)
   }
   // row-group partials -> shared (reusing the tiles), fixed-order sum
-  __syncthreads();
   double* red = tg_smem;  // [G][nmicro][MT*MT]
   if (active) {
 #pragma unroll
@@ -99,11 +113,11 @@ template <int MT>
 static int launch_tall_gram(int nb, int64_t rows, int c, const double* X, int64_t ldx, int d, const double* Y,
                             int64_t ldy, int64_t rpc, double* part, cudaStream_t s) {
   const int cp = (c + MT - 1) / MT * MT + 1, dp = (d + MT - 1) / MT * MT + 1;
-  const size_t tile = (size_t)kTgTile * (cp + dp), red = (size_t)kTgThreads * MT * MT;
+  const size_t tile = (size_t)2 * kTgTile * (cp + dp), red = (size_t)kTgThreads * MT * MT;
   const size_t smem = (tile > red ? tile : red) * sizeof(double);
   static bool attr = false;
   if (!attr) {
-    SPB_CUDA(cudaFuncSetAttribute(tall_gram_kernel<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+    SPB_CUDA(cudaFuncSetAttribute(tall_gram_kernel<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
     attr = true;
   }
   tall_gram_kernel<MT><<<nb, kTgThreads, smem, s>>>(rows, c, X, ldx, d, Y, ldy, rpc, part);
@@ -129,7 +143,7 @@ int tall_gram(int64_t rows, int c, const double* X, int64_t ldx, int d, const do
               double alpha, double beta, double* G, int64_t ldg, cudaStream_t s) {
   SPB_REQUIRE(c >= 1 && d >= 1 && c <= kTallMax && d <= kTallMax, "tall_gram supports widths <= 64");
   SPB_REQUIRE(rows >= 1, "tall_gram needs rows >= 1");
-  int nb = (int)std::min<int64_t>(kNumSMs, ceil_div(rows, 2 * kTgTile));
+  int nb = (int)std::min<int64_t>(4 * kNumSMs, ceil_div(rows, 2 * kTgTile));
   const int64_t rpc = ceil_div(ceil_div(rows, nb), kTgTile) * (int64_t)kTgTile;
   nb = (int)ceil_div(rows, rpc);
   Arena ar(s);
@@ -141,7 +155,7 @@ int tall_gram(int64_t rows, int c, const double* X, int64_t ldx, int d, const do
   return split_reduce(part, nb, c, d, alpha, beta, G, ldg, s);
 }
 
-// O = alpha X M + beta O.  A CTA owns R = min(128, 1024 / d) consecutive rows
+// O = alpha X M + beta O.  A CTA owns R = min(512, 2048 / d) consecutive rows
 // and each thread forms output elements t, t + 256, ... of that row-major
 // R x d block, so loads and stores are coalesced whatever d is; the rows of X
 // and all of M are staged in shared memory (cp.async).  Each output row
@@ -201,14 +215,15 @@ tall_mul_kernel(int64_t rows, int c, const double* X, int64_t ldx, int d, const 
 int tall_mul(int64_t rows, int c, const double* X, int64_t ldx, int d, const double* M, int64_t ldm, double alpha,
              double beta, double* O, int64_t ldo, cudaStream_t s, const double* top, int64_t ldt,
              int64_t top_rows) {
-  SPB_REQUIRE(c >= 1 && d >= 1 && c <= kTallMax && d <= kTallMax, "tall_mul supports widths <= 64");
+  SPB_REQUIRE(c >= 1 && d >= 1 && c <= kTallMax && d <= 4 * kTallMax && c * d <= 64 * 64,
+              "tall_mul supports c <= 64, d <= 256, c * d <= 4096");
   if (rows == 0) return SP_OK;
   static bool attr = false;
   if (!attr) {
     SPB_CUDA(cudaFuncSetAttribute(tall_mul_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
     attr = true;
   }
-  const int rpc = std::max(1, std::min(128, 1024 / d));
+  const int rpc = std::max(1, std::min(512, 2048 / d));
   const size_t smem = ((size_t)c * d + (size_t)rpc * (c + 1)) * sizeof(double);
   tall_mul_kernel<<<ceil_div(rows, rpc), kTmThreads, smem, s>>>(rows, c, X, ldx, d, M, ldm, alpha, beta, O, ldo,
                                                                 top, ldt, top ? top_rows : 0, rpc);

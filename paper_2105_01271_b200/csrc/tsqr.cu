@@ -447,7 +447,10 @@ static int tsqr32(int64_t rows, int cols, const double* X, int64_t ldx, double* 
   while (true) {
     Level L;
     L.rows = r;
-    L.cl = (int)std::min<int64_t>(mc, ceil_div(r, kQCH));
+    // clusters only while all chunks fit in one wave: past ~148 CTAs the
+    // per-step cluster exchange costs more than the extra tree level it saves
+    const int64_t ctas = ceil_div(r, kQCH);
+    L.cl = ctas <= kNumSMs ? (int)std::min<int64_t>(mc, ctas) : 1;
     L.nch = (int)ceil_div(r, (int64_t)L.cl * kQCH);
     L.V = ar.alloc<double>((size_t)r * kQB);
     L.T = ar.alloc<double>((size_t)L.nch * kQB * kQB);

@@ -297,3 +297,19 @@ def test_row_id_golden(cuda):
     h = sp.row_id(np.array([[1.0, 2.0], [2.0, 4.0]]), 1)
     np.testing.assert_array_equal(h.indices, [1])
     np.testing.assert_allclose(h.p, [[0.5], [1.0]])
+
+
+@pytest.mark.parametrize("N,r,k", [(2000, 7, 50), (65536, 7, 50), (5000, 5, 200), (300, 1, 64),
+                                   (1000, 20, 220), (500, 32, 96)])
+def test_householder_complete(cuda, N, r, k):
+    """Columns [r, k) become an orthonormal completion of the orthonormal
+    columns [0, r) (Householder reconstruction, sp_householder_complete)."""
+    q, _ = np.linalg.qr(philox(N + r + k).standard_normal((N, r)))
+    out = np.zeros((N, k))
+    out[:, :r] = q
+    d = _dev(out, cuda)
+    kp = cuda.empty((r, k - r), dtype=cuda.float64, device="cuda")
+    _lib.call("sp_householder_complete", N, r, k, d.data_ptr(), k, kp.data_ptr(), _stream(cuda))
+    o = d.cpu().numpy()
+    np.testing.assert_array_equal(o[:, :r], q)  # untouched
+    np.testing.assert_allclose(o.T @ o, np.eye(k), atol=1e-13)
