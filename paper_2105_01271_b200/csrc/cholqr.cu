@@ -228,9 +228,9 @@ mul_gram_kernel(int64_t rows, int c, const double* __restrict__ X, int64_t ldx, 
     const int64_t base = ((int64_t)blockIdx.x * kMgTiles + tile) * kMgRows;
     if (base >= rows) break;  // uniform
     const int nr = (int)imin64(kMgRows, rows - base);
-    for (int e = t; e < nr * c; e += kMgRows) {
-      const int rr = e / c, cc = e - (e / c) * c;
-      cp_async_f64(&ts[rr][cc], X + (base + rr) * ldx + cc, true);
+    if (t < nr) {  // thread per row: no division in the staging loop
+      const double* src = X + (base + t) * ldx;
+      for (int cc = 0; cc < c; ++cc) cp_async_f64(&ts[t][cc], src + cc, true);
     }
     cp_async_wait_all();
     __syncthreads();
@@ -250,9 +250,9 @@ mul_gram_kernel(int64_t rows, int c, const double* __restrict__ X, int64_t ldx, 
     for (int j = 0; j < 32; ++j)
       if (j < c) ts[t][j] = t < nr ? acc[j] : 0.0;
     __syncthreads();
-    for (int e = t; e < nr * c; e += kMgRows) {
-      const int rr = e / c, cc = e - (e / c) * c;
-      Q[(base + rr) * ldq + cc] = ts[rr][cc];
+    if (t < nr) {
+      double* dst = Q + (base + t) * ldq;
+      for (int cc = 0; cc < c; ++cc) dst[cc] = ts[t][cc];
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {

@@ -46,6 +46,8 @@ int fill_uniform(int64_t rows, int64_t cols, double* X, int64_t ldx, uint64_t se
 int householder_complete(int64_t N, int r, int k, double* out, int64_t ldo, cudaStream_t s,
                          double* kp_out = nullptr);
 int fill_identity(int k, double* out, int64_t ldo, cudaStream_t s);
+int product_with_completion(int64_t N, int r, int k, const double* X, int64_t ldx, const double* B, int64_t ldb,
+                            double* out, int64_t ldo, cudaStream_t s);
 int max_abs(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* out, cudaStream_t s);
 int fill_uniform_scaled(int64_t rows, int64_t cols, double* X, int64_t ldx, uint64_t seed, const double* scale,
                         double factor, cudaStream_t s);

@@ -251,6 +251,22 @@ static int finish_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t 
   retry:
     SPB_TRY(transpose(r, r, Ry, r, Ryt, r, s));
     SPB_TRY(jacobi_svd(r, Ryt, r, Us, r, Sr, Vs, r, s));                  // Ry^T = Us Sr Vs^T
+    if (qflag) {
+      int h = 0;
+      SPB_CUDA(cudaMemcpyAsync(&h, qflag, sizeof(int), cudaMemcpyDeviceToHost, s));
+      SPB_CUDA(cudaStreamSynchronize(s));
+      qflag = nullptr;
+      if (h) {  // CholeskyQR2 broke down: Householder TSQR and redo the core
+        SPB_TRY(tsqr(n, r, Y, r, Qy, r, Ry, r, s));
+        goto retry;
+      }
+    }
+    if (r < k && product_with_completion(m, r, k, Z, ldz, Us, r, U, k, s) == SP_OK &&
+        product_with_completion(n, r, k, Qy, r, Vs, r, V, k, s) == SP_OK) {
+      // U = [Z Us | completion], V = [Qy Vs | completion], one pass each
+      SPB_CUDA(cudaMemcpyAsync(S, Sr, kk * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      return SP_OK;
+    }
     if (r <= k) {
       SPB_TRY(gemm(0, 0, m, r, r, 1.0, Z, ldz, Us, r, 0.0, U, k, s));     // U = Z Us
       SPB_TRY(gemm(0, 0, n, r, r, 1.0, Qy, r, Vs, r, 0.0, V, k, s));      // V = Qy Vs
@@ -263,16 +279,6 @@ static int finish_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t 
       SPB_TRY(copy2d(n, kk, Vf, r, V, k, s));
     }
     SPB_CUDA(cudaMemcpyAsync(S, Sr, kk * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    if (qflag) {
-      int h = 0;
-      SPB_CUDA(cudaMemcpyAsync(&h, qflag, sizeof(int), cudaMemcpyDeviceToHost, s));
-      SPB_CUDA(cudaStreamSynchronize(s));
-      qflag = nullptr;
-      if (h) {  // CholeskyQR2 broke down: Householder TSQR and redo the core
-        SPB_TRY(tsqr(n, r, Y, r, Qy, r, Ry, r, s));
-        goto retry;
-      }
-    }
   }
   SPB_TRY(complete_basis(m, kk, k, U, k, 0xC0FFEEull, s));
   SPB_TRY(complete_basis(n, kk, k, V, k, 0xBEEFull, s));

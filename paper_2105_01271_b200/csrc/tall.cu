@@ -19,14 +19,18 @@ constexpr int kTgTile = 64;  // rows per staged tile
 __device__ __forceinline__ int round_up_dev(int x, int m) { return (x + m - 1) / m * m; }
 
 // Copies rows [base, base + nr) of X (cols c) into s (stride sp, zero pad up
-// to sp - 1 columns and up to `tile` rows).
+// to sp - 1 columns and up to `tile` rows).  Four threads per row (no integer
+// division in the address computation; each row's bytes are read by
+// neighbouring lanes).
 __device__ __forceinline__ void stage_rows(double* s, int sp, int tile, const double* X, int64_t ldx,
                                            int64_t base, int nr, int c) {
   const int width = sp - 1;
-  for (int e = threadIdx.x; e < tile * width; e += blockDim.x) {
-    const int rr = e / width, cc = e - rr * width;
-    const bool ok = rr < nr && cc < c;
-    cp_async_f64(&s[rr * sp + cc], ok ? X + (base + rr) * ldx + cc : X, ok);
+  for (int rr = threadIdx.x >> 2; rr < tile; rr += blockDim.x >> 2) {
+    const double* src = X + (base + (rr < nr ? rr : 0)) * ldx;
+    for (int cc = threadIdx.x & 3; cc < width; cc += 4) {
+      const bool ok = rr < nr && cc < c;
+      cp_async_f64(&s[rr * sp + cc], ok ? src + cc : X, ok);
+    }
   }
 }
 
@@ -155,12 +159,13 @@ int tall_gram(int64_t rows, int c, const double* X, int64_t ldx, int d, const do
   return split_reduce(part, nb, c, d, alpha, beta, G, ldg, s);
 }
 
-// O = alpha X M + beta O.  A CTA owns R = min(512, 2048 / d) consecutive rows
-// and each thread forms output elements t, t + 256, ... of that row-major
-// R x d block, so loads and stores are coalesced whatever d is; the rows of X
-// and all of M are staged in shared memory (cp.async).  Each output row
-// depends only on the same row of X, and the CTA's rows are staged before
-// any output is written, so O may alias X (same rows, any columns).
+// O = alpha X M + beta O.  Row tiles of R = min(512, 2048 / d) rows are
+// visited grid-stride (M staged once per CTA); within a tile each thread forms
+// output elements t, t + 256, ... of the row-major R x d block (coalesced
+// loads and stores whatever d is; the (row, column) of the next element is
+// stepped without division).  Each output row depends only on the same row
+// of X, and a tile is staged before any of it is written, so O may alias X
+// (same rows, any columns).
 constexpr int kTmThreads = 256;
 
 __global__ void __launch_bounds__(kTmThreads)
@@ -171,42 +176,140 @@ tall_mul_kernel(int64_t rows, int c, const double* X, int64_t ldx, int d, const 
   const int sp = c + 1;
   double* ms = tm_smem;          // [c][d]
   double* ts = tm_smem + c * d;  // [rpc][sp]
-  const int64_t base = (int64_t)blockIdx.x * rpc;
-  const int nr = (int)imin64(rpc, rows - base);
-  for (int e = threadIdx.x; e < c * d; e += kTmThreads) {
-    const int i = e / d, j = e - (e / d) * d;
-    cp_async_f64(&ms[e], M + (int64_t)i * ldm + j, true);
-  }
-  for (int e = threadIdx.x; e < nr * c; e += kTmThreads) {
-    const int rr = e / c, cc = e - (e / c) * c;
-    cp_async_f64(&ts[rr * sp + cc], X + (base + rr) * ldx + cc, true);
-  }
-  cp_async_wait_all();
-  __syncthreads();
-  const int ne = nr * d;
-  for (int e0 = threadIdx.x; e0 < ne; e0 += 4 * kTmThreads) {
-    double acc[4], old[4];
-    int rr[4], cc[4];
+  for (int i = threadIdx.x >> 2; i < c; i += kTmThreads >> 2)
+    for (int j = threadIdx.x & 3; j < d; j += 4) cp_async_f64(&ms[i * d + j], M + (int64_t)i * ldm + j, true);
+  const int rstep = kTmThreads / d, cstep = kTmThreads - (kTmThreads / d) * d;
+  const int r_first = threadIdx.x / d, c_first = threadIdx.x - (threadIdx.x / d) * d;
+  for (int64_t base = (int64_t)blockIdx.x * rpc; base < rows; base += (int64_t)gridDim.x * rpc) {
+    const int nr = (int)imin64(rpc, rows - base);
+    __syncthreads();  // the previous tile's reads of ts are done
+    for (int rr = threadIdx.x >> 2; rr < nr; rr += kTmThreads >> 2) {
+      const double* src = X + (base + rr) * ldx;
+      for (int cc = threadIdx.x & 3; cc < c; cc += 4) cp_async_f64(&ts[rr * sp + cc], src + cc, true);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    int rr = r_first, cc = c_first;
+    while (rr < nr) {
+      // four elements per round: their beta * O reads are in flight together
+      int er[4], ec[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int e = e0 + u * kTmThreads;
-      rr[u] = e < ne ? e / d : 0;
-      cc[u] = e < ne ? e - rr[u] * d : 0;
-      acc[u] = 0.0;
-      old[u] = (beta != 0.0 && e < ne) ? O[(base + rr[u]) * ldo + cc[u]] : 0.0;
+      for (int u = 0; u < 4; ++u) {
+        er[u] = rr;
+        ec[u] = cc;
+        rr += rstep;
+        cc += cstep;
+        if (cc >= d) {
+          cc -= d;
+          ++rr;
+        }
+      }
+      double old[4], acc[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        old[u] = (beta != 0.0 && er[u] < nr) ? O[(base + er[u]) * ldo + ec[u]] : 0.0;
+        acc[u] = 0.0;
+      }
+      for (int i = 0; i < c; ++i) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (er[u] < nr) acc[u] = fma(ts[er[u] * sp + i], ms[i * d + ec[u]], acc[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (er[u] < nr) {
+          const int64_t row = base + er[u];
+          double v = alpha * acc[u];
+          if (row < top_rows) v += top[row * ldt + ec[u]];
+          O[row * ldo + ec[u]] = (beta == 0.0) ? v : fma(beta, old[u], v);
+        }
+      }
+    }
+  }
+}
+
+// Wide outputs (d > 32): one warp per row, lane q*32 + l owns output
+// column l + 32 q (coalesced 256-byte stores), the row of X is loaded by
+// lanes 0..c-1 and broadcast by shuffles, M is read from shared memory with
+// consecutive lanes on consecutive columns.  Rows are visited grid-stride.
+template <int QMAX>
+__global__ void __launch_bounds__(kTmThreads)
+tall_mul_wide_kernel(int64_t rows, int c, const double* X, int64_t ldx, int d, const double* __restrict__ M,
+                     int64_t ldm, double alpha, double beta, double* O, int64_t ldo,
+                     const double* __restrict__ top, int64_t ldt, int64_t top_rows) {
+  extern __shared__ __align__(16) double tw_smem[];
+  for (int i = threadIdx.x >> 5; i < c; i += kTmThreads >> 5)
+    for (int j = threadIdx.x & 31; j < d; j += 32) tw_smem[i * d + j] = M[(int64_t)i * ldm + j];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (kTmThreads >> 5);
+  int64_t row = (int64_t)blockIdx.x * (kTmThreads >> 5) + (threadIdx.x >> 5);
+  // the next row of X is loaded while the current one is processed
+  double nx0 = 0.0, nx1 = 0.0;
+  if (row < rows) {
+    nx0 = lane < c ? X[row * ldx + lane] : 0.0;
+    nx1 = lane + 32 < c ? X[row * ldx + lane + 32] : 0.0;
+  }
+  for (; row < rows; row += nw) {
+    const double x0 = nx0, x1 = nx1;
+    if (row + nw < rows) {
+      nx0 = lane < c ? X[(row + nw) * ldx + lane] : 0.0;
+      nx1 = lane + 32 < c ? X[(row + nw) * ldx + lane + 32] : 0.0;
+    }
+    double* orow = O + row * ldo;
+    double acc[QMAX], old[QMAX];
+#pragma unroll
+    for (int q = 0; q < QMAX; ++q) {
+      acc[q] = 0.0;
+      old[q] = (beta != 0.0 && lane + 32 * q < d) ? orow[lane + 32 * q] : 0.0;
     }
     for (int i = 0; i < c; ++i) {
+      const double xi = __shfl_sync(0xffffffffu, i < 32 ? x0 : x1, i & 31);
+      const double* mr = tw_smem + i * d + lane;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) acc[u] = fma(ts[rr[u] * sp + i], ms[i * d + cc[u]], acc[u]);
+      for (int q = 0; q < QMAX; ++q)
+        if (lane + 32 * q < d) acc[q] = fma(xi, mr[32 * q], acc[q]);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int e = e0 + u * kTmThreads;
-      if (e < ne) {
-        const int64_t row = base + rr[u];
-        double v = alpha * acc[u];
-        if (row < top_rows) v += top[row * ldt + cc[u]];
-        O[row * ldo + cc[u]] = (beta == 0.0) ? v : fma(beta, old[u], v);
+    for (int q = 0; q < QMAX; ++q) {
+      const int j = lane + 32 * q;
+      if (j < d) {
+        double v = alpha * acc[q];
+        if (row < top_rows) v += top[row * ldt + j];
+        orow[j] = (beta == 0.0) ? v : fma(beta, old[q], v);
+      }
+    }
+  }
+}
+
+// Narrow outputs (d <= 16) of long row counts: one thread per row, M
+// broadcast from shared memory; each thread writes its row's d values.
+__global__ void __launch_bounds__(kTmThreads)
+tall_mul_narrow_kernel(int64_t rows, int c, const double* X, int64_t ldx, int d, const double* __restrict__ M,
+                       int64_t ldm, double alpha, double beta, double* O, int64_t ldo,
+                       const double* __restrict__ top, int64_t ldt, int64_t top_rows) {
+  __shared__ double nm[64 * 16];
+  for (int e = threadIdx.x; e < c * d; e += kTmThreads) nm[e] = M[(int64_t)(e / d) * ldm + (e % d)];
+  __syncthreads();
+  const int64_t nt = (int64_t)gridDim.x * kTmThreads;
+  for (int64_t row = (int64_t)blockIdx.x * kTmThreads + threadIdx.x; row < rows; row += nt) {
+    const double* xr = X + row * ldx;
+    double acc[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+    for (int i = 0; i < c; ++i) {
+      const double xi = xr[i];
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < d) acc[j] = fma(xi, nm[i * d + j], acc[j]);
+    }
+    double* orow = O + row * ldo;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (j < d) {
+        double v = alpha * acc[j];
+        if (row < top_rows) v += top[row * ldt + j];
+        orow[j] = (beta == 0.0) ? v : fma(beta, orow[j], v);
       }
     }
   }
@@ -223,10 +326,45 @@ int tall_mul(int64_t rows, int c, const double* X, int64_t ldx, int d, const dou
     SPB_CUDA(cudaFuncSetAttribute(tall_mul_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
     attr = true;
   }
+  const int64_t tr = top ? top_rows : 0;
+  if (rows >= 4096 && d > 32) {  // wide: warp per row
+    const size_t smem = (size_t)c * d * sizeof(double);
+    const int grid = (int)std::min<int64_t>(ceil_div(rows, kTmThreads / 32), 8 * kNumSMs);
+#define SPB_TMW(Q)                                                                                          \
+  do {                                                                                                      \
+    static bool attr_w = false;                                                                             \
+    if (!attr_w) {                                                                                          \
+      SPB_CUDA(cudaFuncSetAttribute(tall_mul_wide_kernel<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                                    64 * 1024));                                                            \
+      attr_w = true;                                                                                        \
+    }                                                                                                       \
+    tall_mul_wide_kernel<Q><<<grid, kTmThreads, smem, s>>>(rows, c, X, ldx, d, M, ldm, alpha, beta, O, ldo, \
+                                                           top, ldt, tr);                                   \
+  } while (0)
+    if (d <= 64)
+      SPB_TMW(2);
+    else if (d <= 128)
+      SPB_TMW(4);
+    else
+      SPB_TMW(8);
+#undef SPB_TMW
+    count_launch();
+    SPB_CHECK_LAUNCH();
+    return SP_OK;
+  }
+  if (rows >= 65536 && d <= 16 && c * d <= 64 * 16) {  // narrow: thread per row
+    const int grid = (int)std::min<int64_t>(ceil_div(rows, kTmThreads), 8 * kNumSMs);
+    tall_mul_narrow_kernel<<<grid, kTmThreads, 0, s>>>(rows, c, X, ldx, d, M, ldm, alpha, beta, O, ldo, top, ldt,
+                                                       tr);
+    count_launch();
+    SPB_CHECK_LAUNCH();
+    return SP_OK;
+  }
   const int rpc = std::max(1, std::min(512, 2048 / d));
   const size_t smem = ((size_t)c * d + (size_t)rpc * (c + 1)) * sizeof(double);
-  tall_mul_kernel<<<ceil_div(rows, rpc), kTmThreads, smem, s>>>(rows, c, X, ldx, d, M, ldm, alpha, beta, O, ldo,
-                                                                top, ldt, top ? top_rows : 0, rpc);
+  const int grid = (int)std::min<int64_t>(ceil_div(rows, rpc), 8 * kNumSMs);
+  tall_mul_kernel<<<grid, kTmThreads, smem, s>>>(rows, c, X, ldx, d, M, ldm, alpha, beta, O, ldo, top, ldt,
+                                                 top ? top_rows : 0, rpc);
   count_launch();
   SPB_CHECK_LAUNCH();
   return SP_OK;

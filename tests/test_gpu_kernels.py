@@ -107,7 +107,8 @@ def test_skinny_atz_f32_and_determinism(cuda):
 @pytest.mark.parametrize("M,N,K", [(64, 64, 16), (100, 37, 259), (3, 200, 4000), (513, 65, 7),
                                    (7, 7, 65536), (40, 33, 3000), (64, 64, 5000), (2, 3, 700),
                                    (3000, 33, 40), (5000, 64, 64), (700, 1, 1), (65536, 43, 7),
-                                   (2000, 32, 4096), (4096, 32, 2000), (130, 5, 300), (129, 31, 70)])
+                                   (2000, 32, 4096), (4096, 32, 2000), (130, 5, 300), (129, 31, 70),
+                                   (70000, 5, 5), (70000, 16, 3), (9000, 200, 5), (5000, 100, 64)])
 def test_gemm(cuda, ta, tb, M, N, K):
     rng = philox(M + N + K + ta * 2 + tb)
     A = rng.standard_normal((K, M) if ta else (M, K))
