@@ -173,12 +173,13 @@ tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t l
       // of step j - 1 on the other buffer, and reads of step j happen before
       // the __syncthreads of step j + 1, which precedes any push of step j + 2
       // by this CTA's peers)
-      dc = 0.0;
-      sigma2 = 0.0;
-      for (int d = 0; d < cl; ++d) {
-        dc += cbuf[buf][d][c];
-        sigma2 += cbuf[buf][d][j];
+      double ac4[4] = {0.0, 0.0, 0.0, 0.0}, sg4[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int d = 0; d < cl; ++d) {  // rank order in 4 interleaved sums (same in every CTA)
+        ac4[d & 3] += cbuf[buf][d][c];
+        sg4[d & 3] += cbuf[buf][d][j];
       }
+      dc = (ac4[0] + ac4[1]) + (ac4[2] + ac4[3]);
+      sigma2 = (sg4[0] + sg4[1]) + (sg4[2] + sg4[3]);
       alpha = crow[buf][j];
       ac = crow[buf][c];
       if (threadIdx.x == 0) mbar_arrive_expect_tx(&cbar[buf], step_bytes);
