@@ -56,44 +56,77 @@ def peaks():
     return 6650.0, "fallback"
 
 
+_SAMPLER_SRC = r"""
+import sys, time
+import pynvml as nv
+nv.nvmlInit()
+h = nv.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+print("ready", mx, flush=True)
+while True:
+    sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+    try:
+        bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+    except Exception:
+        bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+    print(f"{time.monotonic():.6f} {sm} {bits}", flush=True)
+    time.sleep(0.002)
+"""
+
+
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region.
+
+    The sampler runs in a separate process (NVML every 2 ms, timestamped) so
+    it never competes with the timed loop for the interpreter lock; samples
+    are kept between __enter__ and __exit__.  Falls back to nvidia-smi."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu_index: int):
-        self.idx = gpu_index
-        self.samples = []
-        self._stop = threading.Event()
-        self._t = None
-
     # NVML clocks-event-reason bits (nvml.h)
     NVML_BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
                  "hw_thermal_slowdown": 0x40}
 
-    def _run(self):
-        # NVML first: a 2 ms sampling period resolves a tens-of-ms timed region
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.samples = []
+        self._proc = None
+        self._mx = None
+        self._t0 = self._t1 = None
         try:
-            import pynvml as nv
-            nv.nvmlInit()
-            h = nv.nvmlDeviceGetHandleByIndex(self.idx)
-            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-            while not self._stop.is_set():
-                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                try:
-                    bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                except Exception:
-                    bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-                act = ["Active" if bits & self.NVML_BITS[k] else "Not Active"
-                       for k in ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")]
-                self.samples.append([str(sm), str(mx), "", hex(bits)] + act)
-                self._stop.wait(0.002)
-            return
+            self._proc = subprocess.Popen([sys.executable, "-c", _SAMPLER_SRC, str(gpu_index)],
+                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            line = self._proc.stdout.readline().split()
+            if len(line) == 2 and line[0] == "ready":
+                self._mx = line[1]
+            else:
+                self._proc.kill()
+                self._proc = None
         except Exception:
-            pass
-        while not self._stop.is_set():
+            self._proc = None
+
+    def __enter__(self):
+        self._t0 = time.monotonic()
+        return self
+
+    def __exit__(self, *exc):
+        self._t1 = time.monotonic()
+        if self._proc is not None:
+            time.sleep(0.005)
+            self._proc.kill()
+            out, _ = self._proc.communicate(timeout=10)
+            for ln in out.splitlines():
+                parts = ln.split()
+                if len(parts) != 3:
+                    continue
+                t, sm, bits = float(parts[0]), parts[1], int(parts[2])
+                if self._t0 <= t <= self._t1:
+                    act = ["Active" if bits & self.NVML_BITS[k] else "Not Active"
+                           for k in ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")]
+                    self.samples.append([sm, self._mx, "", hex(bits)] + act)
+        if not self.samples:
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True,
@@ -102,23 +135,12 @@ class ClockSampler:
                     self.samples.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
-
-    def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
-        return self
-
-    def __exit__(self, *exc):
-        self._stop.set()
-        if self._t:
-            self._t.join(timeout=10)
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1] and s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4)
                           if len(s) > 4 + i and s[4 + i].lower() == "active"})
