@@ -257,8 +257,9 @@ int sp_power_id(const void* A, int32_t a_dtype, int64_t m, int64_t n, int64_t ld
 /* ---------------------------------------------------------------- K8 -----
  * ||A - U diag(S) V^T||_F^2 and ||A||_F^2 streamed over A (never forming the
  * m x n product): the rel_frob_error metric (src/analysis.py:57-65) of a
- * LowRankSVD.reconstruct() (src/svd.py:42-43).  out2 (host) = {err2, ref2}.
- * Synchronises. */
+ * LowRankSVD.reconstruct() (src/svd.py:42-43) and of the CLI --verify pass
+ * (src/cli.py:125-139, left (m x k) . right (k x n) with S = 1, V = right^T).
+ * k <= 256.  out2 (host) = {err2, ref2}.  Synchronises. */
 int sp_frob_residual(const void* A, int32_t a_dtype, int64_t m, int64_t n, int64_t lda,
                      const double* U, int64_t ldu, const double* S, const double* V,
                      int64_t ldv, int32_t k, double* out2, void* stream);

@@ -682,6 +682,46 @@ def power_id_two_pass(a, idx, w, cols, k, q=1, block_rows=BLOCK, project_ell=Non
 
 
 # ----------------------------------------------------------------------------
+# SPC-ID-ERR: the streamed Gram-gap sweep (src/analysis.py:117-180)
+# ----------------------------------------------------------------------------
+
+def lambda_max_sym(sym):
+    """src/kernels.py:171-181 (largest signed eigenvalue, symmetrised)."""
+    sym = np.asarray(sym, dtype=np.float64)
+    if sym.shape[0] == 0:
+        return 0.0
+    return float(np.linalg.eigvalsh((sym + sym.T) / 2.0)[-1])
+
+
+def epsilon_sweep(a, idx, w, m_c, taus=None, block_rows=BLOCK, points=33, span=100.0):
+    """src/analysis.py:141-180 (streaming_epsilon_sweep) with the default grid
+    of :128-138 (centre (||B_f||_2 / ||B_c||_2)^2, 33 log points, span 100)."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    m = a.shape[0]
+    if not 1 <= m_c <= m:
+        raise OracleConfigError(f"sampled row count m_c={m_c} outside [1, {m}]")
+    stride = m // m_c
+    keep_f, keep_c = [], []
+    for lo, blk in _row_blocks(a, block_rows):
+        first = ((lo // stride) + 1) * stride - 1   # 1-based row i kept when i % stride == 0
+        local = np.arange(first - lo, blk.shape[0], stride)
+        if local.size:
+            sub = blk[local]
+            keep_f.append(sub.copy())
+            keep_c.append(sketch_rows(sub, idx, w))
+    bf, bc = np.vstack(keep_f), np.vstack(keep_c)
+    if taus is None:
+        top_f = np.linalg.svd(bf, compute_uv=False)[0]
+        top_c = np.linalg.svd(bc, compute_uv=False)[0]
+        centre = (top_f / top_c) ** 2
+        taus = np.geomspace(centre / span, centre * span, points)
+    taus = np.asarray(taus, dtype=np.float64)
+    gf, gc = bf @ bf.T, bc @ bc.T
+    vals = np.array([stride * lambda_max_sym(gf - t * gc) for t in taus])
+    return taus, vals, stride
+
+
+# ----------------------------------------------------------------------------
 # metrics used by the parity gates (src/analysis.py:57-74)
 # ----------------------------------------------------------------------------
 

@@ -353,30 +353,33 @@ int thin_svd_t(int64_t rows, int64_t cols, const double* Xt, int64_t ldxt, doubl
 
 // ------------------------------------------------------ K8 residual norm ----
 // err2 = sum_ij (A_ij - sum_c U_ic S_c V_jc)^2, ref2 = sum_ij A_ij^2.
-// One thread per column j holds V[j, :] in shared memory; rows are streamed
-// with U S of the current row broadcast from shared memory.
+// One thread per column j holds V[j, :] in shared memory (dynamic, k <= 256);
+// rows are streamed with U S of the current row broadcast from shared memory.
+// The verify pass of the CLI (src/cli.py:125-139) fused into one A read.
 constexpr int kResThreads = 64;
-constexpr int kResMaxK = 64;
+constexpr int kResMaxK = 256;
 
 template <typename TA>
 __global__ void __launch_bounds__(kResThreads)
 residual_kernel(const TA* __restrict__ A, int64_t m, int64_t n, int64_t lda, const double* __restrict__ U,
                 int64_t ldu, const double* __restrict__ S, const double* __restrict__ V, int64_t ldv,
                 int k, int64_t rows_per_cta, double* partial) {
-  __shared__ double vs[kResThreads][kResMaxK + 1];
-  __shared__ double us[kResMaxK];
+  extern __shared__ double res_smem[];
+  double* vs = res_smem;                           // [kResThreads][k + 1]
+  double* us = res_smem + kResThreads * (k + 1);   // [k]
   __shared__ double red[2][kResThreads / 32];
   const int64_t j = (int64_t)blockIdx.x * kResThreads + threadIdx.x;
-  for (int c = 0; c < k; ++c) vs[threadIdx.x][c] = (j < n) ? V[j * ldv + c] : 0.0;
+  for (int c = 0; c < k; ++c) vs[threadIdx.x * (k + 1) + c] = (j < n) ? V[j * ldv + c] : 0.0;
   const int64_t r0 = (int64_t)blockIdx.y * rows_per_cta, r1 = min(m, r0 + rows_per_cta);
   double e2 = 0.0, a2 = 0.0;
   for (int64_t i = r0; i < r1; ++i) {
     __syncthreads();
-    if (threadIdx.x < k) us[threadIdx.x] = U[i * ldu + threadIdx.x] * S[threadIdx.x];
+    for (int c = threadIdx.x; c < k; c += kResThreads) us[c] = U[i * ldu + c] * S[c];
     __syncthreads();
     if (j < n) {
       double rec = 0.0;
-      for (int c = 0; c < k; ++c) rec = fma(us[c], vs[threadIdx.x][c], rec);
+      const double* vr = vs + threadIdx.x * (k + 1);
+      for (int c = 0; c < k; ++c) rec = fma(us[c], vr[c], rec);
       const double a = widen(A[i * lda + j]);
       const double d = a - rec;
       e2 = fma(d, d, e2);
@@ -405,7 +408,7 @@ residual_kernel(const TA* __restrict__ A, int64_t m, int64_t n, int64_t lda, con
 int frob_residual(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, const double* U,
                   int64_t ldu, const double* S, const double* V, int64_t ldv, int k, double* out2,
                   cudaStream_t s) {
-  SPB_REQUIRE(k >= 0 && k <= kResMaxK, "frob_residual supports k <= 64");
+  SPB_REQUIRE(k >= 0 && k <= kResMaxK, "frob_residual supports k <= 256");
   const int gx = ceil_div(n, kResThreads);
   int gy = std::max(1, std::min<int>(ceil_div(4 * kNumSMs, gx), (int)m));
   const int64_t rpc = ceil_div(m, gy);
@@ -413,10 +416,19 @@ int frob_residual(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda,
   Arena ar(s);
   SPB_ALLOC(ar, double, part, (size_t)2 * gx * gy);
   dim3 g(gx, gy);
+  const size_t smem = ((size_t)kResThreads * (k + 1) + (size_t)std::max(k, 1)) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    SPB_CUDA(cudaFuncSetAttribute(residual_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    SPB_CUDA(cudaFuncSetAttribute(residual_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    attr = true;
+  }
   if (a_dtype == SP_F64)
-    residual_kernel<double><<<g, kResThreads, 0, s>>>((const double*)A, m, n, lda, U, ldu, S, V, ldv, k, rpc, part);
+    residual_kernel<double><<<g, kResThreads, smem, s>>>((const double*)A, m, n, lda, U, ldu, S, V, ldv, k, rpc,
+                                                         part);
   else
-    residual_kernel<float><<<g, kResThreads, 0, s>>>((const float*)A, m, n, lda, U, ldu, S, V, ldv, k, rpc, part);
+    residual_kernel<float><<<g, kResThreads, smem, s>>>((const float*)A, m, n, lda, U, ldu, S, V, ldv, k, rpc,
+                                                        part);
   SPB_LAUNCHED();
   std::vector<double> h((size_t)2 * gx * gy);
   SPB_CUDA(cudaMemcpyAsync(h.data(), part, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));

@@ -64,8 +64,11 @@ class FactoredLifting:
     # ---- implicit right factor: products with A on the device
     def _mm(self, ta, tb, a, b, M, N, K):
         from .device import empty, ptr, stream_handle
+        # left / right may be column slices of wider buffers: pass the row stride
+        a = a if a.stride(1) == 1 else a.contiguous()
+        b = b if b.stride(1) == 1 else b.contiguous()
         out = empty((M, N))
-        _lib.call("sp_gemm", ta, tb, M, N, K, 1.0, ptr(a), a.shape[1], ptr(b), b.shape[1], 0.0, ptr(out), N,
+        _lib.call("sp_gemm", ta, tb, M, N, K, 1.0, ptr(a), a.stride(0), ptr(b), b.stride(0), 0.0, ptr(out), N,
                   stream_handle())
         return out
 

@@ -198,6 +198,15 @@ def twopass_cases(out):
     rec.update(rpw0_s=r.s, rpw0_u=r.u, rpw0_v=r.v)
     f = sp.two_pass_id(sp.ArraySnapshotStream(a), op1, 7)
     rec.update(rtpid_idx=f.indices, rtpid_p=f.p)
+    # SPC-ID-ERR sweeps (src/analysis.py:141-180): cfg1 field and a random matrix
+    from sketchpress.analysis import streaming_epsilon_sweep
+    a = generate_host(cfg)
+    sw = streaming_epsilon_sweep(sp.ArraySnapshotStream(a), op, 50)
+    rec.update(eps_taus=sw.taus, eps_values=sw.values, eps_stride=np.array(sw.sample_stride))
+    a2 = philox(44).standard_normal((90, 120))
+    op2 = sp.build_sketch(sp.SketchSpec("injection", 120, 30))
+    sw = streaming_epsilon_sweep(sp.ArraySnapshotStream(a2), op2, 40)
+    rec.update(eps2_taus=sw.taus, eps2_values=sw.values, eps2_stride=np.array(sw.sample_stride))
     np.savez_compressed(out / "twopass_cases.npz", **rec)
     print("twopass", sorted(rec))
 

@@ -314,3 +314,22 @@ def test_householder_complete(cuda, N, r, k):
     o = d.cpu().numpy()
     np.testing.assert_array_equal(o[:, :r], q)  # untouched
     np.testing.assert_allclose(o.T @ o, np.eye(k), atol=1e-13)
+
+
+@pytest.mark.parametrize("m,n,k,f32", [(300, 1000, 7, False), (257, 700, 64, False), (100, 333, 200, False),
+                                       (120, 500, 20, True)])
+def test_frob_residual(cuda, m, n, k, f32):
+    """K8: ||A - U diag(S) V^T||_F^2 and ||A||_F^2 without forming U S V^T."""
+    rng = philox(m + n + k)
+    a = rng.standard_normal((m, n))
+    if f32:
+        a = a.astype(np.float32)
+    u, s, v = rng.standard_normal((m, k)), rng.random(k), rng.standard_normal((n, k))
+    out = np.zeros(2)
+    da = cuda.from_numpy(a).cuda()
+    du, ds, dv = _dev(u, cuda), _dev(s, cuda), _dev(v, cuda)
+    _lib.call("sp_frob_residual", da.data_ptr(), _lib.SP_F32 if f32 else _lib.SP_F64, m, n, n, du.data_ptr(), k,
+              ds.data_ptr(), dv.data_ptr(), k, k, out.ctypes.data_as(__import__("ctypes").c_void_p), _stream(cuda))
+    a64 = a.astype(np.float64)
+    want = np.sum((a64 - (u * s) @ v.T) ** 2), np.sum(a64 ** 2)
+    np.testing.assert_allclose(out, want, rtol=1e-12)

@@ -201,3 +201,21 @@ def test_oracle_two_pass_variants_match_reference():
     f = oracle.two_pass_id(a, tab1, w1, 7)
     assert np.array_equal(f.indices, g["rtpid_idx"])
     np.testing.assert_allclose(f.p, g["rtpid_p"], rtol=0, atol=1e-11)
+
+
+def test_oracle_epsilon_sweep_matches_reference():
+    """SPC-ID-ERR (src/analysis.py:141-180), oracle vs the reference's outputs."""
+    g = load_golden("twopass_cases.npz")
+    cfg = CONFIGS["cfg1"]
+    a = generate_host(cfg)
+    idx = oracle.grid_coarse_indices(cfg.grid, cfg.stride)
+    taus, vals, stride = oracle.epsilon_sweep(a, idx[None, :], _ones(idx), 50)
+    assert stride == int(g["eps_stride"])
+    np.testing.assert_allclose(taus, g["eps_taus"], rtol=1e-13)
+    np.testing.assert_allclose(vals, g["eps_values"], rtol=0, atol=1e-12 * np.abs(g["eps_values"]).max())
+    a2 = philox(44).standard_normal((90, 120))
+    t1 = oracle.stencil_tables("injection", 120, 30)
+    taus, vals, stride = oracle.epsilon_sweep(a2, t1[0], t1[1], 40)
+    assert stride == int(g["eps2_stride"])
+    np.testing.assert_allclose(taus, g["eps2_taus"], rtol=1e-13)
+    np.testing.assert_allclose(vals, g["eps2_values"], rtol=0, atol=1e-12 * np.abs(g["eps2_values"]).max())
