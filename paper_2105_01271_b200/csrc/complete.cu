@@ -26,7 +26,8 @@ constexpr int kHcMaxK = 256;
 // rows of the completion block E' (k x (k-r), ld lde).
 __global__ void __launch_bounds__(256)
 hh_complete_kernel(int r, int k, const double* __restrict__ Q, int64_t ldq, double* __restrict__ Kp,
-                   double* __restrict__ Etop, int64_t lde) {
+                   double* __restrict__ Etop, int64_t lde, const double* __restrict__ B = nullptr,
+                   int64_t ldb = 0, double* __restrict__ Mf = nullptr, double* __restrict__ Etf = nullptr) {
   __shared__ double W[kHcMaxR][kHcMaxR + 1];    // LU workspace -> L1 (strict lower) + U (upper)
   __shared__ double Ui[kHcMaxR][kHcMaxR + 1];   // U^{-1}
   __shared__ double Li[kHcMaxR][kHcMaxR + 1];   // L1^{-1}
@@ -104,6 +105,25 @@ hh_complete_kernel(int r, int k, const double* __restrict__ Q, int64_t ldq, doub
     const int a = e / kr, j = e % kr;
     Etop[(int64_t)(r + a) * lde + j] = (a == j) ? 1.0 : 0.0;  // rows r..k-1 of E'
   }
+  if (B == nullptr) return;
+  // fused product (product_with_completion): Mf = [B | -B Kp], Etf = [0 | E']
+  __syncthreads();  // Kp / Etop (global) written by this CTA above
+  for (int e = tid; e < r * k; e += nt) {
+    const int i = e / k, j = e % k;
+    double v;
+    if (j < r) {
+      v = B[(int64_t)i * ldb + j];
+    } else {
+      double a = 0.0;
+      for (int q = 0; q < r; ++q) a = fma(B[(int64_t)i * ldb + q], Kp[q * kr + (j - r)], a);
+      v = -a;
+    }
+    Mf[e] = v;
+  }
+  for (int e = tid; e < k * k; e += nt) {
+    const int i = e / k, j = e % k;
+    Etf[e] = j < r ? 0.0 : Etop[(int64_t)i * lde + (j - r)];
+  }
 }
 
 // out (N x k, ld ldo): columns [0, r) orthonormal on entry; columns [r, k)
@@ -144,39 +164,19 @@ int householder_complete(int64_t N, int r, int k, double* out, int64_t ldo, cuda
   return gemm(0, 0, N, kr, r, -1.0, out, ldo, Kp, kr, 1.0, out + r, ldo, s);
 }
 
-// Mf = [B | -B Kp] (r x k), Etf = [0 | Et] (k x k): the right factor and the
-// top-row correction of the fused product below.
-__global__ void fused_factor_kernel(int r, int k, const double* __restrict__ B, int64_t ldb,
-                                    const double* __restrict__ Kp, const double* __restrict__ Et,
-                                    double* __restrict__ Mf, double* __restrict__ Etf) {
-  const int kr = k - r;
-  for (int e = threadIdx.x; e < r * k; e += blockDim.x) {
-    const int i = e / k, j = e % k;
-    double v;
-    if (j < r) {
-      v = B[(int64_t)i * ldb + j];
-    } else {
-      double a = 0.0;
-      for (int q = 0; q < r; ++q) a = fma(B[(int64_t)i * ldb + q], Kp[q * kr + (j - r)], a);
-      v = -a;
-    }
-    Mf[e] = v;
-  }
-  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
-    const int i = e / k, j = e % k;
-    Etf[e] = j < r ? 0.0 : Et[i * kr + (j - r)];
-  }
-}
-
 // out (N x k) = [X B | completion]: the kept factor X B (X: N x r, B: r x r)
 // and its Householder completion written in ONE streaming pass over the N
 // rows (out = X [B | -B K'] + [0 | E'] on the top k rows).  K' only needs the
 // top k rows of X B, formed first.  Returns SP_ECONFIG (caller falls back to
 // product + householder_complete) outside the small-kernel limits.
+bool product_with_completion_ok(int64_t N, int r, int k) {
+  return !(r < 1 || r >= k || r > kHcMaxR || k > kHcMaxK || N < k || r * k > 64 * 64 || k > 256);
+}
+
 int product_with_completion(int64_t N, int r, int k, const double* X, int64_t ldx, const double* B, int64_t ldb,
                             double* out, int64_t ldo, cudaStream_t s) {
   const int kr = k - r;
-  if (r < 1 || r >= k || r > kHcMaxR || k > kHcMaxK || N < k || r * k > 64 * 64 || k > 256) {
+  if (!product_with_completion_ok(N, r, k)) {
     set_error("product_with_completion limits exceeded");
     return SP_ECONFIG;
   }
@@ -186,10 +186,7 @@ int product_with_completion(int64_t N, int r, int k, const double* X, int64_t ld
   SPB_ALLOC(ar, double, Mf, (size_t)r * k);
   SPB_ALLOC(ar, double, Etf, (size_t)k * k);
   SPB_TRY(gemm(0, 0, k, r, r, 1.0, X, ldx, B, ldb, 0.0, out, ldo, s));  // top k rows of X B
-  hh_complete_kernel<<<1, 256, 0, s>>>(r, k, out, ldo, Kp, Et, kr);
-  count_launch();
-  SPB_CHECK_LAUNCH();
-  fused_factor_kernel<<<1, 256, 0, s>>>(r, k, B, ldb, Kp, Et, Mf, Etf);
+  hh_complete_kernel<<<1, 256, 0, s>>>(r, k, out, ldo, Kp, Et, kr, B, ldb, Mf, Etf);
   count_launch();
   SPB_CHECK_LAUNCH();
   return tall_mul(N, r, X, ldx, k, Mf, k, 1.0, 0.0, out, ldo, s, Etf, k, k);

@@ -13,6 +13,7 @@
 // a sweep with no rotation (|w_p.w_q| <= 1e-15 ||w_p|| ||w_q|| for every pair).
 #include "common.cuh"
 #include "launch_count.cuh"
+#include "ops.cuh"
 
 namespace spb {
 
@@ -188,7 +189,7 @@ __device__ __forceinline__ int rr_partner(int x, int r, int na) {
 
 __global__ void __launch_bounds__(kJ32Warps * 32)
 jacobi32_kernel(int n, const double* __restrict__ M, int64_t ldm, double* __restrict__ U, int64_t ldu,
-                double* __restrict__ S, double* __restrict__ Vout, int64_t ldv) {
+                double* __restrict__ S, double* __restrict__ Vout, int64_t ldv, bool trans) {
   __shared__ double part[2][kJ32Warps][32][2];
   __shared__ double nrm_s[kJ32Warps][32];
   __shared__ double sig_s[32];
@@ -200,7 +201,7 @@ jacobi32_kernel(int n, const double* __restrict__ M, int64_t ldm, double* __rest
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const int i = w * 8 + k;
-    x[k] = (i < n && c < n) ? M[(int64_t)i * ldm + c] : 0.0;
+    x[k] = (i < n && c < n) ? (trans ? M[(int64_t)c * ldm + i] : M[(int64_t)i * ldm + c]) : 0.0;
     v[k] = (i == c) ? 1.0 : 0.0;
   }
   // column norms and ||M||_F^2 (fixed order)
@@ -316,14 +317,31 @@ jacobi32_kernel(int n, const double* __restrict__ M, int64_t ldm, double* __rest
 
 int jacobi_svd(int64_t n, const double* M, int64_t ldm, double* U, int64_t ldu, double* S,
                double* V, int64_t ldv, cudaStream_t s) {
+  return jacobi_svd_tr(n, M, ldm, false, U, ldu, S, V, ldv, s);
+}
+
+// SVD of M (trans = false) or of M^T (trans = true, n <= 32 reads M
+// transposed in place; larger n transposes into scratch first)
+int jacobi_svd_tr(int64_t n, const double* M, int64_t ldm, bool trans, double* U, int64_t ldu, double* S,
+                  double* V, int64_t ldv, cudaStream_t s) {
   SPB_REQUIRE(n >= 1 && n <= 256, "Jacobi SVD supports 1 <= n <= 256");
   if (n <= 32) {
-    jacobi32_kernel<<<1, kJ32Warps * 32, 0, s>>>((int)n, M, ldm, U, ldu, S, V, ldv);
+    jacobi32_kernel<<<1, kJ32Warps * 32, 0, s>>>((int)n, M, ldm, U, ldu, S, V, ldv, trans);
     count_launch();
     SPB_CHECK_LAUNCH();
     return SP_OK;
   }
   Arena vscratch(s);
+  if (trans) {
+    double* Mt = vscratch.alloc<double>((size_t)n * n);
+    if (!Mt) {
+      set_error("jacobi workspace allocation failed");
+      return SP_ECUDA;
+    }
+    SPB_TRY(transpose(n, n, M, ldm, Mt, n, s));
+    M = Mt;
+    ldm = n;
+  }
   if (V == nullptr) {  // the multi-warp kernel always accumulates V
     V = vscratch.alloc<double>((size_t)n * n);
     ldv = n;

@@ -38,6 +38,8 @@ int qr_tall(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q,
             int64_t ldr, bool well_conditioned, cudaStream_t s);
 int jacobi_svd(int64_t n, const double* M, int64_t ldm, double* U, int64_t ldu, double* S,
                double* V, int64_t ldv, cudaStream_t s);
+int jacobi_svd_tr(int64_t n, const double* M, int64_t ldm, bool trans, double* U, int64_t ldu, double* S,
+                  double* V, int64_t ldv, cudaStream_t s);
 int transpose(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Y, int64_t ldy,
               cudaStream_t s);
 int copy2d(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Y, int64_t ldy,
@@ -46,6 +48,7 @@ int fill_uniform(int64_t rows, int64_t cols, double* X, int64_t ldx, uint64_t se
 int householder_complete(int64_t N, int r, int k, double* out, int64_t ldo, cudaStream_t s,
                          double* kp_out = nullptr);
 int fill_identity(int k, double* out, int64_t ldo, cudaStream_t s);
+bool product_with_completion_ok(int64_t N, int r, int k);
 int product_with_completion(int64_t N, int r, int k, const double* X, int64_t ldx, const double* B, int64_t ldb,
                             double* out, int64_t ldo, cudaStream_t s);
 int max_abs(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* out, cudaStream_t s);

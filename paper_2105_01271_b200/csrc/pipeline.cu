@@ -132,8 +132,7 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
       // Rayleigh-Ritz: Q^T X = Z^T with Z = X^T Q = P Rz  ->  Q^T X = Rz^T P^T
       SPB_TRY(gemm(1, 0, cols, b, rows, 1.0, X, ldx, Q, b, 0.0, Z, b, s));
       SPB_TRY(tsqr(cols, b, Z, b, P, b, Rz, b, s));
-      SPB_TRY(transpose(b, b, Rz, b, Rt, b, s));
-      SPB_TRY(jacobi_svd(b, Rt, b, Us, b, Sg, want_v ? Vs : nullptr, b, s));
+      SPB_TRY(jacobi_svd_tr(b, Rz, b, /*trans=*/true, Us, b, Sg, want_v ? Vs : nullptr, b, s));
       SPB_CUDA(cudaMemcpyAsync(hs.data(), Sg, b * sizeof(double), cudaMemcpyDeviceToHost, s));
       if (itn == 0) SPB_TRY(read_flag_with(pf, hflag, s));
       SPB_CUDA(cudaStreamSynchronize(s));
@@ -215,6 +214,27 @@ static int complete_basis(int64_t N, int r, int k, double* out, int64_t ldo, uin
   return SP_OK;
 }
 
+// Per-thread side stream (+ fork / join events) for independent small chains.
+struct AuxStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  int dev = -1;
+};
+
+static AuxStream& aux_stream() {
+  static thread_local AuxStream ax[16];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  AuxStream& a = ax[dev & 15];
+  if (a.s == nullptr || a.dev != dev) {
+    cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming);
+    a.dev = dev;
+  }
+  return a;
+}
+
 // Given the kept left basis Z (m x r, ld ldz) of the sketch, one read of A:
 // Y = A^T Z, then the rank-k SVD of Z Z^T A written to U (m x k), S, V (n x k).
 static int finish_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, const double* Z,
@@ -249,8 +269,7 @@ static int finish_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t 
       SPB_TRY(tsqr(n, r, Y, r, Qy, r, Ry, r, s));
     }
   retry:
-    SPB_TRY(transpose(r, r, Ry, r, Ryt, r, s));
-    SPB_TRY(jacobi_svd(r, Ryt, r, Us, r, Sr, Vs, r, s));                  // Ry^T = Us Sr Vs^T
+    SPB_TRY(jacobi_svd_tr(r, Ry, r, /*trans=*/true, Us, r, Sr, Vs, r, s));  // Ry^T = Us Sr Vs^T
     if (qflag) {
       int h = 0;
       SPB_CUDA(cudaMemcpyAsync(&h, qflag, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -261,9 +280,16 @@ static int finish_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t 
         goto retry;
       }
     }
-    if (r < k && product_with_completion(m, r, k, Z, ldz, Us, r, U, k, s) == SP_OK &&
-        product_with_completion(n, r, k, Qy, r, Vs, r, V, k, s) == SP_OK) {
-      // U = [Z Us | completion], V = [Qy Vs | completion], one pass each
+    if (r < k && product_with_completion_ok(m, r, k) && product_with_completion_ok(n, r, k)) {
+      // U = [Z Us | completion], V = [Qy Vs | completion], one pass each; the
+      // (short, latency-bound) U chain runs on a side stream beside V's
+      AuxStream& ax = aux_stream();
+      SPB_CUDA(cudaEventRecord(ax.fork, s));
+      SPB_CUDA(cudaStreamWaitEvent(ax.s, ax.fork, 0));
+      SPB_TRY(product_with_completion(m, r, k, Z, ldz, Us, r, U, k, ax.s));
+      SPB_TRY(product_with_completion(n, r, k, Qy, r, Vs, r, V, k, s));
+      SPB_CUDA(cudaEventRecord(ax.join, ax.s));
+      SPB_CUDA(cudaStreamWaitEvent(s, ax.join, 0));
       SPB_CUDA(cudaMemcpyAsync(S, Sr, kk * sizeof(double), cudaMemcpyDeviceToDevice, s));
       return SP_OK;
     }

@@ -173,13 +173,25 @@ tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t l
       // of step j - 1 on the other buffer, and reads of step j happen before
       // the __syncthreads of step j + 1, which precedes any push of step j + 2
       // by this CTA's peers)
-      double ac4[4] = {0.0, 0.0, 0.0, 0.0}, sg4[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int d = 0; d < cl; ++d) {  // rank order in 4 interleaved sums (same in every CTA)
-        ac4[d & 3] += cbuf[buf][d][c];
-        sg4[d & 3] += cbuf[buf][d][j];
+      // rank order in 4 interleaved sums (same in every CTA); cl is a power of 2
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;
+      int d = 0;
+      for (; d + 3 < cl; d += 4) {
+        a0 += cbuf[buf][d][c];
+        a1 += cbuf[buf][d + 1][c];
+        a2 += cbuf[buf][d + 2][c];
+        a3 += cbuf[buf][d + 3][c];
+        g0 += cbuf[buf][d][j];
+        g1 += cbuf[buf][d + 1][j];
+        g2 += cbuf[buf][d + 2][j];
+        g3 += cbuf[buf][d + 3][j];
       }
-      dc = (ac4[0] + ac4[1]) + (ac4[2] + ac4[3]);
-      sigma2 = (sg4[0] + sg4[1]) + (sg4[2] + sg4[3]);
+      for (; d < cl; ++d) {
+        a0 += cbuf[buf][d][c];
+        g0 += cbuf[buf][d][j];
+      }
+      dc = (a0 + a1) + (a2 + a3);
+      sigma2 = (g0 + g1) + (g2 + g3);
       alpha = crow[buf][j];
       ac = crow[buf][c];
       if (threadIdx.x == 0) mbar_arrive_expect_tx(&cbar[buf], step_bytes);
