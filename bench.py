@@ -22,6 +22,7 @@ Under torchrun (N > 1) every rank factorises its own snapshot matrix
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -249,6 +250,10 @@ def run_ours(args):
             dist.barrier()
 
     warnings.simplefilter("ignore")
+    # like timeit: no cyclic-GC pass (tens of ms on an interpreter holding torch)
+    # inside the timed loop; collected once here, re-enabled after
+    gc.collect()
+    gc.disable()
     for _ in range(args.warmup):
         res = step()
     torch.cuda.synchronize()
@@ -264,6 +269,7 @@ def run_ours(args):
         ev1.record()
         torch.cuda.synchronize()
         barrier()
+    gc.enable()
     launches = (_lib.launch_count() - l0) // max(1, args.steps)
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
@@ -340,12 +346,15 @@ def run_ours(args):
         torch.cuda.synchronize()
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        gc.collect()
+        gc.disable()
         e0.record()
         n_e2e = max(1, min(args.steps, 5))
         for _ in range(n_e2e):
             out = e2e_step()
         e1.record()
         torch.cuda.synchronize()
+        gc.enable()
         e_ms = e0.elapsed_time(e1) / n_e2e
         if world > 1:
             t = torch.tensor([e_ms], device=dev)
