@@ -120,6 +120,12 @@ int sp_tsqr(int64_t rows, int64_t cols, const double* X, int64_t ldx,
 int sp_qr_tall(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq,
                double* R, int64_t ldr, int32_t well_conditioned, void* stream);
 
+/* CholeskyQR2 without a host synchronisation: a Cholesky breakdown ORs 1
+ * into the device int *dflag (caller zeroes it and reads it later, redoing
+ * the factorisation with sp_tsqr if it is set).  cols <= 112. */
+int sp_cholqr2_async(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq,
+                     double* R, int64_t ldr, int32_t* dflag, void* stream);
+
 /* thin_qr (src/kernels.py:74-84): reduced QR of any rows x cols matrix with
  * the reference sign convention (src/kernels.py:52-71).  Q is rows x p,
  * R is p x cols with p = min(rows, cols).  Requires p <= 256. */
@@ -154,6 +160,14 @@ int sp_scale_columns(int64_t rows, int64_t cols, double* X, int64_t ldx, const d
  * fine skeleton rows of the two-pass IDs (_gather_rows, src/rowid.py:82-95). */
 int sp_gather_rows(const void* X, int32_t x_dtype, int64_t ldx, int64_t cols,
                    const int64_t* idx, int64_t k, double* out, int64_t ldo, void* stream);
+
+/* X (rows x cols, ld ldx) = rows [row_offset, row_offset + rows) of the
+ * seed's uniform(-1, 1) test block (counter-based hash of the global index
+ * row * cols + col): the random range-finder block of the sketch basis, so
+ * a rank owning a slab of the coarse columns generates exactly its rows
+ * (column-sharded power_svd). */
+int sp_fill_uniform(int64_t rows, int64_t cols, double* X, int64_t ldx, uint64_t seed,
+                    int64_t row_offset, void* stream);
 
 /* ---------------------------------------------------------------- K6 -----
  * pinv_apply (src/kernels.py:158-168): out = 1/s where s > tol * s[0], else 0. */

@@ -44,12 +44,14 @@ SIGNATURES = {
     "sp_gemm": [_I32, _I32, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64, _P],
     "sp_tsqr": [_I64, _I64, _P, _I64, _P, _I64, _P, _I64, _P],
     "sp_qr_tall": [_I64, _I64, _P, _I64, _P, _I64, _P, _I64, _I32, _P],
+    "sp_cholqr2_async": [_I64, _I64, _P, _I64, _P, _I64, _P, _I64, _P, _P],
     "sp_thin_qr": [_I64, _I64, _P, _I64, _P, _I64, _P, _I64, _P],
     "sp_jacobi_svd": [_I64, _P, _I64, _P, _I64, _P, _P, _I64, _P],
     "sp_thin_svd": [_I64, _I64, _P, _I64, _P, _I64, _P, _P, _I64, _P],
     "sp_thin_svd_t": [_I64, _I64, _P, _I64, _P, _I64, _P, _P, _I64, _P],
     "sp_scale_columns": [_I64, _I64, _P, _I64, _P, _I32, _P],
     "sp_gather_rows": [_P, _I32, _I64, _I64, _P, _I64, _P, _I64, _P],
+    "sp_fill_uniform": [_I64, _I64, _P, _I64, ctypes.c_uint64, _I64, _P],
     "sp_pinv_apply": [_P, _I64, _D, _P, _P],
     "sp_trsm_upper": [_I64, _P, _I64, _I64, _P, _I64, _P, _I64, _P],
     "sp_pivoted_qr": [_I64, _I64, _P, _I64, _I32, _P, _P, _I64, _P, _I64, _P],

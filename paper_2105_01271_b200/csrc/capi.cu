@@ -77,6 +77,11 @@ int sp_qr_tall(int64_t rows, int64_t cols, const double* X, int64_t ldx, double*
   return qr_tall(rows, cols, X, ldx, Q, ldq, R, ldr, well_conditioned != 0, ST(stream));
 }
 
+int sp_cholqr2_async(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq, double* R,
+                     int64_t ldr, int32_t* dflag, void* stream) {
+  return cholqr2_async(rows, cols, X, ldx, Q, ldq, R, ldr, dflag, ST(stream));
+}
+
 int sp_thin_qr(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq,
                double* R, int64_t ldr, void* stream) {
   return thin_qr(rows, cols, X, ldx, Q, ldq, R, ldr, ST(stream));
@@ -105,6 +110,11 @@ int sp_scale_columns(int64_t rows, int64_t cols, double* X, int64_t ldx, const d
 int sp_gather_rows(const void* X, int32_t x_dtype, int64_t ldx, int64_t cols, const int64_t* idx, int64_t k,
                    double* out, int64_t ldo, void* stream) {
   return gather_rows(X, x_dtype, ldx, cols, idx, k, out, ldo, ST(stream));
+}
+
+int sp_fill_uniform(int64_t rows, int64_t cols, double* X, int64_t ldx, uint64_t seed, int64_t row_offset,
+                    void* stream) {
+  return fill_uniform(rows, cols, X, ldx, seed, ST(stream), row_offset);
 }
 
 int sp_pinv_apply(const double* s, int64_t count, double tol, double* out, void* stream) {

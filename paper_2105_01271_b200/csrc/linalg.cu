@@ -55,15 +55,20 @@ int copy2d(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Y, 
   return SP_OK;
 }
 
-__global__ void fill_uniform_kernel(int64_t rows, int64_t cols, double* X, int64_t ldx, uint64_t seed) {
+// X = rows [row_offset, row_offset + rows) of the seed's (.. x cols) uniform
+// block: a rank holding a slab of a globally indexed random test block
+// generates exactly its rows.
+__global__ void fill_uniform_kernel(int64_t rows, int64_t cols, double* X, int64_t ldx, uint64_t seed,
+                                    int64_t row_offset) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= rows * cols) return;
-  X[(e / cols) * ldx + (e % cols)] = hash_uniform(seed, (uint64_t)e);
+  X[(e / cols) * ldx + (e % cols)] = hash_uniform(seed, (uint64_t)(e + row_offset * cols));
 }
 
-int fill_uniform(int64_t rows, int64_t cols, double* X, int64_t ldx, uint64_t seed, cudaStream_t s) {
+int fill_uniform(int64_t rows, int64_t cols, double* X, int64_t ldx, uint64_t seed, cudaStream_t s,
+                 int64_t row_offset) {
   if (rows == 0 || cols == 0) return SP_OK;
-  fill_uniform_kernel<<<ceil_div(rows * cols, 256), 256, 0, s>>>(rows, cols, X, ldx, seed);
+  fill_uniform_kernel<<<ceil_div(rows * cols, 256), 256, 0, s>>>(rows, cols, X, ldx, seed, row_offset);
   SPB_LAUNCHED();
   return SP_OK;
 }

@@ -44,7 +44,8 @@ int transpose(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* 
               cudaStream_t s);
 int copy2d(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Y, int64_t ldy,
            cudaStream_t s);
-int fill_uniform(int64_t rows, int64_t cols, double* X, int64_t ldx, uint64_t seed, cudaStream_t s);
+int fill_uniform(int64_t rows, int64_t cols, double* X, int64_t ldx, uint64_t seed, cudaStream_t s,
+                 int64_t row_offset = 0);
 int householder_complete(int64_t N, int r, int k, double* out, int64_t ldo, cudaStream_t s,
                          double* kp_out = nullptr);
 int fill_identity(int k, double* out, int64_t ldo, cudaStream_t s);

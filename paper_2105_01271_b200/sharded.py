@@ -56,6 +56,13 @@ class TorchComm:
         self.dist.all_gather(parts, pad, group=self.group)
         return ops.cat_cols([p[:, :w] for p, w in zip(parts, ws)])
 
+    def allreduce_sum(self, x, ops):
+        if self.world == 1:
+            return x
+        x = ops.contig(x)
+        self.dist.all_reduce(x, group=self.group)
+        return x
+
     def allgather_rows(self, x, ops):
         if self.world == 1:
             return x
@@ -71,6 +78,81 @@ class TorchComm:
         return x
 
 
+SEED0 = 0x5EED5EED      # the range-finder seed of the device svd_top (csrc/pipeline.cu)
+KEEP_TOL = 1e-12        # src/kernels.py:19
+
+
+def _count_kept(hs, power):
+    if hs.size == 0 or not hs[0] > 0:
+        return 0
+    return int(np.count_nonzero((hs / hs[0]) ** power > KEEP_TOL))
+
+
+def distributed_sketch_basis(c_i, row0: int, ncols: int, power: float, comm, ops):
+    """Kept left basis U_{C,r} of the column-sharded sketch C = [C_1 .. C_P]
+    without gathering C: the randomized block subspace iteration of the device
+    svd_top (csrc/pipeline.cu) with the exchanges confined to m x b and b x b
+    blocks.
+
+      Y   = sum_i C_i Omega_i          (allreduce, m x b; Omega_i = rows
+                                        row0.. of the global test block)
+      Q   = TSQR(Y)                    (replicated, bit-identical)
+      Z_i = C_i^T Q = P_i R_i          (local TSQR leaf)
+      R   = QR([R_1; ...; R_P])        (allgather of b x b factors)
+      R^T = U_s S V_s^T  (Jacobi)      U_C = Q U_s
+
+    Same block size, growth and stopping rules as the single-GPU svd_top, so
+    world size 1 reproduces it.  Returns (U m x r, sigma (host), r)."""
+    m, nci = c_i.shape
+    p = min(m, ncols)
+    if p <= 64:  # exact path of svd_top: gather the (small) sketch
+        c_all = comm.allgather_cols(c_i, ops)
+        return ops.sketch_basis(c_all, power)
+    cap = min(p, 256)
+    b = min(cap, ((max(32, 1 + 16) + 7) // 8) * 8)
+    while True:
+        om = ops.fill_uniform(nci, b, SEED0 + b, row0)
+        y = comm.allreduce_sum(ops.matmul(c_i, om), ops)
+        qy, _ = ops.tsqr(y)
+        prev, kept_prev, grow = None, -1, False
+        for itn in range(24):
+            z = ops.matmul_tn(c_i, qy)                                  # n_c_i x b
+            zp = ops.pad_rows(z, b)                                     # TSQR needs rows >= b
+            pz, rz = ops.tsqr(zp)
+            if comm.world > 1:
+                r_stack = comm.allgather_rows(rz, ops)
+                q_top, r_all = ops.tsqr(r_stack)
+            else:
+                q_top, r_all = None, rz
+            us, sg = ops.svd_small_t(r_all)                             # R^T = U_s S V_s^T
+            hs = ops.to_numpy(sg)
+            kept = _count_kept(hs, power)
+            if kept + 8 > b and b < cap:
+                grow = True
+                break
+            conv = itn == 0 and kept > 0 and b - 8 > kept and hs[b - 8] <= 1e-8 * hs[kept - 1]
+            if (not conv and itn >= 1 and kept == kept_prev and kept > 0 and b - 8 > kept
+                    and (hs[b - 8] / hs[kept - 1]) ** (2.0 * itn + 2.0) <= 1e-16):
+                conv = True
+            if not conv and itn >= 1 and kept == kept_prev:
+                chk = min(b, kept + 1)
+                conv = bool(np.all(np.abs(hs[:chk] - prev[:chk]) <= 1e-14 * hs[0] + 1e-12 * hs[:chk]))
+            if conv:
+                break
+            prev, kept_prev = hs, kept
+            # one more subspace iteration: Y = C P, P_i = P_Z,i Q_top,i
+            p_i = (ops.rows(pz, 0, nci) if q_top is None else
+                   ops.matmul(ops.rows(pz, 0, nci), ops.rows(q_top, comm.rank * b, (comm.rank + 1) * b)))
+            y = comm.allreduce_sum(ops.matmul(c_i, p_i), ops)
+            qy, _ = ops.tsqr(y)
+        if grow:
+            b = min(cap, 2 * b)
+            continue
+        r = kept
+        u = ops.matmul(qy, ops.cols(us, 0, max(r, 1)))
+        return ops.cols(u, 0, r), hs[:r], r
+
+
 def sharded_power_svd(a_local, c_begin: int, cols, k: int, q: int, comm, ops):
     """Rank-local part of the column-sharded single-pass power SVD.
 
@@ -82,9 +164,9 @@ def sharded_power_svd(a_local, c_begin: int, cols, k: int, q: int, comm, ops):
     m, n_i = a_local.shape
     sel = (cols >= c_begin) & (cols < c_begin + n_i)
     c_i = ops.gather(a_local, cols[sel] - c_begin)
-    c_all = comm.allgather_cols(c_i, ops)
     ncols = cols.size
-    z, s_c, r = ops.sketch_basis(c_all, 2.0 * q + 1.0)
+    row0 = int(np.count_nonzero(cols < c_begin))  # this rank's first coarse column (global index)
+    z, s_c, r = distributed_sketch_basis(c_i, row0, ncols, 2.0 * q + 1.0, comm, ops)
     r_use = max(r, 0)
     u = ops.zeros((m, k))
     v = ops.zeros((n_i, k))
@@ -93,16 +175,30 @@ def sharded_power_svd(a_local, c_begin: int, cols, k: int, q: int, comm, ops):
     if r_use > 0:
         y_i = ops.atz(a_local, z)                                   # n_i x r (the A pass)
         kappa = s_c[0] / s_c[r_use - 1] if s_c[r_use - 1] > 0 else np.inf
-        q_i, r_i = ops.qr(y_i, well_conditioned=kappa < 1e6)        # local TSQR leaf
-        r_stack = comm.allgather_rows(r_i, ops)                     # (P r) x r
-        q_top, r_y = ops.qr(r_stack, well_conditioned=False)
-        q_y = ops.matmul(q_i, ops.rows(q_top, comm.rank * r_use, (comm.rank + 1) * r_use))
-        # SVD of R_y^T via that of R_y: R_y = A S B^T  =>  R_y^T = B S A^T
-        a_, s_core, b_ = ops.svd_small(r_y)
-        uf = ops.matmul(z, b_)                                      # U = Z u~,  u~ = B
-        vf = ops.matmul(q_y, a_)                                    # V = Q_Y v~, v~ = A
-        u = ops.set_cols(u, ops.cols(uf, 0, kk), 0)
-        v = ops.set_cols(v, ops.cols(vf, 0, kk), 0)
+        # local QR leaf: CholeskyQR2 without a host sync when the kept spectrum
+        # is narrow (breakdown is checked once, with the result's copy-back)
+        flag = ops.new_flag() if kappa < 1e6 else None
+        while True:
+            q_i, r_i = ops.qr_async(y_i, flag) if flag is not None else ops.tsqr(y_i)
+            if comm.world > 1:
+                r_stack = comm.allgather_rows(r_i, ops)             # (P r) x r
+                q_top, r_y = ops.tsqr(r_stack)
+                q_y = ops.matmul(q_i, ops.rows(q_top, comm.rank * r_use, (comm.rank + 1) * r_use))
+            else:
+                q_y, r_y = q_i, r_i
+            # SVD of R_y^T via that of R_y: R_y = A S B^T  =>  R_y^T = B S A^T
+            a_, s_core, b_ = ops.svd_small(r_y)
+            uf = ops.matmul(z, b_)                                  # U = Z u~,  u~ = B
+            vf = ops.matmul(q_y, a_)                                # V = Q_Y v~, v~ = A
+            u = ops.set_cols(u, ops.cols(uf, 0, kk), 0)
+            v = ops.set_cols(v, ops.cols(vf, 0, kk), 0)
+            if flag is None:
+                break
+            # a breakdown on ANY rank redoes the leaf with Householder on all ranks
+            bad = comm.allreduce_sum(ops.flag_value(flag), ops)
+            if not ops.to_numpy(bad).any():
+                break
+            flag = None
         s[:kk] = ops.to_numpy(s_core)[:kk]
     if kk < k:
         u = ops.complete(u, kk, k)
@@ -172,6 +268,62 @@ class DeviceOps:
             _lib.call("sp_apply_stencil", a.data_ptr(), tag, a.shape[0], a.shape[1], a.stride(0), d_idx.data_ptr(),
                       None, 1, n_c, 1, out.data_ptr(), n_c, self._s())
         return out
+
+    def pad_rows(self, x, r):
+        if x.shape[0] >= r:
+            return x
+        out = self.zeros((r, x.shape[1]))
+        out[:x.shape[0]] = x
+        return out
+
+    def fill_uniform(self, rows, cols, seed, row0):
+        out = self.t.empty((max(rows, 1), cols), dtype=self.t.float64, device=self.tensor_device)[:rows]
+        if rows:
+            _lib.call("sp_fill_uniform", rows, cols, out.data_ptr(), cols, int(seed), int(row0), self._s())
+        return out
+
+    def matmul_tn(self, a, b):
+        """a^T b"""
+        kdim, m = a.shape
+        n = b.shape[1]
+        out = self.t.empty((m, n), dtype=self.t.float64, device=self.tensor_device)
+        if kdim == 0:
+            return out.zero_()
+        _lib.call("sp_gemm", 1, 0, m, n, kdim, 1.0, a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), 0.0,
+                  out.data_ptr(), n, self._s())
+        return out
+
+    def new_flag(self):
+        return self.t.zeros((1,), dtype=self.t.int32, device=self.tensor_device)
+
+    def flag_value(self, flag):
+        return flag.double()
+
+    def qr_async(self, x, flag):
+        rows, c = x.shape
+        qm = self.t.empty((rows, c), dtype=self.t.float64, device=self.tensor_device)
+        rm = self.t.empty((c, c), dtype=self.t.float64, device=self.tensor_device)
+        x = x.contiguous()
+        _lib.call("sp_cholqr2_async", rows, c, x.data_ptr(), c, qm.data_ptr(), c, rm.data_ptr(), c, flag.data_ptr(),
+                  self._s())
+        return qm, rm
+
+    def tsqr(self, x):
+        rows, c = x.shape
+        qm = self.t.empty((rows, c), dtype=self.t.float64, device=self.tensor_device)
+        rm = self.t.empty((c, c), dtype=self.t.float64, device=self.tensor_device)
+        x = x.contiguous()
+        _lib.call("sp_tsqr", rows, c, x.data_ptr(), c, qm.data_ptr(), c, rm.data_ptr(), c, self._s())
+        return qm, rm
+
+    def svd_small_t(self, mtx):
+        """U, S of mtx^T (U only: the left vectors of the transpose)."""
+        n = mtx.shape[0]
+        mt = mtx.t().contiguous()
+        u = self.t.empty((n, n), dtype=self.t.float64, device=self.tensor_device)
+        s = self.t.empty((n,), dtype=self.t.float64, device=self.tensor_device)
+        _lib.call("sp_jacobi_svd", n, mt.data_ptr(), n, u.data_ptr(), n, s.data_ptr(), None, n, self._s())
+        return u, s
 
     def sketch_basis(self, c, power):
         m, nc = c.shape

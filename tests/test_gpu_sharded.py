@@ -34,6 +34,13 @@ class ThreadComm:
     def allgather_rows(self, x, ops):
         return ops.cat_rows(self._exchange(ops.contig(x)))
 
+    def allreduce_sum(self, x, ops):
+        parts = self._exchange(ops.contig(x))
+        total = parts[0].clone()
+        for p in parts[1:]:  # rank order: the same bits on every rank
+            total += p
+        return total
+
     def broadcast(self, x, root, ops):
         return self._exchange(x)[root].clone()
 

@@ -63,6 +63,44 @@ class NumpyOps:
     def gather(self, a, idx):
         return self._t(a.numpy()[:, idx])
 
+    def pad_rows(self, x, r):
+        if x.shape[0] >= r:
+            return x
+        out = self.zeros((r, x.shape[1]))
+        out[:x.shape[0]] = x
+        return out
+
+    def fill_uniform(self, rows, cols, seed, row0):
+        # the device counter-based hash (csrc/common.cuh hash_uniform) on the global index
+        with np.errstate(over="ignore"):
+            i = (np.arange(rows * cols, dtype=np.uint64) + np.uint64(row0 * cols))
+            z = (np.uint64(seed) * np.uint64(0x9E3779B97F4A7C15) + i * np.uint64(0xD1B54A32D192ED03)
+                 + np.uint64(0x8CB92BA72F3D8DD7))
+            z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+            z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+            z ^= z >> np.uint64(31)
+        u = (z >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0) * 2.0 - 1.0
+        return self._t(u.reshape(rows, cols))
+
+    def matmul_tn(self, a, b):
+        return self._t(a.numpy().T @ b.numpy())
+
+    def tsqr(self, x):
+        return self.qr(x, False)
+
+    def new_flag(self):
+        return torch.zeros((1,), dtype=torch.float64)
+
+    def flag_value(self, flag):
+        return flag.clone()
+
+    def qr_async(self, x, flag):
+        return self.qr(x, True)
+
+    def svd_small_t(self, m):
+        u, s, _ = np.linalg.svd(m.numpy().T)
+        return self._t(u), self._t(s)
+
     def sketch_basis(self, c, power):
         u, s, _ = np.linalg.svd(c.numpy(), full_matrices=False)
         r = int(np.count_nonzero((s / s[0]) ** power > 1e-12)) if s[0] > 0 else 0
