@@ -45,6 +45,8 @@ def _compile(src: Path) -> Path:
     cmd = [NVCC, *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)]
     if os.environ.get("SPB_PTXAS_V"):
         cmd += ["-Xptxas", "-v"]
+    if os.environ.get("SPB_NVCC_EXTRA"):  # e.g. -DSPB_JACOBI_TRACE for diagnostic builds
+        cmd += os.environ["SPB_NVCC_EXTRA"].split()
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src.name}:\n{res.stderr}")

@@ -231,6 +231,13 @@ jacobi32_kernel(int n, const double* __restrict__ M, int64_t ldm, double* __rest
   }
   __syncthreads();
   const int na = na_s, mypos = pos_s[c];
+  // the circle-method schedule, once: ptab[round][lane] = partner lane or -1
+  __shared__ signed char ptab[31][32];
+  for (int e = threadIdx.x; e < (na - 1) * 32; e += blockDim.x) {
+    const int rd = e >> 5, ln = e & 31, ps = pos_s[ln];
+    ptab[rd][ln] = (signed char)(ps >= 0 ? act[rr_partner(ps, rd, na)] : -1);
+  }
+  __syncthreads();
   double fro2 = 0.0;
   for (int cc = 0; cc < 32; ++cc) fro2 += ((nrm_s[0][cc] + nrm_s[1][cc]) + (nrm_s[2][cc] + nrm_s[3][cc]));
   const double negl = 1e-30 * fro2;
@@ -238,8 +245,7 @@ jacobi32_kernel(int n, const double* __restrict__ M, int64_t ldm, double* __rest
   for (int sweep = 0; sweep < kJacMaxSweeps && na >= 2; ++sweep) {
     int rotated = 0;
     for (int round = 0; round < na - 1; ++round) {
-      int plane = -1;
-      if (mypos >= 0) plane = act[rr_partner(mypos, round, na)];
+      const int plane = ptab[round][c];
       const int src = plane >= 0 ? plane : c;
       double y[8], z[8];
 #pragma unroll
@@ -248,14 +254,16 @@ jacobi32_kernel(int n, const double* __restrict__ M, int64_t ldm, double* __rest
 #pragma unroll
         for (int k = 0; k < 8; ++k) z[k] = __shfl_sync(0xffffffffu, v[k], src);
       }
-      double pa = 0.0, pg = 0.0;
+      double pa0 = x[0] * x[0], pa1 = x[1] * x[1], pg0 = x[0] * y[0], pg1 = x[1] * y[1];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        pa = fma(x[k], x[k], pa);
-        pg = fma(x[k], y[k], pg);
+      for (int k = 2; k < 8; k += 2) {
+        pa0 = fma(x[k], x[k], pa0);
+        pa1 = fma(x[k + 1], x[k + 1], pa1);
+        pg0 = fma(x[k], y[k], pg0);
+        pg1 = fma(x[k + 1], y[k + 1], pg1);
       }
-      part[buf][w][c][0] = pa;
-      part[buf][w][c][1] = pg;
+      part[buf][w][c][0] = pa0 + pa1;
+      part[buf][w][c][1] = pg0 + pg1;
       __syncthreads();
       const double a = (part[buf][0][c][0] + part[buf][1][c][0]) + (part[buf][2][c][0] + part[buf][3][c][0]);
       const double g = (part[buf][0][c][1] + part[buf][1][c][1]) + (part[buf][2][c][1] + part[buf][3][c][1]);
@@ -286,7 +294,12 @@ jacobi32_kernel(int n, const double* __restrict__ M, int64_t ldm, double* __rest
       }
       rotated = 1;
     }
-    if (!__syncthreads_or(rotated)) break;
+    if (!__syncthreads_or(rotated)) {
+#ifdef SPB_JACOBI_TRACE
+      if (threadIdx.x == 0) printf("jacobi32 n=%d na=%d sweeps=%d\n", n, na, sweep + 1);
+#endif
+      break;
+    }
   }
   // singular values = column norms, sorted descending (stable by index)
   double a1 = 0.0;
