@@ -189,6 +189,258 @@ __global__ void pq_update_kernel(int t, int64_t cols, int64_t rows, double* __re
   }
 }
 
+// ------------------------------------------------------ long candidates ----
+// Candidates much longer than their count (the ID of cfg5: 2000 candidates of
+// length 262144): every step's work is spread over row blocks x column
+// chunks with fixed-order partial reductions, instead of one warp (update)
+// or one CTA (select / re-orthogonalisation) per candidate.  Same pivot rule
+// and arithmetic (norms recomputed from the updated columns every step).
+constexpr int kPlRows = 8192;   // rows per block
+constexpr int kPlCols = 16;     // candidates per update CTA
+constexpr int kPlThreads = 256;
+
+__device__ __forceinline__ double pl_block_sum(double v, double* red) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double acc = 0.0;
+#pragma unroll
+  for (int w = 0; w < kPlThreads / 32; ++w) acc += red[w];
+  return acc;
+}
+
+// argmax with the lowest-original-index tie-break, swap of the small state
+// (perm, norms, R columns); the pivot index goes to *jsel
+__global__ void __launch_bounds__(kPqSelThreads)
+pl_select_kernel(int t, int k, int64_t cols, double* norms, int64_t* perm, double* R, int64_t ldr, int64_t* jsel) {
+  __shared__ PqBest bests[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  PqBest b{-1.0, INT64_MAX, -1};
+  for (int64_t j = t + tid; j < cols; j += blockDim.x) {
+    PqBest c{norms[j], perm[j], j};
+    if (pq_better(c, b)) b = c;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    PqBest c{__shfl_xor_sync(0xffffffffu, b.nrm, o), __shfl_xor_sync(0xffffffffu, b.perm, o),
+             __shfl_xor_sync(0xffffffffu, b.j, o)};
+    if (pq_better(c, b)) b = c;
+  }
+  if (lane == 0) bests[warp] = b;
+  __syncthreads();
+  __shared__ int64_t js_s;
+  if (tid == 0) {
+    PqBest bb = bests[0];
+    for (int w = 1; w < nw; ++w)
+      if (pq_better(bests[w], bb)) bb = bests[w];
+    js_s = bb.j;
+    *jsel = bb.j;
+  }
+  __syncthreads();
+  const int64_t js = js_s;
+  if (js == t) return;
+  for (int s2 = tid; s2 < k; s2 += blockDim.x) {
+    const double a = R[(int64_t)s2 * ldr + t];
+    R[(int64_t)s2 * ldr + t] = R[(int64_t)s2 * ldr + js];
+    R[(int64_t)s2 * ldr + js] = a;
+  }
+  if (tid == 0) {
+    const int64_t p = perm[t];
+    perm[t] = perm[js];
+    perm[js] = p;
+    const double nn = norms[t];
+    norms[t] = norms[js];
+    norms[js] = nn;
+  }
+}
+
+// row block rb: swap candidates t <-> *jsel, then partial[rb][s] = q_s . w_t (s < t)
+__global__ void __launch_bounds__(kPlThreads)
+pl_swap_dots_kernel(int t, int64_t rows, double* __restrict__ WK, const double* __restrict__ Qt,
+                    const int64_t* __restrict__ jsel, double* __restrict__ partial) {
+  __shared__ double red[kPlThreads / 32];
+  const int64_t r0 = (int64_t)blockIdx.x * kPlRows, r1 = imin64(rows, r0 + kPlRows);
+  const int64_t js = *jsel;
+  double* wt = WK + (int64_t)t * rows;
+  if (js != t) {
+    double* wj = WK + js * rows;
+    for (int64_t x = r0 + threadIdx.x; x < r1; x += kPlThreads) {
+      const double a = wt[x];
+      wt[x] = wj[x];
+      wj[x] = a;
+    }
+    __syncthreads();
+  }
+  for (int s2 = 0; s2 < t; ++s2) {
+    const double* q = Qt + (int64_t)s2 * rows;
+    double a = 0.0;
+    for (int64_t x = r0 + threadIdx.x; x < r1; x += kPlThreads) a = fma(q[x], wt[x], a);
+    a = pl_block_sum(a, red);
+    if (threadIdx.x == 0) partial[(int64_t)blockIdx.x * kPqMaxK + s2] = a;
+  }
+}
+
+// delta[s] = sum_rb partial[rb][s]; R[s][t] += delta[s]  (one CTA, fixed order)
+__global__ void pl_delta_kernel(int t, int nb, const double* __restrict__ partial, double* __restrict__ delta,
+                                double* __restrict__ R, int64_t ldr) {
+  for (int s2 = threadIdx.x; s2 < t; s2 += blockDim.x) {
+    double a = 0.0;
+    for (int b = 0; b < nb; ++b) a += partial[(int64_t)b * kPqMaxK + s2];
+    delta[s2] = a;
+    R[(int64_t)s2 * ldr + t] += a;
+  }
+}
+
+// v = w_t - sum_s delta_s q_s into Qt row t; part2[rb] = |v_rb|^2
+__global__ void __launch_bounds__(kPlThreads)
+pl_form_v_kernel(int t, int64_t rows, const double* __restrict__ WK, double* __restrict__ Qt,
+                 const double* __restrict__ delta, double* __restrict__ part2) {
+  __shared__ double red[kPlThreads / 32];
+  __shared__ double ds[kPqMaxK];
+  for (int s2 = threadIdx.x; s2 < t; s2 += kPlThreads) ds[s2] = delta[s2];
+  __syncthreads();
+  const int64_t r0 = (int64_t)blockIdx.x * kPlRows, r1 = imin64(rows, r0 + kPlRows);
+  const double* wt = WK + (int64_t)t * rows;
+  double* v = Qt + (int64_t)t * rows;
+  double p = 0.0;
+  for (int64_t x = r0 + threadIdx.x; x < r1; x += kPlThreads) {
+    double acc = 0.0;
+    for (int s2 = 0; s2 < t; ++s2) acc = fma(Qt[(int64_t)s2 * rows + x], ds[s2], acc);
+    const double vv = wt[x] - acc;
+    v[x] = vv;
+    p = fma(vv, vv, p);
+  }
+  p = pl_block_sum(p, red);
+  if (threadIdx.x == 0) part2[blockIdx.x] = p;
+}
+
+// pn = sqrt(sum part2) (fixed order) -> R[t][t], pnv[0]; status 2 on a zero
+// pivot (the caller redoes the factorisation on the per-candidate path,
+// which owns the deterministic filler)
+__global__ void pl_pivot_norm_kernel(int t, int nb, const double* __restrict__ part2, double* __restrict__ pnv,
+                                     double* __restrict__ R, int64_t ldr, int* status) {
+  if (threadIdx.x != 0) return;
+  double a = 0.0;
+  for (int b = 0; b < nb; ++b) a += part2[b];
+  const double pn = sqrt(a);
+  pnv[0] = pn;
+  R[(int64_t)t * ldr + t] = pn;
+  if (pn == 0.0) *status = 2;
+}
+
+__global__ void pl_normalise_kernel(int t, int64_t rows, double* __restrict__ Qt, const double* __restrict__ pnv) {
+  const double pn = pnv[0];
+  if (pn == 0.0) return;
+  double* v = Qt + (int64_t)t * rows;
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < rows; x += (int64_t)gridDim.x * blockDim.x)
+    v[x] = v[x] / pn;
+}
+
+// pc[rb][j] = v_rb . w_j,rb for the CTA's candidate chunk (j > t)
+__global__ void __launch_bounds__(kPlThreads)
+pl_coef_kernel(int t, int64_t cols, int64_t rows, const double* __restrict__ WK, const double* __restrict__ Qt,
+               double* __restrict__ pc) {
+  __shared__ double red[kPlThreads / 32];
+  const int64_t r0 = (int64_t)blockIdx.x * kPlRows, r1 = imin64(rows, r0 + kPlRows);
+  const double* v = Qt + (int64_t)t * rows;
+  const int64_t j0 = t + 1 + (int64_t)blockIdx.y * kPlCols;
+  for (int u = 0; u < kPlCols; ++u) {
+    const int64_t j = j0 + u;
+    if (j >= cols) break;  // uniform
+    const double* w = WK + j * rows;
+    double a = 0.0;
+    for (int64_t x = r0 + threadIdx.x; x < r1; x += kPlThreads) a = fma(v[x], w[x], a);
+    a = pl_block_sum(a, red);
+    if (threadIdx.x == 0) pc[(int64_t)blockIdx.x * cols + j] = a;
+  }
+}
+
+// coef_j = sum_rb pc[rb][j] -> R[t][j], coef[j]
+__global__ void pl_coef_reduce_kernel(int t, int nb, int64_t cols, const double* __restrict__ pc,
+                                      double* __restrict__ coef, double* __restrict__ R, int64_t ldr) {
+  const int64_t j = t + 1 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= cols) return;
+  double a = 0.0;
+  for (int b = 0; b < nb; ++b) a += pc[(int64_t)b * cols + j];
+  coef[j] = a;
+  R[(int64_t)t * ldr + j] = a;
+}
+
+// w_j -= coef_j v on the CTA's rows; pn2[rb][j] = |w_j,rb|^2 (updated)
+__global__ void __launch_bounds__(kPlThreads)
+pl_update_kernel(int t, int64_t cols, int64_t rows, double* __restrict__ WK, const double* __restrict__ Qt,
+                 const double* __restrict__ coef, double* __restrict__ pn2) {
+  __shared__ double red[kPlThreads / 32];
+  const int64_t r0 = (int64_t)blockIdx.x * kPlRows, r1 = imin64(rows, r0 + kPlRows);
+  const double* v = Qt + (int64_t)t * rows;
+  const int64_t j0 = t + 1 + (int64_t)blockIdx.y * kPlCols;
+  for (int u = 0; u < kPlCols; ++u) {
+    const int64_t j = j0 + u;
+    if (j >= cols) break;  // uniform
+    double* w = WK + j * rows;
+    const double c = coef[j];
+    double a = 0.0;
+    for (int64_t x = r0 + threadIdx.x; x < r1; x += kPlThreads) {
+      const double nv = fma(-c, v[x], w[x]);
+      w[x] = nv;
+      a = fma(nv, nv, a);
+    }
+    a = pl_block_sum(a, red);
+    if (threadIdx.x == 0) pn2[(int64_t)blockIdx.x * cols + j] = a;
+  }
+}
+
+__global__ void pl_norms_kernel(int t, int nb, int64_t cols, const double* __restrict__ pn2, double* __restrict__ norms) {
+  const int64_t j = t + 1 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= cols) return;
+  double a = 0.0;
+  for (int b = 0; b < nb; ++b) a += pn2[(int64_t)b * cols + j];
+  norms[j] = sqrt(a);
+}
+
+// the long-candidate factorisation loop; *fallback = true on a zero pivot
+static int pivoted_qr_long(int64_t rows, int64_t cols, int k, double* WK, double* norms, int64_t* perm, double* Qt,
+                           double* R, int64_t ldr, bool* fallback, cudaStream_t s) {
+  *fallback = false;
+  const int nb = ceil_div(rows, kPlRows);
+  Arena ar(s);
+  SPB_ALLOC(ar, double, partial, (size_t)nb * kPqMaxK);
+  SPB_ALLOC(ar, double, part2, (size_t)nb);
+  SPB_ALLOC(ar, double, pc, (size_t)nb * cols);
+  SPB_ALLOC(ar, double, coef, (size_t)cols);
+  SPB_ALLOC(ar, double, delta, (size_t)kPqMaxK);
+  SPB_ALLOC(ar, double, pnv, 1);
+  SPB_ALLOC(ar, int64_t, jsel, 1);
+  SPB_ALLOC(ar, int, status, 1);
+  SPB_CUDA(cudaMemsetAsync(status, 0, sizeof(int), s));
+  for (int t = 0; t < k; ++t) {
+    pl_select_kernel<<<1, kPqSelThreads, 0, s>>>(t, k, cols, norms, perm, R, ldr, jsel);
+    pl_swap_dots_kernel<<<nb, kPlThreads, 0, s>>>(t, rows, WK, Qt, jsel, partial);
+    if (t > 0) pl_delta_kernel<<<1, 128, 0, s>>>(t, nb, partial, delta, R, ldr);
+    pl_form_v_kernel<<<nb, kPlThreads, 0, s>>>(t, rows, WK, Qt, delta, part2);
+    pl_pivot_norm_kernel<<<1, 32, 0, s>>>(t, nb, part2, pnv, R, ldr, status);
+    pl_normalise_kernel<<<std::min<int64_t>(4 * kNumSMs, ceil_div(rows, 256)), 256, 0, s>>>(t, rows, Qt, pnv);
+    count_launch(t > 0 ? 6 : 5);
+    const int64_t trail = cols - t - 1;
+    if (trail > 0) {
+      dim3 g(nb, ceil_div(trail, kPlCols));
+      pl_coef_kernel<<<g, kPlThreads, 0, s>>>(t, cols, rows, WK, Qt, pc);
+      pl_coef_reduce_kernel<<<ceil_div(trail, 256), 256, 0, s>>>(t, nb, cols, pc, coef, R, ldr);
+      pl_update_kernel<<<g, kPlThreads, 0, s>>>(t, cols, rows, WK, Qt, coef, pc);
+      pl_norms_kernel<<<ceil_div(trail, 256), 256, 0, s>>>(t, nb, cols, pc, norms);
+      count_launch(4);
+    }
+    SPB_CHECK_LAUNCH();
+  }
+  int hst = 0;
+  SPB_CUDA(cudaMemcpyAsync(&hst, status, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SPB_CUDA(cudaStreamSynchronize(s));
+  *fallback = hst != 0;
+  return SP_OK;
+}
+
 int pivoted_qr(int64_t rows, int64_t cols, const double* Mt, int64_t ldmt, int k, int64_t* perm,
                double* Q, int64_t ldq, double* R, int64_t ldr, cudaStream_t s) {
   SPB_REQUIRE(k >= 1 && k <= std::min(rows, cols),
@@ -206,7 +458,19 @@ int pivoted_qr(int64_t rows, int64_t cols, const double* Mt, int64_t ldmt, int k
   pq_init_kernel<<<ceil_div(cols * 32, 256), 256, 0, s>>>(cols, rows, Mt, ldmt, WK, norms, perm);
   count_launch();
   SPB_CHECK_LAUNCH();
-  for (int t = 0; t < k; ++t) {
+  bool done = false;
+  if (rows >= 4 * kPlRows && rows >= 8 * cols) {
+    bool fb = false;
+    SPB_TRY(pivoted_qr_long(rows, cols, k, WK, norms, perm, Qt, R, ldr, &fb, s));
+    done = !fb;
+    if (fb) {  // zero pivot: restart on the per-candidate path (deterministic filler)
+      SPB_CUDA(cudaMemset2DAsync(R, ldr * sizeof(double), 0, cols * sizeof(double), k, s));
+      pq_init_kernel<<<ceil_div(cols * 32, 256), 256, 0, s>>>(cols, rows, Mt, ldmt, WK, norms, perm);
+      count_launch();
+      SPB_CHECK_LAUNCH();
+    }
+  }
+  for (int t = 0; t < k && !done; ++t) {
     pq_select_kernel<<<1, kPqSelThreads, 0, s>>>(t, k, cols, rows, WK, norms, perm, Qt, R, ldr, status);
     count_launch();
     SPB_CHECK_LAUNCH();

@@ -277,7 +277,8 @@ def test_pivoted_qr_duplicate_columns_tie_break(cuda):
     assert fac.perm[0] == 2 and fac.perm[1] == 0
 
 
-@pytest.mark.parametrize("rows,cols,k", [(64, 300, 40), (200, 1000, 100), (9, 6, 6)])
+@pytest.mark.parametrize("rows,cols,k", [(64, 300, 40), (200, 1000, 100), (9, 6, 6),
+                                        (40000, 300, 60), (70000, 64, 64)])
 def test_pivoted_qr_matches_oracle_pivots(cuda, rows, cols, k):
     m = philox(rows * cols).standard_normal((rows, cols)) * np.logspace(0, -2, cols)
     f = sp.pivoted_qr(m, k)
@@ -286,6 +287,18 @@ def test_pivoted_qr_matches_oracle_pivots(cuda, rows, cols, k):
     pstar = k if np.all(gaps > 1e-11) else int(np.argmax(gaps <= 1e-11))
     assert np.array_equal(f.perm[:pstar], perm_o[:pstar])
     np.testing.assert_allclose(f.q @ f.r, m[:, f.perm], atol=1e-10 * np.linalg.norm(m)) if k == min(rows, cols) else None
+
+
+def test_pivoted_qr_long_candidates_rank_deficient(cuda):
+    """Long candidates (the row-block path) with an exact zero residual:
+    falls back to the per-candidate path and its deterministic filler."""
+    rng = philox(77)
+    base = rng.standard_normal((40000, 3))
+    m = np.column_stack([base, base @ rng.standard_normal((3, 5))])  # rank 3, 8 candidates
+    f = sp.pivoted_qr(m, 6)
+    np.testing.assert_allclose(f.q.T @ f.q, np.eye(6), atol=1e-12)
+    q_o, r_o, perm_o = oracle.greedy_pivoted_qr(m, 6)
+    assert np.array_equal(f.perm[:3], perm_o[:3])
 
 
 def test_row_id_golden(cuda):
