@@ -11,6 +11,8 @@
 // each thread owns 16 bytes of columns (2 x f64 or 4 x f32) and keeps its
 // V x R FP64 accumulator in registers; the Z row is a shared-memory broadcast.
 // Bytes in flight per SM = 4 stages x 32 KB, independent of register pressure.
+#include <cstdlib>
+
 #include "async.cuh"
 #include "common.cuh"
 #include "launch_count.cuh"
@@ -34,7 +36,7 @@ struct TmaLayout {
 template <int R, typename TA>
 __global__ void __launch_bounds__(kTmaThreads, 1)
 skinny_tma_kernel(const TA* __restrict__ A, int64_t m, int64_t n, int64_t lda, const double* __restrict__ Zc,
-                  double* __restrict__ Y, int64_t ldy) {
+                  double* __restrict__ Y, int64_t ldy, int splits) {
   constexpr int V = 16 / sizeof(TA);
   constexpr int TC = kTmaConsumers * V;  // columns per tile
   using L = TmaLayout<R>;
@@ -43,10 +45,16 @@ skinny_tma_kernel(const TA* __restrict__ A, int64_t m, int64_t n, int64_t lda, c
   __shared__ __align__(8) uint64_t empty[kTmaStages];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  // contiguous, 16-byte aligned column slab of this CTA
+  // contiguous, 16-byte aligned column slab of this CTA; with splits > 1 the
+  // rows are also divided (CTA b: row part b % splits of slab b / splits) and
+  // each part writes its own partial Y (summed by skinny_split_reduce)
   const int64_t units = n / V;  // n % V == 0 is a launch precondition
-  const int64_t cb = (units * blockIdx.x / gridDim.x) * V;
-  const int64_t ce = (units * (blockIdx.x + 1) / gridDim.x) * V;
+  const int nslab = gridDim.x / splits, sl = blockIdx.x / splits, part = blockIdx.x % splits;
+  const int64_t cb = (units * sl / nslab) * V;
+  const int64_t ce = (units * (sl + 1) / nslab) * V;
+  const int64_t rb = (m * part / splits) / kTmaRows * kTmaRows;
+  const int64_t re = part + 1 == splits ? m : (m * (part + 1) / splits) / kTmaRows * kTmaRows;
+  if (splits > 1) Y += (int64_t)part * n * ldy;
 
   if (tid == 0) {
     for (int s = 0; s < kTmaStages; ++s) {
@@ -64,8 +72,8 @@ skinny_tma_kernel(const TA* __restrict__ A, int64_t m, int64_t n, int64_t lda, c
       uint32_t ph = 0;
       for (int64_t c0 = cb; c0 < ce; c0 += TC) {
         const uint32_t seg = (uint32_t)(imin64(TC, ce - c0) * sizeof(TA));
-        for (int64_t r0 = 0; r0 < m; r0 += kTmaRows) {
-          const int nr = (int)imin64(kTmaRows, m - r0);
+        for (int64_t r0 = rb; r0 < re; r0 += kTmaRows) {
+          const int nr = (int)imin64(kTmaRows, re - r0);
           unsigned char* sb = smem + stage * L::kStageBytes;
           mbar_wait(&empty[stage], ph ^ 1);
           const uint32_t zbytes = (uint32_t)(nr * R * 8);
@@ -93,8 +101,8 @@ skinny_tma_kernel(const TA* __restrict__ A, int64_t m, int64_t n, int64_t lda, c
     for (int v = 0; v < V; ++v)
 #pragma unroll
       for (int c = 0; c < R; ++c) acc[v][c] = 0.0;
-    for (int64_t r0 = 0; r0 < m; r0 += kTmaRows) {
-      const int nr = (int)imin64(kTmaRows, m - r0);
+    for (int64_t r0 = rb; r0 < re; r0 += kTmaRows) {
+      const int nr = (int)imin64(kTmaRows, re - r0);
       const unsigned char* sb = smem + stage * L::kStageBytes;
       const double* zs = reinterpret_cast<const double*>(sb + kTmaRows * kTmaRowBytes);
       mbar_wait(&full[stage], ph);
@@ -148,6 +156,16 @@ skinny_tma_kernel(const TA* __restrict__ A, int64_t m, int64_t n, int64_t lda, c
   }
 }
 
+// Y = sum_p Ypart[p] (fixed order)
+__global__ void skinny_split_reduce(int splits, int64_t count, const double* __restrict__ part,
+                                    double* __restrict__ Y) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= count) return;
+  double a = part[e];
+  for (int p = 1; p < splits; ++p) a += part[(int64_t)p * count + e];
+  Y[e] = a;
+}
+
 template <int R, typename TA>
 int skinny_tma_launch(const TA* A, int64_t m, int64_t n, int64_t lda, const double* Zc, double* Y, int64_t ldy,
                       cudaStream_t s) {
@@ -155,10 +173,32 @@ int skinny_tma_launch(const TA* A, int64_t m, int64_t n, int64_t lda, const doub
   constexpr int V = 16 / sizeof(TA);
   SPB_CUDA(cudaFuncSetAttribute(skinny_tma_kernel<R, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmem));
   const int64_t units = n / V;
-  const int grid = (int)std::min<int64_t>(kNumSMs, std::max<int64_t>(1, units / 16));
-  skinny_tma_kernel<R, TA><<<grid, kTmaThreads, L::kSmem, s>>>(A, m, n, lda, Zc, Y, ldy);
+  // Row splitting (CTA = row part x column slab, partial Y + one reduction)
+  // lengthens each CTA's row segments; measured slower than full-height slabs
+  // at cfg2 (209 / 219 us for 2 / 4 parts vs 191 us), so it is off unless
+  // SPB_K2_SPLIT asks for it (experiments only).
+  int splits = 1;
+  if (const char* e = getenv("SPB_K2_SPLIT")) splits = std::max(1, std::min(8, atoi(e)));
+  if (ldy != R || m < (int64_t)2 * kTmaRows * splits) splits = 1;
+  while (splits > 1 && units / 16 < (kNumSMs / splits)) --splits;
+  int grid = (int)std::min<int64_t>(kNumSMs / splits, std::max<int64_t>(1, units / 16)) * splits;
+  Arena ar(s);
+  double* out = Y;
+  if (splits > 1) {
+    out = ar.alloc<double>((size_t)splits * n * R);
+    if (!out) {
+      set_error("skinny split workspace allocation failed");
+      return SP_ECUDA;
+    }
+  }
+  skinny_tma_kernel<R, TA><<<grid, kTmaThreads, L::kSmem, s>>>(A, m, n, lda, Zc, out, splits > 1 ? R : ldy, splits);
   count_launch();
   SPB_CHECK_LAUNCH();
+  if (splits > 1) {
+    skinny_split_reduce<<<ceil_div(n * R, 256), 256, 0, s>>>(splits, n * R, out, Y);
+    count_launch();
+    SPB_CHECK_LAUNCH();
+  }
   return SP_OK;
 }
 
