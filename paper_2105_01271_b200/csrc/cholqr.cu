@@ -152,47 +152,48 @@ chol_small_kernel(int c, int nb, const double* __restrict__ P, double* __restric
     }
     __syncthreads();
   }
-  // right-looking Cholesky, one warp-synchronous step per column
-  __shared__ int bad;
-  if (tid == 0) bad = 0;
-  __syncthreads();
+  // the factorisation of the c x c core: warp 0 alone, warp-synchronous
+  // (no block barriers on the critical path; the other warps are done)
+  if (tid >= 32) return;
+  const int lane = tid;
+  bool bad = false;
   for (int j = 0; j < c; ++j) {
     const double d = G[j][j];
-    if (!(d > 0.0)) {
-      if (tid == 0) bad = 1;
+    if (!(d > 0.0)) {  // uniform: every lane reads the same d
+      bad = true;
       break;
     }
     const double dinv = 1.0 / d;
-    for (int e = tid; e < (c - j - 1) * (c - j - 1); e += kCsThreads) {
-      const int i = j + 1 + e / (c - j - 1), l = j + 1 + e % (c - j - 1);
+    const int w2 = c - j - 1;
+    for (int e = lane; e < w2 * w2; e += 32) {
+      const int i = j + 1 + e / w2, l = j + 1 + e % w2;
       if (l >= i) G[i][l] = fma(-G[j][i] * dinv, G[j][l], G[i][l]);
     }
-    __syncthreads();
+    __syncwarp();
   }
-  __syncthreads();
   if (bad) {
-    if (tid == 0) atomicOr(flag, 1);
+    if (lane == 0) atomicOr(flag, 1);
     return;
   }
   __shared__ double dsq[32];
-  if (tid < c) dsq[tid] = sqrt(G[tid][tid]);
-  __syncthreads();
-  for (int e = tid; e < nout; e += kCsThreads) {
+  if (lane < c) dsq[lane] = sqrt(G[lane][lane]);
+  __syncwarp();
+  for (int e = lane; e < nout; e += 32) {
     const int i = e / c, l = e % c;
     G[i][l] = (l > i) ? G[i][l] / dsq[i] : (l == i ? dsq[i] : 0.0);
   }
-  __syncthreads();
-  // R^{-1}: column l solved by thread l (back substitution, c <= 32)
-  if (tid < c) {
-    const int l = tid;
+  __syncwarp();
+  // R^{-1}: column l solved by lane l (back substitution, c <= 32)
+  if (lane < c) {
+    const int l = lane;
     for (int i = c - 1; i >= 0; --i) {
       double acc = (i == l) ? 1.0 : 0.0;
       for (int q = i + 1; q <= l; ++q) acc = fma(-G[i][q], Ri[q][l], acc);
       Ri[i][l] = (i <= l) ? acc / G[i][i] : 0.0;
     }
   }
-  __syncthreads();
-  for (int e = tid; e < nout; e += kCsThreads) {
+  __syncwarp();
+  for (int e = lane; e < nout; e += 32) {
     const int i = e / c, l = e % c;
     R[e] = G[i][l];
     Rinv[e] = Ri[i][l];

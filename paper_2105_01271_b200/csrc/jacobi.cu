@@ -187,34 +187,45 @@ __device__ __forceinline__ int rr_partner(int x, int r, int na) {
   return y == x ? 0 : y;
 }
 
-__global__ void __launch_bounds__(kJ32Warps * 32)
+// fixed-order sum of the NW warp partials of lane c
+template <int NW>
+__device__ __forceinline__ double jsum(const double (*p)[32], int c) {
+  if constexpr (NW == 1) return p[0][c];
+  if constexpr (NW == 2) return p[0][c] + p[1][c];
+  return (p[0][c] + p[1][c]) + (p[2][c] + p[3][c]);
+}
+
+// NW warps x RPW rows (NW * RPW >= n); NW = 1 needs no block barrier in the
+// rounds (the n <= 8 cores of the finish stage)
+template <int NW, int RPW>
+__global__ void __launch_bounds__(NW * 32)
 jacobi32_kernel(int n, const double* __restrict__ M, int64_t ldm, double* __restrict__ U, int64_t ldu,
                 double* __restrict__ S, double* __restrict__ Vout, int64_t ldv, bool trans) {
-  __shared__ double part[2][kJ32Warps][32][2];
-  __shared__ double nrm_s[kJ32Warps][32];
+  __shared__ double part[2][NW][32][2];
+  __shared__ double nrm_s[NW][32];
   __shared__ double sig_s[32];
   __shared__ int act[32], pos_s[32];
   __shared__ int na_s;
   const int w = threadIdx.x >> 5, c = threadIdx.x & 31;
   const bool want_v = Vout != nullptr;
-  double x[8], v[8];
+  double x[RPW], v[RPW];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int i = w * 8 + k;
+  for (int k = 0; k < RPW; ++k) {
+    const int i = w * RPW + k;
     x[k] = (i < n && c < n) ? (trans ? M[(int64_t)c * ldm + i] : M[(int64_t)i * ldm + c]) : 0.0;
     v[k] = (i == c) ? 1.0 : 0.0;
   }
   // column norms and ||M||_F^2 (fixed order)
   double a0 = 0.0;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) a0 = fma(x[k], x[k], a0);
+  for (int k = 0; k < RPW; ++k) a0 = fma(x[k], x[k], a0);
   nrm_s[w][c] = a0;
   __syncthreads();
   if (threadIdx.x == 0) {
     double fro = 0.0;
     double cn[32];
     for (int cc = 0; cc < 32; ++cc) {
-      cn[cc] = ((nrm_s[0][cc] + nrm_s[1][cc]) + (nrm_s[2][cc] + nrm_s[3][cc]));
+      cn[cc] = jsum<NW>(nrm_s, cc);
       fro += cn[cc];
     }
     // columns below 1e-15 ||M||_F are rounding noise: left out of the schedule
@@ -239,7 +250,7 @@ jacobi32_kernel(int n, const double* __restrict__ M, int64_t ldm, double* __rest
   }
   __syncthreads();
   double fro2 = 0.0;
-  for (int cc = 0; cc < 32; ++cc) fro2 += ((nrm_s[0][cc] + nrm_s[1][cc]) + (nrm_s[2][cc] + nrm_s[3][cc]));
+  for (int cc = 0; cc < 32; ++cc) fro2 += jsum<NW>(nrm_s, cc);
   const double negl = 1e-30 * fro2;
   int buf = 0;
   for (int sweep = 0; sweep < kJacMaxSweeps && na >= 2; ++sweep) {
@@ -247,26 +258,43 @@ jacobi32_kernel(int n, const double* __restrict__ M, int64_t ldm, double* __rest
     for (int round = 0; round < na - 1; ++round) {
       const int plane = ptab[round][c];
       const int src = plane >= 0 ? plane : c;
-      double y[8], z[8];
+      double y[RPW], z[RPW];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) y[k] = __shfl_sync(0xffffffffu, x[k], src);
+      for (int k = 0; k < RPW; ++k) y[k] = __shfl_sync(0xffffffffu, x[k], src);
       if (want_v) {  // uniform across the CTA
 #pragma unroll
-        for (int k = 0; k < 8; ++k) z[k] = __shfl_sync(0xffffffffu, v[k], src);
+        for (int k = 0; k < RPW; ++k) z[k] = __shfl_sync(0xffffffffu, v[k], src);
       }
       double pa0 = x[0] * x[0], pa1 = x[1] * x[1], pg0 = x[0] * y[0], pg1 = x[1] * y[1];
 #pragma unroll
-      for (int k = 2; k < 8; k += 2) {
+      for (int k = 2; k < RPW; k += 2) {
         pa0 = fma(x[k], x[k], pa0);
         pa1 = fma(x[k + 1], x[k + 1], pa1);
         pg0 = fma(x[k], y[k], pg0);
         pg1 = fma(x[k + 1], y[k + 1], pg1);
       }
-      part[buf][w][c][0] = pa0 + pa1;
-      part[buf][w][c][1] = pg0 + pg1;
-      __syncthreads();
-      const double a = (part[buf][0][c][0] + part[buf][1][c][0]) + (part[buf][2][c][0] + part[buf][3][c][0]);
-      const double g = (part[buf][0][c][1] + part[buf][1][c][1]) + (part[buf][2][c][1] + part[buf][3][c][1]);
+      double a, g;
+      if constexpr (NW == 1) {
+        a = pa0 + pa1;
+        g = pg0 + pg1;
+      } else {
+        part[buf][w][c][0] = pa0 + pa1;
+        part[buf][w][c][1] = pg0 + pg1;
+        __syncthreads();
+        double ta[NW], tg[NW];
+#pragma unroll
+        for (int q = 0; q < NW; ++q) {
+          ta[q] = part[buf][q][c][0];
+          tg[q] = part[buf][q][c][1];
+        }
+        if constexpr (NW == 2) {
+          a = ta[0] + ta[1];
+          g = tg[0] + tg[1];
+        } else {
+          a = (ta[0] + ta[1]) + (ta[2] + ta[3]);
+          g = (tg[0] + tg[1]) + (tg[2] + tg[3]);
+        }
+      }
       const double b = __shfl_sync(0xffffffffu, a, src);
       buf ^= 1;
       if (plane < 0) continue;
@@ -287,10 +315,10 @@ jacobi32_kernel(int n, const double* __restrict__ M, int64_t ldm, double* __rest
       // p' = cs p - sn q ; q' = sn p + cs q
       const double so = low ? -sn : sn;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) x[k] = fma(so, y[k], cs * x[k]);
+      for (int k = 0; k < RPW; ++k) x[k] = fma(so, y[k], cs * x[k]);
       if (want_v) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = fma(so, z[k], cs * v[k]);
+        for (int k = 0; k < RPW; ++k) v[k] = fma(so, z[k], cs * v[k]);
       }
       rotated = 1;
     }
@@ -304,10 +332,10 @@ jacobi32_kernel(int n, const double* __restrict__ M, int64_t ldm, double* __rest
   // singular values = column norms, sorted descending (stable by index)
   double a1 = 0.0;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) a1 = fma(x[k], x[k], a1);
+  for (int k = 0; k < RPW; ++k) a1 = fma(x[k], x[k], a1);
   nrm_s[w][c] = a1;
   __syncthreads();
-  if (w == 0) sig_s[c] = sqrt((nrm_s[0][c] + nrm_s[1][c]) + (nrm_s[2][c] + nrm_s[3][c]));
+  if (w == 0) sig_s[c] = sqrt(jsum<NW>(nrm_s, c));
   __syncthreads();
   const double sc = sig_s[c];
   int rank = 0;
@@ -319,8 +347,8 @@ jacobi32_kernel(int n, const double* __restrict__ M, int64_t ldm, double* __rest
   if (w == 0) S[rank] = sc;
   const double inv = sc > 0.0 ? 1.0 / sc : 0.0;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int i = w * 8 + k;
+  for (int k = 0; k < RPW; ++k) {
+    const int i = w * RPW + k;
     if (i < n) {
       U[(int64_t)i * ldu + rank] = x[k] * inv;
       if (want_v) Vout[(int64_t)i * ldv + rank] = v[k];
@@ -338,8 +366,14 @@ int jacobi_svd(int64_t n, const double* M, int64_t ldm, double* U, int64_t ldu, 
 int jacobi_svd_tr(int64_t n, const double* M, int64_t ldm, bool trans, double* U, int64_t ldu, double* S,
                   double* V, int64_t ldv, cudaStream_t s) {
   SPB_REQUIRE(n >= 1 && n <= 256, "Jacobi SVD supports 1 <= n <= 256");
+  if (n <= 8) {
+    jacobi32_kernel<1, 8><<<1, 32, 0, s>>>((int)n, M, ldm, U, ldu, S, V, ldv, trans);
+    count_launch();
+    SPB_CHECK_LAUNCH();
+    return SP_OK;
+  }
   if (n <= 32) {
-    jacobi32_kernel<<<1, kJ32Warps * 32, 0, s>>>((int)n, M, ldm, U, ldu, S, V, ldv, trans);
+    jacobi32_kernel<kJ32Warps, 8><<<1, kJ32Warps * 32, 0, s>>>((int)n, M, ldm, U, ldu, S, V, ldv, trans);
     count_launch();
     SPB_CHECK_LAUNCH();
     return SP_OK;

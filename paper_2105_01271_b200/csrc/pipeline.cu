@@ -247,7 +247,6 @@ static int finish_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t 
     SPB_ALLOC(ar, double, Y, (size_t)n * r);
     SPB_ALLOC(ar, double, Qy, (size_t)n * r);
     SPB_ALLOC(ar, double, Ry, (size_t)r * r);
-    SPB_ALLOC(ar, double, Ryt, (size_t)r * r);
     SPB_ALLOC(ar, double, Us, (size_t)r * r);
     SPB_ALLOC(ar, double, Vs, (size_t)r * r);
     SPB_ALLOC(ar, double, Sr, (size_t)r);
