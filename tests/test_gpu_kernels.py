@@ -72,7 +72,7 @@ def test_grid_injection_indices_bit_exact(cuda):
 
 
 # ------------------------------------------------------------------ K2 ----
-@pytest.mark.parametrize("r", [1, 3, 7, 8, 16, 24])
+@pytest.mark.parametrize("r", [1, 3, 7, 8, 16, 24, 32])
 @pytest.mark.parametrize("m,n", [(1000, 4096), (257, 1001), (5, 33), (5, 34), (3, 4096), (2001, 20002)])
 def test_skinny_atz(cuda, r, m, n):
     rng = philox(m * r + n)
