@@ -11,9 +11,13 @@
 // The working matrix W and the accumulated rotations V live in shared memory
 // when they fit (n <= 112) and in a global scratch otherwise.  Convergence:
 // a sweep with no rotation (|w_p.w_q| <= 1e-15 ||w_p|| ||w_q|| for every pair).
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "launch_count.cuh"
 #include "ops.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace spb {
 
@@ -356,6 +360,130 @@ jacobi32_kernel(int n, const double* __restrict__ M, int64_t ldm, double* __rest
   }
 }
 
+// ------------------------------------------------- 112 < n <= 256, grid ----
+// W and V (column-major, n_p x n_p) do not fit in one SM's shared memory, so
+// the rounds are spread over a cooperative grid: one warp per column pair
+// (n_p / 2 pairs <= 128 warps), W / V in global memory (L2-resident, 1 MB),
+// one grid barrier per round.  Every CTA derives the same active-column list
+// from the same column norms; rotations, convergence test and sorting are
+// those of the single-CTA kernel.
+constexpr int kJgThreads = 128;
+
+__global__ void __launch_bounds__(kJgThreads)
+jacobi_grid_kernel(int n, int np, const double* __restrict__ M, int64_t ldm, bool trans, double* __restrict__ U,
+                   int64_t ldu, double* __restrict__ S, double* __restrict__ Vout, int64_t ldv,
+                   double* __restrict__ W, double* __restrict__ Vm, double* __restrict__ cn, int* rot) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ int act[256];
+  __shared__ int na_s;
+  const int lane = threadIdx.x & 31;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gthr = (int64_t)gridDim.x * blockDim.x;
+  const int gwarp = (int)(gtid >> 5), nwarps = (int)(gthr >> 5);
+  for (int64_t e = gtid; e < (int64_t)np * np; e += gthr) {
+    const int c = (int)(e / np), i = (int)(e % np);
+    W[e] = (i < n && c < n) ? (trans ? M[(int64_t)c * ldm + i] : M[(int64_t)i * ldm + c]) : 0.0;
+    Vm[e] = (i == c) ? 1.0 : 0.0;
+  }
+  if (gtid < 2) rot[gtid] = 0;
+  grid.sync();
+  for (int c = gwarp; c < np; c += nwarps) {
+    double a = 0.0;
+    for (int i = lane; i < np; i += 32) a = fma(W[(int64_t)c * np + i], W[(int64_t)c * np + i], a);
+    a = warp_sum(a);
+    if (lane == 0) cn[c] = a;
+  }
+  grid.sync();
+  double fro = 0.0;
+  for (int c = 0; c < np; ++c) fro += cn[c];
+  const double negl = 1e-30 * fro;
+  if (threadIdx.x == 0) {
+    int na = 0;
+    for (int c = 0; c < n; ++c)
+      if (cn[c] > negl) act[na++] = c;
+    if (na & 1) act[na++] = -1;
+    na_s = na;
+  }
+  __syncthreads();
+  const int na = na_s;
+  for (int sweep = 0; sweep < kJacMaxSweeps && na >= 2; ++sweep) {
+    for (int round = 0; round < na - 1; ++round) {
+      if (round == 1 && gtid == 0) rot[(sweep + 1) & 1] = 0;  // nobody reads it until this sweep ends
+      for (int k = gwarp; k < na / 2; k += nwarps) {
+        int pi, qi;
+        rr_pair(na, round, k, pi, qi);
+        int p = act[pi], q = act[qi];
+        if (p < 0 || q < 0) continue;
+        if (p > q) {
+          const int t = p;
+          p = q;
+          q = t;
+        }
+        double* wp = W + (int64_t)p * np;
+        double* wq = W + (int64_t)q * np;
+        double a = 0.0, b = 0.0, g = 0.0;
+        for (int i = lane; i < np; i += 32) {
+          const double x = wp[i], y = wq[i];
+          a = fma(x, x, a);
+          b = fma(y, y, b);
+          g = fma(x, y, g);
+        }
+        a = warp_sum(a);
+        b = warp_sum(b);
+        g = warp_sum(g);
+        if (g != 0.0 && fmin(a, b) > negl && fabs(g) > kJacTol * sqrt(a) * sqrt(b)) {
+          const double zeta = (b - a) / (2.0 * g);
+          double t;
+          if (fabs(zeta) > 1e150)
+            t = 0.5 / zeta;
+          else
+            t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+          const double cs = 1.0 / sqrt(fma(t, t, 1.0));
+          const double sn = cs * t;
+          double* vp = Vm + (int64_t)p * np;
+          double* vq = Vm + (int64_t)q * np;
+          for (int i = lane; i < np; i += 32) {
+            const double x = wp[i], y = wq[i];
+            wp[i] = cs * x - sn * y;
+            wq[i] = fma(sn, x, cs * y);
+            const double u = vp[i], w = vq[i];
+            vp[i] = cs * u - sn * w;
+            vq[i] = fma(sn, u, cs * w);
+          }
+          if (lane == 0) atomicOr(&rot[sweep & 1], 1);
+        }
+      }
+      grid.sync();
+    }
+    if (*(volatile int*)&rot[sweep & 1] == 0) break;  // same value in every thread after the barrier
+  }
+  // singular values = column norms, sorted descending (stable by index)
+  for (int c = gwarp; c < np; c += nwarps) {
+    double a = 0.0;
+    for (int i = lane; i < np; i += 32) a = fma(W[(int64_t)c * np + i], W[(int64_t)c * np + i], a);
+    a = warp_sum(a);
+    if (lane == 0) cn[c] = sqrt(a);
+  }
+  grid.sync();
+  for (int c = gwarp; c < n; c += nwarps) {
+    const double sc = cn[c];
+    int rank = 0;
+    for (int d = lane; d < np; d += 32) {
+      const double sd = cn[d];
+      rank += (sd > sc || (sd == sc && d < c)) ? 1 : 0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+    if (rank >= n) continue;
+    if (lane == 0) S[rank] = sc;
+    const double inv = sc > 0.0 ? 1.0 / sc : 0.0;
+    for (int i = lane; i < n; i += 32) {
+      U[(int64_t)i * ldu + rank] = W[(int64_t)c * np + i] * inv;
+      if (Vout) Vout[(int64_t)i * ldv + rank] = Vm[(int64_t)c * np + i];
+    }
+  }
+}
+
 int jacobi_svd(int64_t n, const double* M, int64_t ldm, double* U, int64_t ldu, double* S,
                double* V, int64_t ldv, cudaStream_t s) {
   return jacobi_svd_tr(n, M, ldm, false, U, ldu, S, V, ldv, s);
@@ -401,6 +529,29 @@ int jacobi_svd_tr(int64_t n, const double* M, int64_t ldm, bool trans, double* U
   const int threads = std::min(1024, std::max(64, 32 * (np / 2)));
   const size_t smem = (size_t)2 * np * np * sizeof(double);
   const bool use_smem = smem <= 200 * 1024;
+  if (!use_smem) {
+    // cooperative grid: one warp per column pair, W / V in global memory
+    Arena gar(s);
+    double* gW = gar.alloc<double>((size_t)np * np);
+    double* gV = gar.alloc<double>((size_t)np * np);
+    double* cn = gar.alloc<double>((size_t)np);
+    int* rot = gar.alloc<int>(2);
+    if (!gW || !gV || !cn || !rot) {
+      set_error("jacobi workspace allocation failed");
+      return SP_ECUDA;
+    }
+    const int warps = np / 2;
+    int grid = ceil_div(warps * 32, kJgThreads);
+    int per_sm = 0;
+    SPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_grid_kernel, kJgThreads, 0));
+    grid = std::max(1, std::min(grid, per_sm * kNumSMs));
+    int n_i = (int)n, np_i = np;
+    bool tr = false;  // M was transposed into scratch above when trans
+    void* args[] = {&n_i, &np_i, &M, &ldm, &tr, &U, &ldu, &S, &V, &ldv, &gW, &gV, &cn, &rot};
+    SPB_CUDA(cudaLaunchCooperativeKernel((const void*)jacobi_grid_kernel, dim3(grid), dim3(kJgThreads), args, 0, s));
+    count_launch();
+    return SP_OK;
+  }
   Arena ar(s);
   double *gW = nullptr, *gV = nullptr;
   if (!use_smem) {

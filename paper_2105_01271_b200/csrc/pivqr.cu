@@ -195,7 +195,8 @@ __global__ void pq_update_kernel(int t, int64_t cols, int64_t rows, double* __re
 // chunks with fixed-order partial reductions, instead of one warp (update)
 // or one CTA (select / re-orthogonalisation) per candidate.  Same pivot rule
 // and arithmetic (norms recomputed from the updated columns every step).
-constexpr int kPlRows = 8192;   // rows per block
+constexpr int kPlRows = 8192;   // rows per block (coefficient / update passes)
+constexpr int kPlRowsV = 2048;  // rows per block (re-orthogonalisation passes: t dots per row)
 constexpr int kPlCols = 16;     // candidates per update CTA
 constexpr int kPlThreads = 256;
 
@@ -261,7 +262,7 @@ __global__ void __launch_bounds__(kPlThreads)
 pl_swap_dots_kernel(int t, int64_t rows, double* __restrict__ WK, const double* __restrict__ Qt,
                     const int64_t* __restrict__ jsel, double* __restrict__ partial) {
   __shared__ double red[kPlThreads / 32];
-  const int64_t r0 = (int64_t)blockIdx.x * kPlRows, r1 = imin64(rows, r0 + kPlRows);
+  const int64_t r0 = (int64_t)blockIdx.x * kPlRowsV, r1 = imin64(rows, r0 + kPlRowsV);
   const int64_t js = *jsel;
   double* wt = WK + (int64_t)t * rows;
   if (js != t) {
@@ -273,13 +274,21 @@ pl_swap_dots_kernel(int t, int64_t rows, double* __restrict__ WK, const double* 
     }
     __syncthreads();
   }
-  for (int s2 = 0; s2 < t; ++s2) {
+  // warp w takes s = w, w + 8, ...: no block barrier per dot product
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int s2 = warp; s2 < t; s2 += kPlThreads / 32) {
     const double* q = Qt + (int64_t)s2 * rows;
-    double a = 0.0;
-    for (int64_t x = r0 + threadIdx.x; x < r1; x += kPlThreads) a = fma(q[x], wt[x], a);
-    a = pl_block_sum(a, red);
-    if (threadIdx.x == 0) partial[(int64_t)blockIdx.x * kPqMaxK + s2] = a;
+    double a0 = 0.0, a1 = 0.0;
+    int64_t x = r0 + lane;
+    for (; x + 32 < r1; x += 64) {
+      a0 = fma(q[x], wt[x], a0);
+      a1 = fma(q[x + 32], wt[x + 32], a1);
+    }
+    if (x < r1) a0 = fma(q[x], wt[x], a0);
+    const double a = warp_sum(a0 + a1);
+    if (lane == 0) partial[(int64_t)blockIdx.x * kPqMaxK + s2] = a;
   }
+  (void)red;
 }
 
 // delta[s] = sum_rb partial[rb][s]; R[s][t] += delta[s]  (one CTA, fixed order)
@@ -301,7 +310,7 @@ pl_form_v_kernel(int t, int64_t rows, const double* __restrict__ WK, double* __r
   __shared__ double ds[kPqMaxK];
   for (int s2 = threadIdx.x; s2 < t; s2 += kPlThreads) ds[s2] = delta[s2];
   __syncthreads();
-  const int64_t r0 = (int64_t)blockIdx.x * kPlRows, r1 = imin64(rows, r0 + kPlRows);
+  const int64_t r0 = (int64_t)blockIdx.x * kPlRowsV, r1 = imin64(rows, r0 + kPlRowsV);
   const double* wt = WK + (int64_t)t * rows;
   double* v = Qt + (int64_t)t * rows;
   double p = 0.0;
@@ -404,10 +413,10 @@ __global__ void pl_norms_kernel(int t, int nb, int64_t cols, const double* __res
 static int pivoted_qr_long(int64_t rows, int64_t cols, int k, double* WK, double* norms, int64_t* perm, double* Qt,
                            double* R, int64_t ldr, bool* fallback, cudaStream_t s) {
   *fallback = false;
-  const int nb = ceil_div(rows, kPlRows);
+  const int nb = ceil_div(rows, kPlRows), nbv = ceil_div(rows, kPlRowsV);
   Arena ar(s);
-  SPB_ALLOC(ar, double, partial, (size_t)nb * kPqMaxK);
-  SPB_ALLOC(ar, double, part2, (size_t)nb);
+  SPB_ALLOC(ar, double, partial, (size_t)nbv * kPqMaxK);
+  SPB_ALLOC(ar, double, part2, (size_t)nbv);
   SPB_ALLOC(ar, double, pc, (size_t)nb * cols);
   SPB_ALLOC(ar, double, coef, (size_t)cols);
   SPB_ALLOC(ar, double, delta, (size_t)kPqMaxK);
@@ -417,10 +426,10 @@ static int pivoted_qr_long(int64_t rows, int64_t cols, int k, double* WK, double
   SPB_CUDA(cudaMemsetAsync(status, 0, sizeof(int), s));
   for (int t = 0; t < k; ++t) {
     pl_select_kernel<<<1, kPqSelThreads, 0, s>>>(t, k, cols, norms, perm, R, ldr, jsel);
-    pl_swap_dots_kernel<<<nb, kPlThreads, 0, s>>>(t, rows, WK, Qt, jsel, partial);
-    if (t > 0) pl_delta_kernel<<<1, 128, 0, s>>>(t, nb, partial, delta, R, ldr);
-    pl_form_v_kernel<<<nb, kPlThreads, 0, s>>>(t, rows, WK, Qt, delta, part2);
-    pl_pivot_norm_kernel<<<1, 32, 0, s>>>(t, nb, part2, pnv, R, ldr, status);
+    pl_swap_dots_kernel<<<nbv, kPlThreads, 0, s>>>(t, rows, WK, Qt, jsel, partial);
+    if (t > 0) pl_delta_kernel<<<1, 128, 0, s>>>(t, nbv, partial, delta, R, ldr);
+    pl_form_v_kernel<<<nbv, kPlThreads, 0, s>>>(t, rows, WK, Qt, delta, part2);
+    pl_pivot_norm_kernel<<<1, 32, 0, s>>>(t, nbv, part2, pnv, R, ldr, status);
     pl_normalise_kernel<<<std::min<int64_t>(4 * kNumSMs, ceil_div(rows, 256)), 256, 0, s>>>(t, rows, Qt, pnv);
     count_launch(t > 0 ? 6 : 5);
     const int64_t trail = cols - t - 1;

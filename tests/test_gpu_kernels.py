@@ -196,7 +196,7 @@ def test_tsqr_rank_deficient_keeps_orthonormality(cuda):
 
 
 # ------------------------------------------------------------------ K5 ----
-@pytest.mark.parametrize("n", [1, 2, 7, 32, 64, 120, 200])
+@pytest.mark.parametrize("n", [1, 2, 7, 32, 64, 113, 120, 200, 256])
 def test_jacobi_svd(cuda, n):
     rng = philox(n)
     m = rng.standard_normal((n, n)) @ np.diag(np.logspace(0, -10, n))
