@@ -332,8 +332,7 @@ int cholqr2(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q,
   SPB_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
   SPB_TRY(cholqr2_async(rows, cols, X, ldx, Q, ldq, R, ldr, flag, s));
   int h = 0;
-  SPB_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
-  SPB_CUDA(cudaStreamSynchronize(s));
+  SPB_TRY(read_small(&h, flag, sizeof(int), s));
   *breakdown = (h != 0);
   return SP_OK;
 }

@@ -99,38 +99,34 @@ __device__ __forceinline__ double hash_uniform(uint64_t seed, uint64_t i) {
 }
 
 // ------------------------------------------------------ workspace arena ----
-// Stream-ordered scratch from the default CUDA mempool (cudaMallocAsync);
-// everything allocated through one Arena is released on the same stream when
-// the Arena goes out of scope.
-// Keep freed workspace in the device's default pool across synchronisations
-// (the default release threshold of 0 would hand it back to the driver at
-// every sync and re-map it on the next cudaMallocAsync).
-inline void retain_pool_memory() {
-  static int done[64] = {0};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
-  done[dev] = 1;
-}
+// Stream-ordered scratch.  The pipelines allocate a few dozen small
+// workspaces per call; cudaMallocAsync + cudaFreeAsync cost ~2-4 us of host
+// time each, which sits on the critical path right after every host
+// synchronisation.  ws_alloc / ws_free keep freed blocks in per-(device,
+// stream) free lists keyed by rounded size (reuse is stream ordered on the
+// same stream, hence safe); blocks above kWsCacheMax bytes and overflow past
+// the cache cap go straight back to the CUDA mempool (cudaFreeAsync).  On an
+// allocation failure the cache is drained (device synchronised) and the
+// allocation retried once.
+void* ws_alloc(size_t bytes, cudaStream_t s);
+void ws_free(void* p, size_t bytes, cudaStream_t s);
+void ws_release_all();  // drop every cached block (synchronises the device)
 
 class Arena {
  public:
-  explicit Arena(cudaStream_t s) : stream_(s) { retain_pool_memory(); }
+  explicit Arena(cudaStream_t s) : stream_(s) {}
   ~Arena() {
-    for (int i = 0; i < n_; ++i) cudaFreeAsync(ptrs_[i], stream_);
+    for (int i = n_ - 1; i >= 0; --i) ws_free(ptrs_[i], sizes_[i], stream_);
   }
   template <typename T>
   T* alloc(size_t count) {
     if (count == 0) count = 1;
     void* p = nullptr;
-    if (n_ >= kMax || cudaMallocAsync(&p, count * sizeof(T), stream_) != cudaSuccess) {
+    if (n_ >= kMax || (p = ws_alloc(count * sizeof(T), stream_)) == nullptr) {
       failed_ = true;
       return nullptr;
     }
+    sizes_[n_] = count * sizeof(T);
     ptrs_[n_++] = p;
     return static_cast<T*>(p);
   }
@@ -141,9 +137,32 @@ class Arena {
   static constexpr int kMax = 256;
   cudaStream_t stream_;
   void* ptrs_[kMax];
+  size_t sizes_[kMax];
   int n_ = 0;
   bool failed_ = false;
 };
+
+// Small device -> host reads through a per-thread pinned staging buffer:
+// pageable cudaMemcpyAsync is staged by the driver and blocks the host thread
+// per copy; pinned copies are queued and complete at one stream sync.
+//   PinnedReads rd(s); rd.add(&h, dptr, 4); ...; SPB_TRY(rd.sync());
+class PinnedReads {
+ public:
+  explicit PinnedReads(cudaStream_t s) : s_(s) {}
+  int add(void* host_dst, const void* dev_src, size_t bytes);
+  int sync();  // cudaStreamSynchronize + scatter into the destinations
+
+ private:
+  static constexpr int kMax = 8;
+  cudaStream_t s_;
+  void* dst_[kMax];
+  size_t off_[kMax], len_[kMax];
+  size_t used_ = 0;
+  int n_ = 0;
+};
+
+// one small device -> host read, then a stream sync
+int read_small(void* host_dst, const void* dev_src, size_t bytes, cudaStream_t s);
 
 #define SPB_ALLOC(arena, T, var, count)                                       \
   T* var = (arena).template alloc<T>(count);                                  \

@@ -188,8 +188,7 @@ int check_finite(int64_t rows, int64_t cols, const double* X, int64_t ldx, const
   all_finite_kernel<<<ceil_div(rows * cols, 256), 256, 0, s>>>(rows, cols, X, ldx, bad);
   SPB_LAUNCHED();
   int h = 0;
-  SPB_CUDA(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
-  SPB_CUDA(cudaStreamSynchronize(s));
+  SPB_TRY(read_small(&h, bad, sizeof(int), s));
   if (h) {
     set_error(std::string(what));
     return SP_ENUMERICAL;

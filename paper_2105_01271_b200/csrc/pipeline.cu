@@ -59,9 +59,9 @@ struct PendingFlag {
   bool check_input = false;
 };
 
-static int read_flag_with(const PendingFlag& pf, int& host_flag, cudaStream_t s) {
+static int read_flag_with(const PendingFlag& pf, int& host_flag, PinnedReads& rd) {
   host_flag = 0;
-  if (pf.dev) SPB_CUDA(cudaMemcpyAsync(&host_flag, pf.dev, sizeof(int), cudaMemcpyDeviceToHost, s));
+  if (pf.dev) SPB_TRY(rd.add(&host_flag, pf.dev, sizeof(int)));
   return SP_OK;
 }
 
@@ -79,8 +79,9 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
   if (p <= 64 && pf.dev) {
     // the exact path checks finiteness itself (thin_svd); surface the caller's message
     if (pf.check_input) SPB_TRY(check_finite_async(rows, cols, X, ldx, pf.dev, s));
-    SPB_TRY(read_flag_with(pf, hflag, s));
-    SPB_CUDA(cudaStreamSynchronize(s));
+    PinnedReads rd(s);
+    SPB_TRY(read_flag_with(pf, hflag, rd));
+    SPB_TRY(rd.sync());
     if (hflag) {
       set_error(pf.msg);
       return SP_ENUMERICAL;
@@ -97,8 +98,7 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
     }
     SPB_TRY(thin_svd(rows, cols, X, ldx, out.U, p, out.S, out.V, p, s));
     out.hs.resize(p);
-    SPB_CUDA(cudaMemcpyAsync(out.hs.data(), out.S, p * sizeof(double), cudaMemcpyDeviceToHost, s));
-    SPB_CUDA(cudaStreamSynchronize(s));
+    SPB_TRY(read_small(out.hs.data(), out.S, p * sizeof(double), s));
     out.kept = count_kept(out.hs, power);
     return SP_OK;
   }
@@ -133,9 +133,10 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
       SPB_TRY(gemm(1, 0, cols, b, rows, 1.0, X, ldx, Q, b, 0.0, Z, b, s));
       SPB_TRY(tsqr(cols, b, Z, b, P, b, Rz, b, s));
       SPB_TRY(jacobi_svd_tr(b, Rz, b, /*trans=*/true, Us, b, Sg, want_v ? Vs : nullptr, b, s));
-      SPB_CUDA(cudaMemcpyAsync(hs.data(), Sg, b * sizeof(double), cudaMemcpyDeviceToHost, s));
-      if (itn == 0) SPB_TRY(read_flag_with(pf, hflag, s));
-      SPB_CUDA(cudaStreamSynchronize(s));
+      PinnedReads rd(s);
+      SPB_TRY(rd.add(hs.data(), Sg, b * sizeof(double)));
+      if (itn == 0) SPB_TRY(read_flag_with(pf, hflag, rd));
+      SPB_TRY(rd.sync());
       if (hflag) {
         set_error(pf.msg);
         return SP_ENUMERICAL;
@@ -271,8 +272,7 @@ static int finish_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t 
     SPB_TRY(jacobi_svd_tr(r, Ry, r, /*trans=*/true, Us, r, Sr, Vs, r, s));  // Ry^T = Us Sr Vs^T
     if (qflag) {
       int h = 0;
-      SPB_CUDA(cudaMemcpyAsync(&h, qflag, sizeof(int), cudaMemcpyDeviceToHost, s));
-      SPB_CUDA(cudaStreamSynchronize(s));
+      SPB_TRY(read_small(&h, qflag, sizeof(int), s));
       qflag = nullptr;
       if (h) {  // CholeskyQR2 broke down: Householder TSQR and redo the core
         SPB_TRY(tsqr(n, r, Y, r, Qy, r, Ry, r, s));
@@ -332,8 +332,7 @@ static int sketch_is_columns(const int64_t* idx, const double* w, int depth, int
   count_launch();
   SPB_CHECK_LAUNCH();
   int h = 1;
-  SPB_CUDA(cudaMemcpyAsync(&h, differ, sizeof(int), cudaMemcpyDeviceToHost, s));
-  SPB_CUDA(cudaStreamSynchronize(s));
+  SPB_TRY(read_small(&h, differ, sizeof(int), s));
   same = (h == 0);
   return SP_OK;
 }

@@ -444,8 +444,7 @@ static int pivoted_qr_long(int64_t rows, int64_t cols, int k, double* WK, double
     SPB_CHECK_LAUNCH();
   }
   int hst = 0;
-  SPB_CUDA(cudaMemcpyAsync(&hst, status, sizeof(int), cudaMemcpyDeviceToHost, s));
-  SPB_CUDA(cudaStreamSynchronize(s));
+  SPB_TRY(read_small(&hst, status, sizeof(int), s));
   *fallback = hst != 0;
   return SP_OK;
 }
@@ -490,8 +489,7 @@ int pivoted_qr(int64_t rows, int64_t cols, const double* Mt, int64_t ldmt, int k
     }
   }
   int hst = 0;
-  SPB_CUDA(cudaMemcpyAsync(&hst, status, sizeof(int), cudaMemcpyDeviceToHost, s));
-  SPB_CUDA(cudaStreamSynchronize(s));
+  SPB_TRY(read_small(&hst, status, sizeof(int), s));
   if (hst != 0) {
     set_error("cannot extend orthonormal basis");
     return SP_ENUMERICAL;

@@ -152,8 +152,7 @@ int check_columns(const int64_t* cols, int64_t count, int64_t n, cudaStream_t s)
   count_launch();
   SPB_CHECK_LAUNCH();
   int hbad = 0;
-  SPB_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
-  SPB_CUDA(cudaStreamSynchronize(s));
+  SPB_TRY(read_small(&hbad, bad, sizeof(int), s));
   if (hbad & 1) {
     set_error("column index out of range [0, " + std::to_string(n) + ")");
     return SP_ECONFIG;

@@ -1,0 +1,149 @@
+// Workspace caching allocator and pinned small reads (common.cuh).
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+
+namespace spb {
+
+namespace {
+
+constexpr size_t kWsCacheMax = size_t(256) << 20;   // larger blocks are not cached
+constexpr size_t kWsCacheCap = size_t(4) << 30;     // cached bytes per device
+
+// 512-byte granules up to 64 KB, then 8 steps per power of two (<= 12.5 % slack)
+size_t ws_round(size_t b) {
+  if (b <= 65536) return (b + 511) & ~size_t(511);
+  int e = 63 - __builtin_clzll(b);
+  size_t step = size_t(1) << (e - 3);
+  return (b + step - 1) & ~(step - 1);
+}
+
+struct DevCache {
+  std::map<std::pair<cudaStream_t, size_t>, std::vector<void*>> free;
+  size_t cached = 0;
+  bool pool_tuned = false;
+};
+
+std::mutex g_mu;
+DevCache g_dev[64];
+
+DevCache* dev_cache() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= 64) return nullptr;
+  DevCache* c = &g_dev[d];
+  if (!c->pool_tuned) {
+    // keep freed memory in the device's default pool across synchronisations
+    // (a release threshold of 0 hands it back to the driver at every sync)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    c->pool_tuned = true;
+  }
+  return c;
+}
+
+void drain(DevCache* c) {
+  for (auto& kv : c->free)
+    for (void* p : kv.second) cudaFreeAsync(p, kv.first.first);
+  c->free.clear();
+  c->cached = 0;
+}
+
+}  // namespace
+
+void* ws_alloc(size_t bytes, cudaStream_t s) {
+  const size_t rb = ws_round(bytes);
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevCache* c = dev_cache();
+  if (!c) return nullptr;
+  if (rb <= kWsCacheMax) {
+    auto it = c->free.find({s, rb});
+    if (it != c->free.end() && !it->second.empty()) {
+      void* p = it->second.back();
+      it->second.pop_back();
+      c->cached -= rb;
+      return p;
+    }
+  }
+  void* p = nullptr;
+  if (cudaMallocAsync(&p, rb, s) == cudaSuccess) return p;
+  cudaGetLastError();
+  // out of memory: hand every cached block back and retry once
+  drain(c);
+  cudaDeviceSynchronize();
+  if (cudaMallocAsync(&p, rb, s) == cudaSuccess) return p;
+  cudaGetLastError();
+  return nullptr;
+}
+
+void ws_free(void* p, size_t bytes, cudaStream_t s) {
+  if (!p) return;
+  const size_t rb = ws_round(bytes);
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevCache* c = dev_cache();
+  if (c && rb <= kWsCacheMax && c->cached + rb <= kWsCacheCap) {
+    c->free[{s, rb}].push_back(p);
+    c->cached += rb;
+    return;
+  }
+  cudaFreeAsync(p, s);
+}
+
+void ws_release_all() {
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevCache* c = dev_cache();
+  if (!c) return;
+  drain(c);
+  cudaDeviceSynchronize();
+}
+
+// ------------------------------------------------------------ pinned reads ----
+namespace {
+struct PinnedBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+};
+thread_local PinnedBuf t_pinned;
+}  // namespace
+
+int PinnedReads::add(void* host_dst, const void* dev_src, size_t bytes) {
+  const size_t off = (used_ + 15) & ~size_t(15);
+  if (n_ >= kMax || off + bytes > (size_t(64) << 10)) {
+    set_error("PinnedReads: too many / too large small reads");
+    return SP_ECUDA;
+  }
+  if (!t_pinned.p) {
+    SPB_CUDA(cudaMallocHost(&t_pinned.p, size_t(64) << 10));
+    t_pinned.cap = size_t(64) << 10;
+  }
+  SPB_CUDA(cudaMemcpyAsync(static_cast<char*>(t_pinned.p) + off, dev_src, bytes, cudaMemcpyDeviceToHost, s_));
+  dst_[n_] = host_dst;
+  off_[n_] = off;
+  len_[n_++] = bytes;
+  used_ = off + bytes;
+  return SP_OK;
+}
+
+int PinnedReads::sync() {
+  SPB_CUDA(cudaStreamSynchronize(s_));
+  for (int i = 0; i < n_; ++i) std::memcpy(dst_[i], static_cast<char*>(t_pinned.p) + off_[i], len_[i]);
+  n_ = 0;
+  used_ = 0;
+  return SP_OK;
+}
+
+int read_small(void* host_dst, const void* dev_src, size_t bytes, cudaStream_t s) {
+  PinnedReads r(s);
+  SPB_TRY(r.add(host_dst, dev_src, bytes));
+  return r.sync();
+}
+
+}  // namespace spb
