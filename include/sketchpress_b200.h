@@ -66,6 +66,19 @@ const char* sp_last_error(void);
 /* Number of kernels this library launched on the calling thread so far. */
 int64_t sp_launch_count(void);
 
+/* Deferred status of the calling thread's last pipeline call: the fused
+ * finish stage (r <= 16 kept columns, kappa < 1e6) runs without a host
+ * synchronisation and raises a device flag on a Cholesky breakdown or
+ * non-finite data (S is then NaN).  Waits for that call's completion and
+ * returns the flag in *flag (0 = clean).  The reference raises at the same
+ * point synchronously (NumericalError, src/kernels.py:47-49); the Python
+ * mirror reads this after its device->host copies and re-runs the call with
+ * sp_set_finish_mode(1) (Householder TSQR finish). */
+int sp_deferred_status(int32_t* flag);
+/* 0 = automatic (fused CholeskyQR2 finish when it applies), 1 = Householder
+ * TSQR finish (thread-local). */
+int sp_set_finish_mode(int32_t mode);
+
 /* ---------------------------------------------------------------- K1 -----
  * out[i, c] = sum_t A[i, idx[t, c]] * w[t, c]      (t = 0..depth-1, no FMA)
  * Replaces apply_sketch for the stencil kinds (src/sketch.py:171-184,

@@ -38,6 +38,8 @@ SIGNATURES = {
     "sp_abi_version": [],
     "sp_last_error": [],
     "sp_launch_count": [],
+    "sp_deferred_status": [_P],
+    "sp_set_finish_mode": [_I32],
     "sp_apply_stencil": [_P, _I32, _I64, _I64, _I64, _P, _P, _I32, _I64, _I32, _P, _I64, _P],
     "sp_check_columns": [_P, _I64, _I64, _P],
     "sp_skinny_atz": [_P, _I32, _I64, _I64, _I64, _P, _I64, _I32, _P, _I64, _P],
@@ -122,6 +124,24 @@ def call(name: str, *args) -> None:
 
 def launch_count() -> int:
     return int(load().sp_launch_count())
+
+
+def deferred_status() -> int:
+    """Flag of this thread's last fused-finish pipeline call (waits for it)."""
+    f = ctypes.c_int32(0)
+    check(load().sp_deferred_status(ctypes.byref(f)), "sp_deferred_status")
+    return int(f.value)
+
+
+class householder_finish:
+    """Context: pipeline calls on this thread use the Householder TSQR finish."""
+
+    def __enter__(self):
+        call("sp_set_finish_mode", 1)
+        return self
+
+    def __exit__(self, *exc):
+        call("sp_set_finish_mode", 0)
 
 
 def new_info() -> np.ndarray:

@@ -31,6 +31,8 @@ int power_id(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, cons
              double* lift_right, double* lift_ur, int r_max, int64_t* info, cudaStream_t s);
 int row_id(int64_t m, int64_t cols, const double* M, int64_t ldm, int k, double* P, int64_t* indices,
            int* warn, cudaStream_t s);
+int deferred_status(int* out);
+void set_finish_mode(int mode);
 int sketch_basis(const double* X, int64_t rows, int64_t cols, int64_t ldx, double power, int r_max, double* U,
                  int64_t ldu, double* S, int64_t* info, cudaStream_t s);
 
@@ -45,6 +47,16 @@ extern "C" {
 int sp_abi_version(void) { return SP_ABI_VERSION; }
 const char* sp_last_error(void) { return last_error(); }
 int64_t sp_launch_count(void) { return launches(); }
+int sp_deferred_status(int32_t* flag) {
+  int f = 0;
+  const int st = deferred_status(&f);
+  *flag = f;
+  return st;
+}
+int sp_set_finish_mode(int32_t mode) {
+  set_finish_mode(mode);
+  return SP_OK;
+}
 
 int sp_apply_stencil(const void* A, int32_t a_dtype, int64_t rows, int64_t n, int64_t lda,
                      const int64_t* idx, const double* w, int32_t depth, int64_t n_c,

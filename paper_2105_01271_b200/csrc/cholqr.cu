@@ -128,7 +128,8 @@ constexpr int kCsThreads = 1024;
 // when R1 != nullptr also Rout = R R1 (upper triangular product).
 __global__ void __launch_bounds__(kCsThreads)
 chol_small_kernel(int c, int nb, const double* __restrict__ P, double* __restrict__ R, double* __restrict__ Rinv,
-                  const double* __restrict__ R1, double* __restrict__ Rout, int64_t ldro, int* flag) {
+                  const double* __restrict__ R1, double* __restrict__ Rout, int64_t ldro, int* flag,
+                  double shift_rel = 0.0) {
   __shared__ double G[32][33];
   __shared__ double Ri[32][33];
   __shared__ double part[8][32 * 32 / 8 + 1];
@@ -156,6 +157,15 @@ chol_small_kernel(int c, int nb, const double* __restrict__ P, double* __restric
   // (no block barriers on the critical path; the other warps are done)
   if (tid >= 32) return;
   const int lane = tid;
+  if (shift_rel > 0.0) {
+    // shifted CholeskyQR: G + s I with s = shift_rel tr(G) (lane order sum,
+    // identical in every lane) keeps the factorisation defined
+    double tr = 0.0;
+    for (int i = 0; i < c; ++i) tr += G[i][i];
+    __syncwarp();
+    if (lane < c) G[lane][lane] += shift_rel * tr;
+    __syncwarp();
+  }
   bool bad = false;
   for (int j = 0; j < c; ++j) {
     const double d = G[j][j];
@@ -251,7 +261,7 @@ mul_gram_kernel(int64_t rows, int c, const double* __restrict__ X, int64_t ldx, 
     for (int j = 0; j < 32; ++j)
       if (j < c) ts[t][j] = t < nr ? acc[j] : 0.0;
     __syncthreads();
-    if (t < nr) {
+    if (Q != nullptr && t < nr) {
       double* dst = Q + (base + t) * ldq;
       for (int cc = 0; cc < c; ++cc) dst[cc] = ts[t][cc];
     }
@@ -277,6 +287,29 @@ mul_gram_kernel(int64_t rows, int c, const double* __restrict__ X, int64_t ldx, 
     const int o = t + u * kMgRows;
     if (o < c * c) partial[(int64_t)blockIdx.x * c * c + o] = gacc[u];
   }
+}
+
+// launch wrappers for the fused finish stage (finish.cu)
+int chol_small_launch(int c, int nb, const double* P, double* R, double* Rinv, int* flag, double shift_rel,
+                      cudaStream_t s) {
+  chol_small_kernel<<<1, kCsThreads, 0, s>>>(c, nb, P, R, Rinv, nullptr, nullptr, 0, flag, shift_rel);
+  count_launch();
+  SPB_CHECK_LAUNCH();
+  return SP_OK;
+}
+
+int mul_gram_tiles(int64_t rows) { return mg_tiles(rows); }
+
+// partial Grams of Q1 = X Ri (Q1 written to Q unless Q == nullptr); nb slabs
+int mul_gram_launch(int64_t rows, int c, const double* X, int64_t ldx, const double* Ri, double* Q, int64_t ldq,
+                    double* partial, int* nb_out, cudaStream_t s) {
+  const int tiles = mg_tiles(rows);
+  const int nb = ceil_div(rows, (int64_t)kMgRows * tiles);
+  *nb_out = nb;
+  mul_gram_kernel<<<nb, kMgRows, 0, s>>>(rows, c, X, ldx, Ri, Q, ldq, partial, tiles);
+  count_launch();
+  SPB_CHECK_LAUNCH();
+  return SP_OK;
 }
 
 static int cholqr2_small(int64_t rows, int c, const double* X, int64_t ldx, double* Q, int64_t ldq, double* R,

@@ -236,12 +236,62 @@ static AuxStream& aux_stream() {
   return a;
 }
 
+// ----------------------------------------------------- deferred status ----
+// The fused finish stage never synchronises; its device flag (Cholesky
+// breakdown / non-finite input) is copied to pinned memory behind the call's
+// last kernel and read by sp_deferred_status() after the caller's own sync
+// (the host-result API does this right after its device->host copies and
+// re-runs the call with the Householder finish when it is set).
+struct Deferred {
+  int* host = nullptr;
+  cudaEvent_t ev = nullptr;
+  bool pending = false;
+};
+static thread_local Deferred t_def;
+static thread_local int t_finish_mode = 0;  // 1: Householder TSQR finish
+
+static int defer_flag(const int* dflag, cudaStream_t s) {
+  if (!t_def.host) {
+    SPB_CUDA(cudaMallocHost(&t_def.host, sizeof(int)));
+    SPB_CUDA(cudaEventCreateWithFlags(&t_def.ev, cudaEventDisableTiming));
+  }
+  if (t_def.pending) SPB_CUDA(cudaEventSynchronize(t_def.ev));  // previous value is superseded
+  SPB_CUDA(cudaMemcpyAsync(t_def.host, dflag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SPB_CUDA(cudaEventRecord(t_def.ev, s));
+  t_def.pending = true;
+  return SP_OK;
+}
+
+int deferred_status(int* out) {
+  *out = 0;
+  if (!t_def.pending) return SP_OK;
+  SPB_CUDA(cudaEventSynchronize(t_def.ev));
+  *out = *t_def.host;
+  t_def.pending = false;
+  return SP_OK;
+}
+
+void set_finish_mode(int mode) { t_finish_mode = mode; }
+
+bool finish_fused_ok(int64_t m, int64_t n, int r, int k);
+int finish_fused(int64_t m, int64_t n, const double* Z, int64_t ldz, const double* Y, int r, int k, double* U,
+                 double* S, double* V, int* dflag, cudaStream_t s);
+
 // Given the kept left basis Z (m x r, ld ldz) of the sketch, one read of A:
 // Y = A^T Z, then the rank-k SVD of Z Z^T A written to U (m x k), S, V (n x k).
 static int finish_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, const double* Z,
                       int64_t ldz, int r, int k, double* U, double* S, double* V, double kappa_est,
                       cudaStream_t s) {
   Arena ar(s);
+  if (r > 0 && t_finish_mode == 0 && kappa_est < 1e6 && finish_fused_ok(m, n, r, k)) {
+    // A pass + fused shifted-CholeskyQR2 / Jacobi / completion: no host sync
+    SPB_ALLOC(ar, double, Y, (size_t)n * r);
+    SPB_ALLOC(ar, int, dflag, 1);
+    SPB_CUDA(cudaMemsetAsync(dflag, 0, sizeof(int), s));
+    SPB_TRY(skinny_atz(A, a_dtype, m, n, lda, Z, ldz, r, Y, r, s));
+    SPB_TRY(finish_fused(m, n, Z, ldz, Y, r, k, U, S, V, dflag, s));
+    return defer_flag(dflag, s);
+  }
   SPB_CUDA(cudaMemsetAsync(S, 0, k * sizeof(double), s));
   const int kk = std::min(r, k);
   if (r > 0) {
@@ -255,7 +305,7 @@ static int finish_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t 
     // kappa(Y) ~ the kept spectral range: CholeskyQR2 below 1e6 (breakdown is
     // checked once at the end, and the factorisation redone by Householder
     // TSQR if it happened), else Householder TSQR directly
-    const bool chol = kappa_est < 1e6 && r <= 112;
+    const bool chol = kappa_est < 1e6 && r <= 112 && t_finish_mode == 0;
     int* qflag = nullptr;
     if (chol) {
       qflag = ar.alloc<int>(1);

@@ -135,11 +135,14 @@ def power_svd(stream: SnapshotStream, op: SketchOperator, k: int, cfg: PowerConf
     u, s, v = empty((m, k)), empty((k,)), empty((n, k))
     info = _lib.new_info()
     a = staged.a
-    _lib.call("sp_power_svd", ptr(a), staged.dtype_tag, m, n, a.stride(0), ptr(idx), ptr(w), depth,
-              op.n_c, ptr(om), (op.out_dim if om is not None else 0), ptr(d_cols), cols.size, cfg.q, k,
-              ptr(s0), ptr(c), hints, ptr(u), ptr(s), ptr(v), _lib.info_ptr(info), stream_handle())
+
+    def run():
+        _lib.call("sp_power_svd", ptr(a), staged.dtype_tag, m, n, a.stride(0), ptr(idx), ptr(w), depth,
+                  op.n_c, ptr(om), (op.out_dim if om is not None else 0), ptr(d_cols), cols.size, cfg.q, k,
+                  ptr(s0), ptr(c), hints, ptr(u), ptr(s), ptr(v), _lib.info_ptr(info), stream_handle())
+    run()
     return _finish(u, s, v, k, "power", info, not return_device,
-                   "enriched sketch is rank deficient; using regularized solve")
+                   "enriched sketch is rank deficient; using regularized solve", rerun=run)
 
 
 def _power_svd_two_pass(stream, op, k, cfg, cols, block_rows, return_device):

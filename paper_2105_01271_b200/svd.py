@@ -100,12 +100,23 @@ def _projected_s0(op: SketchOperator, staged, s0_coarse):
     return out
 
 
-def _finish(u, s, v, k, method, info, host, warn_msg):
+def _finish(u, s, v, k, method, info, host, warn_msg, rerun=None):
+    """Warn / convert like the reference.  Host results: the fused finish's
+    deferred device flag is read after the copies (no extra sync) and, if set,
+    the call is re-run with the Householder finish (`rerun`), which reports
+    non-finite data as NumericalError like the reference."""
     from .device import to_host_many
     if info[_lib.INFO_WARN] & _lib.SP_WARN_RANK_DEFICIENT:
         warnings.warn(warn_msg, RankDeficiencyWarning, stacklevel=3)
     if host:
-        u, s, v = to_host_many(u, s, v)
+        u_h, s_h, v_h = to_host_many(u, s, v)
+        if _lib.deferred_status() and rerun is not None:
+            with _lib.householder_finish():
+                rerun()
+            if not np.all(np.isfinite(s.cpu().numpy())):
+                raise NumericalError("non-finite values in the snapshot data")
+            u_h, s_h, v_h = to_host_many(u, s, v)
+        u, s, v = u_h, s_h, v_h
     return LowRankSVD(u=u, s=s, v=v, k=k, method=method, kept_rank=int(info[_lib.INFO_KEPT]))
 
 
@@ -146,11 +157,14 @@ def single_pass_svd(stream: SnapshotStream, op: SketchOperator, k: int,
     u, s, v = empty((m, k)), empty((k,)), empty((n, k))
     info = _lib.new_info()
     a = staged.a
-    _lib.call("sp_single_pass_svd", ptr(a), staged.dtype_tag, m, n, a.stride(0), None, None, 1,
-              op.out_dim, None, 0, k, ptr(s0), ptr(u), ptr(s), ptr(v), _lib.info_ptr(info),
-              stream_handle())
+
+    def run():
+        _lib.call("sp_single_pass_svd", ptr(a), staged.dtype_tag, m, n, a.stride(0), None, None, 1,
+                  op.out_dim, None, 0, k, ptr(s0), ptr(u), ptr(s), ptr(v), _lib.info_ptr(info),
+                  stream_handle())
+    run()
     return _finish(u, s, v, k, "single_pass", info, not return_device,
-                   "coarse sketch is rank deficient; using regularized triangular solve")
+                   "coarse sketch is rank deficient; using regularized triangular solve", rerun=run)
 
 
 # ------------------------------------------------------------ second pass ----

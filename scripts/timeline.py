@@ -50,8 +50,10 @@ memc = [e for e in ev if e.get("cat") in ("gpu_memcpy", "gpu_memset")]
 callw = sorted([e for e in ev if e.get("name") == "CALL" and e.get("cat") == "user_annotation"],
                key=lambda e: e["ts"])
 last = callw[-1]
-t0, t1 = last["ts"], last["ts"] + last["dur"]
-ks = [e for e in kern + memc if t0 <= e["ts"] <= t1]
+t0 = last["ts"]
+# the call returns before its last kernels finish (no trailing sync): take
+# everything launched after its start (the profiled loop syncs after each call)
+ks = [e for e in kern + memc if t0 <= e["ts"]]
 ks.sort(key=lambda e: e["ts"])
 first = ks[0]["ts"]
 prev_end = first
