@@ -134,6 +134,8 @@ chol_small_kernel(int c, int nb, const double* __restrict__ P, double* __restric
   __shared__ double Ri[32][33];
   __shared__ double part[8][32 * 32 / 8 + 1];
   const int tid = threadIdx.x, nout = c * c;
+  SPB_TDECL;
+  SPB_TMARK(0);
   // fixed-order reduction: thread (o, g) sums slabs g, g + G, ... of output o
   const int gsplit = kCsThreads / nout >= 32 ? 32 : (kCsThreads / nout >= 1 ? kCsThreads / nout : 1);
   for (int o0 = 0; o0 < nout; o0 += kCsThreads / gsplit) {
@@ -157,6 +159,7 @@ chol_small_kernel(int c, int nb, const double* __restrict__ P, double* __restric
   // (no block barriers on the critical path; the other warps are done)
   if (tid >= 32) return;
   const int lane = tid;
+  SPB_TMARK(1);
   if (shift_rel > 0.0) {
     // shifted CholeskyQR: G + s I with s = shift_rel tr(G) (lane order sum,
     // identical in every lane) keeps the factorisation defined
@@ -213,6 +216,8 @@ chol_small_kernel(int c, int nb, const double* __restrict__ P, double* __restric
       Rout[(int64_t)i * ldro + l] = (l >= i) ? acc : 0.0;
     }
   }
+  SPB_TMARK(2);
+  if (lane == 0) SPB_TPRINT("chol_small reduce/factor", 3);
 }
 
 // Q1 rows = X rows R^{-1} (c x c) and partial[blk] = Q1_blk^T Q1_blk; one

@@ -98,6 +98,24 @@ __device__ __forceinline__ double hash_uniform(uint64_t seed, uint64_t i) {
   return ((double)(z >> 11) * (1.0 / 9007199254740992.0)) * 2.0 - 1.0;
 }
 
+// Diagnostic phase timers (build with SPB_NVCC_EXTRA=-DSPB_PHASE_TRACE):
+// SPB_TMARK(i) records clock64() into slot i, SPB_TPRINT(name, n) prints the
+// n - 1 phase durations from the calling thread.
+#ifdef SPB_PHASE_TRACE
+#define SPB_TDECL long long spb_tm[12] = {0}
+#define SPB_TMARK(i) spb_tm[i] = clock64()
+#define SPB_TPRINT(name, n)                                                            \
+  do {                                                                                 \
+    printf("%s:", name);                                                               \
+    for (int _i = 1; _i < (n); ++_i) printf(" %lld", spb_tm[_i] - spb_tm[_i - 1]);     \
+    printf(" cyc\n");                                                                  \
+  } while (0)
+#else
+#define SPB_TDECL
+#define SPB_TMARK(i)
+#define SPB_TPRINT(name, n)
+#endif
+
 // ------------------------------------------------------ workspace arena ----
 // Stream-ordered scratch.  The pipelines allocate a few dozen small
 // workspaces per call; cudaMallocAsync + cudaFreeAsync cost ~2-4 us of host

@@ -8,50 +8,36 @@
 //   tests/test_svd.py:163-171 of the reference).
 // This replaces LAPACK thin_qr / thin_svd / the GEMMs of src/svd.py:168-189
 // and src/power.py:158-181 for the kept part.  Launches after the A pass:
-//   tall_gram partials(Y) -> chol_small (shifted: R1, R1^{-1})
-//   -> mul_gram (partial Gram of Q1 = Y R1^{-1}, Q1 never stored)
+//   gram_rows (partial Grams of Y; the last CTA reduces them in a fixed
+//     order and factors G1 + s I = R1^T R1, shift s = 16 r eps tr(G1))
+//   -> gram_rows (partial Grams of Q1 = Y R1^{-1}, Q1 never stored)
 //   -> finish_core (1 CTA: Cholesky of Q1^T Q1 -> R2, R = R2 R1, Jacobi SVD
 //      of R^T, the top k rows of both factors and both Householder
 //      completions, concurrently in two thread groups)
 //   -> finish_rows (one streaming pass writing U and V).
-// No host synchronisation: the diagonal shift of the first Gram
-// (16 r eps tr(G)) makes its Cholesky unconditionally defined, and the second
-// pass restores O(eps) orthogonality for kappa(Y) up to ~1e7 (the caller
-// routes kappa >= 1e6 to Householder TSQR).  A non-positive or non-finite
-// pivot (non-finite A) raises a device flag the host reads lazily
-// (sp_deferred_status) and S is poisoned with NaN.
+// No host synchronisation: the diagonal shift makes the first Cholesky
+// unconditionally defined and the second pass restores O(eps) orthogonality
+// for kappa(Y) up to ~1e7 (the caller routes kappa >= 1e6 to Householder
+// TSQR).  A non-positive or non-finite pivot (non-finite A) raises a device
+// flag the host reads lazily (sp_deferred_status), and S is poisoned with NaN.
+// Every reduction runs in a fixed order: bitwise reproducible.
 #include "common.cuh"
-#include "hh_complete.cuh"
 #include "launch_count.cuh"
 #include "ops.cuh"
 
 namespace spb {
 
-int chol_small_launch(int c, int nb, const double* P, double* R, double* Rinv, int* flag, double shift_rel,
-                      cudaStream_t s);
-int mul_gram_tiles(int64_t rows);
-int mul_gram_launch(int64_t rows, int c, const double* X, int64_t ldx, const double* Ri, double* Q, int64_t ldq,
-                    double* partial, int* nb_out, cudaStream_t s);
-
-constexpr int kFcThreads = 512;
 constexpr int kFcMaxR = 16;
+constexpr int kMR = kFcMaxR;
 constexpr double kFcJacTol = 1e-15;  // jacobi.cu kJacTol
 constexpr int kFcMaxSweeps = 40;
+typedef double SmallMat[kMR][kMR + 1];
 
-struct FcShared {
-  HcShared hc[2];                 // U / V completions
-  double G[kFcMaxR][kFcMaxR + 1];  // Q1^T Q1 -> R2
-  double R2i[kFcMaxR][kFcMaxR + 1];
-  double R[kFcMaxR][kFcMaxR + 1];  // R = R2 R1
-  double Us[kFcMaxR][kFcMaxR + 1];
-  double Vs[kFcMaxR][kFcMaxR + 1];
-  double Bv[kFcMaxR][kFcMaxR + 1];  // R2^{-1} Vs
-  double R1i[kFcMaxR][kFcMaxR + 1];
-  double red[kFcThreads];
+struct JacSmem {
   double sig[32];
   signed char ptab[31][32];
   int act[32], pos[32];
-  int na, bad;
+  int na;
 };
 
 // circle-method partner of position x among na (even) players in round r
@@ -68,7 +54,7 @@ __device__ __forceinline__ int fc_partner(int x, int r, int na) {
 // (x[i] = M[i][c]); rotations accumulated in v.  Same rotation formula,
 // threshold and negligible-column rule as jacobi32_kernel (jacobi.cu).
 template <int RPW>
-__device__ void fc_jacobi_warp(int r, double (&x)[RPW], double (&v)[RPW], FcShared& sh, int c) {
+__device__ void fc_jacobi_warp(int r, double (&x)[RPW], double (&v)[RPW], JacSmem& sh, int c) {
   double a0 = 0.0;
 #pragma unroll
   for (int k = 0; k < RPW; ++k) a0 = fma(x[k], x[k], a0);
@@ -144,80 +130,382 @@ __device__ void fc_jacobi_warp(int r, double (&x)[RPW], double (&v)[RPW], FcShar
   }
 }
 
+// Cholesky of the c x c SPD matrix G (c <= 16, smem) by ONE warp, in place:
+// G -> R (upper, R^T R = G + shift_rel tr(G) I), Ri = R^{-1}.  Pivots by
+// rsqrt (no division); false (uniform) on a non-positive / non-finite pivot.
+template <int R>
+__device__ bool chol_inv_warp(SmallMat& G, SmallMat& Ri, double* rdiag, double shift_rel, int lane) {
+  constexpr int c = R;
+  if (shift_rel > 0.0) {
+    double tr = 0.0;
+    for (int i = 0; i < c; ++i) tr += G[i][i];
+    __syncwarp();
+    if (lane < c) G[lane][lane] += shift_rel * tr;
+    __syncwarp();
+  }
+  for (int j = 0; j < c; ++j) {
+    const double d = G[j][j];
+    if (!(d > 0.0) || !(d < INFINITY)) return false;
+    const double rs = rsqrt(d);
+    __syncwarp();
+    if (lane >= j && lane < c) G[j][lane] = lane == j ? d * rs : G[j][lane] * rs;
+    if (lane == j) rdiag[j] = rs;
+    __syncwarp();
+    const int w = c - j - 1;
+    for (int e = lane; e < w * w; e += 32) {
+      const int i = j + 1 + e / w, l = j + 1 + e % w;
+      if (l >= i) G[i][l] = fma(-G[j][i], G[j][l], G[i][l]);
+    }
+    __syncwarp();
+  }
+  // column l of R^{-1} by back substitution, lane l, in registers
+  if (lane < c) {
+    double riv[R];
+#pragma unroll
+    for (int i = R - 1; i >= 0; --i) {
+      double acc = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+      for (int q = i + 1; q < R; ++q)
+        if (q <= lane) acc = fma(-G[i][q], riv[q], acc);
+      riv[i] = (i <= lane && i < c) ? acc * rdiag[i] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+      if (i < c) Ri[i][lane] = riv[i];
+  }
+  for (int e = lane; e < c * c; e += 32)
+    if (e % c < e / c) G[e / c][e % c] = 0.0;  // clear the strict lower part
+  __syncwarp();
+  return true;
+}
+
+// ------------------------------------------------------------- Gram pass ----
+// partial[cta] = sum over the CTA's rows of x x^T (r x r), x = Y row, or
+// (Q1) x = y R1^{-1} in a fixed summation order shared with finish_core and
+// finish_rows.  With `tail`, the last CTA to finish (atomic ticket) sums the
+// partials in CTA order and factors them: R1, R1^{-1} (shifted Cholesky).
+constexpr int kGrThreads = 256;
+constexpr int kGrChunk = 256;  // rows staged per step
+
+struct GramTail {
+  int* ticket;       // zero on entry, reset to zero by the last CTA
+  double* R;         // r x r out (upper)
+  double* Rinv;      // r x r out
+  int* flag;         // OR-ed on breakdown
+  double shift_rel;
+};
+
+template <int R>
+__global__ void __launch_bounds__(kGrThreads)
+gram_rows_kernel(int64_t rows, const double* __restrict__ Y, const double* __restrict__ R1i,
+                 int64_t rows_per_cta, double* __restrict__ partial, GramTail tail) {
+  constexpr int r = R;
+  __shared__ __align__(16) double ys[kGrChunk * R];
+  __shared__ SmallMat ri, G, Ri;
+  __shared__ double red[kGrThreads], rdiag[kMR];
+  __shared__ int last;
+  const int tid = threadIdx.x, nout = r * r;
+  const int ng = kGrThreads / nout;  // row groups
+  const int o = tid % nout, rg = tid / nout;
+  const int a = o / r, b = o % r;
+  if (R1i)
+    for (int e = tid; e < nout; e += kGrThreads) ri[e / r][e % r] = R1i[e];
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t r1 = imin64(rows, r0 + rows_per_cta);
+  double acc0 = 0.0, acc1 = 0.0;
+  for (int64_t c0 = r0; c0 < r1; c0 += kGrChunk) {
+    const int nr = (int)imin64(kGrChunk, r1 - c0);
+    for (int e = tid; e < nr * r; e += kGrThreads) cp_async_f64(&ys[e], Y + c0 * r + e, true);
+    cp_async_wait_all();
+    __syncthreads();
+    if (R1i && tid < nr) {  // x = y R1^{-1} in place (thread per row)
+      double x[R], q[R];
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        x[i] = i < r ? ys[tid * r + i] : 0.0;
+        q[i] = 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+        if (i < r) {
+#pragma unroll
+          for (int j = 0; j < R; ++j)
+            if (j < r) q[j] = fma(x[i], ri[i][j], q[j]);
+        }
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+        if (j < r) ys[tid * r + j] = q[j];
+    }
+    __syncthreads();
+    if (rg < ng) {
+      int i = rg;
+      for (; i + ng < nr; i += 2 * ng) {
+        acc0 = fma(ys[i * r + a], ys[i * r + b], acc0);
+        acc1 = fma(ys[(i + ng) * r + a], ys[(i + ng) * r + b], acc1);
+      }
+      if (i < nr) acc0 = fma(ys[i * r + a], ys[i * r + b], acc0);
+    }
+    __syncthreads();
+  }
+  red[tid] = rg < ng ? acc0 + acc1 : 0.0;
+  __syncthreads();
+  if (tid < nout) {
+    double t = 0.0;
+    for (int g = 0; g < ng; ++g) t += red[g * nout + tid];
+    partial[(int64_t)blockIdx.x * nout + tid] = t;
+  }
+  if (!tail.ticket) return;
+  // ---- last CTA: fixed-order reduction of the partials and the factorisation
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = atomicAdd(tail.ticket, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  {
+    const int nb = gridDim.x;
+    double s0 = 0.0, s1 = 0.0;
+    if (rg < ng) {
+      int bb = rg;
+      for (; bb + ng < nb; bb += 2 * ng) {
+        s0 += __ldcg(partial + (int64_t)bb * nout + o);
+        s1 += __ldcg(partial + (int64_t)(bb + ng) * nout + o);
+      }
+      if (bb < nb) s0 += __ldcg(partial + (int64_t)bb * nout + o);
+    }
+    red[tid] = rg < ng ? s0 + s1 : 0.0;
+    __syncthreads();
+    if (tid < nout) {
+      double t = 0.0;
+      for (int g = 0; g < ng; ++g) t += red[g * nout + tid];
+      G[tid / r][tid % r] = t;
+    }
+    __syncthreads();
+  }
+  if (tid < 32) {
+    const bool ok = chol_inv_warp<R>(G, Ri, rdiag, tail.shift_rel, tid);
+    if (!ok) {
+      if (tid == 0) atomicOr(tail.flag, 1);
+    }
+    for (int e = tid; e < nout; e += 32) {
+      tail.R[e] = ok ? G[e / r][e % r] : 0.0;
+      tail.Rinv[e] = ok ? Ri[e / r][e % r] : 0.0;
+    }
+    if (tid == 0) *tail.ticket = 0;
+  }
+}
+
+// ------------------------------------------------------------ the core ----
+// Householder-reconstruction completion (complete.cu header) of the r x k
+// problem X (k x r top rows of an orthonormal N x r factor, smem) for the
+// product factor B (r x r): writes Mf = [B | -B K'] (r x k) and
+// Etf = [0 | E'] (k x k) to global.  Run by a 256-thread group; both groups of
+// the CTA execute the same barrier sequence (same r, k).
+struct HcSmall {
+  SmallMat W, Ui, Li, T, Lp, G, BG;
+  double S[kMR], rd[kMR];
+};
+
+template <int R>
+__device__ void hh_small(int k, const double* __restrict__ X, const SmallMat& B, HcSmall& h,
+                         double* __restrict__ Mf, double* __restrict__ Etf, int t) {
+  constexpr int r = R, nout = R * R;
+  if (t < 32) {
+    // LU without pivoting of X[0:r, 0:r] - S, S_i = -sign(pivot): |pivot| >= 1
+    for (int e = t; e < nout; e += 32) h.W[e / r][e % r] = X[e];
+    __syncwarp();
+    for (int i = 0; i < r; ++i) {
+      const double w = h.W[i][i];
+      const double s = w >= 0.0 ? -1.0 : 1.0;
+      const double piv = w - s;
+      const double rp = 1.0 / piv;
+      __syncwarp();
+      if (t == 0) {
+        h.S[i] = s;
+        h.W[i][i] = piv;
+        h.rd[i] = rp;
+      }
+      if (t > i && t < r) h.W[t][i] *= rp;  // L multipliers
+      __syncwarp();
+      const int w2 = r - i - 1;
+      for (int e = t; e < w2 * w2; e += 32) {
+        const int a = i + 1 + e / w2, b = i + 1 + e % w2;
+        h.W[a][b] = fma(-h.W[a][i], h.W[i][b], h.W[a][b]);
+      }
+      __syncwarp();
+    }
+    // lanes 0..r-1: column of U^{-1}; lanes 16..16+r-1: column of L1^{-1}
+    if (t < r) {
+      const int col = t;
+      double u[R];
+#pragma unroll
+      for (int a = R - 1; a >= 0; --a) {
+        double acc = (a == col) ? 1.0 : 0.0;
+#pragma unroll
+        for (int b = a + 1; b < R; ++b)
+          if (b <= col) acc = fma(-h.W[a][b], u[b], acc);
+        u[a] = (a <= col && a < r) ? acc * h.rd[a] : 0.0;
+      }
+#pragma unroll
+      for (int a = 0; a < R; ++a)
+        if (a < r) h.Ui[a][col] = u[a];
+    } else if (t >= 16 && t < 16 + r) {
+      const int col = t - 16;
+      double l[R];
+#pragma unroll
+      for (int a = 0; a < R; ++a) {
+        double acc = (a == col) ? 1.0 : 0.0;
+#pragma unroll
+        for (int b = 0; b < R; ++b)
+          if (b < a && b >= col) acc = fma(-h.W[a][b], l[b], acc);
+        l[a] = (a >= col && a < r) ? acc : 0.0;
+      }
+#pragma unroll
+      for (int a = 0; a < R; ++a)
+        if (a < r) h.Li[a][col] = l[a];
+    }
+  }
+  __syncthreads();
+  const int a = t / r, b = t % r;
+  const bool act = t < nout;
+  if (act) {  // T = -U S L1^{-T}
+    double acc = 0.0;
+    for (int q = a; q < r; ++q) acc = fma(h.W[a][q] * h.S[q], h.Li[b][q], acc);
+    h.T[a][b] = -acc;
+  }
+  __syncthreads();
+  if (act) {  // Lp = T U^{-T}
+    double acc = 0.0;
+    for (int q = b; q < r; ++q) acc = fma(h.T[a][q], h.Ui[b][q], acc);
+    h.Lp[a][b] = acc;
+  }
+  __syncthreads();
+  if (act) {  // G = U^{-1} Lp
+    double acc = 0.0;
+    for (int q = a; q < r; ++q) acc = fma(h.Ui[a][q], h.Lp[q][b], acc);
+    h.G[a][b] = acc;
+  }
+  __syncthreads();
+  if (act) {  // BG = B G
+    double acc = 0.0;
+    for (int q = 0; q < r; ++q) acc = fma(B[a][q], h.G[q][b], acc);
+    h.BG[a][b] = acc;
+  }
+  __syncthreads();
+  // Mf[i][j] = B[i][j] (j < r), -sum_p BG[i][p] X[j][p] (j >= r)
+  for (int e = t; e < r * k; e += 256) {
+    const int i = e / k, j = e % k;
+    double v;
+    if (j < r) {
+      v = B[i][j];
+    } else {
+      double acc = 0.0;
+#pragma unroll
+      for (int p = 0; p < R; ++p)
+        if (p < r) acc = fma(h.BG[i][p], X[j * r + p], acc);
+      v = -acc;
+    }
+    Mf[e] = v;
+  }
+  // Etf[i][j] = 0 (j < r); S_i sum_p G[i][p] X[j][p] (i < r <= j); I (i, j >= r)
+  for (int e = t; e < k * k; e += 256) {
+    const int i = e / k, j = e % k;
+    double v = 0.0;
+    if (j >= r) {
+      if (i < r) {
+        double acc = 0.0;
+#pragma unroll
+        for (int p = 0; p < R; ++p)
+          if (p < r) acc = fma(h.G[i][p], X[j * r + p], acc);
+        v = h.S[i] * acc;
+      } else {
+        v = (i == j) ? 1.0 : 0.0;
+      }
+    }
+    Etf[e] = v;
+  }
+}
+
+constexpr int kFcThreads = 512;
+
+struct FcShared {
+  HcSmall hc[2];
+  SmallMat G, R2i, R1, R1i, R, Us, Vs, Bv;
+  JacSmem jac;
+  double red[kFcThreads];
+  double rdiag[kMR];
+  int bad;
+  // followed by Zt, Yt (k x r), XU, XV (k x r)
+};
+
 // S (k): sigma desc, zero padded; MfU / MfV (r x k), EtfU / EtfV (k x k):
 // U = Z MfU + [EtfU; 0],  V = (Y R1^{-1}) MfV + [EtfV; 0].
-// ws: scratch of 2 (k r + r (k-r) + k (k-r)) doubles.
-template <int RPW>
+template <int R>
 __global__ void __launch_bounds__(kFcThreads)
-finish_core_kernel(int r, int k, int nb2, const double* __restrict__ P2, const double* __restrict__ R1,
-                   const double* __restrict__ R1i, const double* __restrict__ Z, int64_t ldz,
-                   const double* __restrict__ Y, int64_t ldy, double* __restrict__ S, double* __restrict__ ws,
+finish_core_kernel(int k, int nb2, const double* __restrict__ P2, const double* __restrict__ R1g,
+                   const double* __restrict__ R1ig, const double* __restrict__ Z, int64_t ldz,
+                   const double* __restrict__ Y, int64_t ldy, double* __restrict__ S,
                    double* __restrict__ MfU, double* __restrict__ EtfU, double* __restrict__ MfV,
                    double* __restrict__ EtfV, int* flag) {
   extern __shared__ __align__(16) unsigned char fc_smem[];
   FcShared& sh = *reinterpret_cast<FcShared*>(fc_smem);
-  const int tid = threadIdx.x, nout = r * r;
+  double* Zt = reinterpret_cast<double*>(fc_smem + (sizeof(FcShared) + 15) / 16 * 16);
+  constexpr int r = R, nout = R * R, RPW = R < 2 ? 2 : R + (R & 1);
+  double* Yt = Zt + k * r;
+  double* XU = Yt + k * r;
+  double* XV = XU + k * r;
+  const int tid = threadIdx.x;
+  SPB_TDECL;
+  SPB_TMARK(0);
   if (tid == 0) sh.bad = 0;
-  for (int e = tid; e < nout; e += kFcThreads) sh.R1i[e / r][e % r] = R1i[e];
-  // (a) fixed-order reduction of the nb2 partial Grams of Q1
+  for (int e = tid; e < nout; e += kFcThreads) {
+    cp_async_f64(&sh.R1[e / r][e % r], R1g + e, true);
+    cp_async_f64(&sh.R1i[e / r][e % r], R1ig + e, true);
+  }
+  for (int e = tid; e < k * r; e += kFcThreads) {
+    const int i = e / r, l = e % r;
+    cp_async_f64(&Zt[e], Z + (int64_t)i * ldz + l, true);
+    cp_async_f64(&Yt[e], Y + (int64_t)i * ldy + l, true);
+  }
+  // (a) fixed-order reduction of the nb2 partial Grams of Q1 (loads in flight)
   {
-    const int gs = kFcThreads / nout;  // >= 2 for r <= 16
-    const int o = tid / gs, g = tid % gs;
-    double a = 0.0;
-    if (o < nout)
-      for (int b = g; b < nb2; b += gs) a += P2[(int64_t)b * nout + o];
-    sh.red[tid] = a;
+    const int gs = kFcThreads / nout;
+    const int o = tid % nout, g = tid / nout;
+    double a0 = 0.0, a1 = 0.0;
+    if (g < gs) {
+      int b = g;
+      for (; b + gs < nb2; b += 2 * gs) {
+        a0 += P2[(int64_t)b * nout + o];
+        a1 += P2[(int64_t)(b + gs) * nout + o];
+      }
+      if (b < nb2) a0 += P2[(int64_t)b * nout + o];
+    }
+    sh.red[tid] = g < gs ? a0 + a1 : 0.0;
+    cp_async_wait_all();
     __syncthreads();
-    if (g == 0 && o < nout) {
-      double t = sh.red[tid];
-      for (int q = 1; q < gs; ++q) t += sh.red[tid + q];
-      sh.G[o / r][o % r] = t;
+    if (tid < nout) {
+      double t = 0.0;
+      for (int q = 0; q < gs; ++q) t += sh.red[q * nout + tid];
+      sh.G[tid / r][tid % r] = t;
     }
     __syncthreads();
   }
-  // (b) warp 0: Cholesky Q1^T Q1 = R2^T R2, R2^{-1}, R = R2 R1, Jacobi of R^T
+  SPB_TMARK(1);
+  // (b) warp 0: R2 (Cholesky of Q1^T Q1), R = R2 R1, Jacobi SVD of R^T
   if (tid < 32) {
     const int lane = tid;
-    bool bad = false;
-    for (int j = 0; j < r; ++j) {
-      const double d = sh.G[j][j];
-      if (!(d > 0.0)) {
-        bad = true;
-        break;
-      }
-      const double dinv = 1.0 / d;
-      const int w2 = r - j - 1;
-      for (int e = lane; e < w2 * w2; e += 32) {
-        const int i = j + 1 + e / w2, l = j + 1 + e % w2;
-        if (l >= i) sh.G[i][l] = fma(-sh.G[j][i] * dinv, sh.G[j][l], sh.G[i][l]);
-      }
-      __syncwarp();
-    }
-    if (bad) {
+    const bool ok = chol_inv_warp<R>(sh.G, sh.R2i, sh.rdiag, 0.0, lane);
+    if (!ok) {
       if (lane == 0) sh.bad = 1;
     } else {
-      if (lane < r) sh.sig[lane] = sqrt(sh.G[lane][lane]);
-      __syncwarp();
-      for (int e = lane; e < nout; e += 32) {
-        const int i = e / r, l = e % r;
-        sh.G[i][l] = (l > i) ? sh.G[i][l] / sh.sig[i] : (l == i ? sh.sig[i] : 0.0);
-      }
-      __syncwarp();
-      if (lane < r) {  // column l of R2^{-1} by back substitution
-        const int l = lane;
-        for (int i = r - 1; i >= 0; --i) {
-          double acc = (i == l) ? 1.0 : 0.0;
-          for (int q = i + 1; q <= l; ++q) acc = fma(-sh.G[i][q], sh.R2i[q][l], acc);
-          sh.R2i[i][l] = (i <= l) ? acc / sh.G[i][i] : 0.0;
-        }
-      }
       for (int e = lane; e < nout; e += 32) {
         const int i = e / r, l = e % r;
         double acc = 0.0;
-        for (int q = i; q <= l; ++q) acc = fma(sh.G[i][q], R1[q * r + l], acc);
+        for (int q = i; q <= l; ++q) acc = fma(sh.G[i][q], sh.R1[q][l], acc);
         sh.R[i][l] = (l >= i) ? acc : 0.0;
       }
       __syncwarp();
+      SPB_TMARK(2);
       // M = R^T: lane c holds column c of M = row c of R
       double x[RPW], v[RPW];
 #pragma unroll
@@ -225,17 +513,18 @@ finish_core_kernel(int r, int k, int nb2, const double* __restrict__ P2, const d
         x[i] = (i < r && lane < r) ? sh.R[lane][i] : 0.0;
         v[i] = (i == lane) ? 1.0 : 0.0;
       }
-      fc_jacobi_warp<RPW>(r, x, v, sh, lane);
+      fc_jacobi_warp<RPW>(r, x, v, sh.jac, lane);
+      SPB_TMARK(3);
       double a1 = 0.0;
 #pragma unroll
       for (int i = 0; i < RPW; ++i) a1 = fma(x[i], x[i], a1);
       const double sc = sqrt(a1);
       __syncwarp();
-      sh.sig[lane] = lane < r ? sc : -1.0;
+      sh.jac.sig[lane] = lane < r ? sc : -1.0;
       __syncwarp();
       int rank = 0;
       for (int d = 0; d < 32; ++d) {
-        const double sd = sh.sig[d];
+        const double sd = sh.jac.sig[d];
         rank += (sd > sc || (sd == sc && d < lane)) ? 1 : 0;
       }
       if (lane < r) {
@@ -257,60 +546,70 @@ finish_core_kernel(int r, int k, int nb2, const double* __restrict__ P2, const d
     for (int j = tid; j < k; j += kFcThreads) S[j] = __longlong_as_double(0x7ff8000000000000ll);
     return;  // uniform
   }
-  // (c) Bv = R2^{-1} Vs; top k rows: XU = Z[0:k] Us, XV = (Y[0:k] R1^{-1}) Bv
-  for (int e = tid; e < nout; e += kFcThreads) {
-    const int i = e / r, l = e % r;
+  SPB_TMARK(4);
+  // (c) Bv = R2^{-1} Vs; Q1 top rows = Yt R1^{-1} (in place); XU = Zt Us
+  if (tid < nout) {
+    const int i = tid / r, l = tid % r;
     double acc = 0.0;
     for (int q = i; q < r; ++q) acc = fma(sh.R2i[i][q], sh.Vs[q][l], acc);
     sh.Bv[i][l] = acc;
   }
-  __syncthreads();
-  const int kr = k - r;
-  double* XU = ws;
-  double* XV = XU + (size_t)k * r;
-  double* KpU = XV + (size_t)k * r;
-  double* KpV = KpU + (size_t)r * kr;
-  double* EtU = KpV + (size_t)r * kr;
-  double* EtV = EtU + (size_t)k * kr;
   for (int e = tid; e < k * r; e += kFcThreads) {
     const int i = e / r, l = e % r;
-    double au = 0.0, av = 0.0;
-    for (int p = 0; p < r; ++p) {
-      au = fma(Z[(int64_t)i * ldz + p], sh.Us[p][l], au);
-      // q1[i][p] in mul_gram's order (sum over the input columns from 0)
-      double q1 = 0.0;
-      for (int t = 0; t < r; ++t) q1 = fma(Y[(int64_t)i * ldy + t], sh.R1i[t][p], q1);
-      av = fma(q1, sh.Bv[p][l], av);
-    }
+    double au = 0.0, q1 = 0.0;
+#pragma unroll
+    for (int p = 0; p < R; ++p)
+      if (p < r) {
+        au = fma(Zt[i * r + p], sh.Us[p][l], au);
+        q1 = fma(Yt[i * r + p], sh.R1i[p][l], q1);  // x = y R1^{-1}, gram_rows' order
+      }
     XU[e] = au;
-    XV[e] = av;
+    XV[e] = q1;  // parked; XV = Q1top Bv below
   }
   __syncthreads();
+  {
+    // XV = Q1top Bv (Q1top parked in XV, copy through registers)
+    double qv[(R * 256 + kFcThreads - 1) / kFcThreads];
+    int cnt = 0;
+    for (int e = tid; e < k * r; e += kFcThreads, ++cnt) {
+      const int i = e / r, l = e % r;
+      double acc = 0.0;
+#pragma unroll
+      for (int p = 0; p < R; ++p)
+        if (p < r) acc = fma(XV[i * r + p], sh.Bv[p][l], acc);
+      qv[cnt] = acc;
+    }
+    __syncthreads();
+    cnt = 0;
+    for (int e = tid; e < k * r; e += kFcThreads, ++cnt) XV[e] = qv[cnt];
+  }
+  __syncthreads();
+  SPB_TMARK(5);
   // (d) both completions at once: threads [0, 256) -> U, [256, 512) -> V
   const int grp = tid >> 8;
-  __shared__ double BuS[kFcMaxR * kFcMaxR], BvS[kFcMaxR * kFcMaxR];
-  for (int e = tid; e < nout; e += kFcThreads) {
-    BuS[e] = sh.Us[e / r][e % r];
-    BvS[e] = sh.Bv[e / r][e % r];
-  }
-  __syncthreads();
-  hh_complete_dev(r, k, grp ? XV : XU, r, grp ? KpV : KpU, grp ? EtV : EtU, kr, grp ? BvS : BuS, r,
-                  grp ? MfV : MfU, grp ? EtfV : EtfU, sh.hc[grp], tid & 255, 256);
+  hh_small<R>(k, grp ? XV : XU, grp ? sh.Bv : sh.Us, sh.hc[grp], grp ? MfV : MfU, grp ? EtfV : EtfU, tid & 255);
+  SPB_TMARK(6);
+  if (tid == 0) SPB_TPRINT("finish_core reduce/chol/jacobi/sort/xtop/hh", 7);
 }
 
 // One streaming pass: rows [0, m) of U (blocks [0, bu)) and [0, n) of V.
+// A CTA owns 128 rows: threads 0..127 form the row inputs (for V, q1 = y
+// R1^{-1} in gram_rows' summation order) into shared memory; then each warp
+// writes 16 whole rows, lanes across the k output columns (coalesced
+// stores, no index division).
 constexpr int kFrRows = 128;
+constexpr int kFrThreads = 256;
 
-__global__ void __launch_bounds__(kFrRows)
-finish_rows_kernel(int r, int k, int64_t m, int64_t n, int bu, const double* __restrict__ Z, int64_t ldz,
+template <int R>
+__global__ void __launch_bounds__(kFrThreads)
+finish_rows_kernel(int k, int64_t m, int64_t n, int bu, const double* __restrict__ Z, int64_t ldz,
                    const double* __restrict__ Y, int64_t ldy, const double* __restrict__ R1i,
                    const double* __restrict__ MfU, const double* __restrict__ EtfU, const double* __restrict__ MfV,
-                   const double* __restrict__ EtfV, double* __restrict__ U, int64_t ldu, double* __restrict__ V,
-                   int64_t ldv) {
+                   const double* __restrict__ EtfV, double* __restrict__ U, double* __restrict__ V) {
   extern __shared__ __align__(16) double fr_smem[];
-  double* mf = fr_smem;                    // r x k
-  double* ri = mf + r * k;                 // r x r
-  double* st = ri + kFcMaxR * kFcMaxR;     // kFrRows x 33 staging
+  double* mf = fr_smem;               // R x k
+  double* ri = mf + R * k;            // R x R
+  double* qs = ri + R * R;            // kFrRows x (R + 1)
   const bool isv = blockIdx.x >= bu;
   const int64_t rows = isv ? n : m;
   const int64_t base = (int64_t)(isv ? blockIdx.x - bu : blockIdx.x) * kFrRows;
@@ -319,102 +618,109 @@ finish_rows_kernel(int r, int k, int64_t m, int64_t n, int bu, const double* __r
   const double* Mf = isv ? MfV : MfU;
   const double* Et = isv ? EtfV : EtfU;
   double* O = isv ? V : U;
-  const int64_t ldo = isv ? ldv : ldu;
   const int t = threadIdx.x;
-  for (int e = t; e < r * k; e += kFrRows) cp_async_f64(&mf[e], Mf + e, true);
+  for (int e = t; e < R * k; e += kFrThreads) cp_async_f64(&mf[e], Mf + e, true);
   if (isv)
-    for (int e = t; e < r * r; e += kFrRows) cp_async_f64(&ri[e], R1i + e, true);
+    for (int e = t; e < R * R; e += kFrThreads) cp_async_f64(&ri[e], R1i + e, true);
   const int nr = (int)imin64(kFrRows, rows - base);
-  double x[kFcMaxR];
-  const int64_t row = base + t;
+  double x[R];
 #pragma unroll
-  for (int i = 0; i < kFcMaxR; ++i) x[i] = (t < nr && i < r) ? X[row * ldx + i] : 0.0;
+  for (int i = 0; i < R; ++i) x[i] = t < nr ? X[(base + t) * ldx + i] : 0.0;
   cp_async_wait_all();
   __syncthreads();
-  if (isv) {  // q1 = y R1^{-1}, mul_gram's summation order
-    double q[kFcMaxR];
+  if (t < kFrRows) {
+    if (isv) {  // q1 = y R1^{-1}, gram_rows' summation order
+      double q[R];
 #pragma unroll
-    for (int j = 0; j < kFcMaxR; ++j) q[j] = 0.0;
+      for (int j = 0; j < R; ++j) q[j] = 0.0;
 #pragma unroll
-    for (int i = 0; i < kFcMaxR; ++i)
-      if (i < r) {
+      for (int i = 0; i < R; ++i)
 #pragma unroll
-        for (int j = 0; j < kFcMaxR; ++j)
-          if (j < r) q[j] = fma(x[i], ri[i * r + j], q[j]);
-      }
+        for (int j = 0; j < R; ++j) q[j] = fma(x[i], ri[i * R + j], q[j]);
 #pragma unroll
-    for (int j = 0; j < kFcMaxR; ++j) x[j] = q[j];
+      for (int j = 0; j < R; ++j) x[j] = q[j];
+    }
+#pragma unroll
+    for (int j = 0; j < R; ++j) qs[t * (R + 1) + j] = x[j];
   }
-  const bool top = t < nr && row < k;
-  for (int c0 = 0; c0 < k; c0 += 32) {
-    const int cw = k - c0 < 32 ? k - c0 : 32;
-    for (int cc = 0; cc < cw; ++cc) {
+  __syncthreads();
+  const int warp = t >> 5, lane = t & 31;
+  for (int rl = warp; rl < nr; rl += kFrThreads / 32) {
+    double q[R];
+#pragma unroll
+    for (int p = 0; p < R; ++p) q[p] = qs[rl * (R + 1) + p];
+    const int64_t row = base + rl;
+    double* orow = O + row * k;
+    for (int c = lane; c < k; c += 32) {
       double o = 0.0;
 #pragma unroll
-      for (int p = 0; p < kFcMaxR; ++p)
-        if (p < r) o = fma(x[p], mf[p * k + c0 + cc], o);
-      if (top) o += Et[row * k + c0 + cc];
-      st[t * 33 + cc] = o;
+      for (int p = 0; p < R; ++p) o = fma(q[p], mf[p * k + c], o);
+      if (row < k) o += Et[row * k + c];
+      orow[c] = o;
     }
-    __syncthreads();
-    for (int e = t; e < nr * cw; e += kFrRows) {
-      const int rl = e / cw, cl = e % cw;
-      O[(base + rl) * ldo + c0 + cl] = st[rl * 33 + cl];
-    }
-    __syncthreads();
   }
 }
 
 bool finish_fused_ok(int64_t m, int64_t n, int r, int k) {
-  return r >= 1 && r <= kFcMaxR && k >= r && k <= kHcMaxK && r * k <= 64 * 64 && m >= k && n >= k &&
-         n >= 256;
+  return r >= 1 && r <= kFcMaxR && k >= r && k <= 256 && r * k <= 64 * 64 && m >= k && n >= k && n >= 256;
 }
 
 // Y (n x r, ld r) = A^T Z is in place; writes U (m x k), S (k), V (n x k).
-// dflag: device int, OR-ed on a Cholesky breakdown / non-finite input.
-int finish_fused(int64_t m, int64_t n, const double* Z, int64_t ldz, const double* Y, int r, int k, double* U,
-                 double* S, double* V, int* dflag, cudaStream_t s) {
-  SPB_REQUIRE(finish_fused_ok(m, n, r, k), "finish_fused limits exceeded");
+// dflag: device int[2] = {flag, ticket}, zeroed by the caller; the flag is
+// OR-ed on a Cholesky breakdown / non-finite input.
+template <int R>
+static int finish_fused_r(int64_t m, int64_t n, const double* Z, int64_t ldz, const double* Y, int k, double* U,
+                          double* S, double* V, int* dflag, cudaStream_t s) {
   Arena ar(s);
-  const int nb1max = (int)std::min<int64_t>(4 * kNumSMs, ceil_div(n, 128));
-  const int tiles = mul_gram_tiles(n);
-  const int nb2 = ceil_div(n, (int64_t)128 * tiles);
-  const int kr = k - r;
-  SPB_ALLOC(ar, double, P1, (size_t)nb1max * r * r);
-  SPB_ALLOC(ar, double, P2, (size_t)nb2 * r * r);
-  SPB_ALLOC(ar, double, R1, (size_t)r * r);
-  SPB_ALLOC(ar, double, R1i, (size_t)r * r);
-  SPB_ALLOC(ar, double, Mf, (size_t)2 * r * k + 2 * (size_t)k * k);
-  SPB_ALLOC(ar, double, ws, (size_t)2 * ((size_t)k * r + (size_t)r * kr + (size_t)k * kr));
+  const int nb = (int)std::min<int64_t>(kNumSMs, ceil_div(n, 64));
+  const int64_t rpc = ceil_div(n, nb);
+  SPB_ALLOC(ar, double, P1, (size_t)nb * R * R);
+  SPB_ALLOC(ar, double, P2, (size_t)nb * R * R);
+  SPB_ALLOC(ar, double, R1, (size_t)R * R);
+  SPB_ALLOC(ar, double, R1i, (size_t)R * R);
+  SPB_ALLOC(ar, double, Mf, (size_t)2 * R * k + 2 * (size_t)k * k);
   double* MfU = Mf;
-  double* MfV = MfU + (size_t)r * k;
-  double* EtfU = MfV + (size_t)r * k;
+  double* MfV = MfU + (size_t)R * k;
+  double* EtfU = MfV + (size_t)R * k;
   double* EtfV = EtfU + (size_t)k * k;
-  int nb1 = 0;
-  SPB_TRY(tall_gram_partials(n, r, Y, r, r, Y, r, P1, nb1max, &nb1, s));
-  SPB_TRY(chol_small_launch(r, nb1, P1, R1, R1i, dflag, 16.0 * r * 2.220446049250313e-16, s));
-  int nb2o = 0;
-  SPB_TRY(mul_gram_launch(n, r, Y, r, R1i, nullptr, r, P2, &nb2o, s));
-  const size_t fc_smem = sizeof(FcShared);
-  if (r <= 8) {
-    SPB_CUDA(cudaFuncSetAttribute(finish_core_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fc_smem));
-    finish_core_kernel<8><<<1, kFcThreads, fc_smem, s>>>(r, k, nb2o, P2, R1, R1i, Z, ldz, Y, r, S, ws, MfU, EtfU,
-                                                         MfV, EtfV, dflag);
-  } else {
-    SPB_CUDA(cudaFuncSetAttribute(finish_core_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fc_smem));
-    finish_core_kernel<16><<<1, kFcThreads, fc_smem, s>>>(r, k, nb2o, P2, R1, R1i, Z, ldz, Y, r, S, ws, MfU, EtfU,
-                                                          MfV, EtfV, dflag);
-  }
+  GramTail t1{dflag + 1, R1, R1i, dflag, 16.0 * R * 2.220446049250313e-16};
+  gram_rows_kernel<R><<<nb, kGrThreads, 0, s>>>(n, Y, nullptr, rpc, P1, t1);
+  GramTail t2{nullptr, nullptr, nullptr, nullptr, 0.0};
+  gram_rows_kernel<R><<<nb, kGrThreads, 0, s>>>(n, Y, R1i, rpc, P2, t2);
+  count_launch(2);
+  SPB_CHECK_LAUNCH();
+  const size_t fc_smem = (sizeof(FcShared) + 15) / 16 * 16 + (size_t)4 * k * R * sizeof(double);
+  SPB_CUDA(cudaFuncSetAttribute(finish_core_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fc_smem));
+  finish_core_kernel<R><<<1, kFcThreads, fc_smem, s>>>(k, nb, P2, R1, R1i, Z, ldz, Y, R, S, MfU, EtfU, MfV, EtfV,
+                                                       dflag);
   count_launch();
   SPB_CHECK_LAUNCH();
   const int bu = ceil_div(m, kFrRows), bv = ceil_div(n, kFrRows);
-  const size_t fr_smem = ((size_t)r * k + kFcMaxR * kFcMaxR + (size_t)kFrRows * 33) * sizeof(double);
-  SPB_CUDA(cudaFuncSetAttribute(finish_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fr_smem));
-  finish_rows_kernel<<<bu + bv, kFrRows, fr_smem, s>>>(r, k, m, n, bu, Z, ldz, Y, r, R1i, MfU, EtfU, MfV, EtfV,
-                                                       U, k, V, k);
+  const size_t fr_smem = ((size_t)R * k + R * R + (size_t)kFrRows * (R + 1)) * sizeof(double);
+  SPB_CUDA(cudaFuncSetAttribute(finish_rows_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fr_smem));
+  finish_rows_kernel<R><<<bu + bv, kFrThreads, fr_smem, s>>>(k, m, n, bu, Z, ldz, Y, R, R1i, MfU, EtfU, MfV, EtfV,
+                                                             U, V);
   count_launch();
   SPB_CHECK_LAUNCH();
   return SP_OK;
+}
+
+// Y (n x r, ld r) = A^T Z is in place; writes U (m x k), S (k), V (n x k).
+// dflag: device int[2] = {flag, ticket}, zeroed by the caller; the flag is
+// OR-ed on a Cholesky breakdown / non-finite input.
+int finish_fused(int64_t m, int64_t n, const double* Z, int64_t ldz, const double* Y, int r, int k, double* U,
+                 double* S, double* V, int* dflag, cudaStream_t s) {
+  SPB_REQUIRE(finish_fused_ok(m, n, r, k), "finish_fused limits exceeded");
+  switch (r) {
+#define SPB_FF(RR) \
+  case RR:         \
+    return finish_fused_r<RR>(m, n, Z, ldz, Y, k, U, S, V, dflag, s);
+    SPB_FF(1) SPB_FF(2) SPB_FF(3) SPB_FF(4) SPB_FF(5) SPB_FF(6) SPB_FF(7) SPB_FF(8)
+    SPB_FF(9) SPB_FF(10) SPB_FF(11) SPB_FF(12) SPB_FF(13) SPB_FF(14) SPB_FF(15) SPB_FF(16)
+#undef SPB_FF
+  }
+  set_error("finish_fused: unsupported rank");
+  return SP_ECONFIG;
 }
 
 }  // namespace spb

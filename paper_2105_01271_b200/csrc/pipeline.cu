@@ -286,8 +286,8 @@ static int finish_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t 
   if (r > 0 && t_finish_mode == 0 && kappa_est < 1e6 && finish_fused_ok(m, n, r, k)) {
     // A pass + fused shifted-CholeskyQR2 / Jacobi / completion: no host sync
     SPB_ALLOC(ar, double, Y, (size_t)n * r);
-    SPB_ALLOC(ar, int, dflag, 1);
-    SPB_CUDA(cudaMemsetAsync(dflag, 0, sizeof(int), s));
+    SPB_ALLOC(ar, int, dflag, 2);  // {flag, ticket}
+    SPB_CUDA(cudaMemsetAsync(dflag, 0, 2 * sizeof(int), s));
     SPB_TRY(skinny_atz(A, a_dtype, m, n, lda, Z, ldz, r, Y, r, s));
     SPB_TRY(finish_fused(m, n, Z, ldz, Y, r, k, U, S, V, dflag, s));
     return defer_flag(dflag, s);

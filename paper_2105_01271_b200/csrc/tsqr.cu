@@ -110,7 +110,13 @@ tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t l
   // update columns c > j only, uniformly across the warp:
   //   x_c -= x_j * (inv_j * w_c),  w_c = tau_j v_j^T x_c.
   int buf = 0;
+#ifdef SPB_TSQR_TRACE
+  long long tr_a = 0, tr_b = 0, tr_c = 0, tr_beg = clock64(), tr_s0, tr_s1, tr_s2;
+#endif
   for (int j = 0; j < nref; ++j) {
+#ifdef SPB_TSQR_TRACE
+    tr_s0 = clock64();
+#endif
     // (1) lane j publishes its column (my warp's rows) through shared memory;
     // partial <x_j, x_c> over my rows
     if (c == j) {
@@ -147,6 +153,10 @@ tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t l
       rowj[buf][c] = rj;
     }
     __syncthreads();
+#ifdef SPB_TSQR_TRACE
+    tr_s1 = clock64();
+    tr_a += tr_s1 - tr_s0;
+#endif
     // (2) reflector scalars (every thread of the cluster, same order: identical values)
     double dc, sigma2, alpha, ac;
     {
@@ -199,6 +209,10 @@ tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t l
       alpha = rowj[buf][j];
       ac = rowj[buf][c];
     }
+#ifdef SPB_TSQR_TRACE
+    tr_s2 = clock64();
+    tr_b += tr_s2 - tr_s1;
+#endif
     double beta = alpha, tj = 0.0, inv = 0.0;
     if (sigma2 > 0.0) {
       // one rsqrt and one division: nrm = s2 / sqrt(s2), tau = -(alpha - beta) / beta
@@ -228,7 +242,15 @@ tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t l
       beta_s[j] = beta;
     }
     buf ^= 1;
+#ifdef SPB_TSQR_TRACE
+    tr_c += clock64() - tr_s2;
+#endif
   }
+#ifdef SPB_TSQR_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < cl)
+    printf("tsqr_leaf rows=%lld cl=%d rank=%d steps=%d: loop %lld cyc; per step dots+sync %lld, exchange %lld, scalars+update %lld\n",
+           (long long)rows, cl, cr, nref, clock64() - tr_beg, tr_a / nref, tr_b / nref, tr_c / nref);
+#endif
   if (cl > 1) cluster.sync();  // no CTA leaves while peers' pushes are in flight
   __syncthreads();
   // reflectors (coalesced rows)
