@@ -645,6 +645,33 @@ finish_rows_kernel(int k, int64_t m, int64_t n, int bu, const double* __restrict
   }
   __syncthreads();
   const int warp = t >> 5, lane = t & 31;
+  if (k <= 64) {
+    // the lane's (up to) two output columns of Mf stay in registers
+    double m0[R], m1[R];
+#pragma unroll
+    for (int p = 0; p < R; ++p) {
+      m0[p] = lane < k ? mf[p * k + lane] : 0.0;
+      m1[p] = lane + 32 < k ? mf[p * k + lane + 32] : 0.0;
+    }
+    for (int rl = warp; rl < nr; rl += kFrThreads / 32) {
+      double o0 = 0.0, o1 = 0.0;
+#pragma unroll
+      for (int p = 0; p < R; ++p) {
+        const double q = qs[rl * (R + 1) + p];
+        o0 = fma(q, m0[p], o0);
+        o1 = fma(q, m1[p], o1);
+      }
+      const int64_t row = base + rl;
+      double* orow = O + row * k;
+      if (row < k) {
+        if (lane < k) o0 += Et[row * k + lane];
+        if (lane + 32 < k) o1 += Et[row * k + lane + 32];
+      }
+      if (lane < k) orow[lane] = o0;
+      if (lane + 32 < k) orow[lane + 32] = o1;
+    }
+    return;
+  }
   for (int rl = warp; rl < nr; rl += kFrThreads / 32) {
     double q[R];
 #pragma unroll
@@ -690,14 +717,20 @@ static int finish_fused_r(int64_t m, int64_t n, const double* Z, int64_t ldz, co
   count_launch(2);
   SPB_CHECK_LAUNCH();
   const size_t fc_smem = (sizeof(FcShared) + 15) / 16 * 16 + (size_t)4 * k * R * sizeof(double);
-  SPB_CUDA(cudaFuncSetAttribute(finish_core_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fc_smem));
+  static int attr_dev = -1;  // once per device: host overhead is on the critical path here
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    SPB_CUDA(cudaFuncSetAttribute(finish_core_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    SPB_CUDA(cudaFuncSetAttribute(finish_rows_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+    attr_dev = dev;
+  }
   finish_core_kernel<R><<<1, kFcThreads, fc_smem, s>>>(k, nb, P2, R1, R1i, Z, ldz, Y, R, S, MfU, EtfU, MfV, EtfV,
                                                        dflag);
   count_launch();
   SPB_CHECK_LAUNCH();
   const int bu = ceil_div(m, kFrRows), bv = ceil_div(n, kFrRows);
   const size_t fr_smem = ((size_t)R * k + R * R + (size_t)kFrRows * (R + 1)) * sizeof(double);
-  SPB_CUDA(cudaFuncSetAttribute(finish_rows_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fr_smem));
   finish_rows_kernel<R><<<bu + bv, kFrThreads, fr_smem, s>>>(k, m, n, bu, Z, ldz, Y, R, R1i, MfU, EtfU, MfV, EtfV,
                                                              U, V);
   count_launch();

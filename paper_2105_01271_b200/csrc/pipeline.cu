@@ -14,7 +14,9 @@
 // When s0 and C are the same column set (every BASELINE configuration),
 // sigma(G) = sigma(C)^(2q+1) and U_G = U_C, so G is never formed and the kept
 // basis is accurate to ~1e-16 sigma_1 instead of ~1e-16 sigma_1(G).
+#include <atomic>
 #include <cmath>
+#include <cstring>
 #include <vector>
 
 #include "common.cuh"
@@ -24,6 +26,9 @@
 namespace spb {
 
 constexpr double kRankTol = 1e-12;  // src/kernels.py:19
+
+int srht_sketch(int64_t rows, int64_t cols, const double* X, int64_t ldx, int b, uint64_t seed, double* Y,
+                int64_t ldy, int* flag, cudaStream_t s);
 
 static int count_kept(const std::vector<double>& s, double power) {
   if (s.empty() || !(s[0] > 0.0)) return 0;
@@ -62,6 +67,74 @@ struct PendingFlag {
 static int read_flag_with(const PendingFlag& pf, int& host_flag, PinnedReads& rd) {
   host_flag = 0;
   if (pf.dev) SPB_TRY(rd.add(&host_flag, pf.dev, sizeof(int)));
+  return SP_OK;
+}
+
+// -------------------------------------------------------------- doorbell ----
+// Low-latency publication of a small device result (a Ritz spectrum and a
+// pending flag) to the host: a one-CTA kernel copies it into mapped pinned
+// memory and then bumps a sequence word, on which the host spins.  Replaces
+// a device->host copy + stream synchronisation (copy-engine and wake-up
+// latency) on the one host decision of the pipeline, the kept rank.
+struct Doorbell {
+  unsigned char* h = nullptr;  // [seq (u32) | flag (i32) | pad | values (f64)]
+  unsigned next = 0;
+};
+static thread_local Doorbell t_bell;
+constexpr int kBellMax = 1024;  // doubles
+
+__global__ void publish_kernel(const double* __restrict__ v, int nv, const int* __restrict__ flag,
+                               unsigned char* __restrict__ bell, unsigned seq) {
+  double* hv = reinterpret_cast<double*>(bell + 16);
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) hv[i] = v[i];
+  if (threadIdx.x == 0) *reinterpret_cast<volatile int*>(bell + 4) = flag ? *flag : 0;
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) *reinterpret_cast<volatile unsigned*>(bell) = seq;
+}
+
+// enqueue the publication of v[0:nv) (+ *flag) on s; returns the sequence number
+static int bell_publish(const double* v, int nv, const int* flag, unsigned& seq, cudaStream_t s) {
+  if (nv > kBellMax) {
+    set_error("doorbell payload too large");
+    return SP_ECUDA;
+  }
+  if (!t_bell.h) {
+    void* p = nullptr;
+    SPB_CUDA(cudaHostAlloc(&p, 16 + kBellMax * sizeof(double), cudaHostAllocMapped | cudaHostAllocPortable));
+    std::memset(p, 0, 16);
+    t_bell.h = static_cast<unsigned char*>(p);
+  }
+  seq = ++t_bell.next;
+  if (seq == 0) seq = ++t_bell.next;
+  unsigned char* d = nullptr;
+  SPB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d), t_bell.h, 0));
+  publish_kernel<<<1, 128, 0, s>>>(v, nv, flag, d, seq);
+  count_launch();
+  SPB_CHECK_LAUNCH();
+  return SP_OK;
+}
+
+// spin until the publication `seq` has landed; copy it out
+static int bell_wait(unsigned seq, double* v, int nv, int* flag, cudaStream_t s) {
+  volatile unsigned* sq = reinterpret_cast<volatile unsigned*>(t_bell.h);
+  for (unsigned it = 1;; ++it) {
+    if (*sq == seq) break;
+    if ((it & 4095) == 0) {  // the stream failed or drained without publishing
+      const cudaError_t e = cudaStreamQuery(s);
+      if (e == cudaSuccess && *sq != seq) {
+        set_error("doorbell: stream idle without publication");
+        return SP_ECUDA;
+      }
+      if (e != cudaSuccess && e != cudaErrorNotReady) {
+        set_error(std::string("doorbell: ") + cudaGetErrorString(e));
+        return SP_ECUDA;
+      }
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  if (flag) *flag = *reinterpret_cast<volatile int*>(t_bell.h + 4);
+  if (nv > 0) std::memcpy(v, t_bell.h + 16, nv * sizeof(double));
   return SP_OK;
 }
 
@@ -120,23 +193,43 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
       set_error("svd_top workspace allocation failed");
       return SP_ECUDA;
     }
-    SPB_TRY(fill_uniform(cols, b, Om, b, 0x5eed5eedull + (uint64_t)b, s));
-    SPB_TRY(gemm(0, 0, rows, b, cols, 1.0, X, ldx, Om, b, 0.0, Y, b, s));
-    if (pf.dev && pf.check_input) SPB_TRY(check_finite_async(rows, b, Y, b, pf.dev, s));
+    // test block: subsampled randomized Hadamard transform of the rows of X
+    // (srht.cu, also the finite check of X) when the width allows, else a
+    // dense uniform block on the DMMA GEMM (finite check on Y)
+    int* xflag = (pf.dev && pf.check_input) ? pf.dev : nullptr;
+    if (srht_sketch(rows, cols, X, ldx, b, 0x5eed5eedull + (uint64_t)b, Y, b, xflag, s) != SP_OK) {
+      SPB_TRY(fill_uniform(cols, b, Om, b, 0x5eed5eedull + (uint64_t)b, s));
+      SPB_TRY(gemm(0, 0, rows, b, cols, 1.0, X, ldx, Om, b, 0.0, Y, b, s));
+      if (xflag) SPB_TRY(check_finite_async(rows, b, Y, b, xflag, s));
+    }
     SPB_TRY(tsqr(rows, b, Y, b, Q, b, Rt, b, s));
     std::vector<double> prev, hs(b);
     int kept_prev = -1, kept = 0, iters = 0;
     bool grow = false;
     const int max_it = 24;
+    // outputs for this block width (the speculative final products below)
+    double* oU = ar.alloc<double>((size_t)rows * b);
+    double* oS = ar.alloc<double>((size_t)b);
+    double* oV = want_v ? ar.alloc<double>((size_t)cols * b) : nullptr;
+    if (ar.failed()) {
+      set_error("svd_top workspace allocation failed");
+      return SP_ECUDA;
+    }
     for (int itn = 0; itn < max_it; ++itn) {
       // Rayleigh-Ritz: Q^T X = Z^T with Z = X^T Q = P Rz  ->  Q^T X = Rz^T P^T
       SPB_TRY(gemm(1, 0, cols, b, rows, 1.0, X, ldx, Q, b, 0.0, Z, b, s));
       SPB_TRY(tsqr(cols, b, Z, b, P, b, Rz, b, s));
       SPB_TRY(jacobi_svd_tr(b, Rz, b, /*trans=*/true, Us, b, Sg, want_v ? Vs : nullptr, b, s));
-      PinnedReads rd(s);
-      SPB_TRY(rd.add(hs.data(), Sg, b * sizeof(double)));
-      if (itn == 0) SPB_TRY(read_flag_with(pf, hflag, rd));
-      SPB_TRY(rd.sync());
+      // publish the Ritz values, then -- while the host waits for them --
+      // form the final products as if this step converged (it usually does;
+      // otherwise they are recomputed after the next step)
+      unsigned seq = 0;
+      SPB_TRY(bell_publish(Sg, b, itn == 0 ? pf.dev : nullptr, seq, s));
+      SPB_TRY(gemm(0, 0, rows, b, b, 1.0, Q, b, Us, b, 0.0, oU, b, s));
+      if (want_v) SPB_TRY(gemm(0, 0, cols, b, b, 1.0, P, b, Vs, b, 0.0, oV, b, s));
+      SPB_CUDA(cudaMemcpyAsync(oS, Sg, b * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      SPB_TRY(bell_wait(seq, hs.data(), b, &hflag, s));
+      if (!(itn == 0 && pf.dev)) hflag = 0;
       if (hflag) {
         set_error(pf.msg);
         return SP_ENUMERICAL;
@@ -183,16 +276,9 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
     out.kept = kept;
     out.iters = iters;
     out.hs = hs;
-    out.U = ar.alloc<double>((size_t)rows * b);
-    out.S = ar.alloc<double>((size_t)b);
-    if (want_v) out.V = ar.alloc<double>((size_t)cols * b);
-    if (ar.failed()) {
-      set_error("svd_top workspace allocation failed");
-      return SP_ECUDA;
-    }
-    SPB_TRY(gemm(0, 0, rows, b, b, 1.0, Q, b, Us, b, 0.0, out.U, b, s));
-    if (want_v) SPB_TRY(gemm(0, 0, cols, b, b, 1.0, P, b, Vs, b, 0.0, out.V, b, s));
-    SPB_CUDA(cudaMemcpyAsync(out.S, Sg, b * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    out.U = oU;
+    out.S = oS;
+    out.V = oV;
     return SP_OK;
   }
 }

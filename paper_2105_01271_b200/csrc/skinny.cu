@@ -136,8 +136,8 @@ template <int R, typename TA>
 static int launch_skinny_r(const TA* A, int64_t m, int64_t n, int64_t lda, const double* Z,
                            int64_t ldz, double* Y, int64_t ldy, cudaStream_t s) {
   constexpr int V = sizeof(TA) == 8 ? 2 : 4;
-  if (skinny_tma_ok(A, sizeof(TA) == 8 ? SP_F64 : SP_F32, n, lda) && m >= 1 &&
-      !std::getenv("SPB_SKINNY_LEGACY")) {
+  static const bool legacy = std::getenv("SPB_SKINNY_LEGACY") != nullptr;
+  if (skinny_tma_ok(A, sizeof(TA) == 8 ? SP_F64 : SP_F32, n, lda) && m >= 1 && !legacy) {
     // TMA-streamed persistent path: Z packed contiguously (+ pad for the
     // 16-byte rounded bulk copy of the last row group)
     Arena ar(s);

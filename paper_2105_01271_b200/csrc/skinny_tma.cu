@@ -173,14 +173,23 @@ int skinny_tma_launch(const TA* A, int64_t m, int64_t n, int64_t lda, const doub
                       cudaStream_t s) {
   using L = TmaLayout<R>;
   constexpr int V = 16 / sizeof(TA);
-  SPB_CUDA(cudaFuncSetAttribute(skinny_tma_kernel<R, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmem));
+  static int attr_dev = -1;  // set once per device (host overhead sits on the critical path)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    SPB_CUDA(cudaFuncSetAttribute(skinny_tma_kernel<R, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmem));
+    attr_dev = dev;
+  }
   const int64_t units = n / V;
   // Row splitting (CTA = row part x column slab, partial Y + one reduction)
   // lengthens each CTA's row segments; measured slower than full-height slabs
   // at cfg2 (209 / 219 us for 2 / 4 parts vs 191 us), so it is off unless
   // SPB_K2_SPLIT asks for it (experiments only).
-  int splits = 1;
-  if (const char* e = getenv("SPB_K2_SPLIT")) splits = std::max(1, std::min(8, atoi(e)));
+  static const int env_splits = [] {
+    const char* e = getenv("SPB_K2_SPLIT");
+    return e ? std::max(1, std::min(8, atoi(e))) : 1;
+  }();
+  int splits = env_splits;
   if (ldy != R || m < (int64_t)2 * kTmaRows * splits) splits = 1;
   while (splits > 1 && units / 16 < (kNumSMs / splits)) --splits;
   int grid = (int)std::min<int64_t>(kNumSMs / splits, std::max<int64_t>(1, units / 16)) * splits;

@@ -1,0 +1,144 @@
+// Range-finder test block Y = X Omega for the sketch-side subspace iteration
+// (svd_top, pipeline.cu) as a subsampled randomized Hadamard transform:
+//   Omega = D H S  (D random signs, H the Walsh-Hadamard matrix of the
+//   zero-padded width 2^L, S b stratified column samples),
+// i.e. each row of X is sign-flipped, Hadamard-transformed and sampled.
+// A structured random embedding (Halko, Martinsson & Tropp 2011, sec. 4.6)
+// in place of the dense Gaussian block: L 2^L additions per row instead of
+// 2 b 2^L FMAs on the DMMA pipe, one read of X, no Omega in memory.  The
+// block only has to capture the dominant column space; the Rayleigh-Ritz
+// step and the convergence tests that follow are unchanged.
+//
+// One CTA per row (256..1024 threads, 16 elements each, widths up to 16384):
+// the top 4 index bits are transformed in registers straight from the
+// coalesced load, the rest in rounds of 4 bits through padded shared memory
+// (a thread's 16 slots re-mapped to the round's bits), then the b sampled
+// outputs are read out.  Non-finite input raises *flag (the
+// reference checks the sketch before its QR, src/kernels.py:47-49).
+// Fixed operation order: bitwise reproducible.
+#include "common.cuh"
+#include "launch_count.cuh"
+
+namespace spb {
+
+__device__ __forceinline__ uint64_t srht_hash(uint64_t seed, uint64_t t) {
+  uint64_t z = seed * 0x9E3779B97F4A7C15ull + t * 0xD1B54A32D192ED03ull + 0x2545F4914F6CDD1Dull;
+  z = (z ^ (z >> 31)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 29)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 32);
+}
+
+// stratified sample c in [0, b): one position in each of the b blocks of N / b
+__device__ __forceinline__ int srht_sample(uint64_t seed, int c, int blk) {
+  const uint64_t z = srht_hash(seed ^ 0x5851F42D4C957F2Dull, (uint64_t)c);
+  return c * blk + (int)(z % (uint64_t)blk);
+}
+
+__device__ __forceinline__ int srht_pad(int j) { return j + (j >> 4); }
+
+// element index of slot e of thread t in a round over bits [lo, lo + nb):
+// bits [lo, lo+nb) = e's low nb bits, the thread index fills [0, lo) and
+// [lo+nb, LT+nb), e's remaining 4 - nb bits go on top.
+template <int LT>
+__device__ __forceinline__ int srht_index(int t, int e, int lo, int nb) {
+  const int el = e & ((1 << nb) - 1), eh = e >> nb;
+  return (t & ((1 << lo) - 1)) | (el << lo) | ((t >> lo) << (lo + nb)) | (eh << (LT + nb));
+}
+
+// 16 elements per thread; butterflies over slot bits [0, nb)
+__device__ __forceinline__ void srht_stages(double (&v)[16], int nb) {
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    if (s < nb) {
+      const int h = 1 << s;
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        if ((e & h) == 0) {
+          const double a = v[e], c = v[e + h];
+          v[e] = a + c;
+          v[e + h] = a - c;
+        }
+    }
+  }
+}
+
+// One CTA (2^LT threads) per row, N = 16 * 2^LT (zero-padded) elements:
+// the coalesced load is the round over the top 4 bits; then rounds of 4
+// bits through padded shared memory (the last one narrower if LT % 4 != 0).
+template <int LT>
+__global__ void __launch_bounds__(1 << LT)
+srht_kernel(int64_t cols, const double* __restrict__ X, int64_t ldx, int b, uint64_t seed, double* __restrict__ Y,
+            int64_t ldy, int* __restrict__ flag) {
+  constexpr int T = 1 << LT, N = 16 * T;
+  extern __shared__ double sr_smem[];  // srht_pad(N) doubles
+  const int t = threadIdx.x;
+  const int64_t row = blockIdx.x;
+  const double* xr = X + row * ldx;
+  const uint64_t sg = srht_hash(seed, (uint64_t)t);  // sign of element t + T e: bit e
+  double v[16];
+  bool bad = false;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const int64_t j = (int64_t)t + (int64_t)T * e;
+    const double x = j < cols ? xr[j] : 0.0;
+    bad |= !isfinite(x);
+    v[e] = __longlong_as_double(__double_as_longlong(x) ^ (long long)(((sg >> e) & 1ull) << 63));
+  }
+  if (__syncthreads_or(bad)) {
+    if (t == 0 && flag) atomicOr(flag, 1);
+  }
+  srht_stages(v, 4);  // index bits [LT, LT + 4)
+  int plo = LT, pnb = 4;  // layout of the values held
+#pragma unroll
+  for (int lo = 0; lo < LT; lo += 4) {
+    const int nb = LT - lo < 4 ? LT - lo : 4;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) sr_smem[srht_pad(srht_index<LT>(t, e, plo, pnb))] = v[e];
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = sr_smem[srht_pad(srht_index<LT>(t, e, lo, nb))];
+    __syncthreads();
+    srht_stages(v, nb);
+    plo = lo;
+    pnb = nb;
+  }
+#pragma unroll
+  for (int e = 0; e < 16; ++e) sr_smem[srht_pad(srht_index<LT>(t, e, plo, pnb))] = v[e];
+  __syncthreads();
+  if (t < b) Y[row * ldy + t] = sr_smem[srht_pad(srht_sample(seed, t, N / b))];
+}
+
+// Y (rows x b, ld ldy) = X D H S.  Returns SP_ECONFIG when the shape is out of
+// the kernel's range (the caller falls back to a dense block on the GEMM).
+int srht_sketch(int64_t rows, int64_t cols, const double* X, int64_t ldx, int b, uint64_t seed, double* Y,
+                int64_t ldy, int* flag, cudaStream_t s) {
+  int lt = 8;
+  while (lt < 10 && ((int64_t)16 << lt) < cols) ++lt;
+  const int64_t n2 = (int64_t)16 << lt;
+  if (cols < 1 || cols > n2 || b < 1 || b > 32 || rows < 1 || rows > 0x7fffffff) {
+    set_error("srht_sketch: shape out of range");
+    return SP_ECONFIG;
+  }
+  const size_t smem = (size_t)(n2 + n2 / 16) * sizeof(double);
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    SPB_CUDA(cudaFuncSetAttribute(srht_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    SPB_CUDA(cudaFuncSetAttribute(srht_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    SPB_CUDA(cudaFuncSetAttribute(srht_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr_dev = dev;
+  }
+  const dim3 grid((unsigned)rows);
+  if (lt == 8)
+    srht_kernel<8><<<grid, 1 << 8, smem, s>>>(cols, X, ldx, b, seed, Y, ldy, flag);
+  else if (lt == 9)
+    srht_kernel<9><<<grid, 1 << 9, smem, s>>>(cols, X, ldx, b, seed, Y, ldy, flag);
+  else
+    srht_kernel<10><<<grid, 1 << 10, smem, s>>>(cols, X, ldx, b, seed, Y, ldy, flag);
+  count_launch();
+  SPB_CHECK_LAUNCH();
+  return SP_OK;
+}
+
+}  // namespace spb
