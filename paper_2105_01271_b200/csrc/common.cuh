@@ -76,6 +76,29 @@ __device__ __forceinline__ double warp_max(double v) {
 template <typename T>
 __device__ __forceinline__ double widen(T x) { return (double)x; }
 
+// FP64 reciprocal / reciprocal square root from the MUFU approximations
+// (rcp / rsqrt .approx.ftz.f64) refined by two Newton steps: ~1 ulp, at a
+// fraction of the latency of the IEEE-rounded forms on the serial chains of
+// the Householder and Jacobi steps.  The argument must be normal and finite
+// (and > 0 for the rsqrt); callers guard the range.
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ double fast_rsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y * y, 1.0);
+  y = fma(0.5 * y, e, y);
+  e = fma(-x, y * y, 1.0);
+  return fma(0.5 * y, e, y);
+}
+__device__ __forceinline__ bool fast_range(double x) { return x > 1e-290 && x < 1e290; }
+
 // Staging global -> shared without a register round trip: every thread
 // issues all of its 8-byte copies back to back (zero-fill when !pred; gmem
 // must still be a mapped address then, e.g. the array base), so a staging

@@ -113,10 +113,17 @@ __device__ void fc_jacobi_warp(int r, double (&x)[RPW], double (&v)[RPW], JacSme
         continue;
       const double d = aq - ap, h = 2.0 * g;
       const double ad = fabs(d), ah = fabs(h);
-      const double hyp = (ad < 1e150 && ah < 1e150 && (ad > 1e-150 || ah > 1e-150)) ? sqrt(fma(d, d, h * h))
-                                                                                  : hypot(d, h);
-      const double t = copysign(1.0, d) * h / (ad + hyp);
-      const double cs = rsqrt(fma(t, t, 1.0));
+      double t, cs;
+      if (ad < 1e140 && ah < 1e140 && (ad > 1e-140 || ah > 1e-140)) {
+        // fast path: one MUFU rsqrt + Newton for hypot, rcp for t, rsqrt for cos
+        const double s2 = fma(d, d, h * h);
+        const double hyp = s2 * fast_rsqrt(s2);
+        t = copysign(1.0, d) * h * fast_rcp(ad + hyp);
+        cs = fast_rsqrt(fma(t, t, 1.0));
+      } else {
+        t = copysign(1.0, d) * h / (ad + hypot(d, h));
+        cs = rsqrt(fma(t, t, 1.0));
+      }
       const double sn = cs * t;
       const double so = low ? -sn : sn;
 #pragma unroll
@@ -146,7 +153,7 @@ __device__ bool chol_inv_warp(SmallMat& G, SmallMat& Ri, double* rdiag, double s
   for (int j = 0; j < c; ++j) {
     const double d = G[j][j];
     if (!(d > 0.0) || !(d < INFINITY)) return false;
-    const double rs = rsqrt(d);
+    const double rs = fast_range(d) ? fast_rsqrt(d) : rsqrt(d);
     __syncwarp();
     if (lane >= j && lane < c) G[j][lane] = lane == j ? d * rs : G[j][lane] * rs;
     if (lane == j) rdiag[j] = rs;
@@ -318,7 +325,7 @@ __device__ void hh_small(int k, const double* __restrict__ X, const SmallMat& B,
       const double w = h.W[i][i];
       const double s = w >= 0.0 ? -1.0 : 1.0;
       const double piv = w - s;
-      const double rp = 1.0 / piv;
+      const double rp = fast_range(fabs(piv)) ? fast_rcp(piv) : 1.0 / piv;  // |piv| >= 1
       __syncwarp();
       if (t == 0) {
         h.S[i] = s;

@@ -311,10 +311,17 @@ jacobi32_kernel(int n, const double* __restrict__ M, int64_t ldm, double* __rest
         continue;
       const double d = aq - ap, h = 2.0 * g;
       const double ad = fabs(d), ah = fabs(h);
-      const double hyp = (ad < 1e150 && ah < 1e150 && (ad > 1e-150 || ah > 1e-150)) ? sqrt(fma(d, d, h * h))
-                                                                                  : hypot(d, h);
-      const double t = copysign(1.0, d) * h / (ad + hyp);
-      const double cs = rsqrt(fma(t, t, 1.0));
+      double t, cs;
+      if (ad < 1e140 && ah < 1e140 && (ad > 1e-140 || ah > 1e-140)) {
+        // fast path: one MUFU rsqrt + Newton for hypot, rcp for t, rsqrt for cos
+        const double s2 = fma(d, d, h * h);
+        const double hyp = s2 * fast_rsqrt(s2);
+        t = copysign(1.0, d) * h * fast_rcp(ad + hyp);
+        cs = fast_rsqrt(fma(t, t, 1.0));
+      } else {
+        t = copysign(1.0, d) * h / (ad + hypot(d, h));
+        cs = rsqrt(fma(t, t, 1.0));
+      }
       const double sn = cs * t;
       // p' = cs p - sn q ; q' = sn p + cs q
       const double so = low ? -sn : sn;

@@ -170,9 +170,11 @@ tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t l
       sigma2 = ((rq[0] + rq[1]) + (rq[2] + rq[3])) + ((rq[4] + rq[5]) + (rq[6] + rq[7]));
     }
     if (cl > 1) {
-      if (w == 0) {
+      {
+        // the pushes are spread over the warps (warp w serves ranks w, w + 8):
+        // one or two remote stores per lane instead of cl from warp 0 alone
         const double rv = top ? rowj[buf][c] : 0.0;
-        for (int d = 0; d < cl; ++d) {
+        for (int d = w; d < cl; d += kQWarps) {
           const uint32_t bar = cluster_addr(&cbar[buf], d);
           st_async_f64(cluster_addr(&cbuf[buf][cr][c], d), dc, bar);
           if (top) st_async_f64(cluster_addr(&crow[buf][c], d), rv, bar);
@@ -217,11 +219,12 @@ tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t l
     if (sigma2 > 0.0) {
       // one rsqrt and one division: nrm = s2 / sqrt(s2), tau = -(alpha - beta) / beta
       const double s2 = fma(alpha, alpha, sigma2);
-      const double rs = rsqrt(s2);
+      const bool fr = fast_range(s2);
+      const double rs = fr ? fast_rsqrt(s2) : rsqrt(s2);
       const double sg = alpha >= 0.0 ? 1.0 : -1.0;
       beta = -sg * (s2 * rs);
       const double dd = alpha - beta;  // |dd| >= ||x_j(j:)|| > 0
-      inv = 1.0 / dd;
+      inv = fr ? fast_rcp(dd) : 1.0 / dd;
       tj = sg * dd * rs;
     }
     const double vv = fma(inv, dc, ac);  // v_j^T x_c (c > j);  (alpha_c - beta_c) v_c^T v_j (c < j)
