@@ -291,16 +291,18 @@ def run_ours(args):
     Z = res.u[:, :max(r, 1)].contiguous()
     Y = torch.empty((n_local, max(r, 1)), dtype=torch.float64, device=dev)
     s = torch.cuda.current_stream()
-    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
 
     def apass():
         _lib.call("sp_skinny_atz", A.data_ptr(), _lib.SP_F64, cfg.m, n_local, n_local, Z.data_ptr(), Z.shape[1],
                   Z.shape[1], Y.data_ptr(), Z.shape[1], s.cuda_stream)
     for _ in range(3):
         apass()
+    # A (1.05 GB at cfg2) is 8x the 126 MB L2 and K2 streams it in the same
+    # order every launch, so nothing of it survives in L2 between launches:
+    # no flush (a write flush would leave 256 MB of dirty lines for the next
+    # launch to write back, charging K2 for traffic that is not its own)
     durs = []
     for _ in range(10):
-        flush.fill_(1.0)  # evict A's tail from L2 between launches
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s)
         apass()
