@@ -215,6 +215,13 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
       set_error("svd_top workspace allocation failed");
       return SP_ECUDA;
     }
+    auto final_products = [&]() -> int {
+      SPB_TRY(gemm(0, 0, rows, b, b, 1.0, Q, b, Us, b, 0.0, oU, b, s));
+      if (want_v) SPB_TRY(gemm(0, 0, cols, b, b, 1.0, P, b, Vs, b, 0.0, oV, b, s));
+      SPB_CUDA(cudaMemcpyAsync(oS, Sg, b * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      return SP_OK;
+    };
+    bool spec = false;
     for (int itn = 0; itn < max_it; ++itn) {
       // Rayleigh-Ritz: Q^T X = Z^T with Z = X^T Q = P Rz  ->  Q^T X = Rz^T P^T
       SPB_TRY(gemm(1, 0, cols, b, rows, 1.0, X, ldx, Q, b, 0.0, Z, b, s));
@@ -223,11 +230,12 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
       // publish the Ritz values, then -- while the host waits for them --
       // form the final products as if this step converged (it usually does;
       // otherwise they are recomputed after the next step)
+      // (only when they are cheap: a wasted product must not cost more than
+      // the host round trip it hides)
+      spec = (double)b * b * (rows + (want_v ? cols : 0)) <= 64.0 * 1024 * 1024;
       unsigned seq = 0;
       SPB_TRY(bell_publish(Sg, b, itn == 0 ? pf.dev : nullptr, seq, s));
-      SPB_TRY(gemm(0, 0, rows, b, b, 1.0, Q, b, Us, b, 0.0, oU, b, s));
-      if (want_v) SPB_TRY(gemm(0, 0, cols, b, b, 1.0, P, b, Vs, b, 0.0, oV, b, s));
-      SPB_CUDA(cudaMemcpyAsync(oS, Sg, b * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      if (spec) SPB_TRY(final_products());
       SPB_TRY(bell_wait(seq, hs.data(), b, &hflag, s));
       if (!(itn == 0 && pf.dev)) hflag = 0;
       if (hflag) {
@@ -272,6 +280,7 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
       b = std::min(cap, 2 * b);
       continue;
     }
+    if (!spec) SPB_TRY(final_products());
     out.b = b;
     out.kept = kept;
     out.iters = iters;
