@@ -32,6 +32,7 @@ int power_id(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, cons
 int row_id(int64_t m, int64_t cols, const double* M, int64_t ldm, int k, double* P, int64_t* indices,
            int* warn, cudaStream_t s);
 int deferred_status(int* out);
+std::string host_trace_dump();
 void set_finish_mode(int mode);
 int sketch_basis(const double* X, int64_t rows, int64_t cols, int64_t ldx, double power, int r_max, double* U,
                  int64_t ldu, double* S, int64_t* info, cudaStream_t s);
@@ -52,6 +53,12 @@ int sp_deferred_status(int32_t* flag) {
   const int st = deferred_status(&f);
   *flag = f;
   return st;
+}
+// diagnostics: the host-side trace (SPB_HOST_TRACE=1) as text; not in the header
+const char* sp_host_trace(void) {
+  static thread_local std::string t;
+  t = host_trace_dump();
+  return t.c_str();
 }
 int sp_set_finish_mode(int32_t mode) {
   set_finish_mode(mode);

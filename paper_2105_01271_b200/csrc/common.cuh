@@ -121,6 +121,10 @@ __device__ __forceinline__ double hash_uniform(uint64_t seed, uint64_t i) {
   return ((double)(z >> 11) * (1.0 / 9007199254740992.0)) * 2.0 - 1.0;
 }
 
+// Host-side trace of the pipelines' critical path (SPB_HOST_TRACE=1):
+// host_mark(tag) records (tag, steady-clock us); sp_host_trace() dumps them.
+void host_mark(const char* tag);
+
 // Diagnostic phase timers (build with SPB_NVCC_EXTRA=-DSPB_PHASE_TRACE):
 // SPB_TMARK(i) records clock64() into slot i, SPB_TPRINT(name, n) prints the
 // n - 1 phase durations from the calling thread.
@@ -138,6 +142,37 @@ __device__ __forceinline__ double hash_uniform(uint64_t seed, uint64_t i) {
 #define SPB_TMARK(i)
 #define SPB_TPRINT(name, n)
 #endif
+
+// ------------------------------------------- programmatic dependent launch ----
+// The pipelines are chains of small dependent kernels on one stream; with
+// programmatic stream serialization a kernel is scheduled while its
+// predecessor drains instead of after it completes.  Every kernel launched
+// with launch_pdl starts with SPB_PDL_ENTRY(): it lets its own successor
+// launch, then waits (griddepcontrol.wait) until the predecessor grid has
+// completed and its memory is visible -- so no kernel touches global memory
+// before its inputs are final.  Both instructions are no-ops for a kernel
+// launched without the attribute.
+#define SPB_PDL_ENTRY()                                              \
+  do {                                                               \
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); \
+    asm volatile("griddepcontrol.wait;" ::: "memory");              \
+  } while (0)
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 
 // ------------------------------------------------------ workspace arena ----
 // Stream-ordered scratch.  The pipelines allocate a few dozen small

@@ -206,6 +206,7 @@ template <int R>
 __global__ void __launch_bounds__(kGrThreads)
 gram_rows_kernel(int64_t rows, const double* __restrict__ Y, const double* __restrict__ R1i,
                  int64_t rows_per_cta, double* __restrict__ partial, GramTail tail) {
+  SPB_PDL_ENTRY();
   constexpr int r = R;
   __shared__ __align__(16) double ys[kGrChunk * R];
   __shared__ SmallMat ri, G, Ri;
@@ -454,6 +455,7 @@ finish_core_kernel(int k, int nb2, const double* __restrict__ P2, const double* 
                    const double* __restrict__ Y, int64_t ldy, double* __restrict__ S,
                    double* __restrict__ MfU, double* __restrict__ EtfU, double* __restrict__ MfV,
                    double* __restrict__ EtfV, int* flag) {
+  SPB_PDL_ENTRY();
   extern __shared__ __align__(16) unsigned char fc_smem[];
   FcShared& sh = *reinterpret_cast<FcShared*>(fc_smem);
   double* Zt = reinterpret_cast<double*>(fc_smem + (sizeof(FcShared) + 15) / 16 * 16);
@@ -613,6 +615,7 @@ finish_rows_kernel(int k, int64_t m, int64_t n, int bu, const double* __restrict
                    const double* __restrict__ Y, int64_t ldy, const double* __restrict__ R1i,
                    const double* __restrict__ MfU, const double* __restrict__ EtfU, const double* __restrict__ MfV,
                    const double* __restrict__ EtfV, double* __restrict__ U, double* __restrict__ V) {
+  SPB_PDL_ENTRY();
   extern __shared__ __align__(16) double fr_smem[];
   double* mf = fr_smem;               // R x k
   double* ri = mf + R * k;            // R x R
@@ -718,9 +721,9 @@ static int finish_fused_r(int64_t m, int64_t n, const double* Z, int64_t ldz, co
   double* EtfU = MfV + (size_t)R * k;
   double* EtfV = EtfU + (size_t)k * k;
   GramTail t1{dflag + 1, R1, R1i, dflag, 16.0 * R * 2.220446049250313e-16};
-  gram_rows_kernel<R><<<nb, kGrThreads, 0, s>>>(n, Y, nullptr, rpc, P1, t1);
+  SPB_CUDA(launch_pdl((gram_rows_kernel<R>), dim3(nb), dim3(kGrThreads), 0, s, n, Y, nullptr, rpc, P1, t1));
   GramTail t2{nullptr, nullptr, nullptr, nullptr, 0.0};
-  gram_rows_kernel<R><<<nb, kGrThreads, 0, s>>>(n, Y, R1i, rpc, P2, t2);
+  SPB_CUDA(launch_pdl((gram_rows_kernel<R>), dim3(nb), dim3(kGrThreads), 0, s, n, Y, R1i, rpc, P2, t2));
   count_launch(2);
   SPB_CHECK_LAUNCH();
   const size_t fc_smem = (sizeof(FcShared) + 15) / 16 * 16 + (size_t)4 * k * R * sizeof(double);
@@ -732,14 +735,14 @@ static int finish_fused_r(int64_t m, int64_t n, const double* Z, int64_t ldz, co
     SPB_CUDA(cudaFuncSetAttribute(finish_rows_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
     attr_dev = dev;
   }
-  finish_core_kernel<R><<<1, kFcThreads, fc_smem, s>>>(k, nb, P2, R1, R1i, Z, ldz, Y, R, S, MfU, EtfU, MfV, EtfV,
-                                                       dflag);
+  SPB_CUDA(launch_pdl((finish_core_kernel<R>), dim3(1), dim3(kFcThreads), fc_smem, s, k, nb, P2, R1, R1i, Z, ldz, Y, R, S, MfU, EtfU, MfV, EtfV,
+                                                       dflag));
   count_launch();
   SPB_CHECK_LAUNCH();
   const int bu = ceil_div(m, kFrRows), bv = ceil_div(n, kFrRows);
   const size_t fr_smem = ((size_t)R * k + R * R + (size_t)kFrRows * (R + 1)) * sizeof(double);
-  finish_rows_kernel<R><<<bu + bv, kFrThreads, fr_smem, s>>>(k, m, n, bu, Z, ldz, Y, R, R1i, MfU, EtfU, MfV, EtfV,
-                                                             U, V);
+  SPB_CUDA(launch_pdl((finish_rows_kernel<R>), dim3(bu + bv), dim3(kFrThreads), fr_smem, s, k, m, n, bu, Z, ldz, Y, R, R1i, MfU, EtfU, MfV, EtfV,
+                                                             U, V));
   count_launch();
   SPB_CHECK_LAUNCH();
   return SP_OK;

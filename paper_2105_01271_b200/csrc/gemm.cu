@@ -88,6 +88,7 @@ __global__ void __launch_bounds__(kGemmThreads)
 dgemm_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, int64_t lda,
              const double* __restrict__ B, int64_t ldb, double* __restrict__ C, int64_t ldc,
              double alpha, double beta, int64_t k_per_split, bool partial) {
+  SPB_PDL_ENTRY();
   using TL = Tile<BM, BN>;
   // stage sizes for the operand orientations (op(B) tile is stored as (n, k) with orientation !TB)
   constexpr int kSA = TA ? kBK * (BM + 4) : BM * PadK<BM>::v;
@@ -176,6 +177,7 @@ dgemm_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, int6
 __global__ void __launch_bounds__(256) gemm_split_reduce_warp(const double* __restrict__ P, int S, int64_t M,
                                                               int64_t N, double alpha, double beta,
                                                               double* __restrict__ C, int64_t ldc) {
+  SPB_PDL_ENTRY();
   __shared__ double part[8][33];
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
   const int64_t e = (int64_t)blockIdx.x * 32 + lane;
@@ -219,8 +221,10 @@ template <int TA, int TB, int BM, int BN>
 static void launch_dgemm(dim3 grid, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                          const double* B, int64_t ldb, double* C, int64_t ldc, double alpha,
                          double beta, int64_t kps, bool partial, cudaStream_t s) {
-  dgemm_kernel<TA, TB, BM, BN><<<grid, kGemmThreads, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, kps,
-                                                             partial);
+  // errors surface through the caller's cudaGetLastError check
+  if (launch_pdl((dgemm_kernel<TA, TB, BM, BN>), grid, dim3(kGemmThreads), 0, s, M, N, K, A, lda, B, ldb, C, ldc,
+                 alpha, beta, kps, partial) != cudaSuccess)
+    return;
 }
 
 template <int BM, int BN>
@@ -291,7 +295,7 @@ int gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const do
 int split_reduce(const double* P, int S, int64_t M, int64_t N, double alpha, double beta, double* C, int64_t ldc,
                  cudaStream_t s) {
   if (S > 8) {
-    gemm_split_reduce_warp<<<ceil_div(M * N, 32), 256, 0, s>>>(P, S, M, N, alpha, beta, C, ldc);
+    SPB_CUDA(launch_pdl((gemm_split_reduce_warp), dim3(ceil_div(M * N, 32)), dim3(256), 0, s, P, S, M, N, alpha, beta, C, ldc));
   } else {
     gemm_split_reduce<<<ceil_div(M * N, 256), 256, 0, s>>>(P, S, M, N, alpha, beta, C, ldc);
   }

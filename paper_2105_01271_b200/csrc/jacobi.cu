@@ -205,6 +205,7 @@ template <int NW, int RPW>
 __global__ void __launch_bounds__(NW * 32)
 jacobi32_kernel(int n, const double* __restrict__ M, int64_t ldm, double* __restrict__ U, int64_t ldu,
                 double* __restrict__ S, double* __restrict__ Vout, int64_t ldv, bool trans) {
+  SPB_PDL_ENTRY();
   __shared__ double part[2][NW][32][2];
   __shared__ double nrm_s[NW][32];
   __shared__ double sig_s[32];
@@ -502,13 +503,13 @@ int jacobi_svd_tr(int64_t n, const double* M, int64_t ldm, bool trans, double* U
                   double* V, int64_t ldv, cudaStream_t s) {
   SPB_REQUIRE(n >= 1 && n <= 256, "Jacobi SVD supports 1 <= n <= 256");
   if (n <= 8) {
-    jacobi32_kernel<1, 8><<<1, 32, 0, s>>>((int)n, M, ldm, U, ldu, S, V, ldv, trans);
+    SPB_CUDA(launch_pdl((jacobi32_kernel<1, 8>), dim3(1), dim3(32), 0, s, (int)n, M, ldm, U, ldu, S, V, ldv, trans));
     count_launch();
     SPB_CHECK_LAUNCH();
     return SP_OK;
   }
   if (n <= 32) {
-    jacobi32_kernel<kJ32Warps, 8><<<1, kJ32Warps * 32, 0, s>>>((int)n, M, ldm, U, ldu, S, V, ldv, trans);
+    SPB_CUDA(launch_pdl((jacobi32_kernel<kJ32Warps, 8>), dim3(1), dim3(kJ32Warps * 32), 0, s, (int)n, M, ldm, U, ldu, S, V, ldv, trans));
     count_launch();
     SPB_CHECK_LAUNCH();
     return SP_OK;

@@ -42,6 +42,7 @@ int transpose(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* 
 
 __global__ void copy2d_kernel(int64_t rows, int64_t cols, const double* __restrict__ X, int64_t ldx,
                               double* __restrict__ Y, int64_t ldy) {
+  SPB_PDL_ENTRY();
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= rows * cols) return;
   Y[(e / cols) * ldy + (e % cols)] = X[(e / cols) * ldx + (e % cols)];
@@ -50,7 +51,7 @@ __global__ void copy2d_kernel(int64_t rows, int64_t cols, const double* __restri
 int copy2d(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Y, int64_t ldy,
            cudaStream_t s) {
   if (rows == 0 || cols == 0) return SP_OK;
-  copy2d_kernel<<<ceil_div(rows * cols, 256), 256, 0, s>>>(rows, cols, X, ldx, Y, ldy);
+  SPB_CUDA(launch_pdl((copy2d_kernel), dim3(ceil_div(rows * cols, 256)), dim3(256), 0, s, rows, cols, X, ldx, Y, ldy));
   SPB_LAUNCHED();
   return SP_OK;
 }

@@ -15,6 +15,8 @@
 // sigma(G) = sigma(C)^(2q+1) and U_G = U_C, so G is never formed and the kept
 // basis is accurate to ~1e-16 sigma_1 instead of ~1e-16 sigma_1(G).
 #include <atomic>
+#include <map>
+#include <mutex>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -29,6 +31,10 @@ constexpr double kRankTol = 1e-12;  // src/kernels.py:19
 
 int srht_sketch(int64_t rows, int64_t cols, const double* X, int64_t ldx, int b, uint64_t seed, double* Y,
                 int64_t ldy, int* flag, cudaStream_t s);
+bool srht_ok(int64_t rows, int64_t cols, int b);
+int srht_gather(const void* A, int a_dtype, int64_t rows, int64_t lda, const int64_t* gidx, int64_t cols, double* C,
+                int64_t ldc, int b, uint64_t seed, double* Y, int64_t ldy, int* flag, cudaStream_t s);
+constexpr uint64_t kSrhtSeed = 0x5eed5eedull;  // + block width
 
 static int count_kept(const std::vector<double>& s, double power) {
   if (s.empty() || !(s[0] > 0.0)) return 0;
@@ -84,9 +90,13 @@ static thread_local Doorbell t_bell;
 constexpr int kBellMax = 1024;  // doubles
 
 __global__ void publish_kernel(const double* __restrict__ v, int nv, const int* __restrict__ flag,
-                               unsigned char* __restrict__ bell, unsigned seq) {
+                               unsigned char* __restrict__ bell, unsigned seq, double* __restrict__ vcopy) {
+  SPB_PDL_ENTRY();
   double* hv = reinterpret_cast<double*>(bell + 16);
-  for (int i = threadIdx.x; i < nv; i += blockDim.x) hv[i] = v[i];
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+    hv[i] = v[i];
+    if (vcopy) vcopy[i] = v[i];  // device copy of the spectrum (no memcpy node in the chain)
+  }
   if (threadIdx.x == 0) *reinterpret_cast<volatile int*>(bell + 4) = flag ? *flag : 0;
   __threadfence_system();
   __syncthreads();
@@ -94,7 +104,8 @@ __global__ void publish_kernel(const double* __restrict__ v, int nv, const int* 
 }
 
 // enqueue the publication of v[0:nv) (+ *flag) on s; returns the sequence number
-static int bell_publish(const double* v, int nv, const int* flag, unsigned& seq, cudaStream_t s) {
+static int bell_publish(const double* v, int nv, const int* flag, unsigned& seq, cudaStream_t s,
+                        double* vcopy = nullptr) {
   if (nv > kBellMax) {
     set_error("doorbell payload too large");
     return SP_ECUDA;
@@ -109,7 +120,7 @@ static int bell_publish(const double* v, int nv, const int* flag, unsigned& seq,
   if (seq == 0) seq = ++t_bell.next;
   unsigned char* d = nullptr;
   SPB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d), t_bell.h, 0));
-  publish_kernel<<<1, 128, 0, s>>>(v, nv, flag, d, seq);
+  SPB_CUDA(launch_pdl((publish_kernel), dim3(1), dim3(128), 0, s, v, nv, flag, d, seq, vcopy));
   count_launch();
   SPB_CHECK_LAUNCH();
   return SP_OK;
@@ -144,9 +155,12 @@ static int bell_wait(unsigned seq, double* v, int nv, int* flag, cudaStream_t s)
 // still above the cut at its last column does not grow once it holds need + 8
 // values, and values within 10x of the block's tail (an unresolved bulk, e.g.
 // the noise floor of cfg3) are exempt from the stability test.
+// Ypre (rows x 32, ld 32, may be null): the SRHT test block of width 32
+// already formed (fused with the gather of X, srht_gather); used for the
+// first block when it has that width.
 static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int want, double power,
                    TopSvd& out, Arena& ar, cudaStream_t s, PendingFlag pf = PendingFlag(), bool want_v = false,
-                   int need = -1) {
+                   int need = -1, const double* Ypre = nullptr) {
   const int64_t p = std::min(rows, cols);
   int hflag = 0;
   if (p <= 64 && pf.dev) {
@@ -197,12 +211,15 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
     // (srht.cu, also the finite check of X) when the width allows, else a
     // dense uniform block on the DMMA GEMM (finite check on Y)
     int* xflag = (pf.dev && pf.check_input) ? pf.dev : nullptr;
-    if (srht_sketch(rows, cols, X, ldx, b, 0x5eed5eedull + (uint64_t)b, Y, b, xflag, s) != SP_OK) {
+    const double* Y0 = Y;  // the first test block
+    if (Ypre && b == 32) {
+      Y0 = Ypre;
+    } else if (srht_sketch(rows, cols, X, ldx, b, kSrhtSeed + (uint64_t)b, Y, b, xflag, s) != SP_OK) {
       SPB_TRY(fill_uniform(cols, b, Om, b, 0x5eed5eedull + (uint64_t)b, s));
       SPB_TRY(gemm(0, 0, rows, b, cols, 1.0, X, ldx, Om, b, 0.0, Y, b, s));
       if (xflag) SPB_TRY(check_finite_async(rows, b, Y, b, xflag, s));
     }
-    SPB_TRY(tsqr(rows, b, Y, b, Q, b, Rt, b, s));
+    SPB_TRY(tsqr(rows, b, Y0, b, Q, b, Rt, b, s));
     std::vector<double> prev, hs(b);
     int kept_prev = -1, kept = 0, iters = 0;
     bool grow = false;
@@ -215,10 +232,10 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
       set_error("svd_top workspace allocation failed");
       return SP_ECUDA;
     }
-    auto final_products = [&]() -> int {
+    auto final_products = [&](bool copy_s) -> int {
       SPB_TRY(gemm(0, 0, rows, b, b, 1.0, Q, b, Us, b, 0.0, oU, b, s));
       if (want_v) SPB_TRY(gemm(0, 0, cols, b, b, 1.0, P, b, Vs, b, 0.0, oV, b, s));
-      SPB_CUDA(cudaMemcpyAsync(oS, Sg, b * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      if (copy_s) SPB_CUDA(cudaMemcpyAsync(oS, Sg, b * sizeof(double), cudaMemcpyDeviceToDevice, s));
       return SP_OK;
     };
     bool spec = false;
@@ -234,9 +251,12 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
       // the host round trip it hides)
       spec = (double)b * b * (rows + (want_v ? cols : 0)) <= 64.0 * 1024 * 1024;
       unsigned seq = 0;
-      SPB_TRY(bell_publish(Sg, b, itn == 0 ? pf.dev : nullptr, seq, s));
-      if (spec) SPB_TRY(final_products());
+      host_mark("svd_top: rr launched");
+      SPB_TRY(bell_publish(Sg, b, itn == 0 ? pf.dev : nullptr, seq, s, oS));
+      if (spec) SPB_TRY(final_products(false));
+      host_mark("svd_top: spin");
       SPB_TRY(bell_wait(seq, hs.data(), b, &hflag, s));
+      host_mark("svd_top: spectrum in");
       if (!(itn == 0 && pf.dev)) hflag = 0;
       if (hflag) {
         set_error(pf.msg);
@@ -280,7 +300,7 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
       b = std::min(cap, 2 * b);
       continue;
     }
-    if (!spec) SPB_TRY(final_products());
+    if (!spec) SPB_TRY(final_products(false));  // oS was written by the publication
     out.b = b;
     out.kept = kept;
     out.iters = iters;
@@ -345,6 +365,27 @@ struct Deferred {
 static thread_local Deferred t_def;
 static thread_local int t_finish_mode = 0;  // 1: Householder TSQR finish
 
+// Per-stream {flag, ticket} words of the fused finish: zeroed once at
+// creation; the ticket is reset by the Gram tail that consumes it and the flag
+// behind its deferred read (at the end of the call), so no memset node sits
+// inside the call's chain of dependent launches.
+static int finish_words(cudaStream_t s, int** out) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, int*> words;
+  int dev = 0;
+  SPB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = words.find({dev, s});
+  if (it == words.end()) {
+    int* p = nullptr;
+    SPB_CUDA(cudaMalloc(&p, 2 * sizeof(int)));
+    SPB_CUDA(cudaMemsetAsync(p, 0, 2 * sizeof(int), s));
+    it = words.emplace(std::make_pair(dev, s), p).first;
+  }
+  *out = it->second;
+  return SP_OK;
+}
+
 static int defer_flag(const int* dflag, cudaStream_t s) {
   if (!t_def.host) {
     SPB_CUDA(cudaMallocHost(&t_def.host, sizeof(int)));
@@ -381,11 +422,16 @@ static int finish_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t 
   if (r > 0 && t_finish_mode == 0 && kappa_est < 1e6 && finish_fused_ok(m, n, r, k)) {
     // A pass + fused shifted-CholeskyQR2 / Jacobi / completion: no host sync
     SPB_ALLOC(ar, double, Y, (size_t)n * r);
-    SPB_ALLOC(ar, int, dflag, 2);  // {flag, ticket}
-    SPB_CUDA(cudaMemsetAsync(dflag, 0, 2 * sizeof(int), s));
+    int* dflag = nullptr;  // {flag, ticket}, zero on entry
+    SPB_TRY(finish_words(s, &dflag));
+    host_mark("finish: A pass launch");
     SPB_TRY(skinny_atz(A, a_dtype, m, n, lda, Z, ldz, r, Y, r, s));
+    host_mark("finish: A pass launched");
     SPB_TRY(finish_fused(m, n, Z, ldz, Y, r, k, U, S, V, dflag, s));
-    return defer_flag(dflag, s);
+    host_mark("finish: launched");
+    SPB_TRY(defer_flag(dflag, s));
+    SPB_CUDA(cudaMemsetAsync(dflag, 0, sizeof(int), s));  // after its read: ready for the next call
+    return SP_OK;
   }
   SPB_CUDA(cudaMemsetAsync(S, 0, k * sizeof(double), s));
   const int kk = std::min(r, k);
@@ -550,6 +596,7 @@ int power_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, con
               const int64_t* cols, int64_t ncols, int q, int k, const double* pre_s0,
               const double* pre_c, int hints, double* U, double* S, double* V, int64_t* info,
               cudaStream_t s) {
+  host_mark("power_svd enter");
   const int64_t l0 = launches();
   const int64_t out_dim = omega ? ell : nc;
   // src/power.py:235-241, 216-224, 330-331
@@ -567,25 +614,39 @@ int power_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, con
     same = true;
   else if (!(hints & SP_HINT_DIFFERENT_SET))
     SPB_TRY(sketch_is_columns(idx, w, depth, nc, omega, cols, ncols, same, s));
+  SPB_ALLOC(ar, int, fflag, 1);
+  SPB_CUDA(cudaMemsetAsync(fflag, 0, sizeof(int), s));
   const double* C = pre_c;
+  const double* Ypre = nullptr;
   if (!C) {
     double* t = ar.alloc<double>((size_t)m * ncols);
     if (!t) {
       set_error("column block allocation failed");
       return SP_ECUDA;
     }
-    SPB_TRY(apply_stencil(A, a_dtype, m, n, lda, cols, nullptr, 1, ncols, true, t, ncols, s));
+    if (same && std::min<int64_t>(m, ncols) > 64 && srht_ok(m, ncols, 32)) {
+      // K1 fused with the range finder's test block: C and Y = C D H S in one pass
+      double* y = ar.alloc<double>((size_t)m * 32);
+      if (!y) {
+        set_error("test block allocation failed");
+        return SP_ECUDA;
+      }
+      host_mark("gather launch");
+      SPB_TRY(srht_gather(A, a_dtype, m, lda, cols, ncols, t, ncols, 32, kSrhtSeed + 32, y, 32, fflag, s));
+      host_mark("gather launched");
+      Ypre = y;
+    } else {
+      SPB_TRY(apply_stencil(A, a_dtype, m, n, lda, cols, nullptr, 1, ncols, true, t, ncols, s));
+    }
     C = t;
   }
   TopSvd top;
   if (same) {
-    SPB_ALLOC(ar, int, fflag, 1);
-    SPB_CUDA(cudaMemsetAsync(fflag, 0, sizeof(int), s));
     PendingFlag pf;
     pf.dev = fflag;
     pf.check_input = true;
     pf.msg = "power iterate overflowed; enable re-orthonormalization (reorth)";
-    SPB_TRY(svd_top(C, m, ncols, ncols, 1, 2.0 * q + 1.0, top, ar, s, pf));
+    SPB_TRY(svd_top(C, m, ncols, ncols, 1, 2.0 * q + 1.0, top, ar, s, pf, false, -1, Ypre));
     // the reference forms G = (C C^T)^q C explicitly and raises once it
     // overflows (src/power.py:81-85); G is never formed here, so mirror the
     // condition on its largest singular value sigma_1(C)^(2q+1)

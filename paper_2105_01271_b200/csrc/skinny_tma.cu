@@ -39,6 +39,7 @@ template <int R, typename TA>
 __global__ void __launch_bounds__(kTmaThreads, 1)
 skinny_tma_kernel(const TA* __restrict__ A, int64_t m, int64_t n, int64_t lda, const double* __restrict__ Zc,
                   double* __restrict__ Y, int64_t ldy, int splits) {
+  SPB_PDL_ENTRY();
   constexpr int V = 16 / sizeof(TA);
   constexpr int TC = kTmaConsumers * V;  // columns per tile
   using L = TmaLayout<R>;
@@ -202,7 +203,7 @@ int skinny_tma_launch(const TA* A, int64_t m, int64_t n, int64_t lda, const doub
       return SP_ECUDA;
     }
   }
-  skinny_tma_kernel<R, TA><<<grid, kTmaThreads, L::kSmem, s>>>(A, m, n, lda, Zc, out, splits > 1 ? R : ldy, splits);
+  SPB_CUDA(launch_pdl((skinny_tma_kernel<R, TA>), dim3(grid), dim3(kTmaThreads), L::kSmem, s, A, m, n, lda, Zc, out, splits > 1 ? R : ldy, splits));
   count_launch();
   SPB_CHECK_LAUNCH();
   if (splits > 1) {

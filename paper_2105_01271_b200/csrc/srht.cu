@@ -65,10 +65,16 @@ __device__ __forceinline__ void srht_stages(double (&v)[16], int nb) {
 // One CTA (2^LT threads) per row, N = 16 * 2^LT (zero-padded) elements:
 // the coalesced load is the round over the top 4 bits; then rounds of 4
 // bits through padded shared memory (the last one narrower if LT % 4 != 0).
-template <int LT>
+// GATHER: the row of X is gathered on the fly from A (X[row][j] =
+// A[row][gidx[j]], an exact copy, written to X as well): the coarse-column
+// block C = A(:, I) and its test block Y come out of one pass over A (K1 fused
+// with the range finder's first product).  Both modes give bit-identical Y.
+template <int LT, bool GATHER, typename TA>
 __global__ void __launch_bounds__(1 << LT)
 srht_kernel(int64_t cols, const double* __restrict__ X, int64_t ldx, int b, uint64_t seed, double* __restrict__ Y,
-            int64_t ldy, int* __restrict__ flag) {
+            int64_t ldy, int* __restrict__ flag, const TA* __restrict__ A, int64_t lda,
+            const int64_t* __restrict__ gidx, double* __restrict__ Xout) {
+  SPB_PDL_ENTRY();
   constexpr int T = 1 << LT, N = 16 * T;
   extern __shared__ double sr_smem[];  // srht_pad(N) doubles
   const int t = threadIdx.x;
@@ -77,10 +83,35 @@ srht_kernel(int64_t cols, const double* __restrict__ X, int64_t ldx, int b, uint
   const uint64_t sg = srht_hash(seed, (uint64_t)t);  // sign of element t + T e: bit e
   double v[16];
   bool bad = false;
+  if (GATHER) {
+    const TA* ar = A + row * lda;
+    double* orow = Xout + row * ldx;
+    int64_t gi[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int64_t j = (int64_t)t + (int64_t)T * e;
+      gi[e] = j < cols ? __ldg(gidx + j) : 0;
+    }
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int64_t j = (int64_t)t + (int64_t)T * e;
+      v[e] = j < cols ? widen(__ldg(ar + gi[e])) : 0.0;
+    }
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int64_t j = (int64_t)t + (int64_t)T * e;
+      if (j < cols) orow[j] = v[e];
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int64_t j = (int64_t)t + (int64_t)T * e;
+      v[e] = j < cols ? xr[j] : 0.0;
+    }
+  }
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
-    const int64_t j = (int64_t)t + (int64_t)T * e;
-    const double x = j < cols ? xr[j] : 0.0;
+    const double x = v[e];
     bad |= !isfinite(x);
     v[e] = __longlong_as_double(__double_as_longlong(x) ^ (long long)(((sg >> e) & 1ull) << 63));
   }
@@ -108,37 +139,66 @@ srht_kernel(int64_t cols, const double* __restrict__ X, int64_t ldx, int b, uint
   if (t < b) Y[row * ldy + t] = sr_smem[srht_pad(srht_sample(seed, t, N / b))];
 }
 
-// Y (rows x b, ld ldy) = X D H S.  Returns SP_ECONFIG when the shape is out of
-// the kernel's range (the caller falls back to a dense block on the GEMM).
-int srht_sketch(int64_t rows, int64_t cols, const double* X, int64_t ldx, int b, uint64_t seed, double* Y,
-                int64_t ldy, int* flag, cudaStream_t s) {
+static int srht_lt(int64_t cols) {
   int lt = 8;
   while (lt < 10 && ((int64_t)16 << lt) < cols) ++lt;
+  return lt;
+}
+
+bool srht_ok(int64_t rows, int64_t cols, int b) {
+  return cols >= 1 && cols <= ((int64_t)16 << srht_lt(cols)) && b >= 1 && b <= 32 && rows >= 1 &&
+         rows <= 0x7fffffff;
+}
+
+template <bool GATHER, typename TA>
+static int srht_launch(int64_t rows, int64_t cols, const double* X, int64_t ldx, int b, uint64_t seed, double* Y,
+                       int64_t ldy, int* flag, const TA* A, int64_t lda, const int64_t* gidx, double* Xout,
+                       cudaStream_t s) {
+  const int lt = srht_lt(cols);
   const int64_t n2 = (int64_t)16 << lt;
-  if (cols < 1 || cols > n2 || b < 1 || b > 32 || rows < 1 || rows > 0x7fffffff) {
-    set_error("srht_sketch: shape out of range");
-    return SP_ECONFIG;
-  }
   const size_t smem = (size_t)(n2 + n2 / 16) * sizeof(double);
   static int attr_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    SPB_CUDA(cudaFuncSetAttribute(srht_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    SPB_CUDA(cudaFuncSetAttribute(srht_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    SPB_CUDA(cudaFuncSetAttribute(srht_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    SPB_CUDA(cudaFuncSetAttribute(srht_kernel<8, GATHER, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    SPB_CUDA(cudaFuncSetAttribute(srht_kernel<9, GATHER, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    SPB_CUDA(cudaFuncSetAttribute(srht_kernel<10, GATHER, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr_dev = dev;
   }
   const dim3 grid((unsigned)rows);
   if (lt == 8)
-    srht_kernel<8><<<grid, 1 << 8, smem, s>>>(cols, X, ldx, b, seed, Y, ldy, flag);
+    SPB_CUDA(launch_pdl((srht_kernel<8, GATHER, TA>), dim3(grid), dim3(1 << 8), smem, s, cols, X, ldx, b, seed, Y, ldy, flag, A, lda, gidx, Xout));
   else if (lt == 9)
-    srht_kernel<9><<<grid, 1 << 9, smem, s>>>(cols, X, ldx, b, seed, Y, ldy, flag);
+    SPB_CUDA(launch_pdl((srht_kernel<9, GATHER, TA>), dim3(grid), dim3(1 << 9), smem, s, cols, X, ldx, b, seed, Y, ldy, flag, A, lda, gidx, Xout));
   else
-    srht_kernel<10><<<grid, 1 << 10, smem, s>>>(cols, X, ldx, b, seed, Y, ldy, flag);
+    SPB_CUDA(launch_pdl((srht_kernel<10, GATHER, TA>), dim3(grid), dim3(1 << 10), smem, s, cols, X, ldx, b, seed, Y, ldy, flag, A, lda, gidx, Xout));
   count_launch();
   SPB_CHECK_LAUNCH();
   return SP_OK;
+}
+
+// Y (rows x b, ld ldy) = X D H S.  Returns SP_ECONFIG when the shape is out of
+// the kernel's range (the caller falls back to a dense block on the GEMM).
+int srht_sketch(int64_t rows, int64_t cols, const double* X, int64_t ldx, int b, uint64_t seed, double* Y,
+                int64_t ldy, int* flag, cudaStream_t s) {
+  if (!srht_ok(rows, cols, b)) {
+    set_error("srht_sketch: shape out of range");
+    return SP_ECONFIG;
+  }
+  return srht_launch<false, double>(rows, cols, X, ldx, b, seed, Y, ldy, flag, nullptr, 0, nullptr, nullptr, s);
+}
+
+// C (rows x cols, ld ldc) = A(:, gidx) (exact copies) and Y = C D H S, one pass.
+int srht_gather(const void* A, int a_dtype, int64_t rows, int64_t lda, const int64_t* gidx, int64_t cols, double* C,
+                int64_t ldc, int b, uint64_t seed, double* Y, int64_t ldy, int* flag, cudaStream_t s) {
+  if (!srht_ok(rows, cols, b)) {
+    set_error("srht_gather: shape out of range");
+    return SP_ECONFIG;
+  }
+  if (a_dtype == SP_F32)
+    return srht_launch<true, float>(rows, cols, C, ldc, b, seed, Y, ldy, flag, (const float*)A, lda, gidx, C, s);
+  return srht_launch<true, double>(rows, cols, C, ldc, b, seed, Y, ldy, flag, (const double*)A, lda, gidx, C, s);
 }
 
 }  // namespace spb

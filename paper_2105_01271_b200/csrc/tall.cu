@@ -172,6 +172,7 @@ __global__ void __launch_bounds__(kTmThreads)
 tall_mul_kernel(int64_t rows, int c, const double* X, int64_t ldx, int d, const double* __restrict__ M,
                 int64_t ldm, double alpha, double beta, double* O, int64_t ldo, const double* __restrict__ top,
                 int64_t ldt, int64_t top_rows, int rpc) {
+  SPB_PDL_ENTRY();
   extern __shared__ __align__(16) double tm_smem[];
   const int sp = c + 1;
   double* ms = tm_smem;          // [c][d]
@@ -363,8 +364,8 @@ int tall_mul(int64_t rows, int c, const double* X, int64_t ldx, int d, const dou
   const int rpc = std::max(1, std::min(512, 2048 / d));
   const size_t smem = ((size_t)c * d + (size_t)rpc * (c + 1)) * sizeof(double);
   const int grid = (int)std::min<int64_t>(ceil_div(rows, rpc), 8 * kNumSMs);
-  tall_mul_kernel<<<grid, kTmThreads, smem, s>>>(rows, c, X, ldx, d, M, ldm, alpha, beta, O, ldo, top, ldt,
-                                                 top ? top_rows : 0, rpc);
+  SPB_CUDA(launch_pdl((tall_mul_kernel), dim3(grid), dim3(kTmThreads), smem, s, rows, c, X, ldx, d, M, ldm, alpha, beta, O, ldo, top, ldt,
+                                                 top ? top_rows : 0, rpc));
   count_launch();
   SPB_CHECK_LAUNCH();
   return SP_OK;

@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(kQThreads)
 tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t ldx, double* __restrict__ V,
                  double* __restrict__ Tg, double* __restrict__ Rs, double* __restrict__ Rfinal, int64_t ldr,
                  double* __restrict__ sgn) {
+  SPB_PDL_ENTRY();
   __shared__ double red[2][kQWarps][kQB];
   __shared__ double rowj[2][kQB];
   __shared__ double cbuf[2][kQMaxCluster][kQB];  // cluster partials (pushed by peers)
@@ -330,6 +331,7 @@ __global__ void __launch_bounds__(kQThreads)
 tsqr_apply_kernel(const double* __restrict__ V, const double* __restrict__ Tg, int64_t rows, int cols,
                   int chunk_rows, const double* __restrict__ Bin, const double* __restrict__ sgn,
                   double* __restrict__ Out, int64_t ldo) {
+  SPB_PDL_ENTRY();
   constexpr int P = kQB + 1;
   __shared__ double ub[kApRows * P];  // V_top | B_h, later the V rows of the tile
   __shared__ double tsm[kQB * P];     // T_h
@@ -425,13 +427,15 @@ static int launch_leaf(int nch, int cl, const double* in, int64_t r, int cols, i
   cfg.blockDim = dim3(kQThreads);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = cl;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // SPB_PDL_ENTRY in the kernel
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, tsqr_leaf_kernel, in, r, cols, in_ld, V, T, Rs, R, ldr, sgn);
   if (e != cudaSuccess) {
     cudaGetLastError();
@@ -523,8 +527,8 @@ static int tsqr32(int64_t rows, int cols, const double* X, int64_t ldx, double* 
       ldo = kQB;
     }
     const int chunk_rows = L.cl * kQCH;
-    tsqr_apply_kernel<<<L.nch * (chunk_rows / kApRows), kQThreads, 0, s>>>(L.V, L.T, L.rows, cols, chunk_rows, bin,
-                                                                          sgn, out, ldo);
+    SPB_CUDA(launch_pdl((tsqr_apply_kernel), dim3(L.nch * (chunk_rows / kApRows)), dim3(kQThreads), 0, s, L.V, L.T, L.rows, cols, chunk_rows, bin,
+                                                                          sgn, out, ldo));
     count_launch();
     SPB_CHECK_LAUNCH();
     bin = out;

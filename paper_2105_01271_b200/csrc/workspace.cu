@@ -1,5 +1,9 @@
 // Workspace caching allocator and pinned small reads (common.cuh).
+#include <chrono>
+#include <cstdlib>
+#include <cstdio>
 #include <cstring>
+#include <string>
 #include <map>
 #include <mutex>
 #include <vector>
@@ -144,6 +148,35 @@ int read_small(void* host_dst, const void* dev_src, size_t bytes, cudaStream_t s
   PinnedReads r(s);
   SPB_TRY(r.add(host_dst, dev_src, bytes));
   return r.sync();
+}
+
+// ------------------------------------------------------------ host trace ----
+namespace {
+struct HostTrace {
+  std::vector<std::pair<const char*, double>> ev;
+};
+thread_local HostTrace t_trace;
+const bool g_trace_on = std::getenv("SPB_HOST_TRACE") != nullptr;
+}  // namespace
+
+void host_mark(const char* tag) {
+  if (!g_trace_on) return;
+  const double us = std::chrono::duration<double, std::micro>(
+                        std::chrono::steady_clock::now().time_since_epoch()).count();
+  t_trace.ev.emplace_back(tag, us);
+}
+
+std::string host_trace_dump() {
+  std::string out;
+  char buf[160];
+  for (size_t i = 0; i < t_trace.ev.size(); ++i) {
+    const double d = i ? t_trace.ev[i].second - t_trace.ev[i - 1].second : 0.0;
+    std::snprintf(buf, sizeof(buf), "%9.1f %+8.1f  %s\n", t_trace.ev[i].second - t_trace.ev[0].second, d,
+                  t_trace.ev[i].first);
+    out += buf;
+  }
+  t_trace.ev.clear();
+  return out;
 }
 
 }  // namespace spb

@@ -19,12 +19,21 @@ def torch():
     return _torch
 
 
+_cuda_ok = False
+
+
 def require_cuda():
+    """torch, once a CUDA device is known to exist (checked once: the NVML /
+    environment probe of torch.cuda.is_available costs microseconds per call
+    on the pipelines' host path)."""
+    global _cuda_ok
     t = torch()
-    if not t.cuda.is_available():
-        raise SketchpressError(
-            "paper_2105_01271_b200 runs on a CUDA (sm_100a) device; none is available "
-            "(there is deliberately no CPU fallback)")
+    if not _cuda_ok:
+        if not t.cuda.is_available():
+            raise SketchpressError(
+                "paper_2105_01271_b200 runs on a CUDA (sm_100a) device; none is available "
+                "(there is deliberately no CPU fallback)")
+        _cuda_ok = True
     return t
 
 
@@ -46,7 +55,7 @@ def ptr(x) -> int | None:
 def empty(shape, dtype="f64"):
     t = require_cuda()
     td = t.float64 if dtype == "f64" else (t.float32 if dtype == "f32" else t.int64)
-    return t.empty(shape, dtype=td, device=device())
+    return t.empty(shape, dtype=td, device="cuda")
 
 
 def zeros(shape, dtype="f64"):
