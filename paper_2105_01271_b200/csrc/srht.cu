@@ -65,50 +65,14 @@ __device__ __forceinline__ void srht_stages(double (&v)[16], int nb) {
 // One CTA (2^LT threads) per row, N = 16 * 2^LT (zero-padded) elements:
 // the coalesced load is the round over the top 4 bits; then rounds of 4
 // bits through padded shared memory (the last one narrower if LT % 4 != 0).
-// GATHER: the row of X is gathered on the fly from A (X[row][j] =
-// A[row][gidx[j]], an exact copy, written to X as well): the coarse-column
-// block C = A(:, I) and its test block Y come out of one pass over A (K1 fused
-// with the range finder's first product).  Both modes give bit-identical Y.
-template <int LT, bool GATHER, typename TA>
-__global__ void __launch_bounds__(1 << LT)
-srht_kernel(int64_t cols, const double* __restrict__ X, int64_t ldx, int b, uint64_t seed, double* __restrict__ Y,
-            int64_t ldy, int* __restrict__ flag, const TA* __restrict__ A, int64_t lda,
-            const int64_t* __restrict__ gidx, double* __restrict__ Xout) {
-  SPB_PDL_ENTRY();
+// The transform of one row held as v[e] = element t + T e (sign applied
+// here); writes the b sampled outputs to yrow.  Uniform barriers only.
+template <int LT>
+__device__ __forceinline__ void srht_row(double (&v)[16], uint64_t sg, int b, uint64_t seed, double* sr_smem,
+                                         double* __restrict__ yrow, int* __restrict__ flag) {
   constexpr int T = 1 << LT, N = 16 * T;
-  extern __shared__ double sr_smem[];  // srht_pad(N) doubles
   const int t = threadIdx.x;
-  const int64_t row = blockIdx.x;
-  const double* xr = X + row * ldx;
-  const uint64_t sg = srht_hash(seed, (uint64_t)t);  // sign of element t + T e: bit e
-  double v[16];
   bool bad = false;
-  if (GATHER) {
-    const TA* ar = A + row * lda;
-    double* orow = Xout + row * ldx;
-    int64_t gi[16];
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      const int64_t j = (int64_t)t + (int64_t)T * e;
-      gi[e] = j < cols ? __ldg(gidx + j) : 0;
-    }
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      const int64_t j = (int64_t)t + (int64_t)T * e;
-      v[e] = j < cols ? widen(__ldg(ar + gi[e])) : 0.0;
-    }
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      const int64_t j = (int64_t)t + (int64_t)T * e;
-      if (j < cols) orow[j] = v[e];
-    }
-  } else {
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      const int64_t j = (int64_t)t + (int64_t)T * e;
-      v[e] = j < cols ? xr[j] : 0.0;
-    }
-  }
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
     const double x = v[e];
@@ -136,7 +100,72 @@ srht_kernel(int64_t cols, const double* __restrict__ X, int64_t ldx, int b, uint
 #pragma unroll
   for (int e = 0; e < 16; ++e) sr_smem[srht_pad(srht_index<LT>(t, e, plo, pnb))] = v[e];
   __syncthreads();
-  if (t < b) Y[row * ldy + t] = sr_smem[srht_pad(srht_sample(seed, t, N / b))];
+  if (t < b) yrow[t] = sr_smem[srht_pad(srht_sample(seed, t, N / b))];
+  __syncthreads();  // sr_smem is reused by the next row
+}
+
+// GATHER: the rows of X are gathered on the fly from A (X[row][j] =
+// A[row][gidx[j]], exact copies, written to X as well): the coarse-column
+// block C = A(:, I) and its test block Y come out of one pass over A (K1 fused
+// with the range finder's first product).  A gathering CTA takes RPC rows so
+// that RPC x 16 loads per thread are in flight behind one read of the index
+// table.  Both modes give bit-identical Y.
+template <int LT, bool GATHER, int RPC, typename TA>
+__global__ void __launch_bounds__(1 << LT)
+srht_kernel(int64_t rows, int64_t cols, const double* __restrict__ X, int64_t ldx, int b, uint64_t seed,
+            double* __restrict__ Y, int64_t ldy, int* __restrict__ flag, const TA* __restrict__ A, int64_t lda,
+            const int64_t* __restrict__ gidx, double* __restrict__ Xout) {
+  SPB_PDL_ENTRY();
+  constexpr int T = 1 << LT;
+  extern __shared__ double sr_smem[];  // srht_pad(N) doubles
+  const int t = threadIdx.x;
+  const int64_t row0 = (int64_t)blockIdx.x * RPC;
+  const uint64_t sg = srht_hash(seed, (uint64_t)t);  // sign of element t + T e: bit e
+  double v[RPC][16];
+  if (GATHER) {
+    int64_t gi[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int64_t j = (int64_t)t + (int64_t)T * e;
+      gi[e] = j < cols ? __ldg(gidx + j) : 0;
+    }
+#pragma unroll
+    for (int r = 0; r < RPC; ++r) {
+      const bool live = row0 + r < rows;
+      const TA* ar = A + (live ? row0 + r : 0) * lda;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int64_t j = (int64_t)t + (int64_t)T * e;
+        v[r][e] = (live && j < cols) ? widen(__ldg(ar + gi[e])) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RPC; ++r) {
+      if (row0 + r >= rows) break;
+      double* orow = Xout + (row0 + r) * ldx;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int64_t j = (int64_t)t + (int64_t)T * e;
+        if (j < cols) orow[j] = v[r][e];
+      }
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < RPC; ++r) {
+      const bool live = row0 + r < rows;
+      const double* xr = X + (live ? row0 + r : 0) * ldx;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int64_t j = (int64_t)t + (int64_t)T * e;
+        v[r][e] = (live && j < cols) ? xr[j] : 0.0;
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RPC; ++r) {
+    if (row0 + r >= rows) break;  // uniform
+    srht_row<LT>(v[r], sg, b, seed, sr_smem, Y + (row0 + r) * ldy, flag);
+  }
 }
 
 static int srht_lt(int64_t cols) {
@@ -154,6 +183,7 @@ template <bool GATHER, typename TA>
 static int srht_launch(int64_t rows, int64_t cols, const double* X, int64_t ldx, int b, uint64_t seed, double* Y,
                        int64_t ldy, int* flag, const TA* A, int64_t lda, const int64_t* gidx, double* Xout,
                        cudaStream_t s) {
+  constexpr int RPC = GATHER ? 2 : 1;
   const int lt = srht_lt(cols);
   const int64_t n2 = (int64_t)16 << lt;
   const size_t smem = (size_t)(n2 + n2 / 16) * sizeof(double);
@@ -161,18 +191,21 @@ static int srht_launch(int64_t rows, int64_t cols, const double* X, int64_t ldx,
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    SPB_CUDA(cudaFuncSetAttribute(srht_kernel<8, GATHER, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    SPB_CUDA(cudaFuncSetAttribute(srht_kernel<9, GATHER, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    SPB_CUDA(cudaFuncSetAttribute(srht_kernel<10, GATHER, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    SPB_CUDA(cudaFuncSetAttribute(srht_kernel<8, GATHER, RPC, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    SPB_CUDA(cudaFuncSetAttribute(srht_kernel<9, GATHER, RPC, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    SPB_CUDA(cudaFuncSetAttribute(srht_kernel<10, GATHER, RPC, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr_dev = dev;
   }
-  const dim3 grid((unsigned)rows);
+  const dim3 grid((unsigned)((rows + RPC - 1) / RPC));
   if (lt == 8)
-    SPB_CUDA(launch_pdl((srht_kernel<8, GATHER, TA>), dim3(grid), dim3(1 << 8), smem, s, cols, X, ldx, b, seed, Y, ldy, flag, A, lda, gidx, Xout));
+    SPB_CUDA(launch_pdl((srht_kernel<8, GATHER, RPC, TA>), grid, dim3(1 << 8), smem, s, rows, cols, X, ldx, b, seed,
+                        Y, ldy, flag, A, lda, gidx, Xout));
   else if (lt == 9)
-    SPB_CUDA(launch_pdl((srht_kernel<9, GATHER, TA>), dim3(grid), dim3(1 << 9), smem, s, cols, X, ldx, b, seed, Y, ldy, flag, A, lda, gidx, Xout));
+    SPB_CUDA(launch_pdl((srht_kernel<9, GATHER, RPC, TA>), grid, dim3(1 << 9), smem, s, rows, cols, X, ldx, b, seed,
+                        Y, ldy, flag, A, lda, gidx, Xout));
   else
-    SPB_CUDA(launch_pdl((srht_kernel<10, GATHER, TA>), dim3(grid), dim3(1 << 10), smem, s, cols, X, ldx, b, seed, Y, ldy, flag, A, lda, gidx, Xout));
+    SPB_CUDA(launch_pdl((srht_kernel<10, GATHER, RPC, TA>), grid, dim3(1 << 10), smem, s, rows, cols, X, ldx, b,
+                        seed, Y, ldy, flag, A, lda, gidx, Xout));
   count_launch();
   SPB_CHECK_LAUNCH();
   return SP_OK;
