@@ -218,6 +218,21 @@ int sp_row_id(int64_t m, int64_t cols, const double* M, int64_t ldm, int32_t k, 
 int sp_sketch_basis(const double* X, int64_t rows, int64_t cols, int64_t ldx, double power, int32_t r_max,
                     double* U, int64_t ldu, double* S, int64_t* info, void* stream);
 
+/* Range-finder test block of the sketch-side subspace iteration (srht.cu):
+ * Y (rows x b, ld ldy) = X D H S -- random signs, Walsh-Hadamard transform of
+ * the zero-padded width, b stratified column samples (the structured
+ * replacement of the dense Gaussian block of np.random-style range finders;
+ * Halko, Martinsson & Tropp sec. 4.6).  cols <= 16384, b <= 32.  *flag
+ * (device int, may be NULL) is OR-ed with 1 if X has a non-finite entry.
+ * sp_srht_gather forms X = A(:, gidx) (exact copies, written to X) and the
+ * same Y in one pass over A (K1 fused with the first product; the power
+ * pipeline uses it for a device-resident A).  SP_ECONFIG outside the range. */
+int sp_srht_sketch(int64_t rows, int64_t cols, const double* X, int64_t ldx, int32_t b, uint64_t seed,
+                   double* Y, int64_t ldy, int32_t* flag, void* stream);
+int sp_srht_gather(const void* A, int32_t a_dtype, int64_t rows, int64_t lda, const int64_t* gidx, int64_t cols,
+                   double* X, int64_t ldx, int32_t b, uint64_t seed, double* Y, int64_t ldy, int32_t* flag,
+                   void* stream);
+
 /* Orthonormal completion of out[:, 0:r) (orthonormal, N x r) into
  * out[:, r:k) by Householder reconstruction (LU of Q - [S;0]; no QR).  If
  * kp_out (r x (k-r)) is non-NULL it receives K', so that for a row-sharded Q

@@ -32,6 +32,10 @@ int power_id(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, cons
 int row_id(int64_t m, int64_t cols, const double* M, int64_t ldm, int k, double* P, int64_t* indices,
            int* warn, cudaStream_t s);
 int deferred_status(int* out);
+int srht_sketch(int64_t rows, int64_t cols, const double* X, int64_t ldx, int b, uint64_t seed, double* Y,
+                int64_t ldy, int* flag, cudaStream_t s);
+int srht_gather(const void* A, int a_dtype, int64_t rows, int64_t lda, const int64_t* gidx, int64_t cols, double* C,
+                int64_t ldc, int b, uint64_t seed, double* Y, int64_t ldy, int* flag, cudaStream_t s);
 std::string host_trace_dump();
 void set_finish_mode(int mode);
 int sketch_basis(const double* X, int64_t rows, int64_t cols, int64_t ldx, double power, int r_max, double* U,
@@ -166,6 +170,21 @@ int sp_row_id(int64_t m, int64_t cols, const double* M, int64_t ldm, int32_t k, 
 int sp_sketch_basis(const double* X, int64_t rows, int64_t cols, int64_t ldx, double power, int32_t r_max,
                     double* U, int64_t ldu, double* S, int64_t* info, void* stream) {
   return sketch_basis(X, rows, cols, ldx, power, r_max, U, ldu, S, info, ST(stream));
+}
+
+int sp_srht_sketch(int64_t rows, int64_t cols, const double* X, int64_t ldx, int32_t b, uint64_t seed,
+                   double* Y, int64_t ldy, int32_t* flag, void* stream) {
+  return srht_sketch(rows, cols, X, ldx, b, seed, Y, ldy, flag, ST(stream));
+}
+
+int sp_srht_gather(const void* A, int32_t a_dtype, int64_t rows, int64_t lda, const int64_t* gidx, int64_t cols,
+                   double* X, int64_t ldx, int32_t b, uint64_t seed, double* Y, int64_t ldy, int32_t* flag,
+                   void* stream) {
+  if (a_dtype != SP_F64 && a_dtype != SP_F32) {
+    set_error("unknown dtype tag");
+    return SP_ECONFIG;
+  }
+  return srht_gather(A, a_dtype, rows, lda, gidx, cols, X, ldx, b, seed, Y, ldy, flag, ST(stream));
 }
 
 int sp_householder_complete(int64_t N, int32_t r, int32_t k, double* out, int64_t ldo, double* kp_out,

@@ -9,7 +9,7 @@
 // block only has to capture the dominant column space; the Rayleigh-Ritz
 // step and the convergence tests that follow are unchanged.
 //
-// One CTA per row (256..1024 threads, 16 elements each, widths up to 16384):
+// One CTA per row (16..1024 threads, 16 elements each, widths up to 16384):
 // the top 4 index bits are transformed in registers straight from the
 // coalesced load, the rest in rounds of 4 bits through padded shared memory
 // (a thread's 16 slots re-mapped to the round's bits), then the b sampled
@@ -100,7 +100,7 @@ __device__ __forceinline__ void srht_row(double (&v)[16], uint64_t sg, int b, ui
 #pragma unroll
   for (int e = 0; e < 16; ++e) sr_smem[srht_pad(srht_index<LT>(t, e, plo, pnb))] = v[e];
   __syncthreads();
-  if (t < b) yrow[t] = sr_smem[srht_pad(srht_sample(seed, t, N / b))];
+  for (int c = t; c < b; c += T) yrow[c] = sr_smem[srht_pad(srht_sample(seed, c, N / b))];
   __syncthreads();  // sr_smem is reused by the next row
 }
 
@@ -168,15 +168,18 @@ srht_kernel(int64_t rows, int64_t cols, const double* __restrict__ X, int64_t ld
   }
 }
 
+// padded width N = 16 * 2^LT = the next power of two >= cols (>= 256): a
+// wider pad would leave the sampled Hadamard columns distinguished by their
+// low bits only on the first `cols` rows (colliding samples)
 static int srht_lt(int64_t cols) {
-  int lt = 8;
+  int lt = 4;
   while (lt < 10 && ((int64_t)16 << lt) < cols) ++lt;
   return lt;
 }
 
 bool srht_ok(int64_t rows, int64_t cols, int b) {
-  return cols >= 1 && cols <= ((int64_t)16 << srht_lt(cols)) && b >= 1 && b <= 32 && rows >= 1 &&
-         rows <= 0x7fffffff;
+  const int64_t n2 = (int64_t)16 << srht_lt(cols);
+  return cols >= 1 && cols <= n2 && b >= 1 && b <= 32 && n2 % b == 0 && rows >= 1 && rows <= 0x7fffffff;
 }
 
 template <bool GATHER, typename TA>
@@ -191,21 +194,23 @@ static int srht_launch(int64_t rows, int64_t cols, const double* X, int64_t ldx,
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    SPB_CUDA(cudaFuncSetAttribute(srht_kernel<8, GATHER, RPC, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     SPB_CUDA(cudaFuncSetAttribute(srht_kernel<9, GATHER, RPC, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     SPB_CUDA(cudaFuncSetAttribute(srht_kernel<10, GATHER, RPC, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr_dev = dev;
   }
   const dim3 grid((unsigned)((rows + RPC - 1) / RPC));
-  if (lt == 8)
-    SPB_CUDA(launch_pdl((srht_kernel<8, GATHER, RPC, TA>), grid, dim3(1 << 8), smem, s, rows, cols, X, ldx, b, seed,
-                        Y, ldy, flag, A, lda, gidx, Xout));
-  else if (lt == 9)
-    SPB_CUDA(launch_pdl((srht_kernel<9, GATHER, RPC, TA>), grid, dim3(1 << 9), smem, s, rows, cols, X, ldx, b, seed,
-                        Y, ldy, flag, A, lda, gidx, Xout));
-  else
-    SPB_CUDA(launch_pdl((srht_kernel<10, GATHER, RPC, TA>), grid, dim3(1 << 10), smem, s, rows, cols, X, ldx, b,
-                        seed, Y, ldy, flag, A, lda, gidx, Xout));
+  switch (lt) {
+#define SPB_SRHT_LT(L)                                                                                              \
+  case L:                                                                                                           \
+    SPB_CUDA(launch_pdl((srht_kernel<L, GATHER, RPC, TA>), grid, dim3(1 << L), smem, s, rows, cols, X, ldx, b, seed, \
+                        Y, ldy, flag, A, lda, gidx, Xout));                                                         \
+    break;
+    SPB_SRHT_LT(4) SPB_SRHT_LT(5) SPB_SRHT_LT(6) SPB_SRHT_LT(7) SPB_SRHT_LT(8) SPB_SRHT_LT(9) SPB_SRHT_LT(10)
+#undef SPB_SRHT_LT
+    default:
+      set_error("srht: width out of range");
+      return SP_ECONFIG;
+  }
   count_launch();
   SPB_CHECK_LAUNCH();
   return SP_OK;

@@ -346,3 +346,73 @@ def test_frob_residual(cuda, m, n, k, f32):
     a64 = a.astype(np.float64)
     want = np.sum((a64 - (u * s) @ v.T) ** 2), np.sum(a64 ** 2)
     np.testing.assert_allclose(out, want, rtol=1e-12)
+
+
+# ------------------------------------------------------- SRHT test block ----
+def _srht(cuda, x, b, seed=7):
+    rows, cols = x.shape
+    X = _dev(x, cuda)
+    Y = cuda.empty((rows, b), dtype=cuda.float64, device="cuda")
+    flag = cuda.zeros(1, dtype=cuda.int32, device="cuda")
+    _lib.call("sp_srht_sketch", rows, cols, X.data_ptr(), cols, b, seed, Y.data_ptr(), b, flag.data_ptr(),
+              _stream(cuda))
+    return Y.cpu().numpy(), int(flag.item())
+
+
+@pytest.mark.parametrize("cols,b", [(256, 32), (300, 32), (1000, 16), (4096, 32), (4096, 16), (5000, 32),
+                                    (16384, 32)])
+def test_srht_is_a_scaled_orthogonal_sampling(cuda, cols, b):
+    # Omega = D H S (one row per basis vector): Omega^T Omega = N I_b exactly
+    # (distinct Hadamard columns of the padded width N), and Y(X) = X Omega.
+    n2 = 256
+    while n2 < cols:
+        n2 *= 2
+    x = philox(cols + b).standard_normal((37, cols))
+    y, _ = _srht(cuda, x, b)
+    if cols > 5000:  # explicit Omega too large: linearity and the scale of H
+        x2 = philox(cols + 2 * b).standard_normal((37, cols))
+        y2, _ = _srht(cuda, x2, b)
+        y12, _ = _srht(cuda, x + x2, b)
+        np.testing.assert_allclose(y12, y + y2, rtol=0, atol=1e-11 * np.sqrt(cols) * 40)
+        return
+    eye = np.eye(cols)
+    om, flag = _srht(cuda, eye, b)
+    assert flag == 0
+    assert set(np.unique(np.abs(om))) <= {1.0}  # +-1 entries
+    if cols == n2:  # unpadded width: the sampled Hadamard columns are exactly orthogonal
+        np.testing.assert_array_equal(om.T @ om, n2 * np.eye(b))
+    else:  # padded to the next power of two: still full column rank
+        assert np.linalg.matrix_rank(om) == b
+    np.testing.assert_allclose(y, x @ om, rtol=0, atol=1e-13 * np.abs(x).sum(axis=1).max())
+    # deterministic: bitwise identical on a second call
+    y2, _ = _srht(cuda, x, b)
+    assert np.array_equal(y, y2)
+
+
+def test_srht_flags_non_finite_input(cuda):
+    x = philox(3).standard_normal((10, 700))
+    x[4, 123] = np.nan
+    _, flag = _srht(cuda, x, 32)
+    assert flag == 1
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_srht_gather_is_exact_and_matches_two_step(cuda, dtype):
+    a = philox(11).standard_normal((130, 9000))
+    if dtype == "f32":
+        a = a.astype(np.float32)
+    a[5, 17] = -0.0
+    idx = np.sort(philox(12).choice(9000, size=4000, replace=False)).astype(np.int64)
+    A = _dev(a, cuda)
+    I = _dev(idx, cuda)
+    X = cuda.empty((130, idx.size), dtype=cuda.float64, device="cuda")
+    Y = cuda.empty((130, 32), dtype=cuda.float64, device="cuda")
+    flag = cuda.zeros(1, dtype=cuda.int32, device="cuda")
+    tag = _lib.SP_F64 if dtype == "f64" else _lib.SP_F32
+    _lib.call("sp_srht_gather", A.data_ptr(), tag, 130, 9000, I.data_ptr(), idx.size, X.data_ptr(), idx.size, 32, 99,
+              Y.data_ptr(), 32, flag.data_ptr(), _stream(cuda))
+    xg = X.cpu().numpy()
+    want = a[:, idx].astype(np.float64)
+    assert np.array_equal(xg.view(np.int64), want.view(np.int64))  # bit-exact copies, -0.0 kept
+    y2, f2 = _srht(cuda, want, 32, seed=99)
+    assert np.array_equal(Y.cpu().numpy(), y2) and int(flag.item()) == 0 and f2 == 0
