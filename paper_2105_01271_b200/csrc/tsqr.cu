@@ -64,7 +64,7 @@ constexpr int kQDiagSlots = kQB / kQWarps;  // 4
 __global__ void __launch_bounds__(kQThreads)
 tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t ldx, double* __restrict__ V,
                  double* __restrict__ Tg, double* __restrict__ Rs, double* __restrict__ Rfinal, int64_t ldr,
-                 double* __restrict__ sgn) {
+                 double* __restrict__ sgn, double* __restrict__ Mg) {
   SPB_PDL_ENTRY();
   __shared__ double red[2][kQWarps][kQB];
   __shared__ double rowj[2][kQB];
@@ -266,6 +266,16 @@ tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t l
     if (g < nrow) V[(c0 + g) * kQB + c] = (gc > c && c < nref) ? x[i] * inv_c : 0.0;
   }
   if (!top) return;
+  // root with Mg: keep V_top (reflector rows 0..31, unit diagonal) for M below
+  __shared__ double vtop_s[kQB][kQB + 1];
+  __shared__ double sg_s[kQB];
+  if (Mg != nullptr) {
+#pragma unroll
+    for (int i = 0; i < kQDiagSlots; ++i) {
+      const int g = qrow(i, w);
+      vtop_s[g][c] = c < nref ? (g > c ? x[i] * inv_c : (g == c ? 1.0 : 0.0)) : 0.0;
+    }
+  }
   // compact-WY T by recursive doubling: for adjacent blocks [V1 V2] of width
   // b, T12 = -T11 (V1^T V2) T22 (exact for tau = 0 too); 5 levels of two
   // parallel small products instead of a 32-step serial recurrence.
@@ -315,9 +325,66 @@ tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t l
         const double d = __shfl_sync(0xffffffffu, x[i], g);
         const double sg = d < 0.0 ? -1.0 : 1.0;
         if (c < cols) Rfinal[(int64_t)g * ldr + c] = (c >= g) ? sg * x[i] : 0.0;
-        if (c == 0) sgn[g] = sg;
+        if (c == 0) {
+          sgn[g] = sg;
+          sg_s[g] = sg;
+        }
       }
     }
+    if (Mg != nullptr) {
+      // M = T V_top^T diag(sgn) (the root's Q = [diag(sgn); 0] - V M), so the
+      // Q pass (tsqr_q_kernel) is one small product per row
+      __syncthreads();
+      for (int e = threadIdx.x; e < kQB * kQB; e += kQThreads) {
+        const int k = e / kQB, cc = e % kQB;
+        double a = 0.0;
+        if (cc < cols) {
+          for (int l = k; l < kQB; ++l) a = fma(ts[k][l], vtop_s[cc][l], a);
+          a *= sg_s[cc];
+        }
+        Mg[e] = a;
+      }
+    }
+  }
+}
+
+// Q of a single-chunk TSQR: rows [0, rows) of Q = [diag(sgn); 0] - V M, M from
+// the root leaf (32 x 32).  CTA = 64 rows; thread (row, 8-column group).
+__global__ void __launch_bounds__(kQThreads)
+tsqr_q_kernel(const double* __restrict__ V, const double* __restrict__ Mg, const double* __restrict__ sgn,
+              int64_t rows, int cols, double* __restrict__ Q, int64_t ldq) {
+  SPB_PDL_ENTRY();
+  constexpr int P = kQB + 1;
+  __shared__ double ms[kQB * P];
+  __shared__ double vs[64 * P];
+  const int t = threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.x * 64;
+  const int nr = (int)imin64(64, rows - r0);
+  for (int e = t; e < kQB * kQB; e += kQThreads) cp_async_f64(&ms[(e / kQB) * P + (e % kQB)], Mg + e, true);
+  for (int e = t; e < 64 * kQB; e += kQThreads) {
+    const int g = e / kQB, k = e % kQB;
+    cp_async_f64(&vs[g * P + k], V + (r0 + (g < nr ? g : 0)) * kQB + k, g < nr);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  if (r0 < kQB && t < nr && r0 + t < kQB) vs[t * P + r0 + t] = 1.0;  // implicit unit diagonal
+  __syncthreads();
+  const int g = t >> 2, c0 = (t & 3) * 8;
+  if (g >= nr) return;
+  double acc[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+#pragma unroll 8
+  for (int k = 0; k < kQB; ++k) {
+    const double v = vs[g * P + k];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = fma(v, ms[k * P + c0 + u], acc[u]);
+  }
+  const int64_t gr = r0 + g;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int cc = c0 + u;
+    if (cc < cols) Q[gr * ldq + cc] = (gr == cc ? sgn[cc] : 0.0) - acc[u];
   }
 }
 
@@ -421,7 +488,7 @@ tsqr_apply_kernel(const double* __restrict__ V, const double* __restrict__ Tg, i
 static int g_max_cluster = 0;
 
 static int launch_leaf(int nch, int cl, const double* in, int64_t r, int cols, int64_t in_ld, double* V, double* T,
-                       double* Rs, double* R, int64_t ldr, double* sgn, cudaStream_t s) {
+                       double* Rs, double* R, int64_t ldr, double* sgn, cudaStream_t s, double* Mg = nullptr) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nch * cl);
   cfg.blockDim = dim3(kQThreads);
@@ -436,7 +503,7 @@ static int launch_leaf(int nch, int cl, const double* in, int64_t r, int cols, i
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, tsqr_leaf_kernel, in, r, cols, in_ld, V, T, Rs, R, ldr, sgn);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, tsqr_leaf_kernel, in, r, cols, in_ld, V, T, Rs, R, ldr, sgn, Mg);
   if (e != cudaSuccess) {
     cudaGetLastError();
     set_error(std::string("tsqr leaf launch: ") + cudaGetErrorString(e));
@@ -502,6 +569,16 @@ static int tsqr32(int64_t rows, int cols, const double* X, int64_t ldx, double* 
       return SP_ECUDA;
     }
     const bool root = L.nch == 1;
+    if (root && lv.empty()) {
+      // single chunk: the root leaf also forms M; Q is one small product per row
+      SPB_ALLOC(ar, double, Mg, (size_t)kQB * kQB);
+      SPB_TRY(launch_leaf(1, L.cl, in, r, cols, in_ld, L.V, L.T, L.Rs, R, ldr, sgn, s, Mg));
+      SPB_CUDA(launch_pdl((tsqr_q_kernel), dim3(ceil_div(r, 64)), dim3(kQThreads), 0, s, (const double*)L.V,
+                          (const double*)Mg, (const double*)sgn, r, cols, Q, ldq));
+      count_launch();
+      SPB_CHECK_LAUNCH();
+      return SP_OK;
+    }
     SPB_TRY(launch_leaf(L.nch, L.cl, in, r, cols, in_ld, L.V, L.T, L.Rs, root ? R : nullptr, ldr,
                         root ? sgn : nullptr, s));
     lv.push_back(L);
