@@ -303,6 +303,100 @@ gram_rows_kernel(int64_t rows, const double* __restrict__ Y, const double* __res
   }
 }
 
+// Streaming variant for R <= 8 (every BASELINE configuration): thread per
+// row, the R (R + 1) / 2 products accumulated in registers, no shared-memory
+// staging or per-chunk barriers -- a plain read of Y at HBM rate even when n
+// is 10^6..10^7 (the staged kernel above is latency-bound there).  Same tail.
+constexpr int kGsThreads = 256;
+
+template <int R>
+__global__ void __launch_bounds__(kGsThreads)
+gram_stream_kernel(int64_t rows, const double* __restrict__ Y, const double* __restrict__ R1i,
+                   double* __restrict__ partial, GramTail tail) {
+  SPB_PDL_ENTRY();
+  constexpr int NP = R * (R + 1) / 2, nout = R * R;
+  __shared__ double ri[R][R];
+  __shared__ double red[kGsThreads / 32][NP];
+  __shared__ SmallMat G, Ri;
+  __shared__ double rdiag[kMR];
+  __shared__ int last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (R1i)
+    for (int e = tid; e < nout; e += kGsThreads) ri[e / R][e % R] = R1i[e];
+  __syncthreads();
+  double acc[NP];
+#pragma unroll
+  for (int e = 0; e < NP; ++e) acc[e] = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * kGsThreads;
+  for (int64_t row = (int64_t)blockIdx.x * kGsThreads + tid; row < rows; row += stride) {
+    double x[R];
+    const double* yr = Y + row * R;
+#pragma unroll
+    for (int i = 0; i < R; ++i) x[i] = __ldg(yr + i);
+    if (R1i) {  // x = y R1^{-1}, the summation order of gram_rows / finish_core / finish_rows
+      double q[R];
+#pragma unroll
+      for (int j = 0; j < R; ++j) q[j] = 0.0;
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+#pragma unroll
+        for (int j = 0; j < R; ++j) q[j] = fma(x[i], ri[i][j], q[j]);
+#pragma unroll
+      for (int j = 0; j < R; ++j) x[j] = q[j];
+    }
+    int e = 0;
+#pragma unroll
+    for (int a = 0; a < R; ++a)
+#pragma unroll
+      for (int b = a; b < R; ++b) {
+        acc[e] = fma(x[a], x[b], acc[e]);
+        ++e;
+      }
+  }
+  // warp sums (fixed shuffle order), then the 8 warps in order
+#pragma unroll
+  for (int e = 0; e < NP; ++e) {
+    const double v = warp_sum(acc[e]);
+    if (lane == 0) red[warp][e] = v;
+  }
+  __syncthreads();
+  if (tid < nout) {
+    const int a = tid / R, b = tid % R;
+    const int e = a <= b ? a * R - a * (a - 1) / 2 + (b - a) : b * R - b * (b - 1) / 2 + (a - b);
+    double t = 0.0;
+    for (int w = 0; w < kGsThreads / 32; ++w) t += red[w][e];
+    partial[(int64_t)blockIdx.x * nout + tid] = t;
+  }
+  if (!tail.ticket) return;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = atomicAdd(tail.ticket, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (tid < nout) {
+    const int nb = gridDim.x;
+    double s0 = 0.0, s1 = 0.0;
+    int bb = 0;
+    for (; bb + 1 < nb; bb += 2) {
+      s0 += __ldcg(partial + (int64_t)bb * nout + tid);
+      s1 += __ldcg(partial + (int64_t)(bb + 1) * nout + tid);
+    }
+    if (bb < nb) s0 += __ldcg(partial + (int64_t)bb * nout + tid);
+    G[tid / R][tid % R] = s0 + s1;
+  }
+  __syncthreads();
+  if (tid < 32) {
+    const bool ok = chol_inv_warp<R>(G, Ri, rdiag, tail.shift_rel, tid);
+    if (!ok && tid == 0) atomicOr(tail.flag, 1);
+    for (int e = tid; e < nout; e += 32) {
+      tail.R[e] = ok ? G[e / R][e % R] : 0.0;
+      tail.Rinv[e] = ok ? Ri[e / R][e % R] : 0.0;
+    }
+    if (tid == 0) *tail.ticket = 0;
+  }
+}
+
 // ------------------------------------------------------------ the core ----
 // Householder-reconstruction completion (complete.cu header) of the r x k
 // problem X (k x r top rows of an orthonormal N x r factor, smem) for the
@@ -601,13 +695,32 @@ finish_core_kernel(int k, int nb2, const double* __restrict__ P2, const double* 
   if (tid == 0) SPB_TPRINT("finish_core reduce/chol/jacobi/sort/xtop/hh", 7);
 }
 
-// One streaming pass: rows [0, m) of U (blocks [0, bu)) and [0, n) of V.
-// A CTA owns 128 rows: threads 0..127 form the row inputs (for V, q1 = y
-// R1^{-1} in gram_rows' summation order) into shared memory; then each warp
-// writes 16 whole rows, lanes across the k output columns (coalesced
-// stores, no index division).
+// One streaming pass: rows [0, m) of U (tiles [0, bu)) and [0, n) of V.
+// Persistent CTAs walk 128-row tiles; the next tile's input rows are
+// prefetched (cp.async, double buffer) while the current one is written.
+// Per tile: threads 0..127 form the row inputs (for V, q1 = y R1^{-1} in the
+// Gram passes' summation order) into shared memory; then groups of k (warp-
+// rounded) threads write whole rows, the threads across the output columns
+// (coalesced stores), each thread's Mf column in registers.
 constexpr int kFrRows = 128;
 constexpr int kFrThreads = 256;
+
+template <int R>
+__device__ __forceinline__ void fr_prefetch(int64_t tile, int bu, int64_t m, int64_t n, const double* Z, int64_t ldz,
+                                            const double* Y, int64_t ldy, double* buf, int t) {
+  const bool isv = tile >= bu;
+  const int64_t rows = isv ? n : m;
+  const int64_t base = (isv ? tile - bu : tile) * kFrRows;
+  const double* X = isv ? Y : Z;
+  const int64_t ldx = isv ? ldy : ldz;
+  const int nr = (int)imin64(kFrRows, rows - base);
+  for (int e = t; e < kFrRows * R; e += kFrThreads) {
+    const int rl = e / R, i = e - rl * R;
+    const bool ok = rl < nr;
+    cp_async_f64(&buf[e], ok ? X + (base + rl) * ldx + i : X, ok);
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
 
 template <int R>
 __global__ void __launch_bounds__(kFrThreads)
@@ -617,84 +730,81 @@ finish_rows_kernel(int k, int64_t m, int64_t n, int bu, const double* __restrict
                    const double* __restrict__ EtfV, double* __restrict__ U, double* __restrict__ V) {
   SPB_PDL_ENTRY();
   extern __shared__ __align__(16) double fr_smem[];
-  double* mf = fr_smem;               // R x k
-  double* ri = mf + R * k;            // R x R
-  double* qs = ri + R * R;            // kFrRows x (R + 1)
-  const bool isv = blockIdx.x >= bu;
-  const int64_t rows = isv ? n : m;
-  const int64_t base = (int64_t)(isv ? blockIdx.x - bu : blockIdx.x) * kFrRows;
-  const double* X = isv ? Y : Z;
-  const int64_t ldx = isv ? ldy : ldz;
-  const double* Mf = isv ? MfV : MfU;
-  const double* Et = isv ? EtfV : EtfU;
-  double* O = isv ? V : U;
+  double* mfu = fr_smem;                   // R x k
+  double* mfv = mfu + R * k;               // R x k
+  double* ri = mfv + R * k;                // R x R
+  double* xb = ri + R * R;                 // 2 x kFrRows x R (input rows, double buffer)
+  double* qs = xb + 2 * kFrRows * R;       // kFrRows x (R + 1)
   const int t = threadIdx.x;
-  for (int e = t; e < R * k; e += kFrThreads) cp_async_f64(&mf[e], Mf + e, true);
-  if (isv)
-    for (int e = t; e < R * R; e += kFrThreads) cp_async_f64(&ri[e], R1i + e, true);
-  const int nr = (int)imin64(kFrRows, rows - base);
-  double x[R];
-#pragma unroll
-  for (int i = 0; i < R; ++i) x[i] = t < nr ? X[(base + t) * ldx + i] : 0.0;
-  cp_async_wait_all();
-  __syncthreads();
-  if (t < kFrRows) {
-    if (isv) {  // q1 = y R1^{-1}, gram_rows' summation order
-      double q[R];
-#pragma unroll
-      for (int j = 0; j < R; ++j) q[j] = 0.0;
-#pragma unroll
-      for (int i = 0; i < R; ++i)
-#pragma unroll
-        for (int j = 0; j < R; ++j) q[j] = fma(x[i], ri[i * R + j], q[j]);
-#pragma unroll
-      for (int j = 0; j < R; ++j) x[j] = q[j];
-    }
-#pragma unroll
-    for (int j = 0; j < R; ++j) qs[t * (R + 1) + j] = x[j];
+  const int64_t ntiles = (int64_t)bu + (n + kFrRows - 1) / kFrRows;
+  int64_t tile = blockIdx.x;
+  if (tile >= ntiles) return;
+  fr_prefetch<R>(tile, bu, m, n, Z, ldz, Y, ldy, xb, t);
+  for (int e = t; e < R * k; e += kFrThreads) {
+    mfu[e] = MfU[e];
+    mfv[e] = MfV[e];
   }
-  __syncthreads();
-  const int warp = t >> 5, lane = t & 31;
-  if (k <= 64) {
-    // the lane's (up to) two output columns of Mf stay in registers
-    double m0[R], m1[R];
-#pragma unroll
-    for (int p = 0; p < R; ++p) {
-      m0[p] = lane < k ? mf[p * k + lane] : 0.0;
-      m1[p] = lane + 32 < k ? mf[p * k + lane + 32] : 0.0;
+  for (int e = t; e < R * R; e += kFrThreads) ri[e] = R1i[e];
+  // column mapping: kpad = k rounded up to a warp multiple (<= 256), ngrp
+  // thread groups of kpad threads each take every ngrp-th row of a tile
+  const int kpad = (k + 31) / 32 * 32 < kFrThreads ? (k + 31) / 32 * 32 : kFrThreads;
+  const int ngrp = kFrThreads / kpad, grp = t / kpad, cl = t - grp * kpad;
+  for (int it = 0; tile < ntiles; tile += gridDim.x, ++it) {
+    const bool isv = tile >= bu;
+    const int64_t rows = isv ? n : m;
+    const int64_t base = (isv ? tile - bu : tile) * kFrRows;
+    const int nr = (int)imin64(kFrRows, rows - base);
+    const double* Et = isv ? EtfV : EtfU;
+    double* O = isv ? V : U;
+    double* cb = xb + (it & 1) * kFrRows * R;
+    // prefetch the next tile into the other buffer, then wait for this one
+    const int64_t nxt = tile + gridDim.x;
+    if (nxt < ntiles) {
+      fr_prefetch<R>(nxt, bu, m, n, Z, ldz, Y, ldy, xb + ((it + 1) & 1) * kFrRows * R, t);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     }
-    for (int rl = warp; rl < nr; rl += kFrThreads / 32) {
-      double o0 = 0.0, o1 = 0.0;
+    __syncthreads();
+    if (t < nr) {
+      double x[R];
 #pragma unroll
-      for (int p = 0; p < R; ++p) {
-        const double q = qs[rl * (R + 1) + p];
-        o0 = fma(q, m0[p], o0);
-        o1 = fma(q, m1[p], o1);
+      for (int i = 0; i < R; ++i) x[i] = cb[t * R + i];
+      if (isv) {  // q1 = y R1^{-1}, the Gram passes' summation order
+        double q[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) q[j] = 0.0;
+#pragma unroll
+        for (int i = 0; i < R; ++i)
+#pragma unroll
+          for (int j = 0; j < R; ++j) q[j] = fma(x[i], ri[i * R + j], q[j]);
+#pragma unroll
+        for (int j = 0; j < R; ++j) x[j] = q[j];
       }
-      const int64_t row = base + rl;
-      double* orow = O + row * k;
-      if (row < k) {
-        if (lane < k) o0 += Et[row * k + lane];
-        if (lane + 32 < k) o1 += Et[row * k + lane + 32];
+#pragma unroll
+      for (int j = 0; j < R; ++j) qs[t * (R + 1) + j] = x[j];
+    }
+    __syncthreads();
+    const double* mf = isv ? mfv : mfu;
+    // thread (group, column): the column's Mf entries in registers, the rows
+    // of the tile split over the groups; a warp stores 32 consecutive columns
+    for (int c0 = 0; c0 < k; c0 += kpad) {
+      const int c = c0 + cl;
+      double mcol[R];
+#pragma unroll
+      for (int p = 0; p < R; ++p) mcol[p] = c < k ? mf[p * k + c] : 0.0;
+      if (c < k) {
+        for (int rl = grp; rl < nr; rl += ngrp) {
+          double o = 0.0;
+#pragma unroll
+          for (int p = 0; p < R; ++p) o = fma(qs[rl * (R + 1) + p], mcol[p], o);
+          const int64_t row = base + rl;
+          if (row < k) o += Et[row * k + c];
+          O[row * k + c] = o;
+        }
       }
-      if (lane < k) orow[lane] = o0;
-      if (lane + 32 < k) orow[lane + 32] = o1;
     }
-    return;
-  }
-  for (int rl = warp; rl < nr; rl += kFrThreads / 32) {
-    double q[R];
-#pragma unroll
-    for (int p = 0; p < R; ++p) q[p] = qs[rl * (R + 1) + p];
-    const int64_t row = base + rl;
-    double* orow = O + row * k;
-    for (int c = lane; c < k; c += 32) {
-      double o = 0.0;
-#pragma unroll
-      for (int p = 0; p < R; ++p) o = fma(q[p], mf[p * k + c], o);
-      if (row < k) o += Et[row * k + c];
-      orow[c] = o;
-    }
+    __syncthreads();  // qs and this buffer are rewritten next iteration
   }
 }
 
@@ -709,7 +819,10 @@ template <int R>
 static int finish_fused_r(int64_t m, int64_t n, const double* Z, int64_t ldz, const double* Y, int k, double* U,
                           double* S, double* V, int* dflag, cudaStream_t s) {
   Arena ar(s);
-  const int nb = (int)std::min<int64_t>(kNumSMs, ceil_div(n, 64));
+  // staged Gram kernel: one CTA per SM; streaming kernel (R <= 8): up to 4 per SM
+  const bool stream_gram = R <= 8;
+  const int nb = stream_gram ? (int)std::min<int64_t>(4 * kNumSMs, ceil_div(n, kGsThreads))
+                             : (int)std::min<int64_t>(kNumSMs, ceil_div(n, 64));
   const int64_t rpc = ceil_div(n, nb);
   SPB_ALLOC(ar, double, P1, (size_t)nb * R * R);
   SPB_ALLOC(ar, double, P2, (size_t)nb * R * R);
@@ -721,9 +834,14 @@ static int finish_fused_r(int64_t m, int64_t n, const double* Z, int64_t ldz, co
   double* EtfU = MfV + (size_t)R * k;
   double* EtfV = EtfU + (size_t)k * k;
   GramTail t1{dflag + 1, R1, R1i, dflag, 16.0 * R * 2.220446049250313e-16};
-  SPB_CUDA(launch_pdl((gram_rows_kernel<R>), dim3(nb), dim3(kGrThreads), 0, s, n, Y, nullptr, rpc, P1, t1));
   GramTail t2{nullptr, nullptr, nullptr, nullptr, 0.0};
-  SPB_CUDA(launch_pdl((gram_rows_kernel<R>), dim3(nb), dim3(kGrThreads), 0, s, n, Y, R1i, rpc, P2, t2));
+  if constexpr (R <= 8) {
+    SPB_CUDA(launch_pdl((gram_stream_kernel<R>), dim3(nb), dim3(kGsThreads), 0, s, n, Y, (const double*)nullptr, P1, t1));
+    SPB_CUDA(launch_pdl((gram_stream_kernel<R>), dim3(nb), dim3(kGsThreads), 0, s, n, Y, (const double*)R1i, P2, t2));
+  } else {
+    SPB_CUDA(launch_pdl((gram_rows_kernel<R>), dim3(nb), dim3(kGrThreads), 0, s, n, Y, nullptr, rpc, P1, t1));
+    SPB_CUDA(launch_pdl((gram_rows_kernel<R>), dim3(nb), dim3(kGrThreads), 0, s, n, Y, R1i, rpc, P2, t2));
+  }
   count_launch(2);
   SPB_CHECK_LAUNCH();
   const size_t fc_smem = (sizeof(FcShared) + 15) / 16 * 16 + (size_t)4 * k * R * sizeof(double);
@@ -740,9 +858,20 @@ static int finish_fused_r(int64_t m, int64_t n, const double* Z, int64_t ldz, co
   count_launch();
   SPB_CHECK_LAUNCH();
   const int bu = ceil_div(m, kFrRows), bv = ceil_div(n, kFrRows);
-  const size_t fr_smem = ((size_t)R * k + R * R + (size_t)kFrRows * (R + 1)) * sizeof(double);
-  SPB_CUDA(launch_pdl((finish_rows_kernel<R>), dim3(bu + bv), dim3(kFrThreads), fr_smem, s, k, m, n, bu, Z, ldz, Y, R, R1i, MfU, EtfU, MfV, EtfV,
-                                                             U, V));
+  const size_t fr_smem =
+      ((size_t)2 * R * k + R * R + (size_t)2 * kFrRows * R + (size_t)kFrRows * (R + 1)) * sizeof(double);
+  static int fr_occ = 0;  // persistent: as many CTAs as fit walk the tiles
+  if (fr_occ == 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fr_occ, finish_rows_kernel<R>, kFrThreads, fr_smem) !=
+            cudaSuccess ||
+        fr_occ < 1)
+      fr_occ = 1;
+    cudaGetLastError();
+  }
+  const int fr_grid = (int)std::min<int64_t>((int64_t)bu + bv, (int64_t)fr_occ * kNumSMs);
+  SPB_CUDA(launch_pdl((finish_rows_kernel<R>), dim3(fr_grid), dim3(kFrThreads), fr_smem, s, k, m, n, bu, Z, ldz, Y,
+                      (int64_t)R, (const double*)R1i, (const double*)MfU, (const double*)EtfU, (const double*)MfV,
+                      (const double*)EtfV, U, V));
   count_launch();
   SPB_CHECK_LAUNCH();
   return SP_OK;
