@@ -77,9 +77,17 @@ void* ws_alloc(size_t bytes, cudaStream_t s) {
   void* p = nullptr;
   if (cudaMallocAsync(&p, rb, s) == cudaSuccess) return p;
   cudaGetLastError();
-  // out of memory: hand every cached block back and retry once
+  // out of memory: hand every cached block back (and the pool's reserve to
+  // the driver) and retry once
+  if (std::getenv("SPB_HOST_TRACE")) std::fprintf(stderr, "spb ws_alloc: OOM on %zu bytes, draining\n", rb);
   drain(c);
   cudaDeviceSynchronize();
+  {
+    int d = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&d) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess)
+      cudaMemPoolTrimTo(pool, 0);
+  }
   if (cudaMallocAsync(&p, rb, s) == cudaSuccess) return p;
   cudaGetLastError();
   return nullptr;
