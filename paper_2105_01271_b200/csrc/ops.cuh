@@ -18,6 +18,23 @@ int gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const do
          cudaStream_t s);
 int tsqr(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq,
          double* R, int64_t ldr, cudaStream_t s);
+// TSQR of a <= 32-column block in two phases: the leaf tree (R), then Q
+struct TsqrPlan {
+  struct Level {
+    int64_t rows = 0;
+    int nch = 0, cl = 0;
+    double* V = nullptr;
+    double* T = nullptr;
+    double* Rs = nullptr;
+  };
+  std::vector<Level> lv;
+  double* sgn = nullptr;
+  double* Mg = nullptr;  // single-chunk root: M = T V_top^T diag(sgn)
+  int cols = 0;
+};
+int tsqr_factor(int64_t rows, int cols, const double* X, int64_t ldx, double* R, int64_t ldr, TsqrPlan& plan,
+                Arena& ar, cudaStream_t s);
+int tsqr_form_q(const TsqrPlan& plan, double* Q, int64_t ldq, Arena& ar, cudaStream_t s);
 int tall_gram(int64_t rows, int c, const double* X, int64_t ldx, int d, const double* Y, int64_t ldy,
               double alpha, double beta, double* G, int64_t ldg, cudaStream_t s);
 int tall_gram_partials(int64_t rows, int c, const double* X, int64_t ldx, int d, const double* Y, int64_t ldy,

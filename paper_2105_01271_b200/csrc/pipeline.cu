@@ -242,7 +242,14 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
     for (int itn = 0; itn < max_it; ++itn) {
       // Rayleigh-Ritz: Q^T X = Z^T with Z = X^T Q = P Rz  ->  Q^T X = Rz^T P^T
       SPB_TRY(gemm(1, 0, cols, b, rows, 1.0, X, ldx, Q, b, 0.0, Z, b, s));
-      SPB_TRY(tsqr(cols, b, Z, b, P, b, Rz, b, s));
+      // Z = P Rz: only Rz is needed unless V is wanted or another step
+      // follows (then P is formed from the kept factors, below)
+      TsqrPlan zplan;
+      const bool lazy_p = b <= 32 && !want_v;
+      if (lazy_p)
+        SPB_TRY(tsqr_factor(cols, b, Z, b, Rz, b, zplan, it, s));
+      else
+        SPB_TRY(tsqr(cols, b, Z, b, P, b, Rz, b, s));
       SPB_TRY(jacobi_svd_tr(b, Rz, b, /*trans=*/true, Us, b, Sg, want_v ? Vs : nullptr, b, s));
       // publish the Ritz values, then -- while the host waits for them --
       // form the final products as if this step converged (it usually does;
@@ -293,6 +300,7 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
       prev = hs;
       kept_prev = kept;
       // one more subspace iteration: Y = X P, Q = orth(Y)
+      if (lazy_p) SPB_TRY(tsqr_form_q(zplan, P, b, it, s));
       SPB_TRY(gemm(0, 0, rows, b, cols, 1.0, X, ldx, P, b, 0.0, Y, b, s));
       SPB_TRY(tsqr(rows, b, Y, b, Q, b, Rt, b, s));
     }

@@ -26,6 +26,7 @@
 #include "async.cuh"
 #include "common.cuh"
 #include "launch_count.cuh"
+#include "ops.cuh"
 
 #include <cooperative_groups.h>
 #include <vector>
@@ -537,24 +538,24 @@ static int max_cluster() {
   return g_max_cluster;
 }
 
-static int tsqr32(int64_t rows, int cols, const double* X, int64_t ldx, double* Q, int64_t ldq, double* R,
-                  int64_t ldr, cudaStream_t s) {
-  Arena ar(s);
-  struct Level {
-    int64_t rows;
-    int nch, cl;
-    double* V;
-    double* T;
-    double* Rs;
-  };
-  std::vector<Level> lv;
+// Factor phase: the leaf tree (R written to R); the Q phase (tsqr_form_q)
+// is separate so callers that only need R (the Rayleigh-Ritz core of a
+// converged subspace step) skip it.  Workspaces live in `ar`.
+int tsqr_factor(int64_t rows, int cols, const double* X, int64_t ldx, double* R, int64_t ldr, TsqrPlan& plan,
+                Arena& ar, cudaStream_t s) {
+  plan = TsqrPlan();
+  plan.cols = cols;
   const double* in = X;
   int64_t in_ld = ldx;
   int64_t r = rows;
-  SPB_ALLOC(ar, double, sgn, kQB);
+  plan.sgn = ar.alloc<double>(kQB);
+  if (!plan.sgn) {
+    set_error("tsqr workspace allocation failed");
+    return SP_ECUDA;
+  }
   const int mc = max_cluster();
   while (true) {
-    Level L;
+    TsqrPlan::Level L;
     L.rows = r;
     // clusters only while all chunks fit in one wave: past ~148 CTAs the
     // per-step cluster exchange costs more than the extra tree level it saves
@@ -569,27 +570,41 @@ static int tsqr32(int64_t rows, int cols, const double* X, int64_t ldx, double* 
       return SP_ECUDA;
     }
     const bool root = L.nch == 1;
-    if (root && lv.empty()) {
+    if (root && plan.lv.empty()) {
       // single chunk: the root leaf also forms M; Q is one small product per row
-      SPB_ALLOC(ar, double, Mg, (size_t)kQB * kQB);
-      SPB_TRY(launch_leaf(1, L.cl, in, r, cols, in_ld, L.V, L.T, L.Rs, R, ldr, sgn, s, Mg));
-      SPB_CUDA(launch_pdl((tsqr_q_kernel), dim3(ceil_div(r, 64)), dim3(kQThreads), 0, s, (const double*)L.V,
-                          (const double*)Mg, (const double*)sgn, r, cols, Q, ldq));
-      count_launch();
-      SPB_CHECK_LAUNCH();
+      plan.Mg = ar.alloc<double>((size_t)kQB * kQB);
+      if (!plan.Mg) {
+        set_error("tsqr workspace allocation failed");
+        return SP_ECUDA;
+      }
+      SPB_TRY(launch_leaf(1, L.cl, in, r, cols, in_ld, L.V, L.T, L.Rs, R, ldr, plan.sgn, s, plan.Mg));
+      plan.lv.push_back(L);
       return SP_OK;
     }
     SPB_TRY(launch_leaf(L.nch, L.cl, in, r, cols, in_ld, L.V, L.T, L.Rs, root ? R : nullptr, ldr,
-                        root ? sgn : nullptr, s));
-    lv.push_back(L);
+                        root ? plan.sgn : nullptr, s));
+    plan.lv.push_back(L);
     if (root) break;
     in = L.Rs;
     in_ld = kQB;
     r = (int64_t)L.nch * cols;
   }
+  return SP_OK;
+}
+
+int tsqr_form_q(const TsqrPlan& plan, double* Q, int64_t ldq, Arena& ar, cudaStream_t s) {
+  const int cols = plan.cols;
+  if (plan.Mg) {
+    const TsqrPlan::Level& L = plan.lv[0];
+    SPB_CUDA(launch_pdl((tsqr_q_kernel), dim3(ceil_div(L.rows, 64)), dim3(kQThreads), 0, s, (const double*)L.V,
+                        (const double*)plan.Mg, (const double*)plan.sgn, L.rows, cols, Q, ldq));
+    count_launch();
+    SPB_CHECK_LAUNCH();
+    return SP_OK;
+  }
   const double* bin = nullptr;
-  for (int l = (int)lv.size() - 1; l >= 0; --l) {
-    const Level& L = lv[l];
+  for (int l = (int)plan.lv.size() - 1; l >= 0; --l) {
+    const TsqrPlan::Level& L = plan.lv[l];
     double* out;
     int64_t ldo;
     if (l == 0) {
@@ -604,13 +619,22 @@ static int tsqr32(int64_t rows, int cols, const double* X, int64_t ldx, double* 
       ldo = kQB;
     }
     const int chunk_rows = L.cl * kQCH;
-    SPB_CUDA(launch_pdl((tsqr_apply_kernel), dim3(L.nch * (chunk_rows / kApRows)), dim3(kQThreads), 0, s, L.V, L.T, L.rows, cols, chunk_rows, bin,
-                                                                          sgn, out, ldo));
+    SPB_CUDA(launch_pdl((tsqr_apply_kernel), dim3(L.nch * (chunk_rows / kApRows)), dim3(kQThreads), 0, s,
+                        (const double*)L.V, (const double*)L.T, L.rows, cols, chunk_rows, bin,
+                        (const double*)plan.sgn, out, ldo));
     count_launch();
     SPB_CHECK_LAUNCH();
     bin = out;
   }
   return SP_OK;
+}
+
+static int tsqr32(int64_t rows, int cols, const double* X, int64_t ldx, double* Q, int64_t ldq, double* R,
+                  int64_t ldr, cudaStream_t s) {
+  Arena ar(s);
+  TsqrPlan plan;
+  SPB_TRY(tsqr_factor(rows, cols, X, ldx, R, ldr, plan, ar, s));
+  return tsqr_form_q(plan, Q, ldq, ar, s);
 }
 
 __global__ void copy_block(int64_t rows, int64_t cols, const double* src, int64_t lds, double* dst,
