@@ -280,13 +280,19 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
       // (sigma_{b+1}/sigma_kept)^2 when the spectrum has fallen to the
       // rounding floor inside the block (oversampling 8): accept it.
       if (itn == 0 && kept > 0 && b - 8 > kept && hs[b - 8] <= 1e-8 * hs[kept - 1]) conv = true;
-      // A priori: after itn + 1 Rayleigh-Ritz steps the kept Ritz values are
-      // accurate to ~(sigma_{b-7} / sigma_kept)^(2 itn + 2) (oversampling 8;
-      // hs[b-8] >= sigma_{b+1} makes the estimate conservative).  E.g. an
-      // FP32-stored A floors the sketch spectrum at ~1e-7 sigma_1, so the
-      // ratio is ~1e-4 and two steps reach 1e-16 without a third to confirm.
+      // A priori: after itn + 1 Rayleigh-Ritz steps the kept subspace is within
+      // an angle ~rho^(2 itn) of the exact one, rho = sigma_{b-7} / sigma_kept
+      // (oversampling 8; hs[b-8] >= sigma_{b+1} makes the estimate
+      // conservative), and the kept Ritz values within its square.  Stop once
+      // rho^(2 itn + 2) <= 1e-12: an angle below ~1e-11, whose effect on the
+      // singular values of P_r A is second order (~1e-22 sigma_1) and far
+      // inside the 1e-8 principal-angle gate (measured on the cfg3 sketch,
+      // whose noise bulk gives rho = 0.18: 7e-12 when the test first passes;
+      // the earlier 1e-16 bound ran three more steps for nothing).  An
+      // FP32-stored A floors the sketch spectrum at ~1e-7 sigma_1: rho ~1e-4
+      // and the second step passes.
       if (itn >= 1 && kept == kept_prev && kept > 0 && b - 8 > kept &&
-          std::pow(hs[b - 8] / hs[kept - 1], 2.0 * itn + 2.0) <= 1e-16)
+          std::pow(hs[b - 8] / hs[kept - 1], 2.0 * itn + 2.0) <= 1e-12)
         conv = true;
       if (!conv && itn >= 1 && kept == kept_prev) {
         conv = true;
@@ -299,8 +305,15 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
       if (conv) break;
       prev = hs;
       kept_prev = kept;
-      // one more subspace iteration: Y = X P, Q = orth(Y)
-      if (lazy_p) SPB_TRY(tsqr_form_q(zplan, P, b, it, s));
+      // one more subspace iteration, started from the Ritz vectors:
+      // Y = X (Z Us) = X P Vs Sigma (Z = P Rz, Rz^T = Us Sigma Vs^T; the column
+      // scaling leaves the span and the column-wise backward-stable Householder
+      // QR unchanged), Q = orth(Y).  Q then arrives nearly aligned with the
+      // singular vectors, so the next core Rz is nearly diagonal and its Jacobi
+      // SVD takes a few sweeps instead of ~8 (a noise bulk in the block is
+      // nearly invariant under X X^T, so it stays nearly diagonal too).  P is
+      // scratch here: the next step recomputes it.
+      SPB_TRY(gemm(0, 0, cols, b, b, 1.0, Z, b, Us, b, 0.0, P, b, s));
       SPB_TRY(gemm(0, 0, rows, b, cols, 1.0, X, ldx, P, b, 0.0, Y, b, s));
       SPB_TRY(tsqr(rows, b, Y, b, Q, b, Rt, b, s));
     }
