@@ -218,6 +218,14 @@ int sp_row_id(int64_t m, int64_t cols, const double* M, int64_t ldm, int32_t k, 
 int sp_sketch_basis(const double* X, int64_t rows, int64_t cols, int64_t ldx, double power, int32_t r_max,
                     double* U, int64_t ldu, double* S, int64_t* info, void* stream);
 
+/* R factor of a tall block X (rows x b, b <= 32, rows >= b) with
+ * R^T R = X^T X, from the Gram accumulated and Cholesky-factored in
+ * double-double arithmetic (ddgram.cu); pivots below 1e-29 trace(X^T X) give
+ * zero rows.  Replaces thin_qr's R (src/kernels.py:62-84) for the
+ * Rayleigh-Ritz core of the sketch-side subspace iteration, which needs R
+ * only.  R is b x b row-major (ld ldr), zero below the diagonal.  Asynchronous. */
+int sp_gram_chol_dd(int64_t rows, int32_t b, const double* X, int64_t ldx, double* R, int64_t ldr, void* stream);
+
 /* Range-finder test block of the sketch-side subspace iteration (srht.cu):
  * Y (rows x b, ld ldy) = X D H S -- random signs, Walsh-Hadamard transform of
  * the zero-padded width, b stratified column samples (the structured

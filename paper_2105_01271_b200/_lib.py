@@ -60,6 +60,7 @@ SIGNATURES = {
     "sp_row_id": [_I64, _I64, _P, _I64, _I32, _P, _P, _P, _P],
     "sp_sketch_basis": [_P, _I64, _I64, _I64, _D, _I32, _P, _I64, _P, _P, _P],
     "sp_householder_complete": [_I64, _I32, _I32, _P, _I64, _P, _P],
+    "sp_gram_chol_dd": [_I64, _I32, _P, _I64, _P, _I64, _P],
     "sp_srht_sketch": [_I64, _I64, _P, _I64, _I32, ctypes.c_uint64, _P, _I64, _P, _P],
     "sp_srht_gather": [_P, _I32, _I64, _I64, _P, _I64, _P, _I64, _I32, ctypes.c_uint64, _P, _I64, _P, _P],
     "sp_single_pass_svd": [_P, _I32, _I64, _I64, _I64, _P, _P, _I32, _I64, _P, _I64, _I32, _P,

@@ -177,6 +177,11 @@ int sp_srht_sketch(int64_t rows, int64_t cols, const double* X, int64_t ldx, int
   return srht_sketch(rows, cols, X, ldx, b, seed, Y, ldy, flag, ST(stream));
 }
 
+int sp_gram_chol_dd(int64_t rows, int32_t b, const double* X, int64_t ldx, double* R, int64_t ldr, void* stream) {
+  Arena ar(ST(stream));
+  return gram_chol_dd(rows, b, X, ldx, R, ldr, ar, ST(stream));
+}
+
 int sp_srht_gather(const void* A, int32_t a_dtype, int64_t rows, int64_t lda, const int64_t* gidx, int64_t cols,
                    double* X, int64_t ldx, int32_t b, uint64_t seed, double* Y, int64_t ldy, int32_t* flag,
                    void* stream) {

@@ -35,6 +35,10 @@ struct TsqrPlan {
 int tsqr_factor(int64_t rows, int cols, const double* X, int64_t ldx, double* R, int64_t ldr, TsqrPlan& plan,
                 Arena& ar, cudaStream_t s);
 int tsqr_form_q(const TsqrPlan& plan, double* Q, int64_t ldq, Arena& ar, cudaStream_t s);
+// R (b x b upper) with R^T R = X^T X from a double-double Gram (b <= 32)
+bool gram_chol_dd_ok(int64_t rows, int b);
+int gram_chol_dd(int64_t rows, int b, const double* X, int64_t ldx, double* R, int64_t ldr, Arena& ar,
+                 cudaStream_t s);
 int tall_gram(int64_t rows, int c, const double* X, int64_t ldx, int d, const double* Y, int64_t ldy,
               double alpha, double beta, double* G, int64_t ldg, cudaStream_t s);
 int tall_gram_partials(int64_t rows, int c, const double* X, int64_t ldx, int d, const double* Y, int64_t ldy,

@@ -244,10 +244,11 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
       SPB_TRY(gemm(1, 0, cols, b, rows, 1.0, X, ldx, Q, b, 0.0, Z, b, s));
       // Z = P Rz: only Rz is needed unless V is wanted or another step
       // follows (then P is formed from the kept factors, below)
-      TsqrPlan zplan;
-      const bool lazy_p = b <= 32 && !want_v;
+      // (R alone: Cholesky of the double-double Gram, ddgram.cu -- one launch
+      // instead of the 32-step Householder factor)
+      const bool lazy_p = b <= 32 && !want_v && gram_chol_dd_ok(cols, b);
       if (lazy_p)
-        SPB_TRY(tsqr_factor(cols, b, Z, b, Rz, b, zplan, it, s));
+        SPB_TRY(gram_chol_dd(cols, b, Z, b, Rz, b, it, s));
       else
         SPB_TRY(tsqr(cols, b, Z, b, P, b, Rz, b, s));
       SPB_TRY(jacobi_svd_tr(b, Rz, b, /*trans=*/true, Us, b, Sg, want_v ? Vs : nullptr, b, s));

@@ -416,3 +416,56 @@ def test_srht_gather_is_exact_and_matches_two_step(cuda, dtype):
     assert np.array_equal(xg.view(np.int64), want.view(np.int64))  # bit-exact copies, -0.0 kept
     y2, f2 = _srht(cuda, want, 32, seed=99)
     assert np.array_equal(Y.cpu().numpy(), y2) and int(flag.item()) == 0 and f2 == 0
+
+
+# ------------------------------------------------- double-double Gram R ----
+def _gram_chol_dd(cuda, x):
+    rows, b = x.shape
+    X = _dev(x, cuda)
+    R = cuda.full((b, b), float("nan"), dtype=cuda.float64, device="cuda")
+    _lib.call("sp_gram_chol_dd", rows, b, X.data_ptr(), b, R.data_ptr(), b, _stream(cuda))
+    return R.cpu().numpy()
+
+
+@pytest.mark.parametrize("rows,b,decay", [(4096, 32, 0.3), (2000, 32, 0.1), (700, 20, 0.5), (262144, 32, 0.35),
+                                          (64, 32, 0.6), (33, 7, 0.9)])
+def test_gram_chol_dd_matches_householder_r(cuda, rows, b, decay):
+    # graded singular values down to ~1e-17 of the largest (a numerically
+    # rank-deficient subspace block): R must be upper triangular with a
+    # non-negative diagonal, R^T R = X^T X to dd-rounded FP64, and the
+    # singular values of R must match the Householder R's (LAPACK) to ~1e-15
+    # of the largest; the top singular subspace of R^T must match too.
+    rng = philox(rows + 31 * b)
+    u, _ = np.linalg.qr(rng.standard_normal((rows, b)))
+    v, _ = np.linalg.qr(rng.standard_normal((b, b)))
+    sv = np.maximum(decay ** np.arange(b), 1e-17)
+    x = (u * sv) @ v.T
+    r = _gram_chol_dd(cuda, x)
+    assert np.all(np.isfinite(r))
+    assert np.all(np.tril(r, -1) == 0.0)
+    assert np.all(np.diag(r) >= 0.0)
+    _, rh = np.linalg.qr(x)
+    s_dd = np.linalg.svd(r, compute_uv=False)
+    s_hh = np.linalg.svd(rh, compute_uv=False)
+    np.testing.assert_allclose(s_dd, s_hh, rtol=0, atol=1e-14 * s_hh[0])
+    np.testing.assert_allclose(s_dd, sv, rtol=0, atol=1e-14 * sv[0])
+    # kept directions (singular values above 1e-6 of the largest): U of R^T
+    kk = int(np.sum(sv > 1e-6 * sv[0]))
+    ud = np.linalg.svd(r.T)[0][:, :kk]
+    uh = np.linalg.svd(rh.T)[0][:, :kk]
+    cos = np.linalg.svd(ud.T @ uh, compute_uv=False)
+    assert np.min(cos) > 1 - 1e-12
+    # columns of R^T R reproduce X^T X on the retained part
+    g = x.T @ x
+    np.testing.assert_allclose(r.T @ r, g, rtol=0, atol=1e-14 * np.trace(g))
+
+
+def test_gram_chol_dd_zero_and_exact_rank(cuda):
+    # all-zero block -> R = 0; an exactly rank-2 block -> two nonzero rows
+    r = _gram_chol_dd(cuda, np.zeros((500, 8)))
+    assert np.all(r == 0.0)
+    rng = philox(5)
+    x = rng.standard_normal((600, 2)) @ rng.standard_normal((2, 8))
+    r = _gram_chol_dd(cuda, x)
+    assert np.count_nonzero(np.abs(np.diag(r)) > 1e-12 * np.abs(r).max()) == 2
+    np.testing.assert_allclose(r.T @ r, x.T @ x, rtol=0, atol=1e-13 * np.trace(x.T @ x))
