@@ -745,10 +745,14 @@ finish_rows_kernel(int k, int64_t m, int64_t n, int bu, const double* __restrict
     mfv[e] = MfV[e];
   }
   for (int e = t; e < R * R; e += kFrThreads) ri[e] = R1i[e];
-  // column mapping: kpad = k rounded up to a warp multiple (<= 256), ngrp
-  // thread groups of kpad threads each take every ngrp-th row of a tile
-  const int kpad = (k + 31) / 32 * 32 < kFrThreads ? (k + 31) / 32 * 32 : kFrThreads;
-  const int ngrp = kFrThreads / kpad, grp = t / kpad, cl = t - grp * kpad;
+  // column mapping: groups of kh = ceil(k / 2) threads, each thread two
+  // adjacent columns (one 16-byte store per row when k is even and the
+  // outputs are 16-byte aligned); the ngrp groups take every ngrp-th row of a
+  // tile.  Groups are not warp-rounded: a warp's stores then cover the end of
+  // one row and the start of the next, still two contiguous segments.
+  const int kh = (k + 1) / 2;
+  const int ngrp = kFrThreads / kh, grp = t / kh, cl = t - grp * kh;
+  const bool vec = (k % 2 == 0) && ((reinterpret_cast<uintptr_t>(U) | reinterpret_cast<uintptr_t>(V)) & 15) == 0;
   for (int it = 0; tile < ntiles; tile += gridDim.x, ++it) {
     const bool isv = tile >= bu;
     const int64_t rows = isv ? n : m;
@@ -786,21 +790,36 @@ finish_rows_kernel(int k, int64_t m, int64_t n, int bu, const double* __restrict
     }
     __syncthreads();
     const double* mf = isv ? mfv : mfu;
-    // thread (group, column): the column's Mf entries in registers, the rows
-    // of the tile split over the groups; a warp stores 32 consecutive columns
-    for (int c0 = 0; c0 < k; c0 += kpad) {
-      const int c = c0 + cl;
-      double mcol[R];
+    // thread (group, column pair): the columns' Mf entries in registers, the
+    // rows of the tile split over the groups
+    if (grp < ngrp) {
+      const int c = 2 * cl;
+      const bool has1 = c + 1 < k;
+      double m0[R], m1[R];
 #pragma unroll
-      for (int p = 0; p < R; ++p) mcol[p] = c < k ? mf[p * k + c] : 0.0;
-      if (c < k) {
-        for (int rl = grp; rl < nr; rl += ngrp) {
-          double o = 0.0;
+      for (int p = 0; p < R; ++p) {
+        m0[p] = mf[p * k + c];
+        m1[p] = has1 ? mf[p * k + c + 1] : 0.0;
+      }
+      for (int rl = grp; rl < nr; rl += ngrp) {
+        double o0 = 0.0, o1 = 0.0;
 #pragma unroll
-          for (int p = 0; p < R; ++p) o = fma(qs[rl * (R + 1) + p], mcol[p], o);
-          const int64_t row = base + rl;
-          if (row < k) o += Et[row * k + c];
-          O[row * k + c] = o;
+        for (int p = 0; p < R; ++p) {
+          const double q = qs[rl * (R + 1) + p];
+          o0 = fma(q, m0[p], o0);
+          o1 = fma(q, m1[p], o1);
+        }
+        const int64_t row = base + rl;
+        if (row < k) {
+          o0 += Et[row * k + c];
+          if (has1) o1 += Et[row * k + c + 1];
+        }
+        double* dst = O + row * k + c;
+        if (vec) {
+          *reinterpret_cast<double2*>(dst) = make_double2(o0, o1);
+        } else {
+          dst[0] = o0;
+          if (has1) dst[1] = o1;
         }
       }
     }
