@@ -107,9 +107,12 @@ __device__ __forceinline__ void srht_row(double (&v)[16], uint64_t sg, int b, ui
 // GATHER: the rows of X are gathered on the fly from A (X[row][j] =
 // A[row][gidx[j]], exact copies, written to X as well): the coarse-column
 // block C = A(:, I) and its test block Y come out of one pass over A (K1 fused
-// with the range finder's first product).  A gathering CTA takes RPC rows so
-// that RPC x 16 loads per thread are in flight behind one read of the index
-// table.  Both modes give bit-identical Y.
+// with the range finder's first product).  RPC rows per CTA (the kernel is
+// templated on it); one row per CTA is used: 2 rows held 75 -> 103
+// registers, i.e. 3 -> 2 resident CTAs per SM, and the extra CTAs overlap one
+// row's gather loads with another's transform better than the wider batch
+// (measured: cfg2 rows 67.9 -> 60.3 us, cfg4-width rows 458 -> 386 us per
+// 2000 rows).  Both modes give bit-identical Y.
 template <int LT, bool GATHER, int RPC, typename TA>
 __global__ void __launch_bounds__(1 << LT)
 srht_kernel(int64_t rows, int64_t cols, const double* __restrict__ X, int64_t ldx, int b, uint64_t seed,
@@ -186,7 +189,7 @@ template <bool GATHER, typename TA>
 static int srht_launch(int64_t rows, int64_t cols, const double* X, int64_t ldx, int b, uint64_t seed, double* Y,
                        int64_t ldy, int* flag, const TA* A, int64_t lda, const int64_t* gidx, double* Xout,
                        cudaStream_t s) {
-  constexpr int RPC = GATHER ? 2 : 1;
+  constexpr int RPC = 1;
   const int lt = srht_lt(cols);
   const int64_t n2 = (int64_t)16 << lt;
   const size_t smem = (size_t)(n2 + n2 / 16) * sizeof(double);
