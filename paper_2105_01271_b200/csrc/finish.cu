@@ -113,18 +113,23 @@ __device__ void fc_jacobi_warp(int r, double (&x)[RPW], double (&v)[RPW], JacSme
         continue;
       const double d = aq - ap, h = 2.0 * g;
       const double ad = fabs(d), ah = fabs(h);
-      double t, cs;
+      double cs, sn;
       if (ad < 1e140 && ah < 1e140 && (ad > 1e-140 || ah > 1e-140)) {
-        // fast path: one MUFU rsqrt + Newton for hypot, rcp for t, rsqrt for cos
+        // fast path, two dependent MUFU rsqrt (+ Newton) stages: rh =
+        // 1 / hypot(d, h) gives cos 2theta = |d| rh and sin 2theta = h rh
+        // (|theta| <= pi / 4); cs = sqrt((1 + cos 2theta) / 2) and
+        // sn = sin 2theta / (2 cs) share one rsqrt of u in [1/2, 1]
         const double s2 = fma(d, d, h * h);
-        const double hyp = s2 * fast_rsqrt(s2);
-        t = copysign(1.0, d) * h * fast_rcp(ad + hyp);
-        cs = fast_rsqrt(fma(t, t, 1.0));
+        const double rh = fast_rsqrt(s2);
+        const double u = fma(0.5 * ad, rh, 0.5);
+        const double w = fast_rsqrt(u);
+        cs = u * w;
+        sn = (copysign(0.5, d) * h) * (rh * w);
       } else {
-        t = copysign(1.0, d) * h / (ad + hypot(d, h));
+        const double t = copysign(1.0, d) * h / (ad + hypot(d, h));
         cs = rsqrt(fma(t, t, 1.0));
+        sn = cs * t;
       }
-      const double sn = cs * t;
       const double so = low ? -sn : sn;
 #pragma unroll
       for (int k = 0; k < RPW; ++k) {
