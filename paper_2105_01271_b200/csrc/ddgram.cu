@@ -21,8 +21,9 @@
 // One launch: ~sqrt(rows) CTAs (<= 148) each accumulate a partial Gram of a
 // contiguous row range over the 528 upper-triangle entries (rows staged 64 at
 // a time through shared memory; error-free products by FMA, Neumaier-style
-// compensated sums, two entries per thread); the last CTA (atomic ticket)
-// sums the partials in CTA order in dd -- bitwise reproducible -- and factors
+// compensated sums, two entries per thread); the partials are summed in dd
+// in two fixed-order levels (the last CTA of each group of 8 by an atomic
+// ticket, then the last group) -- bitwise reproducible -- and the last CTA factors
 // the dd Gram right-looking in shared memory (pivot by an FP64 rsqrt with one
 // dd Newton correction; the trailing update S_ik -= S_ji S_jk / d_j).  It
 // replaces the 32-step Householder TSQR factor (tsqr.cu), whose per-column
@@ -88,6 +89,8 @@ constexpr int kDgEnt = kDgB * (kDgB + 1) / 2;   // upper-triangle entries (528)
 constexpr int kDgThreads = 288;                  // 2 entries per thread (9 warps)
 constexpr int kDgTile = 64;                      // rows staged per step
 constexpr double kDgFloor = 1e-29;               // pivot floor relative to trace(G)
+constexpr int kDgGroup = 8;                      // partials per first-level group
+constexpr int kDgTickets = 32;                   // 1 + max groups (148 / 8 -> 19)
 
 // upper-triangle entry e -> (i, j), i <= j, row-major over the triangle
 __device__ __forceinline__ void dg_entry(int e, int& i, int& j) {
@@ -115,13 +118,15 @@ __device__ __forceinline__ dd dd_rsqrt(dd d) {
 
 __global__ void __launch_bounds__(kDgThreads)
 ddgram_chol_kernel(int64_t rows, int b, const double* __restrict__ X, int64_t ldx, int64_t rows_per_cta,
-                   double2* __restrict__ partial, int* __restrict__ ticket, double* __restrict__ R, int64_t ldr) {
+                   double2* __restrict__ partial, double2* __restrict__ gpart, int* __restrict__ ticket,
+                   double* __restrict__ R, int64_t ldr) {
   SPB_TDECL;
   SPB_PDL_ENTRY();
   SPB_TMARK(0);
   __shared__ __align__(16) double xs[kDgTile][kDgB + 1];
   __shared__ dd S[kDgB][kDgB + 1];
-  __shared__ dd piv[2][2];  // {1/r_jj, 1/d_j}, double-buffered over steps
+  __shared__ double piv_r[2];  // 1 / r_jj, double-buffered over steps
+  __shared__ dd piv_d[2];      // 1 / d_j
   __shared__ int last;
   const int t = threadIdx.x;
   int ei[2], ej[2];
@@ -169,39 +174,56 @@ ddgram_chol_kernel(int64_t rows, int b, const double* __restrict__ X, int64_t ld
       partial[(int64_t)blockIdx.x * kDgEnt + 2 * t + u] = make_double2(a.hi, a.lo);
     }
   }
-  // ---- last CTA: fixed-order sum of the partials, dd Cholesky
+  // ---- two-level fixed-order reduction: the last CTA of each group of
+  // kDgGroup CTAs sums the group's partials (in CTA order), the last group
+  // sums the group totals (in group order) and factors
   SPB_TMARK(2);
+  const int nb = (int)gridDim.x, ngrp = (nb + kDgGroup - 1) / kDgGroup;
+  const int grp = (int)blockIdx.x / kDgGroup, g0 = grp * kDgGroup;
+  const int gsz = nb - g0 < kDgGroup ? nb - g0 : kDgGroup;
   __threadfence();
   __syncthreads();
-  if (t == 0) last = atomicAdd(ticket, 1) == (int)gridDim.x - 1;
+  if (t == 0) last = atomicAdd(ticket + 1 + grp, 1) == gsz - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  auto sum_rows = [&](const double2* src, int first, int count, dd (&g)[2]) {
+    double2 v[kDgGroup][2];
+#pragma unroll
+    for (int q = 0; q < kDgGroup; ++q)
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        v[q][u] = q < count ? __ldcg(src + (int64_t)(first + q) * kDgEnt + 2 * t + u) : make_double2(0.0, 0.0);
+    g[0] = g[1] = {0.0, 0.0};
+#pragma unroll
+    for (int q = 0; q < kDgGroup; ++q)
+      if (q < count)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) g[u] = dd_add(g[u], {v[q][u].x, v[q][u].y});
+  };
+  if (2 * t < kDgEnt) {
+    dd g[2];
+    sum_rows(partial, g0, gsz, g);
+#pragma unroll
+    for (int u = 0; u < 2; ++u) gpart[(int64_t)grp * kDgEnt + 2 * t + u] = make_double2(g[u].hi, g[u].lo);
+  }
+  __threadfence();
+  __syncthreads();
+  if (t == 0) {
+    ticket[1 + grp] = 0;
+    last = atomicAdd(ticket, 1) == ngrp - 1;
+  }
   __syncthreads();
   if (!last) return;
   __threadfence();
   SPB_TMARK(3);
   if (2 * t < kDgEnt) {
     dd g[2] = {{0.0, 0.0}, {0.0, 0.0}};
-    const int nb = (int)gridDim.x;
-    constexpr int G = 4;
-    double2 cur[G][2], nxt[G][2];
-    auto load = [&](double2 (&v)[G][2], int c) {
+    for (int c0 = 0; c0 < ngrp; c0 += kDgGroup) {
+      dd h[2];
+      sum_rows(gpart, c0, ngrp - c0 < kDgGroup ? ngrp - c0 : kDgGroup, h);
 #pragma unroll
-      for (int q = 0; q < G; ++q)
-#pragma unroll
-        for (int u = 0; u < 2; ++u)
-          v[q][u] = c + q < nb ? __ldcg(partial + (int64_t)(c + q) * kDgEnt + 2 * t + u) : make_double2(0.0, 0.0);
-    };
-    load(cur, 0);
-    for (int c = 0; c < nb; c += G) {
-      if (c + G < nb) load(nxt, c + G);
-#pragma unroll
-      for (int q = 0; q < G; ++q)
-        if (c + q < nb)
-#pragma unroll
-          for (int u = 0; u < 2; ++u) g[u] = dd_add(g[u], {cur[q][u].x, cur[q][u].y});
-#pragma unroll
-      for (int q = 0; q < G; ++q)
-#pragma unroll
-        for (int u = 0; u < 2; ++u) cur[q][u] = nxt[q][u];
+      for (int u = 0; u < 2; ++u) g[u] = dd_add(g[u], h[u]);
     }
 #pragma unroll
     for (int u = 0; u < 2; ++u) S[ei[u]][ej[u]] = g[u];
@@ -212,42 +234,49 @@ ddgram_chol_kernel(int64_t rows, int b, const double* __restrict__ X, int64_t ld
   for (int j = 0; j < b; ++j) tr += S[j][j].hi;
   const double floor_abs = kDgFloor * tr;
   // right-looking Cholesky of the upper triangle; thread (gi, 4 columns).
-  // The pivot of step j + 1 is formed by the owner of S[j+1][j+1] right after
-  // its own update (double-buffered), so a step costs one barrier.
+  // The pivot of step j + 1 is formed by the owner of S[j+1][j+1] from its
+  // freshly updated register value (double-buffered), so a step costs one
+  // barrier.  Pivot data: 1 / r_jj in FP64 (it only scales R's row j, which
+  // is rounded to FP64 anyway) and 1 / d_j in dd (the trailing update).
   const int gi = t >> 3, j0 = (t & 7) * 4;
   const bool chol_thread = t < 256;
-  auto pivot = [&](dd d, dd* out) {
+  auto pivot = [&](dd d, int buf) {
     if (d.hi > floor_abs && d.hi < 1e300) {
-      const dd inv = dd_rsqrt(d);
-      out[0] = inv;
-      out[1] = dd_mul(inv, inv);
+      const bool fr = fast_range(d.hi);
+      piv_r[buf] = fr ? fast_rsqrt(d.hi) : 1.0 / sqrt(d.hi);
+      const double q1 = fr ? fast_rcp(d.hi) : 1.0 / d.hi;
+      const double p = d.hi * q1;
+      const double e = fma(d.hi, q1, -p);
+      const double r = fma(-d.lo, q1, (1.0 - p) - e);  // 1 - d q1 (1 - p exact)
+      piv_d[buf] = dd_quick(q1, r * q1);
     } else {
-      out[0] = {0.0, 0.0};
-      out[1] = {0.0, 0.0};
+      piv_r[buf] = 0.0;
+      piv_d[buf] = {0.0, 0.0};
     }
   };
-  if (t == 0) pivot(S[0][0], piv[0]);
+  if (t == 0) pivot(S[0][0], 0);
   __syncthreads();
   for (int j = 0; j < b; ++j) {
-    const dd inv = piv[j & 1][0], inv2 = piv[j & 1][1];
+    const double rinv = piv_r[j & 1];
+    const dd inv2 = piv_d[j & 1];
     // R row j: R_jk = S_jk / r_jj (k >= j), zeros below the diagonal
     if (chol_thread && gi == j) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int k = j0 + u;
-        if (k < b) R[(int64_t)j * ldr + k] = k >= j ? dd_mul(S[j][k], inv).hi : 0.0;
+        if (k < b) R[(int64_t)j * ldr + k] = k >= j ? S[j][k].hi * rinv : 0.0;
       }
     }
     // trailing update S_ik -= S_ji S_jk / d_j (i <= k).  Step j reads row j
     // only and writes rows > j: no barrier between the two.
     if (chol_thread && gi > j && gi < b) {
-      if (inv2.hi != 0.0) {
-        dd rowj[4], mine[4];
+      dd rowj[4], mine[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          rowj[u] = S[j][j0 + u];
-          mine[u] = S[gi][j0 + u];
-        }
+      for (int u = 0; u < 4; ++u) {
+        rowj[u] = S[j][j0 + u];
+        mine[u] = S[gi][j0 + u];
+      }
+      if (inv2.hi != 0.0) {
         const dd f = dd_mul(S[j][gi], inv2);
 #pragma unroll
         for (int u = 0; u < 4; ++u) mine[u] = dd_add(mine[u], dd_neg(dd_mul(f, rowj[u])));
@@ -257,7 +286,13 @@ ddgram_chol_kernel(int64_t rows, int b, const double* __restrict__ X, int64_t ld
           if (k >= gi && k < b) S[gi][k] = mine[u];
         }
       }
-      if (gi == j + 1 && j0 <= gi && gi < j0 + 4) pivot(S[gi][gi], piv[(j + 1) & 1]);
+      if (gi == j + 1 && j0 <= gi && gi < j0 + 4) {
+        dd dnext = mine[0];
+#pragma unroll
+        for (int u = 1; u < 4; ++u)
+          if (j0 + u == gi) dnext = mine[u];
+        pivot(dnext, (j + 1) & 1);
+      }
     }
     __syncthreads();
   }
@@ -270,7 +305,8 @@ ddgram_chol_kernel(int64_t rows, int b, const double* __restrict__ X, int64_t ld
   }
 }
 
-// Per-(device, stream) ticket word: zeroed once, reset by the kernel's last CTA.
+// Per-(device, stream) ticket words {final, group 0..}: zeroed once, each
+// reset by the CTA that consumes it.
 static int dd_ticket(cudaStream_t s, int** out) {
   static std::mutex mu;
   static std::map<std::pair<int, cudaStream_t>, int*> words;
@@ -280,8 +316,8 @@ static int dd_ticket(cudaStream_t s, int** out) {
   auto it = words.find({dev, s});
   if (it == words.end()) {
     int* p = nullptr;
-    SPB_CUDA(cudaMalloc(&p, sizeof(int)));
-    SPB_CUDA(cudaMemsetAsync(p, 0, sizeof(int), s));
+    SPB_CUDA(cudaMalloc(&p, kDgTickets * sizeof(int)));
+    SPB_CUDA(cudaMemsetAsync(p, 0, kDgTickets * sizeof(int), s));
     it = words.emplace(std::make_pair(dev, s), p).first;
   }
   *out = it->second;
@@ -305,13 +341,14 @@ int gram_chol_dd(int64_t rows, int b, const double* X, int64_t ldx, double* R, i
   const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(kNumSMs, (int64_t)std::sqrt((double)rows)));
   const int64_t per = ceil_div(rows, ctas);
   const int nb = (int)ceil_div(rows, per);
-  double2* part = ar.alloc<double2>((size_t)nb * kDgEnt);
+  double2* part = ar.alloc<double2>((size_t)(nb + (nb + kDgGroup - 1) / kDgGroup) * kDgEnt);
   if (!part) {
     set_error("gram_chol_dd workspace allocation failed");
     return SP_ECUDA;
   }
-  SPB_CUDA(launch_pdl((ddgram_chol_kernel), dim3(nb), dim3(kDgThreads), 0, s, rows, b, X, ldx, per, part, ticket,
-                      R, ldr));
+  double2* gpart = part + (size_t)nb * kDgEnt;
+  SPB_CUDA(launch_pdl((ddgram_chol_kernel), dim3(nb), dim3(kDgThreads), 0, s, rows, b, X, ldx, per, part, gpart,
+                      ticket, R, ldr));
   count_launch();
   SPB_CHECK_LAUNCH();
   return SP_OK;
