@@ -62,6 +62,42 @@ __device__ __forceinline__ int tile_off(int r, int k) {
   return TRANS ? k * (ROWS + 4) + r : r * PadK<ROWS>::v + k;
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int bytes) {
+  unsigned saddr = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(gmem), "r"(bytes));
+}
+
+// Same tile with 16-byte copies of element pairs along the contiguous
+// dimension (ld even, X 16-byte aligned; every smem pair offset is even).
+// A pair straddling the edge copies 8 bytes and zero-fills the other half.
+template <int TRANS, int ROWS>
+__device__ __forceinline__ void load_tile16(double* st, const double* X, int64_t ld, int64_t R,
+                                            int64_t K, int64_t r0, int64_t k0, int64_t k_end) {
+#pragma unroll
+  for (int u = 0; u < (ROWS * kBK) / (2 * kGemmThreads); ++u) {
+    const int e = threadIdx.x + u * kGemmThreads;  // pair index
+    int r, k;
+    int64_t lim;
+    if (TRANS) {  // stored K x R: pairs along r
+      k = e / (ROWS / 2);
+      r = 2 * (e % (ROWS / 2));
+    } else {  // stored R x K: pairs along k
+      r = e / (kBK / 2);
+      k = 2 * (e % (kBK / 2));
+    }
+    const int64_t gr = r0 + r, gk = k0 + k;
+    int n;
+    if (TRANS) {
+      lim = R - gr;
+      n = (gk < k_end && lim > 0) ? (lim >= 2 ? 16 : 8) : 0;
+    } else {
+      lim = k_end - gk;
+      n = (gr < R && lim > 0) ? (lim >= 2 ? 16 : 8) : 0;
+    }
+    cp_async16(st + tile_off<TRANS, ROWS>(r, k), n ? op_ptr<TRANS>(X, ld, gr, gk) : X, n);
+  }
+}
+
 template <int TRANS, int ROWS>
 __device__ __forceinline__ void load_tile(double* st, const double* X, int64_t ld, int64_t R,
                                           int64_t K, int64_t r0, int64_t k0, int64_t k_end) {
@@ -83,7 +119,7 @@ __device__ __forceinline__ void load_tile(double* st, const double* X, int64_t l
   }
 }
 
-template <int TA, int TB, int BM, int BN>
+template <int TA, int TB, int BM, int BN, bool V16>
 __global__ void __launch_bounds__(kGemmThreads)
 dgemm_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, int64_t lda,
              const double* __restrict__ B, int64_t ldb, double* __restrict__ C, int64_t ldc,
@@ -111,17 +147,21 @@ dgemm_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, int6
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  if (ntiles > 0) {
-    load_tile<TA, BM>(sA[0], A, lda, M, K, m0, kb, ke);
-    load_tile<TB ? 0 : 1, BN>(sB[0], B, ldb, N, K, n0, kb, ke);
-  }
+  auto load_stage = [&](int st, int64_t k0) {
+    if constexpr (V16) {
+      load_tile16<TA, BM>(sA[st], A, lda, M, K, m0, k0, ke);
+      load_tile16<TB ? 0 : 1, BN>(sB[st], B, ldb, N, K, n0, k0, ke);
+    } else {
+      load_tile<TA, BM>(sA[st], A, lda, M, K, m0, k0, ke);
+      load_tile<TB ? 0 : 1, BN>(sB[st], B, ldb, N, K, n0, k0, ke);
+    }
+  };
+  if (ntiles > 0) load_stage(0, kb);
   cp_async_commit();
   for (int kt = 0; kt < ntiles; ++kt) {
     const int cur = kt & 1;
     if (kt + 1 < ntiles) {
-      const int64_t kn = kb + (int64_t)(kt + 1) * kBK;
-      load_tile<TA, BM>(sA[cur ^ 1], A, lda, M, K, m0, kn, ke);
-      load_tile<TB ? 0 : 1, BN>(sB[cur ^ 1], B, ldb, N, K, n0, kn, ke);
+      load_stage(cur ^ 1, kb + (int64_t)(kt + 1) * kBK);
       cp_async_commit();
       cp_async_wait<1>();
     } else {
@@ -221,10 +261,17 @@ template <int TA, int TB, int BM, int BN>
 static void launch_dgemm(dim3 grid, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                          const double* B, int64_t ldb, double* C, int64_t ldc, double alpha,
                          double beta, int64_t kps, bool partial, cudaStream_t s) {
+  // 16-byte copies when both operands allow them (even leading dimensions,
+  // 16-byte aligned bases; split-K boundaries are multiples of kBK)
+  const bool v16 = (lda % 2 == 0) && (ldb % 2 == 0) &&
+                   ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0;
   // errors surface through the caller's cudaGetLastError check
-  if (launch_pdl((dgemm_kernel<TA, TB, BM, BN>), grid, dim3(kGemmThreads), 0, s, M, N, K, A, lda, B, ldb, C, ldc,
-                 alpha, beta, kps, partial) != cudaSuccess)
-    return;
+  if (v16)
+    launch_pdl((dgemm_kernel<TA, TB, BM, BN, true>), grid, dim3(kGemmThreads), 0, s, M, N, K, A, lda, B, ldb, C, ldc,
+               alpha, beta, kps, partial);
+  else
+    launch_pdl((dgemm_kernel<TA, TB, BM, BN, false>), grid, dim3(kGemmThreads), 0, s, M, N, K, A, lda, B, ldb, C,
+               ldc, alpha, beta, kps, partial);
 }
 
 template <int BM, int BN>

@@ -21,6 +21,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "launch_count.cuh"
 #include "ops.cuh"
@@ -314,7 +316,16 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
       // SVD takes a few sweeps instead of ~8 (a noise bulk in the block is
       // nearly invariant under X X^T, so it stays nearly diagonal too).  P is
       // scratch here: the next step recomputes it.
-      SPB_TRY(gemm(0, 0, cols, b, b, 1.0, Z, b, Us, b, 0.0, P, b, s));
+      static const bool plain_restart = getenv("SPB_RR_PLAIN") != nullptr;  // experiments: Y = X P
+      if (plain_restart) {
+        if (lazy_p) {
+          TsqrPlan zplan;
+          SPB_TRY(tsqr_factor(cols, b, Z, b, Rz, b, zplan, it, s));
+          SPB_TRY(tsqr_form_q(zplan, P, b, it, s));
+        }
+      } else {
+        SPB_TRY(gemm(0, 0, cols, b, b, 1.0, Z, b, Us, b, 0.0, P, b, s));
+      }
       SPB_TRY(gemm(0, 0, rows, b, cols, 1.0, X, ldx, P, b, 0.0, Y, b, s));
       SPB_TRY(tsqr(rows, b, Y, b, Q, b, Rt, b, s));
     }
