@@ -6,7 +6,7 @@
 // operand is copied to shared memory in its global (coalesced) orientation and
 // the fragment reads are bank-conflict free for both orientations (padded
 // strides 20 and 68 doubles).  64x64x16 CTA tiles, 4 warps of 32x32, 8-byte
-// cp.async with zero-fill at the edges, 2-stage pipeline.  When the tile grid
+// cp.async (16-byte pairs when aligned) with zero-fill at the edges, a 3-stage ring.  When the tile grid
 // cannot fill the 148 SMs, K is split and the partial tiles are reduced in a
 // fixed order (bitwise reproducible).
 //
@@ -20,6 +20,7 @@ namespace spb {
 
 constexpr int kBK = 16;
 constexpr int kGemmThreads = 128;
+constexpr int kGemmStages = 3;  // cp.async ring depth (dynamic shared memory)
 // k-contiguous rows: stride 20 doubles (18 for the 128-row tiles, which
 // would otherwise not fit two stages in 48 KB of static shared memory)
 template <int ROWS>
@@ -119,6 +120,13 @@ __device__ __forceinline__ void load_tile(double* st, const double* X, int64_t l
   }
 }
 
+template <int TA, int TB, int BM, int BN>
+struct StageSizes {
+  static constexpr int kSA = TA ? kBK * (BM + 4) : BM * PadK<BM>::v;
+  static constexpr int kSB = TB ? BN * PadK<BN>::v : kBK * (BN + 4);
+  static constexpr size_t kBytes = (size_t)kGemmStages * (kSA + kSB) * sizeof(double);
+};
+
 template <int TA, int TB, int BM, int BN, bool V16>
 __global__ void __launch_bounds__(kGemmThreads)
 dgemm_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, int64_t lda,
@@ -127,10 +135,12 @@ dgemm_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, int6
   SPB_PDL_ENTRY();
   using TL = Tile<BM, BN>;
   // stage sizes for the operand orientations (op(B) tile is stored as (n, k) with orientation !TB)
-  constexpr int kSA = TA ? kBK * (BM + 4) : BM * PadK<BM>::v;
-  constexpr int kSB = TB ? BN * PadK<BN>::v : kBK * (BN + 4);
-  __shared__ __align__(16) double sA[2][kSA];
-  __shared__ __align__(16) double sB[2][kSB];
+  constexpr int kSA = StageSizes<TA, TB, BM, BN>::kSA;
+  constexpr int kSB = StageSizes<TA, TB, BM, BN>::kSB;
+  // kGemmStages-deep cp.async ring in dynamic shared memory
+  extern __shared__ __align__(16) double gemm_smem[];
+  double (*sA)[kSA] = reinterpret_cast<double (*)[kSA]>(gemm_smem);
+  double (*sB)[kSB] = reinterpret_cast<double (*)[kSB]>(gemm_smem + kGemmStages * kSA);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int wm = (warp % TL::kWarpsM) * 32, wn = (warp / TL::kWarpsM) * 32;
@@ -158,16 +168,19 @@ dgemm_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, int6
   };
   if (ntiles > 0) load_stage(0, kb);
   cp_async_commit();
+  for (int st = 1; st < kGemmStages - 1; ++st) {
+    if (st < ntiles) load_stage(st, kb + (int64_t)st * kBK);
+    cp_async_commit();
+  }
   for (int kt = 0; kt < ntiles; ++kt) {
-    const int cur = kt & 1;
-    if (kt + 1 < ntiles) {
-      load_stage(cur ^ 1, kb + (int64_t)(kt + 1) * kBK);
+    const int cur = kt % kGemmStages;
+    cp_async_wait<kGemmStages - 2>();
+    __syncthreads();  // tile kt landed for every thread; stage (kt - 1) % S is free
+    {
+      const int nx = kt + kGemmStages - 1;
+      if (nx < ntiles) load_stage(nx % kGemmStages, kb + (int64_t)nx * kBK);
       cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
     }
-    __syncthreads();
     const double* a_s = sA[cur];
     const double* b_s = sB[cur];
 #pragma unroll
@@ -183,7 +196,6 @@ dgemm_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, int6
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
-    __syncthreads();
   }
 
   double* Cs = partial ? C + (int64_t)blockIdx.z * M * N : C;
@@ -265,12 +277,21 @@ static void launch_dgemm(dim3 grid, int64_t M, int64_t N, int64_t K, const doubl
   // 16-byte aligned bases; split-K boundaries are multiples of kBK)
   const bool v16 = (lda % 2 == 0) && (ldb % 2 == 0) &&
                    ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0;
+  constexpr size_t smem = StageSizes<TA, TB, BM, BN>::kBytes;
+  static int attr_dev = -1;  // once per device and instantiation
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaFuncSetAttribute(dgemm_kernel<TA, TB, BM, BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(dgemm_kernel<TA, TB, BM, BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_dev = dev;
+  }
   // errors surface through the caller's cudaGetLastError check
   if (v16)
-    launch_pdl((dgemm_kernel<TA, TB, BM, BN, true>), grid, dim3(kGemmThreads), 0, s, M, N, K, A, lda, B, ldb, C, ldc,
-               alpha, beta, kps, partial);
+    launch_pdl((dgemm_kernel<TA, TB, BM, BN, true>), grid, dim3(kGemmThreads), smem, s, M, N, K, A, lda, B, ldb, C,
+               ldc, alpha, beta, kps, partial);
   else
-    launch_pdl((dgemm_kernel<TA, TB, BM, BN, false>), grid, dim3(kGemmThreads), 0, s, M, N, K, A, lda, B, ldb, C,
+    launch_pdl((dgemm_kernel<TA, TB, BM, BN, false>), grid, dim3(kGemmThreads), smem, s, M, N, K, A, lda, B, ldb, C,
                ldc, alpha, beta, kps, partial);
 }
 
@@ -310,8 +331,11 @@ int gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const do
   const int64_t tiles = (int64_t)gx * gy;
   int S = 1;
   if (tiles < 2 * kNumSMs) {
-    // enough K-splits for ~4 CTAs per SM, each split at least 4 k-tiles deep
-    S = (int)std::min<int64_t>(ceil_div(4 * kNumSMs, tiles), std::max<int64_t>(1, K / (4 * kBK)));
+    // K-splits filling exactly one wave of the resident slots (3 CTAs per SM
+    // with the 3-stage ring; a partial second wave costs a whole CTA time),
+    // each split at least 4 k-tiles deep
+    constexpr int kSlots = 3 * kNumSMs;
+    S = (int)std::min<int64_t>(std::max<int64_t>(1, kSlots / tiles), std::max<int64_t>(1, K / (4 * kBK)));
     S = std::max(1, std::min(S, 1024));
   }
   int64_t kps = ceil_div(K, S);
