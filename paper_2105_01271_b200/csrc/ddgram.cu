@@ -117,7 +117,8 @@ __device__ __forceinline__ dd dd_rsqrt(dd d) {
 }
 
 __global__ void __launch_bounds__(kDgThreads)
-ddgram_chol_kernel(int64_t rows, int b, const double* __restrict__ X, int64_t ldx, int64_t rows_per_cta,
+ddgram_chol_kernel(int64_t rows, int b, const double* __restrict__ X, int64_t ldx, int nslab, int64_t slab_stride,
+                   int64_t rows_per_cta,
                    double2* __restrict__ partial, double2* __restrict__ gpart, int* __restrict__ ticket,
                    double* __restrict__ R, int64_t ldr) {
   SPB_TDECL;
@@ -140,12 +141,26 @@ ddgram_chol_kernel(int64_t rows, int b, const double* __restrict__ X, int64_t ld
   const int64_t r1 = imin64(rows, r0 + rows_per_cta);
   for (int64_t c0 = r0; c0 < r1; c0 += kDgTile) {
     const int nr = (int)imin64(kDgTile, r1 - c0);
-    for (int e = t; e < kDgTile * kDgB; e += kDgThreads) {
-      const int rr = e / kDgB, cc = e % kDgB;
-      const bool ok = rr < nr && cc < b;
-      cp_async_f64(&xs[rr][cc], ok ? X + (c0 + rr) * ldx + cc : X, ok);
+    if (nslab == 1) {
+      for (int e = t; e < kDgTile * kDgB; e += kDgThreads) {
+        const int rr = e / kDgB, cc = e % kDgB;
+        const bool ok = rr < nr && cc < b;
+        cp_async_f64(&xs[rr][cc], ok ? X + (c0 + rr) * ldx + cc : X, ok);
+      }
+      cp_async_wait_all();
+    } else {  // X = sum of the split-K slabs, in slab order
+      for (int e = t; e < kDgTile * kDgB; e += kDgThreads) {
+        const int rr = e / kDgB, cc = e % kDgB;
+        double v = 0.0;
+        if (rr < nr && cc < b) {
+          const double* p = X + (c0 + rr) * ldx + cc;
+          v = __ldcg(p);
+#pragma unroll 4
+          for (int q = 1; q < nslab; ++q) v += __ldcg(p + (int64_t)q * slab_stride);
+        }
+        xs[rr][cc] = v;
+      }
     }
-    cp_async_wait_all();
     __syncthreads();
     if (c0 == r0) SPB_TMARK(1);
     if (2 * t < kDgEnt) {
@@ -329,9 +344,11 @@ static int dd_ticket(cudaStream_t s, int** out) {
 bool gram_chol_dd_ok(int64_t rows, int b) { return b >= 1 && b <= kDgB && rows >= b; }
 
 // R (b x b upper, ld ldr; zeros below the diagonal) with
-// R^T R = X^T X, X rows x b (ld ldx).  Asynchronous.
+// R^T R = X^T X, X rows x b (ld ldx), or X = the sum of nslab split-K slabs
+// slab_stride apart (summed in slab order while the tiles are staged).
+// Asynchronous.
 int gram_chol_dd(int64_t rows, int b, const double* X, int64_t ldx, double* R, int64_t ldr, Arena& ar,
-                 cudaStream_t s) {
+                 cudaStream_t s, int nslab, int64_t slab_stride) {
   SPB_REQUIRE(gram_chol_dd_ok(rows, b), "gram_chol_dd: shape out of range");
   int* ticket = nullptr;
   SPB_TRY(dd_ticket(s, &ticket));
@@ -347,7 +364,8 @@ int gram_chol_dd(int64_t rows, int b, const double* X, int64_t ldx, double* R, i
     return SP_ECUDA;
   }
   double2* gpart = part + (size_t)nb * kDgEnt;
-  SPB_CUDA(launch_pdl((ddgram_chol_kernel), dim3(nb), dim3(kDgThreads), 0, s, rows, b, X, ldx, per, part, gpart,
+  SPB_CUDA(launch_pdl((ddgram_chol_kernel), dim3(nb), dim3(kDgThreads), 0, s, rows, b, X, ldx, std::max(1, nslab),
+                      slab_stride, per, part, gpart,
                       ticket, R, ldr));
   count_launch();
   SPB_CHECK_LAUNCH();

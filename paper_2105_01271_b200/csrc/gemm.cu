@@ -363,6 +363,43 @@ int gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const do
   return SP_OK;
 }
 
+// op(A) op(B) as S fixed-order split-K partial slabs P[s] (M x N, row-major,
+// slab stride M * N) for a consumer that sums them itself (the Rz Gram of the
+// Rayleigh-Ritz step reads Z = C^T Q this way: no reduction launch on the
+// critical path).  S = 1 writes the product itself.  DMMA shapes only.
+int gemm_partials(int ta, int tb, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
+                  int64_t ldb, Arena& ar, double** P, int* S_out, cudaStream_t s) {
+  SPB_REQUIRE(M > 0 && N > 0 && K > 0, "gemm_partials: empty GEMM");
+  SPB_REQUIRE(lda >= (ta ? M : K) && ldb >= (tb ? K : N), "bad GEMM leading dimension");
+  const bool narrow = N <= 32;
+  const int bm = narrow ? 128 : 64, bn = narrow ? 32 : 64;
+  const int64_t tiles = (int64_t)ceil_div(N, bn) * ceil_div(M, bm);
+  int S = 1;
+  if (tiles < 2 * kNumSMs) {
+    constexpr int kSlots = 3 * kNumSMs;  // as gemm(): one wave of the resident slots
+    S = (int)std::min<int64_t>(std::max<int64_t>(1, kSlots / tiles), std::max<int64_t>(1, K / (4 * kBK)));
+    S = std::max(1, std::min(S, 1024));
+  }
+  int64_t kps = ceil_div(ceil_div(K, S), kBK) * (int64_t)kBK;
+  S = ceil_div(K, kps);
+  double* out = ar.alloc<double>((size_t)S * M * N);
+  if (!out) {
+    set_error("GEMM split-K workspace allocation failed");
+    return SP_ECUDA;
+  }
+  const dim3 grid((unsigned)tiles, 1, S);
+  const int code = ta * 2 + tb;
+  if (narrow)
+    launch_dgemm_any<128, 32>(code, grid, M, N, K, A, lda, B, ldb, out, N, 1.0, 0.0, kps, true, s);
+  else
+    launch_dgemm_any<64, 64>(code, grid, M, N, K, A, lda, B, ldb, out, N, 1.0, 0.0, kps, true, s);
+  count_launch();
+  SPB_CHECK_LAUNCH();
+  *P = out;
+  *S_out = S;
+  return SP_OK;
+}
+
 int split_reduce(const double* P, int S, int64_t M, int64_t N, double alpha, double beta, double* C, int64_t ldc,
                  cudaStream_t s) {
   if (S > 8) {

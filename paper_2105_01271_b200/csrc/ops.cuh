@@ -38,7 +38,9 @@ int tsqr_form_q(const TsqrPlan& plan, double* Q, int64_t ldq, Arena& ar, cudaStr
 // R (b x b upper) with R^T R = X^T X from a double-double Gram (b <= 32)
 bool gram_chol_dd_ok(int64_t rows, int b);
 int gram_chol_dd(int64_t rows, int b, const double* X, int64_t ldx, double* R, int64_t ldr, Arena& ar,
-                 cudaStream_t s);
+                 cudaStream_t s, int nslab = 1, int64_t slab_stride = 0);
+int gemm_partials(int ta, int tb, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
+                  int64_t ldb, Arena& ar, double** P, int* S_out, cudaStream_t s);
 int tall_gram(int64_t rows, int c, const double* X, int64_t ldx, int d, const double* Y, int64_t ldy,
               double alpha, double beta, double* G, int64_t ldg, cudaStream_t s);
 int tall_gram_partials(int64_t rows, int c, const double* X, int64_t ldx, int d, const double* Y, int64_t ldy,

@@ -243,16 +243,20 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
     bool spec = false;
     for (int itn = 0; itn < max_it; ++itn) {
       // Rayleigh-Ritz: Q^T X = Z^T with Z = X^T Q = P Rz  ->  Q^T X = Rz^T P^T
-      SPB_TRY(gemm(1, 0, cols, b, rows, 1.0, X, ldx, Q, b, 0.0, Z, b, s));
-      // Z = P Rz: only Rz is needed unless V is wanted or another step
-      // follows (then P is formed from the kept factors, below)
-      // (R alone: Cholesky of the double-double Gram, ddgram.cu -- one launch
-      // instead of the 32-step Householder factor)
+      // Z = P Rz: only Rz is needed unless V is wanted (R alone: Cholesky of
+      // the double-double Gram, ddgram.cu -- one launch instead of the 32-step
+      // Householder factor; it sums the split-K slabs of Z itself, and Z is
+      // reduced explicitly only if another step follows)
       const bool lazy_p = b <= 32 && !want_v && gram_chol_dd_ok(cols, b);
-      if (lazy_p)
-        SPB_TRY(gram_chol_dd(cols, b, Z, b, Rz, b, it, s));
-      else
+      double* Zp = nullptr;
+      int zs = 0;
+      if (lazy_p) {
+        SPB_TRY(gemm_partials(1, 0, cols, b, rows, X, ldx, Q, b, it, &Zp, &zs, s));
+        SPB_TRY(gram_chol_dd(cols, b, Zp, b, Rz, b, it, s, zs, (int64_t)cols * b));
+      } else {
+        SPB_TRY(gemm(1, 0, cols, b, rows, 1.0, X, ldx, Q, b, 0.0, Z, b, s));
         SPB_TRY(tsqr(cols, b, Z, b, P, b, Rz, b, s));
+      }
       SPB_TRY(jacobi_svd_tr(b, Rz, b, /*trans=*/true, Us, b, Sg, want_v ? Vs : nullptr, b, s));
       // publish the Ritz values, then -- while the host waits for them --
       // form the final products as if this step converged (it usually does;
@@ -316,6 +320,12 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
       // SVD takes a few sweeps instead of ~8 (a noise bulk in the block is
       // nearly invariant under X X^T, so it stays nearly diagonal too).  P is
       // scratch here: the next step recomputes it.
+      if (lazy_p) {  // Z itself is needed now
+        if (zs > 1)
+          SPB_TRY(split_reduce(Zp, zs, cols, b, 1.0, 0.0, Z, b, s));
+        else
+          SPB_TRY(copy2d(cols, b, Zp, b, Z, b, s));
+      }
       static const bool plain_restart = getenv("SPB_RR_PLAIN") != nullptr;  // experiments: Y = X P
       if (plain_restart) {
         if (lazy_p) {
