@@ -342,9 +342,10 @@ jacobi32_kernel(int n, const double* __restrict__ M, int64_t ldm, double* __rest
       if (big ? fabs(g) > kJacQuad * sqrt(ap) * sqrt(aq) : g * g > (kJacQuad * kJacQuad) * apq) rotated = 1;
     }
     // Stop after a sweep whose rotations were all below kJacQuad in relative
-    // size: cyclic Jacobi converges quadratically, so the next sweep would
-    // find every |w_p.w_q| below ~n kJacQuad^2 / (relative gap) < kJacTol
-    // ||w_p|| ||w_q|| and rotate nothing -- it is not run (5 -> 4 sweeps on
+    // size: cyclic Jacobi converges quadratically, so what the next sweep
+    // would still find is ~n kJacQuad^2 / (relative gap) ~ 1e-15 of
+    // ||w_p|| ||w_q|| (the kJacTol level: column changes ~1e-15, singular
+    // values unchanged to second order) -- it is not run (5 -> 4 sweeps on
     // the cfg2 core).
     if (!__syncthreads_or(rotated)) {
 #ifdef SPB_JACOBI_TRACE
