@@ -234,7 +234,10 @@ int sp_gram_chol_dd(int64_t rows, int32_t b, const double* X, int64_t ldx, doubl
  * (device int, may be NULL) is OR-ed with 1 if X has a non-finite entry.
  * sp_srht_gather forms X = A(:, gidx) (exact copies, written to X) and the
  * same Y in one pass over A (K1 fused with the first product; the power
- * pipeline uses it for a device-resident A).  SP_ECONFIG outside the range. */
+ * pipeline uses it for a device-resident A); wider than 16384 columns, the
+ * row is cut into 16384-column chunks with their own signs and the same
+ * samples, and the chunk transforms are summed in chunk order (a block SRHT:
+ * Omega^T Omega = chunks * 16384 * I).  SP_ECONFIG outside the range. */
 int sp_srht_sketch(int64_t rows, int64_t cols, const double* X, int64_t ldx, int32_t b, uint64_t seed,
                    double* Y, int64_t ldy, int32_t* flag, void* stream);
 int sp_srht_gather(const void* A, int32_t a_dtype, int64_t rows, int64_t lda, const int64_t* gidx, int64_t cols,

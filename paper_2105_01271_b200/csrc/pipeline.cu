@@ -34,6 +34,7 @@ constexpr double kRankTol = 1e-12;  // src/kernels.py:19
 int srht_sketch(int64_t rows, int64_t cols, const double* X, int64_t ldx, int b, uint64_t seed, double* Y,
                 int64_t ldy, int* flag, cudaStream_t s);
 bool srht_ok(int64_t rows, int64_t cols, int b);
+bool srht_gather_ok(int64_t rows, int64_t cols, int b);
 int srht_gather(const void* A, int a_dtype, int64_t rows, int64_t lda, const int64_t* gidx, int64_t cols, double* C,
                 int64_t ldc, int b, uint64_t seed, double* Y, int64_t ldy, int* flag, cudaStream_t s);
 constexpr uint64_t kSrhtSeed = 0x5eed5eedull;  // + block width
@@ -667,7 +668,7 @@ int power_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, con
       set_error("column block allocation failed");
       return SP_ECUDA;
     }
-    if (same && std::min<int64_t>(m, ncols) > 64 && srht_ok(m, ncols, 32)) {
+    if (same && std::min<int64_t>(m, ncols) > 64 && srht_gather_ok(m, ncols, 32)) {
       // K1 fused with the range finder's test block: C and Y = C D H S in one pass
       double* y = ar.alloc<double>((size_t)m * 32);
       if (!y) {

@@ -18,6 +18,7 @@
 // Fixed operation order: bitwise reproducible.
 #include "common.cuh"
 #include "launch_count.cuh"
+#include "ops.cuh"
 
 namespace spb {
 
@@ -117,19 +118,25 @@ template <int LT, bool GATHER, int RPC, typename TA>
 __global__ void __launch_bounds__(1 << LT)
 srht_kernel(int64_t rows, int64_t cols, const double* __restrict__ X, int64_t ldx, int b, uint64_t seed,
             double* __restrict__ Y, int64_t ldy, int* __restrict__ flag, const TA* __restrict__ A, int64_t lda,
-            const int64_t* __restrict__ gidx, double* __restrict__ Xout) {
+            const int64_t* __restrict__ gidx, double* __restrict__ Xout, int64_t ychunk) {
   SPB_PDL_ENTRY();
   constexpr int T = 1 << LT;
   extern __shared__ double sr_smem[];  // srht_pad(N) doubles
   const int t = threadIdx.x;
   const int64_t row0 = (int64_t)blockIdx.x * RPC;
-  const uint64_t sg = srht_hash(seed, (uint64_t)t);  // sign of element t + T e: bit e
+  // chunk (blockIdx.y) of a row wider than the transform (gather mode): its
+  // own random signs, the same Hadamard samples; partial Y at Y + chunk * ychunk
+  const int chunk = blockIdx.y;
+  const int64_t cbase = (int64_t)chunk * (16 * T);
+  Y += chunk * ychunk;
+  const uint64_t sg = srht_hash(chunk ? seed ^ (0xA24BAED4963EE407ull * (uint64_t)chunk) : seed,
+                                (uint64_t)t);  // sign of element t + T e: bit e
   double v[RPC][16];
   if (GATHER) {
     int64_t gi[16];
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
-      const int64_t j = (int64_t)t + (int64_t)T * e;
+      const int64_t j = cbase + t + (int64_t)T * e;
       gi[e] = j < cols ? __ldg(gidx + j) : 0;
     }
 #pragma unroll
@@ -138,7 +145,7 @@ srht_kernel(int64_t rows, int64_t cols, const double* __restrict__ X, int64_t ld
       const TA* ar = A + (live ? row0 + r : 0) * lda;
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
-        const int64_t j = (int64_t)t + (int64_t)T * e;
+        const int64_t j = cbase + t + (int64_t)T * e;
         v[r][e] = (live && j < cols) ? widen(__ldg(ar + gi[e])) : 0.0;
       }
     }
@@ -148,7 +155,7 @@ srht_kernel(int64_t rows, int64_t cols, const double* __restrict__ X, int64_t ld
       double* orow = Xout + (row0 + r) * ldx;
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
-        const int64_t j = (int64_t)t + (int64_t)T * e;
+        const int64_t j = cbase + t + (int64_t)T * e;
         if (j < cols) orow[j] = v[r][e];
       }
     }
@@ -185,11 +192,36 @@ bool srht_ok(int64_t rows, int64_t cols, int b) {
   return cols >= 1 && cols <= n2 && b >= 1 && b <= 32 && n2 % b == 0 && rows >= 1 && rows <= 0x7fffffff;
 }
 
+// gather mode: rows wider than the widest transform (16384) are cut into
+// 16384-column chunks, each transformed with its own signs and the same
+// samples; the partial test blocks are summed in chunk order (a block SRHT,
+// Balabanov, Beaupere, Grigori & Lederer 2022: the columns of Omega stay
+// orthogonal, Omega^T Omega = chunks * N * I)
+constexpr int64_t kSrhtChunk = 16384;
+
+bool srht_gather_ok(int64_t rows, int64_t cols, int b) {
+  if (cols <= kSrhtChunk) return srht_ok(rows, cols, b);
+  return b >= 1 && b <= 32 && kSrhtChunk % b == 0 && rows >= 1 && rows <= 0x7fffffff && cols / kSrhtChunk < 65535;
+}
+
 template <bool GATHER, typename TA>
 static int srht_launch(int64_t rows, int64_t cols, const double* X, int64_t ldx, int b, uint64_t seed, double* Y,
                        int64_t ldy, int* flag, const TA* A, int64_t lda, const int64_t* gidx, double* Xout,
                        cudaStream_t s) {
   constexpr int RPC = 1;
+  const int nchunk = (GATHER && cols > kSrhtChunk) ? (int)ceil_div(cols, kSrhtChunk) : 1;
+  Arena ar(s);
+  double* Yk = Y;
+  int64_t ldyk = ldy, ychunk = 0;
+  if (nchunk > 1) {
+    Yk = ar.alloc<double>((size_t)nchunk * rows * b);
+    if (!Yk) {
+      set_error("srht chunk workspace allocation failed");
+      return SP_ECUDA;
+    }
+    ldyk = b;
+    ychunk = rows * b;
+  }
   const int lt = srht_lt(cols);
   const int64_t n2 = (int64_t)16 << lt;
   const size_t smem = (size_t)(n2 + n2 / 16) * sizeof(double);
@@ -201,12 +233,12 @@ static int srht_launch(int64_t rows, int64_t cols, const double* X, int64_t ldx,
     SPB_CUDA(cudaFuncSetAttribute(srht_kernel<10, GATHER, RPC, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr_dev = dev;
   }
-  const dim3 grid((unsigned)((rows + RPC - 1) / RPC));
+  const dim3 grid((unsigned)((rows + RPC - 1) / RPC), (unsigned)nchunk);
   switch (lt) {
 #define SPB_SRHT_LT(L)                                                                                              \
   case L:                                                                                                           \
     SPB_CUDA(launch_pdl((srht_kernel<L, GATHER, RPC, TA>), grid, dim3(1 << L), smem, s, rows, cols, X, ldx, b, seed, \
-                        Y, ldy, flag, A, lda, gidx, Xout));                                                         \
+                        Yk, ldyk, flag, A, lda, gidx, Xout, ychunk));                                               \
     break;
     SPB_SRHT_LT(4) SPB_SRHT_LT(5) SPB_SRHT_LT(6) SPB_SRHT_LT(7) SPB_SRHT_LT(8) SPB_SRHT_LT(9) SPB_SRHT_LT(10)
 #undef SPB_SRHT_LT
@@ -216,6 +248,7 @@ static int srht_launch(int64_t rows, int64_t cols, const double* X, int64_t ldx,
   }
   count_launch();
   SPB_CHECK_LAUNCH();
+  if (nchunk > 1) return split_reduce(Yk, nchunk, rows, b, 1.0, 0.0, Y, ldy, s);
   return SP_OK;
 }
 
@@ -233,7 +266,7 @@ int srht_sketch(int64_t rows, int64_t cols, const double* X, int64_t ldx, int b,
 // C (rows x cols, ld ldc) = A(:, gidx) (exact copies) and Y = C D H S, one pass.
 int srht_gather(const void* A, int a_dtype, int64_t rows, int64_t lda, const int64_t* gidx, int64_t cols, double* C,
                 int64_t ldc, int b, uint64_t seed, double* Y, int64_t ldy, int* flag, cudaStream_t s) {
-  if (!srht_ok(rows, cols, b)) {
+  if (!srht_gather_ok(rows, cols, b)) {
     set_error("srht_gather: shape out of range");
     return SP_ECONFIG;
   }

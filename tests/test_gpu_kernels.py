@@ -418,6 +418,56 @@ def test_srht_gather_is_exact_and_matches_two_step(cuda, dtype):
     assert np.array_equal(Y.cpu().numpy(), y2) and int(flag.item()) == 0 and f2 == 0
 
 
+def _srht_gather(cuda, a, idx, b=32, seed=99):
+    rows, n = a.shape
+    A, I = _dev(a, cuda), _dev(idx, cuda)
+    X = cuda.empty((rows, idx.size), dtype=cuda.float64, device="cuda")
+    Y = cuda.empty((rows, b), dtype=cuda.float64, device="cuda")
+    flag = cuda.zeros(1, dtype=cuda.int32, device="cuda")
+    tag = _lib.SP_F64 if a.dtype == np.float64 else _lib.SP_F32
+    _lib.call("sp_srht_gather", A.data_ptr(), tag, rows, n, I.data_ptr(), idx.size, X.data_ptr(), idx.size, b, seed,
+              Y.data_ptr(), b, flag.data_ptr(), _stream(cuda))
+    return X.cpu().numpy(), Y.cpu().numpy(), int(flag.item())
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_srht_gather_chunked_rows(cuda, dtype):
+    # rows wider than 16384 gathered columns (cfg5: 262144): 16384-column
+    # chunks with their own signs and the same samples, summed in chunk order
+    rows, n, nc = 70, 60000, 40000  # chunks of 16384, 16384, 7232
+    a = philox(21).standard_normal((rows, n))
+    if dtype == "f32":
+        a = a.astype(np.float32)
+    idx = np.sort(philox(22).choice(n, size=nc, replace=False)).astype(np.int64)
+    x, y, flag = _srht_gather(cuda, a, idx)
+    want = a[:, idx].astype(np.float64)
+    assert flag == 0
+    assert np.array_equal(x.view(np.int64), want.view(np.int64))
+    # chunk 0 alone is the plain 16384-wide transform with the same seed
+    a0 = np.zeros_like(a)
+    a0[:, idx[:16384]] = a[:, idx[:16384]]
+    _, y0, _ = _srht_gather(cuda, a0, idx)
+    y0_ref, _ = _srht(cuda, want[:, :16384], 32, seed=99)
+    assert np.array_equal(y0, y0_ref)
+    # a single entry in chunk 2: +-value at every sample (Hadamard entries are
+    # +-1), and linearity over the chunks (sum of the per-chunk test blocks)
+    e = np.zeros_like(a)
+    e[3, idx[33000]] = 0.75
+    _, ye, _ = _srht_gather(cuda, e, idx)
+    assert np.all(np.abs(ye[3]) == 0.75) and np.all(np.delete(ye, 3, axis=0) == 0.0)
+    a1, a2 = a0, a - a0
+    _, y1, _ = _srht_gather(cuda, a1, idx)
+    _, y2, _ = _srht_gather(cuda, a2, idx)
+    np.testing.assert_allclose(y, y1 + y2, rtol=0, atol=1e-12 * np.abs(y).max())
+    # the chunks' sign patterns differ: the same local position in chunk 1
+    # gives a different row of Omega than in chunk 0
+    e0 = np.zeros_like(a)
+    e0[0, idx[100]] = 1.0
+    e0[1, idx[16384 + 100]] = 1.0
+    _, yd, _ = _srht_gather(cuda, e0, idx)
+    assert np.all(np.abs(yd[:2]) == 1.0) and not np.array_equal(yd[0], yd[1])
+
+
 # ------------------------------------------------- double-double Gram R ----
 def _gram_chol_dd(cuda, x):
     rows, b = x.shape
