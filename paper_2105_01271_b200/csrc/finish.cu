@@ -379,16 +379,30 @@ gram_stream_kernel(int64_t rows, const double* __restrict__ Y, const double* __r
   __syncthreads();
   if (!last) return;
   __threadfence();
-  if (tid < nout) {
+  {
+    // all threads: gs groups of nout, group g sums partials g, g + gs, ...
+    // (two chains), then the group sums in group order -- a fixed order
+    constexpr int gs = kGsThreads / nout;
+    __shared__ double gred[gs * nout];
+    const int o = tid % nout, g = tid / nout;
     const int nb = gridDim.x;
     double s0 = 0.0, s1 = 0.0;
-    int bb = 0;
-    for (; bb + 1 < nb; bb += 2) {
-      s0 += __ldcg(partial + (int64_t)bb * nout + tid);
-      s1 += __ldcg(partial + (int64_t)(bb + 1) * nout + tid);
+    if (g < gs) {
+      int bb = g;
+      for (; bb + gs < nb; bb += 2 * gs) {
+        s0 += __ldcg(partial + (int64_t)bb * nout + o);
+        s1 += __ldcg(partial + (int64_t)(bb + gs) * nout + o);
+      }
+      if (bb < nb) s0 += __ldcg(partial + (int64_t)bb * nout + o);
+      gred[g * nout + o] = s0 + s1;
     }
-    if (bb < nb) s0 += __ldcg(partial + (int64_t)bb * nout + tid);
-    G[tid / R][tid % R] = s0 + s1;
+    __syncthreads();
+    if (tid < nout) {
+      double t = 0.0;
+#pragma unroll
+      for (int q = 0; q < gs; ++q) t += gred[q * nout + tid];
+      G[tid / R][tid % R] = t;
+    }
   }
   __syncthreads();
   if (tid < 32) {
