@@ -845,7 +845,10 @@ int power_id(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, cons
     SPB_REQUIRE(cols != nullptr && ncols > 0, "column index set out of range");
     SPB_REQUIRE(ncols > k, "column set size " + std::to_string(ncols) + " must exceed target rank " + std::to_string(k));
     SPB_REQUIRE(ncols >= nc, "column set size " + std::to_string(ncols) + " must cover the sketch width " + std::to_string(nc));
-    SPB_TRY(check_columns(cols, ncols, n, s));
+    // with the column block supplied (pre_c: the column-sharded driver's
+    // all-gathered C, whose global indices lie outside this shard's n) the
+    // indices are not read here; the caller validated them
+    if (!pre_c) SPB_TRY(check_columns(cols, ncols, n, s));
   }
   Arena ar(s);
   // coarse sketch (always the plain stencil; projections only feed selection)

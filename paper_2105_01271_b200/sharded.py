@@ -132,7 +132,7 @@ def distributed_sketch_basis(c_i, row0: int, ncols: int, power: float, comm, ops
                 break
             conv = itn == 0 and kept > 0 and b - 8 > kept and hs[b - 8] <= 1e-8 * hs[kept - 1]
             if (not conv and itn >= 1 and kept == kept_prev and kept > 0 and b - 8 > kept
-                    and (hs[b - 8] / hs[kept - 1]) ** (2.0 * itn + 2.0) <= 1e-16):
+                    and (hs[b - 8] / hs[kept - 1]) ** (2.0 * itn + 2.0) <= 1e-12):
                 conv = True
             if not conv and itn >= 1 and kept == kept_prev:
                 chk = min(b, kept + 1)
@@ -140,9 +140,9 @@ def distributed_sketch_basis(c_i, row0: int, ncols: int, power: float, comm, ops
             if conv:
                 break
             prev, kept_prev = hs, kept
-            # one more subspace iteration: Y = C P, P_i = P_Z,i Q_top,i
-            p_i = (ops.rows(pz, 0, nci) if q_top is None else
-                   ops.matmul(ops.rows(pz, 0, nci), ops.rows(q_top, comm.rank * b, (comm.rank + 1) * b)))
+            # one more subspace iteration from the Ritz vectors, as svd_top:
+            # Y = C (Z U_s) = sum_i C_i (Z_i U_s)  (Z_i local, U_s replicated)
+            p_i = ops.matmul(z, us)
             y = comm.allreduce_sum(ops.matmul(c_i, p_i), ops)
             qy, _ = ops.tsqr(y)
         if grow:
@@ -379,11 +379,62 @@ class DeviceOps:
                   kp.data_ptr() if r > 0 else None, self._s())
         return x, kp
 
+    def power_id_local(self, a_local, c_all, cols, k, q, r=None):
+        """sp_power_id on this shard with the all-gathered C as both the
+        coarse sketch and the column block (no gather, no index validation)."""
+        import warnings
+
+        from .device import empty, ptr, to_device, to_host_many
+        from .errors import RankDeficiencyWarning
+        m, n_i = a_local.shape
+        ncols = int(c_all.shape[1])
+        c_all = self.contig(c_all)
+        d_cols = to_device(np.asarray(cols, dtype=np.int64))
+        w = self.t.ones(ncols, dtype=self.t.float64, device=c_all.device)
+        r_req = int(r) if r is not None else 0
+        r_max = max(r_req, 2 * k, 1)
+        p, ind, skel = empty((m, k)), empty((k,), "i64"), empty((k, ncols))
+        left, right = empty((ncols, r_max)), empty((r_max, n_i))
+        info = _lib.new_info()
+        tag = _lib.SP_F64 if a_local.dtype == self.t.float64 else _lib.SP_F32
+        _lib.call("sp_power_id", ptr(a_local), tag, m, n_i, a_local.stride(0), ptr(d_cols), ptr(w), 1, ncols,
+                  ptr(d_cols), ncols, q, k, r_req, None, 0, 0, ptr(c_all), ptr(c_all), ptr(p), ptr(ind),
+                  ptr(skel), ptr(left), ptr(right), None, r_max, _lib.info_ptr(info), self._s())
+        warn = int(info[_lib.INFO_WARN])
+        if warn & _lib.SP_WARN_ID_PINV:
+            warnings.warn("ID pivots are rank deficient; using pseudo-inverse solve", RankDeficiencyWarning,
+                          stacklevel=3)
+        r_used = int(info[_lib.INFO_LIFT_R])
+        hp, hind, hskel, hleft = to_host_many(p, ind, skel, left[:, :r_used].contiguous())
+        return hp, hind.astype(np.intp), hskel, hleft, right[:r_used], r_used
+
     def complete_other(self, x, r, k, kp):
         if r > 0:
             _lib.call("sp_gemm", 0, 0, x.shape[0], k - r, r, -1.0, x.data_ptr(), x.stride(0), kp.data_ptr(), k - r,
                       0.0, x[:, r:].data_ptr(), x.stride(0), self._s())
         return x
+
+
+def sharded_power_id(a_local, c_begin: int, cols, k: int, q: int, comm, ops, r=None):
+    """Rank-local part of the column-sharded single-pass power ID (SURVEY.md
+    8(e) item 5, the all-gather variant): the coarse column block C_i is
+    gathered locally and all-gathered (m x |I|, 4.2 GB at cfg5 -- small beside
+    the enrichment's two 2.1-TFLOP products that follow), then every rank runs
+    the selection on the same bytes with the same deterministic kernels, so
+    P, the pivots, the skeleton and the lifting's left factor V_r S_r^-1 come
+    out bitwise identical on every rank; the lifting's right factor U_r^T A_i
+    is this rank's column slab of U_r^T A (the lifting is column-sharded like
+    A).  BASELINE case s0 == A(:, I) (injection at the column set).
+
+    Returns (P m x k, indices k, skeleton k x |I|, left |I| x r, right_i
+    r x n_i, r) -- host arrays for the replicated parts, device for right_i
+    when ops is DeviceOps."""
+    cols = np.asarray(cols, dtype=np.int64)
+    m, n_i = a_local.shape
+    sel = (cols >= c_begin) & (cols < c_begin + n_i)
+    c_i = ops.gather(a_local, cols[sel] - c_begin)
+    c_all = comm.allgather_cols(c_i, ops)                 # m x |I|, global column order
+    return ops.power_id_local(a_local, c_all, cols, k, q, r)
 
 
 def shard_columns(n: int, world: int, rank: int, align: int = 1) -> tuple[int, int]:

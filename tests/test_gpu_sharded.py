@@ -12,7 +12,7 @@ import pytest
 import oracle
 import paper_2105_01271_b200 as sp
 from paper_2105_01271_b200.datagen import CONFIGS, generate_host
-from paper_2105_01271_b200.sharded import DeviceOps, TorchComm, shard_columns, sharded_power_svd
+from paper_2105_01271_b200.sharded import DeviceOps, TorchComm, shard_columns, sharded_power_id, sharded_power_svd
 
 pytestmark = pytest.mark.gpu
 
@@ -100,3 +100,50 @@ def test_two_shards_match_target(cuda):
     np.testing.assert_allclose(v.T @ v, np.eye(50), atol=1e-12)
     np.testing.assert_allclose(u.T @ u, np.eye(50), atol=1e-12)
     np.testing.assert_allclose((u * s) @ v.T, (tu * ts) @ tv.T, atol=1e-10 * np.abs(a).max())
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_sharded_power_id_matches_power_id(cuda, world):
+    # all-gather variant of the column-sharded ID: every shard selects on the
+    # same bytes (bitwise identical P, pivots, skeleton, left factor); the
+    # right factors U_r^T A_i assemble the single-GPU lifting
+    cfg, a, op, cols = _case()
+    k = 20
+    shared = {"slots": [None] * world, "bar": threading.Barrier(world)}
+    results = [None] * world
+    errors = []
+
+    def run(rank):
+        try:
+            cuda.cuda.set_device(0)
+            b, e = shard_columns(cfg.n, world, rank, align=cfg.grid[1])
+            ad = cuda.from_numpy(a[:, b:e].copy()).cuda()
+            comm = ThreadComm(rank, world, shared) if world > 1 else TorchComm()
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                results[rank] = (b,) + sharded_power_id(ad, b, cols, k, 1, comm, DeviceOps())
+        except Exception as exc:  # surface in the main thread
+            errors.append(exc)
+            shared["bar"].abort()
+
+    th = [threading.Thread(target=run, args=(rk,)) for rk in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errors, errors
+    for other in results[1:]:
+        for x, y in zip(results[0][1:5], other[1:5]):
+            assert np.array_equal(x, y)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        ref = sp.power_id(sp.ArraySnapshotStream(a), op, k, sp.PowerConfig(q=1, columns=cols))
+    _, p, ind, skel, left, _, r = results[0]
+    assert np.array_equal(ind, ref.indices)
+    np.testing.assert_allclose(p, ref.p, rtol=0, atol=1e-12 * np.abs(ref.p).max())
+    assert np.array_equal(skel, ref.skeleton)
+    assert r == ref.r
+    right = np.concatenate([res[5].cpu().numpy() for res in results], axis=1)
+    want = ref.lifting.dense()
+    got = left @ right
+    np.testing.assert_allclose(got, want, rtol=0, atol=1e-11 * np.abs(want).max())

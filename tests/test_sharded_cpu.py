@@ -166,6 +166,23 @@ class NumpyOps:
             q[:, r:] = -q[:, :r] @ kp.numpy()
         return x
 
+    def power_id_local(self, a_local, c_all, cols, k, q, r=None):
+        # the oracle's power_id algebra (src/power.py:252-308) on the gathered
+        # C (= the coarse sketch for an injection at the column set), with the
+        # lifting kept factored: left = V_r S_r^-1, right_i = U_r^T A_i
+        import oracle
+        c = c_all.numpy()
+        enriched = c.copy()
+        for _ in range(q):
+            enriched = c @ (c.T @ enriched)
+        picked = oracle.interp_rows(enriched, k)
+        u, sv, v = oracle.svd_thin(c)
+        rank = oracle.kept_rank(sv)
+        r_used = min(max(k, min(2 * k, rank)) if r is None else r, rank)
+        left = v[:, :r_used] / sv[:r_used]
+        right = self._t(u[:, :r_used].T @ a_local.numpy())
+        return picked.p, picked.indices, c[picked.indices].copy(), left, right, r_used
+
 
 def _field():
     from paper_2105_01271_b200.datagen import CONFIGS, coarse_grid_indices, generate_host
@@ -217,3 +234,55 @@ def test_sharded_matches_target(world):
     np.testing.assert_allclose(v.T @ v, np.eye(30), atol=1e-12)
     rec = (u * s) @ v.T
     np.testing.assert_allclose(rec, (tu * ts) @ tv.T, atol=1e-10 * np.abs(a).max())
+
+
+def _id_worker(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2105_01271_b200.sharded import TorchComm, shard_columns, sharded_power_id
+    cfg, a, cols = _field()
+    b, e = shard_columns(cfg.n, world, rank, align=cfg.grid[1])
+    p, ind, skel, left, right, r = sharded_power_id(torch.from_numpy(a[:, b:e].copy()), b, cols, 20, 1,
+                                                    TorchComm(), NumpyOps())
+    parts = [None] * world
+    dist.all_gather_object(parts, (b, p, ind, skel, left, right.numpy()))
+    if rank == 0:
+        out_q.put((parts, r))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_sharded_power_id_matches_single_process(world):
+    # the all-gather variant of the column-sharded ID:
+    # selection replicated bit-for-bit on every rank, the lifting's right
+    # factor column-sharded; against the single-process power_id algebra
+    import oracle
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_id_worker, args=(rk, world, port, q)) for rk in range(world)]
+    for p in procs:
+        p.start()
+    parts, r = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    parts = sorted(parts, key=lambda t: t[0])
+    for other in parts[1:]:  # replicated parts: identical bits on every rank
+        for x, y in zip(parts[0][1:5], other[1:5]):
+            assert np.array_equal(x, y)
+    cfg, a, cols = _field()
+    idx, w = cols[None, :], np.ones((1, cols.size))
+    ref = oracle.spc_power_id(a, idx, w, cols, 20, q=1)
+    _, pp, ind, skel, left, _ = parts[0]
+    assert np.array_equal(ind, ref.indices)
+    np.testing.assert_allclose(pp, ref.p, rtol=0, atol=1e-10 * np.abs(ref.p).max())
+    assert np.array_equal(skel, ref.skeleton)
+    assert r == ref.r
+    # lifting: left @ [right_0 | right_1 | ...] is (V_r S_r^-1)(U_r^T A), the
+    # exact-arithmetic value of the reference's build_lifting
+    right = np.concatenate([t[5] for t in parts], axis=1)
+    u, sv, v = oracle.svd_thin(a[:, cols])
+    want = (v[:, :r] / sv[:r]) @ (u[:, :r].T @ a)
+    np.testing.assert_allclose(left @ right, want, rtol=0, atol=1e-12 * np.abs(want).max())
