@@ -567,7 +567,7 @@ finish_core_kernel(int k, int nb2, const double* __restrict__ P2, const double* 
                    const double* __restrict__ R1ig, const double* __restrict__ Z, int64_t ldz,
                    const double* __restrict__ Y, int64_t ldy, double* __restrict__ S,
                    double* __restrict__ MfU, double* __restrict__ EtfU, double* __restrict__ MfV,
-                   double* __restrict__ EtfV, int* flag) {
+                   double* __restrict__ EtfV, int* flag, int* hflag) {
   SPB_PDL_ENTRY();
   extern __shared__ __align__(16) unsigned char fc_smem[];
   FcShared& sh = *reinterpret_cast<FcShared*>(fc_smem);
@@ -663,10 +663,22 @@ finish_core_kernel(int k, int nb2, const double* __restrict__ P2, const double* 
     }
   }
   __syncthreads();
+  // The call's status word: the last writer of `flag` publishes it to mapped
+  // pinned host memory (read by sp_deferred_status after the caller's sync)
+  // and rezeroes it for the next call -- no copy or memset node in the chain
   if (sh.bad) {
-    if (tid == 0) atomicOr(flag, 1);
+    if (tid == 0) {
+      atomicExch(flag, 0);
+      if (hflag) *(volatile int*)hflag = 1;
+      __threadfence_system();
+    }
     for (int j = tid; j < k; j += kFcThreads) S[j] = __longlong_as_double(0x7ff8000000000000ll);
     return;  // uniform
+  }
+  if (tid == 0) {
+    const int f = atomicExch(flag, 0);
+    if (hflag) *(volatile int*)hflag = f;
+    __threadfence_system();
   }
   SPB_TMARK(4);
   // (c) Bv = R2^{-1} Vs; Q1 top rows = Yt R1^{-1} (in place); XU = Zt Us
@@ -855,7 +867,7 @@ bool finish_fused_ok(int64_t m, int64_t n, int r, int k) {
 // OR-ed on a Cholesky breakdown / non-finite input.
 template <int R>
 static int finish_fused_r(int64_t m, int64_t n, const double* Z, int64_t ldz, const double* Y, int k, double* U,
-                          double* S, double* V, int* dflag, cudaStream_t s) {
+                          double* S, double* V, int* dflag, int* hflag, cudaStream_t s) {
   Arena ar(s);
   // staged Gram kernel: one CTA per SM; streaming kernel (R <= 8): up to 4 per SM
   const bool stream_gram = R <= 8;
@@ -892,7 +904,7 @@ static int finish_fused_r(int64_t m, int64_t n, const double* Z, int64_t ldz, co
     attr_dev = dev;
   }
   SPB_CUDA(launch_pdl((finish_core_kernel<R>), dim3(1), dim3(kFcThreads), fc_smem, s, k, nb, P2, R1, R1i, Z, ldz, Y, R, S, MfU, EtfU, MfV, EtfV,
-                                                       dflag));
+                                                       dflag, hflag));
   count_launch();
   SPB_CHECK_LAUNCH();
   const int bu = ceil_div(m, kFrRows), bv = ceil_div(n, kFrRows);
@@ -916,15 +928,16 @@ static int finish_fused_r(int64_t m, int64_t n, const double* Z, int64_t ldz, co
 }
 
 // Y (n x r, ld r) = A^T Z is in place; writes U (m x k), S (k), V (n x k).
-// dflag: device int[2] = {flag, ticket}, zeroed by the caller; the flag is
-// OR-ed on a Cholesky breakdown / non-finite input.
+// dflag: device int[2] = {flag, ticket}, zero on entry; the flag is OR-ed on
+// a Cholesky breakdown / non-finite input, published to *hflag (mapped pinned
+// host memory, may be null) by finish_core and left zero for the next call.
 int finish_fused(int64_t m, int64_t n, const double* Z, int64_t ldz, const double* Y, int r, int k, double* U,
-                 double* S, double* V, int* dflag, cudaStream_t s) {
+                 double* S, double* V, int* dflag, int* hflag, cudaStream_t s) {
   SPB_REQUIRE(finish_fused_ok(m, n, r, k), "finish_fused limits exceeded");
   switch (r) {
 #define SPB_FF(RR) \
   case RR:         \
-    return finish_fused_r<RR>(m, n, Z, ldz, Y, k, U, S, V, dflag, s);
+    return finish_fused_r<RR>(m, n, Z, ldz, Y, k, U, S, V, dflag, hflag, s);
     SPB_FF(1) SPB_FF(2) SPB_FF(3) SPB_FF(4) SPB_FF(5) SPB_FF(6) SPB_FF(7) SPB_FF(8)
     SPB_FF(9) SPB_FF(10) SPB_FF(11) SPB_FF(12) SPB_FF(13) SPB_FF(14) SPB_FF(15) SPB_FF(16)
 #undef SPB_FF

@@ -430,13 +430,19 @@ static int finish_words(cudaStream_t s, int** out) {
   return SP_OK;
 }
 
-static int defer_flag(const int* dflag, cudaStream_t s) {
+// The fused finish publishes its status word itself (finish_core writes the
+// mapped pinned word and rezeroes the device flag): get the device view of
+// the host word before the launches, record the completion event after them.
+static int defer_begin(int** hdev) {
   if (!t_def.host) {
-    SPB_CUDA(cudaMallocHost(&t_def.host, sizeof(int)));
+    SPB_CUDA(cudaHostAlloc(&t_def.host, sizeof(int), cudaHostAllocMapped));
     SPB_CUDA(cudaEventCreateWithFlags(&t_def.ev, cudaEventDisableTiming));
   }
   if (t_def.pending) SPB_CUDA(cudaEventSynchronize(t_def.ev));  // previous value is superseded
-  SPB_CUDA(cudaMemcpyAsync(t_def.host, dflag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SPB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(hdev), t_def.host, 0));
+  return SP_OK;
+}
+static int defer_end(cudaStream_t s) {
   SPB_CUDA(cudaEventRecord(t_def.ev, s));
   t_def.pending = true;
   return SP_OK;
@@ -455,7 +461,7 @@ void set_finish_mode(int mode) { t_finish_mode = mode; }
 
 bool finish_fused_ok(int64_t m, int64_t n, int r, int k);
 int finish_fused(int64_t m, int64_t n, const double* Z, int64_t ldz, const double* Y, int r, int k, double* U,
-                 double* S, double* V, int* dflag, cudaStream_t s);
+                 double* S, double* V, int* dflag, int* hflag, cudaStream_t s);
 
 // Given the kept left basis Z (m x r, ld ldz) of the sketch, one read of A:
 // Y = A^T Z, then the rank-k SVD of Z Z^T A written to U (m x k), S, V (n x k).
@@ -468,13 +474,14 @@ static int finish_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t 
     SPB_ALLOC(ar, double, Y, (size_t)n * r);
     int* dflag = nullptr;  // {flag, ticket}, zero on entry
     SPB_TRY(finish_words(s, &dflag));
+    int* hflag = nullptr;
+    SPB_TRY(defer_begin(&hflag));
     host_mark("finish: A pass launch");
     SPB_TRY(skinny_atz(A, a_dtype, m, n, lda, Z, ldz, r, Y, r, s));
     host_mark("finish: A pass launched");
-    SPB_TRY(finish_fused(m, n, Z, ldz, Y, r, k, U, S, V, dflag, s));
+    SPB_TRY(finish_fused(m, n, Z, ldz, Y, r, k, U, S, V, dflag, hflag, s));
     host_mark("finish: launched");
-    SPB_TRY(defer_flag(dflag, s));
-    SPB_CUDA(cudaMemsetAsync(dflag, 0, sizeof(int), s));  // after its read: ready for the next call
+    SPB_TRY(defer_end(s));  // finish_core published the flag and rezeroed dflag[0]
     return SP_OK;
   }
   SPB_CUDA(cudaMemsetAsync(S, 0, k * sizeof(double), s));
