@@ -256,3 +256,32 @@ def test_f32_file_stream(cuda, tmp_path):
     tu, ts, tv, r = oracle.projector_target_svd(a64, a64[:, idx], 20, 1)
     assert res.kept_rank == r
     np.testing.assert_allclose(res.s[:r], ts, rtol=0, atol=1e-12 * ts[0])
+
+
+def test_nonfinite_outside_sketch_is_reported_after_the_fused_finish(cuda):
+    # A NaN in a column the sketch never reads passes the sketch-side checks;
+    # the A pass carries it into Y, the fused finish's Gram tail raises its
+    # device flag, finish_core publishes it to mapped host memory, and the
+    # host-result API reads it (sp_deferred_status), re-runs with the
+    # Householder finish and reports the reference's NumericalError.  The
+    # next call on the same stream must start from a clean flag.
+    cfg = CONFIGS["cfg2"].scaled(m=200, grid=(32, 32), name="nan")
+    a = generate_host(cfg)
+    op, cols = sp.grid_injection(cfg.grid, cfg.stride)
+    off = np.setdiff1d(np.arange(cfg.n), cols)[7]
+    bad = a.copy()
+    bad[11, off] = np.nan
+    pc = sp.PowerConfig(q=1, columns=cols)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        with pytest.raises(sp.NumericalError):
+            sp.power_svd(sp.ArraySnapshotStream(bad), op, 10, pc)
+        res = sp.power_svd(sp.ArraySnapshotStream(a), op, 10, pc)
+        ref = sp.power_svd(sp.ArraySnapshotStream(a.copy()), op, 10, pc)
+    assert np.all(np.isfinite(res.s)) and np.array_equal(res.s, ref.s)
+    assert _lib_status() == 0
+
+
+def _lib_status():
+    from paper_2105_01271_b200 import _lib
+    return _lib.deferred_status()
