@@ -59,6 +59,9 @@ extern "C" {
 #define SP_INFO_RANK 4      /* ID: numerical rank of the coarse sketch (>=)   */
 #define SP_INFO_LIFT_R 5    /* ID: lifting rank actually used                 */
 #define SP_INFO_LAUNCHES 6  /* device kernels launched by the call            */
+#define SP_INFO_FUSED 7     /* 1: this call took the fused (deferred-status) finish:
+                               its breakdown / non-finite flag is read with
+                               sp_deferred_status after the caller's sync     */
 #define SP_INFO_LEN 8
 
 int sp_abi_version(void);

@@ -441,7 +441,13 @@ class OracleID:
 
 
 def pivot_gaps(x, k):
-    """Winner/runner-up residual-norm gap at each greedy step, relative to the
+    """Gaps only (see greedy_pivots_and_gaps)."""
+    return greedy_pivots_and_gaps(x, k)[1]
+
+
+def greedy_pivots_and_gaps(x, k):
+    """(pivots, gaps): the first k greedy pivots of src/kernels.py:114-140 and
+    the winner/runner-up residual-norm gap at each step, relative to the
     largest INITIAL column norm.
 
     Test helper for the pivot parity gate (SURVEY.md 8(c) gate 2): replays
@@ -477,7 +483,7 @@ def pivot_gaps(x, k):
         q[:, t] = v
         if t + 1 < cols:
             w[:, t + 1:] -= np.outer(v, v @ w[:, t + 1:])
-    return gaps
+    return perm[:k].copy(), gaps
 
 
 def interp_rows(x, k):

@@ -900,7 +900,8 @@ static int finish_fused_r(int64_t m, int64_t n, const double* Z, int64_t ldz, co
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
     SPB_CUDA(cudaFuncSetAttribute(finish_core_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    SPB_CUDA(cudaFuncSetAttribute(finish_rows_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+    // fr_smem below reaches ~118 KB at (R, k) = (16, 256): allow the opt-in maximum
+    SPB_CUDA(cudaFuncSetAttribute(finish_rows_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_dev = dev;
   }
   SPB_CUDA(launch_pdl((finish_core_kernel<R>), dim3(1), dim3(kFcThreads), fc_smem, s, k, nb, P2, R1, R1i, Z, ldz, Y, R, S, MfU, EtfU, MfV, EtfV,
@@ -910,7 +911,10 @@ static int finish_fused_r(int64_t m, int64_t n, const double* Z, int64_t ldz, co
   const int bu = ceil_div(m, kFrRows), bv = ceil_div(n, kFrRows);
   const size_t fr_smem =
       ((size_t)2 * R * k + R * R + (size_t)2 * kFrRows * R + (size_t)kFrRows * (R + 1)) * sizeof(double);
-  static int fr_occ = 0;  // persistent: as many CTAs as fit walk the tiles
+  // persistent: as many CTAs as fit walk the tiles (occupancy depends on k
+  // through fr_smem: cached per k)
+  static int fr_occ_k[257] = {0};
+  int& fr_occ = fr_occ_k[k];
   if (fr_occ == 0) {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fr_occ, finish_rows_kernel<R>, kFrThreads, fr_smem) !=
             cudaSuccess ||

@@ -177,8 +177,10 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
       return SP_ENUMERICAL;
     }
   }
-  if (p <= 64) {
+  // the exact SVD of X (size-general thin_svd: TSQR / blocked QR + Jacobi)
+  auto exact = [&]() -> int {
     out.b = (int)p;
+    out.iters = 0;
     out.U = ar.alloc<double>((size_t)rows * p);
     out.S = ar.alloc<double>((size_t)p);
     out.V = ar.alloc<double>((size_t)cols * p);
@@ -191,7 +193,20 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
     SPB_TRY(read_small(out.hs.data(), out.S, p * sizeof(double), s));
     out.kept = count_kept(out.hs, power);
     return SP_OK;
-  }
+  };
+  if (p <= 64) return exact();
+  auto exact_fallback = [&]() -> int {
+    if (pf.dev && pf.check_input) {  // the randomized path's input check already ran
+      PinnedReads rd(s);
+      SPB_TRY(read_flag_with(pf, hflag, rd));
+      SPB_TRY(rd.sync());
+      if (hflag) {
+        set_error(pf.msg);
+        return SP_ENUMERICAL;
+      }
+    }
+    return exact();
+  };
   const int cap = (int)std::min<int64_t>(p, 256);
   int b = std::min(cap, (std::max(32, want + 16) + 7) / 8 * 8);
   for (;;) {
@@ -241,7 +256,7 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
       if (copy_s) SPB_CUDA(cudaMemcpyAsync(oS, Sg, b * sizeof(double), cudaMemcpyDeviceToDevice, s));
       return SP_OK;
     };
-    bool spec = false;
+    bool spec = false, conv_seen = false;
     for (int itn = 0; itn < max_it; ++itn) {
       // Rayleigh-Ritz: Q^T X = Z^T with Z = X^T Q = P Rz  ->  Q^T X = Rz^T P^T
       // Z = P Rz: only Rz is needed unless V is wanted (R alone: Cholesky of
@@ -279,9 +294,14 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
       }
       iters = itn + 1;
       kept = count_kept(hs, power);
-      if (kept + 8 > b && b < cap && (need < 0 || kept < need + 8)) {
-        grow = true;
-        break;
+      if (kept + 8 > b && (need < 0 || kept < need + 8)) {
+        if (b < cap) {
+          grow = true;
+          break;
+        }
+        // the block cannot hold every kept direction plus oversampling: never
+        // return a truncated projector (the reference keeps its full QR basis)
+        return exact_fallback();
       }
       bool conv = false;
       // One Rayleigh-Ritz step already resolves the kept triplets to
@@ -310,7 +330,10 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
           if (std::fabs(hs[i] - prev[i]) > 1e-14 * hs[0] + 1e-12 * hs[i]) conv = false;
         }
       }
-      if (conv) break;
+      if (conv) {
+        conv_seen = true;
+        break;
+      }
       prev = hs;
       kept_prev = kept;
       // one more subspace iteration, started from the Ritz vectors:
@@ -344,6 +367,7 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
       b = std::min(cap, 2 * b);
       continue;
     }
+    if (!conv_seen) return exact_fallback();  // max_it exhausted without convergence
     if (!spec) SPB_TRY(final_products(false));  // oS was written by the publication
     out.b = b;
     out.kept = kept;
@@ -467,9 +491,11 @@ int finish_fused(int64_t m, int64_t n, const double* Z, int64_t ldz, const doubl
 // Y = A^T Z, then the rank-k SVD of Z Z^T A written to U (m x k), S, V (n x k).
 static int finish_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, const double* Z,
                       int64_t ldz, int r, int k, double* U, double* S, double* V, double kappa_est,
-                      cudaStream_t s) {
+                      cudaStream_t s, bool* fused) {
   Arena ar(s);
+  *fused = false;
   if (r > 0 && t_finish_mode == 0 && kappa_est < 1e6 && finish_fused_ok(m, n, r, k)) {
+    *fused = true;
     // A pass + fused shifted-CholeskyQR2 / Jacobi / completion: no host sync
     SPB_ALLOC(ar, double, Y, (size_t)n * r);
     int* dflag = nullptr;  // {flag, ticket}, zero on entry
@@ -494,29 +520,37 @@ static int finish_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t 
     SPB_ALLOC(ar, double, Vs, (size_t)r * r);
     SPB_ALLOC(ar, double, Sr, (size_t)r);
     SPB_TRY(skinny_atz(A, a_dtype, m, n, lda, Z, ldz, r, Y, r, s));     // the A pass
+    // A non-finite entry of A outside the sketch columns passes every
+    // sketch-side check and first shows up here, in Y = A^T Z; the reference
+    // raises it from thin_svd(projected) (src/kernels.py:87-91).  Raised as a
+    // device flag read together with the CholeskyQR2 breakdown flag (one read).
+    SPB_ALLOC(ar, int, yflag, 2);
+    SPB_CUDA(cudaMemsetAsync(yflag, 0, 2 * sizeof(int), s));
+    SPB_TRY(check_finite_async(n, r, Y, r, yflag, s));
     // kappa(Y) ~ the kept spectral range: CholeskyQR2 below 1e6 (breakdown is
     // checked once at the end, and the factorisation redone by Householder
     // TSQR if it happened), else Householder TSQR directly
     const bool chol = kappa_est < 1e6 && r <= 112 && t_finish_mode == 0;
     int* qflag = nullptr;
     if (chol) {
-      qflag = ar.alloc<int>(1);
-      if (!qflag) {
-        set_error("finish workspace allocation failed");
-        return SP_ECUDA;
-      }
-      SPB_CUDA(cudaMemsetAsync(qflag, 0, sizeof(int), s));
+      qflag = yflag + 1;
       SPB_TRY(cholqr2_async(n, r, Y, r, Qy, r, Ry, r, qflag, s));
     } else {
       SPB_TRY(tsqr(n, r, Y, r, Qy, r, Ry, r, s));
     }
+    bool y_checked = false;
   retry:
     SPB_TRY(jacobi_svd_tr(r, Ry, r, /*trans=*/true, Us, r, Sr, Vs, r, s));  // Ry^T = Us Sr Vs^T
-    if (qflag) {
-      int h = 0;
-      SPB_TRY(read_small(&h, qflag, sizeof(int), s));
-      qflag = nullptr;
-      if (h) {  // CholeskyQR2 broke down: Householder TSQR and redo the core
+    if (!y_checked) {
+      int h[2] = {0, 0};
+      SPB_TRY(read_small(h, yflag, 2 * sizeof(int), s));
+      y_checked = true;
+      if (h[0]) {
+        set_error("SVD input contains non-finite entries");
+        return SP_ENUMERICAL;
+      }
+      if (qflag && h[1]) {  // CholeskyQR2 broke down: Householder TSQR and redo the core
+        qflag = nullptr;
         SPB_TRY(tsqr(n, r, Y, r, Qy, r, Ry, r, s));
         goto retry;
       }
@@ -635,9 +669,11 @@ int single_pass_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t ld
   SPB_TRY(svd_top(s0, m, out_dim, out_dim, 1, 1.0, top, ar, s, pf));
   const int r = top.kept;
   const double kappa = (r > 0 && top.hs[r - 1] > 0.0) ? top.hs[0] / top.hs[r - 1] : INFINITY;
-  SPB_TRY(finish_svd(A, a_dtype, m, n, lda, top.U, top.b, r, k, U, S, V, kappa, s));
+  bool fused = false;
+  SPB_TRY(finish_svd(A, a_dtype, m, n, lda, top.U, top.b, r, k, U, S, V, kappa, s, &fused));
   const bool healthy = (m >= out_dim) && (r == out_dim);
   fill_info(info, r, healthy ? 0 : SP_WARN_RANK_DEFICIENT, top, l0);
+  if (info) info[SP_INFO_FUSED] = fused ? 1 : 0;
   return SP_OK;
 }
 
@@ -734,9 +770,11 @@ int power_svd(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, con
   }
   const int r = top.kept;
   const double kappa = (r > 0 && top.hs[r - 1] > 0.0) ? top.hs[0] / top.hs[r - 1] : INFINITY;
-  SPB_TRY(finish_svd(A, a_dtype, m, n, lda, top.U, top.b, r, k, U, S, V, kappa, s));
+  bool fused = false;
+  SPB_TRY(finish_svd(A, a_dtype, m, n, lda, top.U, top.b, r, k, U, S, V, kappa, s, &fused));
   const bool healthy = (m >= out_dim) && (r == out_dim);
   fill_info(info, r, healthy ? 0 : SP_WARN_RANK_DEFICIENT, top, l0);
+  if (info) info[SP_INFO_FUSED] = fused ? 1 : 0;
   return SP_OK;
 }
 

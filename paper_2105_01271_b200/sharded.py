@@ -82,6 +82,26 @@ SEED0 = 0x5EED5EED      # the range-finder seed of the device svd_top (csrc/pipe
 KEEP_TOL = 1e-12        # src/kernels.py:19
 
 
+def _validate_cols(cols, k: int, n_total=None) -> np.ndarray:
+    """The global column set I of the sharded drivers: the checks of
+    src/power.py:216-224 (range, size) and src/sketch.py:207-210 (distinct),
+    plus ascending order -- each rank gathers its own slab's columns in index
+    order, so an unsorted I would permute the all-gathered C (and the ID's
+    skeleton / lifting rows) relative to I."""
+    from .errors import ConfigError
+    cols = np.asarray(cols, dtype=np.int64).ravel()
+    if cols.size == 0 or cols.min() < 0 or (n_total is not None and cols.max() >= n_total):
+        raise ConfigError("column index set out of range")
+    if cols.size <= k:
+        raise ConfigError(f"column set size {cols.size} must exceed target rank {k}")
+    d = np.diff(cols)
+    if np.any(d == 0) or np.unique(cols).size != cols.size:
+        raise ConfigError("column indices must be distinct")
+    if np.any(d < 0):
+        raise ConfigError("the sharded drivers need an ascending column set")
+    return cols
+
+
 def _count_kept(hs, power):
     if hs.size == 0 or not hs[0] > 0:
         return 0
@@ -153,14 +173,15 @@ def distributed_sketch_basis(c_i, row0: int, ncols: int, power: float, comm, ops
         return ops.cols(u, 0, r), hs[:r], r
 
 
-def sharded_power_svd(a_local, c_begin: int, cols, k: int, q: int, comm, ops):
+def sharded_power_svd(a_local, c_begin: int, cols, k: int, q: int, comm, ops, n_total=None):
     """Rank-local part of the column-sharded single-pass power SVD.
 
     a_local: this rank's columns [c_begin, c_begin + n_i) of A (m x n_i).
     cols: the global, ascending column set I.  Returns (U m x k, S k, V_i
     n_i x k, kept_rank, rank_deficient_warning) with U, S replicated.
+    ``n_total`` (optional): the global column count, for the range check.
     """
-    cols = np.asarray(cols, dtype=np.int64)
+    cols = _validate_cols(cols, k, n_total)
     m, n_i = a_local.shape
     sel = (cols >= c_begin) & (cols < c_begin + n_i)
     c_i = ops.gather(a_local, cols[sel] - c_begin)
@@ -415,7 +436,7 @@ class DeviceOps:
         return x
 
 
-def sharded_power_id(a_local, c_begin: int, cols, k: int, q: int, comm, ops, r=None):
+def sharded_power_id(a_local, c_begin: int, cols, k: int, q: int, comm, ops, r=None, n_total=None):
     """Rank-local part of the column-sharded single-pass power ID (SURVEY.md
     8(e) item 5, the all-gather variant): the coarse column block C_i is
     gathered locally and all-gathered (m x |I|, 4.2 GB at cfg5 -- small beside
@@ -429,7 +450,7 @@ def sharded_power_id(a_local, c_begin: int, cols, k: int, q: int, comm, ops, r=N
     Returns (P m x k, indices k, skeleton k x |I|, left |I| x r, right_i
     r x n_i, r) -- host arrays for the replicated parts, device for right_i
     when ops is DeviceOps."""
-    cols = np.asarray(cols, dtype=np.int64)
+    cols = _validate_cols(cols, k, n_total)
     m, n_i = a_local.shape
     sel = (cols >= c_begin) & (cols < c_begin + n_i)
     c_i = ops.gather(a_local, cols[sel] - c_begin)

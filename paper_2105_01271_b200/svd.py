@@ -110,7 +110,9 @@ def _finish(u, s, v, k, method, info, host, warn_msg, rerun=None):
         warnings.warn(warn_msg, RankDeficiencyWarning, stacklevel=3)
     if host:
         u_h, s_h, v_h = to_host_many(u, s, v)
-        if _lib.deferred_status() and rerun is not None:
+        # only a call that took the fused finish has a deferred flag of its
+        # own (a stale flag of an earlier return_device call is never read)
+        if info[_lib.INFO_FUSED] and _lib.deferred_status() and rerun is not None:
             with _lib.householder_finish():
                 rerun()
             if not np.all(np.isfinite(s.cpu().numpy())):

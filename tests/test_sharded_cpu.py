@@ -286,3 +286,21 @@ def test_sharded_power_id_matches_single_process(world):
     u, sv, v = oracle.svd_thin(a[:, cols])
     want = (v[:, :r] / sv[:r]) @ (u[:, :r].T @ a)
     np.testing.assert_allclose(left @ right, want, rtol=0, atol=1e-12 * np.abs(want).max())
+
+
+def test_sharded_drivers_validate_the_column_set():
+    # out-of-range / repeated / unsorted I must raise, not be
+    # silently dropped or permuted by the per-shard gather
+    from paper_2105_01271_b200.errors import ConfigError
+    from paper_2105_01271_b200.sharded import sharded_power_id, sharded_power_svd
+
+    class _Comm:
+        rank, world = 0, 1
+
+    a = torch.from_numpy(np.random.default_rng(0).standard_normal((12, 40)))
+    for bad, msg in (([0, 5, 5, 9, 13], "distinct"), ([0, 9, 5, 13, 20], "ascending"),
+                     ([0, 5, 9, 13, 40], "out of range"), ([-1, 5, 9, 13, 20], "out of range"),
+                     ([0, 5], "exceed target rank")):
+        for fn in (sharded_power_svd, sharded_power_id):
+            with pytest.raises(ConfigError, match=msg):
+                fn(a, 0, bad, 2, 1, _Comm(), NumpyOps(), n_total=40)
