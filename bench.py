@@ -1,22 +1,28 @@
 #!/usr/bin/env python
-"""Benchmark: single-pass power-iteration SVD (SPC-SVD + C-PWR, q = 1) on the
-BASELINE cfg2 field (m = 2000 snapshots x n = 65536 = 256^2 dofs, FP64,
-coarse grid stride 4 -> 4096 columns, k = 50), one GPU per rank.
+"""Benchmark: single-pass power-iteration SVD (SPC-SVD + C-PWR) on a BASELINE
+heat field, one GPU per rank.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config cfg2] [--no-e2e] [--no-cpu]
+                  [--config cfg1..cfg5] [--no-e2e] [--no-cpu] [--no-extra]
+
+Default workload: BASELINE cfg4 -- the largest configuration that runs on one
+GPU (m = 10000 snapshots x n = 1024^2 dofs, FP64, 84 GB; coarse grid stride 8
+-> 16384 columns; power_svd q = 1, k = 200).
 
 Metric (BASELINE.json): GB/s of A streamed.  One "step" is one complete
-power_svd over the resident snapshot matrix (gather, sketch SVD, the A pass,
-final factorisation); value = |A| bytes x ranks / max-over-ranks step time.
-``e2e`` is the same metric through the public drop-in API from pinned host
-memory (host->device copy of A and device->host copy of U, S, V inside the
-timed region).  ``--impl reference`` times the CPU restatement of the
-reference algorithm (oracle/, the reference is pure Python + numpy) on a
-bounded sample with all host threads.
+power_svd over the resident snapshot matrix (gather + test block, sketch SVD,
+the A pass, final factorisation); value = |A| bytes / max-over-ranks step
+time.  ``e2e`` is the same metric through the public drop-in API from the
+caller's host array, page-locked in place (host->device copy of A and
+device->host copy of U, S, V inside the timed region).  ``roofline`` is the
+A pass (K2) against the measured HBM copy peak.  ``cpu_baseline`` /
+``--impl reference`` time the CPU restatement of the reference's one pass
+(oracle/, the reference is pure Python + numpy/OpenBLAS and cannot travel
+to the GPU box) on a bounded sample of the same configuration.
+``other_configs`` (N = 1) times cfg2, cfg3 (+ power_id) and cfg5 (+ power_id).
 
-Under torchrun (N > 1) every rank factorises its own snapshot matrix
-(independent datasets, weak scaling, no collective on the data path).
+Under torchrun (N > 1) the configuration's A is column-sharded by x-slabs of
+the grid (strong scaling); only sketch-sized blocks cross NVLink.
 """
 
 from __future__ import annotations
@@ -38,7 +44,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-from paper_2105_01271_b200.datagen import CONFIGS, mode_tables  # noqa: E402
+from paper_2105_01271_b200.datagen import CONFIGS  # noqa: E402
 
 METRIC = "GB/s of A streamed (end-to-end single-pass rank-k SVD)"
 UNIT = "GB/s"
@@ -149,59 +155,173 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def generate_device(cfg, torch, dev):
-    """BASELINE field on the device (input setup, outside every timed region):
-    A[i,(x,y)] = sum_p Sx[x,p] sum_q EC[i,(p,q)] Sy[y,q], FP64 GEMMs."""
-    S, lam, coef, _ = mode_tables(cfg)
-    t = np.linspace(0.0, 1.0, cfg.m)
-    ec = np.exp(-np.outer(t, lam) * np.pi ** 2 * cfg.nu) * coef[None, :]
-    P = cfg.modes
-    EC = torch.from_numpy(ec).to(dev).view(cfg.m, P, P)
-    Sx = torch.from_numpy(S[0]).to(dev)
-    Sy = torch.from_numpy(S[1]).to(dev)
-    T = torch.matmul(EC, Sy.t())                         # m x P(p) x gy
-    A = torch.matmul(Sx, T)                              # m x gx x gy
-    return A.reshape(cfg.m, cfg.n).contiguous()
+# ------------------------------------------------------------ workload ----
+def config_dict(cfg, world, cols_size):
+    """The workload description -- identical in both arms (ours / reference)."""
+    grid = "x".join(str(g) for g in cfg.grid)
+    call = "single_pass_svd" if cfg.q == 0 else f"power_svd single-pass q={cfg.q}"
+    return {"workload": f"{cfg.name}: {call}, k={cfg.k}, m={cfg.m}, n={cfg.n} ({grid} grid), "
+                        f"{'f64' if cfg.dtype == 'f64' else 'f32-stored, f64 accumulation'}, "
+                        f"coarse-grid stride {cfg.stride} -> n_c={cols_size}",
+            "config": cfg.name, "m": cfg.m, "n": cfg.n, "n_c": int(cols_size), "k": cfg.k, "q": cfg.q,
+            "a_bytes": cfg.a_bytes,
+            "l2": f"A ({cfg.a_bytes / 1e9:.1f} GB) >> L2 (126 MB): inputs larger than L2, no flush",
+            "parallelism": ("1 GPU" if world == 1 else
+                            f"A column-sharded by x-slabs of the grid over {world} GPUs (strong scaling: "
+                            f"the whole {cfg.name} matrix is split), NCCL allreduce / all-gather of "
+                            f"sketch-sized blocks only")}
 
 
-def sample_config(cfg):
-    """Bounded CPU sample of the workload: the first 1/8 of the grid rows
-    (an x-slab of the same field), same m, same stride, same k and q."""
-    gx, gy = cfg.grid
-    return cfg.scaled(grid=(max(cfg.stride * 4, gx // 8), gy), name=cfg.name + "-xslab")
+# ------------------------------------------------------------- CPU arm ----
+SAMPLE_ROWS = 256          # one block of the reference stream (src/svd.py:28 DEFAULT_BLOCK_ROWS)
+SAMPLE_SLAB = 16384        # hc rows in the sample (an x-slab of the grid: 16 grid rows at cfg4)
 
 
-def time_cpu_reference(cfg, steps, warmup, threads):
-    """Oracle (numpy restatement of the reference) on the bounded sample."""
+def cpu_sample(cfg):
+    """Bounded sample of the reference's one pass at this configuration:
+    one 256-row stream block, and of its contribution to hc = A^T C the rows
+    of one x-slab of the grid (SAMPLE_SLAB columns), against the FULL coarse
+    column set (n_c columns).  Work per byte of A equals the full pass's
+    (2 n_c flops per element), the finalize (which needs all of hc: 137 GB at
+    cfg4) is not included, so the CPU figure is an upper bound on the
+    reference's throughput."""
+    from paper_2105_01271_b200.datagen import coarse_grid_indices, generate_host_columns
+    idx = coarse_grid_indices(cfg.grid, cfg.stride)
+    slab = np.arange(min(SAMPLE_SLAB, cfg.n), dtype=np.int64)
+    need = np.union1d(slab, idx)
+    blk_cols = generate_host_columns(cfg, min(SAMPLE_ROWS, cfg.m), need)
+    # the block as the reference sees it: the full row would be n wide; only
+    # the slab and the coarse columns are ever read by the timed work, so the
+    # block is materialised on exactly those columns (positions remapped)
+    pos = {int(c): i for i, c in enumerate(need)}
+    idx_l = np.array([pos[int(c)] for c in idx], dtype=np.int64)
+    lo, hi = 0, slab.size                    # slab occupies the first columns of `need`
+    assert np.array_equal(need[:slab.size], slab)
+    blk = np.ascontiguousarray(blk_cols, dtype=np.float64)
+    desc = (f"one {blk.shape[0]}-row stream block x an x-slab of {slab.size} dofs of {cfg.name} "
+            f"against the full coarse set (n_c={idx.size}): s0 / C gathers + hc[slab] += blk[:, slab]^T C_blk "
+            f"(oracle.accumulate_block_slab = src/power.py:198-212 per block); finalize excluded")
+    return blk, idx_l, lo, hi, desc
+
+
+def time_cpu_sample(cfg, steps, warmup, threads):
     import oracle
     from threadpoolctl import threadpool_limits
-    from paper_2105_01271_b200.datagen import coarse_grid_indices, generate_host
-    sc = sample_config(cfg)
-    a = generate_host(sc)
-    idx = coarse_grid_indices(sc.grid, sc.stride)
-    w = np.ones((1, idx.size))
-    k = min(sc.k, idx.size - 1)
+    blk, idx_l, lo, hi, desc = cpu_sample(cfg)
+    w = np.ones((1, idx_l.size))
     times = []
     with threadpool_limits(threads), warnings.catch_warnings():
         warnings.simplefilter("ignore")
         for i in range(warmup + steps):
             t0 = time.perf_counter()
-            if sc.q == 0:
-                oracle.spc_svd(a, idx[None, :], w, k)
-            else:
-                oracle.spc_power_svd(a, idx[None, :], w, idx, k, q=sc.q)
+            oracle.accumulate_block_slab(blk, idx_l[None, :], w, idx_l, lo, hi)
             dt = time.perf_counter() - t0
             if i >= warmup:
                 times.append(dt)
     sec = statistics.mean(times)
-    return {"value": a.nbytes / sec / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{sc.m}x{sc.n} x-slab ({sc.grid[0]}x{sc.grid[1]} grid) of {cfg.name}, "
-                      f"n_c={idx.size}, k={k}, q={sc.q}; oracle/ numpy restatement, "
-                      f"{threads} BLAS thread(s), mean of {steps} after {warmup} warm-up",
-            "sec_per_step": sec}
+    nbytes = blk.shape[0] * (hi - lo) * 8
+    return {"value": nbytes / sec / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": desc + f"; {threads} BLAS thread(s), mean of {steps} after {warmup} warm-up",
+            "sec_per_step": sec, "sample_bytes": nbytes}
+
+
+def host_info():
+    info = {"cpu_model": None, "blas": None, "host_threads": len(os.sched_getaffinity(0))}
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                info["cpu_model"] = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        from threadpoolctl import threadpool_info
+        b = [f"{d.get('internal_api')} {d.get('version')} ({d.get('architecture')})" for d in threadpool_info()
+             if d.get("user_api") == "blas"]
+        info["blas"] = b[0] if b else None
+    except Exception:
+        pass
+    return info
+
+
+def cpu_baseline(cfg, steps):
+    """All host threads (the reported baseline) and one thread (for scale)."""
+    allt = time_cpu_sample(cfg, steps=steps, warmup=1, threads=len(os.sched_getaffinity(0)))
+    one = time_cpu_sample(cfg, steps=1, warmup=0, threads=1)
+    out = {k: allt[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    out.update(single_thread={"value": one["value"], "cores": 1, "sec_per_step": one["sec_per_step"]},
+               sec_per_step=allt["sec_per_step"], **host_info())
+    return out
 
 
 # ------------------------------------------------------------ our arm ----
+def _gen_shard(cfg, rank, world, dev):
+    """This rank's x-slab of A (the whole A at world 1) and its first column."""
+    import torch
+    from paper_2105_01271_b200.datagen import generate_device
+    from paper_2105_01271_b200.sharded import shard_columns
+    if world == 1:
+        return generate_device(cfg, dev), 0
+    rest = int(np.prod(cfg.grid[1:]))
+    b, e = shard_columns(cfg.grid[0], world, rank)
+    if cfg.noise_std:  # noise is drawn row-major over the whole field: generate, keep the slab
+        full = generate_device(cfg, dev)
+        a = full[:, b * rest:e * rest].contiguous()
+        del full
+        torch.cuda.empty_cache()
+        return a, b * rest
+    return generate_device(cfg, dev, x_range=(b, e)), b * rest
+
+
+def _events_ms(fn, reps, torch):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        out = fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps, out
+
+
+def extra_configs(names, dev, torch):
+    """Other BASELINE configurations on this GPU (N = 1): device-resident
+    power_svd (and power_id where the config names it), CUDA-event timed."""
+    import paper_2105_01271_b200 as sp
+    from paper_2105_01271_b200.datagen import generate_device
+    out = {}
+    for name in names:
+        cfg = CONFIGS[name]
+        A = generate_device(cfg, dev)
+        op, cols = sp.grid_injection(cfg.grid, cfg.stride)
+        pc = sp.PowerConfig(q=cfg.q, columns=cols)
+
+        def svd():
+            if cfg.q == 0:
+                return sp.single_pass_svd(sp.DeviceSnapshotStream(A), op, cfg.k, return_device=True)
+            return sp.power_svd(sp.DeviceSnapshotStream(A), op, cfg.k, pc, return_device=True)
+        for _ in range(3):
+            res = svd()
+        ms, res = _events_ms(svd, 10, torch)
+        rec = {"call": "power_svd" if cfg.q else "single_pass_svd", "ms": ms, "GBps_A": cfg.a_bytes / ms / 1e6,
+               "kept_rank": int(res.kept_rank), "m": cfg.m, "n": cfg.n, "n_c": int(cols.size), "k": cfg.k,
+               "dtype": cfg.dtype}
+        del res
+        if name in ("cfg3", "cfg5"):
+            def pid():
+                return sp.power_id(sp.DeviceSnapshotStream(A), op, cfg.k, pc, return_device=True)
+            f = pid()
+            del f
+            ms_id, f = _events_ms(pid, 2, torch)
+            rec["power_id"] = {"ms": ms_id, "k": cfg.k, "lift_r": int(f.r)}
+            del f
+        out[name] = rec
+        del A
+        gc.collect()
+        torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -213,24 +333,17 @@ def run_ours(args):
     import paper_2105_01271_b200 as sp
     from paper_2105_01271_b200 import _lib
     from paper_2105_01271_b200.datagen import coarse_grid_indices
-    from paper_2105_01271_b200.datagen import generate_device as gen_dev
     from paper_2105_01271_b200.sharded import DeviceOps, TorchComm, sharded_power_svd
     cfg = CONFIGS[args.config]
     k = cfg.k
-    if world == 1:
-        A = gen_dev(cfg, dev)
-        op, cols = sp.grid_injection(cfg.grid, cfg.stride)
-        pc = sp.PowerConfig(q=cfg.q, columns=cols)
-    else:
-        # weak scaling of the column-sharded algorithm: rank i owns the x-slab
-        # [i*gx, (i+1)*gx) of a (world*gx) x gy grid -- the cfg2 slab per GPU
-        gx = cfg.grid[0]
-        gcfg = cfg.scaled(grid=(gx * world,) + tuple(cfg.grid[1:]), name=f"{cfg.name}-x{world}")
-        A = gen_dev(gcfg, dev, x_range=(rank * gx, (rank + 1) * gx))
-        cols = coarse_grid_indices(gcfg.grid, gcfg.stride)
-        comm, dops = TorchComm(), DeviceOps()
+    A, c_begin = _gen_shard(cfg, rank, world, dev)
+    torch.cuda.synchronize()
+    op, cols = sp.grid_injection(cfg.grid, cfg.stride)
+    pc = sp.PowerConfig(q=cfg.q, columns=cols)
+    cols_g = coarse_grid_indices(cfg.grid, cfg.stride)
+    comm, dops = (TorchComm(), DeviceOps()) if world > 1 else (None, None)
     n_local = A.shape[1]
-    a_bytes = A.numel() * A.element_size()
+    a_bytes_local = A.numel() * A.element_size()
 
     class _Res:
         def __init__(self, u, r):
@@ -238,7 +351,7 @@ def run_ours(args):
 
     def step():
         if world > 1:
-            u, s_, v, r_, _ = sharded_power_svd(A, rank * n_local, cols, k, cfg.q, comm, dops)
+            u, s_, v, r_, _ = sharded_power_svd(A, c_begin, cols_g, k, cfg.q, comm, dops, n_total=cfg.n)
             return _Res(u, r_)
         stream = sp.DeviceSnapshotStream(A)
         if cfg.q == 0:
@@ -250,12 +363,11 @@ def run_ours(args):
             dist.barrier()
 
     warnings.simplefilter("ignore")
-    # like timeit: no cyclic-GC pass (tens of ms on an interpreter holding torch)
-    # inside the timed loop; collected once here, re-enabled after
+    # like timeit: no cyclic-GC pass inside the timed loop
     gc.collect()
     gc.disable()
-    # W warm-up steps, continued until ~0.3 s of work has run so the clocks
-    # and the allocator pools are at steady state when the timed loop starts
+    # W warm-up steps, continued until ~0.3 s of work has run (clocks and
+    # allocator pools at steady state when the timed loop starts)
     t_w = time.perf_counter()
     done = 0
     while done < args.warmup or time.perf_counter() - t_w < 0.3:
@@ -284,23 +396,22 @@ def run_ours(args):
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = a_bytes * world / (ms * 1e-3) / 1e9
+    value = cfg.a_bytes / (ms * 1e-3) / 1e9     # the whole matrix, over all ranks
 
     # ---- dominant kernel: the A pass (K2) on the launching stream
     r = int(res.kept_rank)
     Z = res.u[:, :max(r, 1)].contiguous()
     Y = torch.empty((n_local, max(r, 1)), dtype=torch.float64, device=dev)
     s = torch.cuda.current_stream()
+    tag = _lib.SP_F64 if A.dtype == torch.float64 else _lib.SP_F32
 
     def apass():
-        _lib.call("sp_skinny_atz", A.data_ptr(), _lib.SP_F64, cfg.m, n_local, n_local, Z.data_ptr(), Z.shape[1],
+        _lib.call("sp_skinny_atz", A.data_ptr(), tag, cfg.m, n_local, n_local, Z.data_ptr(), Z.shape[1],
                   Z.shape[1], Y.data_ptr(), Z.shape[1], s.cuda_stream)
     for _ in range(3):
         apass()
-    # A (1.05 GB at cfg2) is 8x the 126 MB L2 and K2 streams it in the same
-    # order every launch, so nothing of it survives in L2 between launches:
-    # no flush (a write flush would leave 256 MB of dirty lines for the next
-    # launch to write back, charging K2 for traffic that is not its own)
+    # A is far larger than the 126 MB L2 and K2 streams it in the same order
+    # every launch, so nothing of it survives in L2 between launches (no flush)
     durs = []
     for _ in range(10):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -310,24 +421,39 @@ def run_ours(args):
         torch.cuda.synchronize()
         durs.append(e0.elapsed_time(e1))
     apass_ms = statistics.median(durs)
-    algo_bytes = a_bytes + cfg.m * Z.shape[1] * 8 + n_local * Z.shape[1] * 8
+    algo_bytes = a_bytes_local + cfg.m * Z.shape[1] * 8 + n_local * Z.shape[1] * 8
     achieved = algo_bytes / (apass_ms * 1e-3) / 1e9
     peak, peak_kind = peaks()
     traffic = None
     tp = ROOT / "profiles" / "apass_traffic.json"
     if tp.exists():
         try:
-            traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
+            tj = json.loads(tp.read_text())
+            if tj.get("config") == cfg.name:
+                traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+    del Y, Z, res
+
+    # ---- CPU baseline sample (rank 0, N = 1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(cfg, steps=3)
 
     # ---- e2e through the public API from pinned host memory
     e2e = None
-    if not args.no_e2e:
-        host = torch.empty((cfg.m, n_local), dtype=torch.float64, pin_memory=True)
-        host.copy_(A)
-        hv = host.numpy()
+    if not args.no_e2e and (cfg.dtype == "f64" or world > 1):
+        host = np.empty((cfg.m, n_local), dtype=np.float64 if cfg.dtype == "f64" else np.float32)
+        ht = torch.from_numpy(host)
+        # page-lock the caller's array in place (torch's pinned allocator would
+        # round an 84 GB request up to a power of two)
+        rc = torch.cuda.cudart().cudaHostRegister(ht.data_ptr(), ht.numel() * ht.element_size(), 0)
+        pinned = int(rc) == 0
+        ht.copy_(A)
         torch.cuda.synchronize()
+        del A
+        gc.collect()
+        torch.cuda.empty_cache()
 
         class _Out:
             def __init__(self, u, s_, v):
@@ -337,29 +463,25 @@ def run_ours(args):
             if world > 1:
                 # H2D of this rank's slab, the sharded pipeline, D2H of U, S, V_i
                 from paper_2105_01271_b200.device import to_host_many
-                ad = torch.empty((cfg.m, n_local), dtype=torch.float64, device=dev)
-                ad.copy_(host, non_blocking=True)
-                u, s_, v, _, _ = sharded_power_svd(ad, rank * n_local, cols, k, cfg.q, comm, dops)
+                ad = torch.empty((cfg.m, n_local), dtype=ht.dtype, device=dev)
+                ad.copy_(ht, non_blocking=True)
+                u, s_, v, _, _ = sharded_power_svd(ad, c_begin, cols_g, k, cfg.q, comm, dops, n_total=cfg.n)
                 hu, hvv = to_host_many(u, v)
                 return _Out(hu, s_, hvv)
-            stream = sp.ArraySnapshotStream(hv)
+            stream = sp.ArraySnapshotStream(host)
             if cfg.q == 0:
-                out = sp.single_pass_svd(stream, op, k)
-            else:
-                out = sp.power_svd(stream, op, k, pc)
-            return out
-        # warm-up: two live result sets, so the pinned staging buffers of the
-        # D2H copies are in torch's host caching allocator (steady state)
+                return sp.single_pass_svd(stream, op, k)
+            return sp.power_svd(stream, op, k, pc)
         out = e2e_step()
-        out = e2e_step()
-        d2h = out.u.nbytes + out.s.nbytes + out.v.nbytes
+        d2h = out.u.nbytes + np.asarray(out.s).nbytes + out.v.nbytes
+        del out
         torch.cuda.synchronize()
         barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         gc.collect()
         gc.disable()
+        n_e2e = max(1, min(args.steps, 3))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        n_e2e = max(1, min(args.steps, 5))
         for _ in range(n_e2e):
             out = e2e_step()
         e1.record()
@@ -370,37 +492,41 @@ def run_ours(args):
             t = torch.tensor([e_ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
-        e2e = {"value": a_bytes * world / (e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": a_bytes,
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms}
+        e2e = {"value": cfg.a_bytes / (e_ms * 1e-3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": cfg.a_bytes, "d2h_bytes_per_step": int(d2h) * world, "ms_per_step": e_ms,
+               "steps": n_e2e, "host_buffer": "caller's numpy array, page-locked in place" if pinned else "pageable"}
+        del out
+        if pinned:
+            torch.cuda.cudart().cudaHostUnregister(ht.data_ptr())
+        del ht, host
+    else:
+        del A
+    gc.collect()
+    torch.cuda.empty_cache()
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = time_cpu_reference(cfg, steps=1, warmup=1, threads=1)
+    extra = None
+    if rank == 0 and world == 1 and not args.no_extra:
+        names = [c for c in ("cfg2", "cfg3", "cfg5") if c != cfg.name]
+        extra = extra_configs(names, dev, torch)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE cfg2 heat field, seed 1)",
-            "config": {"workload": f"{cfg.name}: power_svd single-pass q={cfg.q}, k={k}, m={cfg.m}, "
-                                   f"n={cfg.n} ({cfg.grid[0]}x{cfg.grid[1]}), stride {cfg.stride} "
-                                   f"-> n_c={cols.size}",
-                       "a_bytes": a_bytes, "l2": "A (1.05 GB) > L2 (126 MB): inputs larger than L2",
-                       "warmup_steps_run": warm_done,
-                       "kept_rank": r,
-                       "parallelism": ("1 GPU" if world == 1 else
-                                       f"column-sharded over {world} GPUs (NCCL all-gather of C and the "
-                                       f"r x r TSQR factors), one {cfg.grid[0]}x{cfg.grid[1]} x-slab per GPU "
-                                       f"(weak): global grid {cfg.grid[0] * world}x{cfg.grid[1]}")},
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": cfg.dtype,
+            "data": f"synthetic (BASELINE {cfg.name} heat field, seed {cfg.seed}, generated on device)",
+            "config": dict(config_dict(cfg, world, cols.size), warmup_steps_run=warm_done, kept_rank=r),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "kernel": "skinny_tma_kernel (K2, Y = A^T U_r, TMA bulk-copy pass)",
-                         "launch_ms": apass_ms,
-                         "algorithmic_bytes_per_launch": algo_bytes},
+                         "launch_ms": apass_ms, "algorithmic_bytes_per_launch": algo_bytes,
+                         "step_frac_of_peak": value / world / peak},
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
+            "other_configs": extra,
         }
         print(json.dumps(line))
     if world > 1:
@@ -412,15 +538,18 @@ def run_reference(args):
     if rank != 0:
         return
     cfg = CONFIGS[args.config]
+    from paper_2105_01271_b200.datagen import coarse_grid_indices
     threads = len(os.sched_getaffinity(0))
-    res = time_cpu_reference(cfg, steps=args.steps, warmup=min(args.warmup, 1), threads=threads)
+    res = time_cpu_sample(cfg, steps=args.steps, warmup=min(args.warmup, 1), threads=threads)
+    n_c = coarse_grid_indices(cfg.grid, cfg.stride).size
     line = {
         "impl": "reference", "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["sec_per_step"] * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (BASELINE cfg2 heat field, seed 1), bounded x-slab sample",
-        "config": {"workload": f"{cfg.name} sample: {res['sample']}"},
-        "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+        "dtype": cfg.dtype,
+        "data": f"synthetic (BASELINE {cfg.name} heat field, seed {cfg.seed}), bounded sample on the host",
+        "config": config_dict(cfg, world, n_c),
+        "cpu_baseline": dict({k: res[k] for k in ("value", "unit", "cores", "kind", "sample")}, **host_info()),
         "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -432,9 +561,10 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2"])
+    ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extra", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -120,6 +120,18 @@ int sp_gemm(int32_t trans_a, int32_t trans_b, int64_t M, int64_t N, int64_t K, d
             const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
             double* C, int64_t ldc, void* stream);
 
+/* --------------------------------------------------------------- K3x -----
+ * C_hi (+ C_lo) = op(A) (B_hi + B_lo), nearly exactly rounded: Ozaki slices of
+ * A's rows and B's columns, every level sum an exact DMMA GEMM, levels summed
+ * in double-double (error below ~2^-56 of sum_l |a_il||b_lj|).  op(A) = A
+ * (trans_a = 0, M x K) or A^T (A is K x M); B is K x N; B_lo and C_lo may be
+ * NULL.  The enrichment E = C (C^T s0) of power_id (src/power.py:282-285),
+ * whose greedy pivots are decided by ulp-level residual differences.
+ */
+int sp_gemm_exact(int32_t trans_a, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                  const double* B_hi, const double* B_lo, int64_t ldb, double* C_hi, double* C_lo,
+                  int64_t ldc, void* stream);
+
 /* ---------------------------------------------------------------- K4 -----
  * Householder QR of a tall matrix X (rows x cols, rows >= cols): explicit
  * Q (rows x cols) and R (cols x cols).  cols <= 32 runs as a register-resident

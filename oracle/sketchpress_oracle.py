@@ -291,6 +291,21 @@ def one_pass_power(a, idx, w, cols, block_rows=BLOCK, coarse_gram=False,
     return s0, c, coarse, gram, hc
 
 
+def accumulate_block_slab(blk, idx, w, cols, lo, hi):
+    """One stream block of src/power.py:198-212 (the loop body of
+    _power_accumulate, with_column_gram=True) restricted to the rows
+    [lo, hi) of hc: s0 and C rows of the block and this block's contribution
+    blk[:, lo:hi]^T C_blk to hc[lo:hi].  The block's work on every other hc
+    row slab is identical in kind and independent, so timing one (block,
+    slab) pair times a known fraction of the reference's accumulate pass --
+    the CPU-baseline sample of bench.py at configurations whose full hc
+    (n x |I|, 137 GB at cfg4) cannot be held."""
+    piece = sketch_rows(blk, idx, w)
+    sub = take_columns(blk, cols)
+    hc_slab = blk[:, lo:hi].T @ sub
+    return piece, sub, hc_slab
+
+
 # ----------------------------------------------------------------------------
 # single-pass SVD (src/svd.py:146-189)
 # ----------------------------------------------------------------------------

@@ -44,6 +44,7 @@ SIGNATURES = {
     "sp_check_columns": [_P, _I64, _I64, _P],
     "sp_skinny_atz": [_P, _I32, _I64, _I64, _I64, _P, _I64, _I32, _P, _I64, _P],
     "sp_gemm": [_I32, _I32, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64, _P],
+    "sp_gemm_exact": [_I32, _I64, _I64, _I64, _P, _I64, _P, _P, _I64, _P, _P, _I64, _P],
     "sp_tsqr": [_I64, _I64, _P, _I64, _P, _I64, _P, _I64, _P],
     "sp_qr_tall": [_I64, _I64, _P, _I64, _P, _I64, _P, _I64, _I32, _P],
     "sp_cholqr2_async": [_I64, _I64, _P, _I64, _P, _I64, _P, _I64, _P, _P],

@@ -90,6 +90,12 @@ int sp_gemm(int32_t trans_a, int32_t trans_b, int64_t M, int64_t N, int64_t K, d
   return gemm(trans_a, trans_b, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ST(stream));
 }
 
+int sp_gemm_exact(int32_t trans_a, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                  const double* B_hi, const double* B_lo, int64_t ldb, double* C_hi, double* C_lo,
+                  int64_t ldc, void* stream) {
+  return gemm_exact(trans_a, M, N, K, A, lda, B_hi, B_lo, ldb, C_hi, C_lo, ldc, ST(stream));
+}
+
 int sp_tsqr(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq, double* R,
             int64_t ldr, void* stream) {
   return tsqr(rows, cols, X, ldx, Q, ldq, R, ldr, ST(stream));

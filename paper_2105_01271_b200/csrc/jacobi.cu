@@ -381,11 +381,14 @@ jacobi32_kernel(int n, const double* __restrict__ M, int64_t ldm, double* __rest
   }
 }
 
-// ------------------------------------------------- 112 < n <= 256, grid ----
+// ------------------------------------------------------- n > 112, grid ----
 // W and V (column-major, n_p x n_p) do not fit in one SM's shared memory, so
 // the rounds are spread over a cooperative grid: one warp per column pair
-// (n_p / 2 pairs <= 128 warps), W / V in global memory (L2-resident, 1 MB),
-// one grid barrier per round.  Every CTA derives the same active-column list
+// (n_p / 2 pairs), W / V in global memory (L2-resident up to n ~ 2500), one
+// grid barrier per round.  Used for the sketch cores (n <= 256) and for the
+// size-general thin_svd of the drop-in (n up to the sketch widths, 16384);
+// columns below 1e-15 ||M||_F never enter the schedule, so a numerically
+// low-rank M (the BASELINE sketches) costs rounds only for its rank.  Every CTA derives the same active-column list
 // from the same column norms; rotations, convergence test and sorting are
 // those of the single-CTA kernel.
 constexpr int kJgThreads = 128;
@@ -395,7 +398,7 @@ jacobi_grid_kernel(int n, int np, const double* __restrict__ M, int64_t ldm, boo
                    int64_t ldu, double* __restrict__ S, double* __restrict__ Vout, int64_t ldv,
                    double* __restrict__ W, double* __restrict__ Vm, double* __restrict__ cn, int* rot) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ int act[256];
+  extern __shared__ int act[];  // np entries (dynamic: n is not capped at 256)
   __shared__ int na_s;
   const int lane = threadIdx.x & 31;
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -514,7 +517,7 @@ int jacobi_svd(int64_t n, const double* M, int64_t ldm, double* U, int64_t ldu, 
 // transposed in place; larger n transposes into scratch first)
 int jacobi_svd_tr(int64_t n, const double* M, int64_t ldm, bool trans, double* U, int64_t ldu, double* S,
                   double* V, int64_t ldv, cudaStream_t s) {
-  SPB_REQUIRE(n >= 1 && n <= 256, "Jacobi SVD supports 1 <= n <= 256");
+  SPB_REQUIRE(n >= 1 && n <= 50000, "Jacobi SVD supports 1 <= n <= 50000");
   if (n <= 8) {
     SPB_CUDA(launch_pdl((jacobi32_kernel<1, 8>), dim3(1), dim3(32), 0, s, (int)n, M, ldm, U, ldu, S, V, ldv, trans));
     count_launch();
@@ -563,13 +566,17 @@ int jacobi_svd_tr(int64_t n, const double* M, int64_t ldm, bool trans, double* U
     }
     const int warps = np / 2;
     int grid = ceil_div(warps * 32, kJgThreads);
+    const size_t act_smem = (size_t)np * sizeof(int);
+    if (act_smem > 48 * 1024)
+      SPB_CUDA(cudaFuncSetAttribute(jacobi_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)act_smem));
     int per_sm = 0;
-    SPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_grid_kernel, kJgThreads, 0));
+    SPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_grid_kernel, kJgThreads, act_smem));
     grid = std::max(1, std::min(grid, per_sm * kNumSMs));
     int n_i = (int)n, np_i = np;
     bool tr = false;  // M was transposed into scratch above when trans
     void* args[] = {&n_i, &np_i, &M, &ldm, &tr, &U, &ldu, &S, &V, &ldv, &gW, &gV, &cn, &rot};
-    SPB_CUDA(cudaLaunchCooperativeKernel((const void*)jacobi_grid_kernel, dim3(grid), dim3(kJgThreads), args, 0, s));
+    SPB_CUDA(cudaLaunchCooperativeKernel((const void*)jacobi_grid_kernel, dim3(grid), dim3(kJgThreads), args, act_smem,
+                                         s));
     count_launch();
     return SP_OK;
   }

@@ -1,6 +1,9 @@
 // Small dense helpers of the path: sign convention, pseudo-inverse
 // reciprocals, triangular solve, transposes, random blocks, thin QR / SVD
 // drivers, streamed residual norm.
+#include <cmath>
+#include <vector>
+
 #include "common.cuh"
 #include "launch_count.cuh"
 #include "ops.cuh"
@@ -287,13 +290,50 @@ int trsm_upper(int64_t k, const double* R, int64_t ldr, int64_t ncols, const dou
 }
 
 // -------------------------------------------------------- thin QR / SVD ----
+// Sketch-sized cores (p <= 256) keep the round-1 path; wider inputs (the
+// drop-in thin_qr / thin_svd on whole sketches: 2000 x 4096 ... 10000 x 16384)
+// take the size-general one below.
+constexpr int64_t kSmallCore = 256;
+
+// out (N x k, ld ldo): columns [0, r) orthonormal; columns [r, k) receive an
+// orthonormal completion (Householder reconstruction when small, else the
+// Q factor of [out_r | uniform] by the panel TSQR).
+int complete_basis(int64_t N, int r, int k, double* out, int64_t ldo, uint64_t seed, cudaStream_t s) {
+  if (r >= k) return SP_OK;
+  if (householder_complete(N, r, k, out, ldo, s) == SP_OK) return SP_OK;
+  Arena ar(s);
+  SPB_ALLOC(ar, double, W, (size_t)N * k);
+  SPB_ALLOC(ar, double, Qc, (size_t)N * k);
+  SPB_ALLOC(ar, double, Rc, (size_t)k * k);
+  if (r > 0) SPB_TRY(copy2d(N, r, out, ldo, W, k, s));
+  SPB_TRY(fill_uniform(N, k - r, W + r, k, seed, s));
+  SPB_TRY(tsqr(N, k, W, k, Qc, k, Rc, k, s));
+  SPB_TRY(copy2d(N, k - r, Qc + r, k, out + r, ldo, s));
+  return SP_OK;
+}
+
+// The one-sided Jacobi leaves the columns it never rotated (norm below
+// 1e-15 ||M||_F, i.e. S_i ~ 0) unnormalised and not orthogonal to the rest:
+// replace the left factor's columns past the last S_i > 1e-15 ||S||_2-sum by
+// an orthonormal completion (the reference's gesdd returns a full orthonormal
+// U for a rank-deficient input).  Synchronises (reads S).
+static int complete_null_columns(int64_t p, const double* S, double* Ucols, int64_t ldu, cudaStream_t s) {
+  std::vector<double> hs((size_t)p);
+  SPB_TRY(read_small(hs.data(), S, p * sizeof(double), s));
+  double fro2 = 0.0;
+  for (double x : hs) fro2 += x * x;
+  const double thr = 1e-15 * std::sqrt(fro2);
+  int64_t r = 0;
+  while (r < p && hs[r] > thr) ++r;
+  return complete_basis(p, (int)r, (int)p, Ucols, ldu, 0x5eedC0DEull, s);
+}
+
 // src/kernels.py:74-84 thin_qr: Q rows x p, R p x cols, p = min(rows, cols)
 int thin_qr(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq,
             double* R, int64_t ldr, cudaStream_t s) {
   SPB_REQUIRE(rows >= 1 && cols >= 1, "thin_qr needs a non-empty matrix");
-  const int64_t p = std::min(rows, cols);
-  SPB_REQUIRE(p <= 256, "thin_qr supports min(rows, cols) <= 256");
   SPB_TRY(check_finite(rows, cols, X, ldx, "QR input contains non-finite entries", s));
+  const int64_t p = std::min(rows, cols);
   if (rows >= cols) {
     SPB_TRY(tsqr(rows, cols, X, ldx, Q, ldq, R, ldr, s));
   } else {
@@ -310,7 +350,6 @@ int thin_svd(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* U
              double* S, double* V, int64_t ldv, cudaStream_t s) {
   SPB_REQUIRE(rows >= 1 && cols >= 1, "thin_svd needs a non-empty matrix");
   const int64_t p = std::min(rows, cols);
-  SPB_REQUIRE(p <= 256, "thin_svd supports min(rows, cols) <= 256");
   SPB_TRY(check_finite(rows, cols, X, ldx, "SVD input contains non-finite entries", s));
   Arena ar(s);
   SPB_ALLOC(ar, double, Q, (size_t)std::max(rows, cols) * p);
@@ -318,7 +357,17 @@ int thin_svd(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* U
   SPB_ALLOC(ar, double, Rt, (size_t)p * p);
   SPB_ALLOC(ar, double, Us, (size_t)p * p);
   SPB_ALLOC(ar, double, Vs, (size_t)p * p);
-  if (rows >= cols) {
+  if (rows >= cols && p > kSmallCore) {
+    // X = Q R; one-sided Jacobi on the ROWS of R (the columns of R^T):
+    // R^T = U' S V'^T  ->  X = (Q V') S U'^T, so U = Q V' (rotations, always
+    // orthonormal) and V = U' (normalised rows, completed where S ~ 0).  The
+    // rows of R beyond the numerical rank are rounding-sized and never enter
+    // the Jacobi schedule, so a low-rank sketch costs rounds only for its rank.
+    SPB_TRY(tsqr(rows, cols, X, ldx, Q, p, R, p, s));
+    SPB_TRY(jacobi_svd_tr(p, R, p, /*trans=*/true, V, ldv, S, Us, p, s));
+    SPB_TRY(complete_null_columns(p, S, V, ldv, s));
+    SPB_TRY(gemm(0, 0, rows, p, p, 1.0, Q, p, Us, p, 0.0, U, ldu, s));
+  } else if (rows >= cols) {
     // X = Q R, R = Us S Vs^T  ->  U = Q Us, V = Vs
     SPB_TRY(tsqr(rows, cols, X, ldx, Q, p, R, p, s));
     SPB_TRY(jacobi_svd(p, R, p, Us, p, S, Vs, p, s));
@@ -340,7 +389,6 @@ int thin_svd(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* U
 int thin_svd_t(int64_t rows, int64_t cols, const double* Xt, int64_t ldxt, double* U, int64_t ldu, double* S,
                double* V, int64_t ldv, cudaStream_t s) {
   SPB_REQUIRE(rows >= 1 && cols >= rows, "thin_svd_t needs 1 <= rows <= cols");
-  SPB_REQUIRE(rows <= 256, "thin_svd supports min(rows, cols) <= 256");
   SPB_TRY(check_finite(cols, rows, Xt, ldxt, "SVD input contains non-finite entries", s));
   const int64_t p = rows;
   Arena ar(s);
@@ -351,6 +399,7 @@ int thin_svd_t(int64_t rows, int64_t cols, const double* Xt, int64_t ldxt, doubl
   SPB_TRY(tsqr(cols, rows, Xt, ldxt, Q, p, R, p, s));
   SPB_TRY(transpose(p, p, R, p, Rt, p, s));
   SPB_TRY(jacobi_svd(p, Rt, p, U, ldu, S, Vs, p, s));
+  if (p > kSmallCore) SPB_TRY(complete_null_columns(p, S, U, ldu, s));
   SPB_TRY(gemm(0, 0, cols, p, p, 1.0, Q, p, Vs, p, 0.0, V, ldv, s));
   SPB_TRY(sign_fix(rows, p, U, ldu, V, ldv, cols, false, s));
   return SP_OK;

@@ -39,6 +39,9 @@ int tsqr_form_q(const TsqrPlan& plan, double* Q, int64_t ldq, Arena& ar, cudaStr
 bool gram_chol_dd_ok(int64_t rows, int b);
 int gram_chol_dd(int64_t rows, int b, const double* X, int64_t ldx, double* R, int64_t ldr, Arena& ar,
                  cudaStream_t s, int nslab = 1, int64_t slab_stride = 0);
+// op(A) (B_hi + B_lo) nearly exactly rounded (Ozaki slices on DMMA): C_hi (+ C_lo)
+int gemm_exact(int ta, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B_hi,
+               const double* B_lo, int64_t ldb, double* C_hi, double* C_lo, int64_t ldc, cudaStream_t s);
 int gemm_partials(int ta, int tb, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
                   int64_t ldb, Arena& ar, double** P, int* S_out, cudaStream_t s);
 int tall_gram(int64_t rows, int c, const double* X, int64_t ldx, int d, const double* Y, int64_t ldy,
@@ -72,6 +75,7 @@ int fill_uniform(int64_t rows, int64_t cols, double* X, int64_t ldx, uint64_t se
 int householder_complete(int64_t N, int r, int k, double* out, int64_t ldo, cudaStream_t s,
                          double* kp_out = nullptr);
 int fill_identity(int k, double* out, int64_t ldo, cudaStream_t s);
+int complete_basis(int64_t N, int r, int k, double* out, int64_t ldo, uint64_t seed, cudaStream_t s);
 bool product_with_completion_ok(int64_t N, int r, int k);
 int product_with_completion(int64_t N, int r, int k, const double* X, int64_t ldx, const double* B, int64_t ldb,
                             double* out, int64_t ldo, cudaStream_t s);

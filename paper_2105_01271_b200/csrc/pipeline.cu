@@ -380,24 +380,6 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
   }
 }
 
-// out (N x k, ld ldo) has orthonormal columns [0, r); fill [r, k) with an
-// orthonormal completion (Householder QR of [X | random]).
-static int complete_basis(int64_t N, int r, int k, double* out, int64_t ldo, uint64_t seed,
-                          cudaStream_t s) {
-  if (r >= k) return SP_OK;
-  // Householder reconstruction (one small kernel + one GEMM) when it applies
-  if (householder_complete(N, r, k, out, ldo, s) == SP_OK) return SP_OK;
-  Arena ar(s);
-  SPB_ALLOC(ar, double, W, (size_t)N * k);
-  SPB_ALLOC(ar, double, Qc, (size_t)N * k);
-  SPB_ALLOC(ar, double, Rc, (size_t)k * k);
-  if (r > 0) SPB_TRY(copy2d(N, r, out, ldo, W, k, s));
-  SPB_TRY(fill_uniform(N, k - r, W + r, k, seed, s));
-  SPB_TRY(qr_tall(N, k, W, k, Qc, k, Rc, k, /*well_conditioned=*/true, s));
-  SPB_TRY(copy2d(N, k - r, Qc + r, k, out + r, ldo, s));
-  return SP_OK;
-}
-
 // Per-thread side stream (+ fork / join events) for independent small chains.
 struct AuxStream {
   cudaStream_t s = nullptr;
@@ -953,22 +935,40 @@ int power_id(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, cons
       return SP_ECUDA;
     }
     SPB_TRY(copy2d(m, nc, coarse, nc, E, nc, s));
-    const bool ref_order = ncols <= m;  // C (C^T E) as the reference when cheap
+    // C (C^T E) in the reference's association when it is the cheaper one
+    // (src/power.py:282-285), each product nearly exactly rounded (Ozaki
+    // slices on DMMA, exact_gemm.cu) and the iterate carried in double-double:
+    // the greedy pivots past the signal are decided by ulp-level differences
+    // of E's residual norms, and only an E this close to the exact product
+    // gives the reference's pivots (SPB_ID_PLAIN_GEMM=1: plain FP64 GEMMs).
+    // Otherwise (ncols > m, cfg5: C^T C would be 550 GB) W = C C^T, plain FP64.
+    const bool ref_order = ncols <= m;
+    static const bool plain = getenv("SPB_ID_PLAIN_GEMM") != nullptr;
     double* W = nullptr;
-    double* T = nullptr;
-    if (ref_order)
+    double *T = nullptr, *T_lo = nullptr, *E_lo = nullptr, *E2_lo = nullptr;
+    if (ref_order) {
       T = ar.alloc<double>((size_t)ncols * nc);
-    else
+      if (!plain) {
+        T_lo = ar.alloc<double>((size_t)ncols * nc);
+        E_lo = ar.alloc<double>((size_t)m * nc);
+        E2_lo = ar.alloc<double>((size_t)m * nc);
+      }
+    } else {
       W = ar.alloc<double>((size_t)m * m);
+    }
     if (ar.failed()) {
       set_error("enriched sketch allocation failed");
       return SP_ECUDA;
     }
     if (!ref_order) SPB_TRY(gemm(0, 1, m, m, ncols, 1.0, C, ncols, C, ncols, 0.0, W, m, s));
     for (int it = 0; it < q; ++it) {
-      if (ref_order) {
+      if (ref_order && plain) {
         SPB_TRY(gemm(1, 0, ncols, nc, m, 1.0, C, ncols, E, nc, 0.0, T, nc, s));
         SPB_TRY(gemm(0, 0, m, nc, ncols, 1.0, C, ncols, T, nc, 0.0, E2, nc, s));
+      } else if (ref_order) {
+        SPB_TRY(gemm_exact(1, ncols, nc, m, C, ncols, E, it == 0 ? nullptr : E_lo, nc, T, T_lo, nc, s));
+        SPB_TRY(gemm_exact(0, m, nc, ncols, C, ncols, T, T_lo, nc, E2, E2_lo, nc, s));
+        std::swap(E_lo, E2_lo);
       } else {
         SPB_TRY(gemm(0, 0, m, nc, m, 1.0, W, m, E, nc, 0.0, E2, nc, s));
       }

