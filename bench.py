@@ -284,6 +284,44 @@ def _events_ms(fn, reps, torch):
     return e0.elapsed_time(e1) / reps, out
 
 
+def ingest_paths(cfg, A, op, pc, torch):
+    """e2e of the drop-in from the host sources a reference user has: a
+    pageable numpy array and LRSM files (f64, and f32 kept f32 in HBM) --
+    through the page-locked staging ring (host memcpy / pread overlapped with
+    the copy engine and the fused gather).  The files are read back from the
+    page cache (written just before), so this times the ingest path, not a
+    disk.  Wall-clock per call (host-synchronous API), mean of 3 after 1."""
+    import tempfile
+
+    import paper_2105_01271_b200 as sp
+    out = {}
+    a_h = A.cpu().numpy()                      # pageable
+    tmpd = "/dev/shm" if os.path.isdir("/dev/shm") else None
+    with tempfile.TemporaryDirectory(dir=tmpd) as d:
+        f64 = os.path.join(d, "a64.lrsm")
+        f32 = os.path.join(d, "a32.lrsm")
+        sp.write_snapshots(f64, a_h, scalar_kind=0)
+        sp.write_snapshots(f32, a_h.astype(np.float32), scalar_kind=1)
+        cases = {"pageable_array": (lambda: sp.ArraySnapshotStream(a_h), a_h.nbytes),
+                 "lrsm_f64_file": (lambda: sp.open_stream(f64), a_h.nbytes),
+                 "lrsm_f32_file": (lambda: sp.open_stream(f32), a_h.nbytes // 2)}
+        for key, (mk, nbytes) in cases.items():
+            times = []
+            for i in range(4):
+                st = mk()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                res = sp.power_svd(st, op, cfg.k, pc)
+                dt = time.perf_counter() - t0
+                st.close()
+                if i:
+                    times.append(dt)
+            ms = 1e3 * statistics.mean(times)
+            out[key] = {"ms": ms, "GBps_A": nbytes / ms / 1e6, "h2d_bytes": nbytes,
+                        "d2h_bytes": int(res.u.nbytes + res.s.nbytes + res.v.nbytes)}
+    return out
+
+
 def extra_configs(names, dev, torch):
     """Other BASELINE configurations on this GPU (N = 1): device-resident
     power_svd (and power_id where the config names it), CUDA-event timed."""
@@ -307,11 +345,17 @@ def extra_configs(names, dev, torch):
                "kept_rank": int(res.kept_rank), "m": cfg.m, "n": cfg.n, "n_c": int(cols.size), "k": cfg.k,
                "dtype": cfg.dtype}
         del res
+        gc.collect()
+        torch.cuda.empty_cache()   # the library's workspaces come from the CUDA mempool, not torch's cache
+        if name == "cfg2":
+            rec["e2e_ingest"] = ingest_paths(cfg, A, op, pc, torch)
         if name in ("cfg3", "cfg5"):
             def pid():
                 return sp.power_id(sp.DeviceSnapshotStream(A), op, cfg.k, pc, return_device=True)
             f = pid()
             del f
+            gc.collect()
+            torch.cuda.empty_cache()
             ms_id, f = _events_ms(pid, 2, torch)
             rec["power_id"] = {"ms": ms_id, "k": cfg.k, "lift_r": int(f.r)}
             del f

@@ -132,6 +132,20 @@ int sp_gemm_exact(int32_t trans_a, int64_t M, int64_t N, int64_t K, const double
                   const double* B_hi, const double* B_lo, int64_t ldb, double* C_hi, double* C_lo,
                   int64_t ldc, void* stream);
 
+/* Building blocks of sp_gemm_exact for operands split across ranks (the
+ * sharded ID's W = sum_i C_i C_i^T): the slice plan for a total depth K, the
+ * per-row (axis = 1) / per-column (axis = 0) max exponents (allreduce-max them
+ * across ranks so every rank slices on the same grid), the nsl exact level
+ * products (levels: nsl x M x N; exact for any summation order, so their
+ * allreduce-sum is exact) and their double-double sum (+ an inexact tail). */
+int sp_exact_plan(int64_t K, int32_t* bits, int32_t* nsl);
+int sp_exponents(int32_t axis, int64_t rows, int64_t cols, const double* X, int64_t ldx, int32_t* e, void* stream);
+int sp_gemm_exact_levels(int32_t trans_a, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                         const int32_t* ea, const double* B, int64_t ldb, const int32_t* eb, int32_t bits,
+                         int32_t nsl, double* levels, void* stream);
+int sp_dd_levels(int64_t M, int64_t N, const double* levels, int32_t nsl, const double* tail, double* hi,
+                 double* lo, int64_t ldc, void* stream);
+
 /* ---------------------------------------------------------------- K4 -----
  * Householder QR of a tall matrix X (rows x cols, rows >= cols): explicit
  * Q (rows x cols) and R (cols x cols).  cols <= 32 runs as a register-resident
@@ -222,6 +236,37 @@ int sp_pivoted_qr(int64_t rows, int64_t cols, const double* Mt, int64_t ldmt, in
  * SP_WARN_ID_PINV), P (m x k) with P[indices] = I exactly, indices (k). */
 int sp_row_id(int64_t m, int64_t cols, const double* M, int64_t ldm, int32_t k, double* P,
               int64_t* indices, int64_t* info, void* stream);
+
+/* ------------------------------------------------- K7 across ranks -----
+ * The greedy pivoted QR of src/kernels.py:97-142 on candidates (rows of the
+ * enriched sketch E, m of them) whose entries are sharded over ranks: this
+ * rank holds E_i (m x len, candidate j = row j).  Per step t the caller
+ * allreduce-sums the partial outputs between the calls:
+ *   sp_pqd_begin  -> pn2 (m)      partial ||w_j||^2          (before step 0)
+ *   sp_pqd_select(n2 = sum pn2)  -> delta (t) partial Q^T w_t; pivot, swaps
+ *   sp_pqd_orth  (delta summed)   -> part2 (1) partial ||v||^2
+ *   sp_pqd_coef  (part2 summed)   -> coef (m) partial v . w_j
+ *   sp_pqd_update(coef summed)    -> pn2 (m) for the next step
+ * perm (m) and R (k x m, ld ldr) come out identical on every rank; WK (m x len),
+ * Qt (k x len) are this rank's work rows; jsel (1), status (1, zero it first:
+ * SP_ENUMERICAL on an exactly zero pivot) device words. */
+int sp_pqd_begin(int64_t m, int64_t len, int32_t k, const double* E, int64_t lde, double* WK, int64_t* perm,
+                 double* R, int64_t ldr, double* pn2, void* stream);
+int sp_pqd_select(int32_t t, int32_t k, int64_t m, int64_t len, const double* n2, int64_t* perm, double* R,
+                  int64_t ldr, double* WK, const double* Qt, double* delta, int64_t* jsel, void* stream);
+int sp_pqd_orth(int32_t t, int64_t len, const double* delta, double* R, int64_t ldr, const double* WK, double* Qt,
+                double* part2, void* stream);
+int sp_pqd_coef(int32_t t, int64_t m, int64_t len, const double* p2, double* R, int64_t ldr, const double* WK,
+                double* Qt, double* coef, int32_t* status, void* stream);
+int sp_pqd_update(int32_t t, int64_t m, int64_t len, const double* coef, double* R, int64_t ldr, double* WK,
+                  const double* Qt, double* pn2, void* stream);
+
+/* The interpolation coefficients of row_id (src/rowid.py:53-79) from a
+ * pivoted QR of M^T: C = R1^-1 R2 (pseudo-inverse solve, SP_WARN_ID_PINV,
+ * when R1 is rank deficient); P (m x k) with P[perm[:k]] = I and
+ * P[perm[k:]] = C^T; indices = perm[:k]. */
+int sp_id_from_qr(int64_t m, int32_t k, const int64_t* perm, const double* R, int64_t ldr, double* P,
+                  int64_t* indices, int64_t* info, void* stream);
 
 /* Kept left basis of a sketch X (rows x cols): the top singular triplets by
  * randomized block subspace iteration (Householder TSQR + Jacobi Rayleigh-

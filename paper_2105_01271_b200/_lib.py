@@ -45,6 +45,16 @@ SIGNATURES = {
     "sp_skinny_atz": [_P, _I32, _I64, _I64, _I64, _P, _I64, _I32, _P, _I64, _P],
     "sp_gemm": [_I32, _I32, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64, _P],
     "sp_gemm_exact": [_I32, _I64, _I64, _I64, _P, _I64, _P, _P, _I64, _P, _P, _I64, _P],
+    "sp_exact_plan": [_I64, _P, _P],
+    "sp_exponents": [_I32, _I64, _I64, _P, _I64, _P, _P],
+    "sp_gemm_exact_levels": [_I32, _I64, _I64, _I64, _P, _I64, _P, _P, _I64, _P, _I32, _I32, _P, _P],
+    "sp_dd_levels": [_I64, _I64, _P, _I32, _P, _P, _P, _I64, _P],
+    "sp_pqd_begin": [_I64, _I64, _I32, _P, _I64, _P, _P, _P, _I64, _P, _P],
+    "sp_pqd_select": [_I32, _I32, _I64, _I64, _P, _P, _P, _I64, _P, _P, _P, _P, _P],
+    "sp_pqd_orth": [_I32, _I64, _P, _P, _I64, _P, _P, _P, _P],
+    "sp_pqd_coef": [_I32, _I64, _I64, _P, _P, _I64, _P, _P, _P, _P, _P],
+    "sp_pqd_update": [_I32, _I64, _I64, _P, _P, _I64, _P, _P, _P, _P],
+    "sp_id_from_qr": [_I64, _I32, _P, _P, _I64, _P, _P, _P, _P],
     "sp_tsqr": [_I64, _I64, _P, _I64, _P, _I64, _P, _I64, _P],
     "sp_qr_tall": [_I64, _I64, _P, _I64, _P, _I64, _P, _I64, _I32, _P],
     "sp_cholqr2_async": [_I64, _I64, _P, _I64, _P, _I64, _P, _I64, _P, _P],

@@ -96,6 +96,71 @@ int sp_gemm_exact(int32_t trans_a, int64_t M, int64_t N, int64_t K, const double
   return gemm_exact(trans_a, M, N, K, A, lda, B_hi, B_lo, ldb, C_hi, C_lo, ldc, ST(stream));
 }
 
+int sp_exact_plan(int64_t K, int32_t* bits, int32_t* nsl) {
+  if (K < 1 || !bits || !nsl) {
+    set_error("sp_exact_plan: K >= 1 and output pointers required");
+    return SP_ECONFIG;
+  }
+  int b = 0, n = 0;
+  ozaki_plan(K, &b, &n);
+  *bits = b;
+  *nsl = n;
+  return SP_OK;
+}
+
+int sp_exponents(int32_t axis, int64_t rows, int64_t cols, const double* X, int64_t ldx, int32_t* e, void* stream) {
+  return axis == 1 ? row_exponents(rows, cols, X, ldx, e, ST(stream)) : col_exponents(rows, cols, X, ldx, e, ST(stream));
+}
+
+int sp_gemm_exact_levels(int32_t trans_a, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                         const int32_t* ea, const double* B, int64_t ldb, const int32_t* eb, int32_t bits,
+                         int32_t nsl, double* levels, void* stream) {
+  return gemm_exact_levels(trans_a, M, N, K, A, lda, ea, B, ldb, eb, bits, nsl, levels, ST(stream));
+}
+
+int sp_dd_levels(int64_t M, int64_t N, const double* levels, int32_t nsl, const double* tail, double* hi, double* lo,
+                 int64_t ldc, void* stream) {
+  return dd_levels(M, N, levels, nsl, tail, hi, lo, ldc, ST(stream));
+}
+
+int sp_pqd_begin(int64_t m, int64_t len, int32_t k, const double* E, int64_t lde, double* WK, int64_t* perm,
+                 double* R, int64_t ldr, double* pn2, void* stream) {
+  return pqd_begin(m, len, k, E, lde, WK, perm, R, ldr, pn2, ST(stream));
+}
+
+int sp_pqd_select(int32_t t, int32_t k, int64_t m, int64_t len, const double* n2, int64_t* perm, double* R,
+                  int64_t ldr, double* WK, const double* Qt, double* delta, int64_t* jsel, void* stream) {
+  return pqd_select(t, k, m, len, n2, perm, R, ldr, WK, Qt, delta, jsel, ST(stream));
+}
+
+int sp_pqd_orth(int32_t t, int64_t len, const double* delta, double* R, int64_t ldr, const double* WK, double* Qt,
+                double* part2, void* stream) {
+  return pqd_orth(t, len, delta, R, ldr, WK, Qt, part2, ST(stream));
+}
+
+int sp_pqd_coef(int32_t t, int64_t m, int64_t len, const double* p2, double* R, int64_t ldr, const double* WK,
+                double* Qt, double* coef, int32_t* status, void* stream) {
+  return pqd_coef(t, m, len, p2, R, ldr, WK, Qt, coef, status, ST(stream));
+}
+
+int sp_pqd_update(int32_t t, int64_t m, int64_t len, const double* coef, double* R, int64_t ldr, double* WK,
+                  const double* Qt, double* pn2, void* stream) {
+  return pqd_update(t, m, len, coef, R, ldr, WK, Qt, pn2, ST(stream));
+}
+
+int sp_id_from_qr(int64_t m, int32_t k, const int64_t* perm, const double* R, int64_t ldr, double* P,
+                  int64_t* indices, int64_t* info, void* stream) {
+  const int64_t l0 = launches();
+  int warn = 0;
+  const int st = id_from_qr(m, k, perm, R, ldr, P, indices, &warn, ST(stream));
+  if (info) {
+    for (int i = 0; i < SP_INFO_LEN; ++i) info[i] = 0;
+    info[SP_INFO_WARN] = warn;
+    info[SP_INFO_LAUNCHES] = launches() - l0;
+  }
+  return st;
+}
+
 int sp_tsqr(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq, double* R,
             int64_t ldr, void* stream) {
   return tsqr(rows, cols, X, ldx, Q, ldq, R, ldr, ST(stream));

@@ -42,6 +42,26 @@ int gram_chol_dd(int64_t rows, int b, const double* X, int64_t ldx, double* R, i
 // op(A) (B_hi + B_lo) nearly exactly rounded (Ozaki slices on DMMA): C_hi (+ C_lo)
 int gemm_exact(int ta, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B_hi,
                const double* B_lo, int64_t ldb, double* C_hi, double* C_lo, int64_t ldc, cudaStream_t s);
+void ozaki_plan(int64_t K, int* bits, int* nsl);
+int row_exponents(int64_t rows, int64_t cols, const double* X, int64_t ldx, int* e, cudaStream_t s);
+int col_exponents(int64_t rows, int64_t cols, const double* X, int64_t ldx, int* e, cudaStream_t s);
+int gemm_exact_levels(int ta, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const int* ea,
+                      const double* B, int64_t ldb, const int* eb, int bits, int nsl, double* Lv, cudaStream_t s);
+int dd_levels(int64_t M, int64_t N, const double* Lv, int nsl, const double* tail, double* hi, double* lo,
+              int64_t ldc, cudaStream_t s);
+// sharded pivoted QR steps (pivqr_dist.cu) and the ID coefficients from a QR
+int pqd_begin(int64_t m, int64_t len, int k, const double* E, int64_t lde, double* WK, int64_t* perm, double* R,
+              int64_t ldr, double* pn2, cudaStream_t s);
+int pqd_select(int t, int k, int64_t m, int64_t len, const double* n2, int64_t* perm, double* R, int64_t ldr,
+               double* WK, const double* Qt, double* delta, int64_t* jsel, cudaStream_t s);
+int pqd_orth(int t, int64_t len, const double* delta, double* R, int64_t ldr, const double* WK, double* Qt,
+             double* part2, cudaStream_t s);
+int pqd_coef(int t, int64_t m, int64_t len, const double* p2, double* R, int64_t ldr, const double* WK, double* Qt,
+             double* coef, int* status, cudaStream_t s);
+int pqd_update(int t, int64_t m, int64_t len, const double* coef, double* R, int64_t ldr, double* WK, const double* Qt,
+               double* pn2, cudaStream_t s);
+int id_from_qr(int64_t m, int k, const int64_t* perm, const double* R, int64_t ldr, double* P, int64_t* indices,
+               int* warn, cudaStream_t s);
 int gemm_partials(int ta, int tb, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
                   int64_t ldb, Arena& ar, double** P, int* S_out, cudaStream_t s);
 int tall_gram(int64_t rows, int c, const double* X, int64_t ldx, int d, const double* Y, int64_t ldy,

@@ -806,19 +806,15 @@ __global__ void gather_rows_kernel(const int64_t* rows_idx, int k, const double*
   out[i * ldo + c] = X[rows_idx[i] * ldx + c];
 }
 
-// row_id (src/rowid.py:53-79) of M (m x cols): P (m x k), indices (k).
-int row_id(int64_t m, int64_t cols, const double* M, int64_t ldm, int k, double* P, int64_t* indices,
-           int* warn, cudaStream_t s) {
-  SPB_REQUIRE(k >= 1 && k <= std::min(m, cols),
-              "rank k=" + std::to_string(k) + " outside [1, " + std::to_string(std::min(m, cols)) + "]");
+// Interpolation coefficients from a rank-k pivoted QR of M^T (perm: pivot
+// order over the m candidates, R: k x m with R[:, perm-order]):
+// C = R1^-1 R2, or the pseudo-inverse solve when R1 is rank deficient
+// (src/rowid.py:60-75); P[perm[:k]] = I, P[perm[k:]] = C^T; indices = perm[:k].
+int id_from_qr(int64_t m, int k, const int64_t* perm, const double* R, int64_t ldr, double* P, int64_t* indices,
+               int* warn, cudaStream_t s) {
   Arena ar(s);
-  SPB_ALLOC(ar, int64_t, perm, (size_t)m);
-  SPB_ALLOC(ar, double, Qp, (size_t)cols * k);
-  SPB_ALLOC(ar, double, R, (size_t)k * m);
-  // pivoted_qr(M^T): rows = cols of M, candidate columns = rows of M (contiguous)
-  SPB_TRY(pivoted_qr(cols, m, M, ldm, k, perm, Qp, k, R, m, s));
   std::vector<double> hr((size_t)k * k);
-  SPB_CUDA(cudaMemcpy2DAsync(hr.data(), k * sizeof(double), R, m * sizeof(double), k * sizeof(double), k,
+  SPB_CUDA(cudaMemcpy2DAsync(hr.data(), k * sizeof(double), R, ldr * sizeof(double), k * sizeof(double), k,
                              cudaMemcpyDeviceToHost, s));
   SPB_CUDA(cudaStreamSynchronize(s));
   double dmax = 0.0, dmin = INFINITY;
@@ -831,7 +827,7 @@ int row_id(int64_t m, int64_t cols, const double* M, int64_t ldm, int k, double*
   *warn = 0;
   if (nrest > 0) {
     if (dmin > kRankTol * std::max(dmax, 2.2250738585072014e-308)) {
-      SPB_TRY(trsm_upper(k, R, m, nrest, R + k, m, coef, nrest, s));
+      SPB_TRY(trsm_upper(k, R, ldr, nrest, R + k, ldr, coef, nrest, s));
     } else {
       *warn = SP_WARN_ID_PINV;
       // coef = V diag(pinv(s)) (U^T r2)
@@ -841,12 +837,11 @@ int row_id(int64_t m, int64_t cols, const double* M, int64_t ldm, int k, double*
       SPB_ALLOC(ar, double, Si, (size_t)k);
       SPB_ALLOC(ar, double, T, (size_t)k * nrest);
       SPB_ALLOC(ar, double, R1, (size_t)k * k);
-      SPB_TRY(copy2d(k, k, R, m, R1, k, s));
+      SPB_TRY(copy2d(k, k, R, ldr, R1, k, s));
       SPB_TRY(thin_svd(k, k, R1, k, Uu, k, Ss, Vv, k, s));
       SPB_TRY(pinv_apply(Ss, k, kRankTol, Si, s));
-      SPB_TRY(gemm(1, 0, k, nrest, k, 1.0, Uu, k, R + k, m, 0.0, T, nrest, s));
-      // T = diag(Si) T : scale rows -> transpose trick via scale_cols on T^T is
-      // avoided; fold into V instead: coef = (V diag(Si)) T
+      SPB_TRY(gemm(1, 0, k, nrest, k, 1.0, Uu, k, R + k, ldr, 0.0, T, nrest, s));
+      // coef = (V diag(Si)) T
       SPB_TRY(scale_cols(k, k, Vv, k, Si, s));
       SPB_TRY(gemm(0, 0, k, nrest, k, 1.0, Vv, k, T, nrest, 0.0, coef, nrest, s));
     }
@@ -858,6 +853,20 @@ int row_id(int64_t m, int64_t cols, const double* M, int64_t ldm, int k, double*
   SPB_CHECK_LAUNCH();
   SPB_CUDA(cudaMemcpyAsync(indices, perm, k * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
   return SP_OK;
+}
+
+// row_id (src/rowid.py:53-79) of M (m x cols): P (m x k), indices (k).
+int row_id(int64_t m, int64_t cols, const double* M, int64_t ldm, int k, double* P, int64_t* indices,
+           int* warn, cudaStream_t s) {
+  SPB_REQUIRE(k >= 1 && k <= std::min(m, cols),
+              "rank k=" + std::to_string(k) + " outside [1, " + std::to_string(std::min(m, cols)) + "]");
+  Arena ar(s);
+  SPB_ALLOC(ar, int64_t, perm, (size_t)m);
+  SPB_ALLOC(ar, double, Qp, (size_t)cols * k);
+  SPB_ALLOC(ar, double, R, (size_t)k * m);
+  // pivoted_qr(M^T): rows = cols of M, candidate columns = rows of M (contiguous)
+  SPB_TRY(pivoted_qr(cols, m, M, ldm, k, perm, Qp, k, R, m, s));
+  return id_from_qr(m, k, perm, R, m, P, indices, warn, s);
 }
 
 // ------------------------------------------------------------ power_id ----

@@ -41,15 +41,19 @@ class TorchComm:
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
 
-    def allgather_cols(self, x, ops):
-        """Concatenate each rank's (m x w_i) block along columns, rank order."""
+    def allgather_cols(self, x, ops, widths=None):
+        """Concatenate each rank's (m x w_i) block along columns, rank order.
+        ``widths`` (every rank's w_i, known to the caller from the column
+        layout) avoids the width exchange and its host synchronisation."""
         if self.world == 1:
             return x
-        import torch
-        widths = torch.tensor([x.shape[1]], dtype=torch.int64, device=ops.tensor_device)
-        ws = [torch.zeros_like(widths) for _ in range(self.world)]
-        self.dist.all_gather(ws, widths, group=self.group)
-        ws = [int(w.item()) for w in ws]
+        if widths is None:
+            import torch
+            wt = torch.tensor([x.shape[1]], dtype=torch.int64, device=ops.tensor_device)
+            ws = [torch.zeros_like(wt) for _ in range(self.world)]
+            self.dist.all_gather(ws, wt, group=self.group)
+            widths = [int(w.item()) for w in ws]
+        ws = list(widths)
         wmax = max(ws)
         pad = ops.pad_cols(x, wmax)
         parts = [ops.empty_like(pad) for _ in range(self.world)]
@@ -61,6 +65,13 @@ class TorchComm:
             return x
         x = ops.contig(x)
         self.dist.all_reduce(x, group=self.group)
+        return x
+
+    def allreduce_max(self, x, ops):
+        if self.world == 1:
+            return x
+        x = ops.contig(x)
+        self.dist.all_reduce(x, op=self.dist.ReduceOp.MAX, group=self.group)
         return x
 
     def allgather_rows(self, x, ops):
@@ -108,7 +119,8 @@ def _count_kept(hs, power):
     return int(np.count_nonzero((hs / hs[0]) ** power > KEEP_TOL))
 
 
-def distributed_sketch_basis(c_i, row0: int, ncols: int, power: float, comm, ops):
+def distributed_sketch_basis(c_i, row0: int, ncols: int, power: float, comm, ops, need: int = -1,
+                             widths=None):
     """Kept left basis U_{C,r} of the column-sharded sketch C = [C_1 .. C_P]
     without gathering C: the randomized block subspace iteration of the device
     svd_top (csrc/pipeline.cu) with the exchanges confined to m x b and b x b
@@ -122,11 +134,13 @@ def distributed_sketch_basis(c_i, row0: int, ncols: int, power: float, comm, ops
       R^T = U_s S V_s^T  (Jacobi)      U_C = Q U_s
 
     Same block size, growth and stopping rules as the single-GPU svd_top, so
-    world size 1 reproduces it.  Returns (U m x r, sigma (host), r)."""
+    world size 1 reproduces it.  ``need`` >= 0 is svd_top's ID mode (only the
+    leading ``need`` triplets and whether the rank reaches them).  Returns
+    (U m x r, sigma (host), r) -- r the kept count, U's width min(r, block)."""
     m, nci = c_i.shape
     p = min(m, ncols)
     if p <= 64:  # exact path of svd_top: gather the (small) sketch
-        c_all = comm.allgather_cols(c_i, ops)
+        c_all = comm.allgather_cols(c_i, ops, widths)
         return ops.sketch_basis(c_all, power)
     cap = min(p, 256)
     b = min(cap, ((max(32, 1 + 16) + 7) // 8) * 8)
@@ -147,7 +161,11 @@ def distributed_sketch_basis(c_i, row0: int, ncols: int, power: float, comm, ops
             us, sg = ops.svd_small_t(r_all)                             # R^T = U_s S V_s^T
             hs = ops.to_numpy(sg)
             kept = _count_kept(hs, power)
-            if kept + 8 > b and b < cap:
+            if kept + 8 > b and (need < 0 or kept < need + 8):
+                if b >= cap:
+                    from .errors import ConfigError
+                    raise ConfigError(f"sketch numerical rank {kept} exceeds the sharded range finder's "
+                                      f"{cap}-column block")
                 grow = True
                 break
             conv = itn == 0 and kept > 0 and b - 8 > kept and hs[b - 8] <= 1e-8 * hs[kept - 1]
@@ -155,7 +173,10 @@ def distributed_sketch_basis(c_i, row0: int, ncols: int, power: float, comm, ops
                     and (hs[b - 8] / hs[kept - 1]) ** (2.0 * itn + 2.0) <= 1e-12):
                 conv = True
             if not conv and itn >= 1 and kept == kept_prev:
-                chk = min(b, kept + 1)
+                chk = min(b, kept + 1) if need < 0 else min(b, need)
+                if need >= 0:  # an unresolved bulk near the block's tail is exempt
+                    bulk = np.flatnonzero(hs[:chk] <= 10.0 * hs[b - 1])
+                    chk = int(bulk[0]) if bulk.size else chk
                 conv = bool(np.all(np.abs(hs[:chk] - prev[:chk]) <= 1e-14 * hs[0] + 1e-12 * hs[:chk]))
             if conv:
                 break
@@ -169,8 +190,9 @@ def distributed_sketch_basis(c_i, row0: int, ncols: int, power: float, comm, ops
             b = min(cap, 2 * b)
             continue
         r = kept
-        u = ops.matmul(qy, ops.cols(us, 0, max(r, 1)))
-        return ops.cols(u, 0, r), hs[:r], r
+        w = min(r, b)
+        u = ops.matmul(qy, ops.cols(us, 0, max(w, 1)))
+        return ops.cols(u, 0, w), hs[:w], r
 
 
 def sharded_power_svd(a_local, c_begin: int, cols, k: int, q: int, comm, ops, n_total=None):
@@ -400,34 +422,133 @@ class DeviceOps:
                   kp.data_ptr() if r > 0 else None, self._s())
         return x, kp
 
-    def power_id_local(self, a_local, c_all, cols, k, q, r=None):
-        """sp_power_id on this shard with the all-gathered C as both the
-        coarse sketch and the column block (no gather, no index validation)."""
-        import warnings
+    # --- the sharded ID (exact enrichment levels, distributed pivoted QR)
+    def exponents(self, x, axis):
+        rows, cols = x.shape
+        e = self.t.empty((rows if axis == 1 else cols,), dtype=self.t.int32, device=self.tensor_device)
+        _lib.call("sp_exponents", int(axis), rows, cols, x.data_ptr(), x.stride(0), e.data_ptr(), self._s())
+        return e
 
-        from .device import empty, ptr, to_device, to_host_many
-        from .errors import RankDeficiencyWarning
-        m, n_i = a_local.shape
-        ncols = int(c_all.shape[1])
-        c_all = self.contig(c_all)
-        d_cols = to_device(np.asarray(cols, dtype=np.int64))
-        w = self.t.ones(ncols, dtype=self.t.float64, device=c_all.device)
-        r_req = int(r) if r is not None else 0
-        r_max = max(r_req, 2 * k, 1)
-        p, ind, skel = empty((m, k)), empty((k,), "i64"), empty((k, ncols))
-        left, right = empty((ncols, r_max)), empty((r_max, n_i))
+    def exact_plan(self, K):
+        import ctypes
+        b, n = ctypes.c_int32(0), ctypes.c_int32(0)
+        _lib.call("sp_exact_plan", int(K), ctypes.byref(b), ctypes.byref(n))
+        return int(b.value), int(n.value)
+
+    def transpose(self, x):
+        return x.t().contiguous()
+
+    def exact_levels(self, ta, a, ea, b, eb, bits, nsl):
+        M = a.shape[1] if ta else a.shape[0]
+        K = a.shape[0] if ta else a.shape[1]
+        N = b.shape[1]
+        lv = self.t.empty((nsl, M, N), dtype=self.t.float64, device=self.tensor_device)
+        _lib.call("sp_gemm_exact_levels", int(ta), M, N, K, a.data_ptr(), a.stride(0), ea.data_ptr(), b.data_ptr(),
+                  b.stride(0), eb.data_ptr(), bits, nsl, lv.data_ptr(), self._s())
+        return lv
+
+    def dd_levels(self, lv, nsl, tail):
+        _, M, N = lv.shape
+        hi = self.t.empty((M, N), dtype=self.t.float64, device=self.tensor_device)
+        lo = self.t.empty_like(hi)
+        _lib.call("sp_dd_levels", M, N, lv.data_ptr(), nsl, None if tail is None else tail.data_ptr(), hi.data_ptr(),
+                  lo.data_ptr(), N, self._s())
+        return hi, lo
+
+    def exact_mm(self, ta, a_hi, a_lo, b, b_lo):
+        """(a_hi + a_lo)(b + b_lo) for A, B double-doubles (ta = 0 only): the
+        product W E of the sharded enrichment, returned as a double-double."""
+        assert ta == 0
+        M, K = a_hi.shape
+        N = b.shape[1]
+        # op(A) B with A = W (dd): W_hi (B_hi + B_lo) nearly exact + W_lo B
+        hi = self.t.empty((M, N), dtype=self.t.float64, device=self.tensor_device)
+        lo = self.t.empty_like(hi)
+        b = b.contiguous()
+        _lib.call("sp_gemm_exact", 0, M, N, K, a_hi.data_ptr(), K, b.data_ptr(),
+                  None if b_lo is None else b_lo.data_ptr(), N, hi.data_ptr(), lo.data_ptr(), N, self._s())
+        tail = self.t.empty_like(hi)
+        _lib.call("sp_gemm", 0, 0, M, N, K, 1.0, a_lo.data_ptr(), K, b.data_ptr(), N, 0.0, tail.data_ptr(), N,
+                  self._s())
+        # (hi, lo) += tail: one more double-double level
+        lv = self.t.stack([hi, lo + tail])
+        return self.dd_levels(lv, 2, None)
+
+    def check_finite(self, x, msg):
+        from .errors import NumericalError
+        if not bool(self.t.isfinite(x).all()):
+            raise NumericalError(msg)
+
+    class _PqdState:
+        pass
+
+    def pqd_state(self, e_i, k):
+        m, n_i = e_i.shape
+        st = self._PqdState()
+        st.m, st.len, st.k = m, n_i, k
+        f64 = dict(dtype=self.t.float64, device=self.tensor_device)
+        st.wk = self.t.empty((m, max(n_i, 1)), **f64)
+        st.qt = self.t.zeros((k, max(n_i, 1)), **f64)
+        st.r = self.t.empty((k, m), **f64)
+        st.perm = self.t.empty((m,), dtype=self.t.int64, device=self.tensor_device)
+        st.pn2 = self.t.empty((m,), **f64)
+        st.delta = self.t.zeros((max(k, 1),), **f64)
+        st.part2 = self.t.empty((1,), **f64)
+        st.coef = self.t.zeros((m,), **f64)
+        st.jsel = self.t.empty((1,), dtype=self.t.int64, device=self.tensor_device)
+        st.status = self.t.zeros((1,), dtype=self.t.int32, device=self.tensor_device)
+        e_i = e_i.contiguous()
+        _lib.call("sp_pqd_begin", m, n_i, k, e_i.data_ptr(), max(n_i, 1), st.wk.data_ptr(), st.perm.data_ptr(),
+                  st.r.data_ptr(), m, st.pn2.data_ptr(), self._s())
+        return st
+
+    def pqd_select(self, st, t, n2):
+        _lib.call("sp_pqd_select", t, st.k, st.m, st.len, n2.data_ptr(), st.perm.data_ptr(), st.r.data_ptr(), st.m,
+                  st.wk.data_ptr(), st.qt.data_ptr(), st.delta.data_ptr(), st.jsel.data_ptr(), self._s())
+        return st.delta[:t]
+
+    def pqd_orth(self, st, t, delta):
+        d = delta if t > 0 else st.delta
+        _lib.call("sp_pqd_orth", t, st.len, d.data_ptr(), st.r.data_ptr(), st.m, st.wk.data_ptr(), st.qt.data_ptr(),
+                  st.part2.data_ptr(), self._s())
+        return st.part2
+
+    def pqd_coef(self, st, t, part2):
+        _lib.call("sp_pqd_coef", t, st.m, st.len, part2.data_ptr(), st.r.data_ptr(), st.m, st.wk.data_ptr(),
+                  st.qt.data_ptr(), st.coef.data_ptr(), st.status.data_ptr(), self._s())
+        return st.coef
+
+    def pqd_update(self, st, t, coef):
+        _lib.call("sp_pqd_update", t, st.m, st.len, coef.data_ptr(), st.r.data_ptr(), st.m, st.wk.data_ptr(),
+                  st.qt.data_ptr(), st.pn2.data_ptr(), self._s())
+        return st.pn2
+
+    def pqd_check(self, st):
+        from .errors import NumericalError
+        if int(st.status.item()) != 0:
+            raise NumericalError("sharded pivoted QR: exactly zero pivot (the deterministic filler of "
+                                 "src/kernels.py:145-155 needs the unsharded candidates)")
+
+    def id_from_qr(self, perm, rr, k):
+        m = perm.shape[0]
+        p = self.t.empty((m, k), dtype=self.t.float64, device=self.tensor_device)
+        ind = self.t.empty((k,), dtype=self.t.int64, device=self.tensor_device)
         info = _lib.new_info()
-        tag = _lib.SP_F64 if a_local.dtype == self.t.float64 else _lib.SP_F32
-        _lib.call("sp_power_id", ptr(a_local), tag, m, n_i, a_local.stride(0), ptr(d_cols), ptr(w), 1, ncols,
-                  ptr(d_cols), ncols, q, k, r_req, None, 0, 0, ptr(c_all), ptr(c_all), ptr(p), ptr(ind),
-                  ptr(skel), ptr(left), ptr(right), None, r_max, _lib.info_ptr(info), self._s())
-        warn = int(info[_lib.INFO_WARN])
-        if warn & _lib.SP_WARN_ID_PINV:
-            warnings.warn("ID pivots are rank deficient; using pseudo-inverse solve", RankDeficiencyWarning,
-                          stacklevel=3)
-        r_used = int(info[_lib.INFO_LIFT_R])
-        hp, hind, hskel, hleft = to_host_many(p, ind, skel, left[:, :r_used].contiguous())
-        return hp, hind.astype(np.intp), hskel, hleft, right[:r_used], r_used
+        _lib.call("sp_id_from_qr", m, k, perm.data_ptr(), rr.data_ptr(), m, p.data_ptr(), ind.data_ptr(),
+                  _lib.info_ptr(info), self._s())
+        return p, ind, bool(info[_lib.INFO_WARN] & _lib.SP_WARN_ID_PINV)
+
+    def take_rows(self, x, ind):
+        return x.index_select(0, ind).contiguous() if x.shape[1] else x[:ind.shape[0]]
+
+    def scale_cols(self, x, d):
+        dd = self.t.from_numpy(np.ascontiguousarray(d)).to(self.tensor_device)
+        _lib.call("sp_scale_columns", x.shape[0], x.shape[1], x.data_ptr(), x.stride(0), dd.data_ptr(), 0, self._s())
+        return x
+
+    def atz_t(self, a, z):
+        """z^T a for an FP32 a (the TMA A pass widens in registers), r x n."""
+        return self.atz(a, z).t().contiguous()
 
     def complete_other(self, x, r, k, kp):
         if r > 0:
@@ -436,26 +557,103 @@ class DeviceOps:
         return x
 
 
+def _sharded_enrichment(c_i, q, n_c, comm, ops):
+    """E_i = (C C^T)^q C_i, column-sharded like C, with no rank repeating
+    another's products: W = sum_i C_i C_i^T is formed from nearly exact
+    per-rank level products (Ozaki slices on DMMA, csrc/exact_gemm.cu) on a
+    slicing grid common to all ranks (allreduce-max of the row exponents), so
+    the allreduce-sum of the levels is EXACT; then E_i = W C_i locally, nearly
+    exactly rounded with W in double-double.  In exact arithmetic this is the
+    reference's C (C^T C) (src/power.py:282-285); computed this close to it,
+    the greedy pivots downstream are the exact product's."""
+    if q == 0:
+        return c_i
+    e_rows = comm.allreduce_max(ops.exponents(c_i, axis=1), ops)       # per row of C (m)
+    bits, nsl = ops.exact_plan(n_c)
+    ct = ops.transpose(c_i)                                             # n_ci x m: B = C_i^T
+    lv = comm.allreduce_sum(ops.exact_levels(0, c_i, e_rows, ct, e_rows, bits, nsl), ops)
+    w_hi, w_lo = ops.dd_levels(lv, nsl, None)
+    e = c_i
+    lo = None
+    for _ in range(q):
+        e, lo = ops.exact_mm(0, w_hi, w_lo, e, lo)   # (W_hi + W_lo)(E + E_lo)
+    ops.check_finite(e, "power iterate overflowed; enable re-orthonormalization (reorth)")
+    return e
+
+
+def distributed_pivoted_qr(e_i, k: int, comm, ops):
+    """Greedy column-pivoted QR of E^T (src/kernels.py:97-142) where the
+    candidates are the m rows of E and every candidate is sharded across the
+    ranks (E_i: m x n_ci): per step the partial norms, re-orthogonalisation
+    dots, pivot norm and update coefficients are allreduce-summed (m, t, 1, m
+    values).  Returns (perm (m), R (k x m)) -- the same
+    on every rank."""
+    m, n_i = e_i.shape
+    st = ops.pqd_state(e_i, k)
+    pn2 = st.pn2
+    for t in range(k):
+        n2 = comm.allreduce_sum(pn2, ops)
+        delta = ops.pqd_select(st, t, n2)
+        if t > 0:
+            delta = comm.allreduce_sum(delta, ops)
+        part2 = comm.allreduce_sum(ops.pqd_orth(st, t, delta), ops)
+        coef = ops.pqd_coef(st, t, part2)
+        if t + 1 < m:
+            coef = comm.allreduce_sum(coef, ops)
+            pn2 = ops.pqd_update(st, t, coef)
+    ops.pqd_check(st)
+    return st.perm, st.r
+
+
 def sharded_power_id(a_local, c_begin: int, cols, k: int, q: int, comm, ops, r=None, n_total=None):
     """Rank-local part of the column-sharded single-pass power ID (SURVEY.md
-    8(e) item 5, the all-gather variant): the coarse column block C_i is
-    gathered locally and all-gathered (m x |I|, 4.2 GB at cfg5 -- small beside
-    the enrichment's two 2.1-TFLOP products that follow), then every rank runs
-    the selection on the same bytes with the same deterministic kernels, so
-    P, the pivots, the skeleton and the lifting's left factor V_r S_r^-1 come
-    out bitwise identical on every rank; the lifting's right factor U_r^T A_i
-    is this rank's column slab of U_r^T A (the lifting is column-sharded like
-    A).  BASELINE case s0 == A(:, I) (injection at the column set).
+    8(e) item 5, the per-step-allreduce variant; src/power.py:252-308 with an
+    injection sketch at the column set, the BASELINE case s0 == A(:, I)).
 
-    Returns (P m x k, indices k, skeleton k x |I|, left |I| x r, right_i
-    r x n_i, r) -- host arrays for the replicated parts, device for right_i
-    when ops is DeviceOps."""
+    Rank i gathers its coarse columns C_i locally; the enrichment E_i (column
+    slab of C C^T C) and the greedy pivoted QR of E^T are distributed with
+    sketch-sized allreduces only; P and the pivots come out identical on every
+    rank.  The lifting T = (V_r S_r^-1)(U_r^T A) stays factored and sharded:
+    U_r, S_r from the distributed range finder (no gather of C), the left
+    factor's rows V_r,i S_r^-1 = C_i^T U_r S_r^-2 for this rank's coarse
+    columns, the right factor's columns U_r^T A_i for its slab.
+
+    Returns (P m x k, indices k, skeleton_i k x n_ci, left_i n_ci x r,
+    right_i r x n_i, r): P / indices replicated; skeleton and left row-blocks
+    of the coarse index order (rank order = global order: I is ascending and
+    the slabs are contiguous)."""
     cols = _validate_cols(cols, k, n_total)
     m, n_i = a_local.shape
     sel = (cols >= c_begin) & (cols < c_begin + n_i)
     c_i = ops.gather(a_local, cols[sel] - c_begin)
-    c_all = comm.allgather_cols(c_i, ops)                 # m x |I|, global column order
-    return ops.power_id_local(a_local, c_all, cols, k, q, r)
+    n_c = cols.size
+    if k > min(m, n_c):
+        from .errors import ConfigError
+        raise ConfigError(f"rank k={k} outside [1, {min(m, n_c)}]")
+    e_i = _sharded_enrichment(c_i, q, n_c, comm, ops)
+    perm, rr = distributed_pivoted_qr(e_i, k, comm, ops)
+    p, ind, warn = ops.id_from_qr(perm, rr, k)
+    if warn:
+        import warnings as _w
+        from .errors import RankDeficiencyWarning
+        _w.warn("ID pivots are rank deficient; using pseudo-inverse solve", RankDeficiencyWarning, stacklevel=2)
+    skel_i = ops.take_rows(c_i, ind)
+    # lifting rank r = max(k, min(2k, rank)) clamped to the rank (src/rowid.py:130-134)
+    r_req = int(r) if r is not None else 0
+    row0 = int(np.count_nonzero(cols < c_begin))
+    need = max(2 * k, r_req)
+    u, s_c, rank = distributed_sketch_basis(c_i, row0, n_c, 1.0, comm, ops, need=need)
+    r_use = r_req if r_req else max(k, min(2 * k, rank))
+    if r_use > rank:
+        import warnings as _w
+        from .errors import RankDeficiencyWarning
+        _w.warn(f"lifting rank {r_use} clamped to sketch rank {rank}", RankDeficiencyWarning, stacklevel=2)
+        r_use = rank
+    ur = ops.cols(u, 0, r_use)
+    inv2 = 1.0 / (np.asarray(s_c[:r_use], dtype=np.float64) ** 2)
+    left_i = ops.scale_cols(ops.matmul_tn(c_i, ur), inv2)             # C_i^T U_r S_r^-2
+    right_i = ops.matmul_tn(ur, ops.contig(a_local)) if a_local.dtype.itemsize == 8 else ops.atz_t(a_local, ur)
+    return p, ind, skel_i, left_i, right_i, r_use
 
 
 def shard_columns(n: int, world: int, rank: int, align: int = 1) -> tuple[int, int]:

@@ -1,0 +1,103 @@
+"""Host -> HBM ingest: the page-locked staging ring
+for pageable arrays and LRSM files, the direct path for page-locked arrays,
+the fused per-chunk gather, and the pass accounting of src/snapshot_io.py:77-152.
+Bit-exact: the staged matrix and the gathered sketch equal the source bytes."""
+
+import numpy as np
+import pytest
+
+from conftest import philox
+
+import paper_2105_01271_b200 as sp
+from paper_2105_01271_b200 import snapshot_io as sio
+from paper_2105_01271_b200.svd import _sketch_on_ingest
+
+pytestmark = pytest.mark.gpu
+
+
+def _stage(stream, block_rows, op=None, cols=None):
+    s0, c, on_block = (None, None, None)
+    if op is not None:
+        s0, c, on_block = _sketch_on_ingest(op, stream.m, cols)
+    st = sio.stage_stream(stream, block_rows, on_block)
+    return st, s0, c
+
+
+@pytest.mark.parametrize("block_rows", [1, 7, 256, 5000])
+def test_pageable_array_through_the_ring(cuda, block_rows, monkeypatch):
+    monkeypatch.setattr(sio, "CHUNK_BYTES", 1 << 20)  # many chunks, ring wrap-around
+    a = philox(60).standard_normal((700, 3000))
+    a[3, 5] = -0.0
+    op = sp.build_sketch(sp.SketchSpec("injection", 3000, 300))
+    cols = np.arange(0, 3000, 7)
+    stream = sp.ArraySnapshotStream(a)
+    st, s0, c = _stage(stream, block_rows, op, cols)
+    assert stream.passes_completed == 1 and stream.cursor == 700
+    got = st.a.cpu().numpy()
+    assert got.tobytes() == a.tobytes()
+    np.testing.assert_array_equal(s0.cpu().numpy(), sp.apply_sketch(op, a))
+    np.testing.assert_array_equal(c.cpu().numpy(), a[:, cols])
+    assert st.h2d_bytes == a.nbytes
+
+
+def test_pinned_array_is_copied_directly(cuda):
+    a = philox(61).standard_normal((300, 2000))
+    ht = cuda.from_numpy(a).pin_memory()
+    pinned = ht.numpy()
+    assert sio._is_pinned(cuda, pinned)
+    st, _, _ = _stage(sp.ArraySnapshotStream(pinned), 64)
+    assert st.a.cpu().numpy().tobytes() == a.tobytes()
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_lrsm_file_through_the_ring(cuda, tmp_path, kind, monkeypatch):
+    monkeypatch.setattr(sio, "CHUNK_BYTES", 1 << 20)
+    a = philox(62).standard_normal((513, 2100))
+    if kind == 1:
+        a = a.astype(np.float32)
+    path = tmp_path / "a.lrsm"
+    sp.write_snapshots(path, a, scalar_kind=kind)
+    with sp.open_stream(path) as stream:
+        st, _, _ = _stage(stream, 100)
+        assert stream.passes_completed == 1
+        got = st.a.cpu().numpy()
+        assert got.dtype == (np.float32 if kind == 1 else np.float64)
+        assert got.tobytes() == a.tobytes()
+        # the reference's pass audit: a second pass needs a rewind
+        stream.rewind()
+        st2, _, _ = _stage(stream, 1000)
+        assert stream.passes_completed == 2 and st2.a.cpu().numpy().tobytes() == a.tobytes()
+
+
+def test_truncated_file_poisons_the_stream(cuda, tmp_path):
+    a = philox(63).standard_normal((50, 400))
+    path = tmp_path / "a.lrsm"
+    sp.write_snapshots(path, a)
+    stream = sp.open_stream(path)
+    # truncate after opening (the header check passed): the pass must fail loudly
+    with open(path, "r+b") as fh:
+        fh.truncate(sio.HEADER_BYTES + 20 * 400 * 8)
+    with pytest.raises(sp.StreamPoisonedError):
+        _stage(stream, 16)
+    with pytest.raises(sp.StreamPoisonedError):
+        stream.next_block(4)
+    stream.close()
+
+
+def test_power_svd_from_a_pageable_array_and_a_file_agree(cuda, tmp_path):
+    import warnings
+    from paper_2105_01271_b200.datagen import CONFIGS, generate_host
+    cfg = CONFIGS["cfg2"].scaled(m=300, grid=(48, 48), name="ingest")
+    a = generate_host(cfg)
+    op, idx = sp.grid_injection(cfg.grid, cfg.stride)
+    path = tmp_path / "f.lrsm"
+    sp.write_snapshots(path, a)
+    pc = sp.PowerConfig(q=1, columns=idx)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        r1 = sp.power_svd(sp.ArraySnapshotStream(a), op, 10, pc)
+        with sp.open_stream(path) as fs:
+            r2 = sp.power_svd(fs, op, 10, pc, block_rows=33)
+            assert fs.passes_completed == 1
+    assert r1.s.tobytes() == r2.s.tobytes()
+    assert r1.u.tobytes() == r2.u.tobytes() and r1.v.tobytes() == r2.v.tobytes()
