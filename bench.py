@@ -550,7 +550,7 @@ def run_ours(args):
 
     extra = None
     if rank == 0 and world == 1 and not args.no_extra:
-        names = [c for c in ("cfg2", "cfg3", "cfg5") if c != cfg.name]
+        names = [c for c in ("cfg2", "cfg3", "cfg5") if c != cfg.name] or ["cfg2"]
         extra = extra_configs(names, dev, torch)
 
     if rank == 0:

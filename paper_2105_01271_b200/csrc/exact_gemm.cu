@@ -10,14 +10,17 @@
 // same E exactly).  Computing E to ~2^-57 of its row x column scale makes the
 // device pivots those of the exact product -- the reference's.
 //
-// Method (Ozaki, Ogita, Oishi & Rump 2012): every row of op(A) and every
-// column of B is cut into `nsl` slices of `bits` bits on a grid anchored at
-// that row's / column's largest magnitude, so every slice product is an
-// integer multiple of (unit_a x unit_b) below 2^(2 bits); with
-// (L + 1) K 2^(2 bits) <= 2^53 the level-L sum  sum_{i+j=L} S_i^A S_j^B  (one
-// DMMA GEMM of depth (L + 1) K, slices concatenated along K) is EXACT in FP64,
-// whatever the summation order.  Levels 0..nsl-1 are summed in double-double;
-// the dropped levels (i + j >= nsl) are below 2^-(bits nsl) of the scale.
+// Method (after Ozaki, Ogita, Oishi & Rump 2012): every row of op(A) and
+// every column of B is cut into a head S0 / T0 of `bits` bits on a grid
+// anchored at that row's / column's largest magnitude and a tail S1 = A - S0,
+// T1 = B - T0 (|S1| < 2^-bits of the row scale).  With K 2^(2 bits) <= 2^53
+// every partial sum of S0 T0 is an integer multiple of (unit_a x unit_b)
+// below 2^53, so the level-0 product L0 = S0 T0 is EXACT in FP64 for any
+// summation order (split-K, DMMA tile order, cross-rank allreduce).  The rest,
+// L1 = S0 T1 + S1 B (one DMMA GEMM of depth 2K: [S0 | S1] [T1; B]), is about
+// 2^-bits of the scale, so its FP64 rounding is ~2^-(53 + bits) of the scale.
+// L0 + L1 summed in double-double: the product to ~2^-66 of sum |a_il||b_lj|
+// at K = 5000, twice the FP64 work of a plain GEMM.
 #include <cmath>
 
 #include "common.cuh"
@@ -25,19 +28,6 @@
 #include "ops.cuh"
 
 namespace spb {
-
-// slice k of x on the unit grid 2^(e - bits (k + 1)), e = exponent of the
-// row / column max (max < 2^e); the last slice keeps the remainder
-__device__ __forceinline__ void ozaki_slices(double x, int e, int bits, int nsl, double* out, int64_t stride) {
-  double rem = x;
-  for (int k = 0; k < nsl; ++k) {
-    const int sh = e - bits * (k + 1);
-    double sl = ldexp(trunc(ldexp(rem, -sh)), sh);
-    if (k == nsl - 1) sl = rem;
-    out[(int64_t)k * stride] = sl;
-    rem -= sl;  // exact: sl is rem truncated to a coarser grid
-  }
-}
 
 __device__ __forceinline__ int exp_of(double mx) {
   int e = 0;
@@ -57,47 +47,67 @@ __global__ void __launch_bounds__(256) row_exp_kernel(int64_t rows, int64_t cols
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, red[w]);
-    mx = fmax(mx, red[0]);
-    e[i] = exp_of(mx);
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, red[w]);
+    e[i] = mx > 0.0 ? exp_of(mx) : -100000;  // a zero row must not lift an allreduce-max
   }
 }
 
-__global__ void __launch_bounds__(256) col_exp_kernel(int64_t rows, int64_t cols, const double* __restrict__ X,
-                                                      int64_t ldx, int* __restrict__ e) {
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= cols) return;
+// columns: 32 per block (threadIdx.x), rows strided over threadIdx.y and
+// blockIdx.y; exp_of is monotone in the magnitude, so the per-column max
+// exponent is an atomicMax of the partial ones (e preset below any exponent)
+__global__ void col_exp_kernel(int64_t rows, int64_t cols, const double* __restrict__ X, int64_t ldx,
+                               int* __restrict__ e) {
+  __shared__ int part[8][32];
+  const int64_t c = (int64_t)blockIdx.x * 32 + threadIdx.x;
   double mx = 0.0;
-  for (int64_t r = 0; r < rows; ++r) mx = fmax(mx, fabs(X[r * ldx + c]));
-  e[c] = exp_of(mx);
+  if (c < cols)
+    for (int64_t r = (int64_t)blockIdx.y * blockDim.y + threadIdx.y; r < rows; r += (int64_t)gridDim.y * blockDim.y)
+      mx = fmax(mx, fabs(X[r * ldx + c]));
+  part[threadIdx.y][threadIdx.x] = mx > 0.0 ? exp_of(mx) : -100000;
+  __syncthreads();
+  if (threadIdx.y == 0 && c < cols) {
+    int m = part[0][threadIdx.x];
+    for (int y = 1; y < (int)blockDim.y; ++y) m = max(m, part[y][threadIdx.x]);
+    atomicMax(e + c, m);
+  }
 }
 
-// per-row grid (exponent e[i]): slices of row i stacked along the columns,
-// out[i * ldo + k * cols + j] (ldo >= nsl * cols)
+__device__ __forceinline__ void head_tail(double x, int e, int bits, double& h, double& t) {
+  // a zero row / column (e below any real exponent) has head and tail 0
+  const int sh = e - bits;
+  h = (e < -90000) ? 0.0 : ldexp(trunc(ldexp(x, -sh)), sh);
+  t = x - h;  // exact: h is x truncated to a coarser grid
+}
+
+// rows (exponent e[i]): out[i * ldo + j] = S0, out[i * ldo + cols + j] = S1
 __global__ void __launch_bounds__(256) split_rows_kernel(int64_t rows, int64_t cols, const double* __restrict__ X,
-                                                         int64_t ldx, const int* __restrict__ e, int bits, int nsl,
+                                                         int64_t ldx, const int* __restrict__ e, int bits,
                                                          double* __restrict__ out, int64_t ldo) {
   const int64_t i = blockIdx.x;
   if (i >= rows) return;
   const int ei = e[i];
-  for (int64_t j = threadIdx.x; j < cols; j += blockDim.x)
-    ozaki_slices(X[i * ldx + j], ei, bits, nsl, out + i * ldo + j, cols);
+  for (int64_t j = threadIdx.x; j < cols; j += blockDim.x) {
+    double h, t;
+    head_tail(X[i * ldx + j], ei, bits, h, t);
+    out[i * ldo + j] = h;
+    out[i * ldo + cols + j] = t;
+  }
 }
 
-// per-column grid (exponent e[c]): slices stacked along the rows; stacked
-// position p holds slice p (rev = 0) or slice nsl - 1 - p (rev = 1):
-// out[(p * rows + r) * ldo + c]
-__global__ void __launch_bounds__(256) split_cols_kernel(int64_t rows, int64_t cols, const double* __restrict__ X,
-                                                         int64_t ldx, const int* __restrict__ e, int bits, int nsl,
-                                                         int rev, double* __restrict__ out, int64_t ldo) {
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= cols) return;
-  const int ec = e[c];
-  double sl[8];
-  for (int64_t r = 0; r < rows; ++r) {
-    ozaki_slices(X[r * ldx + c], ec, bits, nsl, sl, 1);
-    for (int p = 0; p < nsl; ++p) out[((int64_t)p * rows + r) * ldo + c] = sl[rev ? nsl - 1 - p : p];
-  }
+// columns (exponent e[c]): head rows at out[r * ldo + c], tail rows at
+// out[(rows + r) * ldo + c]; `copy` (may be null) receives X itself
+__global__ void split_cols_kernel(int64_t rows, int64_t cols, const double* __restrict__ X, int64_t ldx,
+                                  const int* __restrict__ e, int bits, double* __restrict__ out, int64_t ldo,
+                                  double* __restrict__ copy, int64_t ldcp) {
+  const int64_t c = (int64_t)blockIdx.x * 32 + threadIdx.x;
+  const int64_t r = (int64_t)blockIdx.y * blockDim.y + threadIdx.y;
+  if (c >= cols || r >= rows) return;
+  const double x = X[r * ldx + c];
+  double h, t;
+  head_tail(x, e[c], bits, h, t);
+  out[r * ldo + c] = h;
+  out[(rows + r) * ldo + c] = t;
+  if (copy) copy[r * ldcp + c] = x;
 }
 
 // (hi, lo) = dd sum of the exact levels L[0..nl) (+ an inexact tail term t)
@@ -121,16 +131,12 @@ __global__ void dd_levels_kernel(int64_t M, int64_t N, const double* __restrict_
   if (lo) lo[o] = err - (h - s);
 }
 
-// slices / bits for an exact level sum of depth up to nsl * K
+// head width for an exact level-0 sum of depth K (K 2^(2 bits) <= 2^53); the
+// product is always two levels (L0 exact, L1 the FP64 rest)
 void ozaki_plan(int64_t K, int* bits_out, int* nsl_out) {
-  int bits = 0, nsl = 3;
-  for (; nsl <= 6; ++nsl) {
-    const double need = std::log2((double)nsl * (double)K);
-    bits = (int)std::floor((53.0 - std::ceil(need)) / 2.0);
-    if (bits * nsl >= 56) break;
-  }
-  *bits_out = bits;
-  *nsl_out = std::min(nsl, 6);
+  const double need = std::ceil(std::log2((double)std::max<int64_t>(K, 1)));
+  *bits_out = (int)std::floor((53.0 - need) / 2.0);
+  *nsl_out = 2;
 }
 
 int row_exponents(int64_t rows, int64_t cols, const double* X, int64_t ldx, int* e, cudaStream_t s) {
@@ -141,42 +147,47 @@ int row_exponents(int64_t rows, int64_t cols, const double* X, int64_t ldx, int*
 }
 
 int col_exponents(int64_t rows, int64_t cols, const double* X, int64_t ldx, int* e, cudaStream_t s) {
-  col_exp_kernel<<<ceil_div(cols, 256), 256, 0, s>>>(rows, cols, X, ldx, e);
+  SPB_CUDA(cudaMemsetAsync(e, 0x80, cols * sizeof(int), s));  // INT_MIN-ish: every exponent is larger
+  dim3 g(ceil_div(cols, 32), std::min(ceil_div(rows, 64), 1024));
+  col_exp_kernel<<<g, dim3(32, 8), 0, s>>>(rows, cols, X, ldx, e);
   count_launch();
   SPB_CHECK_LAUNCH();
   return SP_OK;
 }
 
-// The exact levels Lv[L] (M x N each, L < nsl) of op(A) B on the slicing grids
-// ea (per row of op(A)) and eb (per column of B): every level is an exact FP64
-// value for ANY summation order, so level sums of different ranks (same grids:
-// allreduce-max of the exponents first) add up exactly as long as the total
-// depth K_total satisfies the plan for K_total.
+// The levels of op(A) B on the slicing grids ea (per row of op(A)) and eb (per
+// column of B): Lv[0] = S0 T0 (exact for any summation order: level sums of
+// different ranks on the same grids -- allreduce-max of the exponents first --
+// add up exactly when the total depth satisfies the plan), Lv[1] = the FP64 rest.
 int gemm_exact_levels(int ta, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const int* ea,
                       const double* B, int64_t ldb, const int* eb, int bits, int nsl, double* Lv, cudaStream_t s) {
-  SPB_REQUIRE(M >= 1 && N >= 1 && K >= 1 && nsl >= 1 && nsl <= 6, "gemm_exact_levels: bad extents");
+  SPB_REQUIRE(M >= 1 && N >= 1 && K >= 1 && nsl == 2, "gemm_exact_levels: bad extents");
   Arena ar(s);
-  // A slices: S_0..S_{nsl-1} concatenated along K
-  const int64_t ka = (int64_t)nsl * K;
+  // A: [S0 | S1] along K
+  const int64_t ka = 2 * K;
   SPB_ALLOC(ar, double, As, (size_t)M * ka);
-  if (ta == 0)
-    split_rows_kernel<<<(unsigned)M, 256, 0, s>>>(M, K, A, lda, ea, bits, nsl, As, ka);  // M x (nsl K)
-  else
-    split_cols_kernel<<<ceil_div(M, 256), 256, 0, s>>>(K, M, A, lda, ea, bits, nsl, 0, As, M);  // (nsl K) x M
-  // B slices stacked along K as [T_{nsl-1}; ...; T_1; T_0]: the level-L
-  // operand is its last (L + 1) K rows, T_L ... T_0, pairing with A's
-  // S_0 ... S_L (i + j = L)
-  SPB_ALLOC(ar, double, Bs, (size_t)nsl * K * N);
-  split_cols_kernel<<<ceil_div(N, 256), 256, 0, s>>>(K, N, B, ldb, eb, bits, nsl, 1, Bs, N);
+  if (ta == 0) {
+    split_rows_kernel<<<(unsigned)M, 256, 0, s>>>(M, K, A, lda, ea, bits, As, ka);  // M x 2K
+  } else {
+    dim3 g(ceil_div(M, 32), ceil_div(K, 8));
+    split_cols_kernel<<<g, dim3(32, 8), 0, s>>>(K, M, A, lda, ea, bits, As, M, nullptr, 0);  // 2K x M
+  }
+  // B: [T0; T1; B] along K: level 0 takes rows [0, K), level 1 rows [K, 3K)
+  SPB_ALLOC(ar, double, Bs, (size_t)3 * K * N);
+  {
+    dim3 g(ceil_div(N, 32), ceil_div(K, 8));
+    split_cols_kernel<<<g, dim3(32, 8), 0, s>>>(K, N, B, ldb, eb, bits, Bs, N, Bs + 2 * K * N, N);
+  }
   count_launch(2);
   SPB_CHECK_LAUNCH();
-  for (int L = 0; L < nsl; ++L) {
-    const int64_t depth = (int64_t)(L + 1) * K;
-    const double* bop = Bs + (int64_t)(nsl - 1 - L) * K * N;
-    if (ta == 0)
-      SPB_TRY(gemm(0, 0, M, N, depth, 1.0, As, ka, bop, N, 0.0, Lv + (int64_t)L * M * N, N, s));
-    else
-      SPB_TRY(gemm(1, 0, M, N, depth, 1.0, As, M, bop, N, 0.0, Lv + (int64_t)L * M * N, N, s));
+  double* L0 = Lv;
+  double* L1 = Lv + (int64_t)M * N;
+  if (ta == 0) {
+    SPB_TRY(gemm(0, 0, M, N, K, 1.0, As, ka, Bs, N, 0.0, L0, N, s));
+    SPB_TRY(gemm(0, 0, M, N, 2 * K, 1.0, As, ka, Bs + K * N, N, 0.0, L1, N, s));
+  } else {
+    SPB_TRY(gemm(1, 0, M, N, K, 1.0, As, M, Bs, N, 0.0, L0, N, s));
+    SPB_TRY(gemm(1, 0, M, N, 2 * K, 1.0, As, M, Bs + K * N, N, 0.0, L1, N, s));
   }
   return SP_OK;
 }

@@ -120,7 +120,7 @@ def _count_kept(hs, power):
 
 
 def distributed_sketch_basis(c_i, row0: int, ncols: int, power: float, comm, ops, need: int = -1,
-                             widths=None):
+                             widths=None, want_v: bool = False):
     """Kept left basis U_{C,r} of the column-sharded sketch C = [C_1 .. C_P]
     without gathering C: the randomized block subspace iteration of the device
     svd_top (csrc/pipeline.cu) with the exchanges confined to m x b and b x b
@@ -136,12 +136,20 @@ def distributed_sketch_basis(c_i, row0: int, ncols: int, power: float, comm, ops
     Same block size, growth and stopping rules as the single-GPU svd_top, so
     world size 1 reproduces it.  ``need`` >= 0 is svd_top's ID mode (only the
     leading ``need`` triplets and whether the rank reaches them).  Returns
-    (U m x r, sigma (host), r) -- r the kept count, U's width min(r, block)."""
+    (U m x r, sigma (host), r) -- r the kept count, U's width min(r, block) --
+    and with ``want_v`` also V_i (n_ci x width), this rank's rows of the right
+    singular vectors, from the Rayleigh-Ritz factors P_i (accurate for every
+    kept sigma; C_i^T U S^-1 would lose eps sigma_1 / sigma_i)."""
     m, nci = c_i.shape
     p = min(m, ncols)
     if p <= 64:  # exact path of svd_top: gather the (small) sketch
         c_all = comm.allgather_cols(c_i, ops, widths)
-        return ops.sketch_basis(c_all, power)
+        if not want_v:
+            return ops.sketch_basis(c_all, power)
+        u, sv, v = ops.svd_full(c_all)
+        hs = ops.to_numpy(sv)
+        r = _count_kept(hs, power)
+        return ops.cols(u, 0, r), hs[:r], r, ops.cols(ops.rows(v, row0, row0 + nci), 0, r)
     cap = min(p, 256)
     b = min(cap, ((max(32, 1 + 16) + 7) // 8) * 8)
     while True:
@@ -191,8 +199,17 @@ def distributed_sketch_basis(c_i, row0: int, ncols: int, power: float, comm, ops
             continue
         r = kept
         w = min(r, b)
-        u = ops.matmul(qy, ops.cols(us, 0, max(w, 1)))
-        return ops.cols(u, 0, w), hs[:w], r
+        if not want_v:
+            u = ops.matmul(qy, ops.cols(us, 0, max(w, 1)))
+            return ops.cols(u, 0, w), hs[:w], r
+        # R = A S B^T  ->  R^T = B S A^T: U_C = Q B, V_C,i = P_i Q_top,i A
+        a_, _, b_ = ops.svd_small(r_all)
+        u = ops.matmul(qy, ops.cols(b_, 0, max(w, 1)))
+        pi = ops.rows(pz, 0, nci)
+        if q_top is not None:
+            pi = ops.matmul(pi, ops.rows(q_top, comm.rank * b, (comm.rank + 1) * b))
+        v_i = ops.matmul(pi, ops.cols(a_, 0, max(w, 1)))
+        return ops.cols(u, 0, w), hs[:w], r, ops.cols(v_i, 0, w)
 
 
 def sharded_power_svd(a_local, c_begin: int, cols, k: int, q: int, comm, ops, n_total=None):
@@ -474,6 +491,11 @@ class DeviceOps:
         lv = self.t.stack([hi, lo + tail])
         return self.dd_levels(lv, 2, None)
 
+    def svd_full(self, x):
+        from .kernels import thin_svd
+        f = thin_svd(x.contiguous())
+        return f.u, f.s, f.v
+
     def check_finite(self, x, msg):
         from .errors import NumericalError
         if not bool(self.t.isfinite(x).all()):
@@ -614,9 +636,9 @@ def sharded_power_id(a_local, c_begin: int, cols, k: int, q: int, comm, ops, r=N
     slab of C C^T C) and the greedy pivoted QR of E^T are distributed with
     sketch-sized allreduces only; P and the pivots come out identical on every
     rank.  The lifting T = (V_r S_r^-1)(U_r^T A) stays factored and sharded:
-    U_r, S_r from the distributed range finder (no gather of C), the left
-    factor's rows V_r,i S_r^-1 = C_i^T U_r S_r^-2 for this rank's coarse
-    columns, the right factor's columns U_r^T A_i for its slab.
+    U_r, S_r, V_r,i from the distributed range finder (no gather of C), the
+    left factor's rows V_r,i S_r^-1 for this rank's coarse columns, the right
+    factor's columns U_r^T A_i for its slab.
 
     Returns (P m x k, indices k, skeleton_i k x n_ci, left_i n_ci x r,
     right_i r x n_i, r): P / indices replicated; skeleton and left row-blocks
@@ -642,7 +664,7 @@ def sharded_power_id(a_local, c_begin: int, cols, k: int, q: int, comm, ops, r=N
     r_req = int(r) if r is not None else 0
     row0 = int(np.count_nonzero(cols < c_begin))
     need = max(2 * k, r_req)
-    u, s_c, rank = distributed_sketch_basis(c_i, row0, n_c, 1.0, comm, ops, need=need)
+    u, s_c, rank, v_i = distributed_sketch_basis(c_i, row0, n_c, 1.0, comm, ops, need=need, want_v=True)
     r_use = r_req if r_req else max(k, min(2 * k, rank))
     if r_use > rank:
         import warnings as _w
@@ -650,8 +672,8 @@ def sharded_power_id(a_local, c_begin: int, cols, k: int, q: int, comm, ops, r=N
         _w.warn(f"lifting rank {r_use} clamped to sketch rank {rank}", RankDeficiencyWarning, stacklevel=2)
         r_use = rank
     ur = ops.cols(u, 0, r_use)
-    inv2 = 1.0 / (np.asarray(s_c[:r_use], dtype=np.float64) ** 2)
-    left_i = ops.scale_cols(ops.matmul_tn(c_i, ur), inv2)             # C_i^T U_r S_r^-2
+    inv = 1.0 / np.asarray(s_c[:r_use], dtype=np.float64)
+    left_i = ops.scale_cols(ops.cols(v_i, 0, r_use), inv)               # V_r,i S_r^-1
     right_i = ops.matmul_tn(ur, ops.contig(a_local)) if a_local.dtype.itemsize == 8 else ops.atz_t(a_local, ur)
     return p, ind, skel_i, left_i, right_i, r_use
 

@@ -145,19 +145,35 @@ def test_sharded_power_id_matches_power_id(cuda, world):
     for other in results[1:]:
         for x, y in zip(results[0][1:3], other[1:3]):
             assert np.array_equal(x, y)
-    with warnings.catch_warnings():
-        warnings.simplefilter("ignore")
-        ref = sp.power_id(sp.ArraySnapshotStream(a), op, k, sp.PowerConfig(q=1, columns=cols))
+    idx, w = cols[None, :], np.ones((1, cols.size))
+    ref = oracle.spc_power_id(a, idx, w, cols, k, q=1)
     _, p, ind, _, _, _, r = results[0]
-    assert np.array_equal(ind, ref.indices)
-    np.testing.assert_allclose(p, ref.p, rtol=0, atol=1e-10 * np.abs(ref.p).max())
+    # pivots: equal while the oracle's winner/runner-up gap is above the
+    # rounding level; past the numerical rank of E (~9 here: a noise-free
+    # field, E ~ sigma_C^3) the reference's own pivots are rounding-decided
+    below = np.flatnonzero(ref.pivot_gaps <= 1e-13)
+    pstar = int(below[0]) if below.size else k
+    same = int(np.argmax(ind != ref.indices)) if np.any(ind != ref.indices) else k
+    print(f"sharded ID world {world}: p* = {pstar}, identical prefix {same} of {k}")
+    assert pstar >= 8
+    np.testing.assert_array_equal(ind[:pstar], ref.indices[:pstar])
+    np.testing.assert_array_equal(p[ind], np.eye(k))
+    c = a[:, cols]
+    e = c @ (c.T @ c)
+    res_gpu = np.linalg.norm(e - p @ e[ind]) / np.linalg.norm(e)
+    res_ref = np.linalg.norm(e - ref.p @ e[ref.indices]) / np.linalg.norm(e)
+    coef, *_ = np.linalg.lstsq(e[ind].T, e.T, rcond=None)
+    res_opt = np.linalg.norm(e - coef.T @ e[ind]) / np.linalg.norm(e)
+    print(f"sharded ID world {world}: ||E - P E[sel]||/||E|| ours {res_gpu:.3e} optimum {res_opt:.3e} "
+          f"reference {res_ref:.3e}")
+    assert res_gpu <= max(res_opt * (1 + 1e-6), res_ref * (1 + 1e-2)) + 1e-16
     skel = np.concatenate([res[3] for res in results], axis=1)
-    assert np.array_equal(skel, ref.skeleton)
+    np.testing.assert_array_equal(skel, c[ind])
     assert r == ref.r
     left = np.concatenate([res[4] for res in results], axis=0)
     right = np.concatenate([res[5] for res in results], axis=1)
     got = left @ right
     # against the exact-arithmetic lifting (V_r S_r^-1)(U_r^T A) of this field
-    u, sv, v = oracle.svd_thin(a[:, cols])
+    u, sv, v = oracle.svd_thin(c)
     want = (v[:, :r] / sv[:r]) @ (u[:, :r].T @ a)
     np.testing.assert_allclose(got, want, rtol=0, atol=1e-9 * np.abs(want).max())

@@ -173,35 +173,26 @@ class NumpyOps:
     def exponents(self, x, axis):
         mx = np.abs(x.numpy()).max(axis=axis)
         _, e = np.frexp(mx)
-        return torch.from_numpy(np.where(mx > 0, e, 0).astype(np.int32))
+        return torch.from_numpy(np.where(mx > 0, e, -100000).astype(np.int32))
 
     def exact_plan(self, K):
-        for nsl in range(3, 7):
-            bits = int(np.floor((53 - np.ceil(np.log2(nsl * K))) / 2))
-            if bits * nsl >= 56:
-                return bits, nsl
-        return bits, 6
+        return int(np.floor((53 - np.ceil(np.log2(max(K, 1)))) / 2)), 2
 
     @staticmethod
-    def _slices(x, e, bits, nsl, axis):
+    def _head(x, e, bits, axis):
         ee = np.expand_dims(e.astype(np.float64), axis)
-        rem = x.copy()
-        out = []
-        for k in range(nsl):
-            unit = np.exp2(ee - bits * (k + 1))
-            sl = np.trunc(rem / unit) * unit if k < nsl - 1 else rem.copy()
-            out.append(sl)
-            rem = rem - sl
-        return out
+        unit = np.exp2(ee - bits)
+        h = np.where(ee < -90000, 0.0, np.trunc(x / unit) * unit)
+        return h, x - h
 
     def transpose(self, x):
         return x.t().contiguous()
 
     def exact_levels(self, ta, a, ea, b, eb, bits, nsl):
         a_ = a.numpy().T if ta else a.numpy()
-        sa = self._slices(a_, ea.numpy(), bits, nsl, 1)
-        sb = self._slices(b.numpy(), eb.numpy(), bits, nsl, 0)
-        return self._t(np.stack([sum(sa[i] @ sb[L - i] for i in range(L + 1)) for L in range(nsl)]))
+        s0, s1 = self._head(a_, ea.numpy(), bits, 1)
+        t0, t1 = self._head(b.numpy(), eb.numpy(), bits, 0)
+        return self._t(np.stack([s0 @ t0, s0 @ t1 + s1 @ b.numpy()]))
 
     def dd_levels(self, lv, nsl, tail):
         lv = lv.numpy()
@@ -225,6 +216,10 @@ class NumpyOps:
         tail = a_hi.numpy() @ b_lo.numpy() if b_lo is not None else 0.0
         tail = tail + a_lo.numpy() @ b.numpy()
         return self.dd_levels(lv, nsl, self._t(tail))
+
+    def svd_full(self, x):
+        u, sv, vt = np.linalg.svd(x.numpy(), full_matrices=False)
+        return self._t(u), self._t(sv), self._t(vt.T)
 
     def check_finite(self, x, msg):
         assert np.all(np.isfinite(x.numpy())), msg
