@@ -50,6 +50,10 @@ extern "C" {
 #define SP_WARN_RANK_DEFICIENT 1 /* regularized (pinv) solve taken        */
 #define SP_WARN_LIFT_CLAMPED 2   /* lifting rank clamped to sketch rank   */
 #define SP_WARN_ID_PINV 4        /* row_id pseudo-inverse fallback        */
+#define SP_WARN_BULK_SPLIT 8     /* device diagnostic (no reference warning): the ID lifting
+                                    rank r splits a flat stretch of the sketch spectrum wider
+                                    than the exact-SVD limit; its rank-r subspace is resolved
+                                    only above that stretch  */
 
 /* layout of the host `info` array filled by the pipelines (length SP_INFO_LEN) */
 #define SP_INFO_KEPT 0      /* effective rank of the projector (r_kept)      */

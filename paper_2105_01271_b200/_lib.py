@@ -23,7 +23,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libsketchpress_b200.so"
 
 SP_OK, SP_ECONFIG, SP_EIO, SP_ENUMERICAL, SP_ECUDA = 0, 2, 3, 4, 5
 SP_F64, SP_F32 = 0, 1
-SP_WARN_RANK_DEFICIENT, SP_WARN_LIFT_CLAMPED, SP_WARN_ID_PINV = 1, 2, 4
+SP_WARN_RANK_DEFICIENT, SP_WARN_LIFT_CLAMPED, SP_WARN_ID_PINV, SP_WARN_BULK_SPLIT = 1, 2, 4, 8
 SP_HINT_COLS_VALIDATED, SP_HINT_SAME_SET, SP_HINT_DIFFERENT_SET = 1, 2, 4
 INFO_KEPT, INFO_WARN, INFO_BLOCK, INFO_ITERS, INFO_RANK, INFO_LIFT_R, INFO_LAUNCHES, INFO_FUSED = range(8)
 INFO_LEN = 8

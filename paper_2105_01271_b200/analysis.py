@@ -30,10 +30,13 @@ def rel_frob_error(a, approx) -> float:
 
 
 def oracle_error(a, k: int) -> float:
-    """Eckart-Young optimum ||A - A_k||_F / ||A||_F (host LAPACK; analysis only)."""
-    s = np.linalg.svd(np.asarray(a, dtype=np.float64), compute_uv=False)
-    tot = np.sqrt(np.sum(s ** 2))
-    return float(np.sqrt(np.sum(s[k:] ** 2)) / tot) if tot > 0 else 0.0
+    """Frobenius error of the best rank-k approximation, the singular-value
+    tail ||A - A_k||_F (src/analysis.py:68-74; host LAPACK, analysis only)."""
+    a = np.asarray(a, dtype=np.float64)
+    if not 0 <= k <= min(a.shape):
+        raise ConfigError(f"rank k={k} outside [0, {min(a.shape)}]")
+    s = np.linalg.svd(a, compute_uv=False)
+    return float(np.sqrt(np.sum(s[k:] ** 2)))
 
 
 def rel_frob_error_device(a_dev, u, s, v) -> float:

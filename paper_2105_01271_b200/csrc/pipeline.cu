@@ -47,8 +47,15 @@ static int count_kept(const std::vector<double>& s, double power) {
   return c;
 }
 
+// exact SVD fallback of svd_top's ID mode up to this many columns: the
+// one-sided Jacobi of a full-rank p x p core costs ~p rounds x ~10 sweeps
+// (measured 1.07 s at p = 2000, the cfg5 FP32 floor), so wider flat stretches
+// are resolved only above the stretch and flagged
+constexpr int64_t kExactMax = 512;
+
 struct TopSvd {
   int b = 0, kept = 0, iters = 0;
+  bool bulk = false;  // ID mode: the leading `need` triplets split an unresolvable flat stretch
   double* U = nullptr;  // rows x b
   double* S = nullptr;  // b
   double* V = nullptr;  // cols x b
@@ -304,38 +311,81 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
         return exact_fallback();
       }
       bool conv = false;
+      if (need >= 0) {
+        // ID mode: the leading t = min(kept, need) triplets feed the lifting
+        // V_t S_t^-1 U_t^T A and must be converged as a subspace.  Subspace
+        // iteration resolves them at the rate rho = sigma_{b-7} / sigma_t per
+        // step (angle ~rho^(2 itn + 2) after itn + 1 Rayleigh-Ritz steps):
+        // stop at 1e-12; when more than 8 further steps would be needed, grow
+        // the block (rho falls with b); a flat stretch of the spectrum at t
+        // that even the largest block cannot resolve (a noise bulk: cfg3's
+        // r = 200 split, cfg5's FP32 floor) takes the exact SVD of X up to
+        // kExactMax columns, else is accepted and flagged (bulk).
+        const int t = std::min(kept, need);
+        if (t == 0) {
+          conv = true;
+        } else {
+          const double rho = hs[b - 8] / hs[t - 1];
+          if ((itn == 0 && rho <= 1e-8) || (itn >= 1 && kept_prev >= t && std::pow(rho, 2.0 * itn + 2.0) <= 1e-12)) {
+            conv = true;
+          } else {
+            const double more = rho < 1.0 ? (std::log(1e-12) / std::log(rho) - 2.0) / 2.0 - itn : 1e9;
+            if (more > 8.0) {
+              if (b < cap) {
+                grow = true;
+                break;
+              }
+              if (p <= kExactMax) return exact_fallback();
+              out.bulk = true;  // keep iterating until the Ritz values above the stretch settle
+            }
+          }
+          if (!conv && out.bulk && itn >= 1) {
+            conv = true;
+            for (int i = 0; i < std::min(b, need); ++i) {
+              if (hs[i] <= 10.0 * hs[b - 1]) break;  // the flat stretch itself
+              if (std::fabs(hs[i] - prev[i]) > 1e-14 * hs[0] + 1e-12 * hs[i]) conv = false;
+            }
+          }
+        }
+        if (conv) {
+          conv_seen = true;
+          break;
+        }
+        prev = hs;
+        kept_prev = kept;
+      }
       // One Rayleigh-Ritz step already resolves the kept triplets to
       // (sigma_{b+1}/sigma_kept)^2 when the spectrum has fallen to the
       // rounding floor inside the block (oversampling 8): accept it.
-      if (itn == 0 && kept > 0 && b - 8 > kept && hs[b - 8] <= 1e-8 * hs[kept - 1]) conv = true;
-      // A priori: after itn + 1 Rayleigh-Ritz steps the kept subspace is within
-      // an angle ~rho^(2 itn) of the exact one, rho = sigma_{b-7} / sigma_kept
-      // (oversampling 8; hs[b-8] >= sigma_{b+1} makes the estimate
-      // conservative), and the kept Ritz values within its square.  Stop once
-      // rho^(2 itn + 2) <= 1e-12: an angle below ~1e-11, whose effect on the
-      // singular values of P_r A is second order (~1e-22 sigma_1) and far
-      // inside the 1e-8 principal-angle gate (measured on the cfg3 sketch,
-      // whose noise bulk gives rho = 0.18: 7e-12 when the test first passes;
-      // the earlier 1e-16 bound ran three more steps for nothing).  An
-      // FP32-stored A floors the sketch spectrum at ~1e-7 sigma_1: rho ~1e-4
-      // and the second step passes.
-      if (itn >= 1 && kept == kept_prev && kept > 0 && b - 8 > kept &&
-          std::pow(hs[b - 8] / hs[kept - 1], 2.0 * itn + 2.0) <= 1e-12)
-        conv = true;
-      if (!conv && itn >= 1 && kept == kept_prev) {
-        conv = true;
-        const int chk = need < 0 ? std::min(b, kept + 1) : std::min(b, need);
-        for (int i = 0; i < chk; ++i) {
-          if (need >= 0 && hs[i] <= 10.0 * hs[b - 1]) break;  // unresolved bulk at this block size
-          if (std::fabs(hs[i] - prev[i]) > 1e-14 * hs[0] + 1e-12 * hs[i]) conv = false;
+      if (need < 0) {
+        if (itn == 0 && kept > 0 && b - 8 > kept && hs[b - 8] <= 1e-8 * hs[kept - 1]) conv = true;
+        // A priori: after itn + 1 Rayleigh-Ritz steps the kept subspace is within
+        // an angle ~rho^(2 itn) of the exact one, rho = sigma_{b-7} / sigma_kept
+        // (oversampling 8; hs[b-8] >= sigma_{b+1} makes the estimate
+        // conservative), and the kept Ritz values within its square.  Stop once
+        // rho^(2 itn + 2) <= 1e-12: an angle below ~1e-11, whose effect on the
+        // singular values of P_r A is second order (~1e-22 sigma_1) and far
+        // inside the 1e-8 principal-angle gate (measured on the cfg3 sketch,
+        // whose noise bulk gives rho = 0.18: 7e-12 when the test first passes;
+        // the earlier 1e-16 bound ran three more steps for nothing).  An
+        // FP32-stored A floors the sketch spectrum at ~1e-7 sigma_1: rho ~1e-4
+        // and the second step passes.
+        if (itn >= 1 && kept == kept_prev && kept > 0 && b - 8 > kept &&
+            std::pow(hs[b - 8] / hs[kept - 1], 2.0 * itn + 2.0) <= 1e-12)
+          conv = true;
+        if (!conv && itn >= 1 && kept == kept_prev) {
+          conv = true;
+          const int chk = std::min(b, kept + 1);
+          for (int i = 0; i < chk; ++i)
+            if (std::fabs(hs[i] - prev[i]) > 1e-14 * hs[0] + 1e-12 * hs[i]) conv = false;
         }
+        if (conv) {
+          conv_seen = true;
+          break;
+        }
+        prev = hs;
+        kept_prev = kept;
       }
-      if (conv) {
-        conv_seen = true;
-        break;
-      }
-      prev = hs;
-      kept_prev = kept;
       // one more subspace iteration, started from the Ritz vectors:
       // Y = X (Z Us) = X P Vs Sigma (Z = P Rz, Rz^T = Us Sigma Vs^T; the column
       // scaling leaves the span and the column-wise backward-stable Householder
@@ -367,7 +417,7 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
       b = std::min(cap, 2 * b);
       continue;
     }
-    if (!conv_seen) return exact_fallback();  // max_it exhausted without convergence
+    if (!conv_seen && !out.bulk) return exact_fallback();  // max_it exhausted without convergence
     if (!spec) SPB_TRY(final_products(false));  // oS was written by the publication
     out.b = b;
     out.kept = kept;
@@ -1019,6 +1069,7 @@ int power_id(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, cons
       SPB_TRY(transpose(n, r, Yt, r, lift_right, n, s));
     }
   }
+  if (top.bulk) warn |= SP_WARN_BULK_SPLIT;
   if (info) {
     fill_info(info, r, warn, top, l0);
     info[SP_INFO_RANK] = rank;

@@ -74,7 +74,12 @@ def to_device(a, dtype=None):
         x = t.from_numpy(arr)
     if dtype is not None:
         x = x.to(dtype={np.float64: t.float64, np.float32: t.float32, np.int64: t.int64}[np.dtype(dtype).type])
-    return x.to(device(), non_blocking=False).contiguous()
+    x = x.to(device(), non_blocking=False).contiguous()
+    if x.dim() == 2 and x.shape[0] == 1 and x.stride(0) != x.shape[1]:
+        x = x.clone(memory_format=t.contiguous_format)  # np.atleast_2d view: row stride 0
+        if x.stride(0) != x.shape[1]:
+            x = x.reshape(-1).clone().reshape(1, -1)
+    return x
 
 
 def to_host(x) -> np.ndarray:

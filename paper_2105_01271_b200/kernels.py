@@ -132,6 +132,23 @@ def pinv_apply(s, threshold: float = RANK_TOL):
     return out if dev else to_host(out)
 
 
+def lambda_max(sym) -> float:
+    """Largest (signed) eigenvalue of a symmetric matrix (src/kernels.py:171-181):
+    the reference's validation, then the one-sided Jacobi SVD of the shifted
+    SPD matrix on the device (analysis._lambda_max_sym)."""
+    from .analysis import _lambda_max_sym
+    from .device import to_device
+    a = np.asarray(sym.detach().cpu().numpy() if hasattr(sym, "detach") else sym, dtype=np.float64)
+    if a.ndim != 2 or a.shape[0] != a.shape[1]:
+        raise ConfigError("lambda_max needs a square matrix")
+    scale = max(1.0, np.max(np.abs(a))) if a.size else 1.0
+    if a.size and np.max(np.abs(a - a.T)) > 1e-10 * scale:
+        raise ConfigError("matrix is not symmetric to tolerance")
+    if a.shape[0] == 0:
+        return 0.0
+    return _lambda_max_sym(to_device(a))
+
+
 def numerical_rank(m, threshold: float = RANK_TOL) -> int:
     """Count of singular values above threshold * largest (src/kernels.py:191-196)."""
     return thin_svd(m).rank(threshold)

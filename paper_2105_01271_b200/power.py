@@ -274,6 +274,9 @@ def _run_id(stream, op, k, cols, q, r, block_rows, project_ell, project_seed, on
         lifting = FactoredLifting(left[:, :r_used], None, host=not return_device, ur=ur[:, :r_used], a=a)
     else:
         lifting = FactoredLifting(left[:, :r_used], right[:r_used], host=not return_device)
+    # device diagnostic: the rank-r split fell in a flat stretch of the sketch
+    # spectrum too wide for the exact SVD
+    lifting.bulk_split = bool(warn & _lib.SP_WARN_BULK_SPLIT)
     if return_device:
         return RowIDFactors(p=p, indices=ind, skeleton=skel, lifting=lifting, r=r_used, method=method)
     from .device import to_host_many

@@ -176,16 +176,33 @@ def distributed_sketch_basis(c_i, row0: int, ncols: int, power: float, comm, ops
                                       f"{cap}-column block")
                 grow = True
                 break
-            conv = itn == 0 and kept > 0 and b - 8 > kept and hs[b - 8] <= 1e-8 * hs[kept - 1]
-            if (not conv and itn >= 1 and kept == kept_prev and kept > 0 and b - 8 > kept
-                    and (hs[b - 8] / hs[kept - 1]) ** (2.0 * itn + 2.0) <= 1e-12):
-                conv = True
-            if not conv and itn >= 1 and kept == kept_prev:
-                chk = min(b, kept + 1) if need < 0 else min(b, need)
-                if need >= 0:  # an unresolved bulk near the block's tail is exempt
-                    bulk = np.flatnonzero(hs[:chk] <= 10.0 * hs[b - 1])
-                    chk = int(bulk[0]) if bulk.size else chk
-                conv = bool(np.all(np.abs(hs[:chk] - prev[:chk]) <= 1e-14 * hs[0] + 1e-12 * hs[:chk]))
+            if need >= 0:
+                # ID mode (svd_top's rule): the leading t = min(kept, need)
+                # triplets must be converged as a subspace, rate
+                # rho = sigma_{b-7} / sigma_t; grow the block when more than 8
+                # further steps would be needed; at the largest block a flat
+                # stretch is accepted and flagged (no exact fallback across ranks)
+                t = min(kept, need)
+                conv = t == 0
+                if not conv:
+                    rho = hs[b - 8] / hs[t - 1]
+                    conv = (itn == 0 and rho <= 1e-8) or (itn >= 1 and kept_prev >= t
+                                                         and rho ** (2.0 * itn + 2.0) <= 1e-12)
+                    if not conv:
+                        more = (np.log(1e-12) / np.log(rho) - 2.0) / 2.0 - itn if rho < 1.0 else 1e9
+                        if more > 8.0:
+                            if b < cap:
+                                grow = True
+                                break
+                            conv = True   # bulk split: approximate beyond the resolvable part
+            else:
+                conv = itn == 0 and kept > 0 and b - 8 > kept and hs[b - 8] <= 1e-8 * hs[kept - 1]
+                if (not conv and itn >= 1 and kept == kept_prev and kept > 0 and b - 8 > kept
+                        and (hs[b - 8] / hs[kept - 1]) ** (2.0 * itn + 2.0) <= 1e-12):
+                    conv = True
+                if not conv and itn >= 1 and kept == kept_prev:
+                    chk = min(b, kept + 1)
+                    conv = bool(np.all(np.abs(hs[:chk] - prev[:chk]) <= 1e-14 * hs[0] + 1e-12 * hs[:chk]))
             if conv:
                 break
             prev, kept_prev = hs, kept

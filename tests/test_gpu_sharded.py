@@ -109,13 +109,23 @@ def test_two_shards_match_target(cuda):
     np.testing.assert_allclose((u * s) @ v.T, (tu * ts) @ tv.T, atol=1e-10 * np.abs(a).max())
 
 
+def _id_case():
+    """20 gap-determined ID pivots (a slow-decay block, tests/golden/id_slow.npz
+    construction): the per-rank partial sums may not move the selection."""
+    from conftest import philox, rank_deficient
+    a = rank_deficient(philox(41), 300, 3072, rank=80, decay=np.logspace(0, -1, 80))
+    return a, np.arange(0, 3072, 12)
+
+
 @pytest.mark.parametrize("world", [1, 2, 3])
-def test_sharded_power_id_matches_power_id(cuda, world):
+def test_sharded_power_id_matches_oracle(cuda, world):
     # per-step-allreduce variant of the column-sharded ID: exact enrichment
     # levels allreduce-summed, the pivoted QR's partial sums allreduce-summed
     # (pivqr_dist.cu); P and the pivots bitwise identical on every shard and
-    # equal to the single-GPU power_id's; skeleton / lifting factors sharded
-    cfg, a, op, cols = _case()
+    # equal to the oracle's (all 20 gap-determined); skeleton and the lifting
+    # factors sharded and assembled
+    a, cols = _id_case()
+    n = a.shape[1]
     k = 20
     shared = {"slots": [None] * world, "bar": threading.Barrier(world)}
     results = [None] * world
@@ -124,12 +134,12 @@ def test_sharded_power_id_matches_power_id(cuda, world):
     def run(rank):
         try:
             cuda.cuda.set_device(0)
-            b, e = shard_columns(cfg.n, world, rank, align=cfg.grid[1])
+            b, e = shard_columns(n, world, rank, align=96)
             ad = cuda.from_numpy(a[:, b:e].copy()).cuda()
             comm = ThreadComm(rank, world, shared) if world > 1 else TorchComm()
             with warnings.catch_warnings():
                 warnings.simplefilter("ignore")
-                out = sharded_power_id(ad, b, cols, k, 1, comm, DeviceOps(), n_total=cfg.n)
+                out = sharded_power_id(ad, b, cols, k, 1, comm, DeviceOps(), n_total=n)
             cuda.cuda.synchronize()
             results[rank] = (b,) + tuple(x.cpu().numpy() if hasattr(x, "cpu") else x for x in out)
         except Exception as exc:  # surface in the main thread
@@ -147,33 +157,18 @@ def test_sharded_power_id_matches_power_id(cuda, world):
             assert np.array_equal(x, y)
     idx, w = cols[None, :], np.ones((1, cols.size))
     ref = oracle.spc_power_id(a, idx, w, cols, k, q=1)
+    assert np.all(ref.pivot_gaps > 1e-11)
     _, p, ind, _, _, _, r = results[0]
-    # pivots: equal while the oracle's winner/runner-up gap is above the
-    # rounding level; past the numerical rank of E (~9 here: a noise-free
-    # field, E ~ sigma_C^3) the reference's own pivots are rounding-decided
-    below = np.flatnonzero(ref.pivot_gaps <= 1e-13)
-    pstar = int(below[0]) if below.size else k
-    same = int(np.argmax(ind != ref.indices)) if np.any(ind != ref.indices) else k
-    print(f"sharded ID world {world}: p* = {pstar}, identical prefix {same} of {k}")
-    assert pstar >= 8
-    np.testing.assert_array_equal(ind[:pstar], ref.indices[:pstar])
-    np.testing.assert_array_equal(p[ind], np.eye(k))
+    np.testing.assert_array_equal(ind, ref.indices)
+    np.testing.assert_allclose(p, ref.p, rtol=0, atol=1e-10 * np.abs(ref.p).max())
     c = a[:, cols]
-    e = c @ (c.T @ c)
-    res_gpu = np.linalg.norm(e - p @ e[ind]) / np.linalg.norm(e)
-    res_ref = np.linalg.norm(e - ref.p @ e[ref.indices]) / np.linalg.norm(e)
-    coef, *_ = np.linalg.lstsq(e[ind].T, e.T, rcond=None)
-    res_opt = np.linalg.norm(e - coef.T @ e[ind]) / np.linalg.norm(e)
-    print(f"sharded ID world {world}: ||E - P E[sel]||/||E|| ours {res_gpu:.3e} optimum {res_opt:.3e} "
-          f"reference {res_ref:.3e}")
-    assert res_gpu <= max(res_opt * (1 + 1e-6), res_ref * (1 + 1e-2)) + 1e-16
     skel = np.concatenate([res[3] for res in results], axis=1)
     np.testing.assert_array_equal(skel, c[ind])
     assert r == ref.r
     left = np.concatenate([res[4] for res in results], axis=0)
     right = np.concatenate([res[5] for res in results], axis=1)
     got = left @ right
-    # against the exact-arithmetic lifting (V_r S_r^-1)(U_r^T A) of this field
+    # against the exact-arithmetic lifting (V_r S_r^-1)(U_r^T A)
     u, sv, v = oracle.svd_thin(c)
     want = (v[:, :r] / sv[:r]) @ (u[:, :r].T @ a)
     np.testing.assert_allclose(got, want, rtol=0, atol=1e-9 * np.abs(want).max())
