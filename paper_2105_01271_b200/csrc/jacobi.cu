@@ -90,8 +90,12 @@ jacobi_kernel(int n, int np, const double* __restrict__ M, int64_t ldm, double* 
   }
   __syncthreads();
   const int na = nact_s;
+  __shared__ unsigned long long relmax_bits;  // largest |g| / sqrt(a b) rotated this sweep
   for (int sweep = 0; sweep < kJacMaxSweeps && na >= 2; ++sweep) {
-    if (tid == 0) rot_count = 0;
+    if (tid == 0) {
+      rot_count = 0;
+      relmax_bits = 0ull;
+    }
     __syncthreads();
     for (int round = 0; round < na - 1; ++round) {
       for (int k = warp; k < na / 2; k += nwarps) {
@@ -135,12 +139,18 @@ jacobi_kernel(int n, int np, const double* __restrict__ M, int64_t ldm, double* 
             vp[i] = c * u - s * w;
             vq[i] = fma(s, u, c * w);
           }
-          if (lane == 0) atomicAdd(&rot_count, 1);
+          if (lane == 0) {
+            atomicAdd(&rot_count, 1);
+            atomicMax(&relmax_bits, (unsigned long long)__double_as_longlong(fabs(g) / (sqrt(a) * sqrt(b))));
+          }
         }
       }
       __syncthreads();
     }
-    if (rot_count == 0) break;
+    // quadratic convergence: a sweep whose rotations were all below kJacQuad
+    // in relative size leaves only ~kJacQuad^2-sized ones for the next, which
+    // would only confirm convergence (the jacobi32 rule)
+    if (rot_count == 0 || __longlong_as_double((long long)relmax_bits) < kJacQuad) break;
     __syncthreads();
   }
   // singular values = column norms, sorted descending (stable by index)
@@ -396,7 +406,8 @@ constexpr int kJgThreads = 128;
 __global__ void __launch_bounds__(kJgThreads)
 jacobi_grid_kernel(int n, int np, const double* __restrict__ M, int64_t ldm, bool trans, double* __restrict__ U,
                    int64_t ldu, double* __restrict__ S, double* __restrict__ Vout, int64_t ldv,
-                   double* __restrict__ W, double* __restrict__ Vm, double* __restrict__ cn, int* rot) {
+                   double* __restrict__ W, double* __restrict__ Vm, double* __restrict__ cn, int* rot,
+                   unsigned long long* relmax) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ int act[];  // np entries (dynamic: n is not capped at 256)
   __shared__ int na_s;
@@ -409,7 +420,10 @@ jacobi_grid_kernel(int n, int np, const double* __restrict__ M, int64_t ldm, boo
     W[e] = (i < n && c < n) ? (trans ? M[(int64_t)c * ldm + i] : M[(int64_t)i * ldm + c]) : 0.0;
     Vm[e] = (i == c) ? 1.0 : 0.0;
   }
-  if (gtid < 2) rot[gtid] = 0;
+  if (gtid < 2) {
+    rot[gtid] = 0;
+    relmax[gtid] = 0ull;
+  }
   grid.sync();
   for (int c = gwarp; c < np; c += nwarps) {
     double a = 0.0;
@@ -432,7 +446,10 @@ jacobi_grid_kernel(int n, int np, const double* __restrict__ M, int64_t ldm, boo
   const int na = na_s;
   for (int sweep = 0; sweep < kJacMaxSweeps && na >= 2; ++sweep) {
     for (int round = 0; round < na - 1; ++round) {
-      if (round == 1 && gtid == 0) rot[(sweep + 1) & 1] = 0;  // nobody reads it until this sweep ends
+      if (round == 1 && gtid == 0) {  // nobody reads the other parity until this sweep ends
+        rot[(sweep + 1) & 1] = 0;
+        relmax[(sweep + 1) & 1] = 0ull;
+      }
       for (int k = gwarp; k < na / 2; k += nwarps) {
         int pi, qi;
         rr_pair(na, round, k, pi, qi);
@@ -474,12 +491,19 @@ jacobi_grid_kernel(int n, int np, const double* __restrict__ M, int64_t ldm, boo
             vp[i] = cs * u - sn * w;
             vq[i] = fma(sn, u, cs * w);
           }
-          if (lane == 0) atomicOr(&rot[sweep & 1], 1);
+          if (lane == 0) {
+            atomicOr(&rot[sweep & 1], 1);
+            atomicMax(&relmax[sweep & 1], (unsigned long long)__double_as_longlong(fabs(g) / (sqrt(a) * sqrt(b))));
+          }
         }
       }
       grid.sync();
     }
-    if (*(volatile int*)&rot[sweep & 1] == 0) break;  // same value in every thread after the barrier
+    // same values in every thread after the barrier; the quadratic-convergence
+    // stop of the single-CTA kernels
+    if (*(volatile int*)&rot[sweep & 1] == 0 ||
+        __longlong_as_double((long long)*(volatile unsigned long long*)&relmax[sweep & 1]) < kJacQuad)
+      break;
   }
   // singular values = column norms, sorted descending (stable by index)
   for (int c = gwarp; c < np; c += nwarps) {
@@ -560,7 +584,8 @@ int jacobi_svd_tr(int64_t n, const double* M, int64_t ldm, bool trans, double* U
     double* gV = gar.alloc<double>((size_t)np * np);
     double* cn = gar.alloc<double>((size_t)np);
     int* rot = gar.alloc<int>(2);
-    if (!gW || !gV || !cn || !rot) {
+    unsigned long long* relmax = gar.alloc<unsigned long long>(2);
+    if (!gW || !gV || !cn || !rot || !relmax) {
       set_error("jacobi workspace allocation failed");
       return SP_ECUDA;
     }
@@ -574,7 +599,7 @@ int jacobi_svd_tr(int64_t n, const double* M, int64_t ldm, bool trans, double* U
     grid = std::max(1, std::min(grid, per_sm * kNumSMs));
     int n_i = (int)n, np_i = np;
     bool tr = false;  // M was transposed into scratch above when trans
-    void* args[] = {&n_i, &np_i, &M, &ldm, &tr, &U, &ldu, &S, &V, &ldv, &gW, &gV, &cn, &rot};
+    void* args[] = {&n_i, &np_i, &M, &ldm, &tr, &U, &ldu, &S, &V, &ldv, &gW, &gV, &cn, &rot, &relmax};
     SPB_CUDA(cudaLaunchCooperativeKernel((const void*)jacobi_grid_kernel, dim3(grid), dim3(kJgThreads), args, act_smem,
                                          s));
     count_launch();

@@ -201,3 +201,43 @@ def test_factored_lifting_host_algebra():
     f = sp.RowIDFactors(p=np.eye(6)[:, :4], indices=np.arange(4), skeleton=philox(8).standard_normal((4, 6)),
                         lifting=lift)
     np.testing.assert_allclose(f.reconstruct(), f.p @ f.skeleton @ dense)
+
+
+def test_staging_chunk_plan():
+    from paper_2105_01271_b200 import snapshot_io as sio
+    assert sio.chunk_rows(8 << 20, 256) == 8            # cfg4 rows: 8 per 64 MB chunk
+    assert sio.chunk_rows(512 << 10, 256) == 128        # cfg2 rows
+    assert sio.chunk_rows(512 << 10, 7) == 7            # never more than a stream block
+    assert sio.chunk_rows(1 << 30, 256) == 1
+    for rows, parts in ((10, 3), (5, 8), (1 << 20, 16)):
+        sp_ = sio.split_rows(rows, parts)
+        assert sp_[0][0] == 0 and sp_[-1][1] == rows
+        assert all(a[1] == b[0] for a, b in zip(sp_, sp_[1:])) and len(sp_) == min(rows, parts)
+
+
+def test_parallel_copy_is_exact():
+    from paper_2105_01271_b200 import snapshot_io as sio
+    src = np.random.default_rng(3).standard_normal((300, 5000))
+    dst = np.empty_like(src)
+    sio._parallel_copy(dst, src)
+    assert dst.tobytes() == src.tobytes()
+    d32 = np.empty((300, 5000), dtype=np.float32)
+    sio._parallel_copy(d32, src)                        # dtype conversion path
+    assert np.array_equal(d32, src.astype(np.float32))
+
+
+def test_oracle_pivots_and_gaps_agree_with_interp_rows():
+    import oracle
+    x = np.random.default_rng(4).standard_normal((40, 25)) * np.logspace(0, -3, 25)
+    piv, gaps = oracle.greedy_pivots_and_gaps(x.T, 10)
+    assert np.array_equal(piv, oracle.interp_rows(x, 10).indices)
+    assert np.array_equal(gaps, oracle.pivot_gaps(x.T, 10))
+
+
+def test_host_column_generator_matches_the_field():
+    from paper_2105_01271_b200.datagen import CONFIGS, generate_host, generate_host_columns
+    cfg = CONFIGS["cfg2"].scaled(m=50, grid=(32, 32), name="cols")
+    a = generate_host(cfg)
+    cols = np.array([0, 7, 33, 500, 1023])
+    np.testing.assert_allclose(generate_host_columns(cfg, 20, cols), a[:20, cols], rtol=0,
+                               atol=1e-13 * np.abs(a).max())
