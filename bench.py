@@ -209,12 +209,13 @@ def time_cpu_sample(cfg, steps, warmup, threads):
     from threadpoolctl import threadpool_limits
     blk, idx_l, lo, hi, desc = cpu_sample(cfg)
     w = np.ones((1, idx_l.size))
+    hc = np.zeros((hi - lo, idx_l.size))     # the pass's accumulator: allocated once, as the reference's hc
     times = []
     with threadpool_limits(threads), warnings.catch_warnings():
         warnings.simplefilter("ignore")
         for i in range(warmup + steps):
             t0 = time.perf_counter()
-            oracle.accumulate_block_slab(blk, idx_l[None, :], w, idx_l, lo, hi)
+            oracle.accumulate_block_slab(blk, idx_l[None, :], w, idx_l, lo, hi, hc)
             dt = time.perf_counter() - t0
             if i >= warmup:
                 times.append(dt)

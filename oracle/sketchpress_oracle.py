@@ -291,7 +291,7 @@ def one_pass_power(a, idx, w, cols, block_rows=BLOCK, coarse_gram=False,
     return s0, c, coarse, gram, hc
 
 
-def accumulate_block_slab(blk, idx, w, cols, lo, hi):
+def accumulate_block_slab(blk, idx, w, cols, lo, hi, hc_slab=None):
     """One stream block of src/power.py:198-212 (the loop body of
     _power_accumulate, with_column_gram=True) restricted to the rows
     [lo, hi) of hc: s0 and C rows of the block and this block's contribution
@@ -299,10 +299,13 @@ def accumulate_block_slab(blk, idx, w, cols, lo, hi):
     row slab is identical in kind and independent, so timing one (block,
     slab) pair times a known fraction of the reference's accumulate pass --
     the CPU-baseline sample of bench.py at configurations whose full hc
-    (n x |I|, 137 GB at cfg4) cannot be held."""
+    (n x |I|, 137 GB at cfg4) cannot be held.  ``hc_slab`` is the running
+    accumulator (allocated once per pass, as the reference's hc is)."""
     piece = sketch_rows(blk, idx, w)
     sub = take_columns(blk, cols)
-    hc_slab = blk[:, lo:hi].T @ sub
+    if hc_slab is None:
+        hc_slab = np.zeros((hi - lo, sub.shape[1]))
+    hc_slab += blk[:, lo:hi].T @ sub          # the reference's in-place accumulation (:211)
     return piece, sub, hc_slab
 
 

@@ -215,8 +215,14 @@ __device__ __forceinline__ double jsum(const double (*p)[32], int c) {
 template <int NW, int RPW>
 __global__ void __launch_bounds__(NW * 32)
 jacobi32_kernel(int n, const double* __restrict__ M, int64_t ldm, double* __restrict__ U, int64_t ldu,
-                double* __restrict__ S, double* __restrict__ Vout, int64_t ldv, bool trans) {
+                double* __restrict__ S, double* __restrict__ Vout, int64_t ldv, bool trans, int64_t bsM = 0,
+                int64_t bsU = 0, int64_t bsS = 0, int64_t bsV = 0) {
   SPB_PDL_ENTRY();
+  // batched launches (block Jacobi): CTA b works on the b-th core
+  M += blockIdx.x * bsM;
+  U += blockIdx.x * bsU;
+  S += blockIdx.x * bsS;
+  if (Vout) Vout += blockIdx.x * bsV;
   __shared__ double part[2][NW][32][2];
   __shared__ double nrm_s[NW][32];
   __shared__ double sig_s[32];
@@ -532,6 +538,18 @@ jacobi_grid_kernel(int n, int np, const double* __restrict__ M, int64_t ldm, boo
   }
 }
 
+// batch independent n x n SVDs (n <= 32), core b at M + b bsM (its U, S, V
+// likewise): the pair solves of the block Jacobi (bjacobi.cu)
+int jacobi32_batched(int n, int batch, const double* M, int64_t ldm, int64_t bsM, double* U, int64_t ldu,
+                     int64_t bsU, double* S, int64_t bsS, double* V, int64_t ldv, int64_t bsV, cudaStream_t s) {
+  SPB_REQUIRE(n >= 1 && n <= 32 && batch >= 1, "jacobi32_batched: 1 <= n <= 32");
+  jacobi32_kernel<kJ32Warps, 8><<<batch, kJ32Warps * 32, 0, s>>>(n, M, ldm, U, ldu, S, V, ldv, false, bsM, bsU, bsS,
+                                                                  bsV);
+  count_launch();
+  SPB_CHECK_LAUNCH();
+  return SP_OK;
+}
+
 int jacobi_svd(int64_t n, const double* M, int64_t ldm, double* U, int64_t ldu, double* S,
                double* V, int64_t ldv, cudaStream_t s) {
   return jacobi_svd_tr(n, M, ldm, false, U, ldu, S, V, ldv, s);
@@ -543,13 +561,15 @@ int jacobi_svd_tr(int64_t n, const double* M, int64_t ldm, bool trans, double* U
                   double* V, int64_t ldv, cudaStream_t s) {
   SPB_REQUIRE(n >= 1 && n <= 50000, "Jacobi SVD supports 1 <= n <= 50000");
   if (n <= 8) {
-    SPB_CUDA(launch_pdl((jacobi32_kernel<1, 8>), dim3(1), dim3(32), 0, s, (int)n, M, ldm, U, ldu, S, V, ldv, trans));
+    SPB_CUDA(launch_pdl((jacobi32_kernel<1, 8>), dim3(1), dim3(32), 0, s, (int)n, M, ldm, U, ldu, S, V, ldv, trans,
+                        (int64_t)0, (int64_t)0, (int64_t)0, (int64_t)0));
     count_launch();
     SPB_CHECK_LAUNCH();
     return SP_OK;
   }
   if (n <= 32) {
-    SPB_CUDA(launch_pdl((jacobi32_kernel<kJ32Warps, 8>), dim3(1), dim3(kJ32Warps * 32), 0, s, (int)n, M, ldm, U, ldu, S, V, ldv, trans));
+    SPB_CUDA(launch_pdl((jacobi32_kernel<kJ32Warps, 8>), dim3(1), dim3(kJ32Warps * 32), 0, s, (int)n, M, ldm, U, ldu, S,
+                        V, ldv, trans, (int64_t)0, (int64_t)0, (int64_t)0, (int64_t)0));
     count_launch();
     SPB_CHECK_LAUNCH();
     return SP_OK;

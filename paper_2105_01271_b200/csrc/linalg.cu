@@ -317,6 +317,50 @@ int complete_basis(int64_t N, int r, int k, double* out, int64_t ldo, uint64_t s
 // replace the left factor's columns past the last S_i > 1e-15 ||S||_2-sum by
 // an orthonormal completion (the reference's gesdd returns a full orthonormal
 // U for a rank-deficient input).  Synchronises (reads S).
+int block_jacobi_svd(int64_t N, int64_t n, const double* M, int64_t ldm, bool trans, double* U, int64_t ldu,
+                     double* S, double* V, int64_t ldv, cudaStream_t s);
+
+__global__ void row_sumsq_kernel(int64_t rows, int64_t cols, const double* __restrict__ X, int64_t ldx,
+                                 double* __restrict__ out) {
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  double a = 0.0;
+  for (int64_t c = lane; c < cols; c += 32) a = fma(X[r * ldx + c], X[r * ldx + c], a);
+  a = warp_sum(a);
+  if (lane == 0) out[r] = a;
+}
+
+// Columns of M^T (rows of M, p x p) the one-sided Jacobi would rotate: squared
+// norm above 1e-30 of the total (the negligibility rule of jacobi.cu).  Synchronises.
+static int active_rows(int64_t p, const double* M, int64_t ldm, int64_t* count, cudaStream_t s) {
+  Arena ar(s);
+  SPB_ALLOC(ar, double, nr, (size_t)p);
+  row_sumsq_kernel<<<ceil_div(p * 32, 256), 256, 0, s>>>(p, p, M, ldm, nr);
+  SPB_LAUNCHED();
+  std::vector<double> h((size_t)p);
+  SPB_TRY(read_small(h.data(), nr, p * sizeof(double), s));
+  double fro = 0.0;
+  for (double x : h) fro += x;
+  int64_t c = 0;
+  for (double x : h) c += x > 1e-30 * fro ? 1 : 0;
+  *count = c;
+  return SP_OK;
+}
+
+// SVD of M^T for a p x p core M (the rows of M are the Jacobi columns):
+// M^T = U S V^T.  More than kBlockJacobiMin active columns: the block Jacobi
+// (bjacobi.cu, nb - 1 rounds per sweep); otherwise the scalar one-sided Jacobi
+// (jacobi.cu), which skips the negligible columns and is faster for few.
+constexpr int64_t kBlockJacobiMin = 512;
+static int core_svd_rows(int64_t p, const double* M, int64_t ldm, double* U, int64_t ldu, double* S, double* V,
+                         int64_t ldv, cudaStream_t s) {
+  int64_t act = p;
+  if (p > kBlockJacobiMin) SPB_TRY(active_rows(p, M, ldm, &act, s));
+  if (act > kBlockJacobiMin) return block_jacobi_svd(p, p, M, ldm, /*trans=*/true, U, ldu, S, V, ldv, s);
+  return jacobi_svd_tr(p, M, ldm, /*trans=*/true, U, ldu, S, V, ldv, s);
+}
+
 static int complete_null_columns(int64_t p, const double* S, double* Ucols, int64_t ldu, cudaStream_t s) {
   std::vector<double> hs((size_t)p);
   SPB_TRY(read_small(hs.data(), S, p * sizeof(double), s));
@@ -364,7 +408,7 @@ int thin_svd(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* U
     // rows of R beyond the numerical rank are rounding-sized and never enter
     // the Jacobi schedule, so a low-rank sketch costs rounds only for its rank.
     SPB_TRY(tsqr(rows, cols, X, ldx, Q, p, R, p, s));
-    SPB_TRY(jacobi_svd_tr(p, R, p, /*trans=*/true, V, ldv, S, Us, p, s));
+    SPB_TRY(core_svd_rows(p, R, p, V, ldv, S, Us, p, s));
     SPB_TRY(complete_null_columns(p, S, V, ldv, s));
     SPB_TRY(gemm(0, 0, rows, p, p, 1.0, Q, p, Us, p, 0.0, U, ldu, s));
   } else if (rows >= cols) {
@@ -397,9 +441,14 @@ int thin_svd_t(int64_t rows, int64_t cols, const double* Xt, int64_t ldxt, doubl
   SPB_ALLOC(ar, double, Rt, (size_t)p * p);
   SPB_ALLOC(ar, double, Vs, (size_t)p * p);
   SPB_TRY(tsqr(cols, rows, Xt, ldxt, Q, p, R, p, s));
-  SPB_TRY(transpose(p, p, R, p, Rt, p, s));
-  SPB_TRY(jacobi_svd(p, Rt, p, U, ldu, S, Vs, p, s));
-  if (p > kSmallCore) SPB_TRY(complete_null_columns(p, S, U, ldu, s));
+  if (p > kSmallCore) {
+    // X^T = Q R -> X = R^T Q^T; SVD of R^T by Jacobi on the rows of R
+    SPB_TRY(core_svd_rows(p, R, p, U, ldu, S, Vs, p, s));
+    SPB_TRY(complete_null_columns(p, S, U, ldu, s));
+  } else {
+    SPB_TRY(transpose(p, p, R, p, Rt, p, s));
+    SPB_TRY(jacobi_svd(p, Rt, p, U, ldu, S, Vs, p, s));
+  }
   SPB_TRY(gemm(0, 0, cols, p, p, 1.0, Q, p, Vs, p, 0.0, V, ldv, s));
   SPB_TRY(sign_fix(rows, p, U, ldu, V, ldv, cols, false, s));
   return SP_OK;

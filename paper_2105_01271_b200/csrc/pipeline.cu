@@ -264,6 +264,7 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
       return SP_OK;
     };
     bool spec = false, conv_seen = false;
+    int bulk_from = 0;
     for (int itn = 0; itn < max_it; ++itn) {
       // Rayleigh-Ritz: Q^T X = Z^T with Z = X^T Q = P Rz  ->  Q^T X = Rz^T P^T
       // Z = P Rz: only Rz is needed unless V is wanted (R alone: Cholesky of
@@ -336,14 +337,18 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
                 break;
               }
               if (p <= kExactMax) return exact_fallback();
-              out.bulk = true;  // keep iterating until the Ritz values above the stretch settle
+              if (!out.bulk) bulk_from = itn;
+              out.bulk = true;  // a few more steps: the Ritz values above the stretch settle
             }
           }
           if (!conv && out.bulk && itn >= 1) {
-            conv = true;
-            for (int i = 0; i < std::min(b, need); ++i) {
-              if (hs[i] <= 10.0 * hs[b - 1]) break;  // the flat stretch itself
-              if (std::fabs(hs[i] - prev[i]) > 1e-14 * hs[0] + 1e-12 * hs[i]) conv = false;
+            conv = itn - bulk_from >= 3;
+            if (!conv) {
+              conv = true;
+              for (int i = 0; i < std::min(b, need); ++i) {
+                if (hs[i] <= 10.0 * hs[b - 1]) break;  // the flat stretch itself
+                if (std::fabs(hs[i] - prev[i]) > 1e-12 * hs[i]) conv = false;
+              }
             }
           }
         }
