@@ -104,35 +104,34 @@ __device__ __forceinline__ void b_pair(int nbp, int round, int k, int& p, int& q
   }
 }
 
-// one CTA per block pair: dd Gram of the pair's 32 columns of W (N x n_pad,
-// row-major, ld ldw; blocks >= nb are empty padding), the sweep statistic,
-// and the dd Cholesky -> R_p (32 x 32 row-major, zeros below the diagonal)
+constexpr int kBgRows = 512;     // rows per Gram-partial CTA
+
+// Gram partials: CTA (pair, split) accumulates the dd Gram of its row range
+// of the pair's 32 columns of W (column-major, column c at W + c ldw; blocks
+// >= nb are empty padding) -> part[(pair * nsplit + split) * kBpEnt + e], e
+// the row-major upper-triangle index; two entries per thread (a 4 x 4
+// register-blocked variant needed 150 registers, one CTA per SM, and ran
+// 1.8x slower).
 __global__ void __launch_bounds__(kBgThreads)
-bj_gram_chol_kernel(int64_t N, int nb, int nbp, int round, const double* __restrict__ W, int64_t ldw,
-                    double* __restrict__ Rb, unsigned long long* relmax) {
-  __shared__ __align__(16) double xs[kBgTile][kBp + 1];
-  __shared__ bdd S[kBp][kBp + 1];
-  __shared__ double piv_r[2];
-  __shared__ bdd piv_d[2];
+bj_gram_part_kernel(int64_t N, int nb, int nbp, int round, int nsplit, const double* __restrict__ W, int64_t ldw,
+                    double2* __restrict__ part) {
+  __shared__ __align__(16) double xs[kBp][kBgTile + 1];
   int bp, bq;
   b_pair(nbp, round, blockIdx.x, bp, bq);
-  double* R = Rb + (int64_t)blockIdx.x * kBp * kBp;
+  if (bq >= nb) return;
   const int t = threadIdx.x;
-  if (bq >= nb) {  // a pair with the padding block: identity rotation
-    for (int e = t; e < kBp * kBp; e += blockDim.x) R[e] = 0.0;
-    return;
-  }
   int ei[2], ej[2];
 #pragma unroll
   for (int u = 0; u < 2; ++u) b_entry(2 * t + u, ei[u], ej[u]);
   double hi[2] = {0.0, 0.0}, lo[2] = {0.0, 0.0};
   const int64_t offp = (int64_t)bp * kBw, offq = (int64_t)bq * kBw;
-  for (int64_t c0 = 0; c0 < N; c0 += kBgTile) {
-    const int nr = (int)imin64(kBgTile, N - c0);
+  const int64_t r0 = (int64_t)blockIdx.y * kBgRows, r1 = imin64(N, r0 + kBgRows);
+  for (int64_t c0 = r0; c0 < r1; c0 += kBgTile) {
+    const int nr = (int)imin64(kBgTile, r1 - c0);
     for (int e = t; e < kBgTile * kBp; e += kBgThreads) {
-      const int rr = e / kBp, cc = e % kBp;
+      const int cc = e / kBgTile, rr = e % kBgTile;  // consecutive threads: consecutive rows (coalesced)
       const int64_t col = cc < kBw ? offp + cc : offq + (cc - kBw);
-      xs[rr][cc] = rr < nr ? W[(c0 + rr) * ldw + col] : 0.0;
+      xs[cc][rr] = rr < nr ? W[col * ldw + c0 + rr] : 0.0;
     }
     __syncthreads();
     if (2 * t < kBpEnt) {
@@ -140,7 +139,7 @@ bj_gram_chol_kernel(int64_t N, int nb, int nbp, int round, const double* __restr
       for (int rr = 0; rr < kBgTile; ++rr) {
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-          const double xi = xs[rr][ei[u]], xj = xs[rr][ej[u]];
+          const double xi = xs[ei[u]][rr], xj = xs[ej[u]][rr];
           const double p = xi * xj;
           const double pe = fma(xi, xj, -p);
           const double sm = hi[u] + p;
@@ -153,8 +152,46 @@ bj_gram_chol_kernel(int64_t N, int nb, int nbp, int round, const double* __restr
     __syncthreads();
   }
   if (2 * t < kBpEnt) {
+    double2* dst = part + ((int64_t)blockIdx.x * nsplit + blockIdx.y) * kBpEnt;
 #pragma unroll
-    for (int u = 0; u < 2; ++u) S[ei[u]][ej[u]] = b_quick(hi[u], lo[u]);
+    for (int u = 0; u < 2; ++u) {
+      const bdd a = b_quick(hi[u], lo[u]);
+      dst[2 * t + u] = make_double2(a.hi, a.lo);
+    }
+  }
+}
+
+// one CTA per pair: the partials summed in split order (dd), the sweep
+// statistic, and the dd Cholesky -> R_p (32 x 32 row-major, zeros below the
+// diagonal; pivots below 1e-29 tr(G) give zero rows)
+__global__ void __launch_bounds__(kBgThreads)
+bj_chol_kernel(int nb, int nbp, int round, int nsplit, const double2* __restrict__ part, double* __restrict__ Rb,
+               unsigned long long* relmax) {
+  __shared__ bdd S[kBp][kBp + 1];
+  __shared__ double piv_r[2];
+  __shared__ bdd piv_d[2];
+  int bp, bq;
+  b_pair(nbp, round, blockIdx.x, bp, bq);
+  double* R = Rb + (int64_t)blockIdx.x * kBp * kBp;
+  const int t = threadIdx.x;
+  if (bq >= nb) {  // a pair with the padding block: not rotated
+    for (int e = t; e < kBp * kBp; e += blockDim.x) R[e] = 0.0;
+    return;
+  }
+  int ei[2], ej[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) b_entry(2 * t + u, ei[u], ej[u]);
+  if (2 * t < kBpEnt) {
+    const double2* src = part + (int64_t)blockIdx.x * nsplit * kBpEnt;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      bdd a = {0.0, 0.0};
+      for (int q = 0; q < nsplit; ++q) {
+        const double2 v = src[(int64_t)q * kBpEnt + 2 * t + u];
+        a = b_add(a, {v.x, v.y});
+      }
+      S[ei[u]][ej[u]] = a;
+    }
   }
   __syncthreads();
   // sweep statistic: the largest relative cross-block entry
@@ -234,9 +271,12 @@ bj_gram_chol_kernel(int64_t N, int nb, int nbp, int round, const double* __restr
   }
 }
 
-// X_p <- X_p V_p for the pair's 32 columns of W (N rows) and of the rotation
-// accumulator Va (n rows); V_p (32 x 32 row-major) in shared memory.  Pairs
-// with the padding block, or whose R_p is all zero, are left alone.
+// X_p <- X_p V_p for the pair's 32 columns of W (N rows, column-major, ld
+// ldw) and of the rotation accumulator Va (nv rows, ld ldv); V_p (32 x 32
+// row-major) in shared memory; one thread per row (coalesced column loads),
+// the 32 outputs in registers.  No row loop: a loop lets the compiler hoist
+// the 1024 loop-invariant V_p reads into registers and spill them.  Pairs
+// with the padding block are left alone.
 __global__ void __launch_bounds__(256)
 bj_apply_kernel(int64_t N, int64_t nv, int nb, int nbp, int round, double* __restrict__ W, int64_t ldw,
                 double* __restrict__ Va, int64_t ldv, const double* __restrict__ Vb) {
@@ -248,81 +288,89 @@ bj_apply_kernel(int64_t N, int64_t nv, int nb, int nbp, int round, double* __res
   for (int e = threadIdx.x; e < kBp * kBp; e += blockDim.x) vp[e / kBp][e % kBp] = V[e];
   __syncthreads();
   const int64_t offp = (int64_t)bp * kBw, offq = (int64_t)bq * kBw;
-  const int64_t tot = N + nv;
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < tot; r += (int64_t)gridDim.x * blockDim.x) {
-    double* row = r < N ? W + r * ldw : Va + (r - N) * ldv;
-    double x[kBp];
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= N + nv) return;
+  double* base = r < N ? W + r : Va + (r - N);
+  const int64_t ld = r < N ? ldw : ldv;
+  double* pp = base + offp * ld;
+  double* pq = base + offq * ld;
+  double y[kBp];
 #pragma unroll
-    for (int c = 0; c < kBw; ++c) {
-      x[c] = row[offp + c];
-      x[kBw + c] = row[offq + c];
-    }
+  for (int c = 0; c < kBp; ++c) y[c] = 0.0;
 #pragma unroll
-    for (int c = 0; c < kBp; ++c) {
-      double acc = 0.0;
+  for (int k = 0; k < kBp; ++k) {
+    const double xk = k < kBw ? pp[k * ld] : pq[(k - kBw) * ld];
 #pragma unroll
-      for (int k = 0; k < kBp; ++k) acc = fma(x[k], vp[k][c], acc);
-      if (c < kBw)
-        row[offp + c] = acc;
-      else
-        row[offq + (c - kBw)] = acc;
-    }
+    for (int c = 0; c < kBp; ++c) y[c] = fma(xk, vp[k][c], y[c]);
+  }
+#pragma unroll
+  for (int c = 0; c < kBw; ++c) {
+    pp[c * ld] = y[c];
+    pq[c * ld] = y[kBw + c];
   }
 }
 
-// column norms of W (N x npad) and, per column, whether the accumulated
-// rotation there is a padding coordinate's unit vector (the padding
+// column norms of W (N x npad, column-major) and, per column, whether the
+// accumulated rotation there is a padding coordinate's unit vector (padding
 // coordinates never mix with real ones: their columns are zero, outside every
-// pair rotation's active set, and only move by the pair SVD's sorting)
+// pair rotation's active set, and only move by the pair SVD's sorting); one
+// warp per column
 __global__ void bj_norms_kernel(int64_t N, int64_t npad, int64_t n, const double* __restrict__ W, int64_t ldw,
                                 const double* __restrict__ Va, int64_t ldva, double* __restrict__ nrm,
                                 int* __restrict__ pad) {
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (c >= npad) return;
   double a = 0.0;
-  for (int64_t r = 0; r < N; ++r) a = fma(W[r * ldw + c], W[r * ldw + c], a);
-  nrm[c] = sqrt(a);
+  for (int64_t r = lane; r < N; r += 32) a = fma(W[c * ldw + r], W[c * ldw + r], a);
+  a = warp_sum(a);
   double p = 0.0;
-  for (int64_t r = n; r < npad; ++r) p = fma(Va[r * ldva + c], Va[r * ldva + c], p);
-  pad[c] = p > 0.5 ? 1 : 0;
+  for (int64_t r = n + lane; r < npad; r += 32) p = fma(Va[c * ldva + r], Va[c * ldva + r], p);
+  p = warp_sum(p);
+  if (lane == 0) {
+    nrm[c] = sqrt(a);
+    pad[c] = p > 0.5 ? 1 : 0;
+  }
 }
 
 // sorted output: S[rank] = nrm[c], U[:, rank] = W[:, c] / nrm[c],
-// V[:, rank] = Va[:, c]; rank by (real before padding, descending norm, index)
+// V[:, rank] = Va[:, c] (U, V row-major); rank by (real before padding,
+// descending norm, index)
 __global__ void bj_sort_out_kernel(int64_t N, int64_t n, const double* __restrict__ W, int64_t ldw,
                                    const double* __restrict__ Va, int64_t ldva, const double* __restrict__ nrm,
                                    const int* __restrict__ pad, double* __restrict__ U, int64_t ldu,
                                    double* __restrict__ S, double* __restrict__ V, int64_t ldv) {
   const int64_t c = blockIdx.x;
-  __shared__ int64_t rk_s;
+  __shared__ unsigned long long rk_s;
   if (threadIdx.x == 0) rk_s = 0;
   __syncthreads();
   const double sc = nrm[c];
   const int pc = pad[c];
-  int64_t rk = 0;
+  unsigned long long rk = 0;
   for (int64_t d = threadIdx.x; d < n; d += blockDim.x) {
     const double sd = nrm[d];
     const int pd = pad[d];
     rk += (pd < pc || (pd == pc && (sd > sc || (sd == sc && d < c)))) ? 1 : 0;
   }
-  atomicAdd(reinterpret_cast<unsigned long long*>(&rk_s), (unsigned long long)rk);
+  atomicAdd(&rk_s, rk);
   __syncthreads();
-  const int64_t rank = rk_s;
+  const int64_t rank = (int64_t)rk_s;
   if (threadIdx.x == 0) S[rank] = sc;
   const double inv = sc > 0.0 ? 1.0 / sc : 0.0;
-  for (int64_t r = threadIdx.x; r < N; r += blockDim.x) U[r * ldu + rank] = W[r * ldw + c] * inv;
-  for (int64_t r = threadIdx.x; r < n; r += blockDim.x) V[r * ldv + rank] = Va[r * ldva + c];
+  for (int64_t r = threadIdx.x; r < N; r += blockDim.x) U[r * ldu + rank] = W[c * ldw + r] * inv;
+  for (int64_t r = threadIdx.x; r < n; r += blockDim.x) V[r * ldv + rank] = Va[c * ldva + r];
 }
 
+// W (N x npad, column-major) = M (or M^T) zero-padded; Va = I (npad x npad)
 __global__ void bj_init_kernel(int64_t N, int64_t n, int64_t npad, const double* __restrict__ M, int64_t ldm, bool trans,
                                double* __restrict__ W, double* __restrict__ Va) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t wtot = N * npad;
   if (e < wtot) {
-    const int64_t r = e / npad, c = e % npad;
+    const int64_t c = e / N, r = e % N;
     W[e] = c < n ? (trans ? M[c * ldm + r] : M[r * ldm + c]) : 0.0;
   } else if (e < wtot + npad * npad) {
-    const int64_t f = e - wtot, r = f / npad, c = f % npad;
+    const int64_t f = e - wtot, c = f / npad, r = f % npad;
     Va[f] = r == c ? 1.0 : 0.0;
   }
 }
@@ -348,20 +396,23 @@ int block_jacobi_svd(int64_t N, int64_t n, const double* M, int64_t ldm, bool tr
   SPB_ALLOC(ar, double, Vb, (size_t)npairs * kBp * kBp);
   SPB_ALLOC(ar, unsigned long long, relmax, 64);
   SPB_ALLOC(ar, double, nrm, (size_t)npad);
+  const int nsplit = ceil_div(N, kBgRows);
+  SPB_ALLOC(ar, double2, gpart, (size_t)npairs * nsplit * kBpEnt);
   const int64_t init_n = N * npad + npad * npad;
   bj_init_kernel<<<ceil_div(init_n, 256), 256, 0, s>>>(N, n, npad, M, ldm, trans, W, Va);
   count_launch();
   SPB_CHECK_LAUNCH();
   SPB_CUDA(cudaMemsetAsync(relmax, 0, 64 * sizeof(unsigned long long), s));
-  const int apply_x = std::max(1, std::min(ceil_div(N + npad, 256), 1184 / std::max(1, npairs) + 1));
+  const int apply_x = ceil_div(N + npad, 256);  // one row per thread
   constexpr int kMaxSweeps = 40;
   for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
     unsigned long long* rm = relmax + (sweep % 64);
     for (int round = 0; round < nbp - 1; ++round) {
-      bj_gram_chol_kernel<<<npairs, kBgThreads, 0, s>>>(N, nb, nbp, round, W, npad, Rb, rm);
+      bj_gram_part_kernel<<<dim3(npairs, nsplit), kBgThreads, 0, s>>>(N, nb, nbp, round, nsplit, W, N, gpart);
+      bj_chol_kernel<<<npairs, kBgThreads, 0, s>>>(nb, nbp, round, nsplit, gpart, Rb, rm);
       SPB_TRY(jacobi32_batched(kBp, npairs, Rb, kBp, kBp * kBp, Ub, kBp, kBp * kBp, Sb, kBp, Vb, kBp, kBp * kBp, s));
-      bj_apply_kernel<<<dim3(apply_x, npairs), 256, 0, s>>>(N, npad, nb, nbp, round, W, npad, Va, npad, Vb);
-      count_launch(2);
+      bj_apply_kernel<<<dim3(apply_x, npairs), 256, 0, s>>>(N, npad, nb, nbp, round, W, N, Va, npad, Vb);
+      count_launch(3);
       SPB_CHECK_LAUNCH();
     }
     unsigned long long h = 0;
@@ -371,7 +422,7 @@ int block_jacobi_svd(int64_t N, int64_t n, const double* M, int64_t ldm, bool tr
     if (mx < 1e-8) break;  // this sweep's rotations were quadratically small: done
   }
   SPB_ALLOC(ar, int, padf, (size_t)npad);
-  bj_norms_kernel<<<ceil_div(npad, 256), 256, 0, s>>>(N, npad, n, W, npad, Va, npad, nrm, padf);
+  bj_norms_kernel<<<ceil_div(npad * 32, 256), 256, 0, s>>>(N, npad, n, W, N, Va, npad, nrm, padf);
   count_launch();
   SPB_CHECK_LAUNCH();
   // the padding coordinates sort last; write the first n ranks only
@@ -379,7 +430,7 @@ int block_jacobi_svd(int64_t N, int64_t n, const double* M, int64_t ldm, bool tr
   SPB_ALLOC(out, double, Uf, (size_t)N * npad);
   SPB_ALLOC(out, double, Sf, (size_t)npad);
   SPB_ALLOC(out, double, Vf, (size_t)npad * npad);
-  bj_sort_out_kernel<<<(unsigned)npad, 256, 0, s>>>(N, npad, W, npad, Va, npad, nrm, padf, Uf, npad, Sf, Vf, npad);
+  bj_sort_out_kernel<<<(unsigned)npad, 256, 0, s>>>(N, npad, W, N, Va, npad, nrm, padf, Uf, npad, Sf, Vf, npad);
   count_launch();
   SPB_CHECK_LAUNCH();
   SPB_TRY(copy2d(N, n, Uf, npad, U, ldu, s));

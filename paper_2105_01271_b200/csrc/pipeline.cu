@@ -48,10 +48,12 @@ static int count_kept(const std::vector<double>& s, double power) {
 }
 
 // exact SVD fallback of svd_top's ID mode up to this many columns: the
-// one-sided Jacobi of a full-rank p x p core costs ~p rounds x ~10 sweeps
-// (measured 1.07 s at p = 2000, the cfg5 FP32 floor), so wider flat stretches
-// are resolved only above the stretch and flagged
-constexpr int64_t kExactMax = 512;
+// size-general thin_svd (BCGS2 TSQR + block Jacobi) of the whole sketch --
+// ~0.3 s for cfg5's 2000 x 262144 FP32-floor sketch (W, V L2-resident), but
+// 1.9 s at 5000 x 4096 (cfg3), where every block-Jacobi round streams W and V
+// from HBM; wider flat stretches are resolved only above the stretch and
+// flagged
+constexpr int64_t kExactMax = 2048;
 
 struct TopSvd {
   int b = 0, kept = 0, iters = 0;

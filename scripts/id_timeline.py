@@ -37,7 +37,7 @@ kern = sorted([e for e in ev if e.get("cat") in ("kernel", "gpu_memcpy", "gpu_me
 span = kern[-1]["ts"] + kern[-1]["dur"] - kern[0]["ts"]
 agg = collections.defaultdict(lambda: [0, 0.0])
 for e in kern:
-    k = e["name"].split("(")[0][:80]
+    k = e["name"].replace("(anonymous namespace)::", "").split("(")[0][:80]
     agg[k][0] += 1
     agg[k][1] += e["dur"]
 print(f"{name} power_id: device span {span / 1e3:.1f} ms, {len(kern)} launches")
