@@ -48,12 +48,15 @@ static int count_kept(const std::vector<double>& s, double power) {
 }
 
 // exact SVD fallback of svd_top's ID mode up to this many columns: the
-// size-general thin_svd (BCGS2 TSQR + block Jacobi) of the whole sketch --
-// ~0.3 s for cfg5's 2000 x 262144 FP32-floor sketch (W, V L2-resident), but
-// 1.9 s at 5000 x 4096 (cfg3), where every block-Jacobi round streams W and V
-// from HBM; wider flat stretches are resolved only above the stretch and
+// size-general thin_svd (BCGS2 TSQR + block Jacobi) of the whole sketch
+// (1.6 s at 5000 x 4096, cfg3: every block-Jacobi round streams W and V
+// from HBM); wider flat stretches are resolved only above the stretch and
 // flagged
 constexpr int64_t kExactMax = 2048;
+// ... and only while the sketch's long side keeps the panel TSQR cheap: cfg5's
+// 2000 x 262144 FP32-floor sketch costs 1.8 s exact (BCGS2 over 262144 rows
+// + the 2000-wide block Jacobi) against 0.9 s resolved above the floor
+constexpr int64_t kExactLong = 16384;
 
 struct TopSvd {
   int b = 0, kept = 0, iters = 0;
@@ -338,7 +341,7 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
                 grow = true;
                 break;
               }
-              if (p <= kExactMax) return exact_fallback();
+              if (p <= kExactMax && std::max(rows, cols) <= kExactLong) return exact_fallback();
               if (!out.bulk) bulk_from = itn;
               out.bulk = true;  // a few more steps: the Ritz values above the stretch settle
             }
