@@ -337,7 +337,9 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
           } else {
             const double more = rho < 1.0 ? (std::log(1e-12) / std::log(rho) - 2.0) / 2.0 - itn : 1e9;
             if (more > 8.0) {
-              if (b < cap) {
+              // a flat stretch (rho > 0.95: a noise bulk) does not become
+              // resolvable with a wider block -- only a slowly decaying one does
+              if (b < cap && rho <= 0.95) {
                 grow = true;
                 break;
               }

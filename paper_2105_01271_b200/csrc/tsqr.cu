@@ -653,22 +653,31 @@ __global__ void add_block(int64_t rows, int64_t cols, const double* src, int64_t
   dst[i * ldd + c] += src[i * lds + c];
 }
 
-// Wide inputs: 32-column panels, two block Gram-Schmidt passes against the
-// previous panels, then a Householder TSQR of the projected panel.
+// Wide inputs: panels, two block Gram-Schmidt passes against the previous
+// panels, then a Householder TSQR of the projected panel.  Up to 512 columns
+// the panels are 32 wide (the register TSQR); wider inputs use 256-wide
+// panels factored recursively the same way, so the projections against the
+// previous panels are DMMA GEMMs 256 columns wide instead of 32 (round 1's
+// 32-wide panels ran cfg5's 262144 x 2000 at ~13 TF/s plus a split-K reduce
+// per product).
 int tsqr(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, int64_t ldq,
          double* R, int64_t ldr, cudaStream_t s) {
   SPB_REQUIRE(cols >= 1 && rows >= cols, "tsqr needs rows >= cols >= 1");
   SPB_REQUIRE(ldx >= cols && ldq >= cols && ldr >= cols, "bad tsqr leading dimension");
   if (cols <= kQB) return tsqr32(rows, (int)cols, X, ldx, Q, ldq, R, ldr, s);
+  const int pw = cols > 512 ? 256 : kQB;  // panel width
+  auto panel_qr = [&](const double* P, int w, double* Qp, double* Rp) -> int {
+    return pw == kQB ? tsqr32(rows, w, P, w, Qp, ldq, Rp, ldr, s) : tsqr(rows, w, P, w, Qp, ldq, Rp, ldr, s);
+  };
   SPB_CUDA(cudaMemset2DAsync(R, ldr * sizeof(double), 0, cols * sizeof(double), cols, s));
   Arena ar(s);
-  SPB_ALLOC(ar, double, P, (size_t)rows * kQB);
-  SPB_ALLOC(ar, double, T, (size_t)cols * kQB);
-  SPB_ALLOC(ar, double, S2, (size_t)cols * kQB);
-  SPB_ALLOC(ar, double, R2, (size_t)kQB * kQB);
-  SPB_ALLOC(ar, double, R3, (size_t)kQB * kQB);
-  for (int64_t p0 = 0; p0 < cols; p0 += kQB) {
-    const int w = (int)std::min<int64_t>(kQB, cols - p0);
+  SPB_ALLOC(ar, double, P, (size_t)rows * pw);
+  SPB_ALLOC(ar, double, T, (size_t)cols * pw);
+  SPB_ALLOC(ar, double, S2, (size_t)cols * pw);
+  SPB_ALLOC(ar, double, R2, (size_t)pw * pw);
+  SPB_ALLOC(ar, double, R3, (size_t)pw * pw);
+  for (int64_t p0 = 0; p0 < cols; p0 += pw) {
+    const int w = (int)std::min<int64_t>(pw, cols - p0);
     copy_block<<<ceil_div(rows * w, 256), 256, 0, s>>>(rows, w, X + p0, ldx, P, w);
     count_launch();
     SPB_CHECK_LAUNCH();
@@ -684,7 +693,7 @@ int tsqr(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, in
     }
     double* Qp = Q + p0;
     double* Rp = R + p0 * ldr + p0;
-    SPB_TRY(tsqr32(rows, w, P, w, Qp, ldq, Rp, ldr, s));
+    SPB_TRY(panel_qr(P, w, Qp, Rp));
     if (p0 > 0) {
       // A numerically rank-deficient panel leaves a residual P of rounding
       // size whose components along Q[:, :p0] are as large as the rest, so
@@ -703,7 +712,12 @@ int tsqr(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* Q, in
       copy_block<<<ceil_div(rows * w, 256), 256, 0, s>>>(rows, w, Qp, ldq, P, w);
       count_launch();
       SPB_CHECK_LAUNCH();
-      SPB_TRY(tsqr32(rows, w, P, w, Qp, ldq, R2, w, s));
+      // R2 (w x w, ld w): the panel QR writes R into a (w x w) block with ld ldr
+      // in the recursive case, so factor into R2 with its own leading dimension
+      if (pw == kQB)
+        SPB_TRY(tsqr32(rows, w, P, w, Qp, ldq, R2, w, s));
+      else
+        SPB_TRY(tsqr(rows, w, P, w, Qp, ldq, R2, w, s));
       SPB_TRY(gemm(0, 0, w, w, w, 1.0, R2, w, Rp, ldr, 0.0, R3, w, s));
       copy_block<<<ceil_div(w * w, 256), 256, 0, s>>>(w, w, R3, w, Rp, ldr);
       count_launch();

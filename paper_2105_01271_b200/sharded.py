@@ -191,7 +191,7 @@ def distributed_sketch_basis(c_i, row0: int, ncols: int, power: float, comm, ops
                     if not conv:
                         more = (np.log(1e-12) / np.log(rho) - 2.0) / 2.0 - itn if rho < 1.0 else 1e9
                         if more > 8.0:
-                            if b < cap:
+                            if b < cap and rho <= 0.95:   # a flat stretch does not resolve with a wider block
                                 grow = True
                                 break
                             conv = True   # bulk split: approximate beyond the resolvable part
