@@ -47,6 +47,7 @@ sys.path.insert(0, str(ROOT))
 from paper_2105_01271_b200.datagen import CONFIGS  # noqa: E402
 
 METRIC = "GB/s of A streamed (end-to-end single-pass rank-k SVD)"
+DRYRUN = os.environ.get("SPB_BENCH_DRYRUN") == "1"
 UNIT = "GB/s"
 
 
@@ -372,7 +373,12 @@ def run_ours(args):
     import torch.distributed as dist
     rank, world, local = rank_env()
     if world > 1:
-        dist.init_process_group("nccl")
+        # SPB_BENCH_DRYRUN=1 (code-path check only, never a measurement): gloo
+        # collectives and every rank on cuda:0, so the N > 1 path can be
+        # exercised on a one-GPU box without NCCL ranks sharing a device
+        dist.init_process_group("gloo" if DRYRUN else "nccl")
+    if DRYRUN:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     import paper_2105_01271_b200 as sp
@@ -560,7 +566,8 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": cfg.dtype,
-            "data": f"synthetic (BASELINE {cfg.name} heat field, seed {cfg.seed}, generated on device)",
+            "data": f"synthetic (BASELINE {cfg.name} heat field, seed {cfg.seed}, generated on device)"
+                    + (" -- DRY RUN (gloo, all ranks on cuda:0): not a measurement" if DRYRUN else ""),
             "config": dict(config_dict(cfg, world, cols.size), warmup_steps_run=warm_done, kept_rank=r),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
