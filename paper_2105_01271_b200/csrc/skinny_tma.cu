@@ -27,22 +27,38 @@ constexpr int kTmaRows = 16;      // rows per stage
 constexpr int kTmaStages = 3;
 constexpr int kTmaRowBytes = kTmaConsumers * 16;  // 4 KB of A per row per tile
 
-template <int R>
+// MMA variant: the products run on the FP64 tensor pipe (mma.sync m8n8k4,
+// M = 8 columns of A, N = 8 columns of Z, K = 4 rows): one LDS.128 of A feeds
+// V DMMAs (256 FMAs each) instead of V * R scalar DFMAs with R broadcast loads
+// of Z -- ~6x fewer issued instructions per byte of A, which is what keeps the
+// pass at the HBM roofline when a sustained run is power-capped (the scalar
+// loop issues 14 TFLOP/s of DFMA at cfg4).  Rows are pitched 32 bytes past 4 KB
+// so the fragment loads (4 rows x 8 lanes x 16 bytes per quarter warp) are
+// bank-conflict free.
+template <int R, bool MMA>
 struct TmaLayout {
+  static constexpr int kRowPitch = kTmaRowBytes + (MMA ? 32 : 0);
   static constexpr int kZStage = kTmaRows * R * 8;                       // bytes of Z per stage
   static constexpr int kZStagePad = (kZStage + 127) / 128 * 128;
-  static constexpr int kStageBytes = kTmaRows * kTmaRowBytes + kZStagePad;
+  static constexpr int kZOff = (kTmaRows * kRowPitch + 127) / 128 * 128;
+  static constexpr int kStageBytes = kZOff + kZStagePad;
   static constexpr int kSmem = kTmaStages * kStageBytes;
 };
 
-template <int R, typename TA>
+__device__ __forceinline__ void k2_dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int R, typename TA, bool MMA>
 __global__ void __launch_bounds__(kTmaThreads, 1)
 skinny_tma_kernel(const TA* __restrict__ A, int64_t m, int64_t n, int64_t lda, const double* __restrict__ Zc,
                   double* __restrict__ Y, int64_t ldy, int splits) {
   SPB_PDL_ENTRY();
   constexpr int V = 16 / sizeof(TA);
   constexpr int TC = kTmaConsumers * V;  // columns per tile
-  using L = TmaLayout<R>;
+  using L = TmaLayout<R, MMA>;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t full[kTmaStages];
   __shared__ __align__(8) uint64_t empty[kTmaStages];
@@ -82,8 +98,8 @@ skinny_tma_kernel(const TA* __restrict__ A, int64_t m, int64_t n, int64_t lda, c
           const uint32_t zbytes = (uint32_t)(nr * R * 8);
           mbar_arrive_expect_tx(&full[stage], nr * seg + ((zbytes + 15) / 16) * 16);
           for (int i = 0; i < nr; ++i)
-            bulk_g2s(sb + i * kTmaRowBytes, A + (r0 + i) * lda + c0, seg, &full[stage]);
-          bulk_g2s(sb + kTmaRows * kTmaRowBytes, Zc + r0 * R, ((zbytes + 15) / 16) * 16, &full[stage]);
+            bulk_g2s(sb + i * L::kRowPitch, A + (r0 + i) * lda + c0, seg, &full[stage]);
+          bulk_g2s(sb + L::kZOff, Zc + r0 * R, ((zbytes + 15) / 16) * 16, &full[stage]);
           if (++stage == kTmaStages) {
             stage = 0;
             ph ^= 1;
@@ -97,6 +113,81 @@ skinny_tma_kernel(const TA* __restrict__ A, int64_t m, int64_t n, int64_t lda, c
   // -------------------------------------------------------------- consumers
   int stage = 0;
   uint32_t ph = 0;
+  if constexpr (MMA) {
+    // warp w owns columns [w * 32 V, (w + 1) * 32 V) of the tile; lane (g, t):
+    // fragment row t of each 4-row step, the V adjacent columns 4 V j + V g ..
+    // of column group j (each a separate 8-column DMMA tile: m index g)
+    constexpr int NT = (R + 7) / 8;  // 8-wide tiles of Z columns
+    const int g = lane >> 2, t4 = lane & 3;
+    for (int64_t c0 = cb; c0 < ce; c0 += TC) {
+      double acc[4][V][NT][2];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+#pragma unroll
+          for (int q = 0; q < NT; ++q) acc[j][v][q][0] = acc[j][v][q][1] = 0.0;
+      for (int64_t r0 = rb; r0 < re; r0 += kTmaRows) {
+        const int nr = (int)imin64(kTmaRows, re - r0);
+        const unsigned char* sb = smem + stage * L::kStageBytes;
+        const double* zs = reinterpret_cast<const double*>(sb + L::kZOff);
+        mbar_wait(&full[stage], ph);
+#pragma unroll
+        for (int ks = 0; ks < kTmaRows / 4; ++ks) {
+          const int row = 4 * ks + t4;
+          const bool live = row < nr;  // rows past the block hold stale bytes
+          double b[NT];
+#pragma unroll
+          for (int q = 0; q < NT; ++q) b[q] = (live && 8 * q + g < R) ? zs[row * R + 8 * q + g] : 0.0;
+          const unsigned char* ap = sb + row * L::kRowPitch + (warp * 32 + g) * 16;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            double a[V];
+            if constexpr (V == 2) {
+              const double2 x = *reinterpret_cast<const double2*>(ap + j * 128);
+              a[0] = x.x;
+              a[1] = x.y;
+            } else {
+              const float4 x = *reinterpret_cast<const float4*>(ap + j * 128);
+              a[0] = x.x;
+              a[1] = x.y;
+              a[2] = x.z;
+              a[3] = x.w;
+            }
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              const double av = live ? a[v] : 0.0;
+#pragma unroll
+              for (int q = 0; q < NT; ++q) k2_dmma(acc[j][v][q][0], acc[j][v][q][1], av, b[q]);
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (++stage == kTmaStages) {
+          stage = 0;
+          ph ^= 1;
+        }
+      }
+      // C fragment: row g (the column of A), columns 2 t4, 2 t4 + 1 of each Z tile
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const int64_t col = c0 + (int64_t)(warp * 32 + j * 8 + g) * V + v;
+          if (col < ce) {
+#pragma unroll
+            for (int q = 0; q < NT; ++q)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int c = 8 * q + 2 * t4 + e;
+                if (c < R) Y[col * ldy + c] = acc[j][v][q][e];
+              }
+          }
+        }
+    }
+    return;
+  }
   for (int64_t c0 = cb; c0 < ce; c0 += TC) {
     const int64_t col = c0 + (int64_t)tid * V;
     double acc[V][R];
@@ -107,18 +198,18 @@ skinny_tma_kernel(const TA* __restrict__ A, int64_t m, int64_t n, int64_t lda, c
     for (int64_t r0 = rb; r0 < re; r0 += kTmaRows) {
       const int nr = (int)imin64(kTmaRows, re - r0);
       const unsigned char* sb = smem + stage * L::kStageBytes;
-      const double* zs = reinterpret_cast<const double*>(sb + kTmaRows * kTmaRowBytes);
+      const double* zs = reinterpret_cast<const double*>(sb + L::kZOff);
       mbar_wait(&full[stage], ph);
       if (nr == kTmaRows) {
 #pragma unroll
         for (int i = 0; i < kTmaRows; ++i) {
           double a[V];
           if constexpr (V == 2) {
-            const double2 x = *reinterpret_cast<const double2*>(sb + i * kTmaRowBytes + tid * 16);
+            const double2 x = *reinterpret_cast<const double2*>(sb + i * L::kRowPitch + tid * 16);
             a[0] = x.x;
             a[1] = x.y;
           } else {
-            const float4 x = *reinterpret_cast<const float4*>(sb + i * kTmaRowBytes + tid * 16);
+            const float4 x = *reinterpret_cast<const float4*>(sb + i * L::kRowPitch + tid * 16);
             a[0] = x.x;
             a[1] = x.y;
             a[2] = x.z;
@@ -133,7 +224,7 @@ skinny_tma_kernel(const TA* __restrict__ A, int64_t m, int64_t n, int64_t lda, c
         }
       } else {
         for (int i = 0; i < nr; ++i) {
-          const TA* ap = reinterpret_cast<const TA*>(sb + i * kTmaRowBytes) + tid * V;
+          const TA* ap = reinterpret_cast<const TA*>(sb + i * L::kRowPitch) + tid * V;
 #pragma unroll
           for (int c = 0; c < R; ++c) {
             const double z = zs[i * R + c];
@@ -169,16 +260,17 @@ __global__ void skinny_split_reduce(int splits, int64_t count, const double* __r
   Y[e] = a;
 }
 
-template <int R, typename TA>
-int skinny_tma_launch(const TA* A, int64_t m, int64_t n, int64_t lda, const double* Zc, double* Y, int64_t ldy,
-                      cudaStream_t s) {
-  using L = TmaLayout<R>;
+template <int R, typename TA, bool MMA>
+static int skinny_tma_launch_v(const TA* A, int64_t m, int64_t n, int64_t lda, const double* Zc, double* Y,
+                               int64_t ldy, cudaStream_t s) {
+  using L = TmaLayout<R, MMA>;
   constexpr int V = 16 / sizeof(TA);
   static int attr_dev = -1;  // set once per device (host overhead sits on the critical path)
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    SPB_CUDA(cudaFuncSetAttribute(skinny_tma_kernel<R, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmem));
+    SPB_CUDA(cudaFuncSetAttribute(skinny_tma_kernel<R, TA, MMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  L::kSmem));
     attr_dev = dev;
   }
   const int64_t units = n / V;
@@ -203,7 +295,7 @@ int skinny_tma_launch(const TA* A, int64_t m, int64_t n, int64_t lda, const doub
       return SP_ECUDA;
     }
   }
-  SPB_CUDA(launch_pdl((skinny_tma_kernel<R, TA>), dim3(grid), dim3(kTmaThreads), L::kSmem, s, A, m, n, lda, Zc, out, splits > 1 ? R : ldy, splits));
+  SPB_CUDA(launch_pdl((skinny_tma_kernel<R, TA, MMA>), dim3(grid), dim3(kTmaThreads), L::kSmem, s, A, m, n, lda, Zc, out, splits > 1 ? R : ldy, splits));
   count_launch();
   SPB_CHECK_LAUNCH();
   if (splits > 1) {
@@ -212,6 +304,15 @@ int skinny_tma_launch(const TA* A, int64_t m, int64_t n, int64_t lda, const doub
     SPB_CHECK_LAUNCH();
   }
   return SP_OK;
+}
+
+template <int R, typename TA>
+int skinny_tma_launch(const TA* A, int64_t m, int64_t n, int64_t lda, const double* Zc, double* Y, int64_t ldy,
+                      cudaStream_t s) {
+  // SPB_K2_FMA=1: the scalar-DFMA consumers (experiments / comparison)
+  static const bool fma_loop = getenv("SPB_K2_FMA") != nullptr;
+  if (fma_loop) return skinny_tma_launch_v<R, TA, false>(A, m, n, lda, Zc, Y, ldy, s);
+  return skinny_tma_launch_v<R, TA, true>(A, m, n, lda, Zc, Y, ldy, s);
 }
 
 // Preconditions of the bulk-copy path: 16-byte aligned base, row pitch and
