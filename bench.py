@@ -492,10 +492,21 @@ def run_ours(args):
             traffic = None
     del Y, Z, res
 
-    # ---- CPU baseline sample (rank 0, N = 1)
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(cfg, steps=3)
+    # ---- other BASELINE configurations, before the host-buffer leg: page-locking
+    # and releasing an 84 GB host array leaves the host busy for a while, and the
+    # short calls (cfg2: 0.5 ms with one host decision inside) are sensitive to it
+    extra = None
+    do_extra = rank == 0 and world == 1 and not args.no_extra
+    if do_extra:
+        names = [c for c in ("cfg2", "cfg3") if c != cfg.name] or ["cfg2"]
+        extra = extra_configs(names, dev, torch)
+        if cfg.name != "cfg5":          # cfg5 (134 GB) needs the headline's A out of HBM
+            del A
+            gc.collect()
+            torch.cuda.empty_cache()
+            extra.update(extra_configs(["cfg5"], dev, torch))
+            A, c_begin = _gen_shard(cfg, rank, world, dev)
+            torch.cuda.synchronize()
 
     # ---- e2e through the public API from pinned host memory
     e2e = None
@@ -529,7 +540,11 @@ def run_ours(args):
             if cfg.q == 0:
                 return sp.single_pass_svd(stream, op, k)
             return sp.power_svd(stream, op, k, pc)
-        out = e2e_step()
+        # two untimed calls: the first creates the page-locked result staging
+        # buffers and the device copy of A, the second still runs slow (measured
+        # at cfg2: 93, 36, 20.3, 20.1 ms for calls 0-3)
+        for _ in range(2):
+            out = e2e_step()
         d2h = out.u.nbytes + np.asarray(out.s).nbytes + out.v.nbytes
         del out
         torch.cuda.synchronize()
@@ -551,7 +566,8 @@ def run_ours(args):
             e_ms = float(t.item())
         e2e = {"value": cfg.a_bytes / (e_ms * 1e-3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": cfg.a_bytes, "d2h_bytes_per_step": int(d2h) * world, "ms_per_step": e_ms,
-               "steps": n_e2e, "host_buffer": "caller's numpy array, page-locked in place" if pinned else "pageable"}
+               "steps": n_e2e, "warmup": 2,
+               "host_buffer": "caller's numpy array, page-locked in place" if pinned else "pageable"}
         del out
         if pinned:
             torch.cuda.cudart().cudaHostUnregister(ht.data_ptr())
@@ -561,10 +577,10 @@ def run_ours(args):
     gc.collect()
     torch.cuda.empty_cache()
 
-    extra = None
-    if rank == 0 and world == 1 and not args.no_extra:
-        names = [c for c in ("cfg2", "cfg3", "cfg5") if c != cfg.name] or ["cfg2"]
-        extra = extra_configs(names, dev, torch)
+    # ---- CPU baseline sample (rank 0, N = 1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(cfg, steps=3)
 
     if rank == 0:
         line = {

@@ -13,6 +13,8 @@
 // a sweep with no rotation (|w_p.w_q| <= 1e-15 ||w_p|| ||w_q|| for every pair).
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "launch_count.cuh"
 #include "ops.cuh"
@@ -538,6 +540,220 @@ jacobi_grid_kernel(int n, int np, const double* __restrict__ M, int64_t ldm, boo
   }
 }
 
+// ------------------------------------------ 32 < n <= 256, block rounds ----
+// The Rayleigh-Ritz cores of the ID range finder (b = 40 ... 256).  The scalar
+// kernels above pay one (grid) barrier and an L2 round trip per column-pair
+// round: 255 rounds x ~6 sweeps at n = 256, 8 us each (12.5 ms per core, the
+// largest item of a cfg3 power_id).  Here the columns are cut into 16-wide
+// blocks and every OUTER round gives each CTA one block pair (round-robin over
+// the blocks: nb - 1 outer rounds per sweep, one grid barrier each); the CTA
+// holds the pair's 32 columns of W stacked on the same columns of V in shared
+// memory (2 np rows, 128 KB at n = 256) and rotates all 16 x 16 cross pairs in
+// 16 inner rounds of 16 disjoint pairs (one warp per pair, block barriers
+// only); the pairs inside a block are rotated in the first outer round of the
+// sweep, so a sweep visits every pair exactly once.  Rotations, thresholds,
+// the quadratic-convergence stop and the sorted outputs are those of the
+// scalar kernels.
+constexpr int kJbW = 16;           // block width
+constexpr int kJbThreads = 512;    // one warp per pair of the 32 resident columns
+
+template <int RPL>  // rows of W per lane (np = 32 RPL)
+__device__ __forceinline__ void jb_rotate(double* __restrict__ cp, double* __restrict__ cq, int lane, double negl,
+                                          int* rot, unsigned long long* relmax) {
+  double x[2 * RPL], y[2 * RPL];
+#pragma unroll
+  for (int j = 0; j < RPL; ++j) {
+    x[j] = cp[lane + 32 * j];
+    y[j] = cq[lane + 32 * j];
+  }
+  double a = 0.0, b = 0.0, g = 0.0;
+#pragma unroll
+  for (int j = 0; j < RPL; ++j) {
+    a = fma(x[j], x[j], a);
+    b = fma(y[j], y[j], b);
+    g = fma(x[j], y[j], g);
+  }
+  a = warp_sum(a);
+  b = warp_sum(b);
+  g = warp_sum(g);
+  if (g != 0.0 && fmin(a, b) > negl && fabs(g) > kJacTol * sqrt(a) * sqrt(b)) {
+    const double zeta = (b - a) / (2.0 * g);
+    double t;
+    if (fabs(zeta) > 1e150)
+      t = 0.5 / zeta;
+    else
+      t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+    const double cs = 1.0 / sqrt(fma(t, t, 1.0));
+    const double sn = cs * t;
+#pragma unroll
+    for (int j = RPL; j < 2 * RPL; ++j) {  // the V half
+      x[j] = cp[lane + 32 * j];
+      y[j] = cq[lane + 32 * j];
+    }
+#pragma unroll
+    for (int j = 0; j < 2 * RPL; ++j) {
+      cp[lane + 32 * j] = cs * x[j] - sn * y[j];
+      cq[lane + 32 * j] = fma(sn, x[j], cs * y[j]);
+    }
+    if (lane == 0) {
+      atomicOr(rot, 1);
+      atomicMax(relmax, (unsigned long long)__double_as_longlong(fabs(g) / (sqrt(a) * sqrt(b))));
+    }
+  }
+}
+
+template <int RPL>
+__global__ void __launch_bounds__(kJbThreads)
+jacobi_blk_kernel(int n, const double* __restrict__ M, int64_t ldm, bool trans, double* __restrict__ U,
+                  int64_t ldu, double* __restrict__ S, double* __restrict__ Vout, int64_t ldv,
+                  double* __restrict__ W, double* __restrict__ Vm, double* __restrict__ cn, int* rot,
+                  unsigned long long* relmax) {
+  constexpr int np = 32 * RPL;
+  constexpr int nb = np / kJbW;  // even
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double cols[];  // 32 columns x [W (np) | V (np)]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid;
+  const int64_t gthr = (int64_t)gridDim.x * blockDim.x;
+  const int gwarp = (int)(gtid >> 5), nwarps = (int)(gthr >> 5);
+  for (int64_t e = gtid; e < (int64_t)np * np; e += gthr) {
+    const int c = (int)(e / np), i = (int)(e % np);
+    W[e] = (i < n && c < n) ? (trans ? M[(int64_t)c * ldm + i] : M[(int64_t)i * ldm + c]) : 0.0;
+    Vm[e] = (i == c) ? 1.0 : 0.0;
+  }
+  if (gtid < 2) {
+    rot[gtid] = 0;
+    relmax[gtid] = 0ull;
+  }
+  grid.sync();
+  for (int c = gwarp; c < np; c += nwarps) {
+    double a = 0.0;
+    for (int i = lane; i < np; i += 32) a = fma(W[(int64_t)c * np + i], W[(int64_t)c * np + i], a);
+    a = warp_sum(a);
+    if (lane == 0) cn[c] = a;
+  }
+  grid.sync();
+  double fro = 0.0;
+  for (int c = 0; c < np; ++c) fro += cn[c];
+  const double negl = 1e-30 * fro;
+  for (int sweep = 0; sweep < kJacMaxSweeps; ++sweep) {
+    int* rt = &rot[sweep & 1];
+    unsigned long long* rm = &relmax[sweep & 1];
+    for (int round = 0; round < nb - 1; ++round) {
+      if (round == 1 && gtid == 0) {  // nobody reads the other parity until this sweep ends
+        rot[(sweep + 1) & 1] = 0;
+        relmax[(sweep + 1) & 1] = 0ull;
+      }
+      int bi, bj;
+      rr_pair(nb, round, blockIdx.x, bi, bj);
+      // stage the pair's columns: W half, then V half
+      for (int e = tid; e < 32 * (np / 2); e += kJbThreads) {  // double2 units
+        const int c = e / (np / 2), i2 = e % (np / 2);
+        const int gc = (c < kJbW ? bi * kJbW + c : bj * kJbW + (c - kJbW));
+        reinterpret_cast<double2*>(cols + (size_t)c * 2 * np)[i2] =
+            reinterpret_cast<const double2*>(W + (int64_t)gc * np)[i2];
+        reinterpret_cast<double2*>(cols + (size_t)c * 2 * np + np)[i2] =
+            reinterpret_cast<const double2*>(Vm + (int64_t)gc * np)[i2];
+      }
+      __syncthreads();
+      if (round == 0) {
+        // pairs inside each block: warps 0-7 block bi, 8-15 block bj
+        const int half = warp >> 3, k = warp & 7;
+        for (int r = 0; r < kJbW - 1; ++r) {
+          int p, q;
+          rr_pair(kJbW, r, k, p, q);
+          jb_rotate<RPL>(cols + (size_t)(half * kJbW + p) * 2 * np, cols + (size_t)(half * kJbW + q) * 2 * np, lane,
+                         negl, rt, rm);
+          __syncthreads();
+        }
+      }
+      for (int r = 0; r < kJbW; ++r) {
+        const int p = warp, q = kJbW + ((warp + r) & (kJbW - 1));
+        jb_rotate<RPL>(cols + (size_t)p * 2 * np, cols + (size_t)q * 2 * np, lane, negl, rt, rm);
+        __syncthreads();
+      }
+      for (int e = tid; e < 32 * (np / 2); e += kJbThreads) {
+        const int c = e / (np / 2), i2 = e % (np / 2);
+        const int gc = (c < kJbW ? bi * kJbW + c : bj * kJbW + (c - kJbW));
+        reinterpret_cast<double2*>(W + (int64_t)gc * np)[i2] =
+            reinterpret_cast<const double2*>(cols + (size_t)c * 2 * np)[i2];
+        reinterpret_cast<double2*>(Vm + (int64_t)gc * np)[i2] =
+            reinterpret_cast<const double2*>(cols + (size_t)c * 2 * np + np)[i2];
+      }
+      grid.sync();
+    }
+    if (*(volatile int*)rt == 0 || __longlong_as_double((long long)*(volatile unsigned long long*)rm) < kJacQuad)
+      break;
+  }
+  // singular values = column norms, sorted descending (stable by index)
+  for (int c = gwarp; c < np; c += nwarps) {
+    double a = 0.0;
+    for (int i = lane; i < np; i += 32) a = fma(W[(int64_t)c * np + i], W[(int64_t)c * np + i], a);
+    a = warp_sum(a);
+    if (lane == 0) cn[c] = sqrt(a);
+  }
+  grid.sync();
+  for (int c = gwarp; c < n; c += nwarps) {
+    const double sc = cn[c];
+    int rank = 0;
+    for (int d = lane; d < np; d += 32) {
+      const double sd = cn[d];
+      rank += (sd > sc || (sd == sc && d < c)) ? 1 : 0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+    if (rank >= n) continue;
+    if (lane == 0) S[rank] = sc;
+    const double inv = sc > 0.0 ? 1.0 / sc : 0.0;
+    for (int i = lane; i < n; i += 32) {
+      U[(int64_t)i * ldu + rank] = W[(int64_t)c * np + i] * inv;
+      if (Vout) Vout[(int64_t)i * ldv + rank] = Vm[(int64_t)c * np + i];
+    }
+  }
+}
+
+template <int RPL>
+static int jacobi_blk_launch(int n, const double* M, int64_t ldm, bool trans, double* U, int64_t ldu, double* S,
+                             double* V, int64_t ldv, cudaStream_t s) {
+  constexpr int np = 32 * RPL;
+  Arena gar(s);
+  double* gW = gar.alloc<double>((size_t)np * np);
+  double* gV = gar.alloc<double>((size_t)np * np);
+  double* cn = gar.alloc<double>((size_t)np);
+  int* rot = gar.alloc<int>(2);
+  unsigned long long* relmax = gar.alloc<unsigned long long>(2);
+  if (!gW || !gV || !cn || !rot || !relmax) {
+    set_error("jacobi workspace allocation failed");
+    return SP_ECUDA;
+  }
+  const size_t smem = (size_t)32 * 2 * np * sizeof(double);
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    SPB_CUDA(cudaFuncSetAttribute(jacobi_blk_kernel<RPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_dev = dev;
+  }
+  const int grid = np / kJbW / 2;
+  void* args[] = {&n, &M, &ldm, &trans, &U, &ldu, &S, &V, &ldv, &gW, &gV, &cn, &rot, &relmax};
+  SPB_CUDA(cudaLaunchCooperativeKernel((const void*)jacobi_blk_kernel<RPL>, dim3(grid), dim3(kJbThreads), args, smem, s));
+  count_launch();
+  return SP_OK;
+}
+
+static int jacobi_blk(int n, const double* M, int64_t ldm, bool trans, double* U, int64_t ldu, double* S, double* V,
+                      int64_t ldv, cudaStream_t s) {
+  switch ((n + 31) / 32) {
+    case 2: return jacobi_blk_launch<2>(n, M, ldm, trans, U, ldu, S, V, ldv, s);
+    case 3: return jacobi_blk_launch<3>(n, M, ldm, trans, U, ldu, S, V, ldv, s);
+    case 4: return jacobi_blk_launch<4>(n, M, ldm, trans, U, ldu, S, V, ldv, s);
+    case 5: return jacobi_blk_launch<5>(n, M, ldm, trans, U, ldu, S, V, ldv, s);
+    case 6: return jacobi_blk_launch<6>(n, M, ldm, trans, U, ldu, S, V, ldv, s);
+    case 7: return jacobi_blk_launch<7>(n, M, ldm, trans, U, ldu, S, V, ldv, s);
+    default: return jacobi_blk_launch<8>(n, M, ldm, trans, U, ldu, S, V, ldv, s);
+  }
+}
+
 // batch independent n x n SVDs (n <= 32), core b at M + b bsM (its U, S, V
 // likewise): the pair solves of the block Jacobi (bjacobi.cu)
 int jacobi32_batched(int n, int batch, const double* M, int64_t ldm, int64_t bsM, double* U, int64_t ldu,
@@ -574,6 +790,9 @@ int jacobi_svd_tr(int64_t n, const double* M, int64_t ldm, bool trans, double* U
     SPB_CHECK_LAUNCH();
     return SP_OK;
   }
+  // SPB_JACOBI_SCALAR=1: the scalar kernels for every n > 32 (comparison)
+  static const bool scalar_only = getenv("SPB_JACOBI_SCALAR") != nullptr;
+  if (n <= 256 && !scalar_only) return jacobi_blk((int)n, M, ldm, trans, U, ldu, S, V, ldv, s);
   Arena vscratch(s);
   if (trans) {
     double* Mt = vscratch.alloc<double>((size_t)n * n);

@@ -59,11 +59,25 @@ loop("cfg4 call", "cfg4", reps=3)
 gc.collect()
 torch.cuda.empty_cache()
 loop("after cfg4")
-h = np.empty((20000, 1 << 20), dtype=np.float64)
-ht = torch.from_numpy(h)
+from bench import ClockSampler  # noqa: E402
+with ClockSampler(0) as clk:
+    loop("inside a ClockSampler region")
+print(clk.summary())
+loop("after the ClockSampler region")
+cfg = CONFIGS["cfg2"]
+A = generate_device(cfg, dev)
+op, cols = sp.grid_injection(cfg.grid, cfg.stride)
+pc = sp.PowerConfig(q=cfg.q, columns=cols)
+host = np.empty((cfg.m, cfg.n))
+ht = torch.from_numpy(host)
 rc = torch.cuda.cudart().cudaHostRegister(ht.data_ptr(), ht.numel() * 8, 0)
-ht[:1000].fill_(1.0)
-loop("with 168 GB of host memory registered")
+ht.copy_(A)
+torch.cuda.synchronize()
+for i in range(4):
+    t0 = time.perf_counter()
+    out = sp.power_svd(sp.ArraySnapshotStream(host), op, cfg.k, pc)
+    print(f"e2e call {i}: {(time.perf_counter() - t0) * 1e3:.2f} ms", flush=True)
+del out
+loop("after e2e calls (host still registered)")
 torch.cuda.cudart().cudaHostUnregister(ht.data_ptr())
-del h, ht
 loop("after unregistering")
