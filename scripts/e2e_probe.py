@@ -38,25 +38,33 @@ def t(label, fn, reps=3):
 
 
 # (a) torch's pinned allocator, (b) a numpy array registered in place (the bench's e2e buffer)
-hp = torch.empty(A.shape, dtype=A.dtype, pin_memory=True)
-hp.copy_(A)
+big = nbytes > 40e9   # one host copy only, raw H2D lands in A itself
+hp = None
+if not big:
+    hp = torch.empty(A.shape, dtype=A.dtype, pin_memory=True)
+    hp.copy_(A)
 hreg = np.empty(tuple(A.shape), dtype=np.float64 if A.dtype == torch.float64 else np.float32)
 treg = torch.from_numpy(hreg)
 rc = torch.cuda.cudart().cudaHostRegister(treg.data_ptr(), treg.numel() * treg.element_size(), 0)
 treg.copy_(A)
 torch.cuda.synchronize()
-print("registered rc", int(rc), "is_pinned(torch pinned)", _is_pinned(torch, hp.numpy()), "is_pinned(registered)",
-      _is_pinned(torch, hreg))
-d = torch.empty_like(A)
-t("raw H2D copy_ torch-pinned", lambda: d.copy_(hp, non_blocking=True))
+print("registered rc", int(rc), "is_pinned(registered)", _is_pinned(torch, hreg), flush=True)
+d = A if big else torch.empty_like(A)
+if not big:
+    t("raw H2D copy_ torch-pinned", lambda: d.copy_(hp, non_blocking=True))
 t("raw H2D copy_ registered numpy", lambda: d.copy_(torch.from_numpy(hreg), non_blocking=True))
 del d
-for label, hv in (("torch-pinned", hp.numpy()), ("registered", hreg)):
+if big:
+    del A
+    torch.cuda.empty_cache()
+for label, hv in ((("torch-pinned", hp.numpy()),) if not big else ()) + (("registered", hreg),):
     t(f"stage only 256 [{label}]", lambda: stage_stream(sp.ArraySnapshotStream(hv), 256))
     t(f"power_svd host stream -> device result [{label}]",
       lambda: sp.power_svd(sp.ArraySnapshotStream(hv), op, cfg.k, pc, return_device=True))
     t(f"power_svd host stream -> numpy result [{label}]",
       lambda: sp.power_svd(sp.ArraySnapshotStream(hv), op, cfg.k, pc))
+if big:
+    sys.exit(0)
 r = sp.power_svd(sp.DeviceSnapshotStream(A), op, cfg.k, pc, return_device=True)
 t("device-resident power_svd", lambda: sp.power_svd(sp.DeviceSnapshotStream(A), op, cfg.k, pc, return_device=True), reps=10)
 t("D2H of U,S,V (pageable .cpu())", lambda: (r.u.cpu(), r.s.cpu(), r.v.cpu()))

@@ -101,3 +101,33 @@ def test_power_svd_from_a_pageable_array_and_a_file_agree(cuda, tmp_path):
             assert fs.passes_completed == 1
     assert r1.s.tobytes() == r2.s.tobytes()
     assert r1.u.tobytes() == r2.u.tobytes() and r1.v.tobytes() == r2.v.tobytes()
+
+
+def test_result_buffers_are_leased_not_shared(cuda):
+    """Results land in page-locked buffers leased from a pool (device.to_host_many):
+    two live results never share memory, and a dropped result's buffer is
+    reused by the next call."""
+    import gc
+
+    from paper_2105_01271_b200 import device as dv
+    x = cuda.arange(600000, dtype=cuda.float64, device="cuda").reshape(3000, 200)   # 4.8 MB: pooled
+    small = cuda.arange(10, dtype=cuda.float64, device="cuda")                      # torch's allocator
+    a, s = dv.to_host_many(x, small)
+    b, = dv.to_host_many(x * 2.0)
+    assert not np.shares_memory(a, b)
+    np.testing.assert_array_equal(a, np.arange(600000.0).reshape(3000, 200))
+    np.testing.assert_array_equal(b, 2.0 * a)
+    np.testing.assert_array_equal(s, np.arange(10.0))
+    view = a[5:7, :3]
+    addr = a.ctypes.data
+    del a
+    gc.collect()
+    c, = dv.to_host_many(x + 1.0)           # `view` still holds a's lease: no reuse
+    assert c.ctypes.data != addr
+    np.testing.assert_array_equal(view, np.arange(600000.0).reshape(3000, 200)[5:7, :3])
+    del view
+    gc.collect()
+    d, = dv.to_host_many(x + 3.0)           # a's buffer is back in the pool
+    assert d.ctypes.data == addr
+    np.testing.assert_array_equal(d[0, :3], [3.0, 4.0, 5.0])
+    np.testing.assert_array_equal(c[0, :3], [1.0, 2.0, 3.0])
