@@ -277,12 +277,32 @@ def _gen_shard(cfg, rank, world, dev):
 
 def _events_ms(fn, reps, torch):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    trace = bool(os.environ.get("SPB_BENCH_TRACE"))
+    marks, walls = [], []
+    # like timeit (and the headline loop): no cyclic-GC pass inside the timed
+    # region -- a generation-2 collection stalled one call of twenty by 35-180 ms
+    gc.collect()
+    was_on = gc.isenabled()
+    gc.disable()
     torch.cuda.synchronize()
     e0.record()
     for _ in range(reps):
+        t0 = time.perf_counter()
         out = fn()
+        if trace:
+            walls.append(1e3 * (time.perf_counter() - t0))
+            marks.append(torch.cuda.Event(enable_timing=True))
+            marks[-1].record()
     e1.record()
     torch.cuda.synchronize()
+    if was_on:
+        gc.enable()
+    if trace:
+        prev, per = e0, []
+        for mk in marks:
+            per.append(round(prev.elapsed_time(mk), 3))
+            prev = mk
+        sys.stderr.write(f"[trace] per-call device ms {per}\n[trace] per-call host ms {[round(w, 3) for w in walls]}\n")
     return e0.elapsed_time(e1) / reps, out
 
 
@@ -349,6 +369,20 @@ def extra_configs(names, dev, torch):
             if done % 8 == 0:
                 torch.cuda.synchronize()
         ms, res = _events_ms(svd, 20 if name == "cfg2" else 10, torch)
+        if os.environ.get("SPB_BENCH_TRACE"):   # diagnostics: per-call wall times and the C++ host marks
+            import ctypes
+            from paper_2105_01271_b200 import _lib
+            lib = _lib.load()
+            lib.sp_host_trace.restype = ctypes.c_char_p
+            lib.sp_host_trace()
+            for _ in range(4):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                svd()
+                t1 = time.perf_counter()
+                tr = lib.sp_host_trace().decode()
+                torch.cuda.synchronize()
+                sys.stderr.write(f"[trace {name}] call {1e6 * (t1 - t0):.1f} us, idle after {1e6 * (time.perf_counter() - t0):.1f} us\n{tr}\n")
         rec = {"call": "power_svd" if cfg.q else "single_pass_svd", "ms": ms, "GBps_A": cfg.a_bytes / ms / 1e6,
                "kept_rank": int(res.kept_rank), "m": cfg.m, "n": cfg.n, "n_c": int(cols.size), "k": cfg.k,
                "dtype": cfg.dtype}
@@ -360,11 +394,15 @@ def extra_configs(names, dev, torch):
         if name in ("cfg3", "cfg5"):
             def pid():
                 return sp.power_id(sp.DeviceSnapshotStream(A), op, cfg.k, pc, return_device=True)
-            f = pid()
-            del f
+            # two untimed calls: the pools for the large workspaces (enrichment
+            # levels, candidate block) are still growing during the second
+            # (measured: 771, 810, 606, 571, 599, 573 ms for calls 0-5 at cfg5)
+            for _ in range(2):
+                f = pid()
+                del f
             gc.collect()
             torch.cuda.empty_cache()
-            ms_id, f = _events_ms(pid, 2, torch)
+            ms_id, f = _events_ms(pid, 3, torch)
             rec["power_id"] = {"ms": ms_id, "k": cfg.k, "lift_r": int(f.r)}
             del f
         out[name] = rec
