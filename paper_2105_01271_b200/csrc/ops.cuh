@@ -23,6 +23,7 @@ struct TsqrPlan {
   struct Level {
     int64_t rows = 0;
     int nch = 0, cl = 0;
+    int ch = 256;  // rows per CTA of the level's leaf kernel
     double* V = nullptr;
     double* T = nullptr;
     double* Rs = nullptr;

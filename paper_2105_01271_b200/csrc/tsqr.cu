@@ -44,6 +44,7 @@ constexpr int kQWarps = 8;
 constexpr int kQThreads = kQWarps * 32;
 constexpr int kQCH = kQWarps * 32;      // rows per CTA
 constexpr int kQMaxCluster = 16;        // CTAs per chunk (non-portable cluster size)
+constexpr int kQSlotsTall = 40;         // register slots per lane of the 320-row leaf variant
 
 // Row mapping: local row g = 8*i + w lives in warp w, register slot i, so
 // the 32 diagonal rows are spread 4 per warp (slots 0..3): only those slots
@@ -62,6 +63,7 @@ constexpr int kQDiagSlots = kQB / kQWarps;  // 4
 // to Tg, and its cols x cols upper-triangular R to Rs[h * cols ..) (ld 32).
 // When Rfinal != nullptr (single chunk = root) R is also written there with
 // diag(R) >= 0 and the row signs to sgn.
+template <int NS>  // register slots per lane: a CTA holds 8 NS rows (NS = 32: 256, NS = 40: 320)
 __global__ void __launch_bounds__(kQThreads)
 tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t ldx, double* __restrict__ V,
                  double* __restrict__ Tg, double* __restrict__ Rs, double* __restrict__ Rfinal, int64_t ldr,
@@ -75,20 +77,21 @@ tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t l
   __shared__ double zs[kQB][kQB + 1];  // zs[c][j] = v_c^T v_j (c < j)
   __shared__ double ts[kQB][kQB + 1];  // T (upper triangular)
   __shared__ double tau_s[kQB], inv_s[kQB], beta_s[kQB];
-  __shared__ __align__(16) double colb[kQWarps][kQB];
+  __shared__ __align__(16) double colb[kQWarps][NS];
+  constexpr int CH = NS * kQWarps;  // rows per CTA
   cg::cluster_group cluster = cg::this_cluster();
   const int cl = (int)cluster.num_blocks();
   const int cr = (int)cluster.block_rank();
   const int w = threadIdx.x >> 5, c = threadIdx.x & 31;
   const int64_t h = blockIdx.x / cl;
-  const int64_t chunk0 = h * (int64_t)cl * kQCH;
-  const int64_t c0 = chunk0 + (int64_t)cr * kQCH;  // my first row
-  const int nrow = (int)std::max<int64_t>(0, imin64(kQCH, rows - c0));
-  const int chunk_rows = (int)imin64((int64_t)cl * kQCH, rows - chunk0);
+  const int64_t chunk0 = h * (int64_t)cl * CH;
+  const int64_t c0 = chunk0 + (int64_t)cr * CH;  // my first row
+  const int nrow = (int)std::max<int64_t>(0, imin64(CH, rows - c0));
+  const int chunk_rows = (int)imin64((int64_t)cl * CH, rows - chunk0);
   const bool top = cr == 0;  // rows 0..31 of the chunk live in rank 0
-  double x[32];
+  double x[NS];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
+  for (int i = 0; i < NS; ++i) {
     const int g = qrow(i, w);
     x[i] = (g < nrow && c < cols) ? X[(c0 + g) * ldx + c] : 0.0;
   }
@@ -123,12 +126,12 @@ tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t l
     // partial <x_j, x_c> over my rows
     if (c == j) {
 #pragma unroll
-      for (int i = 0; i < 32; i += 2) *reinterpret_cast<double2*>(&colb[w][i]) = make_double2(x[i], x[i + 1]);
+      for (int i = 0; i < NS; i += 2) *reinterpret_cast<double2*>(&colb[w][i]) = make_double2(x[i], x[i + 1]);
     }
     __syncwarp();
-    double xj[32];
+    double xj[NS];
 #pragma unroll
-    for (int i = 0; i < 32; i += 2) {
+    for (int i = 0; i < NS; i += 2) {
       const double2 t = *reinterpret_cast<const double2*>(&colb[w][i]);
       xj[i] = t.x;
       xj[i + 1] = t.y;
@@ -142,7 +145,7 @@ tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t l
 #pragma unroll
     for (int u = 0; u < 8; ++u) pa[u] = xj[u] * x[u];
 #pragma unroll
-    for (int i = 8; i < 32; i += 8)
+    for (int i = 8; i < NS; i += 8)
 #pragma unroll
       for (int u = 0; u < 8; ++u) pa[u] = fma(xj[i + u], x[i + u], pa[u]);
     red[buf][w][c] = ((pa[0] + pa[1]) + (pa[2] + pa[3])) + ((pa[4] + pa[5]) + (pa[6] + pa[7]));
@@ -234,7 +237,7 @@ tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t l
     const double wc = c > j ? tj * vv : 0.0;
     const double sc = inv * wc;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) x[i] = fma(-xj[i], sc, x[i]);
+    for (int i = 0; i < NS; ++i) x[i] = fma(-xj[i], sc, x[i]);
     if (top && w == jw) {
 #pragma unroll
       for (int i = 0; i < kQDiagSlots; ++i)
@@ -261,9 +264,9 @@ tsqr_leaf_kernel(const double* __restrict__ X, int64_t rows, int cols, int64_t l
   // reflectors (coalesced rows)
   const double inv_c = c < nref ? inv_s[c] : 0.0;
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
+  for (int i = 0; i < NS; ++i) {
     const int g = qrow(i, w);
-    const int gc = cr * kQCH + g;  // chunk-local row
+    const int gc = cr * CH + g;  // chunk-local row
     if (g < nrow) V[(c0 + g) * kQB + c] = (gc > c && c < nref) ? x[i] * inv_c : 0.0;
   }
   if (!top) return;
@@ -488,8 +491,9 @@ tsqr_apply_kernel(const double* __restrict__ V, const double* __restrict__ Tg, i
 // (4096 rows); 16-CTA clusters are a non-portable size -- fall back to 8
 static int g_max_cluster = 0;
 
-static int launch_leaf(int nch, int cl, const double* in, int64_t r, int cols, int64_t in_ld, double* V, double* T,
-                       double* Rs, double* R, int64_t ldr, double* sgn, cudaStream_t s, double* Mg = nullptr) {
+static int launch_leaf(int ns, int nch, int cl, const double* in, int64_t r, int cols, int64_t in_ld, double* V,
+                       double* T, double* Rs, double* R, int64_t ldr, double* sgn, cudaStream_t s,
+                       double* Mg = nullptr) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nch * cl);
   cfg.blockDim = dim3(kQThreads);
@@ -504,7 +508,9 @@ static int launch_leaf(int nch, int cl, const double* in, int64_t r, int cols, i
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, tsqr_leaf_kernel, in, r, cols, in_ld, V, T, Rs, R, ldr, sgn, Mg);
+  const cudaError_t e =
+      ns == kQSlotsTall ? cudaLaunchKernelEx(&cfg, tsqr_leaf_kernel<kQSlotsTall>, in, r, cols, in_ld, V, T, Rs, R, ldr, sgn, Mg)
+                        : cudaLaunchKernelEx(&cfg, tsqr_leaf_kernel<32>, in, r, cols, in_ld, V, T, Rs, R, ldr, sgn, Mg);
   if (e != cudaSuccess) {
     cudaGetLastError();
     set_error(std::string("tsqr leaf launch: ") + cudaGetErrorString(e));
@@ -517,7 +523,9 @@ static int launch_leaf(int nch, int cl, const double* in, int64_t r, int cols, i
 static int max_cluster() {
   if (g_max_cluster == 0) {
     int mc = 8;
-    if (cudaFuncSetAttribute(tsqr_leaf_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+    if (cudaFuncSetAttribute(tsqr_leaf_kernel<32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+        cudaFuncSetAttribute(tsqr_leaf_kernel<kQSlotsTall>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+            cudaSuccess) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(kQMaxCluster);
       cfg.blockDim = dim3(kQThreads);
@@ -529,7 +537,9 @@ static int max_cluster() {
       cfg.attrs = attr;
       cfg.numAttrs = 1;
       int nclusters = 0;
-      if (cudaOccupancyMaxActiveClusters(&nclusters, tsqr_leaf_kernel, &cfg) == cudaSuccess && nclusters > 0)
+      int ntall = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclusters, tsqr_leaf_kernel<32>, &cfg) == cudaSuccess && nclusters > 0 &&
+          cudaOccupancyMaxActiveClusters(&ntall, tsqr_leaf_kernel<kQSlotsTall>, &cfg) == cudaSuccess && ntall > 0)
         mc = kQMaxCluster;
     }
     cudaGetLastError();
@@ -559,9 +569,12 @@ int tsqr_factor(int64_t rows, int cols, const double* X, int64_t ldx, double* R,
     L.rows = r;
     // clusters only while all chunks fit in one wave: past ~148 CTAs the
     // per-step cluster exchange costs more than the extra tree level it saves
-    const int64_t ctas = ceil_div(r, kQCH);
+    // 320-row CTAs when that makes the whole level one cluster (one tree
+    // level and two apply launches less: cfg3's 5000-row test blocks)
+    L.ch = (r > (int64_t)mc * kQCH && r <= (int64_t)mc * kQSlotsTall * kQWarps) ? kQSlotsTall * kQWarps : kQCH;
+    const int64_t ctas = ceil_div(r, L.ch);
     L.cl = ctas <= kNumSMs ? (int)std::min<int64_t>(mc, ctas) : 1;
-    L.nch = (int)ceil_div(r, (int64_t)L.cl * kQCH);
+    L.nch = (int)ceil_div(r, (int64_t)L.cl * L.ch);
     L.V = ar.alloc<double>((size_t)r * kQB);
     L.T = ar.alloc<double>((size_t)L.nch * kQB * kQB);
     L.Rs = ar.alloc<double>((size_t)L.nch * cols * kQB);
@@ -577,11 +590,11 @@ int tsqr_factor(int64_t rows, int cols, const double* X, int64_t ldx, double* R,
         set_error("tsqr workspace allocation failed");
         return SP_ECUDA;
       }
-      SPB_TRY(launch_leaf(1, L.cl, in, r, cols, in_ld, L.V, L.T, L.Rs, R, ldr, plan.sgn, s, plan.Mg));
+      SPB_TRY(launch_leaf(L.ch / kQWarps, 1, L.cl, in, r, cols, in_ld, L.V, L.T, L.Rs, R, ldr, plan.sgn, s, plan.Mg));
       plan.lv.push_back(L);
       return SP_OK;
     }
-    SPB_TRY(launch_leaf(L.nch, L.cl, in, r, cols, in_ld, L.V, L.T, L.Rs, root ? R : nullptr, ldr,
+    SPB_TRY(launch_leaf(L.ch / kQWarps, L.nch, L.cl, in, r, cols, in_ld, L.V, L.T, L.Rs, root ? R : nullptr, ldr,
                         root ? plan.sgn : nullptr, s));
     plan.lv.push_back(L);
     if (root) break;
@@ -618,7 +631,7 @@ int tsqr_form_q(const TsqrPlan& plan, double* Q, int64_t ldq, Arena& ar, cudaStr
       }
       ldo = kQB;
     }
-    const int chunk_rows = L.cl * kQCH;
+    const int chunk_rows = L.cl * L.ch;
     SPB_CUDA(launch_pdl((tsqr_apply_kernel), dim3(L.nch * (chunk_rows / kApRows)), dim3(kQThreads), 0, s,
                         (const double*)L.V, (const double*)L.T, L.rows, cols, chunk_rows, bin,
                         (const double*)plan.sgn, out, ldo));

@@ -124,7 +124,8 @@ def test_gemm(cuda, ta, tb, M, N, K):
 # ------------------------------------------------------------------ K4 ----
 @pytest.mark.parametrize("rows,cols", [(1000, 8), (5000, 32), (70000, 20), (300, 64), (2000, 100), (32, 32),
                                        (4096, 32), (65536, 7), (257, 32), (33, 32), (512, 1), (100, 3),
-                                       (200000, 32), (7, 7)])
+                                       (200000, 32), (7, 7), (4097, 32), (5120, 32), (5121, 32), (4800, 17),
+                                       (5000, 216)])
 def test_tsqr(cuda, rows, cols):
     x = philox(rows + cols).standard_normal((rows, cols)) * np.logspace(0, -8, cols)
     dx = _dev(x, cuda)
