@@ -437,18 +437,28 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
       // a TSQR instead of those plus the dd Gram, the Jacobi core, the
       // doorbell round trip and the restart product (cfg3: 250 vs 414 us).
       static const bool no_blind = getenv("SPB_RR_EVERY_STEP") != nullptr;
-      if (need < 0 && itn == 0 && !no_blind && kept > 0 && b - 8 > kept) {
+      // ID mode: the same between the first step and the step at which the
+      // leading-triplet rate test can first pass; in bulk mode (accepted
+      // itn - bulk_from >= 3 steps after the flat stretch was found) the two
+      // steps in between.
+      int blind = 0;
+      if (!no_blind && need < 0 && itn == 0 && kept > 0 && b - 8 > kept) {
         const double rho = hs[b - 8] / hs[kept - 1];
-        if (rho > 0.0 && rho < 1.0) {
-          const int pass_at = (int)std::ceil((std::log(1e-12) / std::log(rho) - 2.0) / 2.0);
-          const int blind = std::min(pass_at - 2, max_it - 3);
-          for (int j = 0; j < blind; ++j) {
-            SPB_TRY(gemm(1, 0, cols, b, rows, 1.0, X, ldx, Q, b, 0.0, Z, b, s));
-            SPB_TRY(gemm(0, 0, rows, b, cols, 1.0, X, ldx, Z, b, 0.0, Y, b, s));
-            SPB_TRY(tsqr(rows, b, Y, b, Q, b, Rt, b, s));
-            ++itn;
-          }
-        }
+        if (rho > 0.0 && rho < 1.0)
+          blind = (int)std::ceil((std::log(1e-12) / std::log(rho) - 2.0) / 2.0) - 2;
+      } else if (!no_blind && need >= 0 && out.bulk && itn == bulk_from) {
+        blind = 2;
+      } else if (!no_blind && need >= 0 && !out.bulk && itn == 0 && std::min(kept, need) > 0) {
+        const double rho = hs[b - 8] / hs[std::min(kept, need) - 1];
+        if (rho > 0.0 && rho < 1.0)
+          blind = std::max(1, (int)std::ceil((std::log(1e-12) / std::log(rho) - 2.0) / 2.0)) - 2;
+      }
+      blind = std::min(blind, max_it - 3 - itn);
+      for (int j = 0; j < blind; ++j) {
+        SPB_TRY(gemm(1, 0, cols, b, rows, 1.0, X, ldx, Q, b, 0.0, Z, b, s));
+        SPB_TRY(gemm(0, 0, rows, b, cols, 1.0, X, ldx, Z, b, 0.0, Y, b, s));
+        SPB_TRY(tsqr(rows, b, Y, b, Q, b, Rt, b, s));
+        ++itn;
       }
     }
     if (grow) {
