@@ -124,6 +124,15 @@ int sp_gemm(int32_t trans_a, int32_t trans_b, int64_t M, int64_t N, int64_t K, d
             const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
             double* C, int64_t ldc, void* stream);
 
+/* W = A A^T (M x M, A row-major M x K): the symmetric product of the power
+ * enrichment in its (C C^T) s0 association (src/power.py:99-108, 282-285; used
+ * when the column set is wider than the snapshot count, cfg5).  Only the
+ * tiles on and above the diagonal are computed, the rest is mirrored: W is
+ * exactly symmetric at half the DMMA work of sp_gemm(0, 1, ...).
+ */
+int sp_gemm_aat(int64_t M, int64_t K, const double* A, int64_t lda, double* W, int64_t ldw,
+                void* stream);
+
 /* --------------------------------------------------------------- K3x -----
  * C_hi (+ C_lo) = op(A) (B_hi + B_lo), nearly exactly rounded: Ozaki slices of
  * A's rows and B's columns, every level sum an exact DMMA GEMM, levels summed

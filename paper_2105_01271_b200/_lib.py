@@ -44,6 +44,7 @@ SIGNATURES = {
     "sp_check_columns": [_P, _I64, _I64, _P],
     "sp_skinny_atz": [_P, _I32, _I64, _I64, _I64, _P, _I64, _I32, _P, _I64, _P],
     "sp_gemm": [_I32, _I32, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64, _P],
+    "sp_gemm_aat": [_I64, _I64, _P, _I64, _P, _I64, _P],
     "sp_gemm_exact": [_I32, _I64, _I64, _I64, _P, _I64, _P, _P, _I64, _P, _P, _I64, _P],
     "sp_exact_plan": [_I64, _P, _P],
     "sp_exponents": [_I32, _I64, _I64, _P, _I64, _P, _P],

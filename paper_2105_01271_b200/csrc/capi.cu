@@ -90,6 +90,10 @@ int sp_gemm(int32_t trans_a, int32_t trans_b, int64_t M, int64_t N, int64_t K, d
   return gemm(trans_a, trans_b, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ST(stream));
 }
 
+int sp_gemm_aat(int64_t M, int64_t K, const double* A, int64_t lda, double* W, int64_t ldw, void* stream) {
+  return gemm_aat(M, K, A, lda, W, ldw, ST(stream));
+}
+
 int sp_gemm_exact(int32_t trans_a, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                   const double* B_hi, const double* B_lo, int64_t ldb, double* C_hi, double* C_lo,
                   int64_t ldc, void* stream) {

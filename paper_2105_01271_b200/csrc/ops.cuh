@@ -33,6 +33,8 @@ struct TsqrPlan {
   double* Mg = nullptr;  // single-chunk root: M = T V_top^T diag(sgn)
   int cols = 0;
 };
+// W = A A^T (M x M) from the tiles on and above the diagonal, mirrored
+int gemm_aat(int64_t M, int64_t K, const double* A, int64_t lda, double* W, int64_t ldw, cudaStream_t s);
 int tsqr_factor(int64_t rows, int cols, const double* X, int64_t ldx, double* R, int64_t ldr, TsqrPlan& plan,
                 Arena& ar, cudaStream_t s);
 int tsqr_form_q(const TsqrPlan& plan, double* Q, int64_t ldq, Arena& ar, cudaStream_t s);

@@ -1067,7 +1067,7 @@ int power_id(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, cons
       set_error("enriched sketch allocation failed");
       return SP_ECUDA;
     }
-    if (!ref_order) SPB_TRY(gemm(0, 1, m, m, ncols, 1.0, C, ncols, C, ncols, 0.0, W, m, s));
+    if (!ref_order) SPB_TRY(gemm_aat(m, ncols, C, ncols, W, m, s));  // W = C C^T, upper tiles + mirror
     for (int it = 0; it < q; ++it) {
       if (ref_order && plain) {
         SPB_TRY(gemm(1, 0, ncols, nc, m, 1.0, C, ncols, E, nc, 0.0, T, nc, s));

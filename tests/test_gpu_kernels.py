@@ -121,6 +121,19 @@ def test_gemm(cuda, ta, tb, M, N, K):
     np.testing.assert_allclose(dC.cpu().numpy(), want, rtol=0, atol=1e-12 * np.sqrt(K) * 8)
 
 
+@pytest.mark.parametrize("M,K", [(1, 5), (64, 300), (65, 300), (200, 1000), (333, 4100), (2000, 9000)])
+def test_gemm_aat_symmetric_product(cuda, M, K):
+    """W = A A^T from the upper tiles + mirror equals the plain product and is
+    exactly symmetric (src/power.py:99-108 in the (C C^T) s0 association)."""
+    A = philox(M + K).standard_normal((M, K))
+    dA = _dev(A, cuda)
+    W = cuda.full((M, M), float("nan"), dtype=cuda.float64, device="cuda")
+    _lib.call("sp_gemm_aat", M, K, dA.data_ptr(), K, W.data_ptr(), M, _stream(cuda))
+    w = W.cpu().numpy()
+    np.testing.assert_array_equal(w, w.T)
+    np.testing.assert_allclose(w, A @ A.T, rtol=0, atol=1e-12 * np.sqrt(K) * 8)
+
+
 # ------------------------------------------------------------------ K4 ----
 @pytest.mark.parametrize("rows,cols", [(1000, 8), (5000, 32), (70000, 20), (300, 64), (2000, 100), (32, 32),
                                        (4096, 32), (65536, 7), (257, 32), (33, 32), (512, 1), (100, 3),
