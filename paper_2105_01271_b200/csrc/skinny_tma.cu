@@ -14,6 +14,7 @@
 // (16 rows per stage: fewer, larger stages measured 0.83 -> 0.90 of the HBM
 // roofline at cfg2, where a CTA's row segment is only 3.5 KB).
 #include <cstdlib>
+#include <type_traits>
 
 #include "async.cuh"
 #include "common.cuh"
@@ -132,36 +133,45 @@ skinny_tma_kernel(const TA* __restrict__ A, int64_t m, int64_t n, int64_t lda, c
         const unsigned char* sb = smem + stage * L::kStageBytes;
         const double* zs = reinterpret_cast<const double*>(sb + L::kZOff);
         mbar_wait(&full[stage], ph);
+        // full stages take the unguarded body (no selects in the hot loop);
+        // the last, ragged row block masks rows past it (stale bytes)
+        auto body = [&](auto guard_tag) {
+          constexpr bool kGuard = decltype(guard_tag)::value;
 #pragma unroll
-        for (int ks = 0; ks < kTmaRows / 4; ++ks) {
-          const int row = 4 * ks + t4;
-          const bool live = row < nr;  // rows past the block hold stale bytes
-          double b[NT];
+          for (int ks = 0; ks < kTmaRows / 4; ++ks) {
+            const int row = 4 * ks + t4;
+            const bool live = !kGuard || row < nr;
+            double b[NT];
 #pragma unroll
-          for (int q = 0; q < NT; ++q) b[q] = (live && 8 * q + g < R) ? zs[row * R + 8 * q + g] : 0.0;
-          const unsigned char* ap = sb + row * L::kRowPitch + (warp * 32 + g) * 16;
+            for (int q = 0; q < NT; ++q) b[q] = (live && 8 * q + g < R) ? zs[row * R + 8 * q + g] : 0.0;
+            const unsigned char* ap = sb + row * L::kRowPitch + (warp * 32 + g) * 16;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            double a[V];
-            if constexpr (V == 2) {
-              const double2 x = *reinterpret_cast<const double2*>(ap + j * 128);
-              a[0] = x.x;
-              a[1] = x.y;
-            } else {
-              const float4 x = *reinterpret_cast<const float4*>(ap + j * 128);
-              a[0] = x.x;
-              a[1] = x.y;
-              a[2] = x.z;
-              a[3] = x.w;
-            }
+            for (int j = 0; j < 4; ++j) {
+              double a[V];
+              if constexpr (V == 2) {
+                const double2 x = *reinterpret_cast<const double2*>(ap + j * 128);
+                a[0] = x.x;
+                a[1] = x.y;
+              } else {
+                const float4 x = *reinterpret_cast<const float4*>(ap + j * 128);
+                a[0] = x.x;
+                a[1] = x.y;
+                a[2] = x.z;
+                a[3] = x.w;
+              }
 #pragma unroll
-            for (int v = 0; v < V; ++v) {
-              const double av = live ? a[v] : 0.0;
+              for (int v = 0; v < V; ++v) {
+                const double av = live ? a[v] : 0.0;
 #pragma unroll
-              for (int q = 0; q < NT; ++q) k2_dmma(acc[j][v][q][0], acc[j][v][q][1], av, b[q]);
+                for (int q = 0; q < NT; ++q) k2_dmma(acc[j][v][q][0], acc[j][v][q][1], av, b[q]);
+              }
             }
           }
-        }
+        };
+        if (nr == kTmaRows)
+          body(std::false_type{});
+        else
+          body(std::true_type{});
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
         if (++stage == kTmaStages) {

@@ -1,26 +1,28 @@
 #!/bin/bash
-# Round-2 profiles: launch list of the default (cfg4) bench step, --set full of
-# the A pass (K2) and the gather, launch lists of one power_id call (cfg3,
-# cfg5), the FP64 peaks.  Every ncu command follows the same command's plain
-# run that exited 0.
-cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
-export SPB_NO_BUILD=1
-mkdir -p gpurun_out
-python scripts/fp64_peak.py > gpurun_out/r2_fp64_peak.json 2>&1; cat gpurun_out/r2_fp64_peak.json
-B="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu --no-extra"
-timeout 600 $B > gpurun_out/r2p_plain.log 2>&1 && \
-timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-  --log-file gpurun_out/r2_bench_launches_cfg4.csv $B > gpurun_out/r2p_ncu_launches.log 2>&1
-echo "launch list rc=$?"
-B1="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-extra"
-timeout 600 $B1 > gpurun_out/r2p_plain1.log 2>&1 && \
-timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"skinny_tma|srht" -s 4 -c 2 \
-  -o gpurun_out/r2_prof_cfg4 $B1 > gpurun_out/r2p_ncu_full.log 2>&1
-echo "full rc=$?"
+# Round-2 (final) profile pass, run on the GPU box through gpurun:
+#   gpurun --timeout 3000 -- 'bash scripts/profile_r2.sh'
+# Every profiled command first runs plain (must exit 0); numbers printed under
+# ncu are never bench values.  Outputs land in gpurun_out/ and are summarised
+# into profiles/ here (scripts/launch_shares.py, scripts/ncu_summary.py).
+set -u
+O=gpurun_out
+mkdir -p $O
+NCU_LIST="ncu --metrics gpu__time_duration.sum --clock-control none --csv"
+B4="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu --no-extra"
+B2="python bench.py --config cfg2 --steps 5 --warmup 3 --no-e2e --no-cpu --no-extra"
+B3="python bench.py --config cfg3 --steps 3 --warmup 3 --no-e2e --no-cpu --no-extra"
+$B4 > $O/r2f_plain_cfg4.json 2> $O/r2f_plain_cfg4.err || { echo "plain cfg4 failed"; exit 1; }
+$NCU_LIST --log-file $O/r2f_launches_cfg4.csv $B4 > $O/r2f_ncu_cfg4.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:'skinny_tma|srht' -s 4 -c 2 -f -o $O/r2f_prof_cfg4 \
+    python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-extra > $O/r2f_ncu_full_cfg4.log 2>&1
+$B2 > $O/r2f_plain_cfg2.json 2> $O/r2f_plain_cfg2.err && \
+  $NCU_LIST --log-file $O/r2f_launches_cfg2.csv $B2 > $O/r2f_ncu_cfg2.log 2>&1
+$B3 > $O/r2f_plain_cfg3.json 2> $O/r2f_plain_cfg3.err && \
+  $NCU_LIST --log-file $O/r2f_launches_cfg3.csv $B3 > $O/r2f_ncu_cfg3.log 2>&1
 for c in cfg3 cfg5; do
-  timeout 600 python scripts/id_call.py $c > gpurun_out/r2p_id_$c.log 2>&1 && \
-  timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-    --log-file gpurun_out/r2_id_launches_$c.csv python scripts/id_call.py $c > gpurun_out/r2p_ncu_id_$c.log 2>&1
-  echo "id $c rc=$?"; cat gpurun_out/r2p_id_$c.log
+  python scripts/id_call.py $c > $O/r2f_id_plain_$c.log 2>&1 && \
+    $NCU_LIST --log-file $O/r2f_id_launches_$c.csv python scripts/id_call.py $c > $O/r2f_id_ncu_$c.log 2>&1
 done
-ls -la gpurun_out | head -30
+ncu --set full --clock-control none --import-source on -k regex:'jacobi_blk' -s 2 -c 1 -f -o $O/r2f_prof_jblk \
+    python scripts/id_call.py cfg3 > $O/r2f_ncu_full_jblk.log 2>&1
+ls -la $O | tail -30
