@@ -480,15 +480,27 @@ jacobi_grid_kernel(int n, int np, const double* __restrict__ M, int64_t ldm, boo
         a = warp_sum(a);
         b = warp_sum(b);
         g = warp_sum(g);
-        if (g != 0.0 && fmin(a, b) > negl && fabs(g) > kJacTol * sqrt(a) * sqrt(b)) {
-          const double zeta = (b - a) / (2.0 * g);
-          double t;
-          if (fabs(zeta) > 1e150)
-            t = 0.5 / zeta;
-          else
-            t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-          const double cs = 1.0 / sqrt(fma(t, t, 1.0));
-          const double sn = cs * t;
+        // thresholds on squares and the MUFU-rsqrt rotation of jacobi32 (the
+        // IEEE sqrt / division forms cost ~3000 dependent cycles per round)
+        const double ab = a * b;
+        const bool big = !(ab < 1e300);
+        if (g != 0.0 && fmin(a, b) > negl &&
+            (big ? fabs(g) > kJacTol * sqrt(a) * sqrt(b) : g * g > (kJacTol * kJacTol) * ab)) {
+          const double d = b - a, h = 2.0 * g;
+          const double ad = fabs(d), ah = fabs(h);
+          double cs, sn;
+          if (ad < 1e140 && ah < 1e140 && (ad > 1e-140 || ah > 1e-140)) {
+            const double s2 = fma(d, d, h * h);
+            const double rh = fast_rsqrt(s2);
+            const double u = fma(0.5 * ad, rh, 0.5);
+            const double w = fast_rsqrt(u);
+            cs = u * w;
+            sn = (copysign(0.5, d) * h) * (rh * w);
+          } else {
+            const double t = copysign(1.0, d) * h / (ad + hypot(d, h));
+            cs = rsqrt(fma(t, t, 1.0));
+            sn = cs * t;
+          }
           double* vp = Vm + (int64_t)p * np;
           double* vq = Vm + (int64_t)q * np;
           for (int i = lane; i < np; i += 32) {
@@ -501,7 +513,9 @@ jacobi_grid_kernel(int n, int np, const double* __restrict__ M, int64_t ldm, boo
           }
           if (lane == 0) {
             atomicOr(&rot[sweep & 1], 1);
-            atomicMax(&relmax[sweep & 1], (unsigned long long)__double_as_longlong(fabs(g) / (sqrt(a) * sqrt(b))));
+            // relmax holds 1.0 once a rotation above kJacQuad in relative size was made
+            if (big ? fabs(g) > kJacQuad * sqrt(a) * sqrt(b) : g * g > (kJacQuad * kJacQuad) * ab)
+              atomicMax(&relmax[sweep & 1], (unsigned long long)__double_as_longlong(1.0));
           }
         }
       }
@@ -559,7 +573,7 @@ constexpr int kJbThreads = 512;    // one warp per pair of the 32 resident colum
 
 template <int RPL>  // rows of W per lane (np = 32 RPL)
 __device__ __forceinline__ void jb_rotate(double* __restrict__ cp, double* __restrict__ cq, int lane, double negl,
-                                          int* rot, unsigned long long* relmax) {
+                                          int* rot) {
   double x[2 * RPL], y[2 * RPL];
 #pragma unroll
   for (int j = 0; j < RPL; ++j) {
@@ -576,30 +590,43 @@ __device__ __forceinline__ void jb_rotate(double* __restrict__ cp, double* __res
   a = warp_sum(a);
   b = warp_sum(b);
   g = warp_sum(g);
-  if (g != 0.0 && fmin(a, b) > negl && fabs(g) > kJacTol * sqrt(a) * sqrt(b)) {
-    const double zeta = (b - a) / (2.0 * g);
-    double t;
-    if (fabs(zeta) > 1e150)
-      t = 0.5 / zeta;
-    else
-      t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-    const double cs = 1.0 / sqrt(fma(t, t, 1.0));
-    const double sn = cs * t;
-#pragma unroll
-    for (int j = RPL; j < 2 * RPL; ++j) {  // the V half
-      x[j] = cp[lane + 32 * j];
-      y[j] = cq[lane + 32 * j];
-    }
-#pragma unroll
-    for (int j = 0; j < 2 * RPL; ++j) {
-      cp[lane + 32 * j] = cs * x[j] - sn * y[j];
-      cq[lane + 32 * j] = fma(sn, x[j], cs * y[j]);
-    }
-    if (lane == 0) {
-      atomicOr(rot, 1);
-      atomicMax(relmax, (unsigned long long)__double_as_longlong(fabs(g) / (sqrt(a) * sqrt(b))));
-    }
+  // thresholds on squares (no square roots) unless the product could overflow;
+  // the rotation from two dependent MUFU rsqrt stages (the jacobi32 forms: the
+  // IEEE sqrt / division sequences of the scalar kernels put ~3000 cycles of
+  // dependent FP64 instructions on every round's critical path)
+  const double ab = a * b;
+  const bool big = !(ab < 1e300);
+  if (!(g != 0.0 && fmin(a, b) > negl &&
+        (big ? fabs(g) > kJacTol * sqrt(a) * sqrt(b) : g * g > (kJacTol * kJacTol) * ab)))
+    return;
+  const double d = b - a, h = 2.0 * g;
+  const double ad = fabs(d), ah = fabs(h);
+  double cs, sn;
+  if (ad < 1e140 && ah < 1e140 && (ad > 1e-140 || ah > 1e-140)) {
+    const double s2 = fma(d, d, h * h);
+    const double rh = fast_rsqrt(s2);
+    const double u = fma(0.5 * ad, rh, 0.5);
+    const double w = fast_rsqrt(u);
+    cs = u * w;
+    sn = (copysign(0.5, d) * h) * (rh * w);
+  } else {
+    const double t = copysign(1.0, d) * h / (ad + hypot(d, h));
+    cs = rsqrt(fma(t, t, 1.0));
+    sn = cs * t;
   }
+#pragma unroll
+  for (int j = RPL; j < 2 * RPL; ++j) {  // the V half
+    x[j] = cp[lane + 32 * j];
+    y[j] = cq[lane + 32 * j];
+  }
+#pragma unroll
+  for (int j = 0; j < 2 * RPL; ++j) {
+    cp[lane + 32 * j] = fma(-sn, y[j], cs * x[j]);
+    cq[lane + 32 * j] = fma(sn, x[j], cs * y[j]);
+  }
+  // a rotation of relative size above kJacQuad keeps the sweeps going
+  if (lane == 0 && (big ? fabs(g) > kJacQuad * sqrt(a) * sqrt(b) : g * g > (kJacQuad * kJacQuad) * ab))
+    *(volatile int*)rot = 1;
 }
 
 template <int RPL>
@@ -637,13 +664,9 @@ jacobi_blk_kernel(int n, const double* __restrict__ M, int64_t ldm, bool trans, 
   for (int c = 0; c < np; ++c) fro += cn[c];
   const double negl = 1e-30 * fro;
   for (int sweep = 0; sweep < kJacMaxSweeps; ++sweep) {
-    int* rt = &rot[sweep & 1];
-    unsigned long long* rm = &relmax[sweep & 1];
+    int* rt = &rot[sweep & 1];  // set by a rotation above kJacQuad in relative size
     for (int round = 0; round < nb - 1; ++round) {
-      if (round == 1 && gtid == 0) {  // nobody reads the other parity until this sweep ends
-        rot[(sweep + 1) & 1] = 0;
-        relmax[(sweep + 1) & 1] = 0ull;
-      }
+      if (round == 1 && gtid == 0) rot[(sweep + 1) & 1] = 0;  // nobody reads the other parity until this sweep ends
       int bi, bj;
       rr_pair(nb, round, blockIdx.x, bi, bj);
       // stage the pair's columns: W half, then V half
@@ -663,13 +686,13 @@ jacobi_blk_kernel(int n, const double* __restrict__ M, int64_t ldm, bool trans, 
           int p, q;
           rr_pair(kJbW, r, k, p, q);
           jb_rotate<RPL>(cols + (size_t)(half * kJbW + p) * 2 * np, cols + (size_t)(half * kJbW + q) * 2 * np, lane,
-                         negl, rt, rm);
+                         negl, rt);
           __syncthreads();
         }
       }
       for (int r = 0; r < kJbW; ++r) {
         const int p = warp, q = kJbW + ((warp + r) & (kJbW - 1));
-        jb_rotate<RPL>(cols + (size_t)p * 2 * np, cols + (size_t)q * 2 * np, lane, negl, rt, rm);
+        jb_rotate<RPL>(cols + (size_t)p * 2 * np, cols + (size_t)q * 2 * np, lane, negl, rt);
         __syncthreads();
       }
       for (int e = tid; e < 32 * (np / 2); e += kJbThreads) {
@@ -682,8 +705,8 @@ jacobi_blk_kernel(int n, const double* __restrict__ M, int64_t ldm, bool trans, 
       }
       grid.sync();
     }
-    if (*(volatile int*)rt == 0 || __longlong_as_double((long long)*(volatile unsigned long long*)rm) < kJacQuad)
-      break;
+    // quadratic convergence: a sweep without a rotation above kJacQuad is the last
+    if (*(volatile int*)rt == 0) break;
   }
   // singular values = column norms, sorted descending (stable by index)
   for (int c = gwarp; c < np; c += nwarps) {
