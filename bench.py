@@ -275,7 +275,11 @@ def _gen_shard(cfg, rank, world, dev):
     return generate_device(cfg, dev, x_range=(b, e)), b * rest
 
 
-def _events_ms(fn, reps, torch):
+def _events_ms(fn, reps, torch, stats=None):
+    """Mean device time per call over `reps` back-to-back calls (CUDA events
+    around the whole loop).  `stats` (a dict) also receives the median and the
+    largest single-call HOST time, so a one-off host stall inside a short loop
+    is visible next to the mean it inflates."""
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     trace = bool(os.environ.get("SPB_BENCH_TRACE"))
     marks, walls = [], []
@@ -289,14 +293,17 @@ def _events_ms(fn, reps, torch):
     for _ in range(reps):
         t0 = time.perf_counter()
         out = fn()
+        walls.append(1e3 * (time.perf_counter() - t0))
         if trace:
-            walls.append(1e3 * (time.perf_counter() - t0))
             marks.append(torch.cuda.Event(enable_timing=True))
             marks[-1].record()
     e1.record()
     torch.cuda.synchronize()
     if was_on:
         gc.enable()
+    if stats is not None:
+        stats["host_ms_median_call"] = statistics.median(walls)
+        stats["host_ms_max_call"] = max(walls)
     if trace:
         prev, per = e0, []
         for mk in marks:
@@ -350,8 +357,13 @@ def extra_configs(names, dev, torch):
     import paper_2105_01271_b200 as sp
     from paper_2105_01271_b200.datagen import generate_device
     out = {}
+    from paper_2105_01271_b200 import _lib as _l
     for name in names:
         cfg = CONFIGS[name]
+        # a new problem size: hand the previous one's cached workspaces back
+        # (cfg5's 134 GB of A + ~25 GB of ID workspaces need the HBM the pool
+        # would otherwise keep for cfg4 / cfg3 block sizes)
+        _l.release_workspaces()
         A = generate_device(cfg, dev)
         op, cols = sp.grid_injection(cfg.grid, cfg.stride)
         pc = sp.PowerConfig(q=cfg.q, columns=cols)
@@ -368,7 +380,8 @@ def extra_configs(names, dev, torch):
             done += 1
             if done % 8 == 0:
                 torch.cuda.synchronize()
-        ms, res = _events_ms(svd, 20 if name == "cfg2" else 10, torch)
+        st = {}
+        ms, res = _events_ms(svd, 200 if name == "cfg2" else 10, torch, st)
         if os.environ.get("SPB_BENCH_TRACE"):   # diagnostics: per-call wall times and the C++ host marks
             import ctypes
             from paper_2105_01271_b200 import _lib
@@ -385,7 +398,7 @@ def extra_configs(names, dev, torch):
                 sys.stderr.write(f"[trace {name}] call {1e6 * (t1 - t0):.1f} us, idle after {1e6 * (time.perf_counter() - t0):.1f} us\n{tr}\n")
         rec = {"call": "power_svd" if cfg.q else "single_pass_svd", "ms": ms, "GBps_A": cfg.a_bytes / ms / 1e6,
                "kept_rank": int(res.kept_rank), "m": cfg.m, "n": cfg.n, "n_c": int(cols.size), "k": cfg.k,
-               "dtype": cfg.dtype}
+               "dtype": cfg.dtype, **st}
         del res
         gc.collect()
         torch.cuda.empty_cache()   # the library's workspaces come from the CUDA mempool, not torch's cache
@@ -402,8 +415,9 @@ def extra_configs(names, dev, torch):
                 del f
             gc.collect()
             torch.cuda.empty_cache()
-            ms_id, f = _events_ms(pid, 3, torch)
-            rec["power_id"] = {"ms": ms_id, "k": cfg.k, "lift_r": int(f.r)}
+            st_id = {}
+            ms_id, f = _events_ms(pid, 3, torch, st_id)
+            rec["power_id"] = {"ms": ms_id, "k": cfg.k, "lift_r": int(f.r), **st_id}
             del f
         out[name] = rec
         del A

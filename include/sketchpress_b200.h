@@ -72,6 +72,14 @@ int sp_abi_version(void);
 const char* sp_last_error(void);
 /* Number of kernels this library launched on the calling thread so far. */
 int64_t sp_launch_count(void);
+/* Hand every cached workspace block of the current device back to the CUDA
+ * memory pool and trim the pool (synchronises the device).  The library keeps
+ * its workspaces across calls (stream-ordered free lists: no allocation on
+ * the critical path of a call); a host application calls this when it wants
+ * the HBM back, e.g. between problems of very different size.  No reference
+ * counterpart (numpy frees its temporaries itself).
+ */
+int sp_release_workspaces(void);
 
 /* Deferred status of the calling thread's last pipeline call: the fused
  * finish stage (r <= 16 kept columns, kappa < 1e6) runs without a host

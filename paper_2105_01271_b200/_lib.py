@@ -38,6 +38,7 @@ SIGNATURES = {
     "sp_abi_version": [],
     "sp_last_error": [],
     "sp_launch_count": [],
+    "sp_release_workspaces": [],
     "sp_deferred_status": [_P],
     "sp_set_finish_mode": [_I32],
     "sp_apply_stencil": [_P, _I32, _I64, _I64, _I64, _P, _P, _I32, _I64, _I32, _P, _I64, _P],
@@ -139,6 +140,11 @@ def call(name: str, *args) -> None:
 
 def launch_count() -> int:
     return int(load().sp_launch_count())
+
+
+def release_workspaces() -> None:
+    """Return the library's cached workspaces (and the CUDA pool's reserve) to the driver."""
+    call("sp_release_workspaces")
 
 
 def deferred_status() -> int:

@@ -52,6 +52,15 @@ extern "C" {
 int sp_abi_version(void) { return SP_ABI_VERSION; }
 const char* sp_last_error(void) { return last_error(); }
 int64_t sp_launch_count(void) { return launches(); }
+int sp_release_workspaces(void) {
+  ws_release_all();
+  int d = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&d) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess)
+    cudaMemPoolTrimTo(pool, 0);
+  cudaGetLastError();
+  return SP_OK;
+}
 int sp_deferred_status(int32_t* flag) {
   int f = 0;
   const int st = deferred_status(&f);
