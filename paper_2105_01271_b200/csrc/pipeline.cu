@@ -441,18 +441,24 @@ static int svd_top(const double* X, int64_t rows, int64_t cols, int64_t ldx, int
       // leading-triplet rate test can first pass; in bulk mode (accepted
       // itn - bulk_from >= 3 steps after the flat stretch was found) the two
       // steps in between.
+      // After ANY unconverged Rayleigh-Ritz step (its rho is the current, better
+      // estimate): blind steps up to two before the predicted passing step, at
+      // most kBlindMax in a row -- a slowly contracting block still sees a
+      // Rayleigh-Ritz step (stagnation test, block growth) every kBlindMax + 1.
+      constexpr int kBlindMax = 6;
       int blind = 0;
-      if (!no_blind && need < 0 && itn == 0 && kept > 0 && b - 8 > kept) {
+      if (!no_blind && need < 0 && kept > 0 && b - 8 > kept) {
         const double rho = hs[b - 8] / hs[kept - 1];
         if (rho > 0.0 && rho < 1.0)
-          blind = (int)std::ceil((std::log(1e-12) / std::log(rho) - 2.0) / 2.0) - 2;
+          blind = (int)std::ceil((std::log(1e-12) / std::log(rho) - 2.0) / 2.0) - 2 - itn;
       } else if (!no_blind && need >= 0 && out.bulk && itn == bulk_from) {
         blind = 2;
-      } else if (!no_blind && need >= 0 && !out.bulk && itn == 0 && std::min(kept, need) > 0) {
+      } else if (!no_blind && need >= 0 && !out.bulk && std::min(kept, need) > 0) {
         const double rho = hs[b - 8] / hs[std::min(kept, need) - 1];
         if (rho > 0.0 && rho < 1.0)
-          blind = std::max(1, (int)std::ceil((std::log(1e-12) / std::log(rho) - 2.0) / 2.0)) - 2;
+          blind = std::max(1, (int)std::ceil((std::log(1e-12) / std::log(rho) - 2.0) / 2.0)) - 2 - itn;
       }
+      blind = std::min(blind, kBlindMax);
       blind = std::min(blind, max_it - 3 - itn);
       for (int j = 0; j < blind; ++j) {
         SPB_TRY(gemm(1, 0, cols, b, rows, 1.0, X, ldx, Q, b, 0.0, Z, b, s));

@@ -285,3 +285,33 @@ def test_nonfinite_outside_sketch_is_reported_after_the_fused_finish(cuda):
 def _lib_status():
     from paper_2105_01271_b200 import _lib
     return _lib.deferred_status()
+
+
+@pytest.mark.parametrize("ratio,noise", [(0.75, 0.0), (0.6, 3e-7), (0.9, 0.0)])
+def test_slowly_decaying_sketch_spectrum_vs_target(cuda, ratio, noise):
+    """The range finder on spectra that contract slowly (several batches of
+    blind subspace steps between Rayleigh-Ritz steps, block growth past 32
+    columns): kept rank and sigma against the dense target of the same
+    projector (src/power.py:124-181), principal angles of the kept U."""
+    rng = philox(int(ratio * 100))
+    m, n, stride, k = 700, 4096, 4, 12
+    r0 = 60
+    u, _ = np.linalg.qr(rng.standard_normal((m, r0)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, r0)))
+    a = (u * ratio ** np.arange(r0)) @ v.T
+    if noise:
+        a = a + noise * rng.standard_normal((m, n))
+    cols = np.arange(0, n, stride)
+    op = sp.build_sketch(sp.SketchSpec("injection", n, cols.size))
+    np.testing.assert_array_equal(op.idx.ravel(), cols)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        res = sp.power_svd(sp.ArraySnapshotStream(a), op, k, sp.PowerConfig(q=1, columns=cols))
+    tu, ts, tv, r = oracle.projector_target_svd(a, a[:, cols], k, 3)
+    assert res.kept_rank == r
+    kk = min(k, r)
+    np.testing.assert_allclose(res.s[:kk], ts[:kk], rtol=0, atol=1e-12 * ts[0])
+    _contracts(res, k)
+    lead = int(np.sum(ts[:kk] > 1e-6 * ts[0]))
+    assert oracle.principal_angle(res.u[:, :lead], tu[:, :lead]) <= 1e-8
+    assert oracle.principal_angle(res.v[:, :lead], tv[:, :lead]) <= 1e-8
