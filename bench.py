@@ -477,9 +477,22 @@ def run_ours(args):
     gc.disable()
     # W warm-up steps, continued until ~0.3 s of work has run (clocks and
     # allocator pools at steady state when the timed loop starts)
+    # (N > 1: every rank must run the SAME number of steps -- the steps hold
+    # collectives -- so the extra count is agreed on with an allreduce-max, never
+    # decided from a rank's own clock)
     t_w = time.perf_counter()
     done = 0
-    while done < args.warmup or time.perf_counter() - t_w < 0.3:
+    for _ in range(max(1, args.warmup)):
+        res = step()
+        done += 1
+    torch.cuda.synchronize()
+    per_step = (time.perf_counter() - t_w) / done
+    extra = int(min(2000, max(0, np.ceil((0.3 - per_step * done) / max(per_step, 1e-6)))))
+    if world > 1:
+        t = torch.tensor([extra], dtype=torch.int64, device=dev if not DRYRUN else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        extra = int(t.item())
+    for i in range(extra):
         res = step()
         done += 1
         if done % 8 == 0:
@@ -694,6 +707,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extra", action="store_true")
     args = ap.parse_args()
+    if os.environ.get("SPB_BENCH_WATCHDOG"):   # diagnostics: dump every thread's stack and exit after N seconds
+        import faulthandler
+        faulthandler.dump_traceback_later(int(os.environ["SPB_BENCH_WATCHDOG"]), exit=True)
     if args.impl == "reference":
         run_reference(args)
     else:

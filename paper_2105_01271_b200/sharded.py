@@ -157,7 +157,9 @@ def distributed_sketch_basis(c_i, row0: int, ncols: int, power: float, comm, ops
         y = comm.allreduce_sum(ops.matmul(c_i, om), ops)
         qy, _ = ops.tsqr(y)
         prev, kept_prev, grow = None, -1, False
-        for itn in range(24):
+        itn = -1
+        while itn < 23:
+            itn += 1
             z = ops.matmul_tn(c_i, qy)                                  # n_c_i x b
             zp = ops.pad_rows(z, b)                                     # TSQR needs rows >= b
             pz, rz = ops.tsqr(zp)
@@ -211,6 +213,22 @@ def distributed_sketch_basis(c_i, row0: int, ncols: int, power: float, comm, ops
             p_i = ops.matmul(z, us)
             y = comm.allreduce_sum(ops.matmul(c_i, p_i), ops)
             qy, _ = ops.tsqr(y)
+            # blind steps (svd_top's rule): up to two before the step at which
+            # the rate test can first pass, at most six in a row -- one allreduce
+            # of m x b each, no R-factor all-gather, Jacobi core or host decision.
+            # hs is replicated, so every rank takes the same number.
+            tt = kept if need < 0 else min(kept, need)
+            blind = 0
+            if tt > 0 and (need >= 0 or b - 8 > kept):
+                rho = hs[b - 8] / hs[tt - 1]
+                if 0.0 < rho < 1.0:
+                    pass_at = int(np.ceil((np.log(1e-12) / np.log(rho) - 2.0) / 2.0))
+                    blind = min(max(pass_at, 1) - 2 - itn, 6, 21 - itn)
+            for _ in range(max(blind, 0)):
+                zb = ops.matmul_tn(c_i, qy)
+                y = comm.allreduce_sum(ops.matmul(c_i, zb), ops)
+                qy, _ = ops.tsqr(y)
+                itn += 1
         if grow:
             b = min(cap, 2 * b)
             continue

@@ -109,6 +109,46 @@ def test_two_shards_match_target(cuda):
     np.testing.assert_allclose((u * s) @ v.T, (tu * ts) @ tv.T, atol=1e-10 * np.abs(a).max())
 
 
+def test_two_shards_noisy_field_blind_steps(cuda):
+    """A noise bulk right below the kept-rank cut (the cfg3 regime): several
+    subspace steps, Rayleigh-Ritz steps with blind steps in between -- the same
+    sequence of exchanges on both shards, U bitwise identical, result against
+    the dense target."""
+    from paper_2105_01271_b200.datagen import FieldConfig
+    cfg = FieldConfig("shard_noisy", 600, (64, 64), 20, 0.5, 0.001, 2, 4, 30, 1, noise_std=1e-4)
+    a = generate_host(cfg)
+    op, cols = sp.grid_injection(cfg.grid, cfg.stride)
+    world = 2
+    shared = {"slots": [None] * world, "bar": threading.Barrier(world, timeout=120)}
+    results = [None] * world
+    errors = []
+
+    def run(rank):
+        try:
+            cuda.cuda.set_device(0)
+            b, e = shard_columns(cfg.n, world, rank, align=cfg.grid[1])
+            ad = cuda.from_numpy(a[:, b:e].copy()).cuda()
+            results[rank] = (b,) + sharded_power_svd(ad, b, cols, 30, 1, ThreadComm(rank, world, shared), DeviceOps())
+        except Exception as exc:  # surface in the main thread
+            errors.append(exc)
+            shared["bar"].abort()
+
+    th = [threading.Thread(target=run, args=(rk,), daemon=True) for rk in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errors, errors
+    assert all(r is not None for r in results)
+    u = results[0][1].cpu().numpy()
+    s, r = results[0][2], results[0][4]
+    assert np.array_equal(results[1][1].cpu().numpy(), u)
+    tu, ts, tv, tr = oracle.projector_target_svd(a, a[:, cols], 30, 3)
+    assert r == tr
+    np.testing.assert_allclose(s[:r], ts, rtol=0, atol=1e-12 * ts[0])
+    assert oracle.principal_angle(u[:, :r], tu) <= 1e-8
+
+
 def _id_case():
     """20 gap-determined ID pivots (a slow-decay block, tests/golden/id_slow.npz
     construction): the per-rank partial sums may not move the selection."""

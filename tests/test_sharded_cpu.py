@@ -288,17 +288,23 @@ class NumpyOps:
     def scale_cols(self, x, d):
         return self._t(x.numpy() * d[None, :])
 
-def _field():
-    from paper_2105_01271_b200.datagen import CONFIGS, coarse_grid_indices, generate_host
-    cfg = CONFIGS["cfg2"].scaled(m=300, grid=(48, 64), name="shard")
+def _field(noisy=False):
+    from paper_2105_01271_b200.datagen import CONFIGS, FieldConfig, coarse_grid_indices, generate_host
+    if noisy:
+        # a noise floor just below the kept-rank cut (the cfg3 regime): the range
+        # finder needs several subspace steps -- Rayleigh-Ritz steps with blind
+        # steps in between, the same number on every rank
+        cfg = FieldConfig("shard_noisy", 300, (48, 64), 20, 0.5, 0.001, 2, 4, 30, 1, noise_std=1e-4)
+    else:
+        cfg = CONFIGS["cfg2"].scaled(m=300, grid=(48, 64), name="shard")
     return cfg, generate_host(cfg), coarse_grid_indices(cfg.grid, cfg.stride)
 
 
-def _worker(rank, world, port, out_q):
+def _worker(rank, world, port, out_q, noisy=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2105_01271_b200.sharded import TorchComm, shard_columns, sharded_power_svd
-    cfg, a, cols = _field()
+    cfg, a, cols = _field(noisy)
     b, e = shard_columns(cfg.n, world, rank, align=cfg.grid[1])  # x-slabs of the grid
     ops = NumpyOps()
     u, s, v, r, warn = sharded_power_svd(torch.from_numpy(a[:, b:e].copy()), b, cols, 30, 1, TorchComm(), ops)
@@ -338,6 +344,29 @@ def test_sharded_matches_target(world):
     np.testing.assert_allclose(v.T @ v, np.eye(30), atol=1e-12)
     rec = (u * s) @ v.T
     np.testing.assert_allclose(rec, (tu * ts) @ tv.T, atol=1e-10 * np.abs(a).max())
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_sharded_noisy_field_blind_steps(world):
+    """Several subspace steps (a noise bulk right below the kept-rank cut):
+    blind steps between the Rayleigh-Ritz steps, identical on every rank (no
+    collective mismatch), result against the dense target."""
+    import oracle
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(rk, world, port, q, True)) for rk in range(world)]
+    for p in procs:
+        p.start()
+    u, s, v, r, warn = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cfg, a, cols = _field(True)
+    tu, ts, tv, tr = oracle.projector_target_svd(a, a[:, cols], 30, 3)
+    assert r == tr
+    np.testing.assert_allclose(s[:r], ts, rtol=0, atol=1e-12 * ts[0])
+    assert oracle.principal_angle(u[:, :r], tu) <= 1e-8
 
 
 def _id_field():
