@@ -160,8 +160,14 @@ int col_exponents(int64_t rows, int64_t cols, const double* X, int64_t ldx, int*
 // different ranks on the same grids -- allreduce-max of the exponents first --
 // add up exactly when the total depth satisfies the plan), Lv[1] = the FP64 rest.
 int gemm_exact_levels(int ta, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const int* ea,
-                      const double* B, int64_t ldb, const int* eb, int bits, int nsl, double* Lv, cudaStream_t s) {
+                      const double* B, int64_t ldb, const int* eb, int bits, int nsl, double* Lv, cudaStream_t s,
+                      bool symmetric) {
   SPB_REQUIRE(M >= 1 && N >= 1 && K >= 1 && nsl == 2, "gemm_exact_levels: bad extents");
+  // symmetric: op(A) = B^T (the Gram T = C^T C): both operands get the same
+  // slices (same vectors, same anchors), so the exact head level is exactly
+  // symmetric and the rest level symmetric up to its own rounding -- only the
+  // tiles on and above the diagonal are computed and mirrored
+  symmetric = symmetric && ta == 1 && M == N;
   Arena ar(s);
   // A: [S0 | S1] along K
   const int64_t ka = 2 * K;
@@ -185,6 +191,11 @@ int gemm_exact_levels(int ta, int64_t M, int64_t N, int64_t K, const double* A, 
   if (ta == 0) {
     SPB_TRY(gemm(0, 0, M, N, K, 1.0, As, ka, Bs, N, 0.0, L0, N, s));
     SPB_TRY(gemm(0, 0, M, N, 2 * K, 1.0, As, ka, Bs + K * N, N, 0.0, L1, N, s));
+  } else if (symmetric) {
+    SPB_TRY(gemm_upper(1, 0, M, N, K, 1.0, As, M, Bs, N, 0.0, L0, N, s));
+    SPB_TRY(gemm_upper(1, 0, M, N, 2 * K, 1.0, As, M, Bs + K * N, N, 0.0, L1, N, s));
+    SPB_TRY(mirror_upper(M, L0, N, s));
+    SPB_TRY(mirror_upper(M, L1, N, s));
   } else {
     SPB_TRY(gemm(1, 0, M, N, K, 1.0, As, M, Bs, N, 0.0, L0, N, s));
     SPB_TRY(gemm(1, 0, M, N, 2 * K, 1.0, As, M, Bs + K * N, N, 0.0, L1, N, s));
@@ -206,8 +217,10 @@ int dd_levels(int64_t M, int64_t N, const double* Lv, int nsl, const double* tai
 // op(A) = A (ta = 0, M x K, lda) or A^T (ta = 1, A is K x M).  B is K x N (ldb),
 // B_lo (same layout, may be null) the low part of a double-double B.
 int gemm_exact(int ta, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B_hi,
-               const double* B_lo, int64_t ldb, double* C_hi, double* C_lo, int64_t ldc, cudaStream_t s) {
+               const double* B_lo, int64_t ldb, double* C_hi, double* C_lo, int64_t ldc, cudaStream_t s,
+               bool symmetric) {
   SPB_REQUIRE(M >= 1 && N >= 1 && K >= 1, "gemm_exact needs non-empty operands");
+  symmetric = symmetric && ta == 1 && M == N && B_lo == nullptr;
   int bits = 0, nsl = 0;
   ozaki_plan(K, &bits, &nsl);
   Arena ar(s);
@@ -219,7 +232,7 @@ int gemm_exact(int ta, int64_t M, int64_t N, int64_t K, const double* A, int64_t
     SPB_TRY(col_exponents(K, M, A, lda, ea, s));
   SPB_TRY(col_exponents(K, N, B_hi, ldb, eb, s));
   SPB_ALLOC(ar, double, Lv, (size_t)nsl * M * N);
-  SPB_TRY(gemm_exact_levels(ta, M, N, K, A, lda, ea, B_hi, ldb, eb, bits, nsl, Lv, s));
+  SPB_TRY(gemm_exact_levels(ta, M, N, K, A, lda, ea, B_hi, ldb, eb, bits, nsl, Lv, s, symmetric));
   double* tail = nullptr;
   if (B_lo) {
     tail = ar.alloc<double>((size_t)M * N);

@@ -342,15 +342,24 @@ __global__ void mirror_upper_kernel(int64_t n, double* __restrict__ W, int64_t l
 // computed (half the DMMA work of the plain product: cfg5's W = C C^T, 2.1
 // TFLOP, 70 -> 37 ms), the lower triangle is their mirror image -- W comes out
 // exactly symmetric.
-int gemm_aat(int64_t M, int64_t K, const double* A, int64_t lda, double* W, int64_t ldw, cudaStream_t s) {
-  SPB_TRY(gemm_impl(0, 1, M, M, K, 1.0, A, lda, A, lda, 0.0, W, ldw, s, true));
-  if (M > 1) {
-    const unsigned nb = (unsigned)ceil_div(M, 32);
-    mirror_upper_kernel<<<dim3(nb, nb), dim3(32, 8), 0, s>>>(M, W, ldw);
+int gemm_upper(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+               const double* B, int64_t ldb, double beta, double* C, int64_t ldc, cudaStream_t s) {
+  return gemm_impl(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, s, true);
+}
+
+int mirror_upper(int64_t n, double* W, int64_t ldw, cudaStream_t s) {
+  if (n > 1) {
+    const unsigned nb = (unsigned)ceil_div(n, 32);
+    mirror_upper_kernel<<<dim3(nb, nb), dim3(32, 8), 0, s>>>(n, W, ldw);
     count_launch();
     SPB_CHECK_LAUNCH();
   }
   return SP_OK;
+}
+
+int gemm_aat(int64_t M, int64_t K, const double* A, int64_t lda, double* W, int64_t ldw, cudaStream_t s) {
+  SPB_TRY(gemm_impl(0, 1, M, M, K, 1.0, A, lda, A, lda, 0.0, W, ldw, s, true));
+  return mirror_upper(M, W, ldw, s);
 }
 
 static int gemm_impl(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,

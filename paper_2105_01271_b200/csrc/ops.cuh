@@ -33,6 +33,11 @@ struct TsqrPlan {
   double* Mg = nullptr;  // single-chunk root: M = T V_top^T diag(sgn)
   int cols = 0;
 };
+// gemm() computing only the tiles on and above the diagonal of a square C (the
+// caller mirrors: mirror_upper), for products known to be symmetric
+int gemm_upper(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+               const double* B, int64_t ldb, double beta, double* C, int64_t ldc, cudaStream_t s);
+int mirror_upper(int64_t n, double* W, int64_t ldw, cudaStream_t s);
 // W = A A^T (M x M) from the tiles on and above the diagonal, mirrored
 int gemm_aat(int64_t M, int64_t K, const double* A, int64_t lda, double* W, int64_t ldw, cudaStream_t s);
 int tsqr_factor(int64_t rows, int cols, const double* X, int64_t ldx, double* R, int64_t ldr, TsqrPlan& plan,
@@ -44,12 +49,14 @@ int gram_chol_dd(int64_t rows, int b, const double* X, int64_t ldx, double* R, i
                  cudaStream_t s, int nslab = 1, int64_t slab_stride = 0);
 // op(A) (B_hi + B_lo) nearly exactly rounded (Ozaki slices on DMMA): C_hi (+ C_lo)
 int gemm_exact(int ta, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B_hi,
-               const double* B_lo, int64_t ldb, double* C_hi, double* C_lo, int64_t ldc, cudaStream_t s);
+               const double* B_lo, int64_t ldb, double* C_hi, double* C_lo, int64_t ldc, cudaStream_t s,
+               bool symmetric = false);
 void ozaki_plan(int64_t K, int* bits, int* nsl);
 int row_exponents(int64_t rows, int64_t cols, const double* X, int64_t ldx, int* e, cudaStream_t s);
 int col_exponents(int64_t rows, int64_t cols, const double* X, int64_t ldx, int* e, cudaStream_t s);
 int gemm_exact_levels(int ta, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const int* ea,
-                      const double* B, int64_t ldb, const int* eb, int bits, int nsl, double* Lv, cudaStream_t s);
+                      const double* B, int64_t ldb, const int* eb, int bits, int nsl, double* Lv, cudaStream_t s,
+                      bool symmetric = false);
 int dd_levels(int64_t M, int64_t N, const double* Lv, int nsl, const double* tail, double* hi, double* lo,
               int64_t ldc, cudaStream_t s);
 // sharded pivoted QR steps (pivqr_dist.cu) and the ID coefficients from a QR

@@ -1073,13 +1073,19 @@ int power_id(const void* A, int a_dtype, int64_t m, int64_t n, int64_t lda, cons
       set_error("enriched sketch allocation failed");
       return SP_ECUDA;
     }
+    bool sym_t = false;
+    if (ref_order && !plain && !proj && ncols == nc && getenv("SPB_ID_FULL_T") == nullptr)
+      SPB_TRY(sketch_is_columns(idx, w, depth, nc, nullptr, cols, ncols, sym_t, s));
     if (!ref_order) SPB_TRY(gemm_aat(m, ncols, C, ncols, W, m, s));  // W = C C^T, upper tiles + mirror
     for (int it = 0; it < q; ++it) {
       if (ref_order && plain) {
         SPB_TRY(gemm(1, 0, ncols, nc, m, 1.0, C, ncols, E, nc, 0.0, T, nc, s));
         SPB_TRY(gemm(0, 0, m, nc, ncols, 1.0, C, ncols, T, nc, 0.0, E2, nc, s));
       } else if (ref_order) {
-        SPB_TRY(gemm_exact(1, ncols, nc, m, C, ncols, E, it == 0 ? nullptr : E_lo, nc, T, T_lo, nc, s));
+        // first step with the sketch on the same column set: E = s0 = C bit for
+        // bit, T = C^T C is symmetric (upper tiles + mirror; SPB_ID_FULL_T=1: all tiles)
+        SPB_TRY(gemm_exact(1, ncols, nc, m, C, ncols, E, it == 0 ? nullptr : E_lo, nc, T, T_lo, nc, s,
+                           it == 0 && sym_t));
         SPB_TRY(gemm_exact(0, m, nc, ncols, C, ncols, T, T_lo, nc, E2, E2_lo, nc, s));
         std::swap(E_lo, E2_lo);
       } else {
