@@ -189,6 +189,54 @@ __global__ void pq_update_kernel(int t, int64_t cols, int64_t rows, double* __re
   }
 }
 
+// Candidates of 1025 .. 4096 entries (cfg3: 5000 candidates of length 4096):
+// one 128-thread CTA per candidate holds it in registers (PER values per
+// thread), so the candidate is read once and written once -- the warp-per-
+// candidate kernel above reads it a second time for the update, from L2 at
+// best (164 MB of candidates against a 126 MB L2).  Same quantities, fixed
+// summation order (thread-strided partials, warp shuffles, warps in order).
+constexpr int kPqRegThreads = 128;
+
+template <int PER>
+__global__ void __launch_bounds__(kPqRegThreads)
+pq_update_reg_kernel(int t, int64_t cols, int64_t rows, double* __restrict__ WK, double* __restrict__ norms,
+                     const double* __restrict__ Qt, double* __restrict__ R, int64_t ldr) {
+  __shared__ double red[2][kPqRegThreads / 32];
+  const int64_t j = t + 1 + (int64_t)blockIdx.x;
+  if (j >= cols) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* v = Qt + (int64_t)t * rows;
+  double* w = WK + j * rows;
+  double x[PER], vv[PER];
+  double c = 0.0;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int64_t e = tid + (int64_t)i * kPqRegThreads;
+    x[i] = e < rows ? w[e] : 0.0;
+    vv[i] = e < rows ? v[e] : 0.0;
+    c = fma(vv[i], x[i], c);
+  }
+  c = warp_sum(c);
+  if (lane == 0) red[0][warp] = c;
+  __syncthreads();
+  c = (red[0][0] + red[0][1]) + (red[0][2] + red[0][3]);
+  double a = 0.0;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int64_t e = tid + (int64_t)i * kPqRegThreads;
+    const double nv = fma(-c, vv[i], x[i]);
+    if (e < rows) w[e] = nv;
+    a = fma(nv, nv, a);
+  }
+  a = warp_sum(a);
+  if (lane == 0) red[1][warp] = a;
+  __syncthreads();
+  if (tid == 0) {
+    R[(int64_t)t * ldr + j] = c;
+    norms[j] = sqrt((red[1][0] + red[1][1]) + (red[1][2] + red[1][3]));
+  }
+}
+
 // ------------------------------------------------------ long candidates ----
 // Candidates much longer than their count (the ID of cfg5: 2000 candidates of
 // length 262144): every step's work is spread over row blocks x column
@@ -483,7 +531,13 @@ int pivoted_qr(int64_t rows, int64_t cols, const double* Mt, int64_t ldmt, int k
     count_launch();
     SPB_CHECK_LAUNCH();
     if (t + 1 < cols) {
-      pq_update_kernel<<<ceil_div((cols - t - 1) * 32, 256), 256, 0, s>>>(t, cols, rows, WK, norms, Qt, R, ldr);
+      const unsigned nc = (unsigned)(cols - t - 1);
+      if (rows > 2048 && rows <= 4096)
+        pq_update_reg_kernel<32><<<nc, kPqRegThreads, 0, s>>>(t, cols, rows, WK, norms, Qt, R, ldr);
+      else if (rows > 1024 && rows <= 2048)
+        pq_update_reg_kernel<16><<<nc, kPqRegThreads, 0, s>>>(t, cols, rows, WK, norms, Qt, R, ldr);
+      else
+        pq_update_kernel<<<ceil_div((cols - t - 1) * 32, 256), 256, 0, s>>>(t, cols, rows, WK, norms, Qt, R, ldr);
       count_launch();
       SPB_CHECK_LAUNCH();
     }
