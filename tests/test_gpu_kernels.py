@@ -295,7 +295,9 @@ def test_pivoted_qr_duplicate_columns_tie_break(cuda):
                                         (40000, 300, 60), (70000, 64, 64),
                                         # register-resident update: 1025 .. 4096 rows, ragged and full
                                         (1025, 700, 50), (2048, 500, 64), (3000, 900, 80), (4096, 1200, 100),
-                                        (4097, 300, 40)])
+                                        (4097, 300, 40),
+                                        # very long candidates (the row-block path), ragged
+                                        (140000, 40, 20), (262144, 24, 24), (200001, 33, 10)])
 def test_pivoted_qr_matches_oracle_pivots(cuda, rows, cols, k):
     m = philox(rows * cols).standard_normal((rows, cols)) * np.logspace(0, -2, cols)
     f = sp.pivoted_qr(m, k)
