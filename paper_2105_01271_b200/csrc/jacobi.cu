@@ -706,7 +706,12 @@ jacobi_blk_kernel(int n, const double* __restrict__ M, int64_t ldm, bool trans, 
       grid.sync();
     }
     // quadratic convergence: a sweep without a rotation above kJacQuad is the last
-    if (*(volatile int*)rt == 0) break;
+    if (*(volatile int*)rt == 0) {
+#ifdef SPB_JACOBI_TRACE
+      if (gtid == 0) printf("jacobi_blk n=%d np=%d sweeps=%d\n", n, np, sweep + 1);
+#endif
+      break;
+    }
   }
   // singular values = column norms, sorted descending (stable by index)
   for (int c = gwarp; c < np; c += nwarps) {
