@@ -131,3 +131,25 @@ def test_result_buffers_are_leased_not_shared(cuda):
     assert d.ctypes.data == addr
     np.testing.assert_array_equal(d[0, :3], [3.0, 4.0, 5.0])
     np.testing.assert_array_equal(c[0, :3], [1.0, 2.0, 3.0])
+
+
+def test_release_workspaces_between_calls(cuda):
+    """sp_release_workspaces hands the cached workspaces back to the driver; the
+    next call re-allocates and gives the same bits."""
+    from paper_2105_01271_b200 import _lib
+    from paper_2105_01271_b200.datagen import CONFIGS, generate_host
+    cfg = CONFIGS["cfg2"].scaled(m=300, grid=(64, 64), name="rel")
+    a = generate_host(cfg)
+    op, cols = sp.grid_injection(cfg.grid, cfg.stride)
+    pc = sp.PowerConfig(q=1, columns=cols)
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        r1 = sp.power_svd(sp.ArraySnapshotStream(a), op, 20, pc)
+        free0 = cuda.cuda.mem_get_info()[0]
+        _lib.release_workspaces()
+        free1 = cuda.cuda.mem_get_info()[0]
+        r2 = sp.power_svd(sp.ArraySnapshotStream(a), op, 20, pc)
+    assert free1 >= free0
+    np.testing.assert_array_equal(r1.s, r2.s)
+    np.testing.assert_array_equal(r1.u, r2.u)
