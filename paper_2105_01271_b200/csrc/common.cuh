@@ -25,6 +25,7 @@ struct Status {
   do {                                                                        \
     cudaError_t _e = (call);                                                  \
     if (_e != cudaSuccess) {                                                  \
+      cudaGetLastError(); /* clear it: a failed call must not poison the next */ \
       ::spb::set_error(std::string(#call) + ": " + cudaGetErrorString(_e));    \
       return SP_ECUDA;                                                        \
     }                                                                         \

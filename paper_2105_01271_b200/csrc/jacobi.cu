@@ -25,7 +25,21 @@ namespace spb {
 
 constexpr int kJacMaxSweeps = 40;
 constexpr double kJacTol = 1e-15;
-constexpr double kJacQuad = 1e-8;  // jacobi32: a sweep with only smaller rotations is the last
+constexpr double kJacQuad = 1e-8;
+// Stopping rule.  A sweep whose rotated couplings g / sqrt(a b) were all below kJacQuad leaves
+// only ~kJacQuad^2-sized ones behind when the singular values are separated (cyclic Jacobi
+// converges quadratically), so it is the last -- UNLESS the sweep contained a large-angle
+// rotation: inside a cluster of (nearly) equal singular values the angle is not small however
+// small the coupling, the two columns' couplings to everything else are mixed, not squared, and
+// what the sweep leaves behind is as large as what it started from (flat stretches of the
+// spectrum were left with 1-4e-9 of non-orthogonality in U; found by scripts/fuzz_api.py).  Such
+// a sweep is the last only once all its couplings were below kJacFloor.  Per-sweep flag bits:
+constexpr double kJacFloor = 1e-11;
+constexpr double kJacSin2 = 1e-8;  // sin^2(2 theta) above which a rotation counts as large-angle
+constexpr int kJfAny = 1, kJfQuad = 2, kJfFloor = 4, kJfWide = 8;
+__host__ __device__ __forceinline__ bool jac_continue(int flags) {
+  return (flags & kJfQuad) || ((flags & kJfFloor) && (flags & kJfWide));
+}
 
 __device__ __forceinline__ void rr_pair(int np, int round, int k, int& p, int& q) {
   const int N1 = np - 1;
@@ -152,7 +166,7 @@ jacobi_kernel(int n, int np, const double* __restrict__ M, int64_t ldm, double* 
     // quadratic convergence: a sweep whose rotations were all below kJacQuad
     // in relative size leaves only ~kJacQuad^2-sized ones for the next, which
     // would only confirm convergence (the jacobi32 rule)
-    if (rot_count == 0 || __longlong_as_double((long long)relmax_bits) < kJacQuad) break;
+    if (rot_count == 0 || __longlong_as_double((long long)relmax_bits) < kJacFloor) break;  // (no quadratic shortcut here)
     __syncthreads();
   }
   // singular values = column norms, sorted descending (stable by index)
@@ -332,6 +346,7 @@ jacobi32_kernel(int n, const double* __restrict__ M, int64_t ldm, double* __rest
       const double d = aq - ap, h = 2.0 * g;
       const double ad = fabs(d), ah = fabs(h);
       double cs, sn;
+      bool wide;  // large-angle rotation (a cluster of equal singular values)
       if (ad < 1e140 && ah < 1e140 && (ad > 1e-140 || ah > 1e-140)) {
         // fast path, two dependent MUFU rsqrt (+ Newton) stages: rh =
         // 1 / hypot(d, h) gives cos 2theta = |d| rh and sin 2theta = h rh
@@ -343,10 +358,12 @@ jacobi32_kernel(int n, const double* __restrict__ M, int64_t ldm, double* __rest
         const double w = fast_rsqrt(u);
         cs = u * w;
         sn = (copysign(0.5, d) * h) * (rh * w);
+        wide = h * h > kJacSin2 * s2;
       } else {
         const double t = copysign(1.0, d) * h / (ad + hypot(d, h));
         cs = rsqrt(fma(t, t, 1.0));
         sn = cs * t;
+        wide = fabs(t) > 5e-5;
       }
       // p' = cs p - sn q ; q' = sn p + cs q
       const double so = low ? -sn : sn;
@@ -357,7 +374,9 @@ jacobi32_kernel(int n, const double* __restrict__ M, int64_t ldm, double* __rest
         for (int k = 0; k < RPW; ++k) v[k] = fma(so, z[k], cs * v[k]);
       }
       // a rotation of relative size above kJacQuad keeps the sweeps going
-      if (big ? fabs(g) > kJacQuad * sqrt(ap) * sqrt(aq) : g * g > (kJacQuad * kJacQuad) * apq) rotated = 1;
+      if (big ? fabs(g) > kJacQuad * sqrt(ap) * sqrt(aq) : g * g > (kJacQuad * kJacQuad) * apq) rotated |= kJfQuad;
+      if (big ? fabs(g) > kJacFloor * sqrt(ap) * sqrt(aq) : g * g > (kJacFloor * kJacFloor) * apq) rotated |= kJfFloor;
+      if (wide) rotated |= kJfWide;
     }
     // Stop after a sweep whose rotations were all below kJacQuad in relative
     // size: cyclic Jacobi converges quadratically, so what the next sweep
@@ -365,7 +384,11 @@ jacobi32_kernel(int n, const double* __restrict__ M, int64_t ldm, double* __rest
     // ||w_p|| ||w_q|| (the kJacTol level: column changes ~1e-15, singular
     // values unchanged to second order) -- it is not run (5 -> 4 sweeps on
     // the cfg2 core).
-    if (!__syncthreads_or(rotated)) {
+    // (__syncthreads_or returns a truth value, not the OR of the bits: one vote per flag)
+    const int fq = __syncthreads_or(rotated & kJfQuad) ? kJfQuad : 0;
+    const int ff = __syncthreads_or(rotated & kJfFloor) ? kJfFloor : 0;
+    const int fw = __syncthreads_or(rotated & kJfWide) ? kJfWide : 0;
+    if (!jac_continue(fq | ff | fw)) {
 #ifdef SPB_JACOBI_TRACE
       if (threadIdx.x == 0) printf("jacobi32 n=%d na=%d sweeps=%d\n", n, na, sweep + 1);
 #endif
@@ -489,6 +512,7 @@ jacobi_grid_kernel(int n, int np, const double* __restrict__ M, int64_t ldm, boo
           const double d = b - a, h = 2.0 * g;
           const double ad = fabs(d), ah = fabs(h);
           double cs, sn;
+          bool wide;  // large-angle rotation (see kJacFloor)
           if (ad < 1e140 && ah < 1e140 && (ad > 1e-140 || ah > 1e-140)) {
             const double s2 = fma(d, d, h * h);
             const double rh = fast_rsqrt(s2);
@@ -496,10 +520,12 @@ jacobi_grid_kernel(int n, int np, const double* __restrict__ M, int64_t ldm, boo
             const double w = fast_rsqrt(u);
             cs = u * w;
             sn = (copysign(0.5, d) * h) * (rh * w);
+            wide = h * h > kJacSin2 * s2;
           } else {
             const double t = copysign(1.0, d) * h / (ad + hypot(d, h));
             cs = rsqrt(fma(t, t, 1.0));
             sn = cs * t;
+            wide = fabs(t) > 5e-5;
           }
           double* vp = Vm + (int64_t)p * np;
           double* vq = Vm + (int64_t)q * np;
@@ -512,10 +538,10 @@ jacobi_grid_kernel(int n, int np, const double* __restrict__ M, int64_t ldm, boo
             vq[i] = fma(sn, u, cs * w);
           }
           if (lane == 0) {
-            atomicOr(&rot[sweep & 1], 1);
-            // relmax holds 1.0 once a rotation above kJacQuad in relative size was made
-            if (big ? fabs(g) > kJacQuad * sqrt(a) * sqrt(b) : g * g > (kJacQuad * kJacQuad) * ab)
-              atomicMax(&relmax[sweep & 1], (unsigned long long)__double_as_longlong(1.0));
+            int fl = kJfAny | (wide ? kJfWide : 0);
+            if (big ? fabs(g) > kJacQuad * sqrt(a) * sqrt(b) : g * g > (kJacQuad * kJacQuad) * ab) fl |= kJfQuad;
+            if (big ? fabs(g) > kJacFloor * sqrt(a) * sqrt(b) : g * g > (kJacFloor * kJacFloor) * ab) fl |= kJfFloor;
+            atomicOr(&rot[sweep & 1], fl);
           }
         }
       }
@@ -523,9 +549,7 @@ jacobi_grid_kernel(int n, int np, const double* __restrict__ M, int64_t ldm, boo
     }
     // same values in every thread after the barrier; the quadratic-convergence
     // stop of the single-CTA kernels
-    if (*(volatile int*)&rot[sweep & 1] == 0 ||
-        __longlong_as_double((long long)*(volatile unsigned long long*)&relmax[sweep & 1]) < kJacQuad)
-      break;
+    if (!jac_continue(*(volatile int*)&rot[sweep & 1])) break;
   }
   // singular values = column norms, sorted descending (stable by index)
   for (int c = gwarp; c < np; c += nwarps) {
@@ -602,6 +626,7 @@ __device__ __forceinline__ void jb_rotate(double* __restrict__ cp, double* __res
   const double d = b - a, h = 2.0 * g;
   const double ad = fabs(d), ah = fabs(h);
   double cs, sn;
+  bool wide;  // large-angle rotation (see kJacFloor)
   if (ad < 1e140 && ah < 1e140 && (ad > 1e-140 || ah > 1e-140)) {
     const double s2 = fma(d, d, h * h);
     const double rh = fast_rsqrt(s2);
@@ -609,10 +634,12 @@ __device__ __forceinline__ void jb_rotate(double* __restrict__ cp, double* __res
     const double w = fast_rsqrt(u);
     cs = u * w;
     sn = (copysign(0.5, d) * h) * (rh * w);
+    wide = h * h > kJacSin2 * s2;
   } else {
     const double t = copysign(1.0, d) * h / (ad + hypot(d, h));
     cs = rsqrt(fma(t, t, 1.0));
     sn = cs * t;
+    wide = fabs(t) > 5e-5;
   }
 #pragma unroll
   for (int j = RPL; j < 2 * RPL; ++j) {  // the V half
@@ -625,8 +652,12 @@ __device__ __forceinline__ void jb_rotate(double* __restrict__ cp, double* __res
     cq[lane + 32 * j] = fma(sn, x[j], cs * y[j]);
   }
   // a rotation of relative size above kJacQuad keeps the sweeps going
-  if (lane == 0 && (big ? fabs(g) > kJacQuad * sqrt(a) * sqrt(b) : g * g > (kJacQuad * kJacQuad) * ab))
-    *(volatile int*)rot = 1;
+  if (lane == 0) {
+    int fl = wide ? kJfWide : 0;
+    if (big ? fabs(g) > kJacQuad * sqrt(a) * sqrt(b) : g * g > (kJacQuad * kJacQuad) * ab) fl |= kJfQuad;
+    if (big ? fabs(g) > kJacFloor * sqrt(a) * sqrt(b) : g * g > (kJacFloor * kJacFloor) * ab) fl |= kJfFloor;
+    if (fl & ~*(volatile int*)rot) atomicOr(rot, fl);
+  }
 }
 
 template <int RPL>
@@ -705,8 +736,8 @@ jacobi_blk_kernel(int n, const double* __restrict__ M, int64_t ldm, bool trans, 
       }
       grid.sync();
     }
-    // quadratic convergence: a sweep without a rotation above kJacQuad is the last
-    if (*(volatile int*)rt == 0) {
+    // the stopping rule above
+    if (!jac_continue(*(volatile int*)rt)) {
 #ifdef SPB_JACOBI_TRACE
       if (gtid == 0) printf("jacobi_blk n=%d np=%d sweeps=%d\n", n, np, sweep + 1);
 #endif

@@ -361,7 +361,10 @@ int tall_mul(int64_t rows, int c, const double* X, int64_t ldx, int d, const dou
     SPB_CHECK_LAUNCH();
     return SP_OK;
   }
-  const int rpc = std::max(1, std::min(512, 2048 / d));
+  // rows per CTA: 2048 outputs, bounded by the shared-memory opt-in (narrow
+  // products -- d <= 4 with c = 64 -- asked for 268 KB and failed to launch)
+  const int rpc_smem = (int)((size_t)(160 * 1024) / sizeof(double) - (size_t)c * d) / (c + 1);
+  const int rpc = std::max(1, std::min(std::min(512, 2048 / d), rpc_smem));
   const size_t smem = ((size_t)c * d + (size_t)rpc * (c + 1)) * sizeof(double);
   const int grid = (int)std::min<int64_t>(ceil_div(rows, rpc), 8 * kNumSMs);
   SPB_CUDA(launch_pdl((tall_mul_kernel), dim3(grid), dim3(kTmThreads), smem, s, rows, c, X, ldx, d, M, ldm, alpha, beta, O, ldo, top, ldt,

@@ -78,5 +78,5 @@ for seed in range(seed0, seed0 + cases):
         bad += 0 if ok else 1
     except Exception as exc:  # the reference raises on the same inputs?  report
         bad += 1
-        print("EXC  ", tag, type(exc).__name__, str(exc)[:160])
+        print("EXC  ", tag, type(exc).__name__, str(exc)[:600 if cases == 1 else 160])
 print(f"{cases} cases, {bad} flagged, {time.time() - t0:.0f} s")

@@ -134,6 +134,20 @@ def test_gemm_aat_symmetric_product(cuda, M, K):
     np.testing.assert_allclose(w, A @ A.T, rtol=0, atol=1e-12 * np.sqrt(K) * 8)
 
 
+@pytest.mark.parametrize("M,N,K", [(300, 1, 64), (300, 2, 64), (1000, 3, 64), (257, 4, 63), (4096, 4, 64)])
+def test_gemm_tall_times_narrow(cuda, M, N, K):
+    """Tall X (M x K <= 64) times a narrow block (N <= 4): the row-tile kernel's
+    shared-memory request is bounded by the opt-in (it asked for 268 KB and the
+    launch failed; found by scripts/fuzz_api.py), and a failed launch no longer
+    leaves its error behind for the next call."""
+    rng = philox(M + N + K)
+    A, B = rng.standard_normal((M, K)), rng.standard_normal((K, N))
+    dA, dB = _dev(A, cuda), _dev(B, cuda)
+    dC = cuda.zeros((M, N), dtype=cuda.float64, device="cuda")
+    _lib.call("sp_gemm", 0, 0, M, N, K, 1.0, dA.data_ptr(), K, dB.data_ptr(), N, 0.0, dC.data_ptr(), N, _stream(cuda))
+    np.testing.assert_allclose(dC.cpu().numpy(), A @ B, rtol=0, atol=1e-12)
+
+
 # ------------------------------------------------------------------ K4 ----
 @pytest.mark.parametrize("rows,cols", [(1000, 8), (5000, 32), (70000, 20), (300, 64), (2000, 100), (32, 32),
                                        (4096, 32), (65536, 7), (257, 32), (33, 32), (512, 1), (100, 3),
@@ -225,6 +239,25 @@ def test_jacobi_svd(cuda, n):
     np.testing.assert_allclose(s, want, rtol=1e-12 * n, atol=1e-15 * want[0] * n)
     np.testing.assert_allclose((u * s) @ v.T, m, atol=1e-14 * want[0] * n)
     np.testing.assert_allclose(v.T @ v, np.eye(n), atol=1e-13)
+
+
+@pytest.mark.parametrize("n", [24, 32, 48, 96, 200, 256, 300])
+def test_jacobi_svd_flat_spectrum_stays_orthonormal(cuda, n):
+    """A flat stretch of (nearly) equal singular values: the rotations inside the
+    cluster are large-angle however small the couplings, so the quadratic-
+    convergence stop alone left 2-4e-9 of non-orthogonality in U (found by
+    scripts/fuzz_api.py); a sweep with a large-angle rotation is the last only once its
+    couplings are below 1e-11."""
+    rng = philox(700 + n)
+    s_true = np.r_[np.logspace(0, -2, 6), np.full(n - 6, 3e-3)]
+    q1, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    q2, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    m = (q1 * s_true) @ q2.T
+    f = sp.thin_svd(m)
+    np.testing.assert_allclose(f.s, np.sort(s_true)[::-1], rtol=0, atol=1e-14)
+    np.testing.assert_allclose(f.u.T @ f.u, np.eye(n), atol=5e-11)
+    np.testing.assert_allclose(f.v.T @ f.v, np.eye(n), atol=5e-11)
+    np.testing.assert_allclose((f.u * f.s) @ f.v.T, m, atol=1e-13)
 
 
 @pytest.mark.parametrize("n,decay", [(3, 0.0), (16, -14.0), (31, -3.0), (32, -16.0), (32, -30.0)])
