@@ -361,7 +361,9 @@ static int core_svd_rows(int64_t p, const double* M, int64_t ldm, double* U, int
   return jacobi_svd_tr(p, M, ldm, /*trans=*/true, U, ldu, S, V, ldv, s);
 }
 
-static int complete_null_columns(int64_t p, const double* S, double* Ucols, int64_t ldu, cudaStream_t s) {
+static int complete_null_columns(int64_t p, const double* S, double* Ucols, int64_t ldu, cudaStream_t s,
+                                 bool* all_zero = nullptr) {
+  if (all_zero) *all_zero = false;
   std::vector<double> hs((size_t)p);
   SPB_TRY(read_small(hs.data(), S, p * sizeof(double), s));
   double fro2 = 0.0;
@@ -369,7 +371,20 @@ static int complete_null_columns(int64_t p, const double* S, double* Ucols, int6
   const double thr = 1e-15 * std::sqrt(fro2);
   int64_t r = 0;
   while (r < p && hs[r] > thr) ++r;
+  if (r == 0) {  // the zero matrix: any orthonormal basis
+    if (all_zero) *all_zero = true;
+    SPB_CUDA(cudaMemset2DAsync(Ucols, ldu * sizeof(double), 0, p * sizeof(double), p, s));
+    return fill_identity((int)p, Ucols, ldu, s);
+  }
   return complete_basis(p, (int)r, (int)p, Ucols, ldu, 0x5eedC0DEull, s);
+}
+
+// out (rows x p) = [I; 0]: the long factor of the zero matrix (its QR factor may
+// repeat columns: an exactly zero panel of the multi-panel TSQR has no direction
+// of its own)
+static int fill_eye_tall(int64_t rows, int64_t p, double* out, int64_t ldo, cudaStream_t s) {
+  SPB_CUDA(cudaMemset2DAsync(out, ldo * sizeof(double), 0, p * sizeof(double), rows, s));
+  return fill_identity((int)p, out, ldo, s);
 }
 
 // src/kernels.py:74-84 thin_qr: Q rows x p, R p x cols, p = min(rows, cols)
@@ -409,13 +424,24 @@ int thin_svd(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* U
     // the Jacobi schedule, so a low-rank sketch costs rounds only for its rank.
     SPB_TRY(tsqr(rows, cols, X, ldx, Q, p, R, p, s));
     SPB_TRY(core_svd_rows(p, R, p, V, ldv, S, Us, p, s));
-    SPB_TRY(complete_null_columns(p, S, V, ldv, s));
-    SPB_TRY(gemm(0, 0, rows, p, p, 1.0, Q, p, Us, p, 0.0, U, ldu, s));
+    bool zero = false;
+    SPB_TRY(complete_null_columns(p, S, V, ldv, s, &zero));
+    if (zero)
+      SPB_TRY(fill_eye_tall(rows, p, U, ldu, s));
+    else
+      SPB_TRY(gemm(0, 0, rows, p, p, 1.0, Q, p, Us, p, 0.0, U, ldu, s));
   } else if (rows >= cols) {
     // X = Q R, R = Us S Vs^T  ->  U = Q Us, V = Vs
     SPB_TRY(tsqr(rows, cols, X, ldx, Q, p, R, p, s));
     SPB_TRY(jacobi_svd(p, R, p, Us, p, S, Vs, p, s));
-    SPB_TRY(gemm(0, 0, rows, p, p, 1.0, Q, p, Us, p, 0.0, U, ldu, s));
+    // Us holds the NORMALISED columns of the rotated R: where S ~ 0 they are
+    // rounding noise (or zero), not an orthonormal completion as LAPACK's U is
+    bool zero = false;
+    SPB_TRY(complete_null_columns(p, S, Us, p, s, &zero));
+    if (zero)
+      SPB_TRY(fill_eye_tall(rows, p, U, ldu, s));
+    else
+      SPB_TRY(gemm(0, 0, rows, p, p, 1.0, Q, p, Us, p, 0.0, U, ldu, s));
     SPB_TRY(copy2d(p, p, Vs, p, V, ldv, s));
   } else {
     SPB_ALLOC(ar, double, Xt, (size_t)cols * rows);
@@ -441,15 +467,20 @@ int thin_svd_t(int64_t rows, int64_t cols, const double* Xt, int64_t ldxt, doubl
   SPB_ALLOC(ar, double, Rt, (size_t)p * p);
   SPB_ALLOC(ar, double, Vs, (size_t)p * p);
   SPB_TRY(tsqr(cols, rows, Xt, ldxt, Q, p, R, p, s));
+  bool zero = false;
   if (p > kSmallCore) {
     // X^T = Q R -> X = R^T Q^T; SVD of R^T by Jacobi on the rows of R
     SPB_TRY(core_svd_rows(p, R, p, U, ldu, S, Vs, p, s));
-    SPB_TRY(complete_null_columns(p, S, U, ldu, s));
+    SPB_TRY(complete_null_columns(p, S, U, ldu, s, &zero));
   } else {
     SPB_TRY(transpose(p, p, R, p, Rt, p, s));
     SPB_TRY(jacobi_svd(p, Rt, p, U, ldu, S, Vs, p, s));
+    SPB_TRY(complete_null_columns(p, S, U, ldu, s, &zero));  // normalised columns: noise where S ~ 0
   }
-  SPB_TRY(gemm(0, 0, cols, p, p, 1.0, Q, p, Vs, p, 0.0, V, ldv, s));
+  if (zero)
+    SPB_TRY(fill_eye_tall(cols, p, V, ldv, s));
+  else
+    SPB_TRY(gemm(0, 0, cols, p, p, 1.0, Q, p, Vs, p, 0.0, V, ldv, s));
   SPB_TRY(sign_fix(rows, p, U, ldu, V, ldv, cols, false, s));
   return SP_OK;
 }

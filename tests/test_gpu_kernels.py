@@ -241,6 +241,23 @@ def test_jacobi_svd(cuda, n):
     np.testing.assert_allclose(v.T @ v, np.eye(n), atol=1e-13)
 
 
+@pytest.mark.parametrize("shape,rank", [((300, 48), 16), ((17, 64), 5), ((33, 2), 1), ((5200, 256), 85),
+                                        ((17, 216), 5), ((64, 64), 0), ((40, 40), 39)])
+def test_thin_svd_rank_deficient_small_core_is_orthonormal(cuda, shape, rank):
+    """Exact zeros in the spectrum with a core of <= 256 columns: U and V stay
+    orthonormal (LAPACK completes the null directions, src/kernels.py:87-94); the
+    normalised Jacobi columns are rounding noise there (found by scripts/fuzz_dense.py)."""
+    rows, cols = shape
+    p = min(rows, cols)
+    m = rank_deficient(philox(rows + cols), rows, cols, rank) if rank else np.zeros(shape)
+    f = sp.thin_svd(m)
+    s_ref = np.linalg.svd(m, compute_uv=False)
+    np.testing.assert_allclose(f.s, s_ref, rtol=0, atol=1e-13 * max(s_ref[0], 1.0))
+    np.testing.assert_allclose(f.u.T @ f.u, np.eye(p), atol=1e-11)
+    np.testing.assert_allclose(f.v.T @ f.v, np.eye(p), atol=1e-11)
+    np.testing.assert_allclose((f.u * f.s) @ f.v.T, m, atol=1e-12 * max(s_ref[0], 1.0))
+
+
 @pytest.mark.parametrize("n", [24, 32, 48, 96, 200, 256, 300])
 def test_jacobi_svd_flat_spectrum_stays_orthonormal(cuda, n):
     """A flat stretch of (nearly) equal singular values: the rotations inside the
