@@ -276,12 +276,16 @@ def _gen_shard(cfg, rank, world, dev):
 
 
 def _events_ms(fn, reps, torch, stats=None):
-    """Mean device time per call over `reps` back-to-back calls (CUDA events
-    around the whole loop).  `stats` (a dict) also receives the median and the
-    largest single-call HOST time, so a one-off host stall inside a short loop
-    is visible next to the mean it inflates."""
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    """Device time per call over `reps` back-to-back calls: CUDA events around
+    the whole loop and around each of up to 10 equal chunks of it; returns the
+    MEDIAN chunk's mean (a one-off host stall -- 20 ms inside a 200 x 0.5 ms
+    loop was seen -- then moves one chunk, not the figure).  `stats` (a dict)
+    receives the plain mean over the whole loop (`ms_mean`) and the median and
+    the largest single-call HOST time, so such a stall stays visible."""
     trace = bool(os.environ.get("SPB_BENCH_TRACE"))
+    nchunk = min(10, reps)
+    bounds = [reps * c // nchunk for c in range(nchunk + 1)]
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(nchunk + 1)]
     marks, walls = [], []
     # like timeit (and the headline loop): no cyclic-GC pass inside the timed
     # region -- a generation-2 collection stalled one call of twenty by 35-180 ms
@@ -289,28 +293,33 @@ def _events_ms(fn, reps, torch, stats=None):
     was_on = gc.isenabled()
     gc.disable()
     torch.cuda.synchronize()
-    e0.record()
-    for _ in range(reps):
+    evs[0].record()
+    nxt = 1
+    for i in range(reps):
         t0 = time.perf_counter()
         out = fn()
         walls.append(1e3 * (time.perf_counter() - t0))
         if trace:
             marks.append(torch.cuda.Event(enable_timing=True))
             marks[-1].record()
-    e1.record()
+        if i + 1 == bounds[nxt]:
+            evs[nxt].record()
+            nxt += 1
     torch.cuda.synchronize()
     if was_on:
         gc.enable()
+    chunk_ms = [evs[c].elapsed_time(evs[c + 1]) / (bounds[c + 1] - bounds[c]) for c in range(nchunk)]
     if stats is not None:
+        stats["ms_mean"] = evs[0].elapsed_time(evs[nchunk]) / reps
         stats["host_ms_median_call"] = statistics.median(walls)
         stats["host_ms_max_call"] = max(walls)
     if trace:
-        prev, per = e0, []
+        prev, per = evs[0], []
         for mk in marks:
             per.append(round(prev.elapsed_time(mk), 3))
             prev = mk
         sys.stderr.write(f"[trace] per-call device ms {per}\n[trace] per-call host ms {[round(w, 3) for w in walls]}\n")
-    return e0.elapsed_time(e1) / reps, out
+    return statistics.median(chunk_ms), out
 
 
 def ingest_paths(cfg, A, op, pc, torch):

@@ -181,8 +181,8 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 // time each, which sits on the critical path right after every host
 // synchronisation.  ws_alloc / ws_free keep freed blocks in per-(device,
 // stream) free lists keyed by rounded size (reuse is stream ordered on the
-// same stream, hence safe); blocks above kWsCacheMax bytes and overflow past
-// the cache cap go straight back to the CUDA mempool (cudaFreeAsync).  On an
+// same stream, hence safe); overflow past the cache cap (64 GB per device)
+// goes straight back to the CUDA mempool (cudaFreeAsync).  On an
 // allocation failure the cache is drained (device synchronised) and the
 // allocation retried once.
 void* ws_alloc(size_t bytes, cudaStream_t s);

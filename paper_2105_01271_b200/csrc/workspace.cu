@@ -14,8 +14,22 @@ namespace spb {
 
 namespace {
 
-constexpr size_t kWsCacheMax = size_t(256) << 20;   // larger blocks are not cached
-constexpr size_t kWsCacheCap = size_t(4) << 30;     // cached bytes per device
+static size_t env_size(const char* name, size_t dflt, int shift) {
+  const char* e = std::getenv(name);
+  return e ? (size_t)std::strtoull(e, nullptr, 10) << shift : dflt;
+}
+// Every block size is cached, up to 64 GB per device (SPB_WS_CACHE_MAX_MB: largest
+// cached block, SPB_WS_CACHE_CAP_GB: cached bytes per device).  Until the last
+// session of round 2 blocks above 256 MB went back to the CUDA mempool; a
+// cudaMallocAsync of a multi-GB block from that pool (release threshold
+// UINT64_MAX, nothing handed back to the driver) still stalled the host for
+// 8 ms - 2 s in about every third cfg5 power_id call (CUPTI timeline,
+// scripts/id_spread.py: kernel time 470 ms in every call, device span 502 -
+// 2882 ms; with the blocks kept here 472 - 506 ms).  The footprint between
+// calls is the same as before (the pool kept the memory too);
+// sp_release_workspaces() hands both back.
+const size_t kWsCacheMax = env_size("SPB_WS_CACHE_MAX_MB", size_t(64) << 30, 20);
+const size_t kWsCacheCap = env_size("SPB_WS_CACHE_CAP_GB", size_t(64) << 30, 30);
 
 // 512-byte granules up to 64 KB, then 8 steps per power of two (<= 12.5 % slack)
 size_t ws_round(size_t b) {

@@ -55,7 +55,16 @@ def ptr(x) -> int | None:
 def empty(shape, dtype="f64"):
     t = require_cuda()
     td = t.float64 if dtype == "f64" else (t.float32 if dtype == "f32" else t.int64)
-    return t.empty(shape, dtype=td, device="cuda")
+    try:
+        return t.empty(shape, dtype=td, device="cuda")
+    except t.OutOfMemoryError:
+        # the library keeps its freed workspaces (csrc/workspace.cu, up to 64 GB of
+        # free lists + the CUDA mempool behind them), which torch's allocator cannot
+        # reclaim: hand them back and retry once
+        from . import _lib
+        _lib.release_workspaces()
+        t.cuda.empty_cache()
+        return t.empty(shape, dtype=td, device="cuda")
 
 
 def zeros(shape, dtype="f64"):
