@@ -153,3 +153,38 @@ def test_release_workspaces_between_calls(cuda):
     assert free1 >= free0
     np.testing.assert_array_equal(r1.s, r2.s)
     np.testing.assert_array_equal(r1.u, r2.u)
+
+
+def test_workspace_drain_under_memory_pressure(cuda):
+    """The library keeps freed workspaces of every size (csrc/workspace.cu).  When
+    the device is nearly full, a call whose workspace no longer fits must drain
+    those cached blocks, retry and give the same bits as without the pressure."""
+    import warnings
+    from paper_2105_01271_b200 import _lib
+    from paper_2105_01271_b200.datagen import CONFIGS, generate_device
+    cfg = CONFIGS["cfg2"].scaled(m=2000, grid=(256, 256), name="press")
+    a = generate_device(cfg, cuda.device("cuda", 0))
+    op, cols = sp.grid_injection(cfg.grid, 2)               # n_c = 16384: a 262 MB column block at m = 2000
+    pc = sp.PowerConfig(q=1, columns=cols)
+    small = a[:1500]                                        # 197 MB column block: another size class
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        _lib.release_workspaces()
+        want = sp.power_svd(sp.DeviceSnapshotStream(small), op, 20, pc)
+        _lib.release_workspaces()
+        cuda.cuda.empty_cache()
+        big = sp.power_svd(sp.DeviceSnapshotStream(a), op, 20, pc)      # leaves > 262 MB in the free lists
+        cuda.cuda.synchronize()
+        free = cuda.cuda.mem_get_info()[0]
+        keep = 128 << 20
+        hog = cuda.empty(free - keep, dtype=cuda.uint8, device="cuda")  # the caller fills the device
+        assert cuda.cuda.mem_get_info()[0] < 1500 * cols.size * 8      # the 197 MB block cannot be allocated
+        got = sp.power_svd(sp.DeviceSnapshotStream(small), op, 20, pc)
+        cuda.cuda.synchronize()
+        del hog
+    assert big.kept_rank >= 1
+    np.testing.assert_array_equal(got.s, want.s)
+    np.testing.assert_array_equal(got.u, want.u)
+    np.testing.assert_array_equal(got.v, want.v)
+    _lib.release_workspaces()
+    cuda.cuda.empty_cache()
