@@ -76,8 +76,11 @@ int64_t sp_launch_count(void);
  * memory pool and trim the pool (synchronises the device).  The library keeps
  * its workspaces across calls (stream-ordered free lists: no allocation on
  * the critical path of a call); a host application calls this when it wants
- * the HBM back, e.g. between problems of very different size.  No reference
- * counterpart (numpy frees its temporaries itself).
+ * the HBM back, e.g. between problems of very different size.  Blocks of every
+ * size are kept, up to 64 GB per device (environment: SPB_WS_CACHE_CAP_GB,
+ * SPB_WS_CACHE_MAX_MB = largest kept block); an allocation failure inside the
+ * library drains them and retries once.  No reference counterpart (numpy frees
+ * its temporaries itself).
  */
 int sp_release_workspaces(void);
 
