@@ -361,6 +361,18 @@ static int core_svd_rows(int64_t p, const double* M, int64_t ldm, double* U, int
   return jacobi_svd_tr(p, M, ldm, /*trans=*/true, U, ldu, S, V, ldv, s);
 }
 
+// out[:, c0:c1) = Q[:, c0:c1) with column j negated where R_jj < 0
+__global__ void copy_signed_cols_kernel(int64_t rows, int64_t c0, int64_t c1, const double* __restrict__ Q,
+                                        int64_t ldq, const double* __restrict__ R, int64_t ldr,
+                                        double* __restrict__ out, int64_t ldo) {
+  const int64_t w = c1 - c0;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * w) return;
+  const int64_t i = e / w, j = c0 + e % w;
+  const double q = Q[i * ldq + j];
+  out[i * ldo + j] = R[j * ldr + j] < 0.0 ? -q : q;
+}
+
 static int complete_null_columns(int64_t p, const double* S, double* Ucols, int64_t ldu, cudaStream_t s,
                                  bool* all_zero = nullptr) {
   if (all_zero) *all_zero = false;
@@ -375,6 +387,28 @@ static int complete_null_columns(int64_t p, const double* S, double* Ucols, int6
     if (all_zero) *all_zero = true;
     SPB_CUDA(cudaMemset2DAsync(Ucols, ldu * sizeof(double), 0, p * sizeof(double), p, s));
     return fill_identity((int)p, Ucols, ldu, s);
+  }
+  // Graded spectra.  A normalised column w_j / S_j of the rotated core carries
+  // the absolute rounding error ~eps S_1 of w_j, i.e. a relative error
+  // ~eps S_1 / S_j: without a grading of the core itself (a Haar-mixed
+  // spectrum down to 1e-13 S_1) the columns of the small S_j come out 1e-3
+  // away from orthogonal to the rest (scripts/fuzz_dense.py seed 30873:
+  // 300 x 256, U^T U - I = 9e-4), where LAPACK's U is orthonormal to eps.
+  // Columns with S_j < 1e-6 S_1 (error above the 1e-10 contract) are
+  // re-orthonormalised against the accurate leading ones and each other:
+  // Householder QR of the first r columns, the Q columns taken with the sign
+  // of R_jj.  The leading columns are left as they are (their R block is I to
+  // rounding); the replaced ones move by their own error, which changes the
+  // reconstruction by ~eps S_1.
+  int64_t r0 = 0;
+  while (r0 < r && hs[r0] >= 1e-6 * hs[0]) ++r0;
+  if (r0 < r) {
+    Arena ar(s);
+    SPB_ALLOC(ar, double, Qc, (size_t)p * r);
+    SPB_ALLOC(ar, double, Rc, (size_t)r * r);
+    SPB_TRY(tsqr(p, r, Ucols, ldu, Qc, r, Rc, r, s));
+    copy_signed_cols_kernel<<<ceil_div(p * (r - r0), 256), 256, 0, s>>>(p, r0, r, Qc, r, Rc, r, Ucols, ldu);
+    SPB_LAUNCHED();
   }
   return complete_basis(p, (int)r, (int)p, Ucols, ldu, 0x5eedC0DEull, s);
 }

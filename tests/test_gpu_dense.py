@@ -50,6 +50,23 @@ def test_thin_svd_beyond_256_full_rank(cuda, shape):
     _check_svd(x, sp.thin_svd(x))
 
 
+@pytest.mark.parametrize("shape", [(300, 256), (256, 300), (700, 130), (64, 64), (900, 520), (33, 33)])
+@pytest.mark.parametrize("decades", [9.0, 13.0])
+def test_thin_svd_graded_haar_mixed_is_orthonormal(cuda, shape, decades):
+    """A graded spectrum (down to 1e-13 sigma_1) mixed by Haar factors: the core has no
+    grading of its own, so the normalised Jacobi columns of the small sigma_j carry a
+    relative error eps sigma_1 / sigma_j (scripts/fuzz_dense.py seed 30873: 300 x 256,
+    U^T U - I = 9e-4 before those columns were re-orthonormalised).  The reference's
+    gesdd factors are orthonormal to eps whatever the spectrum (src/kernels.py:87-94)."""
+    rng = np.random.default_rng(30873)
+    rows, cols = shape
+    p = min(rows, cols)
+    u, _ = np.linalg.qr(rng.standard_normal((rows, p)))
+    v, _ = np.linalg.qr(rng.standard_normal((cols, p)))
+    x = (u * np.logspace(0, -decades, p)) @ v.T
+    _check_svd(x, sp.thin_svd(x))
+
+
 @pytest.mark.parametrize("shape", [(2000, 3000), (3000, 2000)])
 def test_thin_svd_beyond_256_rank_deficient(cuda, shape):
     """A sketch-like matrix: numerical rank 17 (the cfg2 coarse sketch), the
