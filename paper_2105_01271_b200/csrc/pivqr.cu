@@ -308,7 +308,8 @@ pl_select_kernel(int t, int k, int64_t cols, double* norms, int64_t* perm, doubl
 // row block rb: swap candidates t <-> *jsel, then partial[rb][s] = q_s . w_t (s < t)
 __global__ void __launch_bounds__(kPlThreads)
 pl_swap_dots_kernel(int t, int64_t rows, double* __restrict__ WK, const double* __restrict__ Qt,
-                    const int64_t* __restrict__ jsel, double* __restrict__ partial) {
+                    const int64_t* __restrict__ jsel, double* __restrict__ partial,
+                    const double* __restrict__ pend = nullptr) {
   __shared__ double red[kPlThreads / 32];
   const int64_t r0 = (int64_t)blockIdx.x * kPlRowsV, r1 = imin64(rows, r0 + kPlRowsV);
   const int64_t js = *jsel;
@@ -320,6 +321,15 @@ pl_swap_dots_kernel(int t, int64_t rows, double* __restrict__ WK, const double* 
       wt[x] = wj[x];
       wj[x] = a;
     }
+    __syncthreads();
+  }
+  // lagged mode: update t - 1 is still pending on every trailing candidate; the
+  // selected one (now at position t, its coefficient at R[t-1][t] after the
+  // column swap) receives it here, the others in the fused pass of this step
+  if (pend) {
+    const double c = *pend;
+    const double* vp = Qt + (int64_t)(t - 1) * rows;
+    for (int64_t x = r0 + threadIdx.x; x < r1; x += kPlThreads) wt[x] = fma(-c, vp[x], wt[x]);
     __syncthreads();
   }
   // warp w takes s = w, w + 8, ...: no block barrier per dot product
@@ -457,6 +467,62 @@ __global__ void pl_norms_kernel(int t, int nb, int64_t cols, const double* __res
   norms[j] = sqrt(a);
 }
 
+// ---- lagged update: one read + write of the candidates per step instead of a read
+// (coefficients) plus a read + write (update).
+// Pass t applies the PENDING update t - 1 (coefficients in R[t-1][.]) in registers,
+// writes the candidate back, and in the same pass takes its exact squared norm
+// (pn2) and its dot with the new pivot direction v_t (pc).
+__global__ void __launch_bounds__(kPlThreads)
+pl_fused_kernel(int t, int64_t cols, int64_t rows, double* __restrict__ WK, const double* __restrict__ Qt,
+                const double* __restrict__ Rprev, double* __restrict__ pc, double* __restrict__ pn2) {
+  __shared__ double red[kPlThreads / 32];
+  const int64_t r0 = (int64_t)blockIdx.x * kPlRows, r1 = imin64(rows, r0 + kPlRows);
+  const double* v = Qt + (int64_t)t * rows;
+  const double* vp = Rprev ? Qt + (int64_t)(t - 1) * rows : nullptr;
+  const int64_t j0 = t + 1 + (int64_t)blockIdx.y * kPlCols;
+  for (int u = 0; u < kPlCols; ++u) {
+    const int64_t j = j0 + u;
+    if (j >= cols) break;  // uniform
+    double* w = WK + j * rows;
+    double a = 0.0, n2 = 0.0;
+    if (vp) {
+      const double c = Rprev[j];
+      for (int64_t x = r0 + threadIdx.x; x < r1; x += kPlThreads) {
+        const double nv = fma(-c, vp[x], w[x]);
+        w[x] = nv;
+        n2 = fma(nv, nv, n2);
+        a = fma(v[x], nv, a);
+      }
+    } else {
+      for (int64_t x = r0 + threadIdx.x; x < r1; x += kPlThreads) {
+        const double nv = w[x];
+        n2 = fma(nv, nv, n2);
+        a = fma(v[x], nv, a);
+      }
+    }
+    a = pl_block_sum(a, red);
+    n2 = pl_block_sum(n2, red);
+    if (threadIdx.x == 0) {
+      pc[(int64_t)blockIdx.x * cols + j] = a;
+      pn2[(int64_t)blockIdx.x * cols + j] = n2;
+    }
+  }
+}
+
+// norms_j = sqrt(max(0, sum_rb pn2[rb][j] - coef_j^2)) for j > t: the residual
+// norm after update t from the exact squared norm before it (the identity
+// |w - c v|^2 = |w|^2 - c^2 holds for a unit v and c = v . w; rounding
+// ~eps |w|^2 on the square)
+__global__ void pl_downdate_kernel(int t, int nb, int64_t cols, const double* __restrict__ pn2,
+                                   const double* __restrict__ coef, double* __restrict__ norms) {
+  const int64_t j = t + 1 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= cols) return;
+  double a = 0.0;
+  for (int b = 0; b < nb; ++b) a += pn2[(int64_t)b * cols + j];
+  const double e = fma(-coef[j], coef[j], a);
+  norms[j] = e > 0.0 ? sqrt(e) : 0.0;
+}
+
 // the long-candidate factorisation loop; *fallback = true on a zero pivot
 static int pivoted_qr_long(int64_t rows, int64_t cols, int k, double* WK, double* norms, int64_t* perm, double* Qt,
                            double* R, int64_t ldr, bool* fallback, cudaStream_t s) {
@@ -472,9 +538,21 @@ static int pivoted_qr_long(int64_t rows, int64_t cols, int k, double* WK, double
   SPB_ALLOC(ar, int64_t, jsel, 1);
   SPB_ALLOC(ar, int, status, 1);
   SPB_CUDA(cudaMemsetAsync(status, 0, sizeof(int), s));
+  // lagged update (default; SPB_PQ_EAGER=1: the three-pass step, for comparison):
+  // cfg5 power_id 485 -> 447 ms, same pivots / P / reconstruction error
+  static const bool lagged = getenv("SPB_PQ_EAGER") == nullptr;
+  double* pn2l = nullptr;
+  if (lagged) {
+    pn2l = ar.alloc<double>((size_t)nb * cols);
+    if (!pn2l) {
+      set_error("pivoted QR workspace allocation failed");
+      return SP_ECUDA;
+    }
+  }
   for (int t = 0; t < k; ++t) {
     pl_select_kernel<<<1, kPqSelThreads, 0, s>>>(t, k, cols, norms, perm, R, ldr, jsel);
-    pl_swap_dots_kernel<<<nbv, kPlThreads, 0, s>>>(t, rows, WK, Qt, jsel, partial);
+    pl_swap_dots_kernel<<<nbv, kPlThreads, 0, s>>>(t, rows, WK, Qt, jsel, partial,
+                                                   lagged && t > 0 ? R + (int64_t)(t - 1) * ldr + t : nullptr);
     if (t > 0) pl_delta_kernel<<<1, 128, 0, s>>>(t, nbv, partial, delta, R, ldr);
     pl_form_v_kernel<<<nbv, kPlThreads, 0, s>>>(t, rows, WK, Qt, delta, part2);
     pl_pivot_norm_kernel<<<1, 32, 0, s>>>(t, nbv, part2, pnv, R, ldr, status);
@@ -483,6 +561,15 @@ static int pivoted_qr_long(int64_t rows, int64_t cols, int k, double* WK, double
     const int64_t trail = cols - t - 1;
     if (trail > 0) {
       dim3 g(nb, ceil_div(trail, kPlCols));
+      if (lagged) {
+        pl_fused_kernel<<<g, kPlThreads, 0, s>>>(t, cols, rows, WK, Qt, t > 0 ? R + (int64_t)(t - 1) * ldr : nullptr,
+                                                 pc, pn2l);
+        pl_coef_reduce_kernel<<<ceil_div(trail, 256), 256, 0, s>>>(t, nb, cols, pc, coef, R, ldr);
+        pl_downdate_kernel<<<ceil_div(trail, 256), 256, 0, s>>>(t, nb, cols, pn2l, coef, norms);
+        count_launch(3);
+        SPB_CHECK_LAUNCH();
+        continue;
+      }
       pl_coef_kernel<<<g, kPlThreads, 0, s>>>(t, cols, rows, WK, Qt, pc);
       pl_coef_reduce_kernel<<<ceil_div(trail, 256), 256, 0, s>>>(t, nb, cols, pc, coef, R, ldr);
       pl_update_kernel<<<g, kPlThreads, 0, s>>>(t, cols, rows, WK, Qt, coef, pc);
